@@ -1,0 +1,479 @@
+"""BEV-pool benchmark (BASELINE.json metric) -- one JSON line on stdout.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (configs[1], SURVEY.md §8 "S"): nuScenes camera stream, 6 cameras x
+32x88 features, D=118 (1-60 m @ 0.5 m), C=80, 360x360 BEV grid @ 0.3 m,
+batch 1, cached-interval forward.  A step is one reference-API forward
+``pool_interval(features, dist, cache, grid, SUM)``: NHWC staging of the
+features + the interval-reduction kernel, inputs resident in HBM, L2 flushed
+(512 MiB write) between steps.  value = frustum points/s over all ranks (each
+rank pools its own sample: weak scaling, no collective in the loop; NCCL only
+gathers the timings).  e2e = the same step through PoolPlan.run_host with
+host buffers (pinned H2D of features + dist, D2H of the BEV map) in the timed
+region.  N=1 also reports cpu_baseline (the oracle's C port of the
+reference's pool_interval, all host threads) and the other configurations as
+"variants".
+
+``--impl reference`` times the reference's CPU pool_interval (the oracle port
+of pkg/src/bevpool/_kernels.py, OpenMP over all host cores) on the same
+config; under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "bev_pool_points_per_sec"
+UNIT = "points/s"
+CONFIG_NAME = "S"
+FLUSH_BYTES = 512 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--exact", type=int, default=None, help="1: 64-bit bit-exact mode")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def config_dict(spec, extra=None):
+    f, g = spec.frustum, spec.grid
+    d = {"workload": "nuScenes camera stream (configs[1]): cached-interval forward",
+         "cameras": spec.n_cameras, "feature_hw": [f.height, f.width], "depth_bins": f.depth_bins,
+         "channels": spec.channels, "grid": [g.nx, g.ny], "cell_m": g.r, "batch_per_gpu": 1,
+         "points_per_sample": spec.n_points, "reducer": "sum",
+         "l2": "flushed between steps (512 MiB write)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm
+# ---------------------------------------------------------------------------
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def time_cpu_reference(spec, max_seconds, min_reps=3, max_reps=200, warmup=1):
+    """The oracle port of the reference pool_interval (transposes + 64-bit
+    interval_reduce, OpenMP) on all host threads.  Returns (per-step seconds)."""
+    from oracle import oracle as o
+    from paper_2205_13542_b200.workload import gen_workload, synthetic_rig  # noqa: F401 (inputs)
+
+    lib = o.lib()
+    lib.oracle_set_threads(cpu_threads())
+    cfg = o.CONFIGS[CONFIG_NAME]
+    cache = o.build_cache(cfg)
+    f, lg = o.gen_inputs(cfg.n_cameras, cfg.channels, cfg.height, cfg.width, cfg.depth_bins, 0)
+    dist = o.normalize_depth(lg)
+    args = (f, dist, cache["ranks"], cache["interval_starts"], cache["interval_cells"],
+            cfg.n_cells, "sum")
+    for _ in range(warmup):
+        o.pool_interval(*args)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_reps:
+        t0 = time.perf_counter()
+        o.pool_interval(*args)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= min_reps and time.perf_counter() - t_start > max_seconds:
+            break
+    return times, lib.oracle_max_threads()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2205_13542_b200.workload import CONFIGS
+
+    spec = CONFIGS[CONFIG_NAME]
+    reps = max(1, args.steps)
+    times, threads = time_cpu_reference(spec, max_seconds=1e9, min_reps=reps, max_reps=reps,
+                                        warmup=max(1, args.warmup))
+    total = sum(times)
+    value = spec.n_points * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 in / f64 accumulate", "data": "synthetic",
+        "config": config_dict(spec),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{len(times)} full nuScenes-shape pool_interval steps "
+                                   "(oracle C port of _kernels.interval_reduce + NHWC "
+                                   "transposes, OpenMP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU helpers
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self, busy_only=True):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:  # pragma: no cover
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            sm.append(s)
+            smax = m
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        busy = [s for s in sm if s > 0.5 * max(sm)] if busy_only else sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_key):
+    """dram read+write bytes per launch of the headline kernel from the
+    committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel_key, {}).get("dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2205_13542_b200 as bp
+    from paper_2205_13542_b200.bevgrid import ptr, stream_ptr  # noqa: F401
+
+    rank, world, local = dist_env()
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec = bp.CONFIGS[CONFIG_NAME]
+    f = spec.frustum
+    P = spec.n_points
+
+    # ---- inputs: this rank's sample (seed = rank), resident in HBM -------
+    rig, feats_np, logits_np, grid = bp.gen_workload(
+        bp.WorkloadSpec(spec.n_cameras, f, spec.grid, spec.channels, rank))
+    cache = bp.build_cache(rig, f, grid, device=dev)
+    feats = torch.from_numpy(feats_np).to(dev).view(1, *feats_np.shape)
+    dist = bp.normalize_depth(torch.from_numpy(logits_np).to(dev)).view(1, *logits_np.shape)
+    exact = bool(args.exact) if args.exact is not None else bp.pooling.DEFAULT_EXACT
+    plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
+                       f.depth_bins, 1, bp.Reducer.SUM, exact, dev)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        plan.run(feats, dist)
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize(dev)
+    for k in range(K):
+        flush.zero_()
+        ev[k][0].record(stream)
+        plan.transpose(feats)
+        ev[k][1].record(stream)
+        plan.reduce(dist)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        tdist.barrier()
+    step_ms = [e[0].elapsed_time(e[2]) for e in ev]
+    kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    tot_ms = sum(step_ms)
+    # e2e: host buffers (pinned) through the public plan API; H2D of the
+    # inputs, both kernels and D2H of the BEV map inside the timed region
+    h_feats = torch.from_numpy(feats_np).pin_memory()
+    h_dist = dist.cpu().pin_memory()
+    e2e_ms = []
+    for k in range(max(3, args.warmup) + K):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        plan.run_host(h_feats, h_dist)
+        t1 = time.perf_counter()
+        if k >= max(3, args.warmup):
+            e2e_ms.append(1e3 * (t1 - t0))
+    e2e_tot = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms, e2e_tot], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tot_ms, e2e_tot = t.tolist()
+
+    variants = {}
+    if rank == 0 and world == 1 and not args.no_variants:
+        variants = run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush)
+    clk = clocks.stop()
+
+    # ---- roofline of the dominant kernel (interval reduction) -----------
+    n_in, n_int = cache.n_in_range, cache.n_intervals
+    C, NHW, NDHW = spec.channels, spec.n_cameras * f.height * f.width, P
+    alg_bytes = 4 * NHW * C + 4 * NDHW + 4 * n_in + 8 * n_int + 4 * C * grid.n_cells
+    kern_avg_s = statistics.mean(kern_ms) * 1e-3
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / kern_avg_s / 1e9
+    traffic = ncu_traffic("pool_tile_kernel")
+
+    if rank != 0:
+        if world > 1:
+            tdist.destroy_process_group()
+        return
+    value = world * P * K / (tot_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": max(3, args.warmup), "ms_per_step": tot_ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 in, f64 accumulate (bit-exact)" if exact else "f32",
+        "data": "synthetic (reference gen_workload: PCG64 seed=rank, synthetic 6-camera rig)",
+        "config": config_dict(spec, {"parallelism": f"batch-sharded x{world} (1 sample/GPU)",
+                                     "exact": exact}),
+        "latency_ms": {"step_median": statistics.median(step_ms), "step_min": min(step_ms),
+                       "interval_kernel_median": statistics.median(kern_ms)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "pool_tile_kernel (interval reduction, reference formulation)",
+                     "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                     "frac_of_nominal_8TBs": achieved / 8000.0},
+        "e2e": {"value": world * P * K / (e2e_tot * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
+                "ms_per_step": e2e_tot / K,
+                "path": "PoolPlan.run_host (pinned H2D features+dist, 2 launches, D2H map)"},
+        "gpu_launches": 2 * K * world,
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        times, threads = time_cpu_reference(spec, args.cpu_seconds)
+        v = P * len(times) / sum(times)
+        line["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(times)} full nuScenes-shape pool_interval steps "
+                      f"(median {1e3 * statistics.median(times):.1f} ms), oracle C port, OpenMP"}
+    if variants:
+        line["variants"] = variants
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# other configurations (N=1): latency + roofline each, cold L2
+# ---------------------------------------------------------------------------
+
+def _timeit(torch, fn, flush, reps=10, warmup=3):
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        flush.zero_()
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
+    peak, _ = measured_peak()
+    f = spec.frustum
+    C, P = spec.channels, spec.n_points
+    NHW = spec.n_cameras * f.height * f.width
+    n_in, n_int, n_cells = cache.n_in_range, cache.n_intervals, grid.n_cells
+    out = {}
+
+    def rec(name, ms, alg_bytes, **kw):
+        gbs = alg_bytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "points_per_s": P * kw.pop("samples", 1) / (ms * 1e-3),
+                     "alg_bytes": alg_bytes, "GBps": gbs, "hbm_frac": gbs / peak, **kw}
+
+    ref_bytes = 4 * NHW * C + 4 * P + 4 * n_in + 8 * n_int + 4 * C * n_cells
+    for exact in (False, True):
+        plan = bp.PoolPlan(cache, grid, spec.n_cameras, C, f.height, f.width, f.depth_bins, 1,
+                           bp.Reducer.SUM, exact, dev)
+        plan.transpose(feats)
+        ms = _timeit(torch, lambda: plan.reduce(dist), flush)
+        rec("interval_kernel_exact" if exact else "interval_kernel_fast", ms, ref_bytes)
+        ms = _timeit(torch, lambda: plan.run(feats, dist), flush)
+        rec("step_exact" if exact else "step_fast", ms, ref_bytes + 8 * NHW * C)
+    for red in (bp.Reducer.MEAN, bp.Reducer.MAX):
+        plan = bp.PoolPlan(cache, grid, spec.n_cameras, C, f.height, f.width, f.depth_bins, 1,
+                           red, False, dev)
+        ms = _timeit(torch, lambda: plan.run(feats, dist), flush)
+        rec(f"step_fast_{red.value}", ms, ref_bytes + 8 * NHW * C)
+
+    # materialised frustum: the paper's bev_pool input x (P, C)
+    x = bp.lift_features(feats[0], dist[0])
+    ms = _timeit(torch, lambda: bp.lift_features(feats[0], dist[0]), flush)
+    rec("materialised_lift", ms, 4 * NHW * C + 4 * P + 4 * P * C)
+    outx = torch.empty((C, n_cells), dtype=torch.float32, device=dev)
+    from paper_2205_13542_b200 import _lib
+    from paper_2205_13542_b200.bevgrid import ptr, stream_ptr
+
+    def pool_x():
+        _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
+                  ptr(cache.d_interval_cells), ptr(cache.d_tile_first), C, n_cells, 0, ptr(outx),
+                  stream_ptr(dev))
+    ms = _timeit(torch, pool_x, flush)
+    rec("materialised_pool", ms, n_in * (4 * C + 4) + 8 * n_int + 4 * C * n_cells)
+    del x
+
+    # fused bf16 lift+pool
+    lg = torch.randn(dist.shape, device=dev).to(torch.bfloat16)[0]
+    cx = feats[0].to(torch.bfloat16)
+    ms = _timeit(torch, lambda: bp.pool_fused(lg, cx, cache, grid), flush)
+    rec("fused_bf16", ms, 2 * P + 2 * NHW * C + 4 * NHW + 4 * n_in + 8 * n_int + 4 * C * n_cells)
+
+    # cold association (geometry + sort + tables), no host sync
+    builder = bp.CacheBuilder(spec.n_cameras, f, grid, dev)
+    cams = torch.from_numpy(bp.rig_rows(rig)).to(dev)
+    ms = _timeit(torch, lambda: builder.build(cams), flush)
+    rec("association_cold", ms, 12 * P + 4 * n_in + 8 * n_cells + 8 * n_int)
+    ms = _timeit(torch, lambda: bp.reorder_weights(dist[0], cache), flush)
+    rec("association_cached_reorder", ms, 4 * n_in + 4 * n_in + 4 * n_in)
+
+    # paper's "before": prefix-sum pooling on the same GPU
+    try:
+        ms = _timeit(torch, lambda: bp.pool_prefixsum(feats[0], dist[0], cache, grid,
+                                                      check_finite=False), flush, reps=3,
+                     warmup=1)
+        rec("prefixsum_baseline", ms, 8 * n_in * C * 3)
+    except Exception as exc:  # pragma: no cover
+        out["prefixsum_baseline"] = {"error": str(exc)}
+
+    # training step, batch 4: forward + gather backward
+    B = 4
+    Fb = feats.expand(B, *feats.shape[1:]).contiguous().requires_grad_(True)
+    Db = dist.expand(B, *dist.shape[1:]).contiguous().requires_grad_(True)
+    g = torch.randn((B, C, grid.nx, grid.ny), device=dev)
+
+    def train_step():
+        o = bp.bev_pool(Fb, Db, cache, grid)
+        o.backward(g)
+    ms = _timeit(torch, train_step, flush)
+    rec("training_b4_fwd_bwd", ms,
+        B * (ref_bytes + 8 * NHW * C + 4 * C * n_cells + 4 * P + 4 * C * n_int + 4 * NHW * C
+             + 4 * P), samples=B)
+
+    # high-res stress: uncached geometry every frame + forward
+    hs = bp.CONFIGS["H"]
+    hrig, hf, hl, hgrid = bp.gen_workload(hs)
+    hb = bp.CacheBuilder(hs.n_cameras, hs.frustum, hgrid, dev)
+    hcams = torch.from_numpy(bp.rig_rows(hrig)).to(dev)
+    hc = hb.build(hcams)
+    hfe = torch.from_numpy(hf).to(dev)[None]
+    hd = bp.normalize_depth(torch.from_numpy(hl).to(dev))[None]
+    hplan = bp.PoolPlan(hc, hgrid, hs.n_cameras, hs.channels, hs.frustum.height, hs.frustum.width,
+                        hs.frustum.depth_bins, 1, bp.Reducer.SUM, False, dev)
+
+    def hframe():
+        hb.build(hcams)
+        hplan.run(hfe, hd)
+    ms = _timeit(torch, hframe, flush)
+    hP = hs.n_points
+    hn_in, hn_int = hc.n_in_range, hc.n_intervals
+    hbytes = (12 * hP + 4 * hn_in + 8 * hgrid.n_cells + 8 * hn_int) + (
+        12 * hs.n_cameras * hs.frustum.height * hs.frustum.width * hs.channels + 4 * hP
+        + 4 * hn_in + 8 * hn_int + 4 * hs.channels * hgrid.n_cells)
+    out["highres_uncached_frame"] = {"ms": ms, "points_per_s": hP / (ms * 1e-3),
+                                     "alg_bytes": hbytes, "GBps": hbytes / (ms * 1e-3) / 1e9,
+                                     "hbm_frac": hbytes / (ms * 1e-3) / 1e9 / peak}
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,227 @@
+/*
+ * bevpool_b200.h -- C ABI of the B200 (sm_100a) BEV-pooling library
+ * (libbevpool_sm100.so).  Plain pointers and sizes only; every entry point is
+ * stream-ordered on the caller's cudaStream_t (passed as void*), takes DEVICE
+ * pointers allocated by the caller, never allocates, never synchronises, and
+ * returns BVP_OK or an error code with a message in bvp_last_error().
+ *
+ * Reference interfaces replaced (paths relative to the reference's
+ * pkg/src/bevpool/):
+ *   bvp_frustum_cells     generate_frustum + quantize_points
+ *                         (geometry.py:162-191, bevgrid.py:85-98)
+ *   bvp_sort_intervals    ranks_and_intervals (bevgrid.py:142-158)
+ *   bvp_build_cache       build_cache minus the host fingerprint
+ *                         (bevgrid.py:183-203)
+ *   bvp_pool_forward_f32  pool_interval -> _kernels.interval_reduce
+ *                         (pooling.py:206-221, _kernels.py:22-63)
+ *   bvp_reorder_weights   reorder_weights (pooling.py:243-261)
+ *   bvp_normalize_depth   normalize_depth (lift.py:17-31)
+ *   bvp_lift_f32 / bvp_pool_lifted_f32   the paper's materialised frustum
+ *                         x = depth (x) feature then bev_pool
+ *   bvp_fused_pool_bf16   lift+pool fused (no reference counterpart; config F)
+ *   bvp_pool_backward_f32 gather backward (no reference counterpart)
+ *
+ * Cache layout on the device (all uint32, produced by bvp_build_cache):
+ *   cell_of_point[P]        flat cell id per frustum point or 0xFFFFFFFF
+ *   ranks[P]                first n_in entries valid (point ids sorted by cell,
+ *                           stable)
+ *   interval_starts[n_cells+1]  first n_int entries as the reference, plus a
+ *                           sentinel interval_starts[n_int] = n_in
+ *   interval_cells[n_cells] first n_int entries valid
+ *   tile_first[n_tiles+1]   first interval of every BVP_TILE_CELLS-cell tile
+ *   interval_of_point[P]    interval index per point or 0xFFFFFFFF
+ *   counts[2] (int64)       n_in, n_int
+ * so a whole frame can be rebuilt and pooled without a host round trip.
+ */
+#ifndef BEVPOOL_B200_H
+#define BEVPOOL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* exported even when the library is built with -fvisibility=hidden */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define BVP_ABI_VERSION 1
+
+#define BVP_OK 0
+#define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
+#define BVP_ERR_UNSUPPORTED 2  /* shape/mode not compiled -> ConfigurationError  */
+#define BVP_ERR_CUDA 3         /* CUDA runtime/launch error                      */
+
+#define BVP_OUT_OF_RANGE 0xFFFFFFFFu
+#define BVP_TILE_CELLS 32
+
+#define BVP_SUM 0
+#define BVP_MEAN 1
+#define BVP_MAX 2
+
+int bvp_abi_version(void);
+const char *bvp_last_error(void);
+
+/* ---- geometry precompute (cold association) -------------------------- */
+
+/* cams: device, N x 16 float64 rows fx, fy, cx, cy, R[9] (row-major,
+ * camera->ego), t[3].  grid: HOST, 7 float64 x_min, x_max, y_min, y_max,
+ * z_min, z_max, r.  Writes cell_of_point[N*H*W*D]. */
+int bvp_frustum_cells(const double *cams, int N, int H, int W, int D,
+                      double depth_min, double depth_step, const double *grid,
+                      int nx, int ny, uint32_t *cell_of_point, void *stream);
+
+/* Workspace for bvp_sort_intervals / bvp_build_cache. */
+size_t bvp_sort_workspace_bytes(int64_t n_points, int64_t n_cells);
+
+/* Stable bounded-key sort of the in-range points by cell id and interval
+ * detection, from an existing cell_of_point (e.g. a cache loaded from disk).
+ * Outputs as in the cache layout above; interval_of_point may be NULL. */
+int bvp_sort_intervals(const uint32_t *cell_of_point, int64_t n_points,
+                       int64_t n_cells, uint32_t *ranks,
+                       uint32_t *interval_starts, uint32_t *interval_cells,
+                       uint32_t *tile_first, uint32_t *interval_of_point,
+                       int64_t *counts, void *workspace, size_t workspace_bytes,
+                       void *stream);
+
+/* bvp_frustum_cells + bvp_sort_intervals. */
+int bvp_build_cache(const double *cams, int N, int H, int W, int D,
+                    double depth_min, double depth_step, const double *grid,
+                    int nx, int ny, uint32_t *cell_of_point, uint32_t *ranks,
+                    uint32_t *interval_starts, uint32_t *interval_cells,
+                    uint32_t *tile_first, uint32_t *interval_of_point,
+                    int64_t *counts, void *workspace, size_t workspace_bytes,
+                    void *stream);
+
+/* ---- cached forward ---------------------------------------------------- */
+
+/* Workspace for bvp_pool_forward_f32: the NHWC copy of the features. */
+size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
+
+/* features (B,N,C,H,W) f32, dist (B,N,D,H,W) f32 -> out (B,C,n_cells) f32.
+ * Every output element is written (empty cells 0).  mode: BVP_SUM/MEAN/MAX.
+ * exact != 0: 64-bit accumulation in rank order, bit-identical to the
+ * reference's interval_reduce; exact == 0: fp32 accumulation (<=1.2e-7 rel).
+ * feats_nhwc: workspace of bvp_pool_workspace_bytes; left holding the
+ * (B,N,H,W,C) transpose (reused by the backward).  argmax: NULL, or for
+ * BVP_MAX a (B, n_int_max, C) uint32 buffer receiving the winning point id of
+ * every (interval, channel). */
+int bvp_pool_forward_f32(const float *features, const float *dist,
+                         const uint32_t *ranks, const uint32_t *interval_starts,
+                         const uint32_t *interval_cells,
+                         const uint32_t *tile_first, int B, int N, int C, int H,
+                         int W, int D, int64_t n_cells, int64_t n_int_max,
+                         int mode, int exact, float *out, float *feats_nhwc,
+                         uint32_t *argmax, void *stream);
+
+/* (NB, C, H*W) -> (NB, H*W, C) f32 copy (the features' NHWC staging that
+ * bvp_pool_forward_f32 performs first; pooling.py:215). */
+int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst,
+                    void *stream);
+
+/* Same, with the features already NHWC (B,N,H,W,C): skips the transpose. */
+int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,
+                              const uint32_t *ranks,
+                              const uint32_t *interval_starts,
+                              const uint32_t *interval_cells,
+                              const uint32_t *tile_first, int B, int N, int C,
+                              int H, int W, int D, int64_t n_cells,
+                              int64_t n_int_max, int mode, int exact,
+                              float *out, uint32_t *argmax, void *stream);
+
+/* w_sorted[j] = dist_t[ranks[j]] (dist given as (N,D,H,W)), j < n_in. */
+int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in,
+                        int N, int D, int H, int W, float *w_sorted,
+                        void *stream);
+
+/* Softmax over D of (B*N, D, H, W) logits, 64-bit math, f32 out. */
+int bvp_normalize_depth(const float *logits, int NB, int D, int H, int W,
+                        float *dist, void *stream);
+
+/* Non-finite scan of n floats; *flag (device int) set to 1 if any. */
+int bvp_any_nonfinite(const float *x, int64_t n, int *flag, void *stream);
+
+/* ---- materialised frustum (the paper's bev_pool input) ----------------- */
+
+/* x[((n*H+h)*W+w)*D+d, c] = dist[n,d,h,w] * features[n,c,h,w], (P, C) f32. */
+int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H,
+                 int W, int D, float *x, void *stream);
+
+/* Interval reduction over materialised rows x (P, C) -> out (C, n_cells). */
+int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
+                        const uint32_t *interval_starts,
+                        const uint32_t *interval_cells,
+                        const uint32_t *tile_first, int C, int64_t n_cells,
+                        int mode, float *out, void *stream);
+
+/* ---- fused lift + pool, bf16 inputs (config F) ------------------------- */
+
+/* Workspace: per-pixel log-sum-exp (f32) + NHWC bf16 context. */
+size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W);
+
+/* logits (B,N,D,H,W) bf16, context (B,N,C,H,W) bf16 -> out (B,C,n_cells)
+ * f32 = pool(softmax_D(logits) (x) context), fp32 accumulation. */
+int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context,
+                        const uint32_t *ranks, const uint32_t *interval_starts,
+                        const uint32_t *interval_cells,
+                        const uint32_t *tile_first, int B, int N, int C, int H,
+                        int W, int D, int64_t n_cells, int mode, float *out,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---- gather backward (config B) ---------------------------------------- */
+
+/* Workspace: per-interval gradient rows (B, n_int_max, C) f32. */
+size_t bvp_backward_workspace_bytes(int B, int C, int64_t n_int_max);
+
+/* grad_out (B,C,n_cells) -> grad_features (B,N,C,H,W) and grad_dist
+ * (B,N,D,H,W), both fully written.  feats_nhwc as left by the forward;
+ * argmax required for BVP_MAX.  Either grad pointer may be NULL. */
+int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc,
+                          const float *dist, const uint32_t *interval_starts,
+                          const uint32_t *interval_cells,
+                          const uint32_t *tile_first,
+                          const uint32_t *interval_of_point,
+                          const uint32_t *argmax, int B, int N, int C, int H,
+                          int W, int D, int64_t n_cells, int64_t n_int_max,
+                          int mode, float *grad_features, float *grad_dist,
+                          void *workspace, size_t workspace_bytes,
+                          void *stream);
+
+/* Materialised backward: grad_x[p, :] = dL/dx_p (zeros for out-of-range). */
+int bvp_pool_lifted_backward_f32(const float *grad_out,
+                                 const uint32_t *interval_starts,
+                                 const uint32_t *interval_cells,
+                                 const uint32_t *tile_first,
+                                 const uint32_t *interval_of_point, int C,
+                                 int64_t n_points, int64_t n_cells,
+                                 int64_t n_int_max, int mode, float *grad_x,
+                                 void *workspace, size_t workspace_bytes,
+                                 void *stream);
+
+/* ---- the paper's "before": LSS prefix-sum pooling --------- */
+
+/* pool_prefixsum (pooling.py:162-196): materialise the full running sum over
+ * the rank-ordered points per channel, subtract at interval ends. SUM/MEAN.
+ * workspace: n_in * C floats + scan scratch. */
+size_t bvp_prefixsum_workspace_bytes(int64_t n_in, int C);
+int bvp_pool_prefixsum_f32(const float *features, const float *dist,
+                           const uint32_t *ranks,
+                           const uint32_t *interval_starts,
+                           const uint32_t *interval_cells, int64_t n_in,
+                           int64_t n_int, int N, int C, int H, int W, int D,
+                           int64_t n_cells, int mode, float *out,
+                           void *workspace, size_t workspace_bytes,
+                           void *stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BEVPOOL_B200_H */

@@ -1,0 +1,110 @@
+"""ctypes binding of libbevpool_sm100.so (the C ABI in include/bevpool_b200.h).
+
+There is deliberately no fallback: if the shared library is missing or fails
+to load, every GPU entry point raises ``ExtensionMissingError`` -- the
+framework never silently computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import BevPoolError, ConfigurationError, ValidationError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbevpool_sm100.so")
+
+BVP_OK, BVP_ERR_INVALID, BVP_ERR_UNSUPPORTED, BVP_ERR_CUDA = 0, 1, 2, 3
+BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
+TILE_CELLS = 32
+OUT_OF_RANGE = 0xFFFFFFFF
+ABI_VERSION = 1
+
+
+class ExtensionMissingError(BevPoolError, RuntimeError):
+    """libbevpool_sm100.so is not built or cannot be loaded."""
+
+
+class CudaError(BevPoolError, RuntimeError):
+    """A CUDA launch inside the library failed."""
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_L = ctypes.c_int64
+_D = ctypes.c_double
+_S = ctypes.c_size_t
+
+#: name -> (restype, argtypes); mirrors include/bevpool_b200.h one to one
+SIGNATURES = {
+    "bvp_abi_version": (_I, []),
+    "bvp_last_error": (ctypes.c_char_p, []),
+    "bvp_frustum_cells": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _I, _I, _P, _P]),
+    "bvp_sort_workspace_bytes": (_S, [_L, _L]),
+    "bvp_sort_intervals": (_I, [_P, _L, _L, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
+    "bvp_build_cache": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _I, _I, _P, _P, _P, _P, _P, _P,
+                             _P, _P, _S, _P]),
+    "bvp_pool_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
+    "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L, _L, _I,
+                                  _I, _P, _P, _P, _P]),
+    "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L, _L,
+                                       _I, _I, _P, _P, _P]),
+    "bvp_to_nhwc_f32": (_I, [_P, _I, _I, _I, _P, _P]),
+    "bvp_reorder_weights": (_I, [_P, _P, _L, _I, _I, _I, _I, _P, _P]),
+    "bvp_normalize_depth": (_I, [_P, _I, _I, _I, _I, _P, _P]),
+    "bvp_any_nonfinite": (_I, [_P, _L, _P, _P]),
+    "bvp_lift_f32": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P]),
+    "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _I, _L, _I, _P, _P]),
+    "bvp_fused_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
+    "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L, _I, _P,
+                                 _P, _S, _P]),
+    "bvp_backward_workspace_bytes": (_S, [_I, _I, _L]),
+    "bvp_pool_backward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _L,
+                                   _L, _I, _P, _P, _P, _S, _P]),
+    "bvp_pool_lifted_backward_f32": (_I, [_P, _P, _P, _P, _P, _I, _L, _L, _L, _I, _P, _P, _S,
+                                          _P]),
+    "bvp_prefixsum_workspace_bytes": (_S, [_L, _I]),
+    "bvp_pool_prefixsum_f32": (_I, [_P, _P, _P, _P, _P, _L, _L, _I, _I, _I, _I, _I, _L, _I, _P,
+                                    _P, _S, _P]),
+}
+
+_lib = None
+
+
+def load():
+    """Load and type the library (once)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ExtensionMissingError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:  # pragma: no cover - depends on the box
+        raise ExtensionMissingError(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.bvp_abi_version() != ABI_VERSION:
+        raise ExtensionMissingError("libbevpool_sm100.so ABI version mismatch; rebuild it")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == BVP_OK:
+        return
+    msg = f"{what}: {load().bvp_last_error().decode(errors='replace')}"
+    if rc == BVP_ERR_INVALID:
+        raise ValidationError(msg)
+    if rc == BVP_ERR_UNSUPPORTED:
+        raise ConfigurationError(msg)
+    raise CudaError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,79 @@
+"""Training: the interval pooling as a differentiable torch op (config B).
+
+Forward is the cached interval reduction (bvp_pool_forward_f32, fp32
+accumulation); backward is the atomic-free gather backward
+(bvp_pool_backward_f32, csrc/backward.cu) producing gradients for both the
+context features and the depth distribution.  MAX routes each output
+gradient to the first point (rank order) attaining the max, recorded by the
+forward.  The reference has no backward; tests/ check this one
+against an fp64 restatement and torch.autograd.gradcheck.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .bevgrid import AssociationCache, BevGridSpec, ptr, stream_ptr
+from .pooling import _MODE, BevFeatureMap, Reducer, _reducer
+
+
+class _BevPoolFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, features, dist, cache: AssociationCache, n_cells: int, reducer: Reducer,
+                exact: bool):
+        B, N, C, H, W = features.shape
+        D = dist.shape[2]
+        dev = features.device
+        features = features.contiguous()
+        dist = dist.contiguous()
+        out = torch.empty((B, C, n_cells), dtype=torch.float32, device=dev)
+        nhwc = torch.empty(features.numel(), dtype=torch.float32, device=dev)
+        argmax = None
+        if reducer is Reducer.MAX:
+            argmax = torch.empty((B, cache.n_int_max, C), dtype=torch.int32, device=dev)
+        _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(cache.d_ranks),
+                  ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
+                  ptr(cache.d_tile_first), B, N, C, H, W, D, n_cells, cache.n_int_max,
+                  _MODE[reducer], int(exact), ptr(out), ptr(nhwc), ptr(argmax), stream_ptr(dev))
+        ctx.cache, ctx.reducer, ctx.dims = cache, reducer, (B, N, C, H, W, D, n_cells)
+        ctx.save_for_backward(nhwc, dist, argmax)
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        nhwc, dist, argmax = ctx.saved_tensors
+        cache, reducer = ctx.cache, ctx.reducer
+        B, N, C, H, W, D, n_cells = ctx.dims
+        dev = grad_out.device
+        g = grad_out.float().contiguous()
+        need_f, need_w = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
+        gf = torch.empty((B, N, C, H, W), dtype=torch.float32, device=dev) if need_f else None
+        gw = torch.empty((B, N, D, H, W), dtype=torch.float32, device=dev) if need_w else None
+        if need_f or need_w:
+            ws = torch.empty(_lib.load().bvp_backward_workspace_bytes(B, C, cache.n_int_max),
+                             dtype=torch.uint8, device=dev)
+            _lib.call("bvp_pool_backward_f32", ptr(g), ptr(nhwc), ptr(dist),
+                      ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
+                      ptr(cache.d_tile_first), ptr(cache.d_interval_of_point), ptr(argmax), B, N,
+                      C, H, W, D, n_cells, cache.n_int_max, _MODE[reducer], ptr(gf), ptr(gw),
+                      ptr(ws), ws.numel(), stream_ptr(dev))
+        return gf, gw, None, None, None, None
+
+
+def bev_pool(features: torch.Tensor, dist: torch.Tensor, cache: AssociationCache,
+             grid: BevGridSpec, reducer=Reducer.SUM, exact: bool = False) -> torch.Tensor:
+    """Differentiable pooling. features (N,C,H,W) or (B,N,C,H,W), dist
+    (N,D,H,W) or (B,N,D,H,W), float32 CUDA -> (C,nx,ny) or (B,C,nx,ny)."""
+    reducer = _reducer(reducer)
+    batched = features.dim() == 5
+    f = features if batched else features[None]
+    d = dist if batched else dist[None]
+    cache = cache.for_grid(grid.n_cells)
+    out = _BevPoolFn.apply(f.float(), d.float(), cache, grid.n_cells, reducer, exact)
+    out = out.view(f.shape[0], f.shape[2], grid.nx, grid.ny)
+    return out if batched else out[0]
+
+
+def bev_pool_map(features, dist, cache, grid, reducer=Reducer.SUM) -> BevFeatureMap:
+    return BevFeatureMap(bev_pool(features, dist, cache, grid, reducer), grid)

@@ -1,0 +1,378 @@
+"""BEV grid, the point -> cell association cache, and its wire format.
+
+Mirrors the reference's bevgrid module (bevgrid.py:1-298): same grid
+semantics (half-open cells, interior boundaries go up, ix-major flat ids,
+z only gates membership), same AssociationCache contract (stable ranks,
+interval_starts / interval_cells) and the same BVPC file format.  The
+association itself is built on the GPU (csrc/geometry.cu): fp64 frustum ->
+ego -> cell in the reference's exact rounding order, then a stable LSD radix
+sort and interval tables, bit-identical to ``bevpool.build_cache``.
+
+The cache lives in HBM: ``AssociationCache`` holds device tensors (uint32
+values stored in torch.int32) plus two tables the GPU kernels need and the
+reference does not have -- ``tile_first`` (first interval of every 32-cell
+tile) and ``interval_of_point`` (for the gather backward) -- and a sentinel
+``interval_starts[n_int] = n_in`` so no kernel needs host-side counts.
+The reference-typed numpy views (``cache.ranks`` ...) are host copies made
+on first access.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigurationError, FileFormatError, StaleCacheError
+from .geometry import CameraCalibration, FrustumSpec, rig_rows
+
+#: Sentinel cell id of points outside the grid (also the wire encoding).
+OUT_OF_RANGE = 0xFFFFFFFF
+TILE_CELLS = _lib.TILE_CELLS
+
+_CACHE_MAGIC = b"BVPC"
+_CACHE_VERSION = 1
+
+
+@dataclass(frozen=True)
+class BevGridSpec:
+    """Metric extents and cell size of the BEV grid (reference bevgrid.py:30-68)."""
+
+    x_min: float
+    x_max: float
+    y_min: float
+    y_max: float
+    z_min: float
+    z_max: float
+    r: float
+
+    def __post_init__(self):
+        if self.r <= 0:
+            raise ConfigurationError(f"cell size must be positive, got {self.r}")
+        if self.z_min >= self.z_max:
+            raise ConfigurationError(f"need z_min < z_max, got [{self.z_min}, {self.z_max})")
+        for axis, lo, hi in (("x", self.x_min, self.x_max), ("y", self.y_min, self.y_max)):
+            span = hi - lo
+            n = span / self.r
+            if span <= 0 or abs(n - round(n)) > 1e-9 or round(n) < 1:
+                raise ConfigurationError(
+                    f"{axis} extent [{lo}, {hi}) is not a positive integer multiple of r={self.r}")
+
+    @property
+    def nx(self) -> int:
+        return round((self.x_max - self.x_min) / self.r)
+
+    @property
+    def ny(self) -> int:
+        return round((self.y_max - self.y_min) / self.r)
+
+    @property
+    def n_cells(self) -> int:
+        return self.nx * self.ny
+
+    def as_array(self) -> np.ndarray:
+        return np.array([self.x_min, self.x_max, self.y_min, self.y_max, self.z_min, self.z_max,
+                         self.r], dtype=np.float64)
+
+
+#: Benchmark default of the reference: 102.4 m square at r = 0.4 m.
+DEFAULT_GRID = BevGridSpec(-51.2, 51.2, -51.2, 51.2, -10.0, 10.0, 0.4)
+
+
+def quantize(spec: BevGridSpec, p) -> int:
+    """Flat cell id of one ego point (scalar helper, bevgrid.py:71-82)."""
+    x, y, z = float(p[0]), float(p[1]), float(p[2])
+    ix = int(np.floor((x - spec.x_min) / spec.r))
+    iy = int(np.floor((y - spec.y_min) / spec.r))
+    if 0 <= ix < spec.nx and 0 <= iy < spec.ny and spec.z_min <= z < spec.z_max:
+        return ix * spec.ny + iy
+    return OUT_OF_RANGE
+
+
+def cuda_device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.ExtensionMissingError("a CUDA device is required (no CPU fallback)")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ConfigurationError(f"device must be a CUDA device, got {device}")
+    return device
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _u32(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)
+
+
+@dataclass(eq=False)
+class AssociationCache:
+    """Device-resident association of every frustum point with its BEV cell.
+
+    ``ranks`` lists the in-range point ids sorted by cell (stable); interval
+    i covers ranks[interval_starts[i] : interval_starts[i+1]] and all its
+    points share cell interval_cells[i].  Immutable after build.
+    """
+
+    d_cell_of_point: torch.Tensor          # (P,)
+    d_ranks: torch.Tensor                  # (>= n_in,)
+    d_interval_starts: torch.Tensor        # (>= n_int + 1,) with sentinel
+    d_interval_cells: torch.Tensor         # (>= n_int,)
+    d_tile_first: torch.Tensor             # (n_tiles + 1,)
+    d_interval_of_point: torch.Tensor      # (P,)
+    d_counts: torch.Tensor                 # (2,) int64: n_in, n_int
+    fingerprint: int
+    n_cells: int
+    n_cameras: int | None = None
+    frustum: FrustumSpec | None = field(default=None, repr=False)
+    grid: BevGridSpec | None = field(default=None, repr=False)
+    _host_counts: tuple | None = field(default=None, repr=False)
+    _host: dict = field(default_factory=dict, repr=False)
+
+    # ---- sizes ----------------------------------------------------------
+    @property
+    def device(self) -> torch.device:
+        return self.d_cell_of_point.device
+
+    @property
+    def n_points(self) -> int:
+        return int(self.d_cell_of_point.shape[0])
+
+    def _counts(self):
+        if self._host_counts is None:
+            c = self.d_counts.cpu().tolist()
+            self._host_counts = (int(c[0]), int(c[1]))
+        return self._host_counts
+
+    @property
+    def n_in_range(self) -> int:
+        return self._counts()[0]
+
+    @property
+    def n_intervals(self) -> int:
+        return self._counts()[1]
+
+    @property
+    def n_int_max(self) -> int:
+        """Capacity of the interval tables (no host sync)."""
+        return int(self.d_interval_cells.shape[0])
+
+    # ---- reference-typed host views ------------------------------------
+    def _view(self, name, tensor, n):
+        if name not in self._host:
+            arr = _u32(tensor[:n]).copy()
+            arr.flags.writeable = False
+            self._host[name] = arr
+        return self._host[name]
+
+    @property
+    def cell_of_point(self) -> np.ndarray:
+        return self._view("cell_of_point", self.d_cell_of_point, self.n_points)
+
+    @property
+    def ranks(self) -> np.ndarray:
+        return self._view("ranks", self.d_ranks, self.n_in_range)
+
+    @property
+    def interval_starts(self) -> np.ndarray:
+        return self._view("interval_starts", self.d_interval_starts, self.n_intervals)
+
+    @property
+    def interval_cells(self) -> np.ndarray:
+        return self._view("interval_cells", self.d_interval_cells, self.n_intervals)
+
+    @property
+    def interval_of_point(self) -> np.ndarray:
+        return self._view("interval_of_point", self.d_interval_of_point, self.n_points)
+
+    def for_grid(self, n_cells: int) -> "AssociationCache":
+        """This cache with tile tables sized for an ``n_cells`` grid.  Caches
+        loaded from disk carry no grid (reference bevgrid.py:110-113); their
+        tables are re-derived once per pooling grid."""
+        if n_cells == self.n_cells:
+            return self
+        key = ("grid", n_cells)
+        if key not in self._host:
+            self._host[key] = cache_from_cells(self.cell_of_point, n_cells, self.fingerprint,
+                                               self.n_cameras, self.frustum, self.grid,
+                                               self.device)
+        return self._host[key]
+
+
+def _alloc(P: int, n_cells: int, dev) -> dict:
+    n_tiles = -(-n_cells // TILE_CELLS)
+    i32 = dict(dtype=torch.int32, device=dev)
+    return dict(
+        cells=torch.empty(P, **i32), ranks=torch.empty(P, **i32),
+        starts=torch.empty(n_cells + 1, **i32), icells=torch.empty(n_cells, **i32),
+        tile_first=torch.empty(n_tiles + 1, **i32), iop=torch.empty(P, **i32),
+        counts=torch.zeros(2, dtype=torch.int64, device=dev),
+        ws=torch.empty(_lib.load().bvp_sort_workspace_bytes(P, n_cells), dtype=torch.uint8,
+                       device=dev),
+    )
+
+
+class CacheBuilder:
+    """Re-usable GPU association builder: buffers and workspace are allocated
+    once for a (frustum, grid) shape and every ``build`` reruns geometry +
+    sort + interval tables on the current stream with no host round trip
+    (config H: uncached geometry every frame).  The returned cache aliases
+    the builder's buffers until the next ``build``."""
+
+    def __init__(self, n_cameras: int, frustum: FrustumSpec, grid: BevGridSpec, device=None):
+        self.dev = cuda_device(device)
+        self.n_cameras, self.frustum, self.grid = n_cameras, frustum, grid
+        self.P = n_cameras * frustum.points_per_camera
+        self.bufs = _alloc(self.P, grid.n_cells, self.dev)
+        self._grid_arr = grid.as_array()
+
+    def build(self, cams: torch.Tensor, fingerprint: int = 0) -> AssociationCache:
+        """cams: (N, 16) float64 CUDA tensor (see geometry.rig_rows)."""
+        b, f, g = self.bufs, self.frustum, self.grid
+        if cams.dtype != torch.float64 or cams.shape != (self.n_cameras, 16) or not cams.is_cuda:
+            raise ConfigurationError("cams must be a CUDA float64 (N, 16) tensor")
+        cams = cams.contiguous()
+        _lib.call("bvp_build_cache", ptr(cams), self.n_cameras, f.height, f.width, f.depth_bins,
+                  f.depth_min, f.depth_step, self._grid_arr.ctypes.data, g.nx, g.ny,
+                  ptr(b["cells"]), ptr(b["ranks"]), ptr(b["starts"]), ptr(b["icells"]),
+                  ptr(b["tile_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
+                  b["ws"].numel(), stream_ptr(self.dev))
+        return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"],
+                                b["tile_first"], b["iop"], b["counts"], fingerprint,
+                                g.n_cells, self.n_cameras, f, g)
+
+
+def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
+                grid_spec: BevGridSpec, device=None) -> AssociationCache:
+    """Project the rig's frustum, quantise and sort by cell -- on the GPU.
+
+    Drop-in for bevgrid.build_cache (reference bevgrid.py:183-203); the
+    arrays are bit-identical to the reference's.
+    """
+    cams = rig_rows(rig)
+    builder = CacheBuilder(len(rig), frustum_spec, grid_spec, device)
+    cams_d = torch.from_numpy(cams).to(builder.dev)
+    cache = builder.build(cams_d, fingerprint_inputs(rig, frustum_spec, grid_spec))
+    cache._counts()  # one sync: sizes known on the host from here on
+    return cache
+
+
+def cache_from_cells(cell_of_point, n_cells: int, fingerprint: int = 0, n_cameras=None,
+                     frustum=None, grid=None, device=None) -> AssociationCache:
+    """Association cache from given cell ids (a loaded file, a synthetic test
+    cache): GPU stable sort + interval tables (bevgrid.py:142-158)."""
+    dev = cuda_device(device)
+    cells = np.ascontiguousarray(cell_of_point, dtype=np.uint32)
+    P = int(cells.shape[0])
+    if P == 0:
+        raise ConfigurationError("cache must cover at least one point")
+    valid = cells[cells != OUT_OF_RANGE]
+    if valid.size and int(valid.max()) >= n_cells:
+        raise StaleCacheError("cache contains cell ids beyond this grid")
+    b = _alloc(P, n_cells, dev)
+    b["cells"].copy_(torch.from_numpy(cells.view(np.int32)))
+    _lib.call("bvp_sort_intervals", ptr(b["cells"]), P, n_cells, ptr(b["ranks"]),
+              ptr(b["starts"]), ptr(b["icells"]), ptr(b["tile_first"]), ptr(b["iop"]),
+              ptr(b["counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
+    cache = AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["tile_first"],
+                             b["iop"], b["counts"], fingerprint, n_cells, n_cameras, frustum,
+                             grid)
+    cache._counts()
+    return cache
+
+
+def ranks_and_intervals(cells: np.ndarray, n_cells: int | None = None):
+    """GPU restatement of bevgrid.ranks_and_intervals: (ranks, starts, cells)."""
+    cells = np.ascontiguousarray(cells, dtype=np.uint32)
+    if cells.size == 0:
+        e = np.empty(0, dtype=np.uint32)
+        return e, e.copy(), e.copy()
+    if n_cells is None:
+        valid = cells[cells != OUT_OF_RANGE]
+        n_cells = int(valid.max()) + 1 if valid.size else 1
+    c = cache_from_cells(cells, n_cells)
+    return c.ranks.copy(), c.interval_starts.copy(), c.interval_cells.copy()
+
+
+def fingerprint_inputs(rig, frustum: FrustumSpec, grid: BevGridSpec) -> int:
+    """blake2b-64 of the canonical bytes of rig + specs (bevgrid.py:161-180)."""
+    buf = bytearray(struct.pack("<I", len(rig)))
+    for cam in rig:
+        buf += struct.pack("<i4d", cam.camera_id, cam.fx, cam.fy, cam.cx, cam.cy)
+        buf += cam.rotation.astype("<f8").tobytes() + cam.translation.astype("<f8").tobytes()
+    buf += struct.pack("<II2dI", frustum.height, frustum.width, frustum.depth_min,
+                       frustum.depth_step, frustum.depth_bins)
+    buf += struct.pack("<7d", grid.x_min, grid.x_max, grid.y_min, grid.y_max, grid.z_min,
+                       grid.z_max, grid.r)
+    return int.from_bytes(hashlib.blake2b(bytes(buf), digest_size=8).digest(), "little")
+
+
+def validate_cache(cache: AssociationCache, rig, frustum_spec, grid_spec) -> bool:
+    return cache.fingerprint == fingerprint_inputs(rig, frustum_spec, grid_spec)
+
+
+# ---- BVPC wire format (bevgrid.py:216-292): host I/O, not accelerated ------
+def serialize_cache(cache: AssociationCache) -> bytes:
+    out = bytearray(_CACHE_MAGIC) + struct.pack("<HQ", _CACHE_VERSION, cache.fingerprint)
+    for arr in (cache.cell_of_point, cache.ranks, cache.interval_starts, cache.interval_cells):
+        out += struct.pack("<Q", arr.shape[0]) + arr.astype("<u4").tobytes()
+    return bytes(out)
+
+
+def deserialize_cache(data: bytes, n_cells: int | None = None, device=None) -> AssociationCache:
+    """Decode a BVPC blob and rebuild the device tables from its cell ids.
+
+    The file's ranks / intervals must equal the deterministic GPU re-sort of
+    its cell_of_point (they do for every file the reference writes)."""
+    pos = 0
+
+    def take(n, what):
+        nonlocal pos
+        if pos + n > len(data):
+            raise FileFormatError(f"truncated while reading {what}", offset=pos)
+        chunk = data[pos:pos + n]
+        pos += n
+        return chunk
+
+    magic = take(4, "magic")
+    if magic != _CACHE_MAGIC:
+        raise FileFormatError(f"bad magic {magic!r}, expected {_CACHE_MAGIC!r}", offset=0)
+    (version,) = struct.unpack("<H", take(2, "version"))
+    if version != _CACHE_VERSION:
+        raise FileFormatError(f"unsupported cache version {version}", offset=4)
+    (fingerprint,) = struct.unpack("<Q", take(8, "fingerprint"))
+    arrays = []
+    for what in ("cell_of_point", "ranks", "interval_starts", "interval_cells"):
+        (count,) = struct.unpack("<Q", take(8, f"{what} length"))
+        arrays.append(np.frombuffer(take(4 * count, what), dtype="<u4").copy())
+    if pos != len(data):
+        raise FileFormatError("trailing bytes after cache payload", offset=pos)
+    cells, ranks, starts, icells = arrays
+    if n_cells is None:
+        n_cells = int(icells.max()) + 1 if icells.size else 1
+    cache = cache_from_cells(cells, n_cells, fingerprint, device=device)
+    if not (np.array_equal(cache.ranks, ranks) and np.array_equal(cache.interval_starts, starts)
+            and np.array_equal(cache.interval_cells, icells)):
+        raise FileFormatError("ranks / intervals inconsistent with cell_of_point")
+    return cache
+
+
+def save_cache(path, cache: AssociationCache) -> None:
+    with open(path, "wb") as fh:
+        fh.write(serialize_cache(cache))
+
+
+def load_cache(path, n_cells: int | None = None, device=None) -> AssociationCache:
+    with open(path, "rb") as fh:
+        return deserialize_cache(fh.read(), n_cells, device)

@@ -1,0 +1,267 @@
+// backward.cu -- gather backward of the interval pooling (config B).
+//
+// The reference has no backward (SPEC.md:540 lists autograd as a non-goal);
+// the math is the adjoint of pool_interval (pooling.py:206-221):
+//   out[c, cell] = red_{p in cell} w_p * f[pix(p), c]
+//   SUM : dL/dv_p = g[:, cell(p)]        MEAN: ... / len(cell)
+//   MAX : g[c, cell] routed to the winning point of (cell, c) (first in rank
+//         order, recorded by the forward as `argmax`)
+//   grad_f[n,c,h,w] = sum_d w_p dL/dv_p[c],  grad_w[n,d,h,w] = <f[pix], dL/dv_p>
+//
+// No atomics: step 1 turns grad_out (C, n_cells) into per-interval rows
+// gT[i, :] (scaled for MEAN) through a coalesced shared-memory transpose; step
+// 2 walks the frustum in POINT order -- one warp per pixel, its D points'
+// interval ids are contiguous in interval_of_point -- gathering gT rows, so
+// every gradient element is produced by exactly one warp.  The 32 per-point
+// dot products of a depth block are reduced with a 31-shuffle transpose-
+// reduction instead of 32 separate butterflies.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace bvp {
+
+constexpr int kRowPitch = kTileCells + 1;
+
+template <bool MEAN>
+__global__ void __launch_bounds__(128)
+grad_rows_kernel(const float *__restrict__ grad_out, const uint32_t *__restrict__ starts,
+                 const uint32_t *__restrict__ icells, const uint32_t *__restrict__ tile_first,
+                 int C, int64_t n_cells, int64_t n_int_max, float *__restrict__ gT) {
+    extern __shared__ float s[];  // [C][kRowPitch]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x, b = blockIdx.y;
+    const int64_t cell0 = int64_t(tile) * kTileCells;
+    const uint32_t i0 = tile_first[tile], i1 = tile_first[tile + 1];
+    if (i0 == i1) return;
+    const float *g = grad_out + int64_t(b) * C * n_cells + cell0;
+    const int64_t rem = n_cells - cell0;
+    for (int c = warp; c < C; c += 4)
+        s[c * kRowPitch + lane] = lane < rem ? __ldg(g + int64_t(c) * n_cells + lane) : 0.f;
+    __syncthreads();
+    for (uint32_t i = i0 + warp; i < i1; i += 4) {
+        const int lc = static_cast<int>(icells[i] - cell0);
+        const float scale = MEAN ? 1.f / float(starts[i + 1] - starts[i]) : 1.f;
+        float *row = gT + (int64_t(b) * n_int_max + i) * C;
+        for (int c = lane; c < C; c += 32) row[c] = s[c * kRowPitch + lc] * scale;
+    }
+}
+
+__device__ __forceinline__ float transpose_reduce32(float (&part)[32], int lane) {
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+        const bool upper = (lane & sft) != 0;
+#pragma unroll
+        for (int i = 0; i < sft; ++i) {
+            const float send = upper ? part[i] : part[i + sft];
+            const float keep = upper ? part[i + sft] : part[i];
+            part[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, sft);
+        }
+    }
+    return part[0];
+}
+
+// grid (ceil(W/32), N*H, B), 256 threads; CTA = 32 pixels of one image row.
+template <int Q, bool IS_MAX>
+__global__ void __launch_bounds__(256)
+pool_backward_kernel(const float *__restrict__ gT, const uint32_t *__restrict__ argT,
+                     const float *__restrict__ feats_nhwc, const float *__restrict__ dist,
+                     const uint32_t *__restrict__ iop, int N, int C, int H, int W, int D,
+                     int64_t n_int_max, float *__restrict__ grad_f, float *__restrict__ grad_w) {
+    extern __shared__ float sm[];
+    float *s_gf = sm;                       // [C][kRowPitch]
+    float *s_gw = sm + C * kRowPitch;       // [D][kRowPitch]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int w0 = blockIdx.x * 32;
+    const int nh = blockIdx.y, b = blockIdx.z;
+    const int n = nh / H, h = nh - n * H;
+    const int HW = H * W;
+    const int64_t NHW = int64_t(N) * HW;
+    const int64_t P = NHW * D;
+    const float *distb = dist + int64_t(b) * N * D * HW;
+    for (int wl = warp; wl < 32; wl += 8) {
+        const int w = w0 + wl;
+        if (w >= W) break;
+        const int hw = h * W + w;
+        const int64_t pix = int64_t(n) * HW + hw;
+        const int64_t p0 = pix * D;
+        float f[Q], af[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int c = lane + 32 * q;
+            f[q] = c < C ? __ldg(feats_nhwc + (int64_t(b) * NHW + pix) * C + c) : 0.f;
+            af[q] = 0.f;
+        }
+        for (int d0 = 0; d0 < D; d0 += 32) {
+            const int dl = d0 + lane;
+            uint32_t iv_l = kOOR;
+            float wt_l = 0.f;
+            if (dl < D) {
+                iv_l = __ldg(iop + p0 + dl);
+                wt_l = __ldg(distb + (int64_t(n) * D + dl) * HW + hw);
+            }
+            float part[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                part[k] = 0.f;
+                const uint32_t iv = __shfl_sync(0xFFFFFFFFu, iv_l, k);
+                const float wt = __shfl_sync(0xFFFFFFFFu, wt_l, k);
+                if (iv != kOOR) {
+                    const int64_t rbase = (int64_t(b) * n_int_max + iv) * C;
+                    float dot = 0.f;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        const int c = lane + 32 * q;
+                        if (c < C) {
+                            float gv = __ldg(gT + rbase + c);
+                            if (IS_MAX && __ldg(argT + rbase + c) != uint32_t(p0 + d0 + k))
+                                gv = 0.f;
+                            af[q] += wt * gv;
+                            dot += f[q] * gv;
+                        }
+                    }
+                    part[k] = dot;
+                }
+            }
+            const float gw = transpose_reduce32(part, lane);
+            if (dl < D) s_gw[dl * kRowPitch + wl] = gw;
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int c = lane + 32 * q;
+            if (c < C) s_gf[c * kRowPitch + wl] = af[q];
+        }
+    }
+    __syncthreads();
+    const int nw = min(32, W - w0);
+    if (lane < nw) {
+        const int64_t hw = int64_t(h) * W + w0 + lane;
+        if (grad_f) {
+            float *gf = grad_f + (int64_t(b) * N + n) * C * HW + hw;
+            for (int c = warp; c < C; c += 8) gf[int64_t(c) * HW] = s_gf[c * kRowPitch + lane];
+        }
+        if (grad_w) {
+            float *gw = grad_w + (int64_t(b) * N + n) * D * HW + hw;
+            for (int d = warp; d < D; d += 8) gw[int64_t(d) * HW] = s_gw[d * kRowPitch + lane];
+        }
+    }
+    (void)P;
+}
+
+template <bool IS_MAX>
+__global__ void lifted_backward_kernel(const float *__restrict__ gT,
+                                       const uint32_t *__restrict__ argT,
+                                       const uint32_t *__restrict__ iop, int C, int64_t P,
+                                       float *__restrict__ grad_x) {
+    const int64_t total = P * C;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = e / C, c = e - p * C;
+        const uint32_t iv = __ldg(iop + p);
+        float v = 0.f;
+        if (iv != kOOR) {
+            v = __ldg(gT + int64_t(iv) * C + c);
+            if (IS_MAX && __ldg(argT + int64_t(iv) * C + c) != uint32_t(p)) v = 0.f;
+        }
+        grad_x[e] = v;
+    }
+}
+
+static int launch_grad_rows(const float *grad_out, const uint32_t *starts, const uint32_t *icells,
+                            const uint32_t *tile_first, int B, int C, int64_t n_cells,
+                            int64_t n_int_max, bool mean, float *gT, cudaStream_t s) {
+    const size_t smem = size_t(C) * kRowPitch * sizeof(float);
+    BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", C);
+    auto k = mean ? grad_rows_kernel<true> : grad_rows_kernel<false>;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const dim3 grid(static_cast<unsigned>(ceil_div(n_cells, kTileCells)), static_cast<unsigned>(B));
+    k<<<grid, 128, smem, s>>>(grad_out, starts, icells, tile_first, C, n_cells, n_int_max, gT);
+    return BVP_OK;
+}
+
+}  // namespace bvp
+
+using namespace bvp;
+
+extern "C" {
+
+size_t bvp_backward_workspace_bytes(int B, int C, int64_t n_int_max) {
+    return size_t(B) * size_t(n_int_max > 0 ? n_int_max : 1) * C * sizeof(float);
+}
+
+int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc, const float *dist,
+                          const uint32_t *interval_starts, const uint32_t *interval_cells,
+                          const uint32_t *tile_first, const uint32_t *interval_of_point,
+                          const uint32_t *argmax, int B, int N, int C, int H, int W, int D,
+                          int64_t n_cells, int64_t n_int_max, int mode, float *grad_features,
+                          float *grad_dist, void *workspace, size_t workspace_bytes,
+                          void *stream) {
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && n_cells >= 1,
+                BVP_ERR_INVALID, "bad dims");
+    BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
+    BVP_REQUIRE(mode != BVP_MAX || argmax, BVP_ERR_INVALID, "MAX backward needs argmax");
+    const size_t need = bvp_backward_workspace_bytes(B, C, n_int_max);
+    BVP_REQUIRE(workspace && workspace_bytes >= need, BVP_ERR_INVALID,
+                "backward workspace too small: need %zu bytes", need);
+    BVP_REQUIRE(grad_out && feats_nhwc && dist && interval_starts && interval_cells && tile_first &&
+                    interval_of_point,
+                BVP_ERR_INVALID, "null pointer argument");
+    cudaStream_t s = as_stream(stream);
+    if (C == 0) {
+        if (grad_dist) cudaMemsetAsync(grad_dist, 0, size_t(B) * N * D * H * W * sizeof(float), s);
+        return check_launch("pool_backward");
+    }
+    const int Q = (C + 31) / 32;
+    BVP_REQUIRE(Q <= 8, BVP_ERR_UNSUPPORTED, "backward supports C <= 256, got %d", C);
+    float *gT = static_cast<float *>(workspace);
+    int rc = launch_grad_rows(grad_out, interval_starts, interval_cells, tile_first, B, C, n_cells,
+                              n_int_max, mode == BVP_MEAN, gT, s);
+    if (rc != BVP_OK) return rc;
+    const size_t smem = size_t(C + D) * kRowPitch * sizeof(float);
+    BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "C + D too large for the backward");
+    const dim3 grid(static_cast<unsigned>((W + 31) / 32), static_cast<unsigned>(N * H),
+                    static_cast<unsigned>(B));
+    const bool mx = mode == BVP_MAX;
+#define BVP_BWD(QQ)                                                                          \
+    case QQ: {                                                                               \
+        auto k = mx ? pool_backward_kernel<QQ, true> : pool_backward_kernel<QQ, false>;      \
+        if (smem > 48 * 1024)                                                                \
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+        k<<<grid, 256, smem, s>>>(gT, argmax, feats_nhwc, dist, interval_of_point, N, C, H, W, \
+                                  D, n_int_max, grad_features, grad_dist);                   \
+        break;                                                                               \
+    }
+    switch (Q) {
+        BVP_BWD(1) BVP_BWD(2) BVP_BWD(3) BVP_BWD(4) BVP_BWD(5) BVP_BWD(6) BVP_BWD(7) BVP_BWD(8)
+    }
+#undef BVP_BWD
+    return check_launch("pool_backward");
+}
+
+int bvp_pool_lifted_backward_f32(const float *grad_out, const uint32_t *interval_starts,
+                                 const uint32_t *interval_cells, const uint32_t *tile_first,
+                                 const uint32_t *interval_of_point, int C, int64_t n_points,
+                                 int64_t n_cells, int64_t n_int_max, int mode, float *grad_x,
+                                 void *workspace, size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(C >= 1 && n_points >= 1 && n_cells >= 1 && mode >= 0 && mode <= 1,
+                BVP_ERR_INVALID, "bad arguments (lifted backward supports SUM/MEAN)");
+    const size_t need = bvp_backward_workspace_bytes(1, C, n_int_max);
+    BVP_REQUIRE(workspace && workspace_bytes >= need, BVP_ERR_INVALID,
+                "backward workspace too small: need %zu bytes", need);
+    BVP_REQUIRE(grad_out && interval_starts && interval_cells && tile_first && interval_of_point &&
+                    grad_x,
+                BVP_ERR_INVALID, "null pointer argument");
+    cudaStream_t s = as_stream(stream);
+    float *gT = static_cast<float *>(workspace);
+    int rc = launch_grad_rows(grad_out, interval_starts, interval_cells, tile_first, 1, C, n_cells,
+                              n_int_max, mode == BVP_MEAN, gT, s);
+    if (rc != BVP_OK) return rc;
+    const unsigned blocks =
+        static_cast<unsigned>(std::min<int64_t>(ceil_div(n_points * C, 256), 148 * 64));
+    lifted_backward_kernel<false><<<blocks, 256, 0, s>>>(gT, nullptr, interval_of_point, C,
+                                                         n_points, grad_x);
+    return check_launch("pool_lifted_backward");
+}
+
+}  // extern "C"

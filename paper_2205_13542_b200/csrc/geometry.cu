@@ -1,0 +1,407 @@
+// geometry.cu -- cold association on the GPU: frustum -> ego -> BEV cell in
+// float64 with the reference's exact operation order, a stable bounded-key
+// LSD radix sort of the in-range points by cell, and interval / tile tables.
+//
+// Reference: geometry.py:162-191 (generate_frustum), bevgrid.py:85-98
+// (quantize_points), bevgrid.py:142-158 (ranks_and_intervals),
+// bevgrid.py:183-203 (build_cache).  Paths relative to pkg/src/bevpool/.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace bvp {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kKeysPerThread = 16;
+constexpr int kSortTile = kSortThreads * kKeysPerThread;  // 4096 keys per CTA
+constexpr int kMaxDigitBits = 10;
+constexpr int kMaxDigits = 1 << kMaxDigitBits;
+
+struct GridParams {
+    double x_min, y_min, z_min, z_max, r;
+    int nx, ny;
+};
+
+struct FrustumParams {
+    int N, H, W, D;
+    double d_min, d_step;
+};
+
+// One frustum point -> flat cell id.  Every operation is an explicit
+// round-to-nearest intrinsic so nvcc cannot contract or reassociate:
+//   depth = d_min + step*d                         geometry.py:95-99
+//   dx = (w - cx)/fx, dy = (h - cy)/fy             geometry.py:178-179
+//   p = (dx*depth, dy*depth, depth)                geometry.py:184
+//   e_j = fma(R[j][2],pz, fma(R[j][1],py, R[j][0]*px)) + t_j
+//        (the OpenBLAS dgemm rounding of geometry.py:185-186)
+//   ix = floor((x - x_min)/r) ...                  bevgrid.py:88-96
+__device__ __forceinline__ uint32_t point_cell(const double *__restrict__ cams,
+                                               const FrustumParams &f,
+                                               const GridParams &g, int64_t p) {
+    const int d = static_cast<int>(p % f.D);
+    int64_t rest = p / f.D;
+    const int w = static_cast<int>(rest % f.W);
+    rest /= f.W;
+    const int h = static_cast<int>(rest % f.H);
+    const int n = static_cast<int>(rest / f.H);
+    const double *c = cams + 16 * n;
+    const double fx = __ldg(c + 0), fy = __ldg(c + 1), cx = __ldg(c + 2), cy = __ldg(c + 3);
+    const double depth = __dadd_rn(f.d_min, __dmul_rn(f.d_step, static_cast<double>(d)));
+    const double dx = __ddiv_rn(__dsub_rn(static_cast<double>(w), cx), fx);
+    const double dy = __ddiv_rn(__dsub_rn(static_cast<double>(h), cy), fy);
+    const double px = __dmul_rn(dx, depth), py = __dmul_rn(dy, depth), pz = depth;
+    double e[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        double acc = __dmul_rn(__ldg(c + 4 + 3 * j), px);
+        acc = __fma_rn(__ldg(c + 5 + 3 * j), py, acc);
+        acc = __fma_rn(__ldg(c + 6 + 3 * j), pz, acc);
+        e[j] = __dadd_rn(acc, __ldg(c + 13 + j));
+    }
+    const double qx = floor(__ddiv_rn(__dsub_rn(e[0], g.x_min), g.r));
+    const double qy = floor(__ddiv_rn(__dsub_rn(e[1], g.y_min), g.r));
+    if (qx >= 0.0 && qx < static_cast<double>(g.nx) && qy >= 0.0 &&
+        qy < static_cast<double>(g.ny) && e[2] >= g.z_min && e[2] < g.z_max)
+        return static_cast<uint32_t>(static_cast<int64_t>(qx) * g.ny + static_cast<int64_t>(qy));
+    return kOOR;
+}
+
+__global__ void frustum_cells_kernel(const double *__restrict__ cams, FrustumParams f,
+                                     GridParams g, int64_t P, uint32_t *__restrict__ cells) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x)
+        cells[p] = point_cell(cams, f, g, p);
+}
+
+// Pass-0 front end of the sort: (optionally) computes the cells, counts
+// points per cell, and writes the tile histogram of the first radix digit.
+// Tile t covers point ids [t*kSortTile, (t+1)*kSortTile).
+template <bool COMPUTE>
+__global__ void __launch_bounds__(kSortThreads)
+pass0_front_kernel(const double *__restrict__ cams, FrustumParams f, GridParams g,
+                   int64_t P, uint32_t *__restrict__ cells, uint32_t *__restrict__ cell_count,
+                   int digit_bits, uint32_t *__restrict__ hist, int64_t n_tiles) {
+    __shared__ uint32_t sh[kMaxDigits];
+    const int n_digits = 1 << digit_bits;
+    for (int i = threadIdx.x; i < n_digits; i += kSortThreads) sh[i] = 0;
+    __syncthreads();
+    const int64_t base = blockIdx.x * (int64_t)kSortTile;
+    const uint32_t mask = n_digits - 1;
+#pragma unroll 4
+    for (int k = 0; k < kKeysPerThread; ++k) {
+        const int64_t p = base + k * kSortThreads + threadIdx.x;
+        if (p >= P) break;
+        uint32_t c;
+        if (COMPUTE) {
+            c = point_cell(cams, f, g, p);
+            cells[p] = c;
+        } else {
+            c = cells[p];
+        }
+        if (c != kOOR) {
+            atomicAdd(&cell_count[c], 1u);
+            atomicAdd(&sh[c & mask], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_digits; i += kSortThreads)
+        hist[(int64_t)i * n_tiles + blockIdx.x] = sh[i];
+}
+
+// Histogram of the current digit over sorted positions [0, n_valid).
+__global__ void __launch_bounds__(kSortThreads)
+radix_upsweep_kernel(const uint32_t *__restrict__ keys, const int64_t *__restrict__ counts,
+                     int shift, int digit_bits, uint32_t *__restrict__ hist, int64_t n_tiles) {
+    __shared__ uint32_t sh[kMaxDigits];
+    const int n_digits = 1 << digit_bits;
+    for (int i = threadIdx.x; i < n_digits; i += kSortThreads) sh[i] = 0;
+    __syncthreads();
+    const int64_t n_valid = counts[0];
+    const int64_t base = blockIdx.x * (int64_t)kSortTile;
+    const uint32_t mask = n_digits - 1;
+    for (int k = 0; k < kKeysPerThread; ++k) {
+        const int64_t j = base + k * kSortThreads + threadIdx.x;
+        if (j >= n_valid) break;
+        atomicAdd(&sh[(keys[j] >> shift) & mask], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_digits; i += kSortThreads)
+        hist[(int64_t)i * n_tiles + blockIdx.x] = sh[i];
+}
+
+// Stable scatter of one LSD pass.  Warp w of tile t owns the contiguous key
+// range [t*kSortTile + w*512, +512) and walks it in index order 32 keys at a
+// time; __match_any_sync gives each key its rank among equal digits of the
+// round, per-warp running counters (exclusive across warps, seeded with the
+// device-wide digit-major scan of the tile histograms) give the rest.  No
+// atomics decide positions, so ties keep their input order (stability).
+template <bool PASS0>
+__global__ void __launch_bounds__(kSortThreads)
+radix_scatter_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+                     int64_t n_total, const int64_t *__restrict__ counts, int shift,
+                     int digit_bits, const uint32_t *__restrict__ hist_scanned, int64_t n_tiles,
+                     uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out) {
+    __shared__ uint32_t wcnt[kSortWarps][kMaxDigits];
+    const int n_digits = 1 << digit_bits;
+    const uint32_t mask = n_digits - 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n_valid = PASS0 ? n_total : counts[0];
+    const int64_t tile_base = blockIdx.x * (int64_t)kSortTile;
+    const int64_t wbase = tile_base + warp * (32 * kKeysPerThread);
+    for (int i = lane; i < n_digits; i += 32) wcnt[warp][i] = 0;
+    __syncwarp();
+    uint32_t key[kKeysPerThread];
+    bool ok[kKeysPerThread];
+#pragma unroll
+    for (int r = 0; r < kKeysPerThread; ++r) {
+        const int64_t j = wbase + r * 32 + lane;
+        uint32_t k = kOOR;
+        if (j < n_valid) k = keys_in[j];
+        ok[r] = (k != kOOR);
+        key[r] = k;
+    }
+#pragma unroll
+    for (int r = 0; r < kKeysPerThread; ++r) {
+        const uint32_t dg = ok[r] ? ((key[r] >> shift) & mask) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg);
+        if (ok[r] && lane == __ffs(peers) - 1) wcnt[warp][dg] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_digits; i += kSortThreads) {
+        uint32_t run = hist_scanned[(int64_t)i * n_tiles + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < kSortWarps; ++w) {
+            const uint32_t t = wcnt[w][i];
+            wcnt[w][i] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kKeysPerThread; ++r) {
+        const int64_t j = wbase + r * 32 + lane;
+        const uint32_t dg = ok[r] ? ((key[r] >> shift) & mask) : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, dg);
+        uint32_t pos = 0;
+        if (ok[r]) pos = wcnt[warp][dg] + __popc(peers & lanemask_lt());
+        __syncwarp();
+        if (ok[r] && lane == __ffs(peers) - 1) wcnt[warp][dg] += __popc(peers);
+        __syncwarp();
+        if (ok[r]) {
+            if (keys_out) keys_out[pos] = key[r];
+            vals_out[pos] = PASS0 ? static_cast<uint32_t>(j) : vals_in[j];
+        }
+    }
+}
+
+// packed[c] = (count > 0) << 32 | count: one scan yields both the first
+// rank of every cell (low word) and its interval index (high word).
+__global__ void pack_counts_kernel(const uint32_t *__restrict__ cell_count, int64_t n_cells,
+                                   unsigned long long *__restrict__ packed) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = cell_count[c];
+        packed[c] = (static_cast<unsigned long long>(k > 0) << 32) | k;
+    }
+}
+
+__global__ void make_intervals_kernel(const uint32_t *__restrict__ cell_count,
+                                      const unsigned long long *__restrict__ scanned,
+                                      const unsigned long long *__restrict__ total,
+                                      int64_t n_cells, uint32_t *__restrict__ starts,
+                                      uint32_t *__restrict__ icells,
+                                      uint32_t *__restrict__ tile_first,
+                                      int64_t *__restrict__ counts) {
+    const int64_t n_tiles = (n_cells + kTileCells - 1) / kTileCells;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cells;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long ex = scanned[c];
+        const uint32_t iv = static_cast<uint32_t>(ex >> 32);
+        if (cell_count[c] > 0) {
+            starts[iv] = static_cast<uint32_t>(ex & 0xFFFFFFFFull);
+            icells[iv] = static_cast<uint32_t>(c);
+        }
+        if (c % kTileCells == 0) tile_first[c / kTileCells] = iv;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long t = *total;
+        const uint32_t n_in = static_cast<uint32_t>(t & 0xFFFFFFFFull);
+        const uint32_t n_int = static_cast<uint32_t>(t >> 32);
+        starts[n_int] = n_in;
+        tile_first[n_tiles] = n_int;
+        counts[0] = n_in;
+        counts[1] = n_int;
+    }
+}
+
+__global__ void interval_of_point_kernel(const uint32_t *__restrict__ cells, int64_t P,
+                                         const unsigned long long *__restrict__ scanned,
+                                         uint32_t *__restrict__ iop) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = cells[p];
+        iop[p] = (c == kOOR) ? kOOR : static_cast<uint32_t>(scanned[c] >> 32);
+    }
+}
+
+// ---- workspace layout -------------------------------------------------------
+struct SortLayout {
+    int key_bits, passes, digit_bits;
+    int64_t n_tiles, hist_len;
+    size_t off_count, off_packed, off_keys_a, off_vals_a, off_keys_b, off_vals_b, off_hist,
+        off_part64, off_part32, off_total64, off_total32, bytes;
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static SortLayout sort_layout(int64_t P, int64_t n_cells) {
+    SortLayout L{};
+    int bits = 1;
+    while (bits < 32 && (int64_t(1) << bits) < n_cells) ++bits;  // keys < n_cells
+    L.key_bits = bits;
+    L.passes = (bits + kMaxDigitBits - 1) / kMaxDigitBits;
+    L.digit_bits = (bits + L.passes - 1) / L.passes;
+    L.n_tiles = ceil_div(P, kSortTile);
+    L.hist_len = (int64_t(1) << L.digit_bits) * L.n_tiles;
+    size_t o = 0;
+    L.off_count = o; o = align256(o + 4 * size_t(n_cells));
+    L.off_packed = o; o = align256(o + 8 * size_t(n_cells));
+    L.off_keys_a = o; o = align256(o + 4 * size_t(P));
+    L.off_vals_a = o; o = align256(o + 4 * size_t(P));
+    L.off_keys_b = o; o = align256(o + 4 * size_t(P));
+    L.off_vals_b = o; o = align256(o + 4 * size_t(P));
+    L.off_hist = o; o = align256(o + 4 * size_t(L.hist_len));
+    L.off_part64 = o; o = align256(o + 8 * size_t(scan_partials_len<unsigned long long>(n_cells)));
+    L.off_part32 = o; o = align256(o + 4 * size_t(scan_partials_len<uint32_t>(L.hist_len)));
+    L.off_total64 = o; o = align256(o + 8);
+    L.off_total32 = o; o = align256(o + 8);
+    L.bytes = o;
+    return L;
+}
+
+static int sort_impl(const double *cams, const FrustumParams *fp, const GridParams *gp,
+                     uint32_t *cells, int64_t P, int64_t n_cells, uint32_t *ranks,
+                     uint32_t *starts, uint32_t *icells, uint32_t *tile_first, uint32_t *iop,
+                     int64_t *counts, void *ws, size_t ws_bytes, cudaStream_t s) {
+    const SortLayout L = sort_layout(P, n_cells);
+    BVP_REQUIRE(ws != nullptr && ws_bytes >= L.bytes, BVP_ERR_INVALID,
+                "sort workspace too small: need %zu bytes, got %zu", L.bytes, ws_bytes);
+    BVP_REQUIRE(P > 0 && P < (int64_t(1) << 32) - 1, BVP_ERR_INVALID,
+                "point count %lld outside [1, 2^32-1)", (long long)P);
+    BVP_REQUIRE(n_cells > 0 && n_cells < (int64_t(1) << 32) - 1, BVP_ERR_INVALID,
+                "cell count %lld outside [1, 2^32-1)", (long long)n_cells);
+    char *w = static_cast<char *>(ws);
+    auto *cell_count = reinterpret_cast<uint32_t *>(w + L.off_count);
+    auto *packed = reinterpret_cast<unsigned long long *>(w + L.off_packed);
+    uint32_t *ka = reinterpret_cast<uint32_t *>(w + L.off_keys_a);
+    uint32_t *va = reinterpret_cast<uint32_t *>(w + L.off_vals_a);
+    uint32_t *kb = reinterpret_cast<uint32_t *>(w + L.off_keys_b);
+    uint32_t *vb = reinterpret_cast<uint32_t *>(w + L.off_vals_b);
+    auto *hist = reinterpret_cast<uint32_t *>(w + L.off_hist);
+    auto *part64 = reinterpret_cast<unsigned long long *>(w + L.off_part64);
+    auto *part32 = reinterpret_cast<uint32_t *>(w + L.off_part32);
+    auto *total64 = reinterpret_cast<unsigned long long *>(w + L.off_total64);
+    auto *total32 = reinterpret_cast<uint32_t *>(w + L.off_total32);
+
+    cudaMemsetAsync(cell_count, 0, 4 * size_t(n_cells), s);
+    const unsigned tiles = static_cast<unsigned>(L.n_tiles);
+    if (cams)
+        pass0_front_kernel<true><<<tiles, kSortThreads, 0, s>>>(
+            cams, *fp, *gp, P, cells, cell_count, L.digit_bits, hist, L.n_tiles);
+    else
+        pass0_front_kernel<false><<<tiles, kSortThreads, 0, s>>>(
+            nullptr, FrustumParams{}, GridParams{}, P, cells, cell_count, L.digit_bits, hist,
+            L.n_tiles);
+    // interval tables from the per-cell counts (independent of the sort)
+    const unsigned cb = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_cells, 256), 4096));
+    pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
+    device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
+    make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
+                                             icells, tile_first, counts);
+    if (iop) {
+        const unsigned pb = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), 8192));
+        interval_of_point_kernel<<<pb, 256, 0, s>>>(cells, P, packed, iop);
+    }
+    // LSD radix passes; pass 0 drops out-of-range points, so later passes
+    // (and the final ranks) only cover the n_in in-range points.
+    const uint32_t *kin = cells;
+    const uint32_t *vin = nullptr;
+    for (int pass = 0; pass < L.passes; ++pass) {
+        const int shift = pass * L.digit_bits;
+        const bool last = pass == L.passes - 1;
+        uint32_t *kout = last ? nullptr : ((pass & 1) ? kb : ka);
+        uint32_t *vout = last ? ranks : ((pass & 1) ? vb : va);
+        if (pass > 0)
+            radix_upsweep_kernel<<<tiles, kSortThreads, 0, s>>>(kin, counts, shift, L.digit_bits,
+                                                                hist, L.n_tiles);
+        device_excl_scan<uint32_t>(hist, hist, L.hist_len, part32, total32, s);
+        if (pass == 0)
+            radix_scatter_kernel<true><<<tiles, kSortThreads, 0, s>>>(
+                kin, nullptr, P, counts, shift, L.digit_bits, hist, L.n_tiles, kout, vout);
+        else
+            radix_scatter_kernel<false><<<tiles, kSortThreads, 0, s>>>(
+                kin, vin, P, counts, shift, L.digit_bits, hist, L.n_tiles, kout, vout);
+        kin = kout;
+        vin = vout;
+    }
+    return check_launch("sort_intervals");
+}
+
+}  // namespace bvp
+
+using namespace bvp;
+
+extern "C" {
+
+int bvp_frustum_cells(const double *cams, int N, int H, int W, int D, double depth_min,
+                      double depth_step, const double *grid, int nx, int ny,
+                      uint32_t *cell_of_point, void *stream) {
+    BVP_REQUIRE(cams && grid && cell_of_point, BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(N > 0 && H > 0 && W > 0 && D > 0 && nx > 0 && ny > 0, BVP_ERR_INVALID,
+                "frustum/grid dims must be positive");
+    const FrustumParams f{N, H, W, D, depth_min, depth_step};
+    const GridParams g{grid[0], grid[2], grid[4], grid[5], grid[6], nx, ny};
+    const int64_t P = int64_t(N) * H * W * D;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), 148 * 64));
+    frustum_cells_kernel<<<blocks, 256, 0, as_stream(stream)>>>(cams, f, g, P, cell_of_point);
+    return check_launch("frustum_cells");
+}
+
+size_t bvp_sort_workspace_bytes(int64_t n_points, int64_t n_cells) {
+    return sort_layout(n_points, n_cells).bytes;
+}
+
+int bvp_sort_intervals(const uint32_t *cell_of_point, int64_t n_points, int64_t n_cells,
+                       uint32_t *ranks, uint32_t *interval_starts, uint32_t *interval_cells,
+                       uint32_t *tile_first, uint32_t *interval_of_point, int64_t *counts,
+                       void *workspace, size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(cell_of_point && ranks && interval_starts && interval_cells && tile_first &&
+                    counts,
+                BVP_ERR_INVALID, "null pointer argument");
+    return sort_impl(nullptr, nullptr, nullptr, const_cast<uint32_t *>(cell_of_point), n_points,
+                     n_cells, ranks, interval_starts, interval_cells, tile_first,
+                     interval_of_point, counts, workspace, workspace_bytes, as_stream(stream));
+}
+
+int bvp_build_cache(const double *cams, int N, int H, int W, int D, double depth_min,
+                    double depth_step, const double *grid, int nx, int ny,
+                    uint32_t *cell_of_point, uint32_t *ranks, uint32_t *interval_starts,
+                    uint32_t *interval_cells, uint32_t *tile_first, uint32_t *interval_of_point,
+                    int64_t *counts, void *workspace, size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(cams && grid && cell_of_point && ranks && interval_starts && interval_cells &&
+                    tile_first && counts,
+                BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(N > 0 && H > 0 && W > 0 && D > 0 && nx > 0 && ny > 0, BVP_ERR_INVALID,
+                "frustum/grid dims must be positive");
+    const FrustumParams f{N, H, W, D, depth_min, depth_step};
+    const GridParams g{grid[0], grid[2], grid[4], grid[5], grid[6], nx, ny};
+    return sort_impl(cams, &f, &g, cell_of_point, int64_t(N) * H * W * D, int64_t(nx) * ny,
+                     ranks, interval_starts, interval_cells, tile_first, interval_of_point,
+                     counts, workspace, workspace_bytes, as_stream(stream));
+}
+
+}  // extern "C"

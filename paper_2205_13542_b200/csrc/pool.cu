@@ -1,0 +1,341 @@
+// pool.cu -- cached forward (reference formulation and materialised frustum),
+// layout transposes, depth softmax, reorder_weights, finiteness scan.
+//
+// Reference: pooling.py:206-221 (pool_interval), _kernels.py:22-63
+// (interval_reduce), pooling.py:243-261 (reorder_weights), lift.py:17-31
+// (normalize_depth), pooling.py:92-95 (finiteness checks).
+#include <algorithm>
+
+#include "pool_kernel.cuh"
+
+namespace bvp {
+
+// ---- (N, A, HW) -> (N, HW, A) transpose through a 32x32 shared tile --------
+template <typename T>
+__global__ void __launch_bounds__(256)
+to_nhwc_kernel(const T *__restrict__ src, int A, int HW, T *__restrict__ dst) {
+    __shared__ T t[32][33];
+    const int64_t n = blockIdx.z;
+    const int hw0 = blockIdx.x * 32, a0 = blockIdx.y * 32;
+    const T *s = src + n * int64_t(A) * HW;
+    T *d = dst + n * int64_t(A) * HW;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int a = a0 + r, hw = hw0 + threadIdx.x;
+        if (a < A && hw < HW) t[r][threadIdx.x] = s[int64_t(a) * HW + hw];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int hw = hw0 + r, a = a0 + threadIdx.x;
+        if (a < A && hw < HW) d[int64_t(hw) * A + a] = t[threadIdx.x][r];
+    }
+}
+
+template <typename T>
+void launch_to_nhwc(const T *src, int64_t NB, int A, int HW, T *dst, cudaStream_t s) {
+    if (NB == 0 || A == 0 || HW == 0) return;
+    const dim3 grid((HW + 31) / 32, (A + 31) / 32, static_cast<unsigned>(NB));
+    to_nhwc_kernel<T><<<grid, dim3(32, 8), 0, s>>>(src, A, HW, dst);
+}
+template void launch_to_nhwc<float>(const float *, int64_t, int, int, float *, cudaStream_t);
+template void launch_to_nhwc<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, int,
+                                            __nv_bfloat16 *, cudaStream_t);
+
+// ---- dispatch over the instantiated lane shapes ------------------------------
+template <typename Acc, typename Elem, int VEC, int LPP, int CPL, int SRC>
+static void launch_one(const PoolParams &p, bool is_max, dim3 grid, size_t smem,
+                       cudaStream_t s) {
+    auto k = is_max ? pool_tile_kernel<Acc, Elem, VEC, LPP, CPL, true, SRC>
+                    : pool_tile_kernel<Acc, Elem, VEC, LPP, CPL, false, SRC>;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k<<<grid, kPoolThreads, smem, s>>>(p);
+}
+
+#define BVP_SHAPE(L, CP)                                                         \
+    if (sh.lpp == L && sh.cpl == CP) {                                           \
+        launch_one<Acc, Elem, VEC, L, CP, SRC>(p, is_max, grid, smem, s);        \
+        return true;                                                             \
+    }
+
+template <typename Acc, typename Elem, int VEC, int SRC>
+struct ShapeTable;
+
+// fast fp32, 16-byte chunks
+template <typename Elem, int SRC>
+struct ShapeTable<float, Elem, 4, SRC> {
+    using Acc = float;
+    static constexpr int VEC = 4;
+    static bool launch(LaneShape sh, const PoolParams &p, bool is_max, dim3 grid, size_t smem,
+                       cudaStream_t s) {
+        BVP_SHAPE(1, 1) BVP_SHAPE(2, 1) BVP_SHAPE(4, 1) BVP_SHAPE(4, 2) BVP_SHAPE(4, 3)
+        BVP_SHAPE(4, 4) BVP_SHAPE(4, 5) BVP_SHAPE(4, 6) BVP_SHAPE(4, 8) BVP_SHAPE(8, 8)
+        BVP_SHAPE(16, 8) BVP_SHAPE(32, 8)
+        return false;
+    }
+};
+// scalar fallbacks (fast or exact) and the exact 16-byte mode: one point per
+// warp iteration, lanes over channels
+template <typename AccT, typename Elem, int VECT, int SRC>
+struct ShapeTable {
+    using Acc = AccT;
+    static constexpr int VEC = VECT;
+    static bool launch(LaneShape sh, const PoolParams &p, bool is_max, dim3 grid, size_t smem,
+                       cudaStream_t s) {
+        BVP_SHAPE(32, 1) BVP_SHAPE(32, 2) BVP_SHAPE(32, 4) BVP_SHAPE(32, 8)
+        return false;
+    }
+};
+#undef BVP_SHAPE
+
+template <typename Acc, typename Elem, int VEC, int SRC>
+static int run_pool(const PoolParams &p, int B, bool is_max, bool exact, cudaStream_t s) {
+    const int nchunks = p.C / VEC;
+    const LaneShape sh = choose_shape(nchunks, exact || VEC == 1, false);
+    BVP_REQUIRE(sh.lpp > 0, BVP_ERR_UNSUPPORTED, "channel count %d not supported (max %d)", p.C,
+                VEC == 4 ? 1024 : 256);
+    const size_t smem = size_t(p.C) * kTilePitch * sizeof(float);
+    BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
+    const int64_t n_tiles = ceil_div(p.n_cells, kTileCells);
+    const dim3 grid(static_cast<unsigned>(n_tiles), static_cast<unsigned>(B));
+    const bool ok = ShapeTable<Acc, Elem, VEC, SRC>::launch(sh, p, is_max, grid, smem, s);
+    BVP_REQUIRE(ok, BVP_ERR_UNSUPPORTED, "no kernel instance for lpp=%d cpl=%d", sh.lpp, sh.cpl);
+    return BVP_OK;
+}
+
+static int pool_dist_dispatch(PoolParams p, int B, int mode, int exact, cudaStream_t s) {
+    const bool is_max = mode == BVP_MAX;
+    p.mean = mode == BVP_MEAN;
+    if (p.C == 0) return BVP_OK;
+    const bool v4 = (p.C % 4) == 0;
+    if (exact)
+        return v4 ? run_pool<double, float, 4, kSrcDist>(p, B, is_max, true, s)
+                  : run_pool<double, float, 1, kSrcDist>(p, B, is_max, true, s);
+    return v4 ? run_pool<float, float, 4, kSrcDist>(p, B, is_max, false, s)
+              : run_pool<float, float, 1, kSrcDist>(p, B, is_max, false, s);
+}
+
+// ---- depth softmax (lift.py:17-31), 64-bit math ------------------------------
+__global__ void normalize_depth_kernel(const float *__restrict__ logits, int64_t NB, int D,
+                                       int HW, float *__restrict__ dist) {
+    const int64_t total = NB * HW;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = t / HW, hw = t - n * HW;
+        const float *l = logits + n * D * int64_t(HW) + hw;
+        float *o = dist + n * D * int64_t(HW) + hw;
+        float m = -INFINITY;
+        for (int d = 0; d < D; ++d) m = fmaxf(m, l[int64_t(d) * HW]);
+        double sum = 0.0;
+        for (int d = 0; d < D; ++d) sum += exp(double(l[int64_t(d) * HW]) - double(m));
+        for (int d = 0; d < D; ++d)
+            o[int64_t(d) * HW] = float(exp(double(l[int64_t(d) * HW]) - double(m)) / sum);
+    }
+}
+
+__global__ void any_nonfinite_kernel(const float *__restrict__ x, int64_t n, int *flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__any_sync(0xFFFFFFFFu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+__global__ void reorder_weights_kernel(const float *__restrict__ dist,
+                                       const uint32_t *__restrict__ ranks, int64_t n_in, int D,
+                                       int HW, float *__restrict__ w) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_in;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = ranks[j];
+        const uint32_t pix = p / D, d = p - pix * D;
+        const uint32_t n = pix / HW, hw = pix - n * HW;
+        w[j] = __ldg(dist + (int64_t(n) * D + d) * HW + hw);
+    }
+}
+
+// ---- materialised lift: x[(pix*D + d), c] = dist[n,d,h,w] * f[n,c,h,w] -----
+// One warp per pixel; the pixel's feature column (NCHW, strided) and depth
+// weights are staged in shared memory, then its D x C block of x -- contiguous
+// in the reference point order -- is streamed as flat float4s (fully
+// coalesced, evict-first stores).
+__global__ void __launch_bounds__(256)
+lift_kernel(const float *__restrict__ features, const float *__restrict__ dist, int64_t NP,
+            int C, int D, int HW, float *__restrict__ x) {
+    extern __shared__ float sm[];  // per warp: C + D floats
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    float *sf = sm + warp * (C + D);
+    float *sw = sf + C;
+    for (int64_t pix = blockIdx.x * 8LL + warp; pix < NP; pix += gridDim.x * 8LL) {
+        const int64_t n = pix / HW, hw = pix - n * HW;
+        __syncwarp();
+        for (int c = lane; c < C; c += 32) sf[c] = features[(n * C + c) * HW + hw];
+        for (int d = lane; d < D; d += 32) sw[d] = dist[(n * D + d) * HW + hw];
+        __syncwarp();
+        float *xo = x + pix * int64_t(D) * C;
+        const int n4 = (D * C) / 4;
+        for (int q = lane; q < n4; q += 32) {
+            const int e = q * 4;
+            const int d = e / C, c = e - d * C;  // C % 4 == 0: same d for 4 lanes' values
+            const float w = sw[d];
+            st_stream_f4(xo + e, make_float4(w * sf[c], w * sf[c + 1], w * sf[c + 2], w * sf[c + 3]));
+        }
+    }
+}
+
+__global__ void lift_scalar_kernel(const float *__restrict__ features,
+                                   const float *__restrict__ dist, int64_t NP, int C, int D,
+                                   int HW, float *__restrict__ x) {
+    const int64_t total = NP * D * int64_t(C);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = e % C, pd = e / C;
+        const int64_t d = pd % D, pix = pd / D;
+        const int64_t n = pix / HW, hw = pix - n * HW;
+        x[e] = dist[(n * D + d) * HW + hw] * features[(n * C + c) * HW + hw];
+    }
+}
+
+}  // namespace bvp
+
+using namespace bvp;
+
+extern "C" {
+
+size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W) {
+    return size_t(B) * N * C * H * W * sizeof(float);
+}
+
+int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const uint32_t *ranks,
+                              const uint32_t *interval_starts, const uint32_t *interval_cells,
+                              const uint32_t *tile_first, int B, int N, int C, int H, int W,
+                              int D, int64_t n_cells, int64_t n_int_max, int mode, int exact,
+                              float *out, uint32_t *argmax, void *stream) {
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && n_cells >= 1,
+                BVP_ERR_INVALID, "bad dims B=%d N=%d C=%d H=%d W=%d D=%d n_cells=%lld", B, N, C,
+                H, W, D, (long long)n_cells);
+    BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
+    BVP_REQUIRE(out && (C == 0 || (feats_nhwc && dist && ranks && interval_starts &&
+                                   interval_cells && tile_first)),
+                BVP_ERR_INVALID, "null pointer argument");
+    PoolParams p{};
+    p.rows = feats_nhwc;
+    p.wsrc = dist;
+    p.ranks = ranks;
+    p.starts = interval_starts;
+    p.icells = interval_cells;
+    p.tile_first = tile_first;
+    p.out = out;
+    p.argmax = mode == BVP_MAX ? argmax : nullptr;
+    p.C = C;
+    p.D = D;
+    p.HW = H * W;
+    p.NHW = N * H * W;
+    p.n_cells = n_cells;
+    p.n_int_max = n_int_max;
+    p.rows_bstride = int64_t(N) * H * W * C;
+    p.w_bstride = int64_t(N) * D * H * W;
+    const int rc = pool_dist_dispatch(p, B, mode, exact, as_stream(stream));
+    if (rc != BVP_OK) return rc;
+    return check_launch("pool_forward");
+}
+
+int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_t *ranks,
+                         const uint32_t *interval_starts, const uint32_t *interval_cells,
+                         const uint32_t *tile_first, int B, int N, int C, int H, int W, int D,
+                         int64_t n_cells, int64_t n_int_max, int mode, int exact, float *out,
+                         float *feats_nhwc, uint32_t *argmax, void *stream) {
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1, BVP_ERR_INVALID, "bad dims");
+    BVP_REQUIRE(C == 0 || (features && feats_nhwc), BVP_ERR_INVALID, "null pointer argument");
+    launch_to_nhwc<float>(features, int64_t(B) * N, C, H * W, feats_nhwc, as_stream(stream));
+    return bvp_pool_forward_nhwc_f32(feats_nhwc, dist, ranks, interval_starts, interval_cells,
+                                     tile_first, B, N, C, H, W, D, n_cells, n_int_max, mode,
+                                     exact, out, argmax, stream);
+}
+
+int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst, void *stream) {
+    BVP_REQUIRE(NB >= 0 && C >= 0 && HW >= 0, BVP_ERR_INVALID, "bad dims");
+    BVP_REQUIRE(src && dst, BVP_ERR_INVALID, "null pointer argument");
+    launch_to_nhwc<float>(src, NB, C, HW, dst, as_stream(stream));
+    return check_launch("to_nhwc");
+}
+
+int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in, int N, int D,
+                        int H, int W, float *w_sorted, void *stream) {
+    BVP_REQUIRE(n_in == 0 || (dist && ranks && w_sorted), BVP_ERR_INVALID, "null pointer");
+    (void)N;
+    if (n_in == 0) return BVP_OK;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_in, 256), 148 * 32));
+    reorder_weights_kernel<<<blocks, 256, 0, as_stream(stream)>>>(dist, ranks, n_in, D, H * W,
+                                                                  w_sorted);
+    return check_launch("reorder_weights");
+}
+
+int bvp_normalize_depth(const float *logits, int NB, int D, int H, int W, float *dist,
+                        void *stream) {
+    BVP_REQUIRE(logits && dist && NB >= 0 && D >= 1 && H >= 0 && W >= 0, BVP_ERR_INVALID,
+                "bad arguments");
+    const int64_t total = int64_t(NB) * H * W;
+    if (total == 0) return BVP_OK;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 128), 148 * 16));
+    normalize_depth_kernel<<<blocks, 128, 0, as_stream(stream)>>>(logits, NB, D, H * W, dist);
+    return check_launch("normalize_depth");
+}
+
+int bvp_any_nonfinite(const float *x, int64_t n, int *flag, void *stream) {
+    BVP_REQUIRE(flag && (n == 0 || x), BVP_ERR_INVALID, "null pointer");
+    if (n == 0) return BVP_OK;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 148 * 8));
+    any_nonfinite_kernel<<<blocks, 256, 0, as_stream(stream)>>>(x, n, flag);
+    return check_launch("any_nonfinite");
+}
+
+int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H, int W, int D,
+                 float *x, void *stream) {
+    BVP_REQUIRE(features && dist && x && N >= 1 && C >= 1 && H >= 1 && W >= 1 && D >= 1,
+                BVP_ERR_INVALID, "bad arguments");
+    cudaStream_t s = as_stream(stream);
+    const int64_t NP = int64_t(N) * H * W;
+    if (C % 4 == 0) {
+        const size_t smem = size_t(8) * (C + D) * sizeof(float);
+        BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "C + D too large for lift");
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(lift_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(NP, 8), 148 * 16));
+        lift_kernel<<<blocks, 256, smem, s>>>(features, dist, NP, C, D, H * W, x);
+    } else {
+        const int64_t total = NP * D * C;
+        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 148 * 64));
+        lift_scalar_kernel<<<blocks, 256, 0, s>>>(features, dist, NP, C, D, H * W, x);
+    }
+    return check_launch("lift");
+}
+
+int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *interval_starts,
+                        const uint32_t *interval_cells, const uint32_t *tile_first, int C,
+                        int64_t n_cells, int mode, float *out, void *stream) {
+    BVP_REQUIRE(C >= 0 && n_cells >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
+                "bad arguments");
+    BVP_REQUIRE(out && (C == 0 || (x && ranks && interval_starts && interval_cells && tile_first)),
+                BVP_ERR_INVALID, "null pointer argument");
+    if (C == 0) return BVP_OK;
+    PoolParams p{};
+    p.rows = x;
+    p.ranks = ranks;
+    p.starts = interval_starts;
+    p.icells = interval_cells;
+    p.tile_first = tile_first;
+    p.out = out;
+    p.C = C;
+    p.D = 1;
+    p.HW = 1;
+    p.n_cells = n_cells;
+    p.mean = mode == BVP_MEAN;
+    const bool is_max = mode == BVP_MAX;
+    cudaStream_t s = as_stream(stream);
+    const int rc = (C % 4 == 0) ? run_pool<float, float, 4, kSrcX>(p, 1, is_max, false, s)
+                                : run_pool<float, float, 1, kSrcX>(p, 1, is_max, false, s);
+    if (rc != BVP_OK) return rc;
+    return check_launch("pool_lifted");
+}
+
+}  // extern "C"

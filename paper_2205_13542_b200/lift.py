@@ -1,0 +1,57 @@
+"""Depth distributions (reference lift.py:17-63), computed on the GPU."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .bevgrid import cuda_device, ptr, stream_ptr
+from .errors import ValidationError
+
+
+def any_nonfinite(t: torch.Tensor) -> bool:
+    """Device finiteness scan of a float32 CUDA tensor (one host sync)."""
+    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
+    t = t.contiguous()
+    _lib.call("bvp_any_nonfinite", ptr(t), t.numel(), ptr(flag), stream_ptr(t.device))
+    return bool(flag.item())
+
+
+def normalize_depth(logits, check_finite: bool = True):
+    """Softmax over D of (N, D, H, W) (or (B, N, D, H, W)) logits.
+
+    64-bit max-subtracted softmax stored float32, like the reference
+    (lift.py:17-31).  numpy in -> numpy out (one H2D + D2H); CUDA tensor in
+    -> CUDA tensor out.
+    """
+    host = isinstance(logits, np.ndarray)
+    if host:
+        if logits.ndim != 4:
+            raise ValidationError(f"logits must be (N, D, H, W), got shape {logits.shape}")
+        t = torch.from_numpy(np.ascontiguousarray(logits, dtype=np.float32)).to(cuda_device())
+    else:
+        t = logits
+        if t.dim() not in (4, 5):
+            raise ValidationError(f"logits must be (N, D, H, W), got shape {tuple(t.shape)}")
+        if t.dtype != torch.float32:
+            t = t.float()
+        t = t.contiguous()
+    if check_finite and any_nonfinite(t):
+        raise ValidationError("logits contain non-finite values")
+    *lead, D, H, W = t.shape
+    NB = int(np.prod(lead))
+    out = torch.empty_like(t)
+    if t.numel():
+        _lib.call("bvp_normalize_depth", ptr(t), NB, D, H, W, ptr(out), stream_ptr(t.device))
+    return out.cpu().numpy() if host else out
+
+
+def point_weight(dist, n: int, h: int, w: int, d: int) -> float:
+    """Depth probability of frustum point (n, h, w, d) (scalar accessor)."""
+    n_cams, n_bins, height, width = dist.shape
+    for name, value, bound in (("camera", n, n_cams), ("row", h, height), ("col", w, width),
+                               ("depth bin", d, n_bins)):
+        if not 0 <= value < bound:
+            raise IndexError(f"{name} index {value} out of range [0, {bound})")
+    return float(dist[n, d, h, w])

@@ -1,0 +1,400 @@
+"""BEV pooling on the B200: the reference's pooling contract, GPU backends.
+
+Drop-in for the reference's pooling module (pooling.py:1-261):
+
+    value(g, c) = reducer over { dist[n,d,h,w] * features[n,c,h,w] :
+                                 cell_of_point[(n,h,w,d)] = g },  empty -> 0
+
+Backends (``pool(..., backend=...)``):
+  interval   the fast path: cell-tiled interval reduction, one non-atomic
+             store per (channel, cell) (csrc/pool_kernel.cuh).  ``exact=True``
+             accumulates in 64 bits in rank order and is bit-identical to the
+             reference's interval_reduce; ``exact=False`` accumulates in fp32.
+  prefixsum  the paper's "before" (LSS cumsum trick), kept wasteful on purpose.
+The reference's "naive" scatter is its CPU oracle; it is not a GPU backend.
+
+Inputs may be numpy arrays (reference semantics: result is a numpy
+BevFeatureMap; one H2D/D2H) or CUDA tensors (result stays on the device;
+5-D (B, N, C, H, W) / (B, N, D, H, W) batches are accepted and pooled in one
+launch into (B, C, nx, ny)).
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .bevgrid import AssociationCache, BevGridSpec, cuda_device, ptr, stream_ptr
+from .errors import ConfigurationError, StaleCacheError, UnsupportedReducerError, ValidationError
+from .lift import any_nonfinite
+
+#: exact (bit-identical, 64-bit) accumulation by default, like the reference
+DEFAULT_EXACT = True
+
+
+class Reducer(enum.Enum):
+    SUM = "sum"
+    MEAN = "mean"
+    MAX = "max"
+
+    @classmethod
+    def parse(cls, name: str) -> "Reducer":
+        try:
+            return cls(name.lower())
+        except ValueError:
+            raise ConfigurationError(
+                f"unknown reducer {name!r}; expected one of {[r.value for r in cls]}") from None
+
+
+_MODE = {Reducer.SUM: _lib.BVP_SUM, Reducer.MEAN: _lib.BVP_MEAN, Reducer.MAX: _lib.BVP_MAX}
+
+BACKENDS = ("prefixsum", "interval")
+
+
+def _reducer(r) -> Reducer:
+    return r if isinstance(r, Reducer) else Reducer.parse(str(r))
+
+
+@dataclass(eq=False)
+class BevFeatureMap:
+    """Dense C x nx x ny float32 BEV features (numpy or CUDA tensor);
+    batched CUDA results are B x C x nx x ny."""
+
+    values: object
+    grid: BevGridSpec
+
+    def __post_init__(self):
+        shape = tuple(self.values.shape)
+        ok_rank = len(shape) == 3 or (len(shape) == 4 and isinstance(self.values, torch.Tensor))
+        if not ok_rank or shape[-2:] != (self.grid.nx, self.grid.ny):
+            raise ValidationError(
+                f"values shape {shape} does not match grid ({self.grid.nx}, {self.grid.ny})")
+        dt = self.values.dtype
+        if dt not in (np.float32, torch.float32):
+            raise ValidationError(f"values must be float32, got {dt}")
+
+    @property
+    def channels(self) -> int:
+        return self.values.shape[-3]
+
+
+# --------------------------------------------------------------------------
+# input handling (reference _check_inputs, pooling.py:76-115)
+# --------------------------------------------------------------------------
+
+@dataclass
+class _Inputs:
+    feats: torch.Tensor     # (B, N, C, H, W) float32 CUDA, contiguous
+    dist: torch.Tensor      # (B, N, D, H, W)
+    host: bool
+    batched: bool
+    B: int
+    N: int
+    C: int
+    H: int
+    W: int
+    D: int
+
+
+def _check_inputs(features, dist, cache: AssociationCache, grid: BevGridSpec,
+                  check_finite: bool = True) -> _Inputs:
+    host = isinstance(features, np.ndarray)
+    if host:
+        if features.ndim != 4:
+            raise ValidationError("features must be an (N, C, H, W) ndarray")
+        if not isinstance(dist, np.ndarray) or dist.ndim != 4:
+            raise ValidationError("dist must be an (N, D, H, W) ndarray")
+        if features.dtype != np.float32 or dist.dtype != np.float32:
+            raise ValidationError(
+                f"features and dist must be float32, got {features.dtype} and {dist.dtype}")
+    else:
+        if not isinstance(features, torch.Tensor) or features.dim() not in (4, 5):
+            raise ValidationError("features must be an (N, C, H, W) array or CUDA tensor")
+        if not isinstance(dist, torch.Tensor) or dist.dim() != features.dim():
+            raise ValidationError("dist must be an (N, D, H, W) tensor like features")
+        if features.dtype != torch.float32 or dist.dtype != torch.float32:
+            raise ValidationError(
+                f"features and dist must be float32, got {features.dtype} and {dist.dtype}")
+    batched = len(features.shape) == 5
+    fs = tuple(features.shape) if batched else (1, *features.shape)
+    ds = tuple(dist.shape) if batched else (1, *dist.shape)
+    B, n, c, h, w = fs
+    Bd, nd, d, hd, wd = ds
+    if (B, n, h, w) != (Bd, nd, hd, wd):
+        raise ValidationError(
+            f"features {tuple(features.shape)} and dist {tuple(dist.shape)} disagree on (N, H, W)")
+    dev = cuda_device(None if host else features.device)
+    if host:
+        ft = torch.from_numpy(np.ascontiguousarray(features)).to(dev).view(fs)
+        dt = torch.from_numpy(np.ascontiguousarray(dist)).to(dev).view(ds)
+    else:
+        if not features.is_cuda or not dist.is_cuda:
+            raise ValidationError("tensors must live on a CUDA device")
+        ft = features.contiguous().view(fs)
+        dt = dist.contiguous().view(ds)
+    if check_finite:
+        if ft.numel() and any_nonfinite(ft):
+            raise ValidationError("features contain non-finite values")
+        if dt.numel() and any_nonfinite(dt):
+            raise ValidationError("dist contains non-finite values")
+    if cache.n_points != n * h * w * d:
+        raise StaleCacheError(
+            f"cache covers {cache.n_points} points but the workload has {n * h * w * d} "
+            f"(N*H*W*D for N={n}, H={h}, W={w}, D={d})")
+    if cache.grid is not None and cache.grid != grid:
+        raise StaleCacheError("cache was built for a different BEV grid")
+    if cache.frustum is not None and (
+            cache.n_cameras != n or cache.frustum.height != h or cache.frustum.width != w
+            or cache.frustum.depth_bins != d):
+        raise StaleCacheError("cache was built for a different rig/frustum")
+    if cache.grid is None and cache.n_intervals and int(cache.interval_cells.max()) >= grid.n_cells:
+        raise StaleCacheError(
+            "cache contains cell ids beyond this grid; it was built for a different grid")
+    return _Inputs(ft, dt, host, batched, B, n, c, h, w, d)
+
+
+def _finish(out: torch.Tensor, inp: _Inputs, grid: BevGridSpec) -> BevFeatureMap:
+    shape = (inp.B, inp.C, grid.nx, grid.ny)
+    v = out.view(shape)
+    if not inp.batched:
+        v = v[0]
+    if inp.host:
+        v = v.cpu().numpy()
+    return BevFeatureMap(v, grid)
+
+
+# --------------------------------------------------------------------------
+# backends
+# --------------------------------------------------------------------------
+
+def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
+                  reducer=Reducer.SUM, *, exact: bool | None = None,
+                  check_finite: bool = True) -> BevFeatureMap:
+    """Interval-reduction pooling (reference pooling.py:206-221) on the GPU."""
+    reducer = _reducer(reducer)
+    inp = _check_inputs(features, dist, cache, grid, check_finite)
+    cache = cache.for_grid(grid.n_cells)
+    out = torch.empty((inp.B, inp.C, grid.n_cells), dtype=torch.float32, device=inp.feats.device)
+    if inp.C:
+        nhwc = torch.empty(inp.feats.numel(), dtype=torch.float32, device=inp.feats.device)
+        _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
+                  ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
+                  ptr(cache.d_tile_first), inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
+                  grid.n_cells, cache.n_int_max, _MODE[reducer],
+                  int(DEFAULT_EXACT if exact is None else exact), ptr(out), ptr(nhwc), None,
+                  stream_ptr(inp.feats.device))
+    return _finish(out, inp, grid)
+
+
+def pool_prefixsum(features, dist, cache: AssociationCache, grid: BevGridSpec,
+                   reducer=Reducer.SUM, *, check_finite: bool = True) -> BevFeatureMap:
+    """The LSS cumsum baseline (reference pooling.py:162-196) on the GPU."""
+    reducer = _reducer(reducer)
+    if reducer is Reducer.MAX:
+        raise UnsupportedReducerError(
+            "prefix-sum cannot express max; use the interval backend")
+    inp = _check_inputs(features, dist, cache, grid, check_finite)
+    if inp.batched:
+        raise ConfigurationError("the prefix-sum baseline pools one sample at a time")
+    cache = cache.for_grid(grid.n_cells)
+    dev = inp.feats.device
+    out = torch.empty((1, inp.C, grid.n_cells), dtype=torch.float32, device=dev)
+    n_in, n_int = cache.n_in_range, cache.n_intervals
+    ws = torch.empty(_lib.load().bvp_prefixsum_workspace_bytes(n_in, inp.C), dtype=torch.uint8,
+                     device=dev)
+    _lib.call("bvp_pool_prefixsum_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
+              ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), n_in, n_int, inp.N,
+              inp.C, inp.H, inp.W, inp.D, grid.n_cells, _MODE[reducer], ptr(out), ptr(ws),
+              ws.numel(), stream_ptr(dev))
+    return _finish(out, inp, grid)
+
+
+class PoolPlan:
+    """Pre-planned cached forward for fixed shapes (the serving loop).
+
+    Output, NHWC staging and pinned host buffers are allocated once; ``run``
+    is exactly two kernel launches on the current stream (features -> NHWC
+    transpose, interval reduction) with no validation and no host sync, so
+    it can be captured in a CUDA graph.  ``run_host`` is the end-to-end
+    drop-in for host (numpy) buffers: pinned H2D of features + dist, run,
+    D2H of the (C, nx, ny) map.
+    """
+
+    def __init__(self, cache: AssociationCache, grid: BevGridSpec, n_cameras: int,
+                 channels: int, height: int, width: int, depth_bins: int, batch: int = 1,
+                 reducer=Reducer.SUM, exact: bool | None = None, device=None):
+        self.dev = cuda_device(device if device is not None else cache.device)
+        if cache.n_points != n_cameras * height * width * depth_bins:
+            raise StaleCacheError("cache does not match the planned frustum")
+        self.cache = cache.for_grid(grid.n_cells)
+        self.grid = grid
+        self.B, self.N, self.C, self.H, self.W, self.D = (batch, n_cameras, channels, height,
+                                                          width, depth_bins)
+        self.mode = _MODE[_reducer(reducer)]
+        self.exact = int(DEFAULT_EXACT if exact is None else exact)
+        f32 = dict(dtype=torch.float32, device=self.dev)
+        self.out = torch.empty((batch, channels, grid.n_cells), **f32)
+        self.nhwc = torch.empty(batch * n_cameras * height * width * channels, **f32)
+        self._host = None
+
+    @property
+    def feature_shape(self):
+        return (self.B, self.N, self.C, self.H, self.W)
+
+    @property
+    def dist_shape(self):
+        return (self.B, self.N, self.D, self.H, self.W)
+
+    def transpose(self, features: torch.Tensor) -> None:
+        _lib.call("bvp_to_nhwc_f32", ptr(features), self.B * self.N, self.C, self.H * self.W,
+                  ptr(self.nhwc), stream_ptr(self.dev))
+
+    def reduce(self, dist: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        out = self.out if out is None else out
+        c = self.cache
+        _lib.call("bvp_pool_forward_nhwc_f32", ptr(self.nhwc), ptr(dist), ptr(c.d_ranks),
+                  ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_tile_first), self.B,
+                  self.N, self.C, self.H, self.W, self.D, self.grid.n_cells, c.n_int_max,
+                  self.mode, self.exact, ptr(out), None, stream_ptr(self.dev))
+        return out
+
+    def run(self, features: torch.Tensor, dist: torch.Tensor,
+            out: torch.Tensor | None = None) -> torch.Tensor:
+        """features (B,N,C,H,W) / dist (B,N,D,H,W) contiguous float32 CUDA."""
+        self.transpose(features)
+        return self.reduce(dist, out)
+
+    def run_host(self, features, dist) -> np.ndarray:
+        """Host buffers in, host BEV map out.  Pinned CPU tensors are copied
+        straight to the device; numpy arrays are staged through pinned
+        buffers first.  Returns a view of the pinned output buffer."""
+        if self._host is None:
+            pin = dict(dtype=torch.float32, pin_memory=True)
+            self._host = (torch.empty(self.feature_shape, **pin), torch.empty(self.dist_shape, **pin),
+                          torch.empty(tuple(self.out.shape), **pin),
+                          torch.empty(self.feature_shape, dtype=torch.float32, device=self.dev),
+                          torch.empty(self.dist_shape, dtype=torch.float32, device=self.dev))
+        hf, hd, ho, df, dd = self._host
+        if isinstance(features, torch.Tensor) and features.is_pinned():
+            hf = features.view(self.feature_shape)
+        else:
+            hf.numpy()[...] = np.asarray(features, dtype=np.float32).reshape(self.feature_shape)
+        if isinstance(dist, torch.Tensor) and dist.is_pinned():
+            hd = dist.view(self.dist_shape)
+        else:
+            hd.numpy()[...] = np.asarray(dist, dtype=np.float32).reshape(self.dist_shape)
+        df.copy_(hf, non_blocking=True)
+        dd.copy_(hd, non_blocking=True)
+        self.run(df, dd)
+        ho.copy_(self.out, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        return ho.numpy().reshape(self.B, self.C, self.grid.nx, self.grid.ny)
+
+    @property
+    def h2d_bytes(self) -> int:
+        return 4 * (int(np.prod(self.feature_shape)) + int(np.prod(self.dist_shape)))
+
+    @property
+    def d2h_bytes(self) -> int:
+        return 4 * self.out.numel()
+
+
+_BACKEND_FN = {"prefixsum": pool_prefixsum, "interval": pool_interval}
+
+
+def pool(features, dist, cache, grid, reducer=Reducer.SUM, backend: str = "interval",
+         **kwargs) -> BevFeatureMap:
+    """Dispatch to the named backend (reference pooling.py:231-240)."""
+    try:
+        fn = _BACKEND_FN[backend]
+    except KeyError:
+        raise ConfigurationError(
+            f"unknown backend {backend!r}; expected one of {BACKENDS}") from None
+    return fn(features, dist, cache, grid, reducer, **kwargs)
+
+
+def reorder_weights(dist, cache: AssociationCache):
+    """Depth weights of the in-range points in cell-sorted order -- the cached
+    association (reference pooling.py:243-261): a pure GPU gather by ranks."""
+    host = isinstance(dist, np.ndarray)
+    if len(dist.shape) != 4:
+        raise ValidationError(f"dist must be (N, D, H, W), got {tuple(dist.shape)}")
+    nd, d_, hd, wd = dist.shape
+    if cache.n_points != nd * hd * wd * d_:
+        raise StaleCacheError(
+            f"cache covers {cache.n_points} points, dist implies {nd * hd * wd * d_}")
+    dev = cache.device
+    dt = (torch.from_numpy(np.ascontiguousarray(dist, dtype=np.float32)).to(dev) if host
+          else dist.float().contiguous())
+    n_in = cache.n_in_range
+    w = torch.empty(n_in, dtype=torch.float32, device=dev)
+    _lib.call("bvp_reorder_weights", ptr(dt), ptr(cache.d_ranks), n_in, nd, d_, hd, wd, ptr(w),
+              stream_ptr(dev))
+    return w.cpu().numpy() if host else w
+
+
+# --------------------------------------------------------------------------
+# the paper's materialised formulation and the fused bf16 path
+# --------------------------------------------------------------------------
+
+def lift_features(features: torch.Tensor, dist: torch.Tensor) -> torch.Tensor:
+    """Materialise the frustum x (P, C) = dist (x) features in reference point
+    order -- the input of the paper's bev_pool."""
+    if features.dim() != 4 or dist.dim() != 4:
+        raise ValidationError("features (N,C,H,W) and dist (N,D,H,W) expected")
+    N, C, H, W = features.shape
+    D = dist.shape[1]
+    f = features.float().contiguous()
+    d = dist.float().contiguous()
+    x = torch.empty((N * H * W * D, C), dtype=torch.float32, device=f.device)
+    _lib.call("bvp_lift_f32", ptr(f), ptr(d), N, C, H, W, D, ptr(x), stream_ptr(f.device))
+    return x
+
+
+def pool_lifted(x: torch.Tensor, cache: AssociationCache, grid: BevGridSpec,
+                reducer=Reducer.SUM) -> BevFeatureMap:
+    """Interval pooling of materialised frustum rows x (P, C) (fp32 accumulate)."""
+    reducer = _reducer(reducer)
+    if x.dim() != 2 or x.shape[0] != cache.n_points or x.dtype != torch.float32:
+        raise ValidationError("x must be float32 (n_points, C)")
+    cache = cache.for_grid(grid.n_cells)
+    C = x.shape[1]
+    x = x.contiguous()
+    out = torch.empty((C, grid.n_cells), dtype=torch.float32, device=x.device)
+    _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
+              ptr(cache.d_interval_cells), ptr(cache.d_tile_first), C, grid.n_cells,
+              _MODE[reducer], ptr(out), stream_ptr(x.device))
+    return BevFeatureMap(out.view(C, grid.nx, grid.ny), grid)
+
+
+def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCache,
+               grid: BevGridSpec, reducer=Reducer.SUM) -> BevFeatureMap:
+    """Fused lift+pool: pool(softmax_D(logits) (x) context) without forming
+    either the depth distribution or the frustum; bf16 in, fp32 accumulate."""
+    reducer = _reducer(reducer)
+    if logits.dim() not in (4, 5) or context.dim() != logits.dim():
+        raise ValidationError("logits (N,D,H,W) and context (N,C,H,W) expected")
+    batched = logits.dim() == 5
+    lg = (logits if batched else logits[None]).to(torch.bfloat16).contiguous()
+    cx = (context if batched else context[None]).to(torch.bfloat16).contiguous()
+    B, N, D, H, W = lg.shape
+    C = cx.shape[2]
+    if tuple(cx.shape) != (B, N, C, H, W):
+        raise ValidationError("logits and context disagree on (B, N, H, W)")
+    if cache.n_points != N * H * W * D:
+        raise StaleCacheError("cache does not match the logits' frustum")
+    cache = cache.for_grid(grid.n_cells)
+    dev = lg.device
+    out = torch.empty((B, C, grid.n_cells), dtype=torch.float32, device=dev)
+    ws = torch.empty(_lib.load().bvp_fused_workspace_bytes(B, N, C, H, W), dtype=torch.uint8,
+                     device=dev)
+    _lib.call("bvp_fused_pool_bf16", ptr(lg), ptr(cx), ptr(cache.d_ranks),
+              ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_tile_first),
+              B, N, C, H, W, D, grid.n_cells, _MODE[reducer], ptr(out), ptr(ws), ws.numel(),
+              stream_ptr(dev))
+    v = out.view(B, C, grid.nx, grid.ny)
+    return BevFeatureMap(v if batched else v[0], grid)

@@ -56,6 +56,7 @@ def record(rig, frustum, grid, features, logits):
         "n_in": int(cache.n_in_range),
         "n_int": int(cache.n_intervals),
         "nx": int(grid.nx), "ny": int(grid.ny),
+        "fingerprint": int(cache.fingerprint),
         "sha256": {
             "cell_of_point": sha(cache.cell_of_point.astype("<u4")),
             "ranks": sha(cache.ranks.astype("<u4")),

@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (golden SHA-256 digests) and the CPU oracle.
+
+Bars (BASELINE.json north_star): cell ids / ranks / interval tables
+bit-exact; pooled features bit-exact in exact (64-bit) mode and within 1e-5
+(max |a-b| / max(1,|a|)) in fast fp32 mode; 1e-2 for the bf16 fused path.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2205_13542_b200 as bp
+from conftest import max_rel_dev, sha
+from instances import GOLDEN_INSTANCES, random_instance
+from oracle import oracle as o
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 1e-2
+
+
+def rig_of(cams):
+    return [bp.CameraCalibration(fx=r[0], fy=r[1], cx=r[2], cy=r[3], rotation=r[4:13].reshape(3, 3),
+                                 translation=r[13:16], camera_id=k) for k, r in enumerate(cams)]
+
+
+def specs_of(inst):
+    frustum = bp.FrustumSpec(inst.height, inst.width, inst.depth_min, inst.depth_step,
+                             inst.depth_bins)
+    return frustum, bp.BevGridSpec(*inst.grid)
+
+
+def check_against_golden(entry, cache, features, dist_np, grid, exact_pools=True):
+    assert cache.n_in_range == entry["n_in"]
+    assert cache.n_intervals == entry["n_int"]
+    h = entry["sha256"]
+    assert sha(cache.cell_of_point.astype("<u4")) == h["cell_of_point"]
+    assert sha(cache.ranks.astype("<u4")) == h["ranks"]
+    assert sha(cache.interval_starts.astype("<u4")) == h["interval_starts"]
+    assert sha(cache.interval_cells.astype("<u4")) == h["interval_cells"]
+    if exact_pools:
+        for red in bp.Reducer:
+            out = bp.pool_interval(features, dist_np, cache, grid, red, exact=True)
+            assert sha(out.values.astype("<f4")) == h[f"pool_{red.value}"], red
+
+
+# ---- geometry + sort + exact pooling, bit-exact vs the reference ----------
+
+@pytest.mark.parametrize("name", ["T", "S", "H"])
+def test_config_bit_exact_vs_reference(golden, name):
+    spec = bp.CONFIGS[name]
+    rig, features, logits, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    dist = o.normalize_depth(logits)  # reference-identical weights
+    check_against_golden(golden["configs"][name], cache, features, dist, grid)
+
+
+@pytest.mark.parametrize("seed,mhw,md,mc", GOLDEN_INSTANCES)
+def test_instances_bit_exact_vs_reference(golden, seed, mhw, md, mc):
+    inst = random_instance(seed, mhw, md, mc)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    check_against_golden(golden["instances"][str(seed)], cache, inst.features,
+                         o.normalize_depth(inst.logits), grid)
+
+
+@pytest.mark.parametrize("name", ["T", "S"])
+def test_fast_mode_within_tolerance(name):
+    spec = bp.CONFIGS[name]
+    rig, features, logits, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    dist = o.normalize_depth(logits)
+    for red in bp.Reducer:
+        want = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
+                               cache.interval_cells, grid.n_cells, red.value)
+        got = bp.pool_interval(features, dist, cache, grid, red, exact=False)
+        assert max_rel_dev(want, got.values.reshape(want.shape)) <= FP32_TOL, red
+
+
+@pytest.mark.parametrize("seed", [10_000 + s for s in range(6)] + [100, 101, 300])
+def test_fast_mode_random_instances(seed):
+    inst = random_instance(seed, 64, 32, 16)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    dist = o.normalize_depth(inst.logits)
+    for red in bp.Reducer:
+        want = o.pool_naive(inst.features, dist, cache.cell_of_point, grid.n_cells, red.value)
+        got = bp.pool_interval(inst.features, dist, cache, grid, red, exact=False)
+        assert max_rel_dev(want, got.values.reshape(want.shape)) <= FP32_TOL
+
+
+def test_normalize_depth_matches_reference(golden):
+    for name in ("T", "S"):
+        spec = bp.CONFIGS[name]
+        _, _, logits, _ = bp.gen_workload(spec)
+        got = bp.normalize_depth(logits)
+        want = o.normalize_depth(logits)
+        assert np.abs(got.astype(np.float64) - want).max() <= 1e-7
+        assert (got == want).mean() > 0.999
+
+
+# ---- reference KATs (test_pooling.py:141-183, test_bevgrid.py:77-172) ------
+
+def worked_example():
+    frustum = bp.FrustumSpec(1, 4, depth_min=1.0, depth_step=1.0, depth_bins=1)
+    grid = bp.BevGridSpec(0.0, 1.2, 0.0, 0.4, -1, 1, r=0.4)
+    cache = bp.cache_from_cells(np.array([2, 0, 2, 1], np.uint32), grid.n_cells, 0, 1, frustum, grid)
+    features = np.array([1, 2, 3, 4], np.float32).reshape(1, 1, 1, 4)
+    dist = np.ones((1, 1, 1, 4), np.float32)
+    return features, dist, cache, grid
+
+
+@pytest.mark.parametrize("exact", [True, False])
+@pytest.mark.parametrize("red,want", [("sum", [2, 4, 4]), ("mean", [2, 4, 2]), ("max", [2, 4, 3])])
+def test_worked_example(red, want, exact):
+    f, d, cache, grid = worked_example()
+    np.testing.assert_array_equal(cache.ranks, [1, 3, 0, 2])
+    np.testing.assert_array_equal(cache.interval_starts, [0, 1, 2])
+    np.testing.assert_array_equal(cache.interval_cells, [0, 1, 2])
+    out = bp.pool(f, d, cache, grid, bp.Reducer(red), exact=exact)
+    np.testing.assert_array_equal(out.values.reshape(3), want)
+
+
+@pytest.mark.parametrize("red", ["sum", "mean"])
+def test_prefixsum_backend(red):
+    f, d, cache, grid = worked_example()
+    out = bp.pool(f, d, cache, grid, bp.Reducer(red), backend="prefixsum")
+    np.testing.assert_array_equal(out.values.reshape(3), [2, 4, 4] if red == "sum" else [2, 4, 2])
+    inst = random_instance(10_003, 64, 32, 16)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    dist = o.normalize_depth(inst.logits)
+    want = o.pool_naive(inst.features, dist, cache.cell_of_point, grid.n_cells, red)
+    got = bp.pool(inst.features, dist, cache, grid, bp.Reducer(red), backend="prefixsum")
+    assert max_rel_dev(want, got.values.reshape(want.shape)) < 1e-4
+
+
+def test_one_hot_distribution_places_full_feature():
+    rotation = np.column_stack([[0.0, -1.0, 0.0], [-1.0, 0.0, 0.0], [0.0, 0.0, -1.0]])
+    cam = bp.CameraCalibration(fx=1, fy=1, cx=0, cy=0, rotation=rotation,
+                               translation=np.array([0.2, 0.2, 4.0]))
+    frustum = bp.FrustumSpec(1, 1, depth_min=0.5, depth_step=0.5, depth_bins=6)
+    grid = bp.BevGridSpec(-2, 2, -2, 2, -5, 5, r=0.4)
+    cache = bp.build_cache([cam], frustum, grid)
+    assert cache.n_intervals == 1 and cache.n_in_range == 6
+    assert int(cache.interval_cells[0]) == bp.quantize(grid, (0.2, 0.2, 0.0))
+    features = np.full((1, 3, 1, 1), 7.5, np.float32)
+    dist = np.zeros((1, 6, 1, 1), np.float32)
+    dist[0, 2, 0, 0] = 1.0
+    for backend in bp.BACKENDS:
+        flat = bp.pool(features, dist, cache, grid, bp.Reducer.SUM, backend).values.reshape(3, -1)
+        np.testing.assert_allclose(flat[:, int(cache.interval_cells[0])], 7.5, atol=1e-6)
+        assert np.count_nonzero(flat) == 3
+
+
+@pytest.mark.parametrize("backend", bp.BACKENDS)
+def test_zero_weights_give_zero_map(backend):
+    f, d, cache, grid = worked_example()
+    assert not bp.pool(f, np.zeros_like(d), cache, grid, bp.Reducer.SUM, backend).values.any()
+
+
+@pytest.mark.parametrize("backend", bp.BACKENDS)
+def test_empty_ranks_give_zero_map(backend):
+    frustum = bp.FrustumSpec(1, 4, 1.0, 1.0, 1)
+    grid = bp.BevGridSpec(0.0, 1.2, 0.0, 0.4, -1, 1, r=0.4)
+    cache = bp.cache_from_cells(np.full(4, bp.OUT_OF_RANGE, np.uint32), grid.n_cells, 0, 1,
+                                frustum, grid)
+    assert cache.n_in_range == 0 and cache.n_intervals == 0
+    out = bp.pool(np.ones((1, 2, 1, 4), np.float32), np.ones((1, 1, 1, 4), np.float32), cache,
+                  grid, bp.Reducer.SUM, backend)
+    assert out.values.shape == (2, 3, 1) and not out.values.any()
+
+
+@pytest.mark.parametrize("backend", bp.BACKENDS)
+def test_zero_channels(backend):
+    inst = random_instance(17)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    out = bp.pool(inst.features[:, :0], o.normalize_depth(inst.logits), cache, grid,
+                  bp.Reducer.SUM, backend)
+    assert out.values.shape == (0, grid.nx, grid.ny)
+
+
+def test_all_points_out_of_range():
+    inst = random_instance(0)
+    frustum, _ = specs_of(inst)
+    tiny = bp.BevGridSpec(1000, 1001, 1000, 1001, -1, 1, r=1.0)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, tiny)
+    assert cache.n_in_range == 0 and cache.n_intervals == 0
+
+
+def test_bit_identical_rebuild_and_rerun():
+    spec = bp.CONFIGS["S"]
+    rig, features, logits, grid = bp.gen_workload(spec)
+    a = bp.build_cache(rig, spec.frustum, grid)
+    b = bp.build_cache(rig, spec.frustum, grid)
+    assert bp.serialize_cache(a) == bp.serialize_cache(b)
+    dist = o.normalize_depth(logits)
+    for exact in (True, False):
+        x = bp.pool_interval(features, dist, a, grid, exact=exact).values
+        y = bp.pool_interval(features, dist, a, grid, exact=exact).values
+        assert x.tobytes() == y.tobytes()
+
+
+def test_cache_round_trip(tmp_path):
+    inst = random_instance(9)
+    frustum, grid = specs_of(inst)
+    rig = rig_of(inst.cams)
+    cache = bp.build_cache(rig, frustum, grid)
+    path = tmp_path / "cache.bvpc"
+    bp.save_cache(path, cache)
+    loaded = bp.load_cache(path)
+    assert loaded.fingerprint == cache.fingerprint
+    np.testing.assert_array_equal(loaded.ranks, cache.ranks)
+    assert bp.validate_cache(loaded, rig, frustum, grid)
+    dist = o.normalize_depth(inst.logits)
+    a = bp.pool_interval(inst.features, dist, cache, grid).values
+    b = bp.pool_interval(inst.features, dist, loaded, grid).values
+    assert a.tobytes() == b.tobytes()
+
+
+def test_reorder_weights_matches_rank_order():
+    inst = random_instance(40)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    dist = o.normalize_depth(inst.logits)
+    w = bp.reorder_weights(dist, cache)
+    np.testing.assert_array_equal(w, o.reorder_weights(dist, cache.ranks))
+
+
+class TestErrors:
+    def test_unknown_backend(self):
+        f, d, cache, grid = worked_example()
+        with pytest.raises(bp.ConfigurationError, match="backend"):
+            bp.pool(f, d, cache, grid, bp.Reducer.SUM, "gpu")
+
+    def test_prefixsum_rejects_max(self):
+        f, d, cache, grid = worked_example()
+        with pytest.raises(bp.UnsupportedReducerError):
+            bp.pool(f, d, cache, grid, bp.Reducer.MAX, "prefixsum")
+
+    def test_shape_dtype_finite(self):
+        f, d, cache, grid = worked_example()
+        with pytest.raises(bp.ValidationError):
+            bp.pool_interval(f[:, :, :, :2], d, cache, grid)
+        with pytest.raises(bp.ValidationError, match="float32"):
+            bp.pool_interval(f.astype(np.float64), d, cache, grid)
+        bad = f.copy()
+        bad[0, 0, 0, 0] = np.nan
+        with pytest.raises(bp.ValidationError, match="finite"):
+            bp.pool_interval(bad, d, cache, grid)
+
+    def test_stale_cache(self):
+        f, d, cache, grid = worked_example()
+        with pytest.raises(bp.StaleCacheError):
+            bp.pool_interval(np.ones((1, 1, 1, 5), np.float32), np.ones((1, 1, 1, 5), np.float32),
+                             cache, grid)
+        with pytest.raises(bp.StaleCacheError):
+            bp.pool_interval(f, d, cache, bp.BevGridSpec(0.0, 2.4, 0.0, 0.8, -1, 1, r=0.4))
+
+
+# ---- device tensors, batching, materialised and fused paths ---------------
+
+def _S():
+    spec = bp.CONFIGS["S"]
+    rig, features, logits, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    return spec, features, logits, grid, cache
+
+
+def test_batched_device_pool_matches_per_sample():
+    spec, features, logits, grid, cache = _S()
+    dev = torch.device("cuda")
+    feats = []
+    dists = []
+    for seed in range(3):
+        _, f, lg, _ = bp.gen_workload(bp.WorkloadSpec(6, spec.frustum, grid, 80, seed))
+        feats.append(torch.from_numpy(f))
+        dists.append(torch.from_numpy(o.normalize_depth(lg)))
+    F = torch.stack(feats).to(dev)
+    Dd = torch.stack(dists).to(dev)
+    out = bp.pool_interval(F, Dd, cache, grid, exact=True).values
+    assert out.shape == (3, 80, grid.nx, grid.ny)
+    for b in range(3):
+        one = bp.pool_interval(F[b], Dd[b], cache, grid, exact=True).values
+        assert torch.equal(out[b], one)
+
+
+def test_materialised_lift_and_pool():
+    spec, features, logits, grid, cache = _S()
+    dist = o.normalize_depth(logits)
+    dev = torch.device("cuda")
+    x = bp.lift_features(torch.from_numpy(features).to(dev), torch.from_numpy(dist).to(dev))
+    assert x.shape == (cache.n_points, 80)
+    # lift is an exact fp32 product: spot-check rows against the oracle
+    rows = np.random.default_rng(0).choice(cache.n_points, 4096, replace=False)
+    want_x = o.lift(features, dist)[rows]
+    np.testing.assert_array_equal(x[torch.from_numpy(rows).to(dev)].cpu().numpy(), want_x)
+    for red in bp.Reducer:
+        got = bp.pool_lifted(x, cache, grid, red).values.cpu().numpy()
+        want = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
+                               cache.interval_cells, grid.n_cells, red.value)
+        assert max_rel_dev(want, got.reshape(want.shape)) <= FP32_TOL
+
+
+def test_fused_bf16_path():
+    spec, features, logits, grid, cache = _S()
+    dev = torch.device("cuda")
+    ctx = torch.from_numpy(features).to(dev).to(torch.bfloat16)
+    lg = torch.from_numpy(logits).to(dev).to(torch.bfloat16)
+    fb = o.bf16_round(features)
+    lb = o.bf16_round(logits)
+    for red in bp.Reducer:
+        got = bp.pool_fused(lg, ctx, cache, grid, red).values.cpu().numpy().reshape(80, -1)
+        # tight: same bf16 inputs, fp64 oracle
+        want_b = o.fused_pool(fb, lb, cache.ranks, cache.interval_starts, cache.interval_cells,
+                              grid.n_cells, red.value)
+        assert max_rel_dev(want_b, got) <= 1e-5, red
+        # the north-star bar: vs the fp32 reference path on unrounded inputs
+        want = o.pool_interval(features, o.normalize_depth(logits), cache.ranks,
+                               cache.interval_starts, cache.interval_cells, grid.n_cells,
+                               red.value)
+        assert max_rel_dev(want, got) <= BF16_TOL, red
+
+
+def test_cache_builder_no_sync_rebuild_matches():
+    spec, features, logits, grid, cache = _S()
+    rig, _, _, _ = bp.gen_workload(spec)
+    builder = bp.CacheBuilder(6, spec.frustum, grid)
+    cams = torch.from_numpy(bp.rig_rows(rig)).cuda()
+    for _ in range(2):
+        c2 = builder.build(cams)
+        torch.cuda.synchronize()
+        assert c2.n_intervals == cache.n_intervals
+        np.testing.assert_array_equal(c2.ranks, cache.ranks)
+        c2._host_counts = None
+        c2._host.clear()
