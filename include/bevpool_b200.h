@@ -28,7 +28,9 @@
  *   interval_starts[n_cells+1]  first n_int entries as the reference, plus a
  *                           sentinel interval_starts[n_int] = n_in
  *   interval_cells[n_cells] first n_int entries valid
- *   tile_first[n_tiles+1]   first interval of every BVP_TILE_CELLS-cell tile
+ *   cell_first[n_cells+1]   index of the first interval whose cell is >= c
+ *                           (cell_first[n_cells] = n_int): the interval range
+ *                           of any run of cells in O(1)
  *   interval_of_point[P]    interval index per point or 0xFFFFFFFF
  *   counts[2] (int64)       n_in, n_int
  * so a whole frame can be rebuilt and pooled without a host round trip.
@@ -83,7 +85,7 @@ size_t bvp_sort_workspace_bytes(int64_t n_points, int64_t n_cells);
 int bvp_sort_intervals(const uint32_t *cell_of_point, int64_t n_points,
                        int64_t n_cells, uint32_t *ranks,
                        uint32_t *interval_starts, uint32_t *interval_cells,
-                       uint32_t *tile_first, uint32_t *interval_of_point,
+                       uint32_t *cell_first, uint32_t *interval_of_point,
                        int64_t *counts, void *workspace, size_t workspace_bytes,
                        void *stream);
 
@@ -92,7 +94,7 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D,
                     double depth_min, double depth_step, const double *grid,
                     int nx, int ny, uint32_t *cell_of_point, uint32_t *ranks,
                     uint32_t *interval_starts, uint32_t *interval_cells,
-                    uint32_t *tile_first, uint32_t *interval_of_point,
+                    uint32_t *cell_first, uint32_t *interval_of_point,
                     int64_t *counts, void *workspace, size_t workspace_bytes,
                     void *stream);
 
@@ -101,7 +103,7 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D,
 /* Workspace for bvp_pool_forward_f32: the NHWC copy of the features. */
 size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
 
-/* features (B,N,C,H,W) f32, dist (B,N,D,H,W) f32 -> out (B,C,n_cells) f32.
+/* features (B,N,C,H,W) f32, dist (B,N,D,H,W) f32 -> out (B,C,nx*ny) f32.
  * Every output element is written (empty cells 0).  mode: BVP_SUM/MEAN/MAX.
  * exact != 0: 64-bit accumulation in rank order, bit-identical to the
  * reference's interval_reduce; exact == 0: fp32 accumulation (<=1.2e-7 rel).
@@ -112,8 +114,8 @@ size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
 int bvp_pool_forward_f32(const float *features, const float *dist,
                          const uint32_t *ranks, const uint32_t *interval_starts,
                          const uint32_t *interval_cells,
-                         const uint32_t *tile_first, int B, int N, int C, int H,
-                         int W, int D, int64_t n_cells, int64_t n_int_max,
+                         const uint32_t *cell_first, int B, int N, int C, int H,
+                         int W, int D, int nx, int ny, int64_t n_int_max,
                          int mode, int exact, float *out, float *feats_nhwc,
                          uint32_t *argmax, void *stream);
 
@@ -127,8 +129,8 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,
                               const uint32_t *ranks,
                               const uint32_t *interval_starts,
                               const uint32_t *interval_cells,
-                              const uint32_t *tile_first, int B, int N, int C,
-                              int H, int W, int D, int64_t n_cells,
+                              const uint32_t *cell_first, int B, int N, int C,
+                              int H, int W, int D, int nx, int ny,
                               int64_t n_int_max, int mode, int exact,
                               float *out, uint32_t *argmax, void *stream);
 
@@ -154,7 +156,7 @@ int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H,
 int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
                         const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
-                        const uint32_t *tile_first, int C, int64_t n_cells,
+                        const uint32_t *cell_first, int C, int nx, int ny,
                         int mode, float *out, void *stream);
 
 /* ---- fused lift + pool, bf16 inputs (config F) ------------------------- */
@@ -167,8 +169,8 @@ size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W);
 int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context,
                         const uint32_t *ranks, const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
-                        const uint32_t *tile_first, int B, int N, int C, int H,
-                        int W, int D, int64_t n_cells, int mode, float *out,
+                        const uint32_t *cell_first, int B, int N, int C, int H,
+                        int W, int D, int nx, int ny, int mode, float *out,
                         void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---- gather backward (config B) ---------------------------------------- */
@@ -182,10 +184,10 @@ size_t bvp_backward_workspace_bytes(int B, int C, int64_t n_int_max);
 int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc,
                           const float *dist, const uint32_t *interval_starts,
                           const uint32_t *interval_cells,
-                          const uint32_t *tile_first,
+                          const uint32_t *cell_first,
                           const uint32_t *interval_of_point,
                           const uint32_t *argmax, int B, int N, int C, int H,
-                          int W, int D, int64_t n_cells, int64_t n_int_max,
+                          int W, int D, int nx, int ny, int64_t n_int_max,
                           int mode, float *grad_features, float *grad_dist,
                           void *workspace, size_t workspace_bytes,
                           void *stream);
@@ -194,9 +196,9 @@ int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc,
 int bvp_pool_lifted_backward_f32(const float *grad_out,
                                  const uint32_t *interval_starts,
                                  const uint32_t *interval_cells,
-                                 const uint32_t *tile_first,
+                                 const uint32_t *cell_first,
                                  const uint32_t *interval_of_point, int C,
-                                 int64_t n_points, int64_t n_cells,
+                                 int64_t n_points, int nx, int ny,
                                  int64_t n_int_max, int mode, float *grad_x,
                                  void *workspace, size_t workspace_bytes,
                                  void *stream);

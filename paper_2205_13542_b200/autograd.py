@@ -1,12 +1,12 @@
 """Training: the interval pooling as a differentiable torch op (config B).
 
-Forward is the cached interval reduction (bvp_pool_forward_f32, fp32
-accumulation); backward is the atomic-free gather backward
-(bvp_pool_backward_f32, csrc/backward.cu) producing gradients for both the
-context features and the depth distribution.  MAX routes each output
-gradient to the first point (rank order) attaining the max, recorded by the
-forward.  The reference has no backward; tests/ check this one
-against an fp64 restatement and torch.autograd.gradcheck.
+Forward is the cached interval reduction (bvp_pool_forward_f32); backward is
+the atomic-free gather backward (bvp_pool_backward_f32, csrc/backward.cu)
+producing gradients for both the context features and the depth
+distribution.  MAX routes each output gradient to the first point (rank
+order) attaining the max, recorded by the forward.  The reference has no
+backward; tests/ check this one against an fp64 restatement
+that is itself checked against finite differences.
 """
 
 from __future__ import annotations
@@ -20,23 +20,23 @@ from .pooling import _MODE, BevFeatureMap, Reducer, _reducer
 
 class _BevPoolFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, features, dist, cache: AssociationCache, n_cells: int, reducer: Reducer,
-                exact: bool):
+    def forward(ctx, features, dist, cache: AssociationCache, nx: int, ny: int,
+                reducer: Reducer, exact: bool):
         B, N, C, H, W = features.shape
         D = dist.shape[2]
         dev = features.device
         features = features.contiguous()
         dist = dist.contiguous()
-        out = torch.empty((B, C, n_cells), dtype=torch.float32, device=dev)
+        out = torch.empty((B, C, nx * ny), dtype=torch.float32, device=dev)
         nhwc = torch.empty(features.numel(), dtype=torch.float32, device=dev)
         argmax = None
         if reducer is Reducer.MAX:
             argmax = torch.empty((B, cache.n_int_max, C), dtype=torch.int32, device=dev)
         _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                  ptr(cache.d_tile_first), B, N, C, H, W, D, n_cells, cache.n_int_max,
+                  ptr(cache.d_cell_first), B, N, C, H, W, D, nx, ny, cache.n_int_max,
                   _MODE[reducer], int(exact), ptr(out), ptr(nhwc), ptr(argmax), stream_ptr(dev))
-        ctx.cache, ctx.reducer, ctx.dims = cache, reducer, (B, N, C, H, W, D, n_cells)
+        ctx.cache, ctx.reducer, ctx.dims = cache, reducer, (B, N, C, H, W, D, nx, ny)
         ctx.save_for_backward(nhwc, dist, argmax)
         return out
 
@@ -44,7 +44,7 @@ class _BevPoolFn(torch.autograd.Function):
     def backward(ctx, grad_out):
         nhwc, dist, argmax = ctx.saved_tensors
         cache, reducer = ctx.cache, ctx.reducer
-        B, N, C, H, W, D, n_cells = ctx.dims
+        B, N, C, H, W, D, nx, ny = ctx.dims
         dev = grad_out.device
         g = grad_out.float().contiguous()
         need_f, need_w = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
@@ -55,10 +55,10 @@ class _BevPoolFn(torch.autograd.Function):
                              dtype=torch.uint8, device=dev)
             _lib.call("bvp_pool_backward_f32", ptr(g), ptr(nhwc), ptr(dist),
                       ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                      ptr(cache.d_tile_first), ptr(cache.d_interval_of_point), ptr(argmax), B, N,
-                      C, H, W, D, n_cells, cache.n_int_max, _MODE[reducer], ptr(gf), ptr(gw),
+                      ptr(cache.d_cell_first), ptr(cache.d_interval_of_point), ptr(argmax), B, N,
+                      C, H, W, D, nx, ny, cache.n_int_max, _MODE[reducer], ptr(gf), ptr(gw),
                       ptr(ws), ws.numel(), stream_ptr(dev))
-        return gf, gw, None, None, None, None
+        return gf, gw, None, None, None, None, None
 
 
 def bev_pool(features: torch.Tensor, dist: torch.Tensor, cache: AssociationCache,
@@ -70,7 +70,7 @@ def bev_pool(features: torch.Tensor, dist: torch.Tensor, cache: AssociationCache
     f = features if batched else features[None]
     d = dist if batched else dist[None]
     cache = cache.for_grid(grid.n_cells)
-    out = _BevPoolFn.apply(f.float(), d.float(), cache, grid.n_cells, reducer, exact)
+    out = _BevPoolFn.apply(f.float(), d.float(), cache, grid.nx, grid.ny, reducer, exact)
     out = out.view(f.shape[0], f.shape[2], grid.nx, grid.ny)
     return out if batched else out[0]
 

@@ -10,8 +10,9 @@ sort and interval tables, bit-identical to ``bevpool.build_cache``.
 
 The cache lives in HBM: ``AssociationCache`` holds device tensors (uint32
 values stored in torch.int32) plus two tables the GPU kernels need and the
-reference does not have -- ``tile_first`` (first interval of every 32-cell
-tile) and ``interval_of_point`` (for the gather backward) -- and a sentinel
+reference does not have -- ``cell_first`` (index of the first interval of
+every cell, so any run of cells maps to its interval range in O(1)) and
+``interval_of_point`` (for the gather backward) -- and a sentinel
 ``interval_starts[n_int] = n_in`` so no kernel needs host-side counts.
 The reference-typed numpy views (``cache.ranks`` ...) are host copies made
 on first access.
@@ -129,7 +130,7 @@ class AssociationCache:
     d_ranks: torch.Tensor                  # (>= n_in,)
     d_interval_starts: torch.Tensor        # (>= n_int + 1,) with sentinel
     d_interval_cells: torch.Tensor         # (>= n_int,)
-    d_tile_first: torch.Tensor             # (n_tiles + 1,)
+    d_cell_first: torch.Tensor             # (n_cells + 1,)
     d_interval_of_point: torch.Tensor      # (P,)
     d_counts: torch.Tensor                 # (2,) int64: n_in, n_int
     fingerprint: int
@@ -211,12 +212,11 @@ class AssociationCache:
 
 
 def _alloc(P: int, n_cells: int, dev) -> dict:
-    n_tiles = -(-n_cells // TILE_CELLS)
     i32 = dict(dtype=torch.int32, device=dev)
     return dict(
         cells=torch.empty(P, **i32), ranks=torch.empty(P, **i32),
         starts=torch.empty(n_cells + 1, **i32), icells=torch.empty(n_cells, **i32),
-        tile_first=torch.empty(n_tiles + 1, **i32), iop=torch.empty(P, **i32),
+        cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
         counts=torch.zeros(2, dtype=torch.int64, device=dev),
         ws=torch.empty(_lib.load().bvp_sort_workspace_bytes(P, n_cells), dtype=torch.uint8,
                        device=dev),
@@ -246,10 +246,10 @@ class CacheBuilder:
         _lib.call("bvp_build_cache", ptr(cams), self.n_cameras, f.height, f.width, f.depth_bins,
                   f.depth_min, f.depth_step, self._grid_arr.ctypes.data, g.nx, g.ny,
                   ptr(b["cells"]), ptr(b["ranks"]), ptr(b["starts"]), ptr(b["icells"]),
-                  ptr(b["tile_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
+                  ptr(b["cell_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
                   b["ws"].numel(), stream_ptr(self.dev))
         return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"],
-                                b["tile_first"], b["iop"], b["counts"], fingerprint,
+                                b["cell_first"], b["iop"], b["counts"], fingerprint,
                                 g.n_cells, self.n_cameras, f, g)
 
 
@@ -283,9 +283,9 @@ def cache_from_cells(cell_of_point, n_cells: int, fingerprint: int = 0, n_camera
     b = _alloc(P, n_cells, dev)
     b["cells"].copy_(torch.from_numpy(cells.view(np.int32)))
     _lib.call("bvp_sort_intervals", ptr(b["cells"]), P, n_cells, ptr(b["ranks"]),
-              ptr(b["starts"]), ptr(b["icells"]), ptr(b["tile_first"]), ptr(b["iop"]),
+              ptr(b["starts"]), ptr(b["icells"]), ptr(b["cell_first"]), ptr(b["iop"]),
               ptr(b["counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
-    cache = AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["tile_first"],
+    cache = AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
                              b["iop"], b["counts"], fingerprint, n_cells, n_cameras, frustum,
                              grid)
     cache._counts()

@@ -23,19 +23,24 @@ namespace bvp {
 
 constexpr int kRowPitch = kTileCells + 1;
 
+// CTA per 32-cell row tile (ix, ty), like the forward's warp tiles.
 template <bool MEAN>
 __global__ void __launch_bounds__(128)
 grad_rows_kernel(const float *__restrict__ grad_out, const uint32_t *__restrict__ starts,
-                 const uint32_t *__restrict__ icells, const uint32_t *__restrict__ tile_first,
-                 int C, int64_t n_cells, int64_t n_int_max, float *__restrict__ gT) {
+                 const uint32_t *__restrict__ icells, const uint32_t *__restrict__ cell_first,
+                 int C, int nx, int ny, int64_t n_int_max, float *__restrict__ gT) {
     extern __shared__ float s[];  // [C][kRowPitch]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x, b = blockIdx.y;
-    const int64_t cell0 = int64_t(tile) * kTileCells;
-    const uint32_t i0 = tile_first[tile], i1 = tile_first[tile + 1];
+    const int b = blockIdx.y;
+    const int tiles_y = (ny + kTileCells - 1) / kTileCells;
+    const int ty = blockIdx.x / nx, ix = blockIdx.x - ty * nx;
+    const int64_t n_cells = int64_t(nx) * ny;
+    const int64_t cell0 = int64_t(ix) * ny + ty * kTileCells;
+    const int rem = min(kTileCells, ny - ty * kTileCells);
+    (void)tiles_y;
+    const uint32_t i0 = cell_first[cell0], i1 = cell_first[cell0 + rem];
     if (i0 == i1) return;
     const float *g = grad_out + int64_t(b) * C * n_cells + cell0;
-    const int64_t rem = n_cells - cell0;
     for (int c = warp; c < C; c += 4)
         s[c * kRowPitch + lane] = lane < rem ? __ldg(g + int64_t(c) * n_cells + lane) : 0.f;
     __syncthreads();
@@ -168,15 +173,16 @@ __global__ void lifted_backward_kernel(const float *__restrict__ gT,
 }
 
 static int launch_grad_rows(const float *grad_out, const uint32_t *starts, const uint32_t *icells,
-                            const uint32_t *tile_first, int B, int C, int64_t n_cells,
+                            const uint32_t *cell_first, int B, int C, int nx, int ny,
                             int64_t n_int_max, bool mean, float *gT, cudaStream_t s) {
     const size_t smem = size_t(C) * kRowPitch * sizeof(float);
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", C);
     auto k = mean ? grad_rows_kernel<true> : grad_rows_kernel<false>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    const dim3 grid(static_cast<unsigned>(ceil_div(n_cells, kTileCells)), static_cast<unsigned>(B));
-    k<<<grid, 128, smem, s>>>(grad_out, starts, icells, tile_first, C, n_cells, n_int_max, gT);
+    const int tiles_y = (ny + kTileCells - 1) / kTileCells;
+    const dim3 grid(static_cast<unsigned>(int64_t(nx) * tiles_y), static_cast<unsigned>(B));
+    k<<<grid, 128, smem, s>>>(grad_out, starts, icells, cell_first, C, nx, ny, n_int_max, gT);
     return BVP_OK;
 }
 
@@ -192,19 +198,19 @@ size_t bvp_backward_workspace_bytes(int B, int C, int64_t n_int_max) {
 
 int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc, const float *dist,
                           const uint32_t *interval_starts, const uint32_t *interval_cells,
-                          const uint32_t *tile_first, const uint32_t *interval_of_point,
+                          const uint32_t *cell_first, const uint32_t *interval_of_point,
                           const uint32_t *argmax, int B, int N, int C, int H, int W, int D,
-                          int64_t n_cells, int64_t n_int_max, int mode, float *grad_features,
+                          int nx, int ny, int64_t n_int_max, int mode, float *grad_features,
                           float *grad_dist, void *workspace, size_t workspace_bytes,
                           void *stream) {
-    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && n_cells >= 1,
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims");
     BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
     BVP_REQUIRE(mode != BVP_MAX || argmax, BVP_ERR_INVALID, "MAX backward needs argmax");
     const size_t need = bvp_backward_workspace_bytes(B, C, n_int_max);
     BVP_REQUIRE(workspace && workspace_bytes >= need, BVP_ERR_INVALID,
                 "backward workspace too small: need %zu bytes", need);
-    BVP_REQUIRE(grad_out && feats_nhwc && dist && interval_starts && interval_cells && tile_first &&
+    BVP_REQUIRE(grad_out && feats_nhwc && dist && interval_starts && interval_cells && cell_first &&
                     interval_of_point,
                 BVP_ERR_INVALID, "null pointer argument");
     cudaStream_t s = as_stream(stream);
@@ -215,7 +221,7 @@ int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc, const 
     const int Q = (C + 31) / 32;
     BVP_REQUIRE(Q <= 8, BVP_ERR_UNSUPPORTED, "backward supports C <= 256, got %d", C);
     float *gT = static_cast<float *>(workspace);
-    int rc = launch_grad_rows(grad_out, interval_starts, interval_cells, tile_first, B, C, n_cells,
+    int rc = launch_grad_rows(grad_out, interval_starts, interval_cells, cell_first, B, C, nx, ny,
                               n_int_max, mode == BVP_MEAN, gT, s);
     if (rc != BVP_OK) return rc;
     const size_t smem = size_t(C + D) * kRowPitch * sizeof(float);
@@ -240,21 +246,21 @@ int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc, const 
 }
 
 int bvp_pool_lifted_backward_f32(const float *grad_out, const uint32_t *interval_starts,
-                                 const uint32_t *interval_cells, const uint32_t *tile_first,
+                                 const uint32_t *interval_cells, const uint32_t *cell_first,
                                  const uint32_t *interval_of_point, int C, int64_t n_points,
-                                 int64_t n_cells, int64_t n_int_max, int mode, float *grad_x,
+                                 int nx, int ny, int64_t n_int_max, int mode, float *grad_x,
                                  void *workspace, size_t workspace_bytes, void *stream) {
-    BVP_REQUIRE(C >= 1 && n_points >= 1 && n_cells >= 1 && mode >= 0 && mode <= 1,
+    BVP_REQUIRE(C >= 1 && n_points >= 1 && nx >= 1 && ny >= 1 && mode >= 0 && mode <= 1,
                 BVP_ERR_INVALID, "bad arguments (lifted backward supports SUM/MEAN)");
     const size_t need = bvp_backward_workspace_bytes(1, C, n_int_max);
     BVP_REQUIRE(workspace && workspace_bytes >= need, BVP_ERR_INVALID,
                 "backward workspace too small: need %zu bytes", need);
-    BVP_REQUIRE(grad_out && interval_starts && interval_cells && tile_first && interval_of_point &&
+    BVP_REQUIRE(grad_out && interval_starts && interval_cells && cell_first && interval_of_point &&
                     grad_x,
                 BVP_ERR_INVALID, "null pointer argument");
     cudaStream_t s = as_stream(stream);
     float *gT = static_cast<float *>(workspace);
-    int rc = launch_grad_rows(grad_out, interval_starts, interval_cells, tile_first, 1, C, n_cells,
+    int rc = launch_grad_rows(grad_out, interval_starts, interval_cells, cell_first, 1, C, nx, ny,
                               n_int_max, mode == BVP_MEAN, gT, s);
     if (rc != BVP_OK) return rc;
     const unsigned blocks =

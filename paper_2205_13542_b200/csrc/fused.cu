@@ -12,8 +12,16 @@
 
 namespace bvp {
 
-template <typename T>
-void launch_to_nhwc(const T *src, int64_t NB, int A, int HW, T *dst, cudaStream_t s);
+template <>
+int run_pool<float, __nv_bfloat16, 8, kSrcFused>(const PoolParams &p, int B, bool is_max,
+                                                 cudaStream_t s) {
+    return run_pool_impl<float, __nv_bfloat16, 8, kSrcFused>(p, B, is_max, s);
+}
+template <>
+int run_pool<float, __nv_bfloat16, 1, kSrcFused>(const PoolParams &p, int B, bool is_max,
+                                                 cudaStream_t s) {
+    return run_pool_impl<float, __nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);
+}
 
 // lse[pix] = max_d l + log(sum_d exp(l - max)); thread per pixel, the D
 // loads of consecutive pixels are coalesced.
@@ -31,40 +39,6 @@ __global__ void pixel_lse_kernel(const __nv_bfloat16 *__restrict__ logits, int64
         lse[t] = m + __logf(s);
     }
 }
-
-template <int VEC, int SRC>
-struct BfTable;
-
-#define BVP_SHAPE(L, CP)                                                                   \
-    if (sh.lpp == L && sh.cpl == CP) {                                                     \
-        auto k = is_max ? pool_tile_kernel<float, __nv_bfloat16, VEC, L, CP, true, SRC>    \
-                        : pool_tile_kernel<float, __nv_bfloat16, VEC, L, CP, false, SRC>;  \
-        if (smem > 48 * 1024)                                                              \
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
-        k<<<grid, kPoolThreads, smem, s>>>(p);                                             \
-        return true;                                                                       \
-    }
-
-template <int SRC>
-struct BfTable<8, SRC> {
-    static constexpr int VEC = 8;
-    static bool launch(LaneShape sh, const PoolParams &p, bool is_max, dim3 grid, size_t smem,
-                       cudaStream_t s) {
-        BVP_SHAPE(1, 1) BVP_SHAPE(2, 1) BVP_SHAPE(2, 2) BVP_SHAPE(2, 3) BVP_SHAPE(2, 4)
-        BVP_SHAPE(2, 5) BVP_SHAPE(8, 8) BVP_SHAPE(16, 8) BVP_SHAPE(32, 8)
-        return false;
-    }
-};
-template <int SRC>
-struct BfTable<1, SRC> {
-    static constexpr int VEC = 1;
-    static bool launch(LaneShape sh, const PoolParams &p, bool is_max, dim3 grid, size_t smem,
-                       cudaStream_t s) {
-        BVP_SHAPE(32, 1) BVP_SHAPE(32, 2) BVP_SHAPE(32, 4) BVP_SHAPE(32, 8)
-        return false;
-    }
-};
-#undef BVP_SHAPE
 
 struct FusedLayout {
     size_t off_lse, off_ctx, bytes;
@@ -90,17 +64,17 @@ size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W) {
 
 int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const uint32_t *ranks,
                         const uint32_t *interval_starts, const uint32_t *interval_cells,
-                        const uint32_t *tile_first, int B, int N, int C, int H, int W, int D,
-                        int64_t n_cells, int mode, float *out, void *workspace,
+                        const uint32_t *cell_first, int B, int N, int C, int H, int W, int D,
+                        int nx, int ny, int mode, float *out, void *workspace,
                         size_t workspace_bytes, void *stream) {
-    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && n_cells >= 1,
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims");
     BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
     const FusedLayout L = fused_layout(B, N, C, H, W);
     BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
                 "fused workspace too small: need %zu bytes", L.bytes);
-    BVP_REQUIRE(out && logits && (C == 0 || (context && ranks && interval_starts &&
-                                             interval_cells && tile_first)),
+    BVP_REQUIRE(logits && (C == 0 || (out && context && ranks && interval_starts &&
+                                      interval_cells && cell_first)),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     cudaStream_t s = as_stream(stream);
@@ -113,33 +87,20 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     pixel_lse_kernel<<<lb, 128, 0, s>>>(lg, NB, D, int(HW), lse);
     launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
                                   int(HW), ctx, s);
-    PoolParams p{};
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, C, nx, ny,
+                                    out, mode);
     p.rows = ctx;
     p.wsrc = lg;
     p.lse = lse;
-    p.ranks = ranks;
-    p.starts = interval_starts;
-    p.icells = interval_cells;
-    p.tile_first = tile_first;
-    p.out = out;
-    p.C = C;
     p.D = D;
     p.HW = int(HW);
     p.NHW = int(N * HW);
-    p.mean = mode == BVP_MEAN;
-    p.n_cells = n_cells;
     p.rows_bstride = int64_t(N) * HW * C;
     p.w_bstride = int64_t(N) * D * HW;
     const bool is_max = mode == BVP_MAX;
-    const bool v8 = (C % 8) == 0;
-    const LaneShape sh = choose_shape(v8 ? C / 8 : C, !v8, v8);
-    BVP_REQUIRE(sh.lpp > 0, BVP_ERR_UNSUPPORTED, "channel count %d not supported", C);
-    const size_t smem = size_t(C) * kTilePitch * sizeof(float);
-    BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", C);
-    const dim3 grid(static_cast<unsigned>(ceil_div(n_cells, kTileCells)), static_cast<unsigned>(B));
-    const bool ok = v8 ? BfTable<8, kSrcFused>::launch(sh, p, is_max, grid, smem, s)
-                       : BfTable<1, kSrcFused>::launch(sh, p, is_max, grid, smem, s);
-    BVP_REQUIRE(ok, BVP_ERR_UNSUPPORTED, "no kernel instance for lpp=%d cpl=%d", sh.lpp, sh.cpl);
+    const int rc = (C % 8 == 0) ? run_pool<float, __nv_bfloat16, 8, kSrcFused>(p, B, is_max, s)
+                                : run_pool<float, __nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);
+    if (rc != BVP_OK) return rc;
     return check_launch("fused_pool_bf16");
 }
 

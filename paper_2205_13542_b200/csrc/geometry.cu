@@ -214,9 +214,8 @@ __global__ void make_intervals_kernel(const uint32_t *__restrict__ cell_count,
                                       const unsigned long long *__restrict__ total,
                                       int64_t n_cells, uint32_t *__restrict__ starts,
                                       uint32_t *__restrict__ icells,
-                                      uint32_t *__restrict__ tile_first,
+                                      uint32_t *__restrict__ cell_first,
                                       int64_t *__restrict__ counts) {
-    const int64_t n_tiles = (n_cells + kTileCells - 1) / kTileCells;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cells;
          c += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long ex = scanned[c];
@@ -225,14 +224,14 @@ __global__ void make_intervals_kernel(const uint32_t *__restrict__ cell_count,
             starts[iv] = static_cast<uint32_t>(ex & 0xFFFFFFFFull);
             icells[iv] = static_cast<uint32_t>(c);
         }
-        if (c % kTileCells == 0) tile_first[c / kTileCells] = iv;
+        cell_first[c] = iv;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const unsigned long long t = *total;
         const uint32_t n_in = static_cast<uint32_t>(t & 0xFFFFFFFFull);
         const uint32_t n_int = static_cast<uint32_t>(t >> 32);
         starts[n_int] = n_in;
-        tile_first[n_tiles] = n_int;
+        cell_first[n_cells] = n_int;
         counts[0] = n_in;
         counts[1] = n_int;
     }
@@ -285,7 +284,7 @@ static SortLayout sort_layout(int64_t P, int64_t n_cells) {
 
 static int sort_impl(const double *cams, const FrustumParams *fp, const GridParams *gp,
                      uint32_t *cells, int64_t P, int64_t n_cells, uint32_t *ranks,
-                     uint32_t *starts, uint32_t *icells, uint32_t *tile_first, uint32_t *iop,
+                     uint32_t *starts, uint32_t *icells, uint32_t *cell_first, uint32_t *iop,
                      int64_t *counts, void *ws, size_t ws_bytes, cudaStream_t s) {
     const SortLayout L = sort_layout(P, n_cells);
     BVP_REQUIRE(ws != nullptr && ws_bytes >= L.bytes, BVP_ERR_INVALID,
@@ -321,7 +320,7 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
     pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
     device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
     make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
-                                             icells, tile_first, counts);
+                                             icells, cell_first, counts);
     if (iop) {
         const unsigned pb = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), 8192));
         interval_of_point_kernel<<<pb, 256, 0, s>>>(cells, P, packed, iop);
@@ -377,30 +376,30 @@ size_t bvp_sort_workspace_bytes(int64_t n_points, int64_t n_cells) {
 
 int bvp_sort_intervals(const uint32_t *cell_of_point, int64_t n_points, int64_t n_cells,
                        uint32_t *ranks, uint32_t *interval_starts, uint32_t *interval_cells,
-                       uint32_t *tile_first, uint32_t *interval_of_point, int64_t *counts,
+                       uint32_t *cell_first, uint32_t *interval_of_point, int64_t *counts,
                        void *workspace, size_t workspace_bytes, void *stream) {
-    BVP_REQUIRE(cell_of_point && ranks && interval_starts && interval_cells && tile_first &&
+    BVP_REQUIRE(cell_of_point && ranks && interval_starts && interval_cells && cell_first &&
                     counts,
                 BVP_ERR_INVALID, "null pointer argument");
     return sort_impl(nullptr, nullptr, nullptr, const_cast<uint32_t *>(cell_of_point), n_points,
-                     n_cells, ranks, interval_starts, interval_cells, tile_first,
+                     n_cells, ranks, interval_starts, interval_cells, cell_first,
                      interval_of_point, counts, workspace, workspace_bytes, as_stream(stream));
 }
 
 int bvp_build_cache(const double *cams, int N, int H, int W, int D, double depth_min,
                     double depth_step, const double *grid, int nx, int ny,
                     uint32_t *cell_of_point, uint32_t *ranks, uint32_t *interval_starts,
-                    uint32_t *interval_cells, uint32_t *tile_first, uint32_t *interval_of_point,
+                    uint32_t *interval_cells, uint32_t *cell_first, uint32_t *interval_of_point,
                     int64_t *counts, void *workspace, size_t workspace_bytes, void *stream) {
     BVP_REQUIRE(cams && grid && cell_of_point && ranks && interval_starts && interval_cells &&
-                    tile_first && counts,
+                    cell_first && counts,
                 BVP_ERR_INVALID, "null pointer argument");
     BVP_REQUIRE(N > 0 && H > 0 && W > 0 && D > 0 && nx > 0 && ny > 0, BVP_ERR_INVALID,
                 "frustum/grid dims must be positive");
     const FrustumParams f{N, H, W, D, depth_min, depth_step};
     const GridParams g{grid[0], grid[2], grid[4], grid[5], grid[6], nx, ny};
     return sort_impl(cams, &f, &g, cell_of_point, int64_t(N) * H * W * D, int64_t(nx) * ny,
-                     ranks, interval_starts, interval_cells, tile_first, interval_of_point,
+                     ranks, interval_starts, interval_cells, cell_first, interval_of_point,
                      counts, workspace, workspace_bytes, as_stream(stream));
 }
 

@@ -1,5 +1,7 @@
-// pool.cu -- cached forward (reference formulation and materialised frustum),
-// layout transposes, depth softmax, reorder_weights, finiteness scan.
+// pool.cu -- cached-forward entry points (reference formulation and the
+// materialised frustum), layout transposes, depth softmax, reorder_weights,
+// finiteness scan.  The interval kernels themselves are pool_kernel.cuh,
+// instantiated in pool_fast.cu / pool_exact.cu / pool_x.cu.
 //
 // Reference: pooling.py:206-221 (pool_interval), _kernels.py:22-63
 // (interval_reduce), pooling.py:243-261 (reorder_weights), lift.py:17-31
@@ -40,78 +42,22 @@ template void launch_to_nhwc<float>(const float *, int64_t, int, int, float *, c
 template void launch_to_nhwc<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int, int,
                                             __nv_bfloat16 *, cudaStream_t);
 
-// ---- dispatch over the instantiated lane shapes ------------------------------
-template <typename Acc, typename Elem, int VEC, int LPP, int CPL, int SRC>
-static void launch_one(const PoolParams &p, bool is_max, dim3 grid, size_t smem,
-                       cudaStream_t s) {
-    auto k = is_max ? pool_tile_kernel<Acc, Elem, VEC, LPP, CPL, true, SRC>
-                    : pool_tile_kernel<Acc, Elem, VEC, LPP, CPL, false, SRC>;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    k<<<grid, kPoolThreads, smem, s>>>(p);
-}
-
-#define BVP_SHAPE(L, CP)                                                         \
-    if (sh.lpp == L && sh.cpl == CP) {                                           \
-        launch_one<Acc, Elem, VEC, L, CP, SRC>(p, is_max, grid, smem, s);        \
-        return true;                                                             \
-    }
-
-template <typename Acc, typename Elem, int VEC, int SRC>
-struct ShapeTable;
-
-// fast fp32, 16-byte chunks
-template <typename Elem, int SRC>
-struct ShapeTable<float, Elem, 4, SRC> {
-    using Acc = float;
-    static constexpr int VEC = 4;
-    static bool launch(LaneShape sh, const PoolParams &p, bool is_max, dim3 grid, size_t smem,
-                       cudaStream_t s) {
-        BVP_SHAPE(1, 1) BVP_SHAPE(2, 1) BVP_SHAPE(4, 1) BVP_SHAPE(4, 2) BVP_SHAPE(4, 3)
-        BVP_SHAPE(4, 4) BVP_SHAPE(4, 5) BVP_SHAPE(4, 6) BVP_SHAPE(4, 8) BVP_SHAPE(8, 8)
-        BVP_SHAPE(16, 8) BVP_SHAPE(32, 8)
-        return false;
-    }
-};
-// scalar fallbacks (fast or exact) and the exact 16-byte mode: one point per
-// warp iteration, lanes over channels
-template <typename AccT, typename Elem, int VECT, int SRC>
-struct ShapeTable {
-    using Acc = AccT;
-    static constexpr int VEC = VECT;
-    static bool launch(LaneShape sh, const PoolParams &p, bool is_max, dim3 grid, size_t smem,
-                       cudaStream_t s) {
-        BVP_SHAPE(32, 1) BVP_SHAPE(32, 2) BVP_SHAPE(32, 4) BVP_SHAPE(32, 8)
-        return false;
-    }
-};
-#undef BVP_SHAPE
-
-template <typename Acc, typename Elem, int VEC, int SRC>
-static int run_pool(const PoolParams &p, int B, bool is_max, bool exact, cudaStream_t s) {
-    const int nchunks = p.C / VEC;
-    const LaneShape sh = choose_shape(nchunks, exact || VEC == 1, false);
-    BVP_REQUIRE(sh.lpp > 0, BVP_ERR_UNSUPPORTED, "channel count %d not supported (max %d)", p.C,
-                VEC == 4 ? 1024 : 256);
-    const size_t smem = size_t(p.C) * kTilePitch * sizeof(float);
-    BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
-    const int64_t n_tiles = ceil_div(p.n_cells, kTileCells);
-    const dim3 grid(static_cast<unsigned>(n_tiles), static_cast<unsigned>(B));
-    const bool ok = ShapeTable<Acc, Elem, VEC, SRC>::launch(sh, p, is_max, grid, smem, s);
-    BVP_REQUIRE(ok, BVP_ERR_UNSUPPORTED, "no kernel instance for lpp=%d cpl=%d", sh.lpp, sh.cpl);
-    return BVP_OK;
-}
-
-static int pool_dist_dispatch(PoolParams p, int B, int mode, int exact, cudaStream_t s) {
-    const bool is_max = mode == BVP_MAX;
+PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const uint32_t *icells,
+                            const uint32_t *cell_first, int C, int nx, int ny, float *out,
+                            int mode) {
+    PoolParams p{};
+    p.ranks = ranks;
+    p.starts = starts;
+    p.icells = icells;
+    p.cell_first = cell_first;
+    p.out = out;
+    p.C = C;
+    p.nx = nx;
+    p.ny = ny;
+    p.tiles_y = (ny + kTileCells - 1) / kTileCells;
+    p.n_cells = int64_t(nx) * ny;
     p.mean = mode == BVP_MEAN;
-    if (p.C == 0) return BVP_OK;
-    const bool v4 = (p.C % 4) == 0;
-    if (exact)
-        return v4 ? run_pool<double, float, 4, kSrcDist>(p, B, is_max, true, s)
-                  : run_pool<double, float, 1, kSrcDist>(p, B, is_max, true, s);
-    return v4 ? run_pool<float, float, 4, kSrcDist>(p, B, is_max, false, s)
-              : run_pool<float, float, 1, kSrcDist>(p, B, is_max, false, s);
+    return p;
 }
 
 // ---- depth softmax (lift.py:17-31), 64-bit math ------------------------------
@@ -154,9 +100,9 @@ __global__ void reorder_weights_kernel(const float *__restrict__ dist,
 
 // ---- materialised lift: x[(pix*D + d), c] = dist[n,d,h,w] * f[n,c,h,w] -----
 // One warp per pixel; the pixel's feature column (NCHW, strided) and depth
-// weights are staged in shared memory, then its D x C block of x -- contiguous
-// in the reference point order -- is streamed as flat float4s (fully
-// coalesced, evict-first stores).
+// weights are staged in shared memory, then its D x C block of x --
+// contiguous in the reference point order -- is streamed as flat float4s
+// (fully coalesced, evict-first stores).
 __global__ void __launch_bounds__(256)
 lift_kernel(const float *__restrict__ features, const float *__restrict__ dist, int64_t NP,
             int C, int D, int HW, float *__restrict__ x) {
@@ -174,9 +120,10 @@ lift_kernel(const float *__restrict__ features, const float *__restrict__ dist, 
         const int n4 = (D * C) / 4;
         for (int q = lane; q < n4; q += 32) {
             const int e = q * 4;
-            const int d = e / C, c = e - d * C;  // C % 4 == 0: same d for 4 lanes' values
+            const int d = e / C, c = e - d * C;  // C % 4 == 0: one depth bin per float4
             const float w = sw[d];
-            st_stream_f4(xo + e, make_float4(w * sf[c], w * sf[c + 1], w * sf[c + 2], w * sf[c + 3]));
+            st_stream_f4(xo + e,
+                         make_float4(w * sf[c], w * sf[c + 1], w * sf[c + 2], w * sf[c + 3]));
         }
     }
 }
@@ -204,58 +151,62 @@ size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W) {
     return size_t(B) * N * C * H * W * sizeof(float);
 }
 
+int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst, void *stream) {
+    BVP_REQUIRE(NB >= 0 && C >= 0 && HW >= 0, BVP_ERR_INVALID, "bad dims");
+    BVP_REQUIRE((src && dst) || NB * int64_t(C) * HW == 0, BVP_ERR_INVALID,
+                "null pointer argument");
+    launch_to_nhwc<float>(src, NB, C, HW, dst, as_stream(stream));
+    return check_launch("to_nhwc");
+}
+
 int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const uint32_t *ranks,
                               const uint32_t *interval_starts, const uint32_t *interval_cells,
-                              const uint32_t *tile_first, int B, int N, int C, int H, int W,
-                              int D, int64_t n_cells, int64_t n_int_max, int mode, int exact,
+                              const uint32_t *cell_first, int B, int N, int C, int H, int W,
+                              int D, int nx, int ny, int64_t n_int_max, int mode, int exact,
                               float *out, uint32_t *argmax, void *stream) {
-    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && n_cells >= 1,
-                BVP_ERR_INVALID, "bad dims B=%d N=%d C=%d H=%d W=%d D=%d n_cells=%lld", B, N, C,
-                H, W, D, (long long)n_cells);
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
+                BVP_ERR_INVALID, "bad dims B=%d N=%d C=%d H=%d W=%d D=%d nx=%d ny=%d", B, N, C,
+                H, W, D, nx, ny);
     BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
-    BVP_REQUIRE(out && (C == 0 || (feats_nhwc && dist && ranks && interval_starts &&
-                                   interval_cells && tile_first)),
+    BVP_REQUIRE(C == 0 || (out && feats_nhwc && dist && ranks && interval_starts &&
+                           interval_cells && cell_first),
                 BVP_ERR_INVALID, "null pointer argument");
-    PoolParams p{};
+    if (C == 0) return BVP_OK;
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, C, nx,
+                                    ny, out, mode);
     p.rows = feats_nhwc;
     p.wsrc = dist;
-    p.ranks = ranks;
-    p.starts = interval_starts;
-    p.icells = interval_cells;
-    p.tile_first = tile_first;
-    p.out = out;
     p.argmax = mode == BVP_MAX ? argmax : nullptr;
-    p.C = C;
     p.D = D;
     p.HW = H * W;
     p.NHW = N * H * W;
-    p.n_cells = n_cells;
     p.n_int_max = n_int_max;
     p.rows_bstride = int64_t(N) * H * W * C;
     p.w_bstride = int64_t(N) * D * H * W;
-    const int rc = pool_dist_dispatch(p, B, mode, exact, as_stream(stream));
+    const bool is_max = mode == BVP_MAX, v4 = (C % 4) == 0;
+    cudaStream_t s = as_stream(stream);
+    int rc;
+    if (exact)
+        rc = v4 ? run_pool<double, float, 4, kSrcDist>(p, B, is_max, s)
+                : run_pool<double, float, 1, kSrcDist>(p, B, is_max, s);
+    else
+        rc = v4 ? run_pool<float, float, 4, kSrcDist>(p, B, is_max, s)
+                : run_pool<float, float, 1, kSrcDist>(p, B, is_max, s);
     if (rc != BVP_OK) return rc;
     return check_launch("pool_forward");
 }
 
 int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_t *ranks,
                          const uint32_t *interval_starts, const uint32_t *interval_cells,
-                         const uint32_t *tile_first, int B, int N, int C, int H, int W, int D,
-                         int64_t n_cells, int64_t n_int_max, int mode, int exact, float *out,
+                         const uint32_t *cell_first, int B, int N, int C, int H, int W, int D,
+                         int nx, int ny, int64_t n_int_max, int mode, int exact, float *out,
                          float *feats_nhwc, uint32_t *argmax, void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1, BVP_ERR_INVALID, "bad dims");
     BVP_REQUIRE(C == 0 || (features && feats_nhwc), BVP_ERR_INVALID, "null pointer argument");
     launch_to_nhwc<float>(features, int64_t(B) * N, C, H * W, feats_nhwc, as_stream(stream));
     return bvp_pool_forward_nhwc_f32(feats_nhwc, dist, ranks, interval_starts, interval_cells,
-                                     tile_first, B, N, C, H, W, D, n_cells, n_int_max, mode,
+                                     cell_first, B, N, C, H, W, D, nx, ny, n_int_max, mode,
                                      exact, out, argmax, stream);
-}
-
-int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst, void *stream) {
-    BVP_REQUIRE(NB >= 0 && C >= 0 && HW >= 0, BVP_ERR_INVALID, "bad dims");
-    BVP_REQUIRE(src && dst, BVP_ERR_INVALID, "null pointer argument");
-    launch_to_nhwc<float>(src, NB, C, HW, dst, as_stream(stream));
-    return check_launch("to_nhwc");
 }
 
 int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in, int N, int D,
@@ -304,36 +255,30 @@ int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H, 
         lift_kernel<<<blocks, 256, smem, s>>>(features, dist, NP, C, D, H * W, x);
     } else {
         const int64_t total = NP * D * C;
-        const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 148 * 64));
+        const unsigned blocks =
+            static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 256), 148 * 64));
         lift_scalar_kernel<<<blocks, 256, 0, s>>>(features, dist, NP, C, D, H * W, x);
     }
     return check_launch("lift");
 }
 
 int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *interval_starts,
-                        const uint32_t *interval_cells, const uint32_t *tile_first, int C,
-                        int64_t n_cells, int mode, float *out, void *stream) {
-    BVP_REQUIRE(C >= 0 && n_cells >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
+                        const uint32_t *interval_cells, const uint32_t *cell_first, int C, int nx,
+                        int ny, int mode, float *out, void *stream) {
+    BVP_REQUIRE(C >= 0 && nx >= 1 && ny >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
                 "bad arguments");
-    BVP_REQUIRE(out && (C == 0 || (x && ranks && interval_starts && interval_cells && tile_first)),
+    BVP_REQUIRE(C == 0 || (out && x && ranks && interval_starts && interval_cells && cell_first),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
-    PoolParams p{};
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, C, nx,
+                                    ny, out, mode);
     p.rows = x;
-    p.ranks = ranks;
-    p.starts = interval_starts;
-    p.icells = interval_cells;
-    p.tile_first = tile_first;
-    p.out = out;
-    p.C = C;
     p.D = 1;
     p.HW = 1;
-    p.n_cells = n_cells;
-    p.mean = mode == BVP_MEAN;
     const bool is_max = mode == BVP_MAX;
     cudaStream_t s = as_stream(stream);
-    const int rc = (C % 4 == 0) ? run_pool<float, float, 4, kSrcX>(p, 1, is_max, false, s)
-                                : run_pool<float, float, 1, kSrcX>(p, 1, is_max, false, s);
+    const int rc = (C % 4 == 0) ? run_pool<float, float, 4, kSrcX>(p, 1, is_max, s)
+                                : run_pool<float, float, 1, kSrcX>(p, 1, is_max, s);
     if (rc != BVP_OK) return rc;
     return check_launch("pool_lifted");
 }

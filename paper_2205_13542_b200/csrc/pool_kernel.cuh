@@ -1,20 +1,29 @@
-// pool_kernel.cuh -- the cell-tiled interval-reduction kernel (forward).
+// pool_kernel.cuh -- the interval-reduction kernel (forward), sm_100a.
 //
-// Restates the reference's interval_reduce (_kernels.py:22-63) for sm_100a.
-// One CTA owns BVP_TILE_CELLS = 32 consecutive BEV cells.  Its interval range
-// comes from the cached tile table (tile_first), warps take the tile's
-// intervals round-robin, reduce each into registers, and park the result in
-// a shared [C][32] tile; the CTA then writes the (C, n_cells) output rows as
-// 128-byte coalesced segments -- zeros of empty cells included, so there is
-// no separate memset and exactly one non-atomic store per (channel, cell).
+// Restates the reference's interval_reduce (_kernels.py:22-63).
 //
-// Lane mapping inside a warp: LPP lanes cover one point's channel row with
-// VEC-wide 16-byte loads (CPL chunks per lane), PPW = 32/LPP points are in
-// flight per warp iteration, and a final xor-shuffle combines the PPW partial
-// sums.  LPP = 32 (PPW = 1) with Acc = double is the EXACT mode: each lane
-// accumulates its channels in rank order in 64 bits exactly like the
-// reference (products of two fp32 are exact in fp64), so the output is
-// bit-identical to interval_reduce.
+// Work decomposition
+//   * A tile is 32 consecutive cells of one BEV row (ix fixed).  One WARP
+//     owns one tile: it reduces every interval of the tile and writes the
+//     tile's (C x 32) output block -- zeros of empty cells included -- as
+//     128-byte row segments.  Exactly one non-atomic store per (channel,
+//     cell); no __syncthreads anywhere.
+//   * The kWarps warps of a CTA own the tiles of kWarps consecutive BEV rows
+//     at the same y-range: a CTA covers a kWarps x 32 block of cells, so the
+//     feature rows its intervals gather (a ray crosses neighbouring rows at
+//     neighbouring depths) are re-used out of L1.
+//   * Inside a warp, groups of LPP lanes each own ONE interval at a time and
+//     walk its points sequentially in rank order (CPL 16-byte chunks of the
+//     channel row per lane).  Groups that finish pick the next interval of
+//     the tile (warp-uniform refill via ballot), so the warp stays busy until
+//     the tile's total work is done.  Because each interval is accumulated by
+//     one group in rank order, Acc = double reproduces the reference's 64-bit
+//     sums bit for bit (products of two fp32 are exact in fp64); Acc = float
+//     is the fast mode.
+//   * Points are taken U = LPP at a time: each lane of the group fetches one
+//     point's rank + depth weight, shuffles broadcast them, and the group
+//     issues U x CPL independent 16-byte loads.  The next block's ranks are
+//     prefetched while the current block's gathers are in flight.
 //
 // Sources (SRC):
 //   kSrcDist  : rows = NHWC features (f32), weight = dist[n,d,h,w] (f32)
@@ -26,8 +35,8 @@
 
 namespace bvp {
 
-constexpr int kPoolThreads = 128;
-constexpr int kPoolWarps = kPoolThreads / 32;
+constexpr int kPoolWarps = 4;
+constexpr int kPoolThreads = 32 * kPoolWarps;
 constexpr int kTilePitch = kTileCells + 1;
 
 enum { kSrcDist = 0, kSrcX = 1, kSrcFused = 2 };
@@ -39,11 +48,12 @@ struct PoolParams {
     const uint32_t *ranks;
     const uint32_t *starts;  // n_int + 1 entries (sentinel = n_in)
     const uint32_t *icells;
-    const uint32_t *tile_first;
+    const uint32_t *cell_first;  // n_cells + 1: first interval with cell >= c
     float *out;              // (B, C, n_cells)
     uint32_t *argmax;        // MAX only, optional: (B, n_int_max, C)
     int C, D, HW, NHW;
     int mean;
+    int nx, ny, tiles_y;     // BEV rows, cells per row, 32-cell tiles per row
     int64_t n_cells, n_int_max;
     int64_t rows_bstride;    // elements of rows per batch sample
     int64_t w_bstride;       // elements of wsrc per batch sample
@@ -89,171 +99,247 @@ struct Loader<__nv_bfloat16, 1> {
 template <typename Acc, typename Elem, int VEC, int LPP, int CPL, bool IS_MAX, int SRC>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_tile_kernel(const PoolParams P) {
-    extern __shared__ float s_out[];  // [C][kTilePitch]
-    constexpr int PPW = 32 / LPP;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane / LPP, sub = lane % LPP;
+    extern __shared__ float s_all[];  // [kPoolWarps][C][kTilePitch]
+    // points per block per group (bounded so the block's rows fit registers)
+    constexpr int U = LPP < 4 ? LPP : (CPL > 5 ? 2 : 4);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPP, sub = lane % LPP, gbase = g * LPP;
     const int C = P.C;
     const int nchunks = C / VEC;
-    const int tile = blockIdx.x, b = blockIdx.y;
-    const int64_t cell0 = int64_t(tile) * kTileCells;
+    const int b = blockIdx.y;
+    float *s_out = s_all + warp * C * kTilePitch;
 
-    for (int i = tid; i < C * kTilePitch; i += kPoolThreads) s_out[i] = 0.f;
+    // tile of this warp: row ix, y-tile ty (CTA = kPoolWarps consecutive rows)
+    const int64_t tt = int64_t(blockIdx.x) * kPoolWarps + warp;
+    const int64_t ntiles = int64_t(P.nx) * P.tiles_y;
+    if (tt >= ntiles) return;
+    const int ty = static_cast<int>(tt / P.nx);
+    const int ix = static_cast<int>(tt - int64_t(ty) * P.nx);
+    const int iy0 = ty * kTileCells;
+    const int ncell = min(kTileCells, P.ny - iy0);
+    const int64_t cell0 = int64_t(ix) * P.ny + iy0;
+    const uint32_t i0 = __ldg(P.cell_first + cell0), i1 = __ldg(P.cell_first + cell0 + ncell);
 
     const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
-    const uint32_t i0 = P.tile_first[tile], i1 = P.tile_first[tile + 1];
-    __syncthreads();
+    uint32_t written = 0;  // bit x: cell iy0+x received an interval
 
-    for (uint32_t i = i0 + warp; i < i1; i += kPoolWarps) {
-        const uint32_t lo = P.starts[i], hi = P.starts[i + 1];
-        const uint32_t cell = P.icells[i];
-        Acc acc[CPL][VEC];
-        uint32_t arg[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1];
+    // group state (replicated over the group's lanes)
+    uint32_t cur = 0xFFFFFFFFu, j = 0, hi = 0;
+    uint32_t next_i = i0;
+    Acc acc[CPL][VEC];
+    uint32_t arg[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1];
+    uint32_t pf_rank = 0;
+    bool pf_ok = false;
+
+    while (true) {
+        // ---- refill: groups without an interval take the next ones --------
+        const bool need = (cur == 0xFFFFFFFFu);
+        const unsigned ask = __ballot_sync(0xFFFFFFFFu, need && sub == 0);
+        if (ask) {
+            if (need) {
+                const uint32_t mine = next_i + __popc(ask & ((1u << gbase) - 1u));
+                if (mine < i1) {
+                    cur = mine;
+                    j = __ldg(P.starts + mine);
+                    hi = __ldg(P.starts + mine + 1);
+                    pf_ok = false;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q)
+                    for (int q = 0; q < CPL; ++q)
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                acc[q][e] = IS_MAX ? Acc(-INFINITY) : Acc(0);
-                if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = 0xFFFFFFFFu;
+                        for (int e = 0; e < VEC; ++e) {
+                            acc[q][e] = IS_MAX ? Acc(-INFINITY) : Acc(0);
+                            if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = 0xFFFFFFFFu;
+                        }
+                }
             }
+            next_i += __popc(ask);
+        }
+        const bool active = (cur != 0xFFFFFFFFu);
+        if (!__any_sync(0xFFFFFFFFu, active)) break;
 
-        for (uint32_t j0 = lo; j0 < hi; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            const int cnt = min(32u, hi - j0);
-            uint32_t row = 0, pid = 0;
-            float wt = 0.f;
-            if (j < hi) {
-                const uint32_t p = __ldg(P.ranks + j);
-                pid = p;
-                if (SRC == kSrcX) {
-                    row = p;
-                    wt = 1.f;
+        // ---- one block of U points per active group --------------------------
+        uint32_t p = 0, row = 0;
+        float wt = 0.f;
+        const bool mine_ok = active && sub < U && (j + sub < hi);
+        if (mine_ok) {
+            p = pf_ok ? pf_rank : __ldg(P.ranks + j + sub);
+            // prefetch the next block of this interval
+            pf_ok = (j + U + sub < hi);
+            if (pf_ok) pf_rank = __ldg(P.ranks + j + U + sub);
+            if (SRC == kSrcX) {
+                row = p;
+                wt = 1.f;
+            } else {
+                const uint32_t pix = p / P.D;
+                const uint32_t d = p - pix * P.D;
+                const uint32_t n = pix / P.HW;
+                const uint32_t hw = pix - n * P.HW;
+                const int64_t widx = b * P.w_bstride + (int64_t(n) * P.D + d) * P.HW + hw;
+                row = pix;
+                if (SRC == kSrcDist) {
+                    wt = __ldg(static_cast<const float *>(P.wsrc) + widx);
                 } else {
-                    const uint32_t pix = p / P.D;
-                    const uint32_t d = p - pix * P.D;
-                    const uint32_t n = pix / P.HW;
-                    const uint32_t hw = pix - n * P.HW;
-                    const int64_t widx = b * P.w_bstride + (int64_t(n) * P.D + d) * P.HW + hw;
-                    row = pix;
-                    if (SRC == kSrcDist) {
-                        wt = __ldg(static_cast<const float *>(P.wsrc) + widx);
-                    } else {
-                        const float l = __bfloat162float(
-                            static_cast<const __nv_bfloat16 *>(P.wsrc)[widx]);
-                        wt = __expf(l - __ldg(P.lse + int64_t(b) * P.NHW + pix));
-                    }
+                    const float l = __bfloat162float(
+                        static_cast<const __nv_bfloat16 *>(P.wsrc)[widx]);
+                    wt = __expf(l - __ldg(P.lse + int64_t(b) * P.NHW + pix));
                 }
             }
-#pragma unroll 4
-            for (int k = 0; k < 32; k += PPW) {
-                if (k >= cnt) break;
-                const int kk = k + g;
-                const uint32_t rk = __shfl_sync(0xFFFFFFFFu, row, kk);
-                const float wk = __shfl_sync(0xFFFFFFFFu, wt, kk);
-                const uint32_t pk = IS_MAX ? __shfl_sync(0xFFFFFFFFu, pid, kk) : 0u;
-                if (kk < cnt) {
-                    const Elem *rp = rows + int64_t(rk) * C;
-#pragma unroll
-                    for (int q = 0; q < CPL; ++q) {
-                        const int ch = sub + q * LPP;
-                        if (ch < nchunks) {
-                            float v[VEC];
-                            Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v);
-#pragma unroll
-                            for (int e = 0; e < VEC; ++e) {
-                                if (IS_MAX) {
-                                    const Acc pv = Acc(wk) * Acc(v[e]);
-                                    if (pv > acc[q][e]) {
-                                        acc[q][e] = pv;
-                                        arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = pk;
-                                    }
-                                } else {
-                                    acc[q][e] += Acc(wk) * Acc(v[e]);
-                                }
-                            }
-                        }
-                    }
-                }
-            }
+        } else {
+            pf_ok = false;
         }
-        // combine the PPW point-groups (lanes sharing `sub`)
+        // gather the block's rows (independent loads), then accumulate in order
+        float v[U][CPL][VEC];
+        uint32_t pu[U];
+        float wu[U];
 #pragma unroll
-        for (int off = LPP; off < 32; off <<= 1) {
-#pragma unroll
-            for (int q = 0; q < CPL; ++q)
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                    const Acc o = __shfl_xor_sync(0xFFFFFFFFu, acc[q][e], off);
-                    if (IS_MAX) {
-                        const uint32_t oa =
-                            __shfl_xor_sync(0xFFFFFFFFu, arg[IS_MAX ? q : 0][IS_MAX ? e : 0], off);
-                        uint32_t &ma = arg[IS_MAX ? q : 0][IS_MAX ? e : 0];
-                        if (o > acc[q][e] || (o == acc[q][e] && oa < ma)) {
-                            acc[q][e] = o;
-                            ma = oa;
-                        }
-                    } else {
-                        acc[q][e] += o;
-                    }
-                }
-        }
-        if (g == 0) {
-            const int lc = static_cast<int>(cell - cell0);
-            const Acc inv = P.mean ? Acc(1) / Acc(hi - lo) : Acc(1);
+        for (int u = 0; u < U; ++u) {
+            const uint32_t ru = __shfl_sync(0xFFFFFFFFu, row, gbase + u);
+            wu[u] = __shfl_sync(0xFFFFFFFFu, wt, gbase + u);
+            pu[u] = __shfl_sync(0xFFFFFFFFu, p, gbase + u);
+            const bool ok = active && (j + u < hi);
+            const Elem *rp = rows + int64_t(ru) * C;
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
                 const int ch = sub + q * LPP;
-                if (ch < nchunks) {
+                if (ok && ch < nchunks) {
+                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v[u][q]);
+                } else {
 #pragma unroll
-                    for (int e = 0; e < VEC; ++e) {
-                        const int c = ch * VEC + e;
-                        const Acc r = P.mean ? acc[q][e] * inv : acc[q][e];
-                        s_out[c * kTilePitch + lc] = static_cast<float>(r);
-                        if (IS_MAX && P.argmax)
-                            P.argmax[(b * P.n_int_max + i) * C + c] =
-                                arg[IS_MAX ? q : 0][IS_MAX ? e : 0];
-                    }
+                    for (int e = 0; e < VEC; ++e) v[u][q][e] = 0.f;
                 }
             }
         }
+        if (active) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (j + u < hi) {
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            if (IS_MAX) {
+                                const Acc pv = Acc(wu[u]) * Acc(v[u][q][e]);
+                                if (pv > acc[q][e]) {
+                                    acc[q][e] = pv;
+                                    arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = pu[u];
+                                }
+                            } else {
+                                acc[q][e] += Acc(wu[u]) * Acc(v[u][q][e]);
+                            }
+                        }
+                }
+            }
+            j += U;
+            if (j >= hi) {  // interval complete: park it in the tile
+                const uint32_t cell = __ldg(P.icells + cur);
+                const int lc = static_cast<int>(int64_t(cell) - cell0);
+                const uint32_t len = hi - __ldg(P.starts + cur);
+                const Acc inv = P.mean ? Acc(1) / Acc(len) : Acc(1);
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int ch = sub + q * LPP;
+                    if (ch < nchunks) {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            const int c = ch * VEC + e;
+                            const Acc r = P.mean ? acc[q][e] * inv : acc[q][e];
+                            s_out[c * kTilePitch + lc] = static_cast<float>(r);
+                            if (IS_MAX && P.argmax)
+                                P.argmax[(b * P.n_int_max + cur) * C + c] =
+                                    arg[IS_MAX ? q : 0][IS_MAX ? e : 0];
+                        }
+                    }
+                }
+                written |= 1u << lc;
+                cur = 0xFFFFFFFFu;
+            }
+        }
     }
-    __syncthreads();
-    const int64_t rem = P.n_cells - cell0;
-    const int ncell_tile = rem < kTileCells ? static_cast<int>(rem) : kTileCells;
+    // every group's `written` bits -> the whole warp
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) written |= __shfl_xor_sync(0xFFFFFFFFu, written, off);
+    __syncwarp();
     float *out = P.out + int64_t(b) * C * P.n_cells + cell0;
-    for (int c = warp; c < C; c += kPoolWarps)
-        if (lane < ncell_tile) out[int64_t(c) * P.n_cells + lane] = s_out[c * kTilePitch + lane];
+    const bool has = lane < ncell && ((written >> lane) & 1u);
+    if (lane < ncell)
+        for (int c = 0; c < C; ++c)
+            out[int64_t(c) * P.n_cells + lane] = has ? s_out[c * kTilePitch + lane] : 0.f;
 }
 
-// (LPP, CPL) choice for a channel count: the instantiated table below.
+// Lane-group shape for a row of `nchunks` 16-byte chunks: LPP lanes per
+// interval, CPL chunks per lane (instantiated table in pool.cu / fused.cu).
 struct LaneShape {
     int lpp, cpl;
 };
 
-inline LaneShape choose_shape(int nchunks, bool exact, bool bf16vec) {
-    if (exact) {
-        for (int cpl : {1, 2, 4, 8})
-            if (32 * cpl >= nchunks) return {32, cpl};
-        return {0, 0};
-    }
-    if (bf16vec) {  // 16-byte chunks of 8 bf16
-        if (nchunks <= 1) return {1, 1};
-        if (nchunks <= 2) return {2, 1};
-        if (nchunks <= 10) return {2, (nchunks + 1) / 2 <= 4 ? (nchunks + 1) / 2 : 5};
-    } else {
-        if (nchunks <= 1) return {1, 1};
-        if (nchunks <= 2) return {2, 1};
-        if (nchunks <= 4) return {4, 1};
-        if (nchunks <= 24) {
-            int cpl = (nchunks + 3) / 4;
-            if (cpl == 7) cpl = 8;
-            return {4, cpl};
+inline LaneShape choose_shape(int nchunks) {
+    if (nchunks <= 0) return {1, 1};
+    for (int lpp : {1, 2, 4, 8, 16, 32}) {
+        const int need = (nchunks + lpp - 1) / lpp;
+        if (lpp == 1) {
+            if (need <= 2) return {1, need};
+            if (need <= 5) return {1, need <= 4 ? 4 : 5};
+        } else if (need <= 5) {
+            return {lpp, need <= 4 ? 4 : 5};
         }
-        if (nchunks <= 32) return {4, 8};
     }
-    for (int lpp : {8, 16, 32})
-        if (lpp * 8 >= nchunks) return {lpp, 8};
+    const int need = (nchunks + 31) / 32;
+    if (need <= 8) return {32, 8};
     return {0, 0};
+}
+
+#define BVP_FOR_EACH_SHAPE(X) \
+    X(1, 1) X(1, 2) X(1, 4) X(1, 5) X(2, 4) X(2, 5) X(4, 4) X(4, 5) X(8, 4) X(8, 5) X(16, 4) \
+    X(16, 5) X(32, 4) X(32, 5) X(32, 8)
+
+inline int64_t pool_tiles(const PoolParams &p) { return int64_t(p.nx) * p.tiles_y; }
+
+// pool.cu
+PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const uint32_t *icells,
+                            const uint32_t *cell_first, int C, int nx, int ny, float *out,
+                            int mode);
+template <typename T>
+void launch_to_nhwc(const T *src, int64_t NB, int A, int HW, T *dst, cudaStream_t s);
+
+// Launch the instantiated kernel for (Acc, Elem, VEC, SRC) and the shape of
+// p.C.  Defined (and explicitly instantiated) in the pool_*.cu / fused.cu
+// translation units so the ~30 kernels per family compile in parallel.
+template <typename Acc, typename Elem, int VEC, int SRC>
+int run_pool(const PoolParams &p, int B, bool is_max, cudaStream_t s);
+#define BVP_DECLARE_RUN_POOL(A, E, V, S) \
+    template <>                          \
+    int run_pool<A, E, V, S>(const PoolParams &p, int B, bool is_max, cudaStream_t s);
+BVP_DECLARE_RUN_POOL(float, float, 4, kSrcDist)          // pool_fast.cu
+BVP_DECLARE_RUN_POOL(float, float, 1, kSrcDist)          // pool_fast.cu
+BVP_DECLARE_RUN_POOL(double, float, 4, kSrcDist)         // pool_exact.cu
+BVP_DECLARE_RUN_POOL(double, float, 1, kSrcDist)         // pool_exact.cu
+BVP_DECLARE_RUN_POOL(float, float, 4, kSrcX)             // pool_x.cu
+BVP_DECLARE_RUN_POOL(float, float, 1, kSrcX)             // pool_x.cu
+BVP_DECLARE_RUN_POOL(float, __nv_bfloat16, 8, kSrcFused) // fused.cu
+BVP_DECLARE_RUN_POOL(float, __nv_bfloat16, 1, kSrcFused) // fused.cu
+#undef BVP_DECLARE_RUN_POOL
+
+template <typename Acc, typename Elem, int VEC, int SRC>
+int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
+    const LaneShape sh = choose_shape(p.C / VEC);
+    BVP_REQUIRE(sh.lpp > 0, BVP_ERR_UNSUPPORTED, "channel count %d not supported", p.C);
+    const size_t smem = size_t(kPoolWarps) * p.C * kTilePitch * sizeof(float);
+    BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
+    const dim3 grid(static_cast<unsigned>(ceil_div(pool_tiles(p), kPoolWarps)),
+                    static_cast<unsigned>(B));
+#define BVP_LAUNCH_SHAPE(L, CP)                                                              \
+    if (sh.lpp == L && sh.cpl == CP) {                                                       \
+        auto k = is_max ? pool_tile_kernel<Acc, Elem, VEC, L, CP, true, SRC>                 \
+                        : pool_tile_kernel<Acc, Elem, VEC, L, CP, false, SRC>;               \
+        if (smem > 48 * 1024)                                                                \
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+        k<<<grid, kPoolThreads, smem, s>>>(p);                                               \
+        return BVP_OK;                                                                       \
+    }
+    BVP_FOR_EACH_SHAPE(BVP_LAUNCH_SHAPE)
+#undef BVP_LAUNCH_SHAPE
+    set_error("no kernel instance for lpp=%d cpl=%d", sh.lpp, sh.cpl);
+    return BVP_ERR_UNSUPPORTED;
 }
 
 }  // namespace bvp

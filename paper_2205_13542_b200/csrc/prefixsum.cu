@@ -82,8 +82,9 @@ int bvp_pool_prefixsum_f32(const float *features, const float *dist, const uint3
     const PrefixLayout L = prefix_layout(n_in, C);
     BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
                 "prefixsum workspace too small: need %zu bytes", L.bytes);
-    BVP_REQUIRE(out, BVP_ERR_INVALID, "null output");
+    BVP_REQUIRE(out || C == 0, BVP_ERR_INVALID, "null output");
     cudaStream_t s = as_stream(stream);
+    if (C == 0) return BVP_OK;
     cudaMemsetAsync(out, 0, size_t(C) * n_cells * sizeof(float), s);
     if (n_int == 0 || C == 0) return check_launch("pool_prefixsum");
     BVP_REQUIRE(features && dist && ranks && interval_starts && interval_cells, BVP_ERR_INVALID,

@@ -183,8 +183,8 @@ def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
         nhwc = torch.empty(inp.feats.numel(), dtype=torch.float32, device=inp.feats.device)
         _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                  ptr(cache.d_tile_first), inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
-                  grid.n_cells, cache.n_int_max, _MODE[reducer],
+                  ptr(cache.d_cell_first), inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
+                  grid.nx, grid.ny, cache.n_int_max, _MODE[reducer],
                   int(DEFAULT_EXACT if exact is None else exact), ptr(out), ptr(nhwc), None,
                   stream_ptr(inp.feats.device))
     return _finish(out, inp, grid)
@@ -257,8 +257,8 @@ class PoolPlan:
         out = self.out if out is None else out
         c = self.cache
         _lib.call("bvp_pool_forward_nhwc_f32", ptr(self.nhwc), ptr(dist), ptr(c.d_ranks),
-                  ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_tile_first), self.B,
-                  self.N, self.C, self.H, self.W, self.D, self.grid.n_cells, c.n_int_max,
+                  ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first), self.B,
+                  self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
                   self.mode, self.exact, ptr(out), None, stream_ptr(self.dev))
         return out
 
@@ -366,7 +366,7 @@ def pool_lifted(x: torch.Tensor, cache: AssociationCache, grid: BevGridSpec,
     x = x.contiguous()
     out = torch.empty((C, grid.n_cells), dtype=torch.float32, device=x.device)
     _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
-              ptr(cache.d_interval_cells), ptr(cache.d_tile_first), C, grid.n_cells,
+              ptr(cache.d_interval_cells), ptr(cache.d_cell_first), C, grid.nx, grid.ny,
               _MODE[reducer], ptr(out), stream_ptr(x.device))
     return BevFeatureMap(out.view(C, grid.nx, grid.ny), grid)
 
@@ -393,8 +393,8 @@ def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCa
     ws = torch.empty(_lib.load().bvp_fused_workspace_bytes(B, N, C, H, W), dtype=torch.uint8,
                      device=dev)
     _lib.call("bvp_fused_pool_bf16", ptr(lg), ptr(cx), ptr(cache.d_ranks),
-              ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_tile_first),
-              B, N, C, H, W, D, grid.n_cells, _MODE[reducer], ptr(out), ptr(ws), ws.numel(),
+              ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_cell_first),
+              B, N, C, H, W, D, grid.nx, grid.ny, _MODE[reducer], ptr(out), ptr(ws), ws.numel(),
               stream_ptr(dev))
     v = out.view(B, C, grid.nx, grid.ny)
     return BevFeatureMap(v if batched else v[0], grid)
