@@ -98,7 +98,23 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D,
                     int64_t *counts, void *workspace, size_t workspace_bytes,
                     void *stream);
 
+/* ---- work units (cached with the association) -------------------------- */
+
+/* The interval kernels' work units: runs of <= 32 consecutive cells inside
+ * one 32-cell row tile whose intervals hold <= budget in-range points (a
+ * heavier single cell is its own unit), in x-major tile order; 2 uint32 per
+ * unit (first flat cell, cell count).  *n_units (device int64) receives the
+ * count; at most bvp_units_capacity() units are written. */
+int64_t bvp_units_capacity(int nx, int ny, int64_t n_int_max);
+size_t bvp_units_workspace_bytes(int nx, int ny);
+int bvp_make_units(const uint32_t *interval_starts, const uint32_t *cell_first,
+                   int nx, int ny, int budget, uint32_t *units,
+                   int64_t *n_units, void *workspace, size_t workspace_bytes,
+                   void *stream);
+
 /* ---- cached forward ---------------------------------------------------- */
+/* The pooling entry points take the cache's units (units, device count
+ * n_units, and max_units >= count, the launch size). */
 
 /* Workspace for bvp_pool_forward_f32: the NHWC copy of the features. */
 size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
@@ -114,7 +130,9 @@ size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
 int bvp_pool_forward_f32(const float *features, const float *dist,
                          const uint32_t *ranks, const uint32_t *interval_starts,
                          const uint32_t *interval_cells,
-                         const uint32_t *cell_first, int B, int N, int C, int H,
+                         const uint32_t *cell_first, const uint32_t *units,
+                         const int64_t *n_units, int64_t max_units,
+                         int B, int N, int C, int H,
                          int W, int D, int nx, int ny, int64_t n_int_max,
                          int mode, int exact, float *out, float *feats_nhwc,
                          uint32_t *argmax, void *stream);
@@ -129,7 +147,9 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,
                               const uint32_t *ranks,
                               const uint32_t *interval_starts,
                               const uint32_t *interval_cells,
-                              const uint32_t *cell_first, int B, int N, int C,
+                              const uint32_t *cell_first, const uint32_t *units,
+                              const int64_t *n_units, int64_t max_units,
+                              int B, int N, int C,
                               int H, int W, int D, int nx, int ny,
                               int64_t n_int_max, int mode, int exact,
                               float *out, uint32_t *argmax, void *stream);
@@ -156,7 +176,9 @@ int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H,
 int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
                         const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
-                        const uint32_t *cell_first, int C, int nx, int ny,
+                        const uint32_t *cell_first, const uint32_t *units,
+                        const int64_t *n_units, int64_t max_units,
+                        int C, int nx, int ny,
                         int mode, float *out, void *stream);
 
 /* ---- fused lift + pool, bf16 inputs (config F) ------------------------- */
@@ -169,7 +191,9 @@ size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W);
 int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context,
                         const uint32_t *ranks, const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
-                        const uint32_t *cell_first, int B, int N, int C, int H,
+                        const uint32_t *cell_first, const uint32_t *units,
+                        const int64_t *n_units, int64_t max_units,
+                        int B, int N, int C, int H,
                         int W, int D, int nx, int ny, int mode, float *out,
                         void *workspace, size_t workspace_bytes, void *stream);
 

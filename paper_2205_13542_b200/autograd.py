@@ -34,7 +34,8 @@ class _BevPoolFn(torch.autograd.Function):
             argmax = torch.empty((B, cache.n_int_max, C), dtype=torch.int32, device=dev)
         _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                  ptr(cache.d_cell_first), B, N, C, H, W, D, nx, ny, cache.n_int_max,
+                  ptr(cache.d_cell_first), *cache.unit_args(), B, N, C, H, W, D, nx, ny,
+                  cache.n_int_max,
                   _MODE[reducer], int(exact), ptr(out), ptr(nhwc), ptr(argmax), stream_ptr(dev))
         ctx.cache, ctx.reducer, ctx.dims = cache, reducer, (B, N, C, H, W, D, nx, ny)
         ctx.save_for_backward(nhwc, dist, argmax)
@@ -69,7 +70,7 @@ def bev_pool(features: torch.Tensor, dist: torch.Tensor, cache: AssociationCache
     batched = features.dim() == 5
     f = features if batched else features[None]
     d = dist if batched else dist[None]
-    cache = cache.for_grid(grid.n_cells)
+    cache = cache.for_grid(grid)
     out = _BevPoolFn.apply(f.float(), d.float(), cache, grid.nx, grid.ny, reducer, exact)
     out = out.view(f.shape[0], f.shape[2], grid.nx, grid.ny)
     return out if batched else out[0]

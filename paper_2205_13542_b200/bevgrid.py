@@ -117,13 +117,18 @@ def _u32(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy().view(np.uint32)
 
 
+#: points per work unit of the interval kernels (csrc/units.cu)
+UNIT_BUDGET = 256
+
+
 @dataclass(eq=False)
 class AssociationCache:
     """Device-resident association of every frustum point with its BEV cell.
 
     ``ranks`` lists the in-range point ids sorted by cell (stable); interval
     i covers ranks[interval_starts[i] : interval_starts[i+1]] and all its
-    points share cell interval_cells[i].  Immutable after build.
+    points share cell interval_cells[i].  Immutable after build.  ``nx, ny``
+    is the grid shape the work units were cut for.
     """
 
     d_cell_of_point: torch.Tensor          # (P,)
@@ -133,8 +138,12 @@ class AssociationCache:
     d_cell_first: torch.Tensor             # (n_cells + 1,)
     d_interval_of_point: torch.Tensor      # (P,)
     d_counts: torch.Tensor                 # (2,) int64: n_in, n_int
+    d_units: torch.Tensor                  # (2 * max_units,) (first cell, count)
+    d_n_units: torch.Tensor                # (1,) int64
+    max_units: int                         # launch bound (>= device count)
     fingerprint: int
-    n_cells: int
+    nx: int
+    ny: int
     n_cameras: int | None = None
     frustum: FrustumSpec | None = field(default=None, repr=False)
     grid: BevGridSpec | None = field(default=None, repr=False)
@@ -145,6 +154,10 @@ class AssociationCache:
     @property
     def device(self) -> torch.device:
         return self.d_cell_of_point.device
+
+    @property
+    def n_cells(self) -> int:
+        return self.nx * self.ny
 
     @property
     def n_points(self) -> int:
@@ -168,6 +181,14 @@ class AssociationCache:
     def n_int_max(self) -> int:
         """Capacity of the interval tables (no host sync)."""
         return int(self.d_interval_cells.shape[0])
+
+    @property
+    def n_units(self) -> int:
+        return int(self.d_n_units.item())
+
+    def unit_args(self):
+        """(units, n_units, max_units) as the C ABI takes them."""
+        return ptr(self.d_units), ptr(self.d_n_units), self.max_units
 
     # ---- reference-typed host views ------------------------------------
     def _view(self, name, tensor, n):
@@ -197,44 +218,62 @@ class AssociationCache:
     def interval_of_point(self) -> np.ndarray:
         return self._view("interval_of_point", self.d_interval_of_point, self.n_points)
 
-    def for_grid(self, n_cells: int) -> "AssociationCache":
-        """This cache with tile tables sized for an ``n_cells`` grid.  Caches
-        loaded from disk carry no grid (reference bevgrid.py:110-113); their
-        tables are re-derived once per pooling grid."""
-        if n_cells == self.n_cells:
+    def for_grid(self, grid: BevGridSpec) -> "AssociationCache":
+        """This cache with cell tables / work units cut for ``grid``'s shape.
+        Caches loaded from disk carry no grid (reference bevgrid.py:110-113);
+        their tables are re-derived once per pooling grid shape."""
+        if (grid.nx, grid.ny) == (self.nx, self.ny):
             return self
-        key = ("grid", n_cells)
+        key = ("grid", grid.nx, grid.ny)
         if key not in self._host:
-            self._host[key] = cache_from_cells(self.cell_of_point, n_cells, self.fingerprint,
-                                               self.n_cameras, self.frustum, self.grid,
-                                               self.device)
+            self._host[key] = cache_from_cells(self.cell_of_point, grid.nx, grid.ny,
+                                               self.fingerprint, self.n_cameras, self.frustum,
+                                               self.grid, self.device)
         return self._host[key]
 
 
-def _alloc(P: int, n_cells: int, dev) -> dict:
+def _alloc(P: int, nx: int, ny: int, dev) -> dict:
     i32 = dict(dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    n_cells = nx * ny
+    cap = int(lib.bvp_units_capacity(nx, ny, n_cells))
+    ws = max(lib.bvp_sort_workspace_bytes(P, n_cells), lib.bvp_units_workspace_bytes(nx, ny))
     return dict(
         cells=torch.empty(P, **i32), ranks=torch.empty(P, **i32),
         starts=torch.empty(n_cells + 1, **i32), icells=torch.empty(n_cells, **i32),
         cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
         counts=torch.zeros(2, dtype=torch.int64, device=dev),
-        ws=torch.empty(_lib.load().bvp_sort_workspace_bytes(P, n_cells), dtype=torch.uint8,
-                       device=dev),
+        units=torch.empty(2 * cap, **i32), n_units=torch.zeros(1, dtype=torch.int64, device=dev),
+        cap=cap, ws=torch.empty(ws, dtype=torch.uint8, device=dev),
     )
+
+
+def _make_units(b: dict, nx: int, ny: int, budget: int, dev) -> None:
+    _lib.call("bvp_make_units", ptr(b["starts"]), ptr(b["cell_first"]), nx, ny, budget,
+              ptr(b["units"]), ptr(b["n_units"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
+
+
+def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, max_units=None):
+    return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
+                            b["iop"], b["counts"], b["units"], b["n_units"],
+                            b["cap"] if max_units is None else max_units, fingerprint, nx, ny,
+                            n_cameras, frustum, grid)
 
 
 class CacheBuilder:
     """Re-usable GPU association builder: buffers and workspace are allocated
     once for a (frustum, grid) shape and every ``build`` reruns geometry +
-    sort + interval tables on the current stream with no host round trip
-    (config H: uncached geometry every frame).  The returned cache aliases
-    the builder's buffers until the next ``build``."""
+    sort + interval tables + work units on the current stream with no host
+    round trip (config H: uncached geometry every frame).  The returned cache
+    aliases the builder's buffers until the next ``build``."""
 
-    def __init__(self, n_cameras: int, frustum: FrustumSpec, grid: BevGridSpec, device=None):
+    def __init__(self, n_cameras: int, frustum: FrustumSpec, grid: BevGridSpec, device=None,
+                 unit_budget: int = UNIT_BUDGET):
         self.dev = cuda_device(device)
         self.n_cameras, self.frustum, self.grid = n_cameras, frustum, grid
         self.P = n_cameras * frustum.points_per_camera
-        self.bufs = _alloc(self.P, grid.n_cells, self.dev)
+        self.bufs = _alloc(self.P, grid.nx, grid.ny, self.dev)
+        self.unit_budget = unit_budget
         self._grid_arr = grid.as_array()
 
     def build(self, cams: torch.Tensor, fingerprint: int = 0) -> AssociationCache:
@@ -248,9 +287,8 @@ class CacheBuilder:
                   ptr(b["cells"]), ptr(b["ranks"]), ptr(b["starts"]), ptr(b["icells"]),
                   ptr(b["cell_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
                   b["ws"].numel(), stream_ptr(self.dev))
-        return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"],
-                                b["cell_first"], b["iop"], b["counts"], fingerprint,
-                                g.n_cells, self.n_cameras, f, g)
+        _make_units(b, g.nx, g.ny, self.unit_budget, self.dev)
+        return _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g)
 
 
 def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
@@ -265,30 +303,34 @@ def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
     cams_d = torch.from_numpy(cams).to(builder.dev)
     cache = builder.build(cams_d, fingerprint_inputs(rig, frustum_spec, grid_spec))
     cache._counts()  # one sync: sizes known on the host from here on
+    cache.max_units = max(1, cache.n_units)
     return cache
 
 
-def cache_from_cells(cell_of_point, n_cells: int, fingerprint: int = 0, n_cameras=None,
-                     frustum=None, grid=None, device=None) -> AssociationCache:
+def cache_from_cells(cell_of_point, nx: int, ny: int, fingerprint: int = 0, n_cameras=None,
+                     frustum=None, grid=None, device=None,
+                     unit_budget: int = UNIT_BUDGET) -> AssociationCache:
     """Association cache from given cell ids (a loaded file, a synthetic test
-    cache): GPU stable sort + interval tables (bevgrid.py:142-158)."""
+    cache) for an nx x ny grid: GPU stable sort + interval tables
+    (bevgrid.py:142-158) + work units."""
     dev = cuda_device(device)
     cells = np.ascontiguousarray(cell_of_point, dtype=np.uint32)
     P = int(cells.shape[0])
+    n_cells = nx * ny
     if P == 0:
         raise ConfigurationError("cache must cover at least one point")
     valid = cells[cells != OUT_OF_RANGE]
     if valid.size and int(valid.max()) >= n_cells:
         raise StaleCacheError("cache contains cell ids beyond this grid")
-    b = _alloc(P, n_cells, dev)
-    b["cells"].copy_(torch.from_numpy(cells.view(np.int32)))
+    b = _alloc(P, nx, ny, dev)
+    b["cells"].copy_(torch.from_numpy(cells.view(np.int32).copy()))
     _lib.call("bvp_sort_intervals", ptr(b["cells"]), P, n_cells, ptr(b["ranks"]),
               ptr(b["starts"]), ptr(b["icells"]), ptr(b["cell_first"]), ptr(b["iop"]),
               ptr(b["counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
-    cache = AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
-                             b["iop"], b["counts"], fingerprint, n_cells, n_cameras, frustum,
-                             grid)
+    _make_units(b, nx, ny, unit_budget, dev)
+    cache = _cache_of(b, fingerprint, nx, ny, n_cameras, frustum, grid)
     cache._counts()
+    cache.max_units = max(1, cache.n_units)
     return cache
 
 
@@ -301,7 +343,7 @@ def ranks_and_intervals(cells: np.ndarray, n_cells: int | None = None):
     if n_cells is None:
         valid = cells[cells != OUT_OF_RANGE]
         n_cells = int(valid.max()) + 1 if valid.size else 1
-    c = cache_from_cells(cells, n_cells)
+    c = cache_from_cells(cells, 1, n_cells)
     return c.ranks.copy(), c.interval_starts.copy(), c.interval_cells.copy()
 
 
@@ -361,7 +403,7 @@ def deserialize_cache(data: bytes, n_cells: int | None = None, device=None) -> A
     cells, ranks, starts, icells = arrays
     if n_cells is None:
         n_cells = int(icells.max()) + 1 if icells.size else 1
-    cache = cache_from_cells(cells, n_cells, fingerprint, device=device)
+    cache = cache_from_cells(cells, 1, n_cells, fingerprint, device=device)
     if not (np.array_equal(cache.ranks, ranks) and np.array_equal(cache.interval_starts, starts)
             and np.array_equal(cache.interval_cells, icells)):
         raise FileFormatError("ranks / intervals inconsistent with cell_of_point")

@@ -49,12 +49,15 @@ struct PoolParams {
     const uint32_t *starts;  // n_int + 1 entries (sentinel = n_in)
     const uint32_t *icells;
     const uint32_t *cell_first;  // n_cells + 1: first interval with cell >= c
+    const uint32_t *units;   // work units: (first cell, cell count) pairs
+    const int64_t *n_units;  // device count of units
     float *out;              // (B, C, n_cells)
     uint32_t *argmax;        // MAX only, optional: (B, n_int_max, C)
     int C, D, HW, NHW;
     int mean;
     int nx, ny, tiles_y;     // BEV rows, cells per row, 32-cell tiles per row
     int64_t n_cells, n_int_max;
+    int64_t max_units;       // grid size (>= *n_units)
     int64_t rows_bstride;    // elements of rows per batch sample
     int64_t w_bstride;       // elements of wsrc per batch sample
 };
@@ -96,12 +99,43 @@ struct Loader<__nv_bfloat16, 1> {
     }
 };
 
+// Park one finished interval (MEAN scaling, argmax) in the warp's tile.
+template <typename Acc, int VEC, int LPP, int CPL, bool IS_MAX>
+__device__ __forceinline__ void store_interval(const PoolParams &P, float *s_out,
+                                               const Acc (&acc)[CPL][VEC],
+                                               const uint32_t (&arg)[IS_MAX ? CPL : 1]
+                                                                    [IS_MAX ? VEC : 1],
+                                               uint32_t iv, uint32_t hi, int64_t cell0, int b,
+                                               int sub, int nchunks) {
+    const int lc = static_cast<int>(int64_t(__ldg(P.icells + iv)) - cell0);
+    const uint32_t len = hi - __ldg(P.starts + iv);
+    const Acc inv = P.mean ? Acc(1) / Acc(len) : Acc(1);
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+        const int ch = sub + q * LPP;
+        if (ch < nchunks) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                const int c = ch * VEC + e;
+                const Acc r = P.mean ? acc[q][e] * inv : acc[q][e];
+                s_out[c * kTilePitch + lc] = static_cast<float>(r);
+                if (IS_MAX && P.argmax)
+                    P.argmax[(b * P.n_int_max + iv) * P.C + c] = arg[IS_MAX ? q : 0][IS_MAX ? e : 0];
+            }
+        }
+    }
+}
+
 template <typename Acc, typename Elem, int VEC, int LPP, int CPL, bool IS_MAX, int SRC>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_tile_kernel(const PoolParams P) {
     extern __shared__ float s_all[];  // [kPoolWarps][C][kTilePitch]
     // points per block per group (bounded so the block's rows fit registers)
     constexpr int U = LPP < 4 ? LPP : (CPL > 5 ? 2 : 4);
+    constexpr int NG = 32 / LPP;  // interval groups per warp
+    // fast mode may split one long interval over all groups (exact may not)
+    constexpr bool kCoop = sizeof(Acc) == sizeof(float);
+    constexpr uint32_t kCoopMin = 64;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / LPP, sub = lane % LPP, gbase = g * LPP;
     const int C = P.C;
@@ -109,27 +143,47 @@ pool_tile_kernel(const PoolParams P) {
     const int b = blockIdx.y;
     float *s_out = s_all + warp * C * kTilePitch;
 
-    // tile of this warp: row ix, y-tile ty (CTA = kPoolWarps consecutive rows)
-    const int64_t tt = int64_t(blockIdx.x) * kPoolWarps + warp;
-    const int64_t ntiles = int64_t(P.nx) * P.tiles_y;
-    if (tt >= ntiles) return;
-    const int ty = static_cast<int>(tt / P.nx);
-    const int ix = static_cast<int>(tt - int64_t(ty) * P.nx);
-    const int iy0 = ty * kTileCells;
-    const int ncell = min(kTileCells, P.ny - iy0);
-    const int64_t cell0 = int64_t(ix) * P.ny + iy0;
+    // work unit of this warp: a run of <= 32 cells of one row tile
+    const int64_t k = int64_t(blockIdx.x) * kPoolWarps + warp;
+    if (k >= *P.n_units) return;
+    const int64_t cell0 = __ldg(P.units + 2 * k);
+    const int ncell = static_cast<int>(__ldg(P.units + 2 * k + 1));
     const uint32_t i0 = __ldg(P.cell_first + cell0), i1 = __ldg(P.cell_first + cell0 + ncell);
 
     const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
-    uint32_t written = 0;  // bit x: cell iy0+x received an interval
+    uint32_t written = 0;  // bit x: cell cell0+x received an interval
 
     // group state (replicated over the group's lanes)
     uint32_t cur = 0xFFFFFFFFu, j = 0, hi = 0;
     uint32_t next_i = i0;
+    uint32_t stride = U;
     Acc acc[CPL][VEC];
     uint32_t arg[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+            acc[q][e] = IS_MAX ? Acc(-INFINITY) : Acc(0);
+            if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = 0xFFFFFFFFu;
+        }
     uint32_t pf_rank = 0;
     bool pf_ok = false;
+
+    // fast mode, a unit that is one long interval: every group walks a
+    // strided share of it and the shares are combined at the end
+    bool coop = false;
+    if (kCoop && i1 == i0 + 1) {
+        const uint32_t lo = __ldg(P.starts + i0), h = __ldg(P.starts + i0 + 1);
+        if (h - lo > kCoopMin) {
+            coop = true;
+            cur = i0;
+            j = lo + g * U;
+            hi = h;
+            stride = NG * U;
+            next_i = i1;
+            if (j >= hi) cur = 0xFFFFFFFEu;  // nothing for this group
+        }
+    }
 
     while (true) {
         // ---- refill: groups without an interval take the next ones --------
@@ -150,11 +204,13 @@ pool_tile_kernel(const PoolParams P) {
                             acc[q][e] = IS_MAX ? Acc(-INFINITY) : Acc(0);
                             if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = 0xFFFFFFFFu;
                         }
+                } else {
+                    cur = 0xFFFFFFFEu;  // retired
                 }
             }
             next_i += __popc(ask);
         }
-        const bool active = (cur != 0xFFFFFFFFu);
+        const bool active = cur < 0xFFFFFFFEu;
         if (!__any_sync(0xFFFFFFFFu, active)) break;
 
         // ---- one block of U points per active group --------------------------
@@ -163,9 +219,9 @@ pool_tile_kernel(const PoolParams P) {
         const bool mine_ok = active && sub < U && (j + sub < hi);
         if (mine_ok) {
             p = pf_ok ? pf_rank : __ldg(P.ranks + j + sub);
-            // prefetch the next block of this interval
-            pf_ok = (j + U + sub < hi);
-            if (pf_ok) pf_rank = __ldg(P.ranks + j + U + sub);
+            // prefetch this group's next block
+            pf_ok = (j + stride + sub < hi);
+            if (pf_ok) pf_rank = __ldg(P.ranks + j + stride + sub);
             if (SRC == kSrcX) {
                 row = p;
                 wt = 1.f;
@@ -229,31 +285,41 @@ pool_tile_kernel(const PoolParams P) {
                         }
                 }
             }
-            j += U;
-            if (j >= hi) {  // interval complete: park it in the tile
-                const uint32_t cell = __ldg(P.icells + cur);
-                const int lc = static_cast<int>(int64_t(cell) - cell0);
-                const uint32_t len = hi - __ldg(P.starts + cur);
-                const Acc inv = P.mean ? Acc(1) / Acc(len) : Acc(1);
-#pragma unroll
-                for (int q = 0; q < CPL; ++q) {
-                    const int ch = sub + q * LPP;
-                    if (ch < nchunks) {
-#pragma unroll
-                        for (int e = 0; e < VEC; ++e) {
-                            const int c = ch * VEC + e;
-                            const Acc r = P.mean ? acc[q][e] * inv : acc[q][e];
-                            s_out[c * kTilePitch + lc] = static_cast<float>(r);
-                            if (IS_MAX && P.argmax)
-                                P.argmax[(b * P.n_int_max + cur) * C + c] =
-                                    arg[IS_MAX ? q : 0][IS_MAX ? e : 0];
-                        }
-                    }
+            j += stride;
+            if (j >= hi) {
+                if (coop) {
+                    cur = 0xFFFFFFFEu;  // share done; combined after the loop
+                } else {  // interval complete: park it in the unit's tile
+                    store_interval<Acc, VEC, LPP, CPL, IS_MAX>(P, s_out, acc, arg, cur, hi, cell0, b, sub, nchunks);
+                    written |= 1u << static_cast<int>(int64_t(__ldg(P.icells + cur)) - cell0);
+                    cur = 0xFFFFFFFFu;
                 }
-                written |= 1u << lc;
-                cur = 0xFFFFFFFFu;
             }
         }
+    }
+    if (coop) {  // combine the NG shares (fixed xor order: deterministic)
+#pragma unroll
+        for (int off = LPP; off < 32; off <<= 1) {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                    const Acc o = __shfl_xor_sync(0xFFFFFFFFu, acc[q][e], off);
+                    if (IS_MAX) {
+                        uint32_t &ma = arg[IS_MAX ? q : 0][IS_MAX ? e : 0];
+                        const uint32_t oa = __shfl_xor_sync(0xFFFFFFFFu, ma, off);
+                        if (o > acc[q][e] || (o == acc[q][e] && oa < ma)) {
+                            acc[q][e] = o;
+                            ma = oa;
+                        }
+                    } else {
+                        acc[q][e] += o;
+                    }
+                }
+        }
+        if (g == 0) store_interval<Acc, VEC, LPP, CPL, IS_MAX>(P, s_out, acc, arg, i0, __ldg(P.starts + i0 + 1), cell0, b,
+                                   sub, nchunks);
+        written = 1u << static_cast<int>(int64_t(__ldg(P.icells + i0)) - cell0);
     }
     // every group's `written` bits -> the whole warp
 #pragma unroll
@@ -296,8 +362,9 @@ inline int64_t pool_tiles(const PoolParams &p) { return int64_t(p.nx) * p.tiles_
 
 // pool.cu
 PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const uint32_t *icells,
-                            const uint32_t *cell_first, int C, int nx, int ny, float *out,
-                            int mode);
+                            const uint32_t *cell_first, const uint32_t *units,
+                            const int64_t *n_units, int64_t max_units, int C, int nx, int ny,
+                            float *out, int mode);
 template <typename T>
 void launch_to_nhwc(const T *src, int64_t NB, int A, int HW, T *dst, cudaStream_t s);
 
@@ -325,7 +392,7 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     BVP_REQUIRE(sh.lpp > 0, BVP_ERR_UNSUPPORTED, "channel count %d not supported", p.C);
     const size_t smem = size_t(kPoolWarps) * p.C * kTilePitch * sizeof(float);
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
-    const dim3 grid(static_cast<unsigned>(ceil_div(pool_tiles(p), kPoolWarps)),
+    const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps)),
                     static_cast<unsigned>(B));
 #define BVP_LAUNCH_SHAPE(L, CP)                                                              \
     if (sh.lpp == L && sh.cpl == CP) {                                                       \

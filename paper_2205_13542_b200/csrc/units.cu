@@ -1,0 +1,117 @@
+// units.cu -- balanced work units for the interval kernels (part of the
+// cached association; built once per rig like the ranks).
+//
+// A unit is a run of <= 32 consecutive cells inside one 32-cell row tile
+// whose intervals hold <= budget in-range points (a single heavier cell is a
+// unit of its own).  Units are listed in x-major tile order, so the warps of
+// one CTA (consecutive units) cover neighbouring BEV rows.  Bounding the work
+// per warp removes the long tail of dense near-camera tiles; writing every
+// cell of the run (zeros included) keeps exactly one store per output.
+#include <algorithm>
+
+#include "scan.cuh"
+
+namespace bvp {
+
+__device__ __forceinline__ uint32_t cell_points(const uint32_t *__restrict__ starts,
+                                                const uint32_t *__restrict__ cell_first,
+                                                int64_t c) {
+    const uint32_t a = cell_first[c], b = cell_first[c + 1];
+    return b > a ? starts[a + 1] - starts[a] : 0u;  // at most one interval per cell
+}
+
+template <bool WRITE>
+__global__ void units_kernel(const uint32_t *__restrict__ starts,
+                             const uint32_t *__restrict__ cell_first, int nx, int ny,
+                             int tiles_y, uint32_t budget, uint32_t *__restrict__ tile_units,
+                             const uint32_t *__restrict__ offsets, uint32_t *__restrict__ units) {
+    const int64_t ntiles = int64_t(nx) * tiles_y;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int ty = static_cast<int>(t / nx), ix = static_cast<int>(t - int64_t(ty) * nx);
+        const int iy0 = ty * kTileCells;
+        const int n = min(kTileCells, ny - iy0);
+        const int64_t c0 = int64_t(ix) * ny + iy0;
+        uint32_t count = 0, acc = 0;
+        int start = 0;
+        uint32_t out = WRITE ? offsets[t] : 0u;
+        for (int k = 0; k < n; ++k) {
+            const uint32_t p = cell_points(starts, cell_first, c0 + k);
+            if (acc > 0 && acc + p > budget) {
+                if (WRITE) {
+                    units[2 * out] = static_cast<uint32_t>(c0 + start);
+                    units[2 * out + 1] = static_cast<uint32_t>(k - start);
+                    ++out;
+                }
+                ++count;
+                start = k;
+                acc = 0;
+            }
+            acc += p;
+        }
+        if (WRITE) {
+            units[2 * out] = static_cast<uint32_t>(c0 + start);
+            units[2 * out + 1] = static_cast<uint32_t>(n - start);
+        } else {
+            tile_units[t] = count + 1;
+        }
+    }
+}
+
+__global__ void store_count_kernel(const uint32_t *__restrict__ total, int64_t *__restrict__ n) {
+    *n = *total;
+}
+
+struct UnitsLayout {
+    int64_t ntiles;
+    size_t off_tile, off_part, off_total, bytes;
+};
+static UnitsLayout units_layout(int nx, int ny) {
+    UnitsLayout L{};
+    L.ntiles = int64_t(nx) * ((ny + kTileCells - 1) / kTileCells);
+    L.off_tile = 0;
+    L.off_part = (size_t(L.ntiles) * 4 + 255) & ~size_t(255);
+    L.off_total = (L.off_part + size_t(scan_partials_len<uint32_t>(L.ntiles)) * 4 + 255) &
+                  ~size_t(255);
+    L.bytes = L.off_total + 256;
+    return L;
+}
+
+}  // namespace bvp
+
+using namespace bvp;
+
+extern "C" {
+
+int64_t bvp_units_capacity(int nx, int ny, int64_t n_int_max) {
+    return units_layout(nx, ny).ntiles + n_int_max;
+}
+
+size_t bvp_units_workspace_bytes(int nx, int ny) { return units_layout(nx, ny).bytes; }
+
+int bvp_make_units(const uint32_t *interval_starts, const uint32_t *cell_first, int nx, int ny,
+                   int budget, uint32_t *units, int64_t *n_units, void *workspace,
+                   size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(interval_starts && cell_first && units && n_units, BVP_ERR_INVALID,
+                "null pointer argument");
+    BVP_REQUIRE(nx >= 1 && ny >= 1 && budget >= 1, BVP_ERR_INVALID, "bad arguments");
+    const UnitsLayout L = units_layout(nx, ny);
+    BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
+                "units workspace too small: need %zu bytes", L.bytes);
+    cudaStream_t s = as_stream(stream);
+    char *ws = static_cast<char *>(workspace);
+    auto *tile_units = reinterpret_cast<uint32_t *>(ws + L.off_tile);
+    auto *part = reinterpret_cast<uint32_t *>(ws + L.off_part);
+    auto *total = reinterpret_cast<uint32_t *>(ws + L.off_total);
+    const int tiles_y = (ny + kTileCells - 1) / kTileCells;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(L.ntiles, 128), 4096));
+    units_kernel<false><<<blocks, 128, 0, s>>>(interval_starts, cell_first, nx, ny, tiles_y,
+                                               uint32_t(budget), tile_units, nullptr, nullptr);
+    device_excl_scan<uint32_t>(tile_units, tile_units, L.ntiles, part, total, s);
+    units_kernel<true><<<blocks, 128, 0, s>>>(interval_starts, cell_first, nx, ny, tiles_y,
+                                              uint32_t(budget), nullptr, tile_units, units);
+    store_count_kernel<<<1, 1, 0, s>>>(total, n_units);
+    return check_launch("make_units");
+}
+
+}  // extern "C"

@@ -177,13 +177,14 @@ def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
     """Interval-reduction pooling (reference pooling.py:206-221) on the GPU."""
     reducer = _reducer(reducer)
     inp = _check_inputs(features, dist, cache, grid, check_finite)
-    cache = cache.for_grid(grid.n_cells)
+    cache = cache.for_grid(grid)
     out = torch.empty((inp.B, inp.C, grid.n_cells), dtype=torch.float32, device=inp.feats.device)
     if inp.C:
         nhwc = torch.empty(inp.feats.numel(), dtype=torch.float32, device=inp.feats.device)
         _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                  ptr(cache.d_cell_first), inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
+                  ptr(cache.d_cell_first), *cache.unit_args(), inp.B, inp.N, inp.C, inp.H,
+                  inp.W, inp.D,
                   grid.nx, grid.ny, cache.n_int_max, _MODE[reducer],
                   int(DEFAULT_EXACT if exact is None else exact), ptr(out), ptr(nhwc), None,
                   stream_ptr(inp.feats.device))
@@ -200,7 +201,7 @@ def pool_prefixsum(features, dist, cache: AssociationCache, grid: BevGridSpec,
     inp = _check_inputs(features, dist, cache, grid, check_finite)
     if inp.batched:
         raise ConfigurationError("the prefix-sum baseline pools one sample at a time")
-    cache = cache.for_grid(grid.n_cells)
+    cache = cache.for_grid(grid)
     dev = inp.feats.device
     out = torch.empty((1, inp.C, grid.n_cells), dtype=torch.float32, device=dev)
     n_in, n_int = cache.n_in_range, cache.n_intervals
@@ -230,7 +231,7 @@ class PoolPlan:
         self.dev = cuda_device(device if device is not None else cache.device)
         if cache.n_points != n_cameras * height * width * depth_bins:
             raise StaleCacheError("cache does not match the planned frustum")
-        self.cache = cache.for_grid(grid.n_cells)
+        self.cache = cache.for_grid(grid)
         self.grid = grid
         self.B, self.N, self.C, self.H, self.W, self.D = (batch, n_cameras, channels, height,
                                                           width, depth_bins)
@@ -257,7 +258,8 @@ class PoolPlan:
         out = self.out if out is None else out
         c = self.cache
         _lib.call("bvp_pool_forward_nhwc_f32", ptr(self.nhwc), ptr(dist), ptr(c.d_ranks),
-                  ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first), self.B,
+                  ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
+                  *c.unit_args(), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
                   self.mode, self.exact, ptr(out), None, stream_ptr(self.dev))
         return out
@@ -361,12 +363,13 @@ def pool_lifted(x: torch.Tensor, cache: AssociationCache, grid: BevGridSpec,
     reducer = _reducer(reducer)
     if x.dim() != 2 or x.shape[0] != cache.n_points or x.dtype != torch.float32:
         raise ValidationError("x must be float32 (n_points, C)")
-    cache = cache.for_grid(grid.n_cells)
+    cache = cache.for_grid(grid)
     C = x.shape[1]
     x = x.contiguous()
     out = torch.empty((C, grid.n_cells), dtype=torch.float32, device=x.device)
     _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
-              ptr(cache.d_interval_cells), ptr(cache.d_cell_first), C, grid.nx, grid.ny,
+              ptr(cache.d_interval_cells), ptr(cache.d_cell_first), *cache.unit_args(), C,
+              grid.nx, grid.ny,
               _MODE[reducer], ptr(out), stream_ptr(x.device))
     return BevFeatureMap(out.view(C, grid.nx, grid.ny), grid)
 
@@ -387,13 +390,14 @@ def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCa
         raise ValidationError("logits and context disagree on (B, N, H, W)")
     if cache.n_points != N * H * W * D:
         raise StaleCacheError("cache does not match the logits' frustum")
-    cache = cache.for_grid(grid.n_cells)
+    cache = cache.for_grid(grid)
     dev = lg.device
     out = torch.empty((B, C, grid.n_cells), dtype=torch.float32, device=dev)
     ws = torch.empty(_lib.load().bvp_fused_workspace_bytes(B, N, C, H, W), dtype=torch.uint8,
                      device=dev)
     _lib.call("bvp_fused_pool_bf16", ptr(lg), ptr(cx), ptr(cache.d_ranks),
               ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_cell_first),
+              *cache.unit_args(),
               B, N, C, H, W, D, grid.nx, grid.ny, _MODE[reducer], ptr(out), ptr(ws), ws.numel(),
               stream_ptr(dev))
     v = out.view(B, C, grid.nx, grid.ny)

@@ -106,7 +106,8 @@ def test_normalize_depth_matches_reference(golden):
 def worked_example():
     frustum = bp.FrustumSpec(1, 4, depth_min=1.0, depth_step=1.0, depth_bins=1)
     grid = bp.BevGridSpec(0.0, 1.2, 0.0, 0.4, -1, 1, r=0.4)
-    cache = bp.cache_from_cells(np.array([2, 0, 2, 1], np.uint32), grid.n_cells, 0, 1, frustum, grid)
+    cache = bp.cache_from_cells(np.array([2, 0, 2, 1], np.uint32), grid.nx, grid.ny, 0, 1,
+                                frustum, grid)
     features = np.array([1, 2, 3, 4], np.float32).reshape(1, 1, 1, 4)
     dist = np.ones((1, 1, 1, 4), np.float32)
     return features, dist, cache, grid
@@ -165,7 +166,7 @@ def test_zero_weights_give_zero_map(backend):
 def test_empty_ranks_give_zero_map(backend):
     frustum = bp.FrustumSpec(1, 4, 1.0, 1.0, 1)
     grid = bp.BevGridSpec(0.0, 1.2, 0.0, 0.4, -1, 1, r=0.4)
-    cache = bp.cache_from_cells(np.full(4, bp.OUT_OF_RANGE, np.uint32), grid.n_cells, 0, 1,
+    cache = bp.cache_from_cells(np.full(4, bp.OUT_OF_RANGE, np.uint32), grid.nx, grid.ny, 0, 1,
                                 frustum, grid)
     assert cache.n_in_range == 0 and cache.n_intervals == 0
     out = bp.pool(np.ones((1, 2, 1, 4), np.float32), np.ones((1, 1, 1, 4), np.float32), cache,
