@@ -43,8 +43,8 @@ def test_library_is_sm100a_only():
 def test_abi_version_and_errors_without_gpu():
     lib = _lib.load()
     assert lib.bvp_abi_version() == _lib.ABI_VERSION
-    rc = lib.bvp_pool_forward_f32(None, None, None, None, None, None, 0, 1, 1, 1, 1, 1, 1, 1, 1,
-                                  0, 0, None, None, None, None)
+    rc = lib.bvp_pool_forward_f32(None, None, None, None, None, None, None, None, 0, 0, 1, 1, 1,
+                                  1, 1, 1, 1, 1, 0, 0, None, None, None, None)
     assert rc == _lib.BVP_ERR_INVALID
     assert b"bad dims" in lib.bvp_last_error()
     with pytest.raises(bp.ValidationError):
