@@ -107,10 +107,19 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D,
  * count; at most bvp_units_capacity() units are written. */
 int64_t bvp_units_capacity(int nx, int ny, int64_t n_int_max);
 size_t bvp_units_workspace_bytes(int nx, int ny);
-int bvp_make_units(const uint32_t *interval_starts, const uint32_t *cell_first,
-                   int nx, int ny, int budget, uint32_t *units,
-                   int64_t *n_units, void *workspace, size_t workspace_bytes,
-                   void *stream);
+/* ... together with point_meta (2 x uint32 per sorted point: feature row
+ * n*H*W + h*W + w and weight index (n*D + d)*H*W + h*W + w of ranks[j]), the
+ * precomputed gather indices of the fast kernels.  Run after the cache build
+ * (reads n_in from counts). */
+int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
+                      const uint32_t *cell_first, const int64_t *counts, int N,
+                      int H, int W, int D, int nx, int ny, int budget,
+                      uint32_t *units, int64_t *n_units, uint32_t *point_meta,
+                      void *workspace, size_t workspace_bytes, void *stream);
+/* point_meta alone (point_meta may be NULL above, e.g. when the frustum shape
+ * of a loaded cache is only known at pooling time). */
+int bvp_point_meta(const uint32_t *ranks, const int64_t *counts, int N, int H,
+                   int W, int D, uint32_t *point_meta, void *stream);
 
 /* ---- cached forward ---------------------------------------------------- */
 /* The pooling entry points take the cache's units (units, device count
@@ -131,6 +140,7 @@ int bvp_pool_forward_f32(const float *features, const float *dist,
                          const uint32_t *ranks, const uint32_t *interval_starts,
                          const uint32_t *interval_cells,
                          const uint32_t *cell_first, const uint32_t *units,
+                         const uint32_t *point_meta,
                          const int64_t *n_units, int64_t max_units,
                          int B, int N, int C, int H,
                          int W, int D, int nx, int ny, int64_t n_int_max,
@@ -148,6 +158,7 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,
                               const uint32_t *interval_starts,
                               const uint32_t *interval_cells,
                               const uint32_t *cell_first, const uint32_t *units,
+                         const uint32_t *point_meta,
                               const int64_t *n_units, int64_t max_units,
                               int B, int N, int C,
                               int H, int W, int D, int nx, int ny,
@@ -177,6 +188,7 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
                         const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
                         const uint32_t *cell_first, const uint32_t *units,
+                         const uint32_t *point_meta,
                         const int64_t *n_units, int64_t max_units,
                         int C, int nx, int ny,
                         int mode, float *out, void *stream);
@@ -192,6 +204,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context,
                         const uint32_t *ranks, const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
                         const uint32_t *cell_first, const uint32_t *units,
+                         const uint32_t *point_meta,
                         const int64_t *n_units, int64_t max_units,
                         int B, int N, int C, int H,
                         int W, int D, int nx, int ny, int mode, float *out,

@@ -47,20 +47,22 @@ SIGNATURES = {
     "bvp_pool_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
     "bvp_units_capacity": (_L, [_I, _I, _L]),
     "bvp_units_workspace_bytes": (_S, [_I, _I]),
-    "bvp_make_units": (_I, [_P, _P, _I, _I, _I, _P, _P, _P, _S, _P]),
-    "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _I,
-                                  _I, _I, _L, _I, _I, _P, _P, _P, _P]),
-    "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I,
-                                       _I, _I, _I, _L, _I, _I, _P, _P, _P]),
+    "bvp_make_schedule": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _S,
+                               _P]),
+    "bvp_point_meta": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
+    "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I,
+                                  _I, _I, _I, _L, _I, _I, _P, _P, _P, _P]),
+    "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I,
+                                       _I, _I, _I, _I, _L, _I, _I, _P, _P, _P]),
     "bvp_to_nhwc_f32": (_I, [_P, _I, _I, _I, _P, _P]),
     "bvp_reorder_weights": (_I, [_P, _P, _L, _I, _I, _I, _I, _P, _P]),
     "bvp_normalize_depth": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "bvp_any_nonfinite": (_I, [_P, _L, _P, _P]),
     "bvp_lift_f32": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P]),
-    "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P]),
+    "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P]),
     "bvp_fused_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
-    "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _I,
-                                 _I, _I, _I, _P, _P, _S, _P]),
+    "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I,
+                                 _I, _I, _I, _I, _P, _P, _S, _P]),
     "bvp_backward_workspace_bytes": (_S, [_I, _I, _L]),
     "bvp_pool_backward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                    _I, _L, _I, _P, _P, _P, _S, _P]),

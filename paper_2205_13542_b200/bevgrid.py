@@ -140,6 +140,7 @@ class AssociationCache:
     d_counts: torch.Tensor                 # (2,) int64: n_in, n_int
     d_units: torch.Tensor                  # (2 * max_units,) (first cell, count)
     d_n_units: torch.Tensor                # (1,) int64
+    d_meta: torch.Tensor                   # (2 * P,) per sorted point: row, weight index
     max_units: int                         # launch bound (>= device count)
     fingerprint: int
     nx: int
@@ -147,6 +148,7 @@ class AssociationCache:
     n_cameras: int | None = None
     frustum: FrustumSpec | None = field(default=None, repr=False)
     grid: BevGridSpec | None = field(default=None, repr=False)
+    meta_dims: tuple | None = None         # (N, H, W, D) d_meta was derived for
     _host_counts: tuple | None = field(default=None, repr=False)
     _host: dict = field(default_factory=dict, repr=False)
 
@@ -186,9 +188,15 @@ class AssociationCache:
     def n_units(self) -> int:
         return int(self.d_n_units.item())
 
-    def unit_args(self):
-        """(units, n_units, max_units) as the C ABI takes them."""
-        return ptr(self.d_units), ptr(self.d_n_units), self.max_units
+    def unit_args(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1):
+        """(units, point_meta, n_units, max_units) as the C ABI takes them;
+        the point gather table is (re)derived for an (N, H, W, D) frustum
+        (N=None: caller does not read it, e.g. the materialised path)."""
+        if N is not None and self.meta_dims != (N, H, W, D):
+            _lib.call("bvp_point_meta", ptr(self.d_ranks), ptr(self.d_counts), N, H, W, D,
+                      ptr(self.d_meta), stream_ptr(self.device))
+            self.meta_dims = (N, H, W, D)
+        return ptr(self.d_units), ptr(self.d_meta), ptr(self.d_n_units), self.max_units
 
     # ---- reference-typed host views ------------------------------------
     def _view(self, name, tensor, n):
@@ -244,20 +252,24 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
         cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
         counts=torch.zeros(2, dtype=torch.int64, device=dev),
         units=torch.empty(2 * cap, **i32), n_units=torch.zeros(1, dtype=torch.int64, device=dev),
+        meta=torch.empty(2 * P, **i32),
         cap=cap, ws=torch.empty(ws, dtype=torch.uint8, device=dev),
     )
 
 
-def _make_units(b: dict, nx: int, ny: int, budget: int, dev) -> None:
-    _lib.call("bvp_make_units", ptr(b["starts"]), ptr(b["cell_first"]), nx, ny, budget,
-              ptr(b["units"]), ptr(b["n_units"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
+def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None) -> None:
+    """Work units, plus the point gather table when the frustum dims are known."""
+    N, H, W, D = dims if dims is not None else (1, 1, 1, 1)
+    _lib.call("bvp_make_schedule", ptr(b["ranks"]), ptr(b["starts"]), ptr(b["cell_first"]),
+              ptr(b["counts"]), N, H, W, D, nx, ny, budget, ptr(b["units"]), ptr(b["n_units"]),
+              ptr(b["meta"]) if dims is not None else None, ptr(b["ws"]), b["ws"].numel(),
+              stream_ptr(dev))
 
 
-def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, max_units=None):
+def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, dims=None):
     return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
-                            b["iop"], b["counts"], b["units"], b["n_units"],
-                            b["cap"] if max_units is None else max_units, fingerprint, nx, ny,
-                            n_cameras, frustum, grid)
+                            b["iop"], b["counts"], b["units"], b["n_units"], b["meta"],
+                            b["cap"], fingerprint, nx, ny, n_cameras, frustum, grid, dims)
 
 
 class CacheBuilder:
@@ -287,8 +299,9 @@ class CacheBuilder:
                   ptr(b["cells"]), ptr(b["ranks"]), ptr(b["starts"]), ptr(b["icells"]),
                   ptr(b["cell_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
                   b["ws"].numel(), stream_ptr(self.dev))
-        _make_units(b, g.nx, g.ny, self.unit_budget, self.dev)
-        return _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g)
+        dims = (self.n_cameras, f.height, f.width, f.depth_bins)
+        _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims)
+        return _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
 
 
 def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
@@ -327,8 +340,11 @@ def cache_from_cells(cell_of_point, nx: int, ny: int, fingerprint: int = 0, n_ca
     _lib.call("bvp_sort_intervals", ptr(b["cells"]), P, n_cells, ptr(b["ranks"]),
               ptr(b["starts"]), ptr(b["icells"]), ptr(b["cell_first"]), ptr(b["iop"]),
               ptr(b["counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
-    _make_units(b, nx, ny, unit_budget, dev)
-    cache = _cache_of(b, fingerprint, nx, ny, n_cameras, frustum, grid)
+    dims = None
+    if frustum is not None and n_cameras is not None:
+        dims = (n_cameras, frustum.height, frustum.width, frustum.depth_bins)
+    _make_schedule(b, nx, ny, unit_budget, dev, dims)
+    cache = _cache_of(b, fingerprint, nx, ny, n_cameras, frustum, grid, dims)
     cache._counts()
     cache.max_units = max(1, cache.n_units)
     return cache

@@ -64,7 +64,7 @@ size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W) {
 
 int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const uint32_t *ranks,
                         const uint32_t *interval_starts, const uint32_t *interval_cells,
-                        const uint32_t *cell_first, const uint32_t *units,
+                        const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
                         const int64_t *n_units, int64_t max_units, int B, int N, int C, int H,
                         int W, int D, int nx, int ny, int mode, float *out, void *workspace,
                         size_t workspace_bytes, void *stream) {
@@ -88,7 +88,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     pixel_lse_kernel<<<lb, 128, 0, s>>>(lg, NB, D, int(HW), lse);
     launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
                                   int(HW), ctx, s);
-    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units,
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units, point_meta,
                                     n_units, max_units, C, nx, ny, out, mode);
     p.rows = ctx;
     p.wsrc = lg;

@@ -43,7 +43,7 @@ template void launch_to_nhwc<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int,
                                             __nv_bfloat16 *, cudaStream_t);
 
 PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const uint32_t *icells,
-                            const uint32_t *cell_first, const uint32_t *units,
+                            const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
                             const int64_t *n_units, int64_t max_units, int C, int nx, int ny,
                             float *out, int mode) {
     PoolParams p{};
@@ -52,6 +52,7 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
     p.icells = icells;
     p.cell_first = cell_first;
     p.units = units;
+    p.meta = reinterpret_cast<const uint2 *>(point_meta);
     p.n_units = n_units;
     p.max_units = max_units;
     p.out = out;
@@ -165,7 +166,7 @@ int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst, void *s
 
 int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const uint32_t *ranks,
                               const uint32_t *interval_starts, const uint32_t *interval_cells,
-                              const uint32_t *cell_first, const uint32_t *units,
+                              const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
                               const int64_t *n_units, int64_t max_units, int B, int N, int C,
                               int H, int W, int D, int nx, int ny, int64_t n_int_max, int mode,
                               int exact, float *out, uint32_t *argmax, void *stream) {
@@ -177,7 +178,7 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
                            interval_cells && cell_first && units && n_units),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
-    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units,
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units, point_meta,
                                     n_units, max_units, C, nx, ny, out, mode);
     p.rows = feats_nhwc;
     p.wsrc = dist;
@@ -203,7 +204,7 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
 
 int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_t *ranks,
                          const uint32_t *interval_starts, const uint32_t *interval_cells,
-                         const uint32_t *cell_first, const uint32_t *units,
+                         const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
                          const int64_t *n_units, int64_t max_units, int B, int N, int C, int H,
                          int W, int D, int nx, int ny, int64_t n_int_max, int mode, int exact,
                          float *out, float *feats_nhwc, uint32_t *argmax, void *stream) {
@@ -211,7 +212,7 @@ int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_
     BVP_REQUIRE(C == 0 || (features && feats_nhwc), BVP_ERR_INVALID, "null pointer argument");
     launch_to_nhwc<float>(features, int64_t(B) * N, C, H * W, feats_nhwc, as_stream(stream));
     return bvp_pool_forward_nhwc_f32(feats_nhwc, dist, ranks, interval_starts, interval_cells,
-                                     cell_first, units, n_units, max_units, B, N, C, H, W, D, nx,
+                                     cell_first, units, point_meta, n_units, max_units, B, N, C, H, W, D, nx,
                                      ny, n_int_max, mode, exact, out, argmax, stream);
 }
 
@@ -270,7 +271,7 @@ int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H, 
 
 int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *interval_starts,
                         const uint32_t *interval_cells, const uint32_t *cell_first,
-                        const uint32_t *units, const int64_t *n_units, int64_t max_units, int C,
+                        const uint32_t *units, const uint32_t *point_meta, const int64_t *n_units, int64_t max_units, int C,
                         int nx, int ny, int mode, float *out, void *stream) {
     BVP_REQUIRE(C >= 0 && nx >= 1 && ny >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
                 "bad arguments");
@@ -278,7 +279,7 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *i
                            units && n_units),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
-    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units,
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units, point_meta,
                                     n_units, max_units, C, nx, ny, out, mode);
     p.rows = x;
     p.D = 1;

@@ -51,6 +51,7 @@ struct PoolParams {
     const uint32_t *cell_first;  // n_cells + 1: first interval with cell >= c
     const uint32_t *units;   // work units: (first cell, cell count) pairs
     const int64_t *n_units;  // device count of units
+    const uint2 *meta;       // per sorted point: (feature row, weight index)
     float *out;              // (B, C, n_cells)
     uint32_t *argmax;        // MAX only, optional: (B, n_int_max, C)
     int C, D, HW, NHW;
@@ -332,6 +333,253 @@ pool_tile_kernel(const PoolParams P) {
             out[int64_t(c) * P.n_cells + lane] = has ? s_out[c * kTilePitch + lane] : 0.f;
 }
 
+// Per-warp shared memory of pool_slice_kernel: output tile, partial slots
+// (values + argmax ids) and slot interval ids.
+__host__ __device__ inline size_t slice_smem_per_warp(int C, int ng) {
+    return (size_t(C) * kTilePitch + size_t(ng) * 2 * C * 2 + size_t(ng) * 2) * 4;
+}
+
+// ---------------------------------------------------------------------------
+// Fast (fp32) kernel: balanced slices.
+//
+// The unit's intervals occupy one contiguous range [J0, J1) of the sorted
+// point stream.  Lane-group g reduces the slice [J0 + L*g/NG, J0 + L*(g+1)/NG)
+// sequentially, U points per step, reading each point's precomputed gather
+// indices (feature row, weight index) -- no division, no shuffles in the
+// loop.  Intervals that start and end inside a slice go straight to the
+// output tile; the (at most two) intervals cut by a slice edge leave partial
+// sums in shared slots that are combined afterwards in group order, so the
+// result is deterministic for a given cache.  Every group does the same
+// amount of work whatever the interval lengths.
+// ---------------------------------------------------------------------------
+template <typename Elem, int VEC, int LPP, int CPL, bool IS_MAX, int SRC>
+__global__ void __launch_bounds__(kPoolThreads)
+pool_slice_kernel(const PoolParams P) {
+    extern __shared__ float s_all[];
+    constexpr int NG = 32 / LPP;
+    constexpr int U = CPL > 5 ? 2 : 4;
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane / LPP, sub = lane % LPP;
+    const int C = P.C;
+    const int nchunks = C / VEC;
+    const int b = blockIdx.y;
+    float *s_out = s_all + size_t(warp) * (slice_smem_per_warp(C, NG) / 4);
+    float *s_part = s_out + C * kTilePitch;                                    // [NG][2][C]
+    uint32_t *s_parg = reinterpret_cast<uint32_t *>(s_part + NG * 2 * C);      // [NG][2][C]
+    uint32_t *s_piv = s_parg + NG * 2 * C;                                     // [NG][2]
+
+    const int64_t k = int64_t(blockIdx.x) * kPoolWarps + warp;
+    if (k >= *P.n_units) return;
+    const int64_t cell0 = __ldg(P.units + 2 * k);
+    const int ncell = static_cast<int>(__ldg(P.units + 2 * k + 1));
+    const uint32_t i0 = __ldg(P.cell_first + cell0), i1 = __ldg(P.cell_first + cell0 + ncell);
+    bool has = false;
+    if (lane < ncell)
+        has = __ldg(P.cell_first + cell0 + lane + 1) > __ldg(P.cell_first + cell0 + lane);
+
+    const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
+    const uint32_t J0 = __ldg(P.starts + i0), J1 = __ldg(P.starts + i1);
+    const uint32_t L = J1 - J0;
+    if (L > 0) {
+        const uint32_t ja = J0 + uint32_t((uint64_t(L) * g) / NG);
+        const uint32_t jb = J0 + uint32_t((uint64_t(L) * (g + 1)) / NG);
+        // interval containing ja: the unit has <= 32 intervals, one per lane
+        const uint32_t nint = i1 - i0;
+        const uint32_t s_l = uint32_t(lane) < nint ? __ldg(P.starts + i0 + lane) : kNone;
+        uint32_t loc = 0;
+#pragma unroll 1
+        for (int gg = 0; gg < NG; ++gg) {
+            const uint32_t x = J0 + uint32_t((uint64_t(L) * gg) / NG);
+            const unsigned m = __ballot_sync(0xFFFFFFFFu, s_l <= x);
+            if (g == gg) loc = __popc(m) - 1;
+        }
+        uint32_t iv = i0 + loc;
+        uint32_t hi = __ldg(P.starts + iv + 1);
+        bool cut_first = ja > __ldg(P.starts + iv);  // interval began in an earlier slice
+        uint32_t piv0 = kNone, piv1 = kNone;
+
+        float acc[CPL][VEC];
+        uint32_t arg[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1];
+        auto reset = [&]() {
+#pragma unroll
+            for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                    acc[q][e] = IS_MAX ? -INFINITY : 0.f;
+                    if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = kNone;
+                }
+        };
+        // park the current interval: complete ones in the tile, cut ones in a slot
+        auto park = [&](bool complete, int slot) {
+            if (complete) {
+                const int lc = static_cast<int>(int64_t(__ldg(P.icells + iv)) - cell0);
+                const float inv = P.mean ? 1.f / float(hi - __ldg(P.starts + iv)) : 1.f;
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int ch = sub + q * LPP;
+                    if (ch < nchunks)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            const int c = ch * VEC + e;
+                            s_out[c * kTilePitch + lc] = P.mean ? acc[q][e] * inv : acc[q][e];
+                            if (IS_MAX && P.argmax)
+                                P.argmax[(b * P.n_int_max + iv) * C + c] =
+                                    __ldg(P.ranks + arg[IS_MAX ? q : 0][IS_MAX ? e : 0]);
+                        }
+                }
+            } else {
+                float *dst = s_part + (g * 2 + slot) * C;
+                uint32_t *dsta = s_parg + (g * 2 + slot) * C;
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int ch = sub + q * LPP;
+                    if (ch < nchunks)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            dst[ch * VEC + e] = acc[q][e];
+                            if (IS_MAX) dsta[ch * VEC + e] = arg[IS_MAX ? q : 0][IS_MAX ? e : 0];
+                        }
+                }
+                if (slot == 0) piv0 = iv; else piv1 = iv;
+            }
+        };
+        reset();
+
+        const uint32_t per = (L + NG - 1) / NG;          // longest slice
+        const uint32_t nstep = (per + U - 1) / U;
+        uint2 mn[U];                                      // prefetched gather indices
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t jj = ja + u;
+            if (SRC == kSrcX) mn[u] = make_uint2(jj < jb ? __ldg(P.ranks + jj) : 0u, 0u);
+            else mn[u] = jj < jb ? __ldg(P.meta + jj) : make_uint2(0u, 0u);
+        }
+#pragma unroll 1
+        for (uint32_t st = 0; st < nstep; ++st) {
+            const uint32_t j = ja + st * U;
+            uint2 m[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                m[u] = mn[u];
+                const uint32_t jj = j + U + u;
+                if (SRC == kSrcX) mn[u] = make_uint2(jj < jb ? __ldg(P.ranks + jj) : 0u, 0u);
+                else mn[u] = jj < jb ? __ldg(P.meta + jj) : make_uint2(0u, 0u);
+            }
+            float w[U];
+            float v[U][CPL][VEC];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool ok = j + u < jb;
+                if (SRC == kSrcX) {
+                    w[u] = ok ? 1.f : 0.f;
+                } else if (SRC == kSrcDist) {
+                    w[u] = ok ? __ldg(static_cast<const float *>(P.wsrc) + b * P.w_bstride + m[u].y)
+                              : 0.f;
+                } else {
+                    w[u] = ok ? __expf(__bfloat162float(static_cast<const __nv_bfloat16 *>(
+                                           P.wsrc)[b * P.w_bstride + m[u].y]) -
+                                       __ldg(P.lse + int64_t(b) * P.NHW + m[u].x))
+                              : 0.f;
+                }
+                const Elem *rp = rows + size_t(m[u].x) * C;
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) {
+                    const int ch = sub + q * LPP;
+                    if (ok && ch < nchunks) {
+                        Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v[u][q]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) v[u][q][e] = 0.f;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t jj = j + u;
+                if (jj < jb) {
+                    if (jj == hi) {  // the slice crosses into the next interval
+                        park(!cut_first, 0);
+                        reset();
+                        cut_first = false;
+                        ++iv;
+                        hi = __ldg(P.starts + iv + 1);
+                    }
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) {
+                            if (IS_MAX) {
+                                const float pv = w[u] * v[u][q][e];
+                                if (pv > acc[q][e]) {
+                                    acc[q][e] = pv;
+                                    // sorted position; converted to the point id
+                                    // (ranks[pos]) when written out
+                                    arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = jj;
+                                }
+                            } else {
+                                acc[q][e] = fmaf(w[u], v[u][q][e], acc[q][e]);
+                            }
+                        }
+                }
+            }
+        }
+        if (jb > ja) park(!cut_first && jb == hi, 1);
+        if (sub == 0) {
+            s_piv[g * 2] = piv0;
+            s_piv[g * 2 + 1] = piv1;
+        }
+        __syncwarp();
+        // combine the cut intervals' partial sums in slice order
+        for (int c = lane; c < C; c += 32) {
+            uint32_t run_iv = kNone, run_arg = kNone;
+            float run = 0.f;
+            for (int t = 0; t < 2 * NG; ++t) {
+                const uint32_t x = s_piv[t];
+                if (x == kNone) continue;
+                const float val = s_part[t * C + c];
+                const uint32_t va = IS_MAX ? s_parg[t * C + c] : 0u;
+                if (x != run_iv) {
+                    if (run_iv != kNone) {
+                        const int lc = static_cast<int>(int64_t(__ldg(P.icells + run_iv)) - cell0);
+                        const float inv = P.mean ? 1.f / float(__ldg(P.starts + run_iv + 1) -
+                                                               __ldg(P.starts + run_iv))
+                                                 : 1.f;
+                        s_out[c * kTilePitch + lc] = run * inv;
+                        if (IS_MAX && P.argmax)
+                            P.argmax[(b * P.n_int_max + run_iv) * C + c] =
+                                __ldg(P.ranks + run_arg);
+                    }
+                    run_iv = x;
+                    run = val;
+                    run_arg = va;
+                } else if (IS_MAX) {
+                    if (val > run || (val == run && va < run_arg)) {
+                        run = val;
+                        run_arg = va;
+                    }
+                } else {
+                    run += val;
+                }
+            }
+            if (run_iv != kNone) {
+                const int lc = static_cast<int>(int64_t(__ldg(P.icells + run_iv)) - cell0);
+                const float inv = P.mean ? 1.f / float(__ldg(P.starts + run_iv + 1) -
+                                                       __ldg(P.starts + run_iv))
+                                         : 1.f;
+                s_out[c * kTilePitch + lc] = run * inv;
+                if (IS_MAX && P.argmax)
+                    P.argmax[(b * P.n_int_max + run_iv) * C + c] = __ldg(P.ranks + run_arg);
+            }
+        }
+    }
+    __syncwarp();
+    float *out = P.out + int64_t(b) * C * P.n_cells + cell0;
+    if (lane < ncell)
+        for (int c = 0; c < C; ++c)
+            out[int64_t(c) * P.n_cells + lane] = has ? s_out[c * kTilePitch + lane] : 0.f;
+}
+
 // Lane-group shape for a row of `nchunks` 16-byte chunks: LPP lanes per
 // interval, CPL chunks per lane (instantiated table in pool.cu / fused.cu).
 struct LaneShape {
@@ -362,7 +610,7 @@ inline int64_t pool_tiles(const PoolParams &p) { return int64_t(p.nx) * p.tiles_
 
 // pool.cu
 PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const uint32_t *icells,
-                            const uint32_t *cell_first, const uint32_t *units,
+                            const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
                             const int64_t *n_units, int64_t max_units, int C, int nx, int ny,
                             float *out, int mode);
 template <typename T>
@@ -390,14 +638,23 @@ template <typename Acc, typename Elem, int VEC, int SRC>
 int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     const LaneShape sh = choose_shape(p.C / VEC);
     BVP_REQUIRE(sh.lpp > 0, BVP_ERR_UNSUPPORTED, "channel count %d not supported", p.C);
-    const size_t smem = size_t(kPoolWarps) * p.C * kTilePitch * sizeof(float);
+    constexpr bool kFast = sizeof(Acc) == sizeof(float);
+    const size_t smem = kFast ? kPoolWarps * slice_smem_per_warp(p.C, 32 / sh.lpp)
+                              : size_t(kPoolWarps) * p.C * kTilePitch * sizeof(float);
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
+    BVP_REQUIRE(!kFast || SRC == kSrcX || p.meta, BVP_ERR_INVALID,
+                "the cache's point gather table (point_meta) is required");
     const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps)),
                     static_cast<unsigned>(B));
 #define BVP_LAUNCH_SHAPE(L, CP)                                                              \
     if (sh.lpp == L && sh.cpl == CP) {                                                       \
-        auto k = is_max ? pool_tile_kernel<Acc, Elem, VEC, L, CP, true, SRC>                 \
-                        : pool_tile_kernel<Acc, Elem, VEC, L, CP, false, SRC>;               \
+        void (*k)(const PoolParams);                                                         \
+        if constexpr (kFast)                                                                 \
+            k = is_max ? pool_slice_kernel<Elem, VEC, L, CP, true, SRC>                      \
+                       : pool_slice_kernel<Elem, VEC, L, CP, false, SRC>;                    \
+        else                                                                                 \
+            k = is_max ? pool_tile_kernel<Acc, Elem, VEC, L, CP, true, SRC>                  \
+                       : pool_tile_kernel<Acc, Elem, VEC, L, CP, false, SRC>;                \
         if (smem > 48 * 1024)                                                                \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         k<<<grid, kPoolThreads, smem, s>>>(p);                                               \

@@ -58,6 +58,21 @@ __global__ void units_kernel(const uint32_t *__restrict__ starts,
     }
 }
 
+// Per sorted point: (feature row = pixel, weight index into (N,D,H,W)) so the
+// interval kernels never divide.
+__global__ void point_meta_kernel(const uint32_t *__restrict__ ranks,
+                                  const int64_t *__restrict__ counts, int64_t P, int D, int HW,
+                                  uint2 *__restrict__ meta) {
+    const int64_t n_in = counts[0];
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_in && j < P;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = ranks[j];
+        const uint32_t pix = p / D, d = p - pix * D;
+        const uint32_t n = pix / HW, hw = pix - n * HW;
+        meta[j] = make_uint2(pix, (n * D + d) * HW + hw);
+    }
+}
+
 __global__ void store_count_kernel(const uint32_t *__restrict__ total, int64_t *__restrict__ n) {
     *n = *total;
 }
@@ -89,12 +104,15 @@ int64_t bvp_units_capacity(int nx, int ny, int64_t n_int_max) {
 
 size_t bvp_units_workspace_bytes(int nx, int ny) { return units_layout(nx, ny).bytes; }
 
-int bvp_make_units(const uint32_t *interval_starts, const uint32_t *cell_first, int nx, int ny,
-                   int budget, uint32_t *units, int64_t *n_units, void *workspace,
-                   size_t workspace_bytes, void *stream) {
-    BVP_REQUIRE(interval_starts && cell_first && units && n_units, BVP_ERR_INVALID,
-                "null pointer argument");
-    BVP_REQUIRE(nx >= 1 && ny >= 1 && budget >= 1, BVP_ERR_INVALID, "bad arguments");
+int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
+                      const uint32_t *cell_first, const int64_t *counts, int N, int H, int W,
+                      int D, int nx, int ny, int budget, uint32_t *units, int64_t *n_units,
+                      uint32_t *point_meta, void *workspace, size_t workspace_bytes,
+                      void *stream) {
+    BVP_REQUIRE(ranks && interval_starts && cell_first && counts && units && n_units,
+                BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(nx >= 1 && ny >= 1 && budget >= 1 && N >= 1 && H >= 1 && W >= 1 && D >= 1,
+                BVP_ERR_INVALID, "bad arguments");
     const UnitsLayout L = units_layout(nx, ny);
     BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
                 "units workspace too small: need %zu bytes", L.bytes);
@@ -111,7 +129,22 @@ int bvp_make_units(const uint32_t *interval_starts, const uint32_t *cell_first, 
     units_kernel<true><<<blocks, 128, 0, s>>>(interval_starts, cell_first, nx, ny, tiles_y,
                                               uint32_t(budget), nullptr, tile_units, units);
     store_count_kernel<<<1, 1, 0, s>>>(total, n_units);
-    return check_launch("make_units");
+    if (point_meta) {
+        const int rc = bvp_point_meta(ranks, counts, N, H, W, D, point_meta, stream);
+        if (rc != BVP_OK) return rc;
+    }
+    return check_launch("make_schedule");
+}
+
+int bvp_point_meta(const uint32_t *ranks, const int64_t *counts, int N, int H, int W, int D,
+                   uint32_t *point_meta, void *stream) {
+    BVP_REQUIRE(ranks && counts && point_meta, BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(N >= 1 && H >= 1 && W >= 1 && D >= 1, BVP_ERR_INVALID, "bad dims");
+    const int64_t P = int64_t(N) * H * W * D;
+    const unsigned mb = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), 148 * 32));
+    point_meta_kernel<<<mb, 256, 0, as_stream(stream)>>>(ranks, counts, P, D, H * W,
+                                                         reinterpret_cast<uint2 *>(point_meta));
+    return check_launch("point_meta");
 }
 
 }  // extern "C"

@@ -43,8 +43,9 @@ def test_library_is_sm100a_only():
 def test_abi_version_and_errors_without_gpu():
     lib = _lib.load()
     assert lib.bvp_abi_version() == _lib.ABI_VERSION
-    rc = lib.bvp_pool_forward_f32(None, None, None, None, None, None, None, None, 0, 0, 1, 1, 1,
-                                  1, 1, 1, 1, 1, 0, 0, None, None, None, None)
+    # every pointer NULL, every size 0 (B = 0 is rejected before any CUDA call)
+    argtypes = _lib.SIGNATURES["bvp_pool_forward_f32"][1]
+    rc = lib.bvp_pool_forward_f32(*[None if t is ctypes.c_void_p else 0 for t in argtypes])
     assert rc == _lib.BVP_ERR_INVALID
     assert b"bad dims" in lib.bvp_last_error()
     with pytest.raises(bp.ValidationError):
