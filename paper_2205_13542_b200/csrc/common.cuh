@@ -5,12 +5,15 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/bevpool_b200.h"
 
 namespace bvp {
 
 constexpr uint32_t kOOR = BVP_OUT_OF_RANGE;
-constexpr int kTileCells = BVP_TILE_CELLS;
+constexpr int kTileCells = BVP_TILE_CELLS;  // row tile of the backward's grad transpose
+constexpr int kUnitCells = 8;               // cells per work unit of the interval kernels
 
 // ---- error channel (host) --------------------------------------------------
 void set_error(const char *fmt, ...);

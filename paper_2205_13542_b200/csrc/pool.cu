@@ -59,7 +59,6 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
     p.C = C;
     p.nx = nx;
     p.ny = ny;
-    p.tiles_y = (ny + kTileCells - 1) / kTileCells;
     p.n_cells = int64_t(nx) * ny;
     p.mean = mode == BVP_MEAN;
     return p;

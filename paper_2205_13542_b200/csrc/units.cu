@@ -29,8 +29,8 @@ __global__ void units_kernel(const uint32_t *__restrict__ starts,
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int ty = static_cast<int>(t / nx), ix = static_cast<int>(t - int64_t(ty) * nx);
-        const int iy0 = ty * kTileCells;
-        const int n = min(kTileCells, ny - iy0);
+        const int iy0 = ty * kUnitCells;
+        const int n = min(kUnitCells, ny - iy0);
         const int64_t c0 = int64_t(ix) * ny + iy0;
         uint32_t count = 0, acc = 0;
         int start = 0;
@@ -83,7 +83,7 @@ struct UnitsLayout {
 };
 static UnitsLayout units_layout(int nx, int ny) {
     UnitsLayout L{};
-    L.ntiles = int64_t(nx) * ((ny + kTileCells - 1) / kTileCells);
+    L.ntiles = int64_t(nx) * ((ny + kUnitCells - 1) / kUnitCells);
     L.off_tile = 0;
     L.off_part = (size_t(L.ntiles) * 4 + 255) & ~size_t(255);
     L.off_total = (L.off_part + size_t(scan_partials_len<uint32_t>(L.ntiles)) * 4 + 255) &
@@ -121,7 +121,7 @@ int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
     auto *tile_units = reinterpret_cast<uint32_t *>(ws + L.off_tile);
     auto *part = reinterpret_cast<uint32_t *>(ws + L.off_part);
     auto *total = reinterpret_cast<uint32_t *>(ws + L.off_total);
-    const int tiles_y = (ny + kTileCells - 1) / kTileCells;
+    const int tiles_y = (ny + kUnitCells - 1) / kUnitCells;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(L.ntiles, 128), 4096));
     units_kernel<false><<<blocks, 128, 0, s>>>(interval_starts, cell_first, nx, ny, tiles_y,
                                                uint32_t(budget), tile_units, nullptr, nullptr);
