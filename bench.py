@@ -406,7 +406,7 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
 
     def pool_x():
         _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
-                  ptr(cache.d_interval_cells), ptr(cache.d_cell_first), *cache.unit_args(), C,
+                  ptr(cache.d_interval_cells), ptr(cache.d_cell_first), cache.schedule(), C,
                   grid.nx, grid.ny, 0,
                   ptr(outx),
                   stream_ptr(dev))

@@ -14,17 +14,22 @@
  *                         (bevgrid.py:183-203)
  *   bvp_pool_forward_f32  pool_interval -> _kernels.interval_reduce
  *                         (pooling.py:206-221, _kernels.py:22-63)
+ *   bvp_pool_prefixsum_f32  pool_prefixsum (pooling.py:162-196)
  *   bvp_reorder_weights   reorder_weights (pooling.py:243-261)
  *   bvp_normalize_depth   normalize_depth (lift.py:17-31)
+ *   bvp_any_nonfinite     the finiteness checks of _check_inputs
+ *                         (pooling.py:92-95)
  *   bvp_lift_f32 / bvp_pool_lifted_f32   the paper's materialised frustum
- *                         x = depth (x) feature then bev_pool
- *   bvp_fused_pool_bf16   lift+pool fused (no reference counterpart; config F)
- *   bvp_pool_backward_f32 gather backward (no reference counterpart)
+ *                         x = depth (x) feature, then bev_pool
+ *   bvp_fused_pool_bf16   lift + pool fused (config F; no reference
+ *                         counterpart, semantics normalize_depth + pool)
+ *   bvp_pool_backward_f32 gather backward (config B; SPEC.md:540 lists
+ *                         autograd as a reference non-goal)
  *
- * Cache layout on the device (all uint32, produced by bvp_build_cache):
+ * Cache layout on the device (all uint32 unless noted), from bvp_build_cache:
  *   cell_of_point[P]        flat cell id per frustum point or 0xFFFFFFFF
- *   ranks[P]                first n_in entries valid (point ids sorted by cell,
- *                           stable)
+ *   ranks[P]                first n_in entries valid (point ids sorted by
+ *                           cell, stable)
  *   interval_starts[n_cells+1]  first n_int entries as the reference, plus a
  *                           sentinel interval_starts[n_int] = n_in
  *   interval_cells[n_cells] first n_int entries valid
@@ -33,7 +38,9 @@
  *                           of any run of cells in O(1)
  *   interval_of_point[P]    interval index per point or 0xFFFFFFFF
  *   counts[2] (int64)       n_in, n_int
- * so a whole frame can be rebuilt and pooled without a host round trip.
+ * and from bvp_make_schedule the work schedule of the interval kernels
+ * (bvp_schedule below).  A whole frame can be rebuilt and pooled without a
+ * host round trip.
  */
 #ifndef BEVPOOL_B200_H
 #define BEVPOOL_B200_H
@@ -50,7 +57,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BVP_ABI_VERSION 1
+#define BVP_ABI_VERSION 2
 
 #define BVP_OK 0
 #define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
@@ -63,6 +70,25 @@ extern "C" {
 #define BVP_SUM 0
 #define BVP_MEAN 1
 #define BVP_MAX 2
+
+/* Work schedule of the interval kernels (device pointers; built once per
+ * cache by bvp_make_schedule).
+ *   units       2 x uint32 per unit: first flat cell, cell count (<= 8) with
+ *               bit 31 set for a "long" unit (one cell holding more than the
+ *               point budget; the fast kernels split it over a CTA)
+ *   point_meta  2 x uint32 per sorted point j: feature row n*H*W + h*W + w
+ *               and weight index (n*D + d)*H*W + h*W + w of ranks[j]
+ *   long_units  unit indices of the long units
+ *   counts      device int64[2]: n_units, n_long
+ *   max_units, max_long  host launch sizes (>= the device counts) */
+typedef struct bvp_schedule {
+    const uint32_t *units;
+    const uint32_t *point_meta;
+    const uint32_t *long_units;
+    const int64_t *counts;
+    int64_t max_units;
+    int64_t max_long;
+} bvp_schedule;
 
 int bvp_abi_version(void);
 const char *bvp_last_error(void);
@@ -98,32 +124,29 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D,
                     int64_t *counts, void *workspace, size_t workspace_bytes,
                     void *stream);
 
-/* ---- work units (cached with the association) -------------------------- */
+/* ---- work schedule (cached with the association) ---------------------- */
 
-/* The interval kernels' work units: runs of <= 32 consecutive cells inside
- * one 32-cell row tile whose intervals hold <= budget in-range points (a
- * heavier single cell is its own unit), in x-major tile order; 2 uint32 per
- * unit (first flat cell, cell count).  *n_units (device int64) receives the
- * count; at most bvp_units_capacity() units are written. */
+/* Capacities of the schedule arrays and the builder's workspace. */
 int64_t bvp_units_capacity(int nx, int ny, int64_t n_int_max);
 size_t bvp_units_workspace_bytes(int nx, int ny);
-/* ... together with point_meta (2 x uint32 per sorted point: feature row
- * n*H*W + h*W + w and weight index (n*D + d)*H*W + h*W + w of ranks[j]), the
- * precomputed gather indices of the fast kernels.  Run after the cache build
- * (reads n_in from counts). */
+
+/* Cut the grid into work units (runs of <= 8 cells of one BEV row holding
+ * <= budget in-range points, x-major order), list the long units, and fill
+ * the point gather table (skipped when point_meta is NULL).  sched_counts:
+ * device int64[2] receiving n_units, n_long.  Run after the cache build. */
 int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
                       const uint32_t *cell_first, const int64_t *counts, int N,
                       int H, int W, int D, int nx, int ny, int budget,
-                      uint32_t *units, int64_t *n_units, uint32_t *point_meta,
+                      uint32_t *units, uint32_t *long_units,
+                      int64_t *sched_counts, uint32_t *point_meta,
                       void *workspace, size_t workspace_bytes, void *stream);
-/* point_meta alone (point_meta may be NULL above, e.g. when the frustum shape
- * of a loaded cache is only known at pooling time). */
+
+/* The point gather table alone (e.g. when a loaded cache's frustum shape is
+ * only known at pooling time). */
 int bvp_point_meta(const uint32_t *ranks, const int64_t *counts, int N, int H,
                    int W, int D, uint32_t *point_meta, void *stream);
 
 /* ---- cached forward ---------------------------------------------------- */
-/* The pooling entry points take the cache's units (units, device count
- * n_units, and max_units >= count, the launch size). */
 
 /* Workspace for bvp_pool_forward_f32: the NHWC copy of the features. */
 size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
@@ -139,29 +162,25 @@ size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
 int bvp_pool_forward_f32(const float *features, const float *dist,
                          const uint32_t *ranks, const uint32_t *interval_starts,
                          const uint32_t *interval_cells,
-                         const uint32_t *cell_first, const uint32_t *units,
-                         const uint32_t *point_meta,
-                         const int64_t *n_units, int64_t max_units,
-                         int B, int N, int C, int H,
-                         int W, int D, int nx, int ny, int64_t n_int_max,
-                         int mode, int exact, float *out, float *feats_nhwc,
-                         uint32_t *argmax, void *stream);
+                         const uint32_t *cell_first, const bvp_schedule *schedule,
+                         int B, int N, int C, int H, int W, int D, int nx,
+                         int ny, int64_t n_int_max, int mode, int exact,
+                         float *out, float *feats_nhwc, uint32_t *argmax,
+                         void *stream);
 
 /* (NB, C, H*W) -> (NB, H*W, C) f32 copy (the features' NHWC staging that
  * bvp_pool_forward_f32 performs first; pooling.py:215). */
 int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst,
                     void *stream);
 
-/* Same, with the features already NHWC (B,N,H,W,C): skips the transpose. */
+/* Same as bvp_pool_forward_f32 with the features already NHWC (B,N,H,W,C). */
 int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,
                               const uint32_t *ranks,
                               const uint32_t *interval_starts,
                               const uint32_t *interval_cells,
-                              const uint32_t *cell_first, const uint32_t *units,
-                         const uint32_t *point_meta,
-                              const int64_t *n_units, int64_t max_units,
-                              int B, int N, int C,
-                              int H, int W, int D, int nx, int ny,
+                              const uint32_t *cell_first,
+                              const bvp_schedule *schedule, int B, int N,
+                              int C, int H, int W, int D, int nx, int ny,
                               int64_t n_int_max, int mode, int exact,
                               float *out, uint32_t *argmax, void *stream);
 
@@ -183,14 +202,12 @@ int bvp_any_nonfinite(const float *x, int64_t n, int *flag, void *stream);
 int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H,
                  int W, int D, float *x, void *stream);
 
-/* Interval reduction over materialised rows x (P, C) -> out (C, n_cells). */
+/* Interval reduction over materialised rows x (P, C) -> out (C, nx*ny). */
 int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
                         const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
-                        const uint32_t *cell_first, const uint32_t *units,
-                         const uint32_t *point_meta,
-                        const int64_t *n_units, int64_t max_units,
-                        int C, int nx, int ny,
+                        const uint32_t *cell_first,
+                        const bvp_schedule *schedule, int C, int nx, int ny,
                         int mode, float *out, void *stream);
 
 /* ---- fused lift + pool, bf16 inputs (config F) ------------------------- */
@@ -198,24 +215,23 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
 /* Workspace: per-pixel log-sum-exp (f32) + NHWC bf16 context. */
 size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W);
 
-/* logits (B,N,D,H,W) bf16, context (B,N,C,H,W) bf16 -> out (B,C,n_cells)
+/* logits (B,N,D,H,W) bf16, context (B,N,C,H,W) bf16 -> out (B,C,nx*ny)
  * f32 = pool(softmax_D(logits) (x) context), fp32 accumulation. */
 int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context,
                         const uint32_t *ranks, const uint32_t *interval_starts,
                         const uint32_t *interval_cells,
-                        const uint32_t *cell_first, const uint32_t *units,
-                         const uint32_t *point_meta,
-                        const int64_t *n_units, int64_t max_units,
-                        int B, int N, int C, int H,
-                        int W, int D, int nx, int ny, int mode, float *out,
-                        void *workspace, size_t workspace_bytes, void *stream);
+                        const uint32_t *cell_first,
+                        const bvp_schedule *schedule, int B, int N, int C,
+                        int H, int W, int D, int nx, int ny, int mode,
+                        float *out, void *workspace, size_t workspace_bytes,
+                        void *stream);
 
 /* ---- gather backward (config B) ---------------------------------------- */
 
 /* Workspace: per-interval gradient rows (B, n_int_max, C) f32. */
 size_t bvp_backward_workspace_bytes(int B, int C, int64_t n_int_max);
 
-/* grad_out (B,C,n_cells) -> grad_features (B,N,C,H,W) and grad_dist
+/* grad_out (B,C,nx*ny) -> grad_features (B,N,C,H,W) and grad_dist
  * (B,N,D,H,W), both fully written.  feats_nhwc as left by the forward;
  * argmax required for BVP_MAX.  Either grad pointer may be NULL. */
 int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc,
@@ -243,8 +259,8 @@ int bvp_pool_lifted_backward_f32(const float *grad_out,
 /* ---- the paper's "before": LSS prefix-sum pooling --------- */
 
 /* pool_prefixsum (pooling.py:162-196): materialise the full running sum over
- * the rank-ordered points per channel, subtract at interval ends. SUM/MEAN.
- * workspace: n_in * C floats + scan scratch. */
+ * the rank-ordered points per channel (64-bit), subtract at interval ends.
+ * SUM / MEAN only.  workspace: bvp_prefixsum_workspace_bytes. */
 size_t bvp_prefixsum_workspace_bytes(int64_t n_in, int C);
 int bvp_pool_prefixsum_f32(const float *features, const float *dist,
                            const uint32_t *ranks,

@@ -18,7 +18,7 @@ BVP_OK, BVP_ERR_INVALID, BVP_ERR_UNSUPPORTED, BVP_ERR_CUDA = 0, 1, 2, 3
 BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
 TILE_CELLS = 32
 OUT_OF_RANGE = 0xFFFFFFFF
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class ExtensionMissingError(BevPoolError, RuntimeError):
@@ -35,6 +35,15 @@ _L = ctypes.c_int64
 _D = ctypes.c_double
 _S = ctypes.c_size_t
 
+
+class Schedule(ctypes.Structure):
+    """struct bvp_schedule (include/bevpool_b200.h)."""
+    _fields_ = [("units", _P), ("point_meta", _P), ("long_units", _P), ("counts", _P),
+                ("max_units", _L), ("max_long", _L)]
+
+
+_SP = ctypes.POINTER(Schedule)
+
 #: name -> (restype, argtypes); mirrors include/bevpool_b200.h one to one
 SIGNATURES = {
     "bvp_abi_version": (_I, []),
@@ -47,22 +56,22 @@ SIGNATURES = {
     "bvp_pool_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
     "bvp_units_capacity": (_L, [_I, _I, _L]),
     "bvp_units_workspace_bytes": (_S, [_I, _I]),
-    "bvp_make_schedule": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _S,
-                               _P]),
+    "bvp_make_schedule": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
+                               _S, _P]),
     "bvp_point_meta": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
-    "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I,
-                                  _I, _I, _I, _L, _I, _I, _P, _P, _P, _P]),
-    "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I,
-                                       _I, _I, _I, _I, _L, _I, _I, _P, _P, _P]),
+    "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
+                                  _L, _I, _I, _P, _P, _P, _P]),
+    "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I,
+                                       _I, _L, _I, _I, _P, _P, _P]),
     "bvp_to_nhwc_f32": (_I, [_P, _I, _I, _I, _P, _P]),
     "bvp_reorder_weights": (_I, [_P, _P, _L, _I, _I, _I, _I, _P, _P]),
     "bvp_normalize_depth": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "bvp_any_nonfinite": (_I, [_P, _L, _P, _P]),
     "bvp_lift_f32": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P]),
-    "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P]),
+    "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _P, _P]),
     "bvp_fused_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
-    "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _I, _I, _I, _I, _I,
-                                 _I, _I, _I, _I, _P, _P, _S, _P]),
+    "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
+                                 _I, _P, _P, _S, _P]),
     "bvp_backward_workspace_bytes": (_S, [_I, _I, _L]),
     "bvp_pool_backward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                    _I, _L, _I, _P, _P, _P, _S, _P]),

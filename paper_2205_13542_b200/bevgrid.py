@@ -118,7 +118,7 @@ def _u32(t: torch.Tensor) -> np.ndarray:
 
 
 #: points per work unit of the interval kernels (csrc/units.cu)
-UNIT_BUDGET = 256
+UNIT_BUDGET = 128
 
 
 @dataclass(eq=False)
@@ -138,10 +138,12 @@ class AssociationCache:
     d_cell_first: torch.Tensor             # (n_cells + 1,)
     d_interval_of_point: torch.Tensor      # (P,)
     d_counts: torch.Tensor                 # (2,) int64: n_in, n_int
-    d_units: torch.Tensor                  # (2 * max_units,) (first cell, count)
-    d_n_units: torch.Tensor                # (1,) int64
+    d_units: torch.Tensor                  # (2 * max_units,) (first cell, count | long)
+    d_long_units: torch.Tensor             # (max_long,) unit ids of split cells
+    d_sched_counts: torch.Tensor           # (2,) int64: n_units, n_long
     d_meta: torch.Tensor                   # (2 * P,) per sorted point: row, weight index
-    max_units: int                         # launch bound (>= device count)
+    max_units: int                         # launch bounds (>= the device counts)
+    max_long: int
     fingerprint: int
     nx: int
     ny: int
@@ -186,17 +188,32 @@ class AssociationCache:
 
     @property
     def n_units(self) -> int:
-        return int(self.d_n_units.item())
+        return int(self.d_sched_counts[0].item())
 
-    def unit_args(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1):
-        """(units, point_meta, n_units, max_units) as the C ABI takes them;
-        the point gather table is (re)derived for an (N, H, W, D) frustum
-        (N=None: caller does not read it, e.g. the materialised path)."""
+    @property
+    def n_long(self) -> int:
+        return int(self.d_sched_counts[1].item())
+
+    def fit_launch(self) -> None:
+        """Shrink the launch bounds to the exact unit counts (one host sync)."""
+        c = self.d_sched_counts.cpu().tolist()
+        self.max_units, self.max_long = max(1, int(c[0])), int(c[1])
+        self._host.pop("schedule", None)
+
+    def schedule(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1):
+        """The bvp_schedule the C ABI takes; the point gather table is
+        (re)derived for an (N, H, W, D) frustum (N=None: the caller does not
+        read it, e.g. the materialised path)."""
         if N is not None and self.meta_dims != (N, H, W, D):
             _lib.call("bvp_point_meta", ptr(self.d_ranks), ptr(self.d_counts), N, H, W, D,
                       ptr(self.d_meta), stream_ptr(self.device))
             self.meta_dims = (N, H, W, D)
-        return ptr(self.d_units), ptr(self.d_meta), ptr(self.d_n_units), self.max_units
+        s = self._host.get("schedule")
+        if s is None:
+            s = _lib.Schedule(ptr(self.d_units), ptr(self.d_meta), ptr(self.d_long_units),
+                              ptr(self.d_sched_counts), self.max_units, self.max_long)
+            self._host["schedule"] = s
+        return s
 
     # ---- reference-typed host views ------------------------------------
     def _view(self, name, tensor, n):
@@ -251,7 +268,8 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
         starts=torch.empty(n_cells + 1, **i32), icells=torch.empty(n_cells, **i32),
         cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
         counts=torch.zeros(2, dtype=torch.int64, device=dev),
-        units=torch.empty(2 * cap, **i32), n_units=torch.zeros(1, dtype=torch.int64, device=dev),
+        units=torch.empty(2 * cap, **i32), long_units=torch.empty(n_cells, **i32),
+        sched_counts=torch.zeros(2, dtype=torch.int64, device=dev),
         meta=torch.empty(2 * P, **i32),
         cap=cap, ws=torch.empty(ws, dtype=torch.uint8, device=dev),
     )
@@ -261,15 +279,19 @@ def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None) -> No
     """Work units, plus the point gather table when the frustum dims are known."""
     N, H, W, D = dims if dims is not None else (1, 1, 1, 1)
     _lib.call("bvp_make_schedule", ptr(b["ranks"]), ptr(b["starts"]), ptr(b["cell_first"]),
-              ptr(b["counts"]), N, H, W, D, nx, ny, budget, ptr(b["units"]), ptr(b["n_units"]),
+              ptr(b["counts"]), N, H, W, D, nx, ny, budget, ptr(b["units"]),
+              ptr(b["long_units"]), ptr(b["sched_counts"]),
               ptr(b["meta"]) if dims is not None else None, ptr(b["ws"]), b["ws"].numel(),
               stream_ptr(dev))
 
 
 def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, dims=None):
+    """A cache over the buffers b; launch bounds are the capacities until
+    fit_launch() (no host sync needed to pool)."""
     return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
-                            b["iop"], b["counts"], b["units"], b["n_units"], b["meta"],
-                            b["cap"], fingerprint, nx, ny, n_cameras, frustum, grid, dims)
+                            b["iop"], b["counts"], b["units"], b["long_units"],
+                            b["sched_counts"], b["meta"], b["cap"], int(b["long_units"].numel()),
+                            fingerprint, nx, ny, n_cameras, frustum, grid, dims)
 
 
 class CacheBuilder:
@@ -316,7 +338,7 @@ def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
     cams_d = torch.from_numpy(cams).to(builder.dev)
     cache = builder.build(cams_d, fingerprint_inputs(rig, frustum_spec, grid_spec))
     cache._counts()  # one sync: sizes known on the host from here on
-    cache.max_units = max(1, cache.n_units)
+    cache.fit_launch()
     return cache
 
 
@@ -346,7 +368,7 @@ def cache_from_cells(cell_of_point, nx: int, ny: int, fingerprint: int = 0, n_ca
     _make_schedule(b, nx, ny, unit_budget, dev, dims)
     cache = _cache_of(b, fingerprint, nx, ny, n_cameras, frustum, grid, dims)
     cache._counts()
-    cache.max_units = max(1, cache.n_units)
+    cache.fit_launch()
     return cache
 
 

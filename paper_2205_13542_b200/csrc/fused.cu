@@ -64,10 +64,9 @@ size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W) {
 
 int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const uint32_t *ranks,
                         const uint32_t *interval_starts, const uint32_t *interval_cells,
-                        const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
-                        const int64_t *n_units, int64_t max_units, int B, int N, int C, int H,
-                        int W, int D, int nx, int ny, int mode, float *out, void *workspace,
-                        size_t workspace_bytes, void *stream) {
+                        const uint32_t *cell_first, const bvp_schedule *schedule, int B, int N,
+                        int C, int H, int W, int D, int nx, int ny, int mode, float *out,
+                        void *workspace, size_t workspace_bytes, void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims");
     BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
@@ -75,7 +74,8 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
                 "fused workspace too small: need %zu bytes", L.bytes);
     BVP_REQUIRE(logits && (C == 0 || (out && context && ranks && interval_starts &&
-                                      interval_cells && cell_first && units && n_units)),
+                                      interval_cells && cell_first && schedule &&
+                                      schedule->units && schedule->counts)),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     cudaStream_t s = as_stream(stream);
@@ -88,8 +88,8 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     pixel_lse_kernel<<<lb, 128, 0, s>>>(lg, NB, D, int(HW), lse);
     launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
                                   int(HW), ctx, s);
-    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units, point_meta,
-                                    n_units, max_units, C, nx, ny, out, mode);
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
+                                    C, nx, ny, out, mode);
     p.rows = ctx;
     p.wsrc = lg;
     p.lse = lse;

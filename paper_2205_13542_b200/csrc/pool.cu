@@ -43,18 +43,19 @@ template void launch_to_nhwc<__nv_bfloat16>(const __nv_bfloat16 *, int64_t, int,
                                             __nv_bfloat16 *, cudaStream_t);
 
 PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const uint32_t *icells,
-                            const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
-                            const int64_t *n_units, int64_t max_units, int C, int nx, int ny,
-                            float *out, int mode) {
+                            const uint32_t *cell_first, const bvp_schedule *sched, int C, int nx,
+                            int ny, float *out, int mode) {
     PoolParams p{};
     p.ranks = ranks;
     p.starts = starts;
     p.icells = icells;
     p.cell_first = cell_first;
-    p.units = units;
-    p.meta = reinterpret_cast<const uint2 *>(point_meta);
-    p.n_units = n_units;
-    p.max_units = max_units;
+    p.units = sched->units;
+    p.meta = reinterpret_cast<const uint2 *>(sched->point_meta);
+    p.long_units = sched->long_units;
+    p.sched_counts = sched->counts;
+    p.max_units = sched->max_units;
+    p.max_long = sched->max_long;
     p.out = out;
     p.C = C;
     p.nx = nx;
@@ -165,20 +166,21 @@ int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst, void *s
 
 int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const uint32_t *ranks,
                               const uint32_t *interval_starts, const uint32_t *interval_cells,
-                              const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
-                              const int64_t *n_units, int64_t max_units, int B, int N, int C,
-                              int H, int W, int D, int nx, int ny, int64_t n_int_max, int mode,
-                              int exact, float *out, uint32_t *argmax, void *stream) {
+                              const uint32_t *cell_first, const bvp_schedule *schedule, int B,
+                              int N, int C, int H, int W, int D, int nx, int ny,
+                              int64_t n_int_max, int mode, int exact, float *out,
+                              uint32_t *argmax, void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims B=%d N=%d C=%d H=%d W=%d D=%d nx=%d ny=%d", B, N, C,
                 H, W, D, nx, ny);
     BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
     BVP_REQUIRE(C == 0 || (out && feats_nhwc && dist && ranks && interval_starts &&
-                           interval_cells && cell_first && units && n_units),
+                           interval_cells && cell_first && schedule && schedule->units &&
+                           schedule->counts),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
-    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units, point_meta,
-                                    n_units, max_units, C, nx, ny, out, mode);
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
+                                    C, nx, ny, out, mode);
     p.rows = feats_nhwc;
     p.wsrc = dist;
     p.argmax = mode == BVP_MAX ? argmax : nullptr;
@@ -203,16 +205,16 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
 
 int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_t *ranks,
                          const uint32_t *interval_starts, const uint32_t *interval_cells,
-                         const uint32_t *cell_first, const uint32_t *units, const uint32_t *point_meta,
-                         const int64_t *n_units, int64_t max_units, int B, int N, int C, int H,
-                         int W, int D, int nx, int ny, int64_t n_int_max, int mode, int exact,
-                         float *out, float *feats_nhwc, uint32_t *argmax, void *stream) {
+                         const uint32_t *cell_first, const bvp_schedule *schedule, int B, int N,
+                         int C, int H, int W, int D, int nx, int ny, int64_t n_int_max, int mode,
+                         int exact, float *out, float *feats_nhwc, uint32_t *argmax,
+                         void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1, BVP_ERR_INVALID, "bad dims");
     BVP_REQUIRE(C == 0 || (features && feats_nhwc), BVP_ERR_INVALID, "null pointer argument");
     launch_to_nhwc<float>(features, int64_t(B) * N, C, H * W, feats_nhwc, as_stream(stream));
     return bvp_pool_forward_nhwc_f32(feats_nhwc, dist, ranks, interval_starts, interval_cells,
-                                     cell_first, units, point_meta, n_units, max_units, B, N, C, H, W, D, nx,
-                                     ny, n_int_max, mode, exact, out, argmax, stream);
+                                     cell_first, schedule, B, N, C, H, W, D, nx, ny, n_int_max,
+                                     mode, exact, out, argmax, stream);
 }
 
 int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in, int N, int D,
@@ -270,16 +272,16 @@ int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H, 
 
 int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *interval_starts,
                         const uint32_t *interval_cells, const uint32_t *cell_first,
-                        const uint32_t *units, const uint32_t *point_meta, const int64_t *n_units, int64_t max_units, int C,
-                        int nx, int ny, int mode, float *out, void *stream) {
+                        const bvp_schedule *schedule, int C, int nx, int ny, int mode,
+                        float *out, void *stream) {
     BVP_REQUIRE(C >= 0 && nx >= 1 && ny >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
                 "bad arguments");
     BVP_REQUIRE(C == 0 || (out && x && ranks && interval_starts && interval_cells && cell_first &&
-                           units && n_units),
+                           schedule && schedule->units && schedule->counts),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
-    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, units, point_meta,
-                                    n_units, max_units, C, nx, ny, out, mode);
+    PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
+                                    C, nx, ny, out, mode);
     p.rows = x;
     p.D = 1;
     p.HW = 1;

@@ -49,16 +49,17 @@ struct PoolParams {
     const uint32_t *starts;  // n_int + 1 entries (sentinel = n_in)
     const uint32_t *icells;
     const uint32_t *cell_first;  // n_cells + 1: first interval with cell >= c
-    const uint32_t *units;   // work units: (first cell, cell count) pairs
-    const int64_t *n_units;  // device count of units
-    const uint2 *meta;       // per sorted point: (feature row, weight index)
+    const uint32_t *units;       // work units: (first cell, cell count | long flag)
+    const uint2 *meta;           // per sorted point: (feature row, weight index)
+    const uint32_t *long_units;  // indices of the long (split) units
+    const int64_t *sched_counts; // device: n_units, n_long
     float *out;              // (B, C, n_cells)
     uint32_t *argmax;        // MAX only, optional: (B, n_int_max, C)
     int C, D, HW, NHW;
     int mean;
     int nx, ny;
     int64_t n_cells, n_int_max;
-    int64_t max_units;       // grid size (>= *n_units)
+    int64_t max_units, max_long;  // launch sizes (>= the device counts)
     int64_t rows_bstride;    // elements of rows per batch sample
     int64_t w_bstride;       // elements of wsrc per batch sample
 };
@@ -116,13 +117,100 @@ __device__ __forceinline__ float point_weight(const PoolParams &P, int b, uint2 
     return __expf(l - __ldg(P.lse + int64_t(b) * P.NHW + m.x));
 }
 
-// CH = 16-byte (VEC-element) chunks of the channel row per lane.
-template <typename Acc, typename Elem, int VEC, int CH, bool IS_MAX, int SRC>
+// Walk the sorted points [a, e) in rank order, calling f(jj, w, v) for each
+// with the point's weight and this lane's CH x VEC slice of its row.  Gather
+// records are read 32 at a time, one per lane, two blocks ahead; the block's
+// weights one block ahead; rows one step (U points) ahead into a register
+// double buffer -- so a step costs issue time, not a memory latency.
+template <typename Elem, int VEC, int CH, int SRC, typename F>
+__device__ __forceinline__ void warp_walk(const PoolParams &P, int b, const Elem *rows, uint32_t a,
+                                          uint32_t e, F &&f) {
+    constexpr int U = CH == 1 ? 4 : (CH == 2 ? 2 : 1);
+    constexpr int STEPS = 32 / U;
+    const int lane = threadIdx.x & 31;
+    const int C = P.C;
+    const int nchunks = C / VEC;
+    auto rec_of = [&](uint32_t j) {
+        return j < e ? point_record<SRC>(P, j) : make_uint2(0u, 0u);
+    };
+    uint32_t jb = a;
+    uint2 r0 = rec_of(jb + lane);
+    uint2 r1 = rec_of(jb + 32 + lane);
+    float w0 = (jb + lane < e) ? point_weight<SRC>(P, b, r0) : 0.f;
+    float v[2][U][CH][VEC];
+    // rows of step s of the block whose records are `r` (block start jbb)
+    auto issue = [&](int buf, int s, uint2 r, uint32_t jbb) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t rx = __shfl_sync(0xFFFFFFFFu, r.x, s * U + u);
+            const bool ok = jbb + s * U + u < e;
+            const Elem *rp = rows + size_t(rx) * C;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                const int ch = lane + 32 * q;
+                if (ok && ch < nchunks) {
+                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v[buf][u][q]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < VEC; ++k) v[buf][u][q][k] = 0.f;
+                }
+            }
+        }
+    };
+    issue(0, 0, r0, jb);
+#pragma unroll 1
+    for (; jb < e; jb += 32) {
+        const uint2 r2 = rec_of(jb + 64 + lane);
+        const float w1 = (jb + 32 + lane < e) ? point_weight<SRC>(P, b, r1) : 0.f;
+#pragma unroll
+        for (int s = 0; s < STEPS; ++s) {
+            if (jb + s * U >= e) break;  // warp-uniform
+            if (s + 1 < STEPS) {
+                if (jb + (s + 1) * U < e) issue((s + 1) & 1, s + 1, r0, jb);
+            } else if (jb + 32 < e) {
+                issue(0, 0, r1, jb + 32);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t jj = jb + s * U + u;
+                const float w = __shfl_sync(0xFFFFFFFFu, w0, s * U + u);
+                if (jj < e) f(jj, w, v[s & 1][u]);
+            }
+        }
+        r0 = r1;
+        r1 = r2;
+        w0 = w1;
+    }
+}
+
+template <typename Acc, int CH, int VEC, bool IS_MAX>
+__device__ __forceinline__ void acc_point(Acc (&acc)[CH][VEC],
+                                          uint32_t (&arg)[IS_MAX ? CH : 1][IS_MAX ? VEC : 1],
+                                          uint32_t jj, float w, const float (&v)[CH][VEC]) {
+#pragma unroll
+    for (int q = 0; q < CH; ++q)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            if (IS_MAX) {
+                const Acc pv = Acc(w) * Acc(v[q][k]);
+                if (pv > acc[q][k]) {
+                    acc[q][k] = pv;
+                    arg[IS_MAX ? q : 0][IS_MAX ? k : 0] = jj;  // sorted position
+                }
+            } else {
+                acc[q][k] += Acc(w) * Acc(v[q][k]);
+            }
+        }
+}
+
+constexpr uint32_t kLongUnit = 0x80000000u;  // unit flag: split by pool_long_kernel
+
+// One warp per work unit.  SPLIT: units flagged long are left to
+// pool_long_kernel (fast mode); the exact mode walks them here, in order.
+template <typename Acc, typename Elem, int VEC, int CH, bool IS_MAX, int SRC, bool SPLIT>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_stream_kernel(const PoolParams P) {
     extern __shared__ float s_all[];  // per warp: [C][kUnitPitch]
-    // rows per pipeline step (x2 buffers in registers)
-    constexpr int U = CH == 1 ? 4 : (CH == 2 ? 2 : 1);
     constexpr uint32_t kNone = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int C = P.C;
@@ -131,9 +219,11 @@ pool_stream_kernel(const PoolParams P) {
     float *s_tile = s_all + warp * C * kUnitPitch;
 
     const int64_t k = int64_t(blockIdx.x) * kPoolWarps + warp;
-    if (k >= *P.n_units) return;
+    if (k >= P.sched_counts[0]) return;
     const int64_t cell0 = __ldg(P.units + 2 * k);
-    const int ncell = static_cast<int>(__ldg(P.units + 2 * k + 1));
+    const uint32_t word = __ldg(P.units + 2 * k + 1);
+    if (SPLIT && (word & kLongUnit)) return;
+    const int ncell = static_cast<int>(word & 0xFFu);
     const uint32_t i0 = __ldg(P.cell_first + cell0), i1 = __ldg(P.cell_first + cell0 + ncell);
     const uint32_t J0 = __ldg(P.starts + i0), J1 = __ldg(P.starts + i1);
     // which of the unit's cells own an interval (bit x <-> cell0 + x)
@@ -174,87 +264,18 @@ pool_stream_kernel(const PoolParams P) {
         }
     };
     reset();
-
-    // software pipeline: rows of step t+1 are in flight while step t is summed
-    float v[2][U][CH][VEC];
-    float w[2][U];
-    uint2 mrec[U];
-    auto issue = [&](int buf, uint32_t j) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const bool ok = j + u < J1;
-            w[buf][u] = ok ? point_weight<SRC>(P, b, mrec[u]) : 0.f;
-            const Elem *rp = rows + size_t(mrec[u].x) * C;
-#pragma unroll
-            for (int q = 0; q < CH; ++q) {
-                const int ch = lane + 32 * q;
-                if (ok && ch < nchunks) {
-                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v[buf][u][q]);
-                } else {
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) v[buf][u][q][e] = 0.f;
-                }
-            }
-        }
-    };
-    auto fetch_rec = [&](uint32_t j) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            mrec[u] = (j + u < J1) ? point_record<SRC>(P, j + u) : make_uint2(0u, 0u);
-    };
-
-    // accumulate step j out of buffer CUR (compile-time, so v stays in registers)
-    auto consume = [&](auto cur_c, uint32_t j) {
-        constexpr int cur = decltype(cur_c)::value;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t jj = j + u;
-            if (jj < J1) {
-                if (jj == hi) {  // interval boundary (warp-uniform)
-                    park();
-                    reset();
-                    ++iv;
-                    lo = hi;
-                    hi = __ldg(P.starts + iv + 1);
-                }
-#pragma unroll
-                for (int q = 0; q < CH; ++q)
-#pragma unroll
-                    for (int e = 0; e < VEC; ++e) {
-                        if (IS_MAX) {
-                            const Acc pv = Acc(w[cur][u]) * Acc(v[cur][u][q][e]);
-                            if (pv > acc[q][e]) {
-                                acc[q][e] = pv;
-                                arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = jj;
-                            }
-                        } else {
-                            acc[q][e] += Acc(w[cur][u]) * Acc(v[cur][u][q][e]);
-                        }
-                    }
-            }
-        }
-    };
-    using B0 = std::integral_constant<int, 0>;
-    using B1 = std::integral_constant<int, 1>;
-
     if (J1 > J0) {
-        fetch_rec(J0);
-        issue(0, J0);
-        fetch_rec(J0 + U);
-#pragma unroll 1
-        for (uint32_t j = J0; j < J1; j += 2 * U) {
-            if (j + U < J1) {  // warp-uniform
-                issue(1, j + U);
-                fetch_rec(j + 2 * U);
+        warp_walk<Elem, VEC, CH, SRC>(P, b, rows, J0, J1,
+                                      [&](uint32_t jj, float w, const float (&v)[CH][VEC]) {
+            if (jj == hi) {  // interval boundary (warp-uniform)
+                park();
+                reset();
+                ++iv;
+                lo = hi;
+                hi = __ldg(P.starts + iv + 1);
             }
-            consume(B0{}, j);
-            if (j + U >= J1) break;
-            if (j + 2 * U < J1) {
-                issue(0, j + 2 * U);
-                fetch_rec(j + 3 * U);
-            }
-            consume(B1{}, j + U);
-        }
+            acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, jj, w, v);
+        });
         park();
     }
     __syncwarp();
@@ -262,6 +283,78 @@ pool_stream_kernel(const PoolParams P) {
     for (int idx = lane; idx < C * ncell; idx += 32) {
         const int c = idx / ncell, x = idx - c * ncell;
         out[int64_t(c) * P.n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
+    }
+}
+
+// Fast mode: one CTA per heavy cell (a single interval above the unit point
+// budget).  Its 8 warps walk equal slices of the interval; the slices'
+// partial results are combined in slice order in shared memory, so the sum
+// is deterministic and the heavy cell no longer sets the kernel's critical
+// path.
+template <typename Elem, int VEC, int CH, bool IS_MAX, int SRC>
+__global__ void __launch_bounds__(kPoolThreads)
+pool_long_kernel(const PoolParams P) {
+    extern __shared__ float s_all[];  // [kPoolWarps][C] values + [kPoolWarps][C] argmax
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int C = P.C;
+    const int nchunks = C / VEC;
+    const int b = blockIdx.y;
+    if (int64_t(blockIdx.x) >= P.sched_counts[1]) return;
+    const uint32_t k = __ldg(P.long_units + blockIdx.x);
+    const int64_t cell = __ldg(P.units + 2 * size_t(k));
+    const uint32_t iv = __ldg(P.cell_first + cell);
+    const uint32_t lo = __ldg(P.starts + iv), hi = __ldg(P.starts + iv + 1);
+    const uint32_t L = hi - lo;
+    const uint32_t a = lo + uint32_t(uint64_t(L) * warp / kPoolWarps);
+    const uint32_t e = lo + uint32_t(uint64_t(L) * (warp + 1) / kPoolWarps);
+    const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
+    float acc[CH][VEC];
+    uint32_t arg[IS_MAX ? CH : 1][IS_MAX ? VEC : 1];
+#pragma unroll
+    for (int q = 0; q < CH; ++q)
+#pragma unroll
+        for (int x = 0; x < VEC; ++x) {
+            acc[q][x] = IS_MAX ? -INFINITY : 0.f;
+            if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? x : 0] = kNone;
+        }
+    if (e > a)
+        warp_walk<Elem, VEC, CH, SRC>(P, b, rows, a, e,
+                                      [&](uint32_t jj, float w, const float (&v)[CH][VEC]) {
+            acc_point<float, CH, VEC, IS_MAX>(acc, arg, jj, w, v);
+        });
+    float *s_val = s_all;
+    uint32_t *s_arg = reinterpret_cast<uint32_t *>(s_all + kPoolWarps * C);
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+        const int ch = lane + 32 * q;
+        if (ch < nchunks)
+#pragma unroll
+            for (int x = 0; x < VEC; ++x) {
+                s_val[warp * C + ch * VEC + x] = acc[q][x];
+                if (IS_MAX) s_arg[warp * C + ch * VEC + x] = arg[IS_MAX ? q : 0][IS_MAX ? x : 0];
+            }
+    }
+    __syncthreads();
+    float *out = P.out + int64_t(b) * C * P.n_cells + cell;
+    const float inv = P.mean ? 1.f / float(L) : 1.f;
+    for (int c = threadIdx.x; c < C; c += kPoolThreads) {
+        float run = s_val[c];
+        uint32_t ra = IS_MAX ? s_arg[c] : 0u;
+        for (int wv = 1; wv < kPoolWarps; ++wv) {
+            const float x = s_val[wv * C + c];
+            if (IS_MAX) {
+                const uint32_t xa = s_arg[wv * C + c];
+                if (x > run || (x == run && xa < ra)) {
+                    run = x;
+                    ra = xa;
+                }
+            } else {
+                run += x;
+            }
+        }
+        out[int64_t(c) * P.n_cells] = run * inv;
+        if (IS_MAX && P.argmax) P.argmax[(b * P.n_int_max + iv) * C + c] = __ldg(P.ranks + ra);
     }
 }
 
@@ -274,9 +367,8 @@ inline int choose_ch(int nchunks) {
 
 // pool.cu
 PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const uint32_t *icells,
-                            const uint32_t *cell_first, const uint32_t *units,
-                            const uint32_t *point_meta, const int64_t *n_units, int64_t max_units,
-                            int C, int nx, int ny, float *out, int mode);
+                            const uint32_t *cell_first, const bvp_schedule *sched, int C, int nx,
+                            int ny, float *out, int mode);
 template <typename T>
 void launch_to_nhwc(const T *src, int64_t NB, int A, int HW, T *dst, cudaStream_t s);
 
@@ -307,15 +399,28 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
     BVP_REQUIRE(SRC == kSrcX || p.meta, BVP_ERR_INVALID,
                 "the cache's point gather table (point_meta) is required");
+    // fast mode: heavy cells are split over a CTA by pool_long_kernel; the
+    // exact mode must walk every interval in order and does not split
+    constexpr bool kSplit = sizeof(Acc) == sizeof(float);
     const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps)),
                     static_cast<unsigned>(B));
+    const size_t lsmem = size_t(kPoolWarps) * p.C * 2 * sizeof(float);
 #define BVP_LAUNCH_CH(CHV)                                                                   \
     if (ch == CHV) {                                                                         \
-        auto k = is_max ? pool_stream_kernel<Acc, Elem, VEC, CHV, true, SRC>                 \
-                        : pool_stream_kernel<Acc, Elem, VEC, CHV, false, SRC>;               \
+        auto k = is_max ? pool_stream_kernel<Acc, Elem, VEC, CHV, true, SRC, kSplit>         \
+                        : pool_stream_kernel<Acc, Elem, VEC, CHV, false, SRC, kSplit>;       \
         if (smem > 48 * 1024)                                                                \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         k<<<grid, kPoolThreads, smem, s>>>(p);                                               \
+        if (kSplit && p.max_long > 0) {                                                      \
+            auto kl = is_max ? pool_long_kernel<Elem, VEC, CHV, true, SRC>                   \
+                             : pool_long_kernel<Elem, VEC, CHV, false, SRC>;                 \
+            if (lsmem > 48 * 1024)                                                           \
+                cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                     int(lsmem));                                            \
+            kl<<<dim3(static_cast<unsigned>(p.max_long), static_cast<unsigned>(B)),          \
+                 kPoolThreads, lsmem, s>>>(p);                                               \
+        }                                                                                    \
         return BVP_OK;                                                                       \
     }
     BVP_LAUNCH_CH(1) BVP_LAUNCH_CH(2) BVP_LAUNCH_CH(4) BVP_LAUNCH_CH(8)

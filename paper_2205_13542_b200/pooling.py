@@ -183,7 +183,7 @@ def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
         nhwc = torch.empty(inp.feats.numel(), dtype=torch.float32, device=inp.feats.device)
         _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                  ptr(cache.d_cell_first), *cache.unit_args(inp.N, inp.H, inp.W, inp.D), inp.B, inp.N, inp.C, inp.H,
+                  ptr(cache.d_cell_first), cache.schedule(inp.N, inp.H, inp.W, inp.D), inp.B, inp.N, inp.C, inp.H,
                   inp.W, inp.D,
                   grid.nx, grid.ny, cache.n_int_max, _MODE[reducer],
                   int(DEFAULT_EXACT if exact is None else exact), ptr(out), ptr(nhwc), None,
@@ -259,7 +259,7 @@ class PoolPlan:
         c = self.cache
         _lib.call("bvp_pool_forward_nhwc_f32", ptr(self.nhwc), ptr(dist), ptr(c.d_ranks),
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
-                  *c.unit_args(self.N, self.H, self.W, self.D), self.B,
+                  c.schedule(self.N, self.H, self.W, self.D), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
                   self.mode, self.exact, ptr(out), None, stream_ptr(self.dev))
         return out
@@ -368,7 +368,7 @@ def pool_lifted(x: torch.Tensor, cache: AssociationCache, grid: BevGridSpec,
     x = x.contiguous()
     out = torch.empty((C, grid.n_cells), dtype=torch.float32, device=x.device)
     _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
-              ptr(cache.d_interval_cells), ptr(cache.d_cell_first), *cache.unit_args(), C,
+              ptr(cache.d_interval_cells), ptr(cache.d_cell_first), cache.schedule(), C,
               grid.nx, grid.ny,
               _MODE[reducer], ptr(out), stream_ptr(x.device))
     return BevFeatureMap(out.view(C, grid.nx, grid.ny), grid)
@@ -397,7 +397,7 @@ def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCa
                      device=dev)
     _lib.call("bvp_fused_pool_bf16", ptr(lg), ptr(cx), ptr(cache.d_ranks),
               ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_cell_first),
-              *cache.unit_args(N, H, W, D),
+              cache.schedule(N, H, W, D),
               B, N, C, H, W, D, grid.nx, grid.ny, _MODE[reducer], ptr(out), ptr(ws), ws.numel(),
               stream_ptr(dev))
     v = out.view(B, C, grid.nx, grid.ny)

@@ -45,7 +45,8 @@ def test_abi_version_and_errors_without_gpu():
     assert lib.bvp_abi_version() == _lib.ABI_VERSION
     # every pointer NULL, every size 0 (B = 0 is rejected before any CUDA call)
     argtypes = _lib.SIGNATURES["bvp_pool_forward_f32"][1]
-    rc = lib.bvp_pool_forward_f32(*[None if t is ctypes.c_void_p else 0 for t in argtypes])
+    is_ptr = lambda t: t is ctypes.c_void_p or issubclass(t, ctypes._Pointer)  # noqa: E731
+    rc = lib.bvp_pool_forward_f32(*[None if is_ptr(t) else 0 for t in argtypes])
     assert rc == _lib.BVP_ERR_INVALID
     assert b"bad dims" in lib.bvp_last_error()
     with pytest.raises(bp.ValidationError):
