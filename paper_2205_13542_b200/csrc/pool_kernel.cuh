@@ -1,29 +1,32 @@
-// pool_kernel.cuh -- the interval-reduction kernel (forward), sm_100a.
+// pool_kernel.cuh -- the interval-reduction kernels (forward), sm_100a.
 //
 // Restates the reference's interval_reduce (_kernels.py:22-63).
 //
-// Work decomposition (the choice is measured):
+// Work decomposition (measured; DESIGN.md §4 records the alternatives):
 //   * The cached schedule cuts the BEV grid into work UNITS: runs of at most
 //     kUnitCells consecutive cells of one row holding at most a budget of
-//     in-range points (a heavier single cell is a unit of its own).  A unit's
-//     intervals occupy one contiguous range [J0, J1) of the rank-ordered
-//     point stream.
+//     in-range points.  A unit's intervals occupy one contiguous range
+//     [J0, J1) of the rank-ordered point stream.
 //   * One WARP owns one unit and walks its point stream in rank order.  The
-//     lanes span the channel row (16-byte chunks), so every point's row is
-//     one coalesced warp load and interval boundaries are warp-uniform: the
-//     accumulation is sequential in rank order per interval, exactly like the
-//     reference.  With Acc = double the sums are therefore bit-identical to
+//     lanes span the channel row (16-byte chunks), so a point's row is one
+//     coalesced warp load and interval boundaries are warp-uniform: every
+//     interval is accumulated sequentially in rank order, exactly like the
+//     reference.  With Acc = double the sums are bit-identical to
 //     interval_reduce (fp32 x fp32 products are exact in fp64); Acc = float is
 //     the fast mode.
-//   * Per point the warp reads a precomputed gather record (feature row,
-//     weight index) -- no division in the loop -- and the next U rows are in
-//     flight while the current U are accumulated (register double buffer).
-//     The kernel is a gather from L2: it needs occupancy, so its footprint is
-//     kept small (no per-lane shuffles, one small shared tile per warp).
-//   * A finished interval is parked in the warp's shared [C][kUnitCells] tile;
-//     the warp then writes its cells' output columns once -- zeros of empty
-//     cells included -- so there is no memset and exactly one non-atomic store
-//     per (channel, cell).
+//   * Gather records (feature row, weight index; precomputed per sorted point
+//     so the loop never divides) are read 32 at a time, one per lane, two
+//     blocks ahead; weights one block ahead; rows one 4-point step ahead into
+//     a register double buffer.  Boundaries are tested once per step: steps
+//     inside one interval take a branch-free path.
+//   * A finished interval is parked in the warp's shared [C][kUnitCells]
+//     tile; the warp then writes its cells' output columns once -- zeros of
+//     empty cells included -- so there is no memset and exactly one
+//     non-atomic store per (channel, cell).
+//   * Fast mode only: a cell holding more points than the unit budget is a
+//     "long" unit; pool_long_kernel splits it over the 8 warps of a CTA and
+//     combines the slices in order in shared memory, so a heavy cell does not
+//     set the kernel's critical path.
 //
 // Sources (SRC):
 //   kSrcDist  : rows = NHWC features (f32), weight = dist[n,d,h,w] (f32)
@@ -38,6 +41,7 @@ namespace bvp {
 constexpr int kPoolWarps = 8;
 constexpr int kPoolThreads = 32 * kPoolWarps;
 constexpr int kUnitPitch = kUnitCells + 1;
+constexpr uint32_t kLongUnit = 0x80000000u;  // unit flag: split by pool_long_kernel
 
 enum { kSrcDist = 0, kSrcX = 1, kSrcFused = 2 };
 
@@ -101,87 +105,65 @@ struct Loader<__nv_bfloat16, 1> {
     }
 };
 
-// Gather record of sorted point j: (feature row, weight index).
-template <int SRC>
-__device__ __forceinline__ uint2 point_record(const PoolParams &P, uint32_t j) {
-    if (SRC == kSrcX) return make_uint2(__ldg(P.ranks + j), 0u);
-    return __ldg(P.meta + j);
-}
+// Per-warp gather context: every pointer batch-offset once, 32-bit element
+// offsets in the loop (callers guarantee rows * C < 2^32).
+template <typename Elem, int VEC, int CH, int SRC>
+struct Gather {
+    static constexpr int U = CH == 1 ? 4 : (CH == 2 ? 2 : 1);  // rows per step
+    static constexpr int STEPS = 32 / U;
+    const Elem *rows;
+    const float *wdist;
+    const __nv_bfloat16 *wlog;
+    const float *lse;
+    const uint2 *meta;
+    const uint32_t *ranks;
+    uint32_t C;
+    int nchunks;
+    int lane;
 
-template <int SRC>
-__device__ __forceinline__ float point_weight(const PoolParams &P, int b, uint2 m) {
-    if (SRC == kSrcX) return 1.f;
-    if (SRC == kSrcDist) return __ldg(static_cast<const float *>(P.wsrc) + b * P.w_bstride + m.y);
-    const float l =
-        __bfloat162float(static_cast<const __nv_bfloat16 *>(P.wsrc)[b * P.w_bstride + m.y]);
-    return __expf(l - __ldg(P.lse + int64_t(b) * P.NHW + m.x));
-}
-
-// Walk the sorted points [a, e) in rank order, calling f(jj, w, v) for each
-// with the point's weight and this lane's CH x VEC slice of its row.  Gather
-// records are read 32 at a time, one per lane, two blocks ahead; the block's
-// weights one block ahead; rows one step (U points) ahead into a register
-// double buffer -- so a step costs issue time, not a memory latency.
-template <typename Elem, int VEC, int CH, int SRC, typename F>
-__device__ __forceinline__ void warp_walk(const PoolParams &P, int b, const Elem *rows, uint32_t a,
-                                          uint32_t e, F &&f) {
-    constexpr int U = CH == 1 ? 4 : (CH == 2 ? 2 : 1);
-    constexpr int STEPS = 32 / U;
-    const int lane = threadIdx.x & 31;
-    const int C = P.C;
-    const int nchunks = C / VEC;
-    auto rec_of = [&](uint32_t j) {
-        return j < e ? point_record<SRC>(P, j) : make_uint2(0u, 0u);
-    };
-    uint32_t jb = a;
-    uint2 r0 = rec_of(jb + lane);
-    uint2 r1 = rec_of(jb + 32 + lane);
-    float w0 = (jb + lane < e) ? point_weight<SRC>(P, b, r0) : 0.f;
-    float v[2][U][CH][VEC];
+    __device__ __forceinline__ Gather(const PoolParams &P, int b) {
+        rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
+        wdist = static_cast<const float *>(P.wsrc) + (SRC == kSrcDist ? b * P.w_bstride : 0);
+        wlog = static_cast<const __nv_bfloat16 *>(P.wsrc) + (SRC == kSrcFused ? b * P.w_bstride : 0);
+        lse = P.lse + (SRC == kSrcFused ? int64_t(b) * P.NHW : 0);
+        meta = P.meta;
+        ranks = P.ranks;
+        C = static_cast<uint32_t>(P.C);
+        nchunks = P.C / VEC;
+        lane = threadIdx.x & 31;
+    }
+    __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t e) const {
+        if (j >= e) return make_uint2(0u, 0u);
+        if (SRC == kSrcX) return make_uint2(__ldg(ranks + j), 0u);
+        return __ldg(meta + j);
+    }
+    __device__ __forceinline__ float weight(uint2 m, bool ok) const {
+        if (!ok) return 0.f;
+        if (SRC == kSrcX) return 1.f;
+        if (SRC == kSrcDist) return __ldg(wdist + m.y);
+        return __expf(__bfloat162float(wlog[m.y]) - __ldg(lse + m.x));
+    }
     // rows of step s of the block whose records are `r` (block start jbb)
-    auto issue = [&](int buf, int s, uint2 r, uint32_t jbb) {
+    __device__ __forceinline__ void issue(float (&v)[U][CH][VEC], int s, uint2 r, uint32_t jbb,
+                                          uint32_t e) const {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t rx = __shfl_sync(0xFFFFFFFFu, r.x, s * U + u);
             const bool ok = jbb + s * U + u < e;
-            const Elem *rp = rows + size_t(rx) * C;
+            const Elem *rp = rows + rx * C;
 #pragma unroll
             for (int q = 0; q < CH; ++q) {
                 const int ch = lane + 32 * q;
                 if (ok && ch < nchunks) {
-                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v[buf][u][q]);
+                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v[u][q]);
                 } else {
 #pragma unroll
-                    for (int k = 0; k < VEC; ++k) v[buf][u][q][k] = 0.f;
+                    for (int k = 0; k < VEC; ++k) v[u][q][k] = 0.f;
                 }
             }
         }
-    };
-    issue(0, 0, r0, jb);
-#pragma unroll 1
-    for (; jb < e; jb += 32) {
-        const uint2 r2 = rec_of(jb + 64 + lane);
-        const float w1 = (jb + 32 + lane < e) ? point_weight<SRC>(P, b, r1) : 0.f;
-#pragma unroll
-        for (int s = 0; s < STEPS; ++s) {
-            if (jb + s * U >= e) break;  // warp-uniform
-            if (s + 1 < STEPS) {
-                if (jb + (s + 1) * U < e) issue((s + 1) & 1, s + 1, r0, jb);
-            } else if (jb + 32 < e) {
-                issue(0, 0, r1, jb + 32);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t jj = jb + s * U + u;
-                const float w = __shfl_sync(0xFFFFFFFFu, w0, s * U + u);
-                if (jj < e) f(jj, w, v[s & 1][u]);
-            }
-        }
-        r0 = r1;
-        r1 = r2;
-        w0 = w1;
     }
-}
+};
 
 template <typename Acc, int CH, int VEC, bool IS_MAX>
 __device__ __forceinline__ void acc_point(Acc (&acc)[CH][VEC],
@@ -203,20 +185,28 @@ __device__ __forceinline__ void acc_point(Acc (&acc)[CH][VEC],
         }
 }
 
-constexpr uint32_t kLongUnit = 0x80000000u;  // unit flag: split by pool_long_kernel
+template <typename Acc, int CH, int VEC, bool IS_MAX>
+__device__ __forceinline__ void acc_reset(Acc (&acc)[CH][VEC],
+                                          uint32_t (&arg)[IS_MAX ? CH : 1][IS_MAX ? VEC : 1]) {
+#pragma unroll
+    for (int q = 0; q < CH; ++q)
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) {
+            acc[q][k] = IS_MAX ? Acc(-INFINITY) : Acc(0);
+            if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? k : 0] = 0xFFFFFFFFu;
+        }
+}
 
 // One warp per work unit.  SPLIT: units flagged long are left to
 // pool_long_kernel (fast mode); the exact mode walks them here, in order.
 template <typename Acc, typename Elem, int VEC, int CH, bool IS_MAX, int SRC, bool SPLIT>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_stream_kernel(const PoolParams P) {
+    using G = Gather<Elem, VEC, CH, SRC>;
+    constexpr int U = G::U, STEPS = G::STEPS;
     extern __shared__ float s_all[];  // per warp: [C][kUnitPitch]
-    constexpr uint32_t kNone = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int C = P.C;
-    const int nchunks = C / VEC;
     const int b = blockIdx.y;
-    float *s_tile = s_all + warp * C * kUnitPitch;
 
     const int64_t k = int64_t(blockIdx.x) * kPoolWarps + warp;
     if (k >= P.sched_counts[0]) return;
@@ -224,81 +214,109 @@ pool_stream_kernel(const PoolParams P) {
     const uint32_t word = __ldg(P.units + 2 * k + 1);
     if (SPLIT && (word & kLongUnit)) return;
     const int ncell = static_cast<int>(word & 0xFFu);
+    const uint32_t *starts = P.starts;
     const uint32_t i0 = __ldg(P.cell_first + cell0), i1 = __ldg(P.cell_first + cell0 + ncell);
-    const uint32_t J0 = __ldg(P.starts + i0), J1 = __ldg(P.starts + i1);
+    const uint32_t J0 = __ldg(starts + i0), J1 = __ldg(starts + i1);
     // which of the unit's cells own an interval (bit x <-> cell0 + x)
     bool mine = false;
     if (lane < ncell)
         mine = __ldg(P.cell_first + cell0 + lane + 1) > __ldg(P.cell_first + cell0 + lane);
     const unsigned has = __ballot_sync(0xFFFFFFFFu, mine);
+    const int C = P.C;
+    float *s_tile = s_all + warp * C * kUnitPitch;
 
-    const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
+    const G g(P, b);
     Acc acc[CH][VEC];
     uint32_t arg[IS_MAX ? CH : 1][IS_MAX ? VEC : 1];
-    auto reset = [&]() {
-#pragma unroll
-        for (int q = 0; q < CH; ++q)
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-                acc[q][e] = IS_MAX ? Acc(-INFINITY) : Acc(0);
-                if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? e : 0] = kNone;
-            }
-    };
-    uint32_t iv = i0, lo = J0, hi = __ldg(P.starts + i0 + 1);
+    acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
+    uint32_t iv = i0, lo = J0, hi = __ldg(starts + i0 + 1);
     auto park = [&]() {  // interval iv = [lo, hi) complete
         const int lc = static_cast<int>(int64_t(__ldg(P.icells + iv)) - cell0);
         const Acc inv = P.mean ? Acc(1) / Acc(hi - lo) : Acc(1);
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
             const int ch = lane + 32 * q;
-            if (ch < nchunks)
+            if (ch < g.nchunks)
 #pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                    const int c = ch * VEC + e;
-                    const Acc r = P.mean ? acc[q][e] * inv : acc[q][e];
-                    s_tile[c * kUnitPitch + lc] = static_cast<float>(r);
+                for (int x = 0; x < VEC; ++x) {
+                    const int c = ch * VEC + x;
+                    s_tile[c * kUnitPitch + lc] = static_cast<float>(acc[q][x] * inv);
                     if (IS_MAX && P.argmax)
                         P.argmax[(b * P.n_int_max + iv) * C + c] =
-                            __ldg(P.ranks + arg[IS_MAX ? q : 0][IS_MAX ? e : 0]);
+                            __ldg(P.ranks + arg[IS_MAX ? q : 0][IS_MAX ? x : 0]);
                 }
         }
     };
-    reset();
+
     if (J1 > J0) {
-        warp_walk<Elem, VEC, CH, SRC>(P, b, rows, J0, J1,
-                                      [&](uint32_t jj, float w, const float (&v)[CH][VEC]) {
-            if (jj == hi) {  // interval boundary (warp-uniform)
-                park();
-                reset();
-                ++iv;
-                lo = hi;
-                hi = __ldg(P.starts + iv + 1);
+        float v[2][U][CH][VEC];
+        uint32_t jb = J0;
+        uint2 r0 = g.rec(jb + lane, J1), r1 = g.rec(jb + 32 + lane, J1);
+        float w0 = g.weight(r0, jb + lane < J1);
+        g.issue(v[0], 0, r0, jb, J1);
+#pragma unroll 1
+        for (; jb < J1; jb += 32) {
+            const uint2 r2 = g.rec(jb + 64 + lane, J1);
+            const float w1 = g.weight(r1, jb + 32 + lane < J1);
+#pragma unroll
+            for (int s = 0; s < STEPS; ++s) {
+                const uint32_t js = jb + s * U;
+                if (js >= J1) break;  // warp-uniform
+                if (s + 1 < STEPS) {
+                    if (js + U < J1) g.issue(v[(s + 1) & 1], s + 1, r0, jb, J1);
+                } else if (jb + 32 < J1) {
+                    g.issue(v[0], 0, r1, jb + 32, J1);
+                }
+                float ws[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) ws[u] = __shfl_sync(0xFFFFFFFFu, w0, s * U + u);
+                if (js + U <= hi) {  // whole step inside the current interval
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, js + u, ws[u], v[s & 1][u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const uint32_t jj = js + u;
+                        if (jj >= J1) break;
+                        if (jj == hi) {  // interval boundary (warp-uniform)
+                            park();
+                            acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
+                            ++iv;
+                            lo = hi;
+                            hi = __ldg(starts + iv + 1);
+                        }
+                        acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, jj, ws[u], v[s & 1][u]);
+                    }
+                }
             }
-            acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, jj, w, v);
-        });
+            r0 = r1;
+            r1 = r2;
+            w0 = w1;
+        }
         park();
     }
     __syncwarp();
     float *out = P.out + int64_t(b) * C * P.n_cells + cell0;
+    const int64_t n_cells = P.n_cells;
     for (int idx = lane; idx < C * ncell; idx += 32) {
         const int c = idx / ncell, x = idx - c * ncell;
-        out[int64_t(c) * P.n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
+        out[int64_t(c) * n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
     }
 }
 
 // Fast mode: one CTA per heavy cell (a single interval above the unit point
 // budget).  Its 8 warps walk equal slices of the interval; the slices'
 // partial results are combined in slice order in shared memory, so the sum
-// is deterministic and the heavy cell no longer sets the kernel's critical
-// path.
+// is deterministic and the heavy cell no longer sets the critical path.
 template <typename Elem, int VEC, int CH, bool IS_MAX, int SRC>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_long_kernel(const PoolParams P) {
+    using G = Gather<Elem, VEC, CH, SRC>;
+    constexpr int U = G::U, STEPS = G::STEPS;
     extern __shared__ float s_all[];  // [kPoolWarps][C] values + [kPoolWarps][C] argmax
-    constexpr uint32_t kNone = 0xFFFFFFFFu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int C = P.C;
-    const int nchunks = C / VEC;
     const int b = blockIdx.y;
     if (int64_t(blockIdx.x) >= P.sched_counts[1]) return;
     const uint32_t k = __ldg(P.long_units + blockIdx.x);
@@ -308,27 +326,47 @@ pool_long_kernel(const PoolParams P) {
     const uint32_t L = hi - lo;
     const uint32_t a = lo + uint32_t(uint64_t(L) * warp / kPoolWarps);
     const uint32_t e = lo + uint32_t(uint64_t(L) * (warp + 1) / kPoolWarps);
-    const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
+    const G g(P, b);
     float acc[CH][VEC];
     uint32_t arg[IS_MAX ? CH : 1][IS_MAX ? VEC : 1];
+    acc_reset<float, CH, VEC, IS_MAX>(acc, arg);
+    if (e > a) {
+        float v[2][U][CH][VEC];
+        uint32_t jb = a;
+        uint2 r0 = g.rec(jb + lane, e), r1 = g.rec(jb + 32 + lane, e);
+        float w0 = g.weight(r0, jb + lane < e);
+        g.issue(v[0], 0, r0, jb, e);
+#pragma unroll 1
+        for (; jb < e; jb += 32) {
+            const uint2 r2 = g.rec(jb + 64 + lane, e);
+            const float w1 = g.weight(r1, jb + 32 + lane < e);
 #pragma unroll
-    for (int q = 0; q < CH; ++q)
+            for (int s = 0; s < STEPS; ++s) {
+                const uint32_t js = jb + s * U;
+                if (js >= e) break;
+                if (s + 1 < STEPS) {
+                    if (js + U < e) g.issue(v[(s + 1) & 1], s + 1, r0, jb, e);
+                } else if (jb + 32 < e) {
+                    g.issue(v[0], 0, r1, jb + 32, e);
+                }
 #pragma unroll
-        for (int x = 0; x < VEC; ++x) {
-            acc[q][x] = IS_MAX ? -INFINITY : 0.f;
-            if (IS_MAX) arg[IS_MAX ? q : 0][IS_MAX ? x : 0] = kNone;
+                for (int u = 0; u < U; ++u) {
+                    const float w = __shfl_sync(0xFFFFFFFFu, w0, s * U + u);
+                    if (!IS_MAX || js + u < e)
+                        acc_point<float, CH, VEC, IS_MAX>(acc, arg, js + u, w, v[s & 1][u]);
+                }
+            }
+            r0 = r1;
+            r1 = r2;
+            w0 = w1;
         }
-    if (e > a)
-        warp_walk<Elem, VEC, CH, SRC>(P, b, rows, a, e,
-                                      [&](uint32_t jj, float w, const float (&v)[CH][VEC]) {
-            acc_point<float, CH, VEC, IS_MAX>(acc, arg, jj, w, v);
-        });
+    }
     float *s_val = s_all;
     uint32_t *s_arg = reinterpret_cast<uint32_t *>(s_all + kPoolWarps * C);
 #pragma unroll
     for (int q = 0; q < CH; ++q) {
         const int ch = lane + 32 * q;
-        if (ch < nchunks)
+        if (ch < g.nchunks)
 #pragma unroll
             for (int x = 0; x < VEC; ++x) {
                 s_val[warp * C + ch * VEC + x] = acc[q][x];
@@ -372,7 +410,7 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
 template <typename T>
 void launch_to_nhwc(const T *src, int64_t NB, int A, int HW, T *dst, cudaStream_t s);
 
-// Launch the instantiated kernel for (Acc, Elem, VEC, SRC) and the shape of
+// Launch the instantiated kernels for (Acc, Elem, VEC, SRC) and the shape of
 // p.C.  Defined (and explicitly instantiated) in the pool_*.cu / fused.cu
 // translation units so the kernel families compile in parallel.
 template <typename Acc, typename Elem, int VEC, int SRC>
