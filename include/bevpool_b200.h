@@ -79,15 +79,20 @@ extern "C" {
  *   point_meta  2 x uint32 per sorted point j: feature row n*H*W + h*W + w
  *               and weight index (n*D + d)*H*W + h*W + w of ranks[j]
  *   long_units  unit indices of the long units
- *   counts      device int64[2]: n_units, n_long
- *   max_units, max_long  host launch sizes (>= the device counts) */
+ *   tasks       8 x uint32 per task (a run of consecutive units one warp
+ *               walks as one point stream): first unit, unit count (bit 31:
+ *               long), first and end sorted point, first and end interval
+ *   counts      device int64[3]: n_units, n_long, n_tasks
+ *   max_units, max_long, max_tasks  host launch sizes (>= the device counts) */
 typedef struct bvp_schedule {
     const uint32_t *units;
     const uint32_t *point_meta;
     const uint32_t *long_units;
+    const uint32_t *tasks;
     const int64_t *counts;
     int64_t max_units;
     int64_t max_long;
+    int64_t max_tasks;
 } bvp_schedule;
 
 int bvp_abi_version(void);
@@ -131,15 +136,18 @@ int64_t bvp_units_capacity(int nx, int ny, int64_t n_int_max);
 size_t bvp_units_workspace_bytes(int nx, int ny);
 
 /* Cut the grid into work units (runs of <= 8 cells of one BEV row holding
- * <= budget in-range points, x-major order), list the long units, and fill
- * the point gather table (skipped when point_meta is NULL).  sched_counts:
- * device int64[2] receiving n_units, n_long.  Run after the cache build. */
+ * <= budget in-range points, cell order), list the long units, group the
+ * units into tasks of ~task_budget points, and fill the point gather table
+ * (skipped when point_meta is NULL).  Capacities: units and tasks
+ * bvp_units_capacity(), long_units n_cells.  sched_counts: device int64[3]
+ * receiving n_units, n_long, n_tasks.  Run after the cache build. */
 int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
                       const uint32_t *cell_first, const int64_t *counts, int N,
                       int H, int W, int D, int nx, int ny, int budget,
-                      uint32_t *units, uint32_t *long_units,
-                      int64_t *sched_counts, uint32_t *point_meta,
-                      void *workspace, size_t workspace_bytes, void *stream);
+                      int task_budget, uint32_t *units, uint32_t *long_units,
+                      uint32_t *tasks, int64_t *sched_counts,
+                      uint32_t *point_meta, void *workspace,
+                      size_t workspace_bytes, void *stream);
 
 /* The point gather table alone (e.g. when a loaded cache's frustum shape is
  * only known at pooling time). */

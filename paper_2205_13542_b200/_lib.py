@@ -38,8 +38,8 @@ _S = ctypes.c_size_t
 
 class Schedule(ctypes.Structure):
     """struct bvp_schedule (include/bevpool_b200.h)."""
-    _fields_ = [("units", _P), ("point_meta", _P), ("long_units", _P), ("counts", _P),
-                ("max_units", _L), ("max_long", _L)]
+    _fields_ = [("units", _P), ("point_meta", _P), ("long_units", _P), ("tasks", _P),
+                ("counts", _P), ("max_units", _L), ("max_long", _L), ("max_tasks", _L)]
 
 
 _SP = ctypes.POINTER(Schedule)
@@ -56,8 +56,8 @@ SIGNATURES = {
     "bvp_pool_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
     "bvp_units_capacity": (_L, [_I, _I, _L]),
     "bvp_units_workspace_bytes": (_S, [_I, _I]),
-    "bvp_make_schedule": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P,
-                               _S, _P]),
+    "bvp_make_schedule": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P,
+                               _P, _P, _S, _P]),
     "bvp_point_meta": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
                                   _L, _I, _I, _P, _P, _P, _P]),

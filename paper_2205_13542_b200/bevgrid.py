@@ -119,6 +119,8 @@ def _u32(t: torch.Tensor) -> np.ndarray:
 
 #: points per work unit of the interval kernels (csrc/units.cu)
 UNIT_BUDGET = 128
+#: points per warp task (a run of consecutive units walked as one stream)
+TASK_BUDGET = 384
 
 
 @dataclass(eq=False)
@@ -140,10 +142,12 @@ class AssociationCache:
     d_counts: torch.Tensor                 # (2,) int64: n_in, n_int
     d_units: torch.Tensor                  # (2 * max_units,) (first cell, count | long)
     d_long_units: torch.Tensor             # (max_long,) unit ids of split cells
-    d_sched_counts: torch.Tensor           # (2,) int64: n_units, n_long
+    d_tasks: torch.Tensor                  # (8 * max_tasks,) warp tasks
+    d_sched_counts: torch.Tensor           # (3,) int64: n_units, n_long, n_tasks
     d_meta: torch.Tensor                   # (2 * P,) per sorted point: row, weight index
     max_units: int                         # launch bounds (>= the device counts)
     max_long: int
+    max_tasks: int
     fingerprint: int
     nx: int
     ny: int
@@ -197,7 +201,7 @@ class AssociationCache:
     def fit_launch(self) -> None:
         """Shrink the launch bounds to the exact unit counts (one host sync)."""
         c = self.d_sched_counts.cpu().tolist()
-        self.max_units, self.max_long = max(1, int(c[0])), int(c[1])
+        self.max_units, self.max_long, self.max_tasks = max(1, int(c[0])), int(c[1]), max(1, int(c[2]))
         self._host.pop("schedule", None)
 
     def schedule(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1):
@@ -211,7 +215,8 @@ class AssociationCache:
         s = self._host.get("schedule")
         if s is None:
             s = _lib.Schedule(ptr(self.d_units), ptr(self.d_meta), ptr(self.d_long_units),
-                              ptr(self.d_sched_counts), self.max_units, self.max_long)
+                              ptr(self.d_tasks), ptr(self.d_sched_counts), self.max_units,
+                              self.max_long, self.max_tasks)
             self._host["schedule"] = s
         return s
 
@@ -269,18 +274,21 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
         cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
         counts=torch.zeros(2, dtype=torch.int64, device=dev),
         units=torch.empty(2 * cap, **i32), long_units=torch.empty(n_cells, **i32),
-        sched_counts=torch.zeros(2, dtype=torch.int64, device=dev),
+        tasks=torch.empty(8 * cap, **i32),
+        sched_counts=torch.zeros(3, dtype=torch.int64, device=dev),
         meta=torch.empty(2 * P, **i32),
         cap=cap, ws=torch.empty(ws, dtype=torch.uint8, device=dev),
     )
 
 
-def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None) -> None:
-    """Work units, plus the point gather table when the frustum dims are known."""
+def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
+                   task_budget: int = TASK_BUDGET) -> None:
+    """Work units and tasks, plus the point gather table when the frustum
+    dims are known."""
     N, H, W, D = dims if dims is not None else (1, 1, 1, 1)
     _lib.call("bvp_make_schedule", ptr(b["ranks"]), ptr(b["starts"]), ptr(b["cell_first"]),
-              ptr(b["counts"]), N, H, W, D, nx, ny, budget, ptr(b["units"]),
-              ptr(b["long_units"]), ptr(b["sched_counts"]),
+              ptr(b["counts"]), N, H, W, D, nx, ny, budget, task_budget, ptr(b["units"]),
+              ptr(b["long_units"]), ptr(b["tasks"]), ptr(b["sched_counts"]),
               ptr(b["meta"]) if dims is not None else None, ptr(b["ws"]), b["ws"].numel(),
               stream_ptr(dev))
 
@@ -289,9 +297,9 @@ def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, dims=None)
     """A cache over the buffers b; launch bounds are the capacities until
     fit_launch() (no host sync needed to pool)."""
     return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
-                            b["iop"], b["counts"], b["units"], b["long_units"],
+                            b["iop"], b["counts"], b["units"], b["long_units"], b["tasks"],
                             b["sched_counts"], b["meta"], b["cap"], int(b["long_units"].numel()),
-                            fingerprint, nx, ny, n_cameras, frustum, grid, dims)
+                            b["cap"], fingerprint, nx, ny, n_cameras, frustum, grid, dims)
 
 
 class CacheBuilder:

@@ -53,9 +53,11 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
     p.units = sched->units;
     p.meta = reinterpret_cast<const uint2 *>(sched->point_meta);
     p.long_units = sched->long_units;
+    p.tasks = reinterpret_cast<const uint4 *>(sched->tasks);
     p.sched_counts = sched->counts;
     p.max_units = sched->max_units;
     p.max_long = sched->max_long;
+    p.max_tasks = sched->max_tasks;
     p.out = out;
     p.C = C;
     p.nx = nx;

@@ -3,30 +3,31 @@
 // Restates the reference's interval_reduce (_kernels.py:22-63).
 //
 // Work decomposition (measured; DESIGN.md §4 records the alternatives):
-//   * The cached schedule cuts the BEV grid into work UNITS: runs of at most
-//     kUnitCells consecutive cells of one row holding at most a budget of
-//     in-range points.  A unit's intervals occupy one contiguous range
-//     [J0, J1) of the rank-ordered point stream.
-//   * One WARP owns one unit and walks its point stream in rank order.  The
-//     lanes span the channel row (16-byte chunks), so a point's row is one
-//     coalesced warp load and interval boundaries are warp-uniform: every
-//     interval is accumulated sequentially in rank order, exactly like the
-//     reference.  With Acc = double the sums are bit-identical to
-//     interval_reduce (fp32 x fp32 products are exact in fp64); Acc = float is
-//     the fast mode.
+//   * The cached schedule (units.cu) cuts the BEV grid into UNITS -- runs of
+//     at most kUnitCells consecutive cells of one row -- and groups
+//     consecutive units into TASKS of about a fixed number of in-range
+//     points.  Units and tasks are in cell order, so a task's intervals are
+//     one contiguous range [J0, J1) of the rank-ordered point stream.
+//   * One WARP walks one task's stream in rank order.  The lanes span the
+//     channel row (16-byte chunks), so a point's row is one coalesced warp
+//     load and interval boundaries are warp-uniform: every interval is
+//     accumulated sequentially in rank order, exactly like the reference.
+//     With Acc = double the sums are bit-identical to interval_reduce (fp32 x
+//     fp32 products are exact in fp64); Acc = float is the fast mode.
 //   * Gather records (feature row, weight index; precomputed per sorted point
 //     so the loop never divides) are read 32 at a time, one per lane, two
 //     blocks ahead; weights one block ahead; rows one 4-point step ahead into
-//     a register double buffer.  Boundaries are tested once per step: steps
-//     inside one interval take a branch-free path.
-//   * A finished interval is parked in the warp's shared [C][kUnitCells]
-//     tile; the warp then writes its cells' output columns once -- zeros of
-//     empty cells included -- so there is no memset and exactly one
-//     non-atomic store per (channel, cell).
+//     a register double buffer.  Interval boundaries are tested once per
+//     step; steps inside one interval take a branch-free path, and the next
+//     interval's end and cell are prefetched.
+//   * Finished intervals are parked in the warp's shared [C][kUnitCells] tile
+//     of the current unit; when the stream leaves a unit the warp writes its
+//     cells' output columns once -- zeros of empty cells included -- so there
+//     is no memset and exactly one non-atomic store per (channel, cell).
 //   * Fast mode only: a cell holding more points than the unit budget is a
-//     "long" unit; pool_long_kernel splits it over the 8 warps of a CTA and
-//     combines the slices in order in shared memory, so a heavy cell does not
-//     set the kernel's critical path.
+//     "long" unit (its own task); pool_long_kernel splits it over the 8 warps
+//     of a CTA and combines the slices in order in shared memory, so a heavy
+//     cell does not set the kernel's critical path.
 //
 // Sources (SRC):
 //   kSrcDist  : rows = NHWC features (f32), weight = dist[n,d,h,w] (f32)
@@ -41,7 +42,7 @@ namespace bvp {
 constexpr int kPoolWarps = 8;
 constexpr int kPoolThreads = 32 * kPoolWarps;
 constexpr int kUnitPitch = kUnitCells + 1;
-constexpr uint32_t kLongUnit = 0x80000000u;  // unit flag: split by pool_long_kernel
+constexpr uint32_t kLongUnit = 0x80000000u;  // unit / task flag: split by pool_long_kernel
 
 enum { kSrcDist = 0, kSrcX = 1, kSrcFused = 2 };
 
@@ -53,17 +54,18 @@ struct PoolParams {
     const uint32_t *starts;  // n_int + 1 entries (sentinel = n_in)
     const uint32_t *icells;
     const uint32_t *cell_first;  // n_cells + 1: first interval with cell >= c
-    const uint32_t *units;       // work units: (first cell, cell count | long flag)
+    const uint32_t *units;       // (first cell, ncell | has << 8 | long flag)
     const uint2 *meta;           // per sorted point: (feature row, weight index)
     const uint32_t *long_units;  // indices of the long (split) units
-    const int64_t *sched_counts; // device: n_units, n_long
+    const uint4 *tasks;          // 2 x uint4 per task (units.cu)
+    const int64_t *sched_counts; // device: n_units, n_long, n_tasks
     float *out;              // (B, C, n_cells)
     uint32_t *argmax;        // MAX only, optional: (B, n_int_max, C)
     int C, D, HW, NHW;
     int mean;
     int nx, ny;
     int64_t n_cells, n_int_max;
-    int64_t max_units, max_long;  // launch sizes (>= the device counts)
+    int64_t max_units, max_long, max_tasks;  // launch sizes (>= the device counts)
     int64_t rows_bstride;    // elements of rows per batch sample
     int64_t w_bstride;       // elements of wsrc per batch sample
 };
@@ -105,13 +107,15 @@ struct Loader<__nv_bfloat16, 1> {
     }
 };
 
-// Per-warp gather context: every pointer batch-offset once, 32-bit element
-// offsets in the loop (callers guarantee rows * C < 2^32).
+// Per-warp gather context: pointers batch-offset once, the lane's chunk
+// folded into the row base, 32-bit element offsets in the loop (callers
+// guarantee rows * C < 2^32).  Lanes beyond the row read chunk 0 of the same
+// row (same sectors: no extra traffic, no predicates in the loop).
 template <typename Elem, int VEC, int CH, int SRC>
 struct Gather {
     static constexpr int U = CH == 1 ? 4 : (CH == 2 ? 2 : 1);  // rows per step
     static constexpr int STEPS = 32 / U;
-    const Elem *rows;
+    const Elem *rows;   // + this lane's chunk offset
     const float *wdist;
     const __nv_bfloat16 *wlog;
     const float *lse;
@@ -122,15 +126,16 @@ struct Gather {
     int lane;
 
     __device__ __forceinline__ Gather(const PoolParams &P, int b) {
-        rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride;
+        lane = threadIdx.x & 31;
+        nchunks = P.C / VEC;
+        const int ch0 = lane < nchunks ? lane : 0;
+        rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride + ch0 * VEC;
         wdist = static_cast<const float *>(P.wsrc) + (SRC == kSrcDist ? b * P.w_bstride : 0);
         wlog = static_cast<const __nv_bfloat16 *>(P.wsrc) + (SRC == kSrcFused ? b * P.w_bstride : 0);
         lse = P.lse + (SRC == kSrcFused ? int64_t(b) * P.NHW : 0);
         meta = P.meta;
         ranks = P.ranks;
         C = static_cast<uint32_t>(P.C);
-        nchunks = P.C / VEC;
-        lane = threadIdx.x & 31;
     }
     __device__ __forceinline__ uint2 rec(uint32_t j, uint32_t e) const {
         if (j >= e) return make_uint2(0u, 0u);
@@ -143,23 +148,24 @@ struct Gather {
         if (SRC == kSrcDist) return __ldg(wdist + m.y);
         return __expf(__bfloat162float(wlog[m.y]) - __ldg(lse + m.x));
     }
-    // rows of step s of the block whose records are `r` (block start jbb)
+    // rows of step s of the block whose records are `r`.  FULL: the whole
+    // step lies before e (no per-point test); otherwise points >= e load row
+    // 0 (their weight is 0 and MAX skips them).
+    template <bool FULL>
     __device__ __forceinline__ void issue(float (&v)[U][CH][VEC], int s, uint2 r, uint32_t jbb,
                                           uint32_t e) const {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint32_t rx = __shfl_sync(0xFFFFFFFFu, r.x, s * U + u);
-            const bool ok = jbb + s * U + u < e;
+            uint32_t rx = __shfl_sync(0xFFFFFFFFu, r.x, s * U + u);
+            if (!FULL && jbb + s * U + u >= e) rx = 0;
             const Elem *rp = rows + rx * C;
 #pragma unroll
             for (int q = 0; q < CH; ++q) {
-                const int ch = lane + 32 * q;
-                if (ok && ch < nchunks) {
-                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + ch * VEC, v[u][q]);
-                } else {
+                if (q == 0 || lane + 32 * q < nchunks)
+                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + 32 * q * VEC, v[u][q]);
+                else
 #pragma unroll
                     for (int k = 0; k < VEC; ++k) v[u][q][k] = 0.f;
-                }
             }
         }
     }
@@ -197,41 +203,106 @@ __device__ __forceinline__ void acc_reset(Acc (&acc)[CH][VEC],
         }
 }
 
-// One warp per work unit.  SPLIT: units flagged long are left to
-// pool_long_kernel (fast mode); the exact mode walks them here, in order.
+// The gather pipeline over sorted points [a, e): calls on_step(js, ws, v)
+// for every full step inside one block (caller decides fast / slow path).
+// Kept as a macro-free template so both kernels share it.
+template <typename G, typename Buf, typename StepFn>
+__device__ __forceinline__ void gather_stream(const G &g, uint32_t a, uint32_t e, Buf &v,
+                                              StepFn &&on_step) {
+    constexpr int U = G::U, STEPS = G::STEPS;
+    const int lane = g.lane;
+    uint32_t jb = a;
+    uint2 r0 = g.rec(jb + lane, e), r1 = g.rec(jb + 32 + lane, e);
+    float w0 = g.weight(r0, jb + lane < e);
+    if (jb + U <= e) g.template issue<true>(v[0], 0, r0, jb, e);
+    else g.template issue<false>(v[0], 0, r0, jb, e);
+#pragma unroll 1
+    for (; jb < e; jb += 32) {
+        const uint2 r2 = g.rec(jb + 64 + lane, e);
+        const float w1 = g.weight(r1, jb + 32 + lane < e);
+#pragma unroll
+        for (int s = 0; s < STEPS; ++s) {
+            const uint32_t js = jb + s * U;
+            if (js >= e) break;  // warp-uniform
+            if (s + 1 < STEPS) {
+                const uint32_t jn = js + U;
+                if (jn + U <= e) g.template issue<true>(v[(s + 1) & 1], s + 1, r0, jb, e);
+                else if (jn < e) g.template issue<false>(v[(s + 1) & 1], s + 1, r0, jb, e);
+            } else {
+                const uint32_t jn = jb + 32;
+                if (jn + U <= e) g.template issue<true>(v[0], 0, r1, jn, e);
+                else if (jn < e) g.template issue<false>(v[0], 0, r1, jn, e);
+            }
+            float ws[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) ws[u] = __shfl_sync(0xFFFFFFFFu, w0, s * U + u);
+            on_step(js, ws, v[s & 1]);
+        }
+        r0 = r1;
+        r1 = r2;
+        w0 = w1;
+    }
+}
+
+// One warp per task.  SPLIT: long tasks are left to pool_long_kernel (fast
+// mode); the exact mode walks them here, in order.
 template <typename Acc, typename Elem, int VEC, int CH, bool IS_MAX, int SRC, bool SPLIT>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_stream_kernel(const PoolParams P) {
     using G = Gather<Elem, VEC, CH, SRC>;
-    constexpr int U = G::U, STEPS = G::STEPS;
+    constexpr int U = G::U;
     extern __shared__ float s_all[];  // per warp: [C][kUnitPitch]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y;
 
-    const int64_t k = int64_t(blockIdx.x) * kPoolWarps + warp;
-    if (k >= P.sched_counts[0]) return;
-    const int64_t cell0 = __ldg(P.units + 2 * k);
-    const uint32_t word = __ldg(P.units + 2 * k + 1);
-    if (SPLIT && (word & kLongUnit)) return;
-    const int ncell = static_cast<int>(word & 0xFFu);
-    const uint32_t *starts = P.starts;
-    const uint32_t i0 = __ldg(P.cell_first + cell0), i1 = __ldg(P.cell_first + cell0 + ncell);
-    const uint32_t J0 = __ldg(starts + i0), J1 = __ldg(starts + i1);
-    // which of the unit's cells own an interval (bit x <-> cell0 + x)
-    bool mine = false;
-    if (lane < ncell)
-        mine = __ldg(P.cell_first + cell0 + lane + 1) > __ldg(P.cell_first + cell0 + lane);
-    const unsigned has = __ballot_sync(0xFFFFFFFFu, mine);
+    const int64_t t = int64_t(blockIdx.x) * kPoolWarps + warp;
+    if (t >= P.sched_counts[2]) return;
+    const uint4 ta = __ldg(P.tasks + 2 * t), tb = __ldg(P.tasks + 2 * t + 1);
+    if (SPLIT && (ta.y & kLongUnit)) return;
+    const uint32_t u_end = ta.x + (ta.y & 0xFFFFu);
+    const uint32_t J0 = ta.z, J1 = ta.w;
     const int C = P.C;
+    const int64_t n_cells = P.n_cells;
+    const uint32_t *starts = P.starts;
+    const uint32_t *icells = P.icells;
     float *s_tile = s_all + warp * C * kUnitPitch;
+    float *out_b = P.out + int64_t(b) * C * n_cells;
+
+    // current unit
+    uint32_t u = ta.x;
+    uint2 ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + u);
+    int64_t cell0 = ur.x;
+    auto flush_unit = [&]() {  // write the current unit's columns, advance
+        const int ncell = static_cast<int>(ur.y & 0xFFu);
+        const uint32_t has = (ur.y >> 8) & 0xFFu;
+        __syncwarp();
+        float *o = out_b + cell0;
+        for (int idx = lane; idx < C * ncell; idx += 32) {
+            const int c = idx / ncell, x = idx - c * ncell;
+            o[int64_t(c) * n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
+        }
+        __syncwarp();
+        ++u;
+        if (u < u_end) {
+            ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + u);
+            cell0 = ur.x;
+        }
+    };
 
     const G g(P, b);
     Acc acc[CH][VEC];
     uint32_t arg[IS_MAX ? CH : 1][IS_MAX ? VEC : 1];
     acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
-    uint32_t iv = i0, lo = J0, hi = __ldg(starts + i0 + 1);
+    // current interval [lo, hi) with its cell; the next one prefetched
+    uint32_t iv = tb.x;
+    uint32_t lo = J0, hi = __ldg(starts + iv + 1);
+    uint32_t cell = __ldg(icells + iv);
+    uint32_t nhi = __ldg(starts + iv + 2), ncell_id = __ldg(icells + iv + 1);
+    auto enter_interval = [&]() {  // make the unit containing `cell` current
+        while (int64_t(cell) >= cell0 + int64_t(ur.y & 0xFFu)) flush_unit();
+    };
     auto park = [&]() {  // interval iv = [lo, hi) complete
-        const int lc = static_cast<int>(int64_t(__ldg(P.icells + iv)) - cell0);
+        const int lc = static_cast<int>(int64_t(cell) - cell0);
         const Acc inv = P.mean ? Acc(1) / Acc(hi - lo) : Acc(1);
 #pragma unroll
         for (int q = 0; q < CH; ++q) {
@@ -249,60 +320,38 @@ pool_stream_kernel(const PoolParams P) {
     };
 
     if (J1 > J0) {
+        enter_interval();
         float v[2][U][CH][VEC];
-        uint32_t jb = J0;
-        uint2 r0 = g.rec(jb + lane, J1), r1 = g.rec(jb + 32 + lane, J1);
-        float w0 = g.weight(r0, jb + lane < J1);
-        g.issue(v[0], 0, r0, jb, J1);
-#pragma unroll 1
-        for (; jb < J1; jb += 32) {
-            const uint2 r2 = g.rec(jb + 64 + lane, J1);
-            const float w1 = g.weight(r1, jb + 32 + lane < J1);
+        gather_stream(g, J0, J1, v, [&](uint32_t js, const float (&ws)[U],
+                                        const float (&vb)[U][CH][VEC]) {
+            if (js + U <= hi) {  // whole step inside the current interval
 #pragma unroll
-            for (int s = 0; s < STEPS; ++s) {
-                const uint32_t js = jb + s * U;
-                if (js >= J1) break;  // warp-uniform
-                if (s + 1 < STEPS) {
-                    if (js + U < J1) g.issue(v[(s + 1) & 1], s + 1, r0, jb, J1);
-                } else if (jb + 32 < J1) {
-                    g.issue(v[0], 0, r1, jb + 32, J1);
-                }
-                float ws[U];
+                for (int k = 0; k < U; ++k)
+                    acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, js + k, ws[k], vb[k]);
+            } else {
 #pragma unroll
-                for (int u = 0; u < U; ++u) ws[u] = __shfl_sync(0xFFFFFFFFu, w0, s * U + u);
-                if (js + U <= hi) {  // whole step inside the current interval
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, js + u, ws[u], v[s & 1][u]);
-                } else {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const uint32_t jj = js + u;
-                        if (jj >= J1) break;
-                        if (jj == hi) {  // interval boundary (warp-uniform)
-                            park();
-                            acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
-                            ++iv;
-                            lo = hi;
-                            hi = __ldg(starts + iv + 1);
-                        }
-                        acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, jj, ws[u], v[s & 1][u]);
+                for (int k = 0; k < U; ++k) {
+                    const uint32_t jj = js + k;
+                    if (jj >= J1) break;
+                    if (jj == hi) {  // interval boundary (warp-uniform)
+                        park();
+                        acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
+                        ++iv;
+                        lo = hi;
+                        hi = nhi;
+                        cell = ncell_id;
+                        nhi = __ldg(starts + iv + 2);
+                        ncell_id = __ldg(icells + iv + 1);
+                        enter_interval();
                     }
+                    acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, jj, ws[k], vb[k]);
                 }
             }
-            r0 = r1;
-            r1 = r2;
-            w0 = w1;
-        }
+        });
         park();
     }
-    __syncwarp();
-    float *out = P.out + int64_t(b) * C * P.n_cells + cell0;
-    const int64_t n_cells = P.n_cells;
-    for (int idx = lane; idx < C * ncell; idx += 32) {
-        const int c = idx / ncell, x = idx - c * ncell;
-        out[int64_t(c) * n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
-    }
+    // the last unit with an interval and every empty unit after it
+    while (u < u_end) flush_unit();
 }
 
 // Fast mode: one CTA per heavy cell (a single interval above the unit point
@@ -313,7 +362,7 @@ template <typename Elem, int VEC, int CH, bool IS_MAX, int SRC>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_long_kernel(const PoolParams P) {
     using G = Gather<Elem, VEC, CH, SRC>;
-    constexpr int U = G::U, STEPS = G::STEPS;
+    constexpr int U = G::U;
     extern __shared__ float s_all[];  // [kPoolWarps][C] values + [kPoolWarps][C] argmax
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int C = P.C;
@@ -332,34 +381,13 @@ pool_long_kernel(const PoolParams P) {
     acc_reset<float, CH, VEC, IS_MAX>(acc, arg);
     if (e > a) {
         float v[2][U][CH][VEC];
-        uint32_t jb = a;
-        uint2 r0 = g.rec(jb + lane, e), r1 = g.rec(jb + 32 + lane, e);
-        float w0 = g.weight(r0, jb + lane < e);
-        g.issue(v[0], 0, r0, jb, e);
-#pragma unroll 1
-        for (; jb < e; jb += 32) {
-            const uint2 r2 = g.rec(jb + 64 + lane, e);
-            const float w1 = g.weight(r1, jb + 32 + lane < e);
+        gather_stream(g, a, e, v, [&](uint32_t js, const float (&ws)[U],
+                                      const float (&vb)[U][CH][VEC]) {
 #pragma unroll
-            for (int s = 0; s < STEPS; ++s) {
-                const uint32_t js = jb + s * U;
-                if (js >= e) break;
-                if (s + 1 < STEPS) {
-                    if (js + U < e) g.issue(v[(s + 1) & 1], s + 1, r0, jb, e);
-                } else if (jb + 32 < e) {
-                    g.issue(v[0], 0, r1, jb + 32, e);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const float w = __shfl_sync(0xFFFFFFFFu, w0, s * U + u);
-                    if (!IS_MAX || js + u < e)
-                        acc_point<float, CH, VEC, IS_MAX>(acc, arg, js + u, w, v[s & 1][u]);
-                }
-            }
-            r0 = r1;
-            r1 = r2;
-            w0 = w1;
-        }
+            for (int k2 = 0; k2 < U; ++k2)
+                if (!IS_MAX || js + k2 < e)
+                    acc_point<float, CH, VEC, IS_MAX>(acc, arg, js + k2, ws[k2], vb[k2]);
+        });
     }
     float *s_val = s_all;
     uint32_t *s_arg = reinterpret_cast<uint32_t *>(s_all + kPoolWarps * C);
@@ -437,10 +465,11 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
     BVP_REQUIRE(SRC == kSrcX || p.meta, BVP_ERR_INVALID,
                 "the cache's point gather table (point_meta) is required");
+    BVP_REQUIRE(p.tasks, BVP_ERR_INVALID, "the cache's task table is required");
     // fast mode: heavy cells are split over a CTA by pool_long_kernel; the
     // exact mode must walk every interval in order and does not split
     constexpr bool kSplit = sizeof(Acc) == sizeof(float);
-    const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps)),
+    const dim3 grid(static_cast<unsigned>(ceil_div(p.max_tasks, kPoolWarps)),
                     static_cast<unsigned>(B));
     const size_t lsmem = size_t(kPoolWarps) * p.C * 2 * sizeof(float);
 #define BVP_LAUNCH_CH(CHV)                                                                   \
