@@ -273,7 +273,7 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
         starts=torch.empty(n_cells + 1, **i32), icells=torch.empty(n_cells, **i32),
         cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
         counts=torch.zeros(2, dtype=torch.int64, device=dev),
-        units=torch.empty(2 * cap, **i32), long_units=torch.empty(n_cells, **i32),
+        units=torch.empty(4 * (cap + 1), **i32), long_units=torch.empty(n_cells, **i32),
         tasks=torch.empty(8 * cap, **i32),
         sched_counts=torch.zeros(3, dtype=torch.int64, device=dev),
         meta=torch.empty(2 * P, **i32),

@@ -244,6 +244,109 @@ __device__ __forceinline__ void gather_stream(const G &g, uint32_t a, uint32_t e
     }
 }
 
+// One warp per work unit (<= 8 cells, <= budget points): the simple loop the
+// gather microbenchmark (scripts/l2_gather_bench.cu) shows is fastest on
+// B200 -- U rows per step, every lane loading the step's gather records and
+// weights itself (same address across the warp: one L1 transaction), no
+// register double buffer, so the kernel stays near 40 registers and the SM
+// holds enough warps to cover the L2 latency.  SPLIT: long units are left to
+// pool_long_kernel (fast mode); the exact mode walks them here, in order.
+#ifndef BVP_UNIT_MIN_BLOCKS
+#define BVP_UNIT_MIN_BLOCKS 6  // 48 warps/SM: caps registers at 40
+#endif
+template <typename Acc, typename Elem, int VEC, int CH, bool IS_MAX, int SRC, bool SPLIT>
+__global__ void __launch_bounds__(kPoolThreads, BVP_UNIT_MIN_BLOCKS)
+pool_unit_kernel(const PoolParams P) {
+    constexpr int U = CH == 1 ? 4 : (CH == 2 ? 2 : 1);
+    extern __shared__ float s_all[];  // per warp: [C][kUnitPitch]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b = blockIdx.y;
+    const int64_t k = int64_t(blockIdx.x) * kPoolWarps + warp;
+    if (k >= P.sched_counts[0]) return;
+    const uint4 ur = __ldg(reinterpret_cast<const uint4 *>(P.units) + k);
+    if (SPLIT && (ur.y & kLongUnit)) return;
+    const uint4 un = __ldg(reinterpret_cast<const uint4 *>(P.units) + k + 1);
+    const int64_t cell0 = ur.x;
+    const int ncell = static_cast<int>(ur.y & 0xFFu);
+    const uint32_t has = (ur.y >> 8) & 0xFFu;
+    const uint32_t J0 = ur.w, J1 = un.w;
+    const int C = P.C;
+    const int nchunks = C / VEC;
+    const uint32_t *starts = P.starts;
+    float *s_tile = s_all + warp * C * kUnitPitch;
+    const Gather<Elem, VEC, CH, SRC> g(P, b);
+
+    Acc acc[CH][VEC];
+    uint32_t arg[IS_MAX ? CH : 1][IS_MAX ? VEC : 1];
+    acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
+    uint32_t iv = ur.z, lo = J0;
+    uint32_t hi = J1 > J0 ? __ldg(starts + iv + 1) : 0u;
+    auto park = [&]() {  // interval iv = [lo, hi) complete
+        const int lc = static_cast<int>(int64_t(__ldg(P.icells + iv)) - cell0);
+        const Acc inv = P.mean ? Acc(1) / Acc(hi - lo) : Acc(1);
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+            const int ch = lane + 32 * q;
+            if (ch < nchunks)
+#pragma unroll
+                for (int x = 0; x < VEC; ++x) {
+                    const int c = ch * VEC + x;
+                    s_tile[c * kUnitPitch + lc] = static_cast<float>(acc[q][x] * inv);
+                    if (IS_MAX && P.argmax)
+                        P.argmax[(b * P.n_int_max + iv) * C + c] =
+                            __ldg(P.ranks + arg[IS_MAX ? q : 0][IS_MAX ? x : 0]);
+                }
+        }
+    };
+#pragma unroll 1
+    for (uint32_t js = J0; js < J1; js += U) {
+        float w[U];
+        float v[U][CH][VEC];
+        const bool full = js + U <= J1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool ok = full || js + u < J1;
+            const uint2 m = g.rec(ok ? js + u : J0, J1);
+            w[u] = g.weight(m, ok);
+            const Elem *rp = g.rows + m.x * g.C;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                if (q == 0 || lane + 32 * q < nchunks)
+                    Loader<Elem, VEC>::template load<SRC == kSrcX>(rp + 32 * q * VEC, v[u][q]);
+                else
+#pragma unroll
+                    for (int x = 0; x < VEC; ++x) v[u][q][x] = 0.f;
+            }
+        }
+        if (js + U <= hi) {  // whole step inside the current interval
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, js + u, w[u], v[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t jj = js + u;
+                if (jj >= J1) break;
+                if (jj == hi) {  // interval boundary (warp-uniform)
+                    park();
+                    acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
+                    ++iv;
+                    lo = hi;
+                    hi = __ldg(starts + iv + 1);
+                }
+                acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, jj, w[u], v[u]);
+            }
+        }
+    }
+    if (J1 > J0) park();
+    __syncwarp();
+    float *out = P.out + int64_t(b) * C * P.n_cells + cell0;
+    const int64_t n_cells = P.n_cells;
+    for (int idx = lane; idx < C * ncell; idx += 32) {
+        const int c = idx / ncell, x = idx - c * ncell;
+        out[int64_t(c) * n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
+    }
+}
+
 // One warp per task.  SPLIT: long tasks are left to pool_long_kernel (fast
 // mode); the exact mode walks them here, in order.
 template <typename Acc, typename Elem, int VEC, int CH, bool IS_MAX, int SRC, bool SPLIT>
@@ -270,7 +373,7 @@ pool_stream_kernel(const PoolParams P) {
 
     // current unit
     uint32_t u = ta.x;
-    uint2 ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + u);
+    uint2 ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + 2 * size_t(u));
     int64_t cell0 = ur.x;
     auto flush_unit = [&]() {  // write the current unit's columns, advance
         const int ncell = static_cast<int>(ur.y & 0xFFu);
@@ -284,7 +387,7 @@ pool_stream_kernel(const PoolParams P) {
         __syncwarp();
         ++u;
         if (u < u_end) {
-            ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + u);
+            ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + 2 * size_t(u));
             cell0 = ur.x;
         }
     };
@@ -369,7 +472,7 @@ pool_long_kernel(const PoolParams P) {
     const int b = blockIdx.y;
     if (int64_t(blockIdx.x) >= P.sched_counts[1]) return;
     const uint32_t k = __ldg(P.long_units + blockIdx.x);
-    const int64_t cell = __ldg(P.units + 2 * size_t(k));
+    const int64_t cell = __ldg(P.units + 4 * size_t(k));
     const uint32_t iv = __ldg(P.cell_first + cell);
     const uint32_t lo = __ldg(P.starts + iv), hi = __ldg(P.starts + iv + 1);
     const uint32_t L = hi - lo;
@@ -469,13 +572,13 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     // fast mode: heavy cells are split over a CTA by pool_long_kernel; the
     // exact mode must walk every interval in order and does not split
     constexpr bool kSplit = sizeof(Acc) == sizeof(float);
-    const dim3 grid(static_cast<unsigned>(ceil_div(p.max_tasks, kPoolWarps)),
+    const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps)),
                     static_cast<unsigned>(B));
     const size_t lsmem = size_t(kPoolWarps) * p.C * 2 * sizeof(float);
 #define BVP_LAUNCH_CH(CHV)                                                                   \
     if (ch == CHV) {                                                                         \
-        auto k = is_max ? pool_stream_kernel<Acc, Elem, VEC, CHV, true, SRC, kSplit>         \
-                        : pool_stream_kernel<Acc, Elem, VEC, CHV, false, SRC, kSplit>;       \
+        auto k = is_max ? pool_unit_kernel<Acc, Elem, VEC, CHV, true, SRC, kSplit>           \
+                        : pool_unit_kernel<Acc, Elem, VEC, CHV, false, SRC, kSplit>;         \
         if (smem > 48 * 1024)                                                                \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
         k<<<grid, kPoolThreads, smem, s>>>(p);                                               \

@@ -55,9 +55,12 @@ __global__ void units_kernel(const uint32_t *__restrict__ starts,
         auto emit = [&](int from, int to, bool is_long) {
             if (WRITE) {
                 const uint32_t m = (has >> from) & ((1u << (to - from)) - 1u);
-                units[2 * out] = static_cast<uint32_t>(c0 + from);
-                units[2 * out + 1] =
+                const uint32_t iv0 = cell_first[c0 + from];
+                units[4 * out] = static_cast<uint32_t>(c0 + from);
+                units[4 * out + 1] =
                     static_cast<uint32_t>(to - from) | (m << 8) | (is_long ? kLongFlag : 0u);
+                units[4 * out + 2] = iv0;
+                units[4 * out + 3] = starts[iv0];
                 if (is_long) long_units[atomicAdd(n_long, 1ull)] = out;
                 ++out;
             }
@@ -89,7 +92,7 @@ __global__ void units_kernel(const uint32_t *__restrict__ starts,
 __device__ __forceinline__ uint32_t unit_j0(const uint32_t *__restrict__ units,
                                             const uint32_t *__restrict__ starts,
                                             const uint32_t *__restrict__ cell_first, int64_t u) {
-    return starts[cell_first[units[2 * u]]];
+    return starts[cell_first[units[4 * u]]];
 }
 
 // flag[u] = 1 if unit u starts a task (see the header comment).
@@ -103,7 +106,7 @@ __global__ void task_flags_kernel(const uint32_t *__restrict__ units,
          u += (int64_t)gridDim.x * blockDim.x) {
         uint32_t f = 1;
         if (u > 0) {
-            const bool lg = units[2 * u + 1] & kLongFlag, lg_prev = units[2 * u - 1] & kLongFlag;
+            const bool lg = units[4 * u + 1] & kLongFlag, lg_prev = units[4 * u - 3] & kLongFlag;
             const uint32_t a = unit_j0(units, starts, cell_first, u - 1);
             const uint32_t b = unit_j0(units, starts, cell_first, u);
             f = (lg || lg_prev || (a / task_budget) != (b / task_budget)) ? 1u : 0u;
@@ -128,11 +131,11 @@ __global__ void tasks_kernel(const uint32_t *__restrict__ units,
         int64_t v = u + 1;
         while (v < n_units && !flag[v]) ++v;  // next task start (tasks are short)
         const uint32_t t = task_of[u];
-        const uint32_t iv0 = cell_first[units[2 * u]];
-        const uint32_t iv1 = v < n_units ? cell_first[units[2 * v]] : static_cast<uint32_t>(counts[1]);
+        const uint32_t iv0 = cell_first[units[4 * u]];
+        const uint32_t iv1 = v < n_units ? cell_first[units[4 * v]] : static_cast<uint32_t>(counts[1]);
         uint32_t *r = tasks + 8 * size_t(t);
         r[0] = static_cast<uint32_t>(u);
-        r[1] = static_cast<uint32_t>(v - u) | (units[2 * u + 1] & kLongFlag);
+        r[1] = static_cast<uint32_t>(v - u) | (units[4 * u + 1] & kLongFlag);
         r[2] = starts[iv0];
         r[3] = starts[iv1];
         r[4] = iv0;
@@ -156,13 +159,21 @@ __global__ void point_meta_kernel(const uint32_t *__restrict__ ranks,
     }
 }
 
+// Counts, plus the sentinel unit record at index n_units (its first interval
+// and first point are the ends of the last unit: n_int, n_in).
 __global__ void store_counts_kernel(const uint32_t *__restrict__ n_units,
                                     const unsigned long long *__restrict__ n_long,
                                     const uint32_t *__restrict__ n_tasks,
-                                    int64_t *__restrict__ out) {
-    out[0] = *n_units;
+                                    const int64_t *__restrict__ counts,
+                                    uint32_t *__restrict__ units, int64_t *__restrict__ out) {
+    const uint32_t nu = *n_units;
+    out[0] = nu;
     out[1] = static_cast<int64_t>(*n_long);
     out[2] = *n_tasks;
+    units[4 * size_t(nu)] = 0u;
+    units[4 * size_t(nu) + 1] = 0u;
+    units[4 * size_t(nu) + 2] = static_cast<uint32_t>(counts[1]);
+    units[4 * size_t(nu) + 3] = static_cast<uint32_t>(counts[0]);
 }
 
 struct UnitsLayout {
@@ -255,7 +266,7 @@ int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
     device_excl_scan<uint32_t>(flag, task_of, L.cap, tpart, n_tasks, s);
     tasks_kernel<<<ub, 256, 0, s>>>(units, interval_starts, cell_first, n_units, flag, task_of,
                                     counts, tasks);
-    store_counts_kernel<<<1, 1, 0, s>>>(n_units, n_long, n_tasks, sched_counts);
+    store_counts_kernel<<<1, 1, 0, s>>>(n_units, n_long, n_tasks, counts, units, sched_counts);
     if (point_meta) {
         const int rc = bvp_point_meta(ranks, counts, N, H, W, D, point_meta, stream);
         if (rc != BVP_OK) return rc;
