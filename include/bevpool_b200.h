@@ -57,7 +57,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BVP_ABI_VERSION 2
+#define BVP_ABI_VERSION 3
 
 #define BVP_OK 0
 #define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
@@ -83,7 +83,11 @@ extern "C" {
  *               walks as one point stream): first unit, unit count (bit 31:
  *               long), first and end sorted point, first and end interval
  *   counts      device int64[3]: n_units, n_long, n_tasks
- *   max_units, max_long, max_tasks  host launch sizes (>= the device counts) */
+ *   max_units, max_long, max_tasks  host launch sizes (>= the device counts)
+ *   order       optional (may be NULL): launch order of the units, a
+ *               permutation of [0, n_units) grouping units of one 2D block
+ *               of BEV cells so a CTA's warps share feature rows in L1
+ *   order_rep   units per warp of the unit kernel (>= 1) */
 typedef struct bvp_schedule {
     const uint32_t *units;
     const uint32_t *point_meta;
@@ -93,6 +97,8 @@ typedef struct bvp_schedule {
     int64_t max_units;
     int64_t max_long;
     int64_t max_tasks;
+    const uint32_t *order;
+    int64_t order_rep;
 } bvp_schedule;
 
 int bvp_abi_version(void);

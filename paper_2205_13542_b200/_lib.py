@@ -18,7 +18,7 @@ BVP_OK, BVP_ERR_INVALID, BVP_ERR_UNSUPPORTED, BVP_ERR_CUDA = 0, 1, 2, 3
 BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
 TILE_CELLS = 32
 OUT_OF_RANGE = 0xFFFFFFFF
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class ExtensionMissingError(BevPoolError, RuntimeError):
@@ -39,7 +39,8 @@ _S = ctypes.c_size_t
 class Schedule(ctypes.Structure):
     """struct bvp_schedule (include/bevpool_b200.h)."""
     _fields_ = [("units", _P), ("point_meta", _P), ("long_units", _P), ("tasks", _P),
-                ("counts", _P), ("max_units", _L), ("max_long", _L), ("max_tasks", _L)]
+                ("counts", _P), ("max_units", _L), ("max_long", _L), ("max_tasks", _L),
+                ("order", _P), ("order_rep", _L)]
 
 
 _SP = ctypes.POINTER(Schedule)

@@ -21,6 +21,7 @@ on first access.
 from __future__ import annotations
 
 import hashlib
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -121,6 +122,8 @@ def _u32(t: torch.Tensor) -> np.ndarray:
 UNIT_BUDGET = 128
 #: points per warp task (a run of consecutive units walked as one stream)
 TASK_BUDGET = 384
+#: unit launch order "BX,BY,R" (2D cell blocks, units per warp); "" = cell order
+UNIT_ORDER = ""
 
 
 @dataclass(eq=False)
@@ -214,11 +217,28 @@ class AssociationCache:
             self.meta_dims = (N, H, W, D)
         s = self._host.get("schedule")
         if s is None:
+            order, rep = self._unit_order()
             s = _lib.Schedule(ptr(self.d_units), ptr(self.d_meta), ptr(self.d_long_units),
                               ptr(self.d_tasks), ptr(self.d_sched_counts), self.max_units,
-                              self.max_long, self.max_tasks)
+                              self.max_long, self.max_tasks, ptr(order), rep)
             self._host["schedule"] = s
         return s
+
+    def _unit_order(self):
+        """Launch order of the work units: 2D blocks of BX x BY cells, so the
+        warps of one CTA pool neighbouring cells and share feature rows in L1."""
+        cfg = os.environ.get("BVP_UNIT_ORDER", UNIT_ORDER)
+        if not cfg:
+            return None, 1
+        bx, by, rep = (int(v) for v in cfg.split(","))
+        n = int(self.d_sched_counts[0].item())
+        u = self.d_units[: 4 * n].view(n, 4)[:, 0].to(torch.int64) & 0xFFFFFFFF
+        ix, iy = u // self.ny, u % self.ny
+        nby = (self.ny + by - 1) // by
+        key = ((ix // bx) * nby + iy // by) * (bx * self.ny) + (ix % bx) * self.ny + iy
+        order = torch.argsort(key, stable=True).to(torch.int32)
+        self._host["order"] = order
+        return order, rep
 
     # ---- reference-typed host views ------------------------------------
     def _view(self, name, tensor, n):

@@ -58,6 +58,8 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
     p.max_units = sched->max_units;
     p.max_long = sched->max_long;
     p.max_tasks = sched->max_tasks;
+    p.order = sched->order;
+    p.order_rep = sched->order_rep > 0 ? sched->order_rep : 1;
     p.out = out;
     p.C = C;
     p.nx = nx;

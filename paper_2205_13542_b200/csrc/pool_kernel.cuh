@@ -66,6 +66,8 @@ struct PoolParams {
     int nx, ny;
     int64_t n_cells, n_int_max;
     int64_t max_units, max_long, max_tasks;  // launch sizes (>= the device counts)
+    const uint32_t *order;   // optional launch order of the units (2D blocks)
+    int64_t order_rep;       // units per warp
     int64_t rows_bstride;    // elements of rows per batch sample
     int64_t w_bstride;       // elements of wsrc per batch sample
 };
@@ -261,10 +263,15 @@ pool_unit_kernel(const PoolParams P) {
     extern __shared__ float s_all[];  // per warp: [C][kUnitPitch]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y;
-    const int64_t k = int64_t(blockIdx.x) * kPoolWarps + warp;
-    if (k >= P.sched_counts[0]) return;
+    const int64_t n_units = P.sched_counts[0];
+    const int rep = static_cast<int>(P.order_rep);
+#pragma unroll 1
+    for (int r = 0; r < rep; ++r) {
+    const int64_t kk = (int64_t(blockIdx.x) * rep + r) * kPoolWarps + warp;
+    if (kk >= n_units) break;
+    const int64_t k = P.order ? int64_t(__ldg(P.order + kk)) : kk;
     const uint4 ur = __ldg(reinterpret_cast<const uint4 *>(P.units) + k);
-    if (SPLIT && (ur.y & kLongUnit)) return;
+    if (SPLIT && (ur.y & kLongUnit)) continue;
     const uint4 un = __ldg(reinterpret_cast<const uint4 *>(P.units) + k + 1);
     const int64_t cell0 = ur.x;
     const int ncell = static_cast<int>(ur.y & 0xFFu);
@@ -344,6 +351,8 @@ pool_unit_kernel(const PoolParams P) {
     for (int idx = lane; idx < C * ncell; idx += 32) {
         const int c = idx / ncell, x = idx - c * ncell;
         out[int64_t(c) * n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
+    }
+    __syncwarp();
     }
 }
 
@@ -572,7 +581,7 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     // fast mode: heavy cells are split over a CTA by pool_long_kernel; the
     // exact mode must walk every interval in order and does not split
     constexpr bool kSplit = sizeof(Acc) == sizeof(float);
-    const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps)),
+    const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps * p.order_rep)),
                     static_cast<unsigned>(B));
     const size_t lsmem = size_t(kPoolWarps) * p.C * 2 * sizeof(float);
 #define BVP_LAUNCH_CH(CHV)                                                                   \
