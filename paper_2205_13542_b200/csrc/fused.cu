@@ -23,20 +23,51 @@ int run_pool<float, __nv_bfloat16, 1, kSrcFused>(const PoolParams &p, int B, boo
     return run_pool_impl<float, __nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);
 }
 
-// lse[pix] = max_d l + log(sum_d exp(l - max)); thread per pixel, the D
-// loads of consecutive pixels are coalesced.
-__global__ void pixel_lse_kernel(const __nv_bfloat16 *__restrict__ logits, int64_t NB, int D,
-                                 int HW, float *__restrict__ lse) {
-    const int64_t total = NB * HW;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t n = t / HW, hw = t - n * HW;
-        const __nv_bfloat16 *l = logits + n * D * int64_t(HW) + hw;
-        float m = -INFINITY;
-        for (int d = 0; d < D; ++d) m = fmaxf(m, __bfloat162float(l[int64_t(d) * HW]));
-        float s = 0.f;
-        for (int d = 0; d < D; ++d) s += __expf(__bfloat162float(l[int64_t(d) * HW]) - m);
-        lse[t] = m + __logf(s);
+// lse[pix] = max_d l + log(sum_d exp(l - max)).  A CTA covers 32 consecutive
+// pixels of one camera; its 8 warps split the D depth planes (warp w takes
+// d = w, w+8, ...), so each warp's loads are 64 contiguous bytes of one
+// plane and every thread keeps ~D/8 independent loads in flight.  Partial
+// (max, sum) pairs are merged in shared memory.
+constexpr int kLseWarps = 8;
+__global__ void __launch_bounds__(32 * kLseWarps)
+pixel_lse_kernel(const __nv_bfloat16 *__restrict__ logits, int64_t NB, int D, int HW,
+                 float *__restrict__ lse) {
+    __shared__ float s_m[kLseWarps][32], s_s[kLseWarps][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tiles = (HW + 31) / 32;
+    const int64_t n = blockIdx.x / tiles;
+    const int hw = (blockIdx.x - n * tiles) * 32 + lane;
+    const bool ok = hw < HW;
+    const __nv_bfloat16 *l = logits + n * D * int64_t(HW) + (ok ? hw : 0);
+    float m = -INFINITY, sum = 0.f;
+    int d = warp;
+#pragma unroll 1
+    for (; d + 3 * kLseWarps < D; d += 4 * kLseWarps) {
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __bfloat162float(l[int64_t(d + k * kLseWarps) * HW]);
+        const float mm = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+        const float nm = fmaxf(m, mm);
+        sum = sum * __expf(m - nm) + __expf(v[0] - nm) + __expf(v[1] - nm) + __expf(v[2] - nm) +
+              __expf(v[3] - nm);
+        m = nm;
+    }
+    for (; d < D; d += kLseWarps) {
+        const float v = __bfloat162float(l[int64_t(d) * HW]);
+        const float nm = fmaxf(m, v);
+        sum = sum * __expf(m - nm) + __expf(v - nm);
+        m = nm;
+    }
+    s_m[warp][lane] = m;
+    s_s[warp][lane] = sum;
+    __syncthreads();
+    if (warp == 0 && ok) {
+        float M = s_m[0][lane];
+        for (int w = 1; w < kLseWarps; ++w) M = fmaxf(M, s_m[w][lane]);
+        float S = 0.f;
+        for (int w = 0; w < kLseWarps; ++w)
+            if (s_m[w][lane] != -INFINITY) S += s_s[w][lane] * __expf(s_m[w][lane] - M);
+        lse[n * HW + hw] = M + __logf(S);
     }
 }
 
@@ -83,9 +114,9 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     float *lse = reinterpret_cast<float *>(ws + L.off_lse);
     auto *ctx = reinterpret_cast<__nv_bfloat16 *>(ws + L.off_ctx);
     const int64_t NB = int64_t(B) * N, HW = int64_t(H) * W;
-    const unsigned lb = static_cast<unsigned>(std::min<int64_t>(ceil_div(NB * HW, 128), 148 * 16));
     auto *lg = reinterpret_cast<const __nv_bfloat16 *>(logits);
-    pixel_lse_kernel<<<lb, 128, 0, s>>>(lg, NB, D, int(HW), lse);
+    const unsigned lb = static_cast<unsigned>(NB * ceil_div(HW, 32));
+    pixel_lse_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), lse);
     launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
                                   int(HW), ctx, s);
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,

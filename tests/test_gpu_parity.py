@@ -338,3 +338,71 @@ def test_cache_builder_no_sync_rebuild_matches():
         np.testing.assert_array_equal(c2.ranks, cache.ranks)
         c2._host_counts = None
         c2._host.clear()
+
+
+# ---- gather backward (config B) vs the fp64 restatement --------------------
+
+def _backward_case(name="T", seed=0):
+    spec = bp.CONFIGS[name]
+    rig, features, logits, grid = bp.gen_workload(bp.WorkloadSpec(
+        spec.n_cameras, spec.frustum, spec.grid, spec.channels, seed))
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    dist = o.normalize_depth(logits)
+    g = np.random.default_rng(seed + 7).normal(size=(features.shape[1], grid.n_cells))
+    return spec, features, dist, grid, cache, g.astype(np.float32)
+
+
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+def test_backward_matches_fp64_restatement(red):
+    spec, features, dist, grid, cache, g = _backward_case("T")
+    dev = torch.device("cuda")
+    f = torch.from_numpy(features).to(dev).requires_grad_(True)
+    d = torch.from_numpy(dist).to(dev).requires_grad_(True)
+    out = bp.bev_pool(f, d, cache, grid, red)
+    want_out = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
+                               cache.interval_cells, grid.n_cells, red)
+    assert max_rel_dev(want_out, out.detach().cpu().numpy().reshape(want_out.shape)) <= FP32_TOL
+    out.backward(torch.from_numpy(g).to(dev).view_as(out))
+    gf, gw = o.pool_backward(features, dist, cache.cell_of_point, g.astype(np.float64),
+                             cache.ranks, cache.interval_starts, cache.interval_cells, red)
+    assert max_rel_dev(gf, f.grad.cpu().numpy()) <= FP32_TOL
+    assert max_rel_dev(gw, d.grad.cpu().numpy()) <= FP32_TOL
+
+
+def test_backward_batched_matches_per_sample():
+    spec, features, dist, grid, cache, g = _backward_case("T")
+    dev = torch.device("cuda")
+    _, f2, l2, _ = bp.gen_workload(bp.WorkloadSpec(spec.n_cameras, spec.frustum, grid,
+                                                   spec.channels, 1))
+    F = torch.from_numpy(np.stack([features, f2])).to(dev).requires_grad_(True)
+    Dd = torch.from_numpy(np.stack([dist, o.normalize_depth(l2)])).to(dev).requires_grad_(True)
+    G = torch.from_numpy(np.stack([g, -g])).to(dev).view(2, spec.channels, grid.nx, grid.ny)
+    bp.bev_pool(F, Dd, cache, grid).backward(G)
+    for b in range(2):
+        fb = F[b].detach().clone().requires_grad_(True)
+        db = Dd[b].detach().clone().requires_grad_(True)
+        bp.bev_pool(fb, db, cache, grid).backward(G[b])
+        assert torch.equal(fb.grad, F.grad[b])
+        assert torch.equal(db.grad, Dd.grad[b])
+
+
+def test_backward_nuscenes_shape_sum():
+    """SUM gradients at the S shape, restated per camera in fp64 (the full
+    (P, C) fp64 oracle would need 1.3 GB)."""
+    spec, features, dist, grid, cache, g = _backward_case("S")
+    dev = torch.device("cuda")
+    f = torch.from_numpy(features).to(dev).requires_grad_(True)
+    d = torch.from_numpy(dist).to(dev).requires_grad_(True)
+    bp.bev_pool(f, d, cache, grid).backward(torch.from_numpy(g).to(dev).view(80, grid.nx, grid.ny))
+    N, C, H, W = features.shape
+    D = dist.shape[1]
+    cells = cache.cell_of_point.reshape(N, H, W, D)
+    g64 = np.concatenate([g.astype(np.float64), np.zeros((C, 1))], axis=1)  # OOR -> zero column
+    gf_got, gw_got = f.grad.cpu().numpy(), d.grad.cpu().numpy()
+    for n in range(N):
+        idx = np.where(cells[n] == bp.OUT_OF_RANGE, grid.n_cells, cells[n]).astype(np.int64)
+        gc = g64[:, idx]                                   # C, H, W, D
+        gf = np.einsum("chwd,dhw->chw", gc, dist[n].astype(np.float64))
+        gw = np.einsum("chwd,chw->dhw", gc, features[n].astype(np.float64))
+        assert max_rel_dev(gf, gf_got[n]) <= FP32_TOL
+        assert max_rel_dev(gw, gw_got[n]) <= FP32_TOL
