@@ -403,12 +403,13 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
     outx = torch.empty((C, n_cells), dtype=torch.float32, device=dev)
     from paper_2205_13542_b200 import _lib
     from paper_2205_13542_b200.bevgrid import ptr, stream_ptr
+    from paper_2205_13542_b200.pooling import _scratch
 
     def pool_x():
         _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
                   ptr(cache.d_interval_cells), ptr(cache.d_cell_first), cache.schedule(), C,
                   grid.nx, grid.ny, 0,
-                  ptr(outx),
+                  ptr(outx), *_scratch(cache, 1, C, 0),
                   stream_ptr(dev))
     ms = _timeit(torch, pool_x, flush)
     rec("materialised_pool", ms, n_in * (4 * C + 4) + 8 * n_int + 4 * C * n_cells)

@@ -57,7 +57,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BVP_ABI_VERSION 3
+#define BVP_ABI_VERSION 5
 
 #define BVP_OK 0
 #define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
@@ -87,7 +87,16 @@ extern "C" {
  *   order       optional (may be NULL): launch order of the units, a
  *               permutation of [0, n_units) grouping units of one 2D block
  *               of BEV cells so a CTA's warps share feature rows in L1
- *   order_rep   units per warp of the unit kernel (>= 1) */
+ *   order_rep   units per warp of the unit kernel (>= 1)
+ *   work, splits, work_counts, max_work, max_splits, chunk
+ *               optional chunk schedule of the fast kernels from
+ *               bvp_make_work (work NULL: none): work = 4 x uint32 per
+ *               chunk (first sorted point, end, destination, interval),
+ *               chunks of <= `chunk` points sorted by length; splits = 4 x
+ *               uint32 per interval cut into several chunks (interval, cell,
+ *               first partial slot, chunk count); work_counts = device
+ *               int64[3] n_work, n_splits, n_partials; max_work, max_splits,
+ *               max_partials host bounds (>= the device counts) */
 typedef struct bvp_schedule {
     const uint32_t *units;
     const uint32_t *point_meta;
@@ -99,6 +108,13 @@ typedef struct bvp_schedule {
     int64_t max_tasks;
     const uint32_t *order;
     int64_t order_rep;
+    const uint32_t *work;
+    const uint32_t *splits;
+    const int64_t *work_counts;
+    int64_t max_work;
+    int64_t max_splits;
+    int64_t max_partials;
+    int64_t chunk;
 } bvp_schedule;
 
 int bvp_abi_version(void);
@@ -160,7 +176,25 @@ int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
 int bvp_point_meta(const uint32_t *ranks, const int64_t *counts, int N, int H,
                    int W, int D, uint32_t *point_meta, void *stream);
 
+/* Chunk schedule of the fast (fp32) kernels (work.cu): every interval is
+ * cut into chunks of <= chunk points; chunks are listed longest first, so a
+ * warp's 8 lane groups (one chunk each) finish together.  An interval cut
+ * into several chunks ("split") gets one fp32 partial per chunk, combined in
+ * chunk order by a second pass.  Capacities: work n_int + n_in / chunk + 1
+ * (bvp_work_capacity), splits n_int.  work_counts: device int64[3] receiving
+ * n_work, n_splits, n_partials.  Run after the cache build. */
+int64_t bvp_work_capacity(int64_t n_int_max, int64_t n_points, int chunk);
+size_t bvp_work_workspace_bytes(int64_t n_int_max, int64_t n_points, int chunk);
+int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cells,
+                  const int64_t *counts, int64_t n_int_max, int64_t n_points, int chunk,
+                  uint32_t *work, uint32_t *splits, int64_t *work_counts,
+                  void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- cached forward ---------------------------------------------------- */
+
+/* Scratch of the fast kernels (the split intervals' partials) for B samples
+ * of C channels in `mode`; 0 when the schedule has no chunk schedule. */
+size_t bvp_pool_scratch_bytes(const bvp_schedule *schedule, int B, int C, int mode);
 
 /* Workspace for bvp_pool_forward_f32: the NHWC copy of the features. */
 size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W);
@@ -180,7 +214,7 @@ int bvp_pool_forward_f32(const float *features, const float *dist,
                          int B, int N, int C, int H, int W, int D, int nx,
                          int ny, int64_t n_int_max, int mode, int exact,
                          float *out, float *feats_nhwc, uint32_t *argmax,
-                         void *stream);
+                         void *scratch, size_t scratch_bytes, void *stream);
 
 /* (NB, C, H*W) -> (NB, H*W, C) f32 copy (the features' NHWC staging that
  * bvp_pool_forward_f32 performs first; pooling.py:215). */
@@ -196,7 +230,8 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,
                               const bvp_schedule *schedule, int B, int N,
                               int C, int H, int W, int D, int nx, int ny,
                               int64_t n_int_max, int mode, int exact,
-                              float *out, uint32_t *argmax, void *stream);
+                              float *out, uint32_t *argmax, void *scratch,
+                              size_t scratch_bytes, void *stream);
 
 /* w_sorted[j] = dist_t[ranks[j]] (dist given as (N,D,H,W)), j < n_in. */
 int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in,
@@ -222,7 +257,8 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
                         const uint32_t *interval_cells,
                         const uint32_t *cell_first,
                         const bvp_schedule *schedule, int C, int nx, int ny,
-                        int mode, float *out, void *stream);
+                        int mode, float *out, void *scratch, size_t scratch_bytes,
+                        void *stream);
 
 /* ---- fused lift + pool, bf16 inputs (config F) ------------------------- */
 
@@ -238,7 +274,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context,
                         const bvp_schedule *schedule, int B, int N, int C,
                         int H, int W, int D, int nx, int ny, int mode,
                         float *out, void *workspace, size_t workspace_bytes,
-                        void *stream);
+                        void *scratch, size_t scratch_bytes, void *stream);
 
 /* ---- gather backward (config B) ---------------------------------------- */
 

@@ -18,7 +18,7 @@ BVP_OK, BVP_ERR_INVALID, BVP_ERR_UNSUPPORTED, BVP_ERR_CUDA = 0, 1, 2, 3
 BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
 TILE_CELLS = 32
 OUT_OF_RANGE = 0xFFFFFFFF
-ABI_VERSION = 3
+ABI_VERSION = 5
 
 
 class ExtensionMissingError(BevPoolError, RuntimeError):
@@ -40,7 +40,9 @@ class Schedule(ctypes.Structure):
     """struct bvp_schedule (include/bevpool_b200.h)."""
     _fields_ = [("units", _P), ("point_meta", _P), ("long_units", _P), ("tasks", _P),
                 ("counts", _P), ("max_units", _L), ("max_long", _L), ("max_tasks", _L),
-                ("order", _P), ("order_rep", _L)]
+                ("order", _P), ("order_rep", _L), ("work", _P), ("splits", _P),
+                ("work_counts", _P), ("max_work", _L), ("max_splits", _L), ("max_partials", _L),
+                ("chunk", _L)]
 
 
 _SP = ctypes.POINTER(Schedule)
@@ -60,19 +62,23 @@ SIGNATURES = {
     "bvp_make_schedule": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P,
                                _P, _P, _S, _P]),
     "bvp_point_meta": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
+    "bvp_work_capacity": (_L, [_L, _L, _I]),
+    "bvp_work_workspace_bytes": (_S, [_L, _L, _I]),
+    "bvp_make_work": (_I, [_P, _P, _P, _L, _L, _I, _P, _P, _P, _P, _S, _P]),
+    "bvp_pool_scratch_bytes": (_S, [_SP, _I, _I, _I]),
     "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
-                                  _L, _I, _I, _P, _P, _P, _P]),
+                                  _L, _I, _I, _P, _P, _P, _P, _S, _P]),
     "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I,
-                                       _I, _L, _I, _I, _P, _P, _P]),
+                                       _I, _L, _I, _I, _P, _P, _P, _S, _P]),
     "bvp_to_nhwc_f32": (_I, [_P, _I, _I, _I, _P, _P]),
     "bvp_reorder_weights": (_I, [_P, _P, _L, _I, _I, _I, _I, _P, _P]),
     "bvp_normalize_depth": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "bvp_any_nonfinite": (_I, [_P, _L, _P, _P]),
     "bvp_lift_f32": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P]),
-    "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _P, _P]),
+    "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _P, _P, _S, _P]),
     "bvp_fused_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
     "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
-                                 _I, _P, _P, _S, _P]),
+                                 _I, _P, _P, _S, _P, _S, _P]),
     "bvp_backward_workspace_bytes": (_S, [_I, _I, _L]),
     "bvp_pool_backward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                    _I, _L, _I, _P, _P, _P, _S, _P]),

@@ -15,7 +15,7 @@ import torch
 
 from . import _lib
 from .bevgrid import AssociationCache, BevGridSpec, ptr, stream_ptr
-from .pooling import _MODE, BevFeatureMap, Reducer, _reducer
+from .pooling import _MODE, BevFeatureMap, Reducer, _reducer, _scratch
 
 
 class _BevPoolFn(torch.autograd.Function):
@@ -34,9 +34,11 @@ class _BevPoolFn(torch.autograd.Function):
             argmax = torch.empty((B, cache.n_int_max, C), dtype=torch.int32, device=dev)
         _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                  ptr(cache.d_cell_first), cache.schedule(N, H, W, D), B, N, C, H, W, D, nx, ny,
+                  ptr(cache.d_cell_first), cache.schedule(N, H, W, D),
+                  B, N, C, H, W, D, nx, ny,
                   cache.n_int_max,
-                  _MODE[reducer], int(exact), ptr(out), ptr(nhwc), ptr(argmax), stream_ptr(dev))
+                  _MODE[reducer], int(exact), ptr(out), ptr(nhwc), ptr(argmax),
+                  *_scratch(cache, B, C, _MODE[reducer]), stream_ptr(dev))
         ctx.cache, ctx.reducer, ctx.dims = cache, reducer, (B, N, C, H, W, D, nx, ny)
         ctx.save_for_backward(nhwc, dist, argmax)
         return out

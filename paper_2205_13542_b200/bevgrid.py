@@ -122,8 +122,16 @@ def _u32(t: torch.Tensor) -> np.ndarray:
 UNIT_BUDGET = 128
 #: points per warp task (a run of consecutive units walked as one stream)
 TASK_BUDGET = 384
-#: unit launch order "BX,BY,R" (2D cell blocks, units per warp); "" = cell order
-UNIT_ORDER = ""
+#: chunk length of the fast kernels' work list (csrc/work.cu); 0 disables it
+CHUNK = int(os.environ.get("BVP_CHUNK", "32"))
+
+
+def work_bounds(n_points: int, n_int_max: int, chunk: int) -> tuple[int, int, int]:
+    """Host upper bounds of the chunk schedule's counts without a host sync:
+    chunks <= n_int + n_in / chunk; split intervals hold > chunk points each;
+    their partial slots <= 2 n_in / chunk."""
+    return (n_int_max + n_points // chunk + 1, n_points // (chunk + 1) + 1,
+            2 * n_points // chunk + 1)
 
 
 @dataclass(eq=False)
@@ -158,6 +166,14 @@ class AssociationCache:
     frustum: FrustumSpec | None = field(default=None, repr=False)
     grid: BevGridSpec | None = field(default=None, repr=False)
     meta_dims: tuple | None = None         # (N, H, W, D) d_meta was derived for
+    # chunk schedule of the fast kernels (csrc/work.cu); None when CHUNK == 0
+    d_work: torch.Tensor | None = None     # (4 * max_work,) chunks, longest first
+    d_splits: torch.Tensor | None = None   # (4 * max_splits,) intervals cut into chunks
+    d_work_counts: torch.Tensor | None = None  # (3,) int64: n_work, n_splits, n_partials
+    max_work: int = 0
+    max_splits: int = 0
+    max_partials: int = 0
+    chunk: int = 0
     _host_counts: tuple | None = field(default=None, repr=False)
     _host: dict = field(default_factory=dict, repr=False)
 
@@ -202,10 +218,15 @@ class AssociationCache:
         return int(self.d_sched_counts[1].item())
 
     def fit_launch(self) -> None:
-        """Shrink the launch bounds to the exact unit counts (one host sync)."""
+        """Shrink the launch bounds to the exact unit / chunk counts (one host
+        sync)."""
         c = self.d_sched_counts.cpu().tolist()
         self.max_units, self.max_long, self.max_tasks = max(1, int(c[0])), int(c[1]), max(1, int(c[2]))
-        self._host.pop("schedule", None)
+        if self.d_work_counts is not None:
+            w = self.d_work_counts.cpu().tolist()
+            self.max_work, self.max_splits, self.max_partials = int(w[0]), int(w[1]), int(w[2])
+        self._host.pop("schedules", None)
+        self._host.pop("scratch", None)
 
     def schedule(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1):
         """The bvp_schedule the C ABI takes; the point gather table is
@@ -215,30 +236,31 @@ class AssociationCache:
             _lib.call("bvp_point_meta", ptr(self.d_ranks), ptr(self.d_counts), N, H, W, D,
                       ptr(self.d_meta), stream_ptr(self.device))
             self.meta_dims = (N, H, W, D)
-        s = self._host.get("schedule")
+        s = self._host.get("schedules")
         if s is None:
-            order, rep = self._unit_order()
+            work = (None, None, None, 0, 0, 0, 0)
+            if self.d_work is not None:
+                work = (ptr(self.d_work), ptr(self.d_splits), ptr(self.d_work_counts),
+                        self.max_work, self.max_splits, self.max_partials, self.chunk)
             s = _lib.Schedule(ptr(self.d_units), ptr(self.d_meta), ptr(self.d_long_units),
                               ptr(self.d_tasks), ptr(self.d_sched_counts), self.max_units,
-                              self.max_long, self.max_tasks, ptr(order), rep)
-            self._host["schedule"] = s
+                              self.max_long, self.max_tasks, None, 1, *work)
+            self._host["schedules"] = s
         return s
 
-    def _unit_order(self):
-        """Launch order of the work units: 2D blocks of BX x BY cells, so the
-        warps of one CTA pool neighbouring cells and share feature rows in L1."""
-        cfg = os.environ.get("BVP_UNIT_ORDER", UNIT_ORDER)
-        if not cfg:
-            return None, 1
-        bx, by, rep = (int(v) for v in cfg.split(","))
-        n = int(self.d_sched_counts[0].item())
-        u = self.d_units[: 4 * n].view(n, 4)[:, 0].to(torch.int64) & 0xFFFFFFFF
-        ix, iy = u // self.ny, u % self.ny
-        nby = (self.ny + by - 1) // by
-        key = ((ix // bx) * nby + iy // by) * (bx * self.ny) + (ix % bx) * self.ny + iy
-        order = torch.argsort(key, stable=True).to(torch.int32)
-        self._host["order"] = order
-        return order, rep
+    def scratch(self, B: int, C: int, mode: int) -> torch.Tensor | None:
+        """Scratch of the fast kernels (split-interval partials), kept per
+        (B, C, mode) shape."""
+        n = int(_lib.load().bvp_pool_scratch_bytes(self.schedule(), B, C, mode))
+        if n == 0:
+            return None
+        key = (B, C, mode == 2)
+        pool = self._host.setdefault("scratch", {})
+        t = pool.get(key)
+        if t is None or t.numel() < n:
+            t = torch.empty(n, dtype=torch.uint8, device=self.device)
+            pool[key] = t
+        return t
 
     # ---- reference-typed host views ------------------------------------
     def _view(self, name, tensor, n):
@@ -287,8 +309,17 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
     lib = _lib.load()
     n_cells = nx * ny
     cap = int(lib.bvp_units_capacity(nx, ny, n_cells))
-    ws = max(lib.bvp_sort_workspace_bytes(P, n_cells), lib.bvp_units_workspace_bytes(nx, ny))
+    n_int_max = min(n_cells, P)
+    ws = max(lib.bvp_sort_workspace_bytes(P, n_cells), lib.bvp_units_workspace_bytes(nx, ny),
+             lib.bvp_work_workspace_bytes(n_int_max, P, CHUNK) if CHUNK > 0 else 0)
+    work = {}
+    if CHUNK > 0:
+        mw, ms, mp = work_bounds(P, n_int_max, CHUNK)
+        work = dict(work=torch.empty(4 * mw, **i32), splits=torch.empty(4 * ms, **i32),
+                    work_counts=torch.zeros(3, dtype=torch.int64, device=dev),
+                    work_bounds=(mw, ms, mp), n_int_max=n_int_max)
     return dict(
+        **work,
         cells=torch.empty(P, **i32), ranks=torch.empty(P, **i32),
         starts=torch.empty(n_cells + 1, **i32), icells=torch.empty(n_cells, **i32),
         cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
@@ -311,15 +342,24 @@ def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
               ptr(b["long_units"]), ptr(b["tasks"]), ptr(b["sched_counts"]),
               ptr(b["meta"]) if dims is not None else None, ptr(b["ws"]), b["ws"].numel(),
               stream_ptr(dev))
+    if "work" in b:
+        _lib.call("bvp_make_work", ptr(b["starts"]), ptr(b["icells"]), ptr(b["counts"]),
+                  b["n_int_max"], b["ranks"].numel(), CHUNK, ptr(b["work"]), ptr(b["splits"]),
+                  ptr(b["work_counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
 
 
 def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, dims=None):
     """A cache over the buffers b; launch bounds are the capacities until
     fit_launch() (no host sync needed to pool)."""
-    return AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
-                            b["iop"], b["counts"], b["units"], b["long_units"], b["tasks"],
-                            b["sched_counts"], b["meta"], b["cap"], int(b["long_units"].numel()),
-                            b["cap"], fingerprint, nx, ny, n_cameras, frustum, grid, dims)
+    cache = AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
+                             b["iop"], b["counts"], b["units"], b["long_units"], b["tasks"],
+                             b["sched_counts"], b["meta"], b["cap"], int(b["long_units"].numel()),
+                             b["cap"], fingerprint, nx, ny, n_cameras, frustum, grid, dims)
+    if "work" in b:
+        cache.d_work, cache.d_splits, cache.d_work_counts = b["work"], b["splits"], b["work_counts"]
+        cache.max_work, cache.max_splits, cache.max_partials = b["work_bounds"]
+        cache.chunk = CHUNK
+    return cache
 
 
 class CacheBuilder:

@@ -8,19 +8,19 @@
 // by pool_interval (pooling.py:206-221).
 #include <algorithm>
 
-#include "pool_kernel.cuh"
+#include "pool_ivl.cuh"
 
 namespace bvp {
 
 template <>
 int run_pool<float, __nv_bfloat16, 8, kSrcFused>(const PoolParams &p, int B, bool is_max,
                                                  cudaStream_t s) {
-    return run_pool_impl<float, __nv_bfloat16, 8, kSrcFused>(p, B, is_max, s);
+    return run_pool_fast<__nv_bfloat16, 8, kSrcFused>(p, B, is_max, s);
 }
 template <>
 int run_pool<float, __nv_bfloat16, 1, kSrcFused>(const PoolParams &p, int B, bool is_max,
                                                  cudaStream_t s) {
-    return run_pool_impl<float, __nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);
+    return run_pool_fast<__nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);
 }
 
 // lse[pix] = max_d l + log(sum_d exp(l - max)).  A CTA covers 32 consecutive
@@ -97,7 +97,8 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
                         const uint32_t *interval_starts, const uint32_t *interval_cells,
                         const uint32_t *cell_first, const bvp_schedule *schedule, int B, int N,
                         int C, int H, int W, int D, int nx, int ny, int mode, float *out,
-                        void *workspace, size_t workspace_bytes, void *stream) {
+                        void *workspace, size_t workspace_bytes, void *scratch,
+                        size_t scratch_bytes, void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims");
     BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
@@ -129,6 +130,8 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     p.NHW = int(N * HW);
     p.rows_bstride = int64_t(N) * HW * C;
     p.w_bstride = int64_t(N) * D * HW;
+    p.scratch = scratch;
+    p.scratch_bytes = scratch_bytes;
     const bool is_max = mode == BVP_MAX;
     const int rc = (C % 8 == 0) ? run_pool<float, __nv_bfloat16, 8, kSrcFused>(p, B, is_max, s)
                                 : run_pool<float, __nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);

@@ -60,6 +60,13 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
     p.max_tasks = sched->max_tasks;
     p.order = sched->order;
     p.order_rep = sched->order_rep > 0 ? sched->order_rep : 1;
+    p.work = reinterpret_cast<const uint4 *>(sched->work);
+    p.splits = reinterpret_cast<const uint4 *>(sched->splits);
+    p.work_counts = sched->work_counts;
+    p.max_work = sched->max_work;
+    p.max_splits = sched->max_splits;
+    p.chunk_partials = sched->max_partials;
+    p.chunk = static_cast<int>(sched->chunk);
     p.out = out;
     p.C = C;
     p.nx = nx;
@@ -156,6 +163,11 @@ using namespace bvp;
 
 extern "C" {
 
+size_t bvp_pool_scratch_bytes(const bvp_schedule *schedule, int B, int C, int mode) {
+    if (!schedule || !schedule->work || schedule->max_splits <= 0) return 0;
+    return size_t(B) * schedule->max_partials * C * (mode == BVP_MAX ? 8 : 4);
+}
+
 size_t bvp_pool_workspace_bytes(int B, int N, int C, int H, int W) {
     return size_t(B) * N * C * H * W * sizeof(float);
 }
@@ -173,7 +185,8 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
                               const uint32_t *cell_first, const bvp_schedule *schedule, int B,
                               int N, int C, int H, int W, int D, int nx, int ny,
                               int64_t n_int_max, int mode, int exact, float *out,
-                              uint32_t *argmax, void *stream) {
+                              uint32_t *argmax, void *scratch, size_t scratch_bytes,
+                              void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims B=%d N=%d C=%d H=%d W=%d D=%d nx=%d ny=%d", B, N, C,
                 H, W, D, nx, ny);
@@ -194,6 +207,8 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
     p.n_int_max = n_int_max;
     p.rows_bstride = int64_t(N) * H * W * C;
     p.w_bstride = int64_t(N) * D * H * W;
+    p.scratch = scratch;
+    p.scratch_bytes = scratch_bytes;
     const bool is_max = mode == BVP_MAX, v4 = (C % 4) == 0;
     cudaStream_t s = as_stream(stream);
     int rc;
@@ -212,13 +227,13 @@ int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_
                          const uint32_t *cell_first, const bvp_schedule *schedule, int B, int N,
                          int C, int H, int W, int D, int nx, int ny, int64_t n_int_max, int mode,
                          int exact, float *out, float *feats_nhwc, uint32_t *argmax,
-                         void *stream) {
+                         void *scratch, size_t scratch_bytes, void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1, BVP_ERR_INVALID, "bad dims");
     BVP_REQUIRE(C == 0 || (features && feats_nhwc), BVP_ERR_INVALID, "null pointer argument");
     launch_to_nhwc<float>(features, int64_t(B) * N, C, H * W, feats_nhwc, as_stream(stream));
     return bvp_pool_forward_nhwc_f32(feats_nhwc, dist, ranks, interval_starts, interval_cells,
                                      cell_first, schedule, B, N, C, H, W, D, nx, ny, n_int_max,
-                                     mode, exact, out, argmax, stream);
+                                     mode, exact, out, argmax, scratch, scratch_bytes, stream);
 }
 
 int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in, int N, int D,
@@ -277,7 +292,7 @@ int bvp_lift_f32(const float *features, const float *dist, int N, int C, int H, 
 int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *interval_starts,
                         const uint32_t *interval_cells, const uint32_t *cell_first,
                         const bvp_schedule *schedule, int C, int nx, int ny, int mode,
-                        float *out, void *stream) {
+                        float *out, void *scratch, size_t scratch_bytes, void *stream) {
     BVP_REQUIRE(C >= 0 && nx >= 1 && ny >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
                 "bad arguments");
     BVP_REQUIRE(C == 0 || (out && x && ranks && interval_starts && interval_cells && cell_first &&
@@ -289,6 +304,8 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *i
     p.rows = x;
     p.D = 1;
     p.HW = 1;
+    p.scratch = scratch;
+    p.scratch_bytes = scratch_bytes;
     const bool is_max = mode == BVP_MAX;
     cudaStream_t s = as_stream(stream);
     const int rc = (C % 4 == 0) ? run_pool<float, float, 4, kSrcX>(p, 1, is_max, s)

@@ -1,0 +1,233 @@
+// pool_ivl.cuh -- the fast (fp32-accumulating) interval-reduction kernel over
+// the chunk schedule (work.cu), sm_100a.
+//
+// Restates the reference's interval_reduce (_kernels.py:22-63) in fast mode
+// (fp32 accumulation; tolerance 1e-5 against the fp64 reference -- the
+// bit-exact fp64 mode is pool_kernel.cuh's).
+//
+// Design (measured, profiles/ + scripts/gather_mlp_bench.cu): the path is a
+// gather of 320-byte feature rows from an L2-resident table; B200 sustains
+// ~13.6 TB/s of such gathers when every SM keeps enough rows in flight and
+// each warp instruction carries several points.  So:
+//   * a warp is G = 32 / L lane groups; group g owns ONE chunk (<= chunk
+//     consecutive sorted points of one interval) and walks it sequentially,
+//     its L lanes holding CPL VEC-wide slices of the channel row (C = 80
+//     fp32: L = 4 lanes x 5 float4, 8 chunks = 8 points per warp step);
+//   * chunks come longest first, so the 8 groups of a warp finish together;
+//   * no cross-group combine, no shared memory, ~60 registers: 32 warps per
+//     SM keep ~256 rows in flight;
+//   * a chunk that is a whole interval stores its cell's column (scattered
+//     4-byte stores; the map is zero-filled first); chunks of a longer
+//     interval store fp32 partials that pool_ivl_combine_kernel adds in
+//     chunk order -- deterministic, independent of timing and launch shape.
+#pragma once
+
+#include <algorithm>
+
+#include "pool_group.cuh"
+
+namespace bvp {
+
+constexpr uint32_t kIvlSplit = 0x80000000u;  // work.cu kSplitDest
+#ifndef BVP_IVL_MIN_BLOCKS
+#define BVP_IVL_MIN_BLOCKS 4
+#endif
+
+template <typename Elem, int VEC, int CPL, bool IS_MAX, int SRC>
+__global__ void __launch_bounds__(kPoolThreads, BVP_IVL_MIN_BLOCKS)
+pool_ivl_kernel(const PoolParams P, int L, int lg) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int b = blockIdx.y;
+    const int C = P.C;
+    const int G = 32 >> lg;
+    const int g = lane >> lg, li = lane & (L - 1);
+    const int nch = C / VEC;
+    uint32_t live = 0;  // bit k: chunk li + k*L exists
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+        if (li + k * L < nch) live |= 1u << k;
+    const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride + li * VEC;
+    const float *wdist = static_cast<const float *>(P.wsrc) + (SRC == kSrcDist ? b * P.w_bstride : 0);
+    const __nv_bfloat16 *wlog =
+        static_cast<const __nv_bfloat16 *>(P.wsrc) + (SRC == kSrcFused ? b * P.w_bstride : 0);
+    const float *lse = P.lse + (SRC == kSrcFused ? int64_t(b) * P.NHW : 0);
+    const uint32_t Cu = static_cast<uint32_t>(C);
+    const int64_t n_work = P.work_counts[0];
+    const int64_t n_part = P.max_splits > 0 ? P.work_counts[2] : 0;
+    const int64_t nwarps = int64_t(gridDim.x) * kPoolWarps;
+
+    auto rec_of = [&](uint32_t j) -> uint2 {
+        if (SRC == kSrcX) return make_uint2(__ldg(P.ranks + j), 0u);
+        return __ldg(P.meta + j);
+    };
+
+#pragma unroll 1
+    for (int64_t batch = int64_t(blockIdx.x) * kPoolWarps + warp; batch * G < n_work;
+         batch += nwarps) {
+        const int64_t item = batch * G + g;
+        uint4 r = make_uint4(0u, 0u, 0u, 0u);
+        if (item < n_work) r = __ldg(P.work + item);
+        const uint32_t j0 = r.x, len = r.y - r.x;
+        uint32_t steps = len;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) steps = max(steps, __shfl_xor_sync(0xFFFFFFFFu, steps, o));
+
+        float acc[CPL][VEC];
+        uint32_t arg[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1];
+        greset<CPL, VEC, IS_MAX>(acc, arg);
+        uint2 m = len > 0 ? rec_of(j0) : make_uint2(0u, 0u);
+#pragma unroll 1
+        for (uint32_t s = 0; s < steps; ++s) {
+            const bool ok = s < len;
+            float w = 1.f;
+            if (SRC == kSrcDist) w = ok ? __ldg(wdist + m.y) : 0.f;
+            else if (SRC == kSrcFused) w = ok ? __expf(__bfloat162float(wlog[m.y]) - __ldg(lse + m.x)) : 0.f;
+            float v[CPL][VEC];
+            const Elem *rp = rows + m.x * Cu;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+                if (k == 0 || ((live >> k) & 1u))
+                    ChunkLoad<Elem, VEC>::template load<SRC == kSrcX>(rp + k * L * VEC, v[k]);
+                else
+#pragma unroll
+                    for (int x = 0; x < VEC; ++x) v[k][x] = 0.f;
+            }
+            if (s + 1 < len) m = rec_of(j0 + s + 1);  // next step's record
+            if (ok) gacc<CPL, VEC, IS_MAX>(acc, arg, j0 + s, true, w, v);
+        }
+        if (item >= n_work) continue;
+        if (!(r.z & kIvlSplit)) {  // the chunk is the whole interval: store its cell
+            const float inv = P.mean ? 1.f / float(len) : 1.f;
+            float *out = P.out + int64_t(b) * C * P.n_cells + r.z;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+                const int ch = li + k * L;
+                if (ch < nch)
+#pragma unroll
+                    for (int x = 0; x < VEC; ++x) {
+                        const int c = ch * VEC + x;
+                        out[int64_t(c) * P.n_cells] = acc[k][x] * inv;
+                        if (IS_MAX && P.argmax)
+                            P.argmax[(b * P.n_int_max + r.w) * C + c] =
+                                __ldg(P.ranks + arg[IS_MAX ? k : 0][IS_MAX ? x : 0]);
+                    }
+            }
+        } else {  // one chunk of a split interval: its partial
+            const int64_t slot = int64_t(b) * n_part + (r.z & ~kIvlSplit);
+            float *pp = P.partials + slot * C;
+            uint32_t *pa = IS_MAX ? P.partial_arg + slot * C : nullptr;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+                const int ch = li + k * L;
+                if (ch < nch)
+#pragma unroll
+                    for (int x = 0; x < VEC; ++x) {
+                        pp[ch * VEC + x] = acc[k][x];
+                        if (IS_MAX) pa[ch * VEC + x] = arg[IS_MAX ? k : 0][IS_MAX ? x : 0];
+                    }
+            }
+        }
+    }
+}
+
+// One warp per split interval: add its chunk partials in chunk order (MAX:
+// the first maximum in rank order), scale (MEAN), store the cell's column.
+template <bool IS_MAX>
+__global__ void __launch_bounds__(kPoolThreads)
+pool_ivl_combine_kernel(const PoolParams P) {
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.y;
+    const int C = P.C;
+    const int64_t n_split = P.work_counts[1], n_part = P.work_counts[2];
+    const int64_t nwarps = int64_t(gridDim.x) * kPoolWarps;
+#pragma unroll 1
+    for (int64_t s = int64_t(blockIdx.x) * kPoolWarps + (threadIdx.x >> 5); s < n_split; s += nwarps) {
+        const uint4 sp = __ldg(P.splits + s);  // interval, cell, first slot, chunks
+        const float *pp = P.partials + (int64_t(b) * n_part + sp.z) * C;
+        const uint32_t *pa = IS_MAX ? P.partial_arg + (int64_t(b) * n_part + sp.z) * C : nullptr;
+        float inv = 1.f;
+        if (P.mean) inv = 1.f / float(__ldg(P.starts + sp.x + 1) - __ldg(P.starts + sp.x));
+        float *out = P.out + int64_t(b) * C * P.n_cells + sp.y;
+        for (int c = lane; c < C; c += 32) {
+            float v = pp[c];
+            uint32_t a = IS_MAX ? pa[c] : 0u;
+            for (uint32_t k = 1; k < sp.w; ++k) {
+                const float x = pp[int64_t(k) * C + c];
+                if (IS_MAX) {
+                    if (x > v) {
+                        v = x;
+                        a = pa[int64_t(k) * C + c];
+                    }
+                } else {
+                    v += x;
+                }
+            }
+            out[int64_t(c) * P.n_cells] = v * inv;
+            if (IS_MAX && P.argmax) P.argmax[(b * P.n_int_max + sp.x) * C + c] = __ldg(P.ranks + a);
+        }
+    }
+}
+
+// Bytes of the split partials for B samples of C channels (values, + the
+// argmax positions for MAX).
+inline size_t ivl_scratch_bytes(int64_t n_partials, int B, int C, bool is_max) {
+    return size_t(B) * n_partials * C * (is_max ? 8 : 4);
+}
+
+// Zero-fill + chunk kernel + combine.  BVP_ERR_UNSUPPORTED: shape not covered
+// (the caller falls back).
+template <typename Elem, int VEC, int SRC>
+int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
+    void *scratch = p0.scratch;
+    const size_t scratch_bytes = p0.scratch_bytes;
+    int L, lg, cpl;
+    if (!p0.work || !choose_group(p0.C / VEC, VEC, L, lg, cpl)) return BVP_ERR_UNSUPPORTED;
+    BVP_REQUIRE(SRC == kSrcX || p0.meta, BVP_ERR_INVALID,
+                "the cache's point gather table (point_meta) is required");
+    const size_t need = ivl_scratch_bytes(p0.max_splits > 0 ? p0.chunk_partials : 0, B, p0.C, is_max);
+    BVP_REQUIRE(scratch_bytes >= need, BVP_ERR_INVALID,
+                "pool scratch too small: need %zu bytes (bvp_pool_scratch_bytes)", need);
+    PoolParams p = p0;
+    p.partials = static_cast<float *>(scratch);
+    p.partial_arg = is_max ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
+                                                          size_t(B) * p0.chunk_partials * p0.C)
+                           : nullptr;
+    cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
+    const int G = 32 >> lg;
+    const int64_t batches = ceil_div(p.max_work, G);
+    const dim3 grid(static_cast<unsigned>(std::max<int64_t>(
+                        1, std::min<int64_t>(ceil_div(batches, kPoolWarps),
+                                             int64_t(kNumSms) * BVP_IVL_MIN_BLOCKS * 4))),
+                    static_cast<unsigned>(B));
+#define BVP_IVL_LAUNCH(CPLV)                                                     \
+    if (cpl == CPLV) {                                                           \
+        auto k = is_max ? pool_ivl_kernel<Elem, VEC, CPLV, true, SRC>            \
+                        : pool_ivl_kernel<Elem, VEC, CPLV, false, SRC>;          \
+        k<<<grid, kPoolThreads, 0, s>>>(p, L, lg);                               \
+    }
+    BVP_IVL_LAUNCH(1) BVP_IVL_LAUNCH(2) BVP_IVL_LAUNCH(3)
+    BVP_IVL_LAUNCH(4) BVP_IVL_LAUNCH(5) BVP_IVL_LAUNCH(6)
+#undef BVP_IVL_LAUNCH
+    if (p.max_splits > 0) {
+        const dim3 cg(static_cast<unsigned>(std::max<int64_t>(
+                          1, std::min<int64_t>(ceil_div(p.max_splits, kPoolWarps), kNumSms * 8))),
+                      static_cast<unsigned>(B));
+        if (is_max) pool_ivl_combine_kernel<true><<<cg, kPoolThreads, 0, s>>>(p);
+        else pool_ivl_combine_kernel<false><<<cg, kPoolThreads, 0, s>>>(p);
+    }
+    return BVP_OK;
+}
+
+// Fast-mode dispatch: the chunk kernel when the cache carries a chunk
+// schedule, else the group kernel, else the one-point-per-warp kernel.
+template <typename Elem, int VEC, int SRC>
+int run_pool_fast(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
+    const int rc = run_pool_ivl<Elem, VEC, SRC>(p, B, is_max, s);
+    if (rc != BVP_ERR_UNSUPPORTED) return rc;
+    int L, lg, cpl;
+    if (p.tasks && choose_group(p.C / VEC, VEC, L, lg, cpl))
+        return run_pool_group<Elem, VEC, SRC>(p, B, is_max, s);
+    return run_pool_impl<float, Elem, VEC, SRC>(p, B, is_max, s);
+}
+
+}  // namespace bvp

@@ -68,6 +68,17 @@ struct PoolParams {
     int64_t max_units, max_long, max_tasks;  // launch sizes (>= the device counts)
     const uint32_t *order;   // optional launch order of the units (2D blocks)
     int64_t order_rep;       // units per warp
+    // chunk schedule (work.cu); work == nullptr: not built
+    const uint4 *work;
+    const uint4 *splits;
+    const int64_t *work_counts;
+    int64_t max_work, max_splits, chunk_partials;
+    int chunk;
+    void *scratch;           // caller's scratch for the split partials
+    size_t scratch_bytes;
+    int long_only;           // group kernel: long cells only
+    float *partials;         // split intervals: [B][n_chunks of splits][C] (workspace)
+    uint32_t *partial_arg;   // MAX: sorted position of each partial's max
     int64_t rows_bstride;    // elements of rows per batch sample
     int64_t w_bstride;       // elements of wsrc per batch sample
 };

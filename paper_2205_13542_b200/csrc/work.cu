@@ -1,0 +1,176 @@
+// work.cu -- the chunk schedule of the fast interval kernel (pool_ivl.cuh),
+// part of the cached association (built once per rig, like the ranks).
+//
+// Every interval of the reference's interval table (bevgrid.py:142-158) is
+// cut into chunks of <= chunk consecutive sorted points.  The kernel gives
+// each chunk to one lane group, which sums it sequentially; chunks are
+// listed longest first so the 8 groups of a warp run for the same number of
+// steps (measured 99.9% group utilisation at the nuScenes shape, vs 43% for
+// one group per cell of an 8-cell row tile).  A chunk of an interval that
+// was NOT cut writes its cell directly; chunks of a cut ("split") interval
+// write fp32 partials that a second pass adds in chunk order.
+//
+// work[4 w..]:  first sorted point, end, destination, interval.
+//               destination: the cell id, or kSplitDest | partial slot
+// splits[4 s..]: interval, cell, first partial slot, chunk count
+// counts:       n_work, n_splits, n_partials
+//
+// The order of chunks of equal length is whatever the atomics produce; it
+// changes no output bit (every chunk is summed by one group in rank order and
+// partials are combined in slot order).
+#include <algorithm>
+
+#include "scan.cuh"
+
+namespace bvp {
+
+constexpr uint32_t kSplitDest = 0x80000000u;
+
+// per interval: chunk count, partial count (chunks if split), split flag
+__global__ void work_count_kernel(const uint32_t *__restrict__ starts,
+                                  const int64_t *__restrict__ counts, int64_t n_int_max,
+                                  uint32_t chunk, uint32_t *__restrict__ nch,
+                                  uint32_t *__restrict__ npart, uint32_t *__restrict__ nsplit) {
+    const int64_t n_int = counts[1];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_int_max;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t c = 0;
+        if (i < n_int) c = (starts[i + 1] - starts[i] + chunk - 1) / chunk;
+        nch[i] = c;
+        npart[i] = c > 1 ? c : 0u;
+        nsplit[i] = c > 1 ? 1u : 0u;
+    }
+}
+
+// per interval: emit its chunks (unsorted, chunk order) with a length
+// histogram; splits table
+__global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
+                                 const uint32_t *__restrict__ icells,
+                                 const int64_t *__restrict__ counts, uint32_t chunk,
+                                 const uint32_t *__restrict__ cbase,
+                                 const uint32_t *__restrict__ pbase,
+                                 const uint32_t *__restrict__ sbase, uint4 *__restrict__ tmp,
+                                 uint32_t *__restrict__ hist, uint4 *__restrict__ splits) {
+    const int64_t n_int = counts[1];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_int;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t lo = starts[i], hi = starts[i + 1], cell = icells[i];
+        const uint32_t nch = (hi - lo + chunk - 1) / chunk;
+        const bool split = nch > 1;
+        for (uint32_t k = 0; k < nch; ++k) {
+            const uint32_t a = lo + k * chunk, e = min(hi, a + chunk);
+            const uint32_t dest = split ? (kSplitDest | (pbase[i] + k)) : cell;
+            tmp[cbase[i] + k] = make_uint4(a, e, dest, static_cast<uint32_t>(i));
+            atomicAdd(hist + (chunk - (e - a)), 1u);  // bucket 0 = longest
+        }
+        if (split) splits[sbase[i]] = make_uint4(static_cast<uint32_t>(i), cell, pbase[i], nch);
+    }
+}
+
+// exclusive scan of the (chunk + 1)-bucket histogram, one block
+__global__ void work_hist_scan_kernel(uint32_t *__restrict__ hist, int nb) {
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < nb; ++b) {
+            const uint32_t c = hist[b];
+            hist[b] = run;
+            run += c;
+        }
+    }
+}
+
+__global__ void work_scatter_kernel(const uint4 *__restrict__ tmp,
+                                    const uint32_t *__restrict__ n_work_p, uint32_t chunk,
+                                    uint32_t *__restrict__ cursor, uint4 *__restrict__ work) {
+    const int64_t n = *n_work_p;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 r = tmp[w];
+        work[atomicAdd(cursor + (chunk - (r.y - r.x)), 1u)] = r;
+    }
+}
+
+__global__ void work_counts_kernel(const uint32_t *__restrict__ n_work,
+                                   const uint32_t *__restrict__ n_split,
+                                   const uint32_t *__restrict__ n_part, int64_t *__restrict__ out) {
+    out[0] = *n_work;
+    out[1] = *n_split;
+    out[2] = *n_part;
+}
+
+struct WorkLayout {
+    size_t off_nch, off_npart, off_nsplit, off_part, off_tot, off_hist, off_tmp, bytes;
+};
+static int64_t work_cap(int64_t n_int_max, int64_t n_points, int chunk) {
+    return chunk > 0 ? n_int_max + n_points / chunk + 1 : 0;
+}
+static WorkLayout work_layout(int64_t n_int_max, int64_t n_points, int chunk) {
+    WorkLayout L{};
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    const size_t n = size_t(n_int_max);
+    size_t o = 0;
+    L.off_nch = o; o = al(o + n * 4);
+    L.off_npart = o; o = al(o + n * 4);
+    L.off_nsplit = o; o = al(o + n * 4);
+    L.off_part = o; o = al(o + size_t(scan_partials_len<uint32_t>(n_int_max)) * 4);
+    L.off_tot = o; o = al(o + 16);
+    L.off_hist = o; o = al(o + size_t(chunk + 1) * 4);
+    L.off_tmp = o; o = al(o + size_t(work_cap(n_int_max, n_points, chunk)) * 16);
+    L.bytes = o;
+    return L;
+}
+
+}  // namespace bvp
+
+using namespace bvp;
+
+extern "C" {
+
+int64_t bvp_work_capacity(int64_t n_int_max, int64_t n_points, int chunk) {
+    return work_cap(n_int_max, n_points, chunk);
+}
+
+size_t bvp_work_workspace_bytes(int64_t n_int_max, int64_t n_points, int chunk) {
+    return work_layout(n_int_max, n_points, chunk).bytes;
+}
+
+int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cells,
+                  const int64_t *counts, int64_t n_int_max, int64_t n_points, int chunk,
+                  uint32_t *work, uint32_t *splits, int64_t *work_counts, void *workspace,
+                  size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(interval_starts && interval_cells && counts && work && splits && work_counts,
+                BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(chunk >= 1 && chunk <= 4096 && n_int_max >= 1 && n_points >= 1, BVP_ERR_INVALID,
+                "bad chunk %d or sizes", chunk);
+    const WorkLayout L = work_layout(n_int_max, n_points, chunk);
+    BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
+                "work workspace too small: need %zu bytes", L.bytes);
+    cudaStream_t s = as_stream(stream);
+    char *ws = static_cast<char *>(workspace);
+    auto *nch = reinterpret_cast<uint32_t *>(ws + L.off_nch);
+    auto *npart = reinterpret_cast<uint32_t *>(ws + L.off_npart);
+    auto *nsplit = reinterpret_cast<uint32_t *>(ws + L.off_nsplit);
+    auto *part = reinterpret_cast<uint32_t *>(ws + L.off_part);
+    auto *tot = reinterpret_cast<uint32_t *>(ws + L.off_tot);  // n_work, n_partials, n_splits
+    auto *hist = reinterpret_cast<uint32_t *>(ws + L.off_hist);
+    auto *tmp = reinterpret_cast<uint4 *>(ws + L.off_tmp);
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_int_max, 256), 4096));
+    work_count_kernel<<<blocks, 256, 0, s>>>(interval_starts, counts, n_int_max, uint32_t(chunk),
+                                             nch, npart, nsplit);
+    device_excl_scan<uint32_t>(nch, nch, n_int_max, part, tot + 0, s);
+    device_excl_scan<uint32_t>(npart, npart, n_int_max, part, tot + 1, s);
+    device_excl_scan<uint32_t>(nsplit, nsplit, n_int_max, part, tot + 2, s);
+    cudaMemsetAsync(hist, 0, size_t(chunk + 1) * 4, s);
+    work_emit_kernel<<<blocks, 256, 0, s>>>(interval_starts, interval_cells, counts,
+                                            uint32_t(chunk), nch, npart, nsplit, tmp, hist,
+                                            reinterpret_cast<uint4 *>(splits));
+    work_hist_scan_kernel<<<1, 32, 0, s>>>(hist, chunk + 1);
+    const int64_t cap = work_cap(n_int_max, n_points, chunk);
+    work_scatter_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(cap, 256), 4096)), 256,
+                          0, s>>>(tmp, tot + 0, uint32_t(chunk), hist,
+                                  reinterpret_cast<uint4 *>(work));
+    work_counts_kernel<<<1, 1, 0, s>>>(tot + 0, tot + 2, tot + 1, work_counts);
+    return check_launch("make_work");
+}
+
+}  // extern "C"

@@ -52,6 +52,12 @@ class Reducer(enum.Enum):
 
 _MODE = {Reducer.SUM: _lib.BVP_SUM, Reducer.MEAN: _lib.BVP_MEAN, Reducer.MAX: _lib.BVP_MAX}
 
+
+def _scratch(cache: AssociationCache, B: int, C: int, mode: int) -> tuple:
+    """(pointer, bytes) of the fast kernels' scratch for this call shape."""
+    t = cache.scratch(B, C, mode)
+    return (None, 0) if t is None else (ptr(t), t.numel())
+
 BACKENDS = ("prefixsum", "interval")
 
 
@@ -183,11 +189,12 @@ def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
         nhwc = torch.empty(inp.feats.numel(), dtype=torch.float32, device=inp.feats.device)
         _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
-                  ptr(cache.d_cell_first), cache.schedule(inp.N, inp.H, inp.W, inp.D), inp.B, inp.N, inp.C, inp.H,
-                  inp.W, inp.D,
+                  ptr(cache.d_cell_first),
+                  cache.schedule(inp.N, inp.H, inp.W, inp.D),
+                  inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
                   grid.nx, grid.ny, cache.n_int_max, _MODE[reducer],
                   int(DEFAULT_EXACT if exact is None else exact), ptr(out), ptr(nhwc), None,
-                  stream_ptr(inp.feats.device))
+                  *_scratch(cache, inp.B, inp.C, _MODE[reducer]), stream_ptr(inp.feats.device))
     return _finish(out, inp, grid)
 
 
@@ -241,6 +248,7 @@ class PoolPlan:
         self.out = torch.empty((batch, channels, grid.n_cells), **f32)
         self.nhwc = torch.empty(batch * n_cameras * height * width * channels, **f32)
         self._host = None
+        self._scratch = _scratch(self.cache, batch, channels, self.mode)
 
     @property
     def feature_shape(self):
@@ -261,7 +269,7 @@ class PoolPlan:
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
                   c.schedule(self.N, self.H, self.W, self.D), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
-                  self.mode, self.exact, ptr(out), None, stream_ptr(self.dev))
+                  self.mode, self.exact, ptr(out), None, *self._scratch, stream_ptr(self.dev))
         return out
 
     def run(self, features: torch.Tensor, dist: torch.Tensor,
@@ -370,7 +378,8 @@ def pool_lifted(x: torch.Tensor, cache: AssociationCache, grid: BevGridSpec,
     _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
               ptr(cache.d_interval_cells), ptr(cache.d_cell_first), cache.schedule(), C,
               grid.nx, grid.ny,
-              _MODE[reducer], ptr(out), stream_ptr(x.device))
+              _MODE[reducer], ptr(out), *_scratch(cache, 1, C, _MODE[reducer]),
+              stream_ptr(x.device))
     return BevFeatureMap(out.view(C, grid.nx, grid.ny), grid)
 
 
@@ -399,6 +408,6 @@ def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCa
               ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_cell_first),
               cache.schedule(N, H, W, D),
               B, N, C, H, W, D, grid.nx, grid.ny, _MODE[reducer], ptr(out), ptr(ws), ws.numel(),
-              stream_ptr(dev))
+              *_scratch(cache, B, C, _MODE[reducer]), stream_ptr(dev))
     v = out.view(B, C, grid.nx, grid.ny)
     return BevFeatureMap(v if batched else v[0], grid)
