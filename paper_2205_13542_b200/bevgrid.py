@@ -123,7 +123,7 @@ UNIT_BUDGET = 128
 #: points per warp task (a run of consecutive units walked as one stream)
 TASK_BUDGET = 384
 #: chunk length of the fast kernels' work list (csrc/work.cu); 0 disables it
-CHUNK = int(os.environ.get("BVP_CHUNK", "32"))
+CHUNK = int(os.environ.get("BVP_CHUNK", "64"))
 
 
 def work_bounds(n_points: int, n_int_max: int, chunk: int) -> tuple[int, int, int]:

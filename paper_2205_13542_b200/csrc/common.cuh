@@ -52,6 +52,13 @@ __device__ __forceinline__ float4 ldg_stream_f4(const float *p) {
                  : "l"(p));
     return r;
 }
+__device__ __forceinline__ uint4 ldg_stream_u4(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
 __device__ __forceinline__ void st_stream_f4(float *p, float4 v) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x),
                  "f"(v.y), "f"(v.z), "f"(v.w)

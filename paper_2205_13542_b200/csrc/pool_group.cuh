@@ -60,7 +60,7 @@ template <>
 struct ChunkLoad<__nv_bfloat16, 8> {
     template <bool STREAM>
     __device__ __forceinline__ static void load(const __nv_bfloat16 *p, float (&v)[8]) {
-        const uint4 t = __ldg(reinterpret_cast<const uint4 *>(p));
+        const uint4 t = STREAM ? ldg_stream_u4(p) : __ldg(reinterpret_cast<const uint4 *>(p));
         const uint32_t w[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {

@@ -30,7 +30,7 @@ namespace bvp {
 
 constexpr uint32_t kIvlSplit = 0x80000000u;  // work.cu kSplitDest
 #ifndef BVP_IVL_MIN_BLOCKS
-#define BVP_IVL_MIN_BLOCKS 4
+#define BVP_IVL_MIN_BLOCKS 3
 #endif
 
 template <typename Elem, int VEC, int CPL, bool IS_MAX, int SRC>
@@ -75,14 +75,14 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
         float acc[CPL][VEC];
         uint32_t arg[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1];
         greset<CPL, VEC, IS_MAX>(acc, arg);
+        // rows of two steps in flight: fetch(s + 1) is issued before the
+        // FMAs of step s; each fetch also loads the next step's record
         uint2 m = len > 0 ? rec_of(j0) : make_uint2(0u, 0u);
-#pragma unroll 1
-        for (uint32_t s = 0; s < steps; ++s) {
+        auto fetch = [&](uint32_t s, float &w, float (&v)[CPL][VEC]) {
             const bool ok = s < len;
-            float w = 1.f;
+            w = 1.f;
             if (SRC == kSrcDist) w = ok ? __ldg(wdist + m.y) : 0.f;
             else if (SRC == kSrcFused) w = ok ? __expf(__bfloat162float(wlog[m.y]) - __ldg(lse + m.x)) : 0.f;
-            float v[CPL][VEC];
             const Elem *rp = rows + m.x * Cu;
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
@@ -92,8 +92,17 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) v[k][x] = 0.f;
             }
-            if (s + 1 < len) m = rec_of(j0 + s + 1);  // next step's record
-            if (ok) gacc<CPL, VEC, IS_MAX>(acc, arg, j0 + s, true, w, v);
+            if (s + 1 < len) m = rec_of(j0 + s + 1);
+        };
+        float wa, wb, va[CPL][VEC], vb[CPL][VEC];
+        if (steps > 0) fetch(0, wa, va);
+#pragma unroll 1
+        for (uint32_t s = 0; s < steps; s += 2) {
+            if (s + 1 < steps) fetch(s + 1, wb, vb);
+            if (s < len) gacc<CPL, VEC, IS_MAX>(acc, arg, j0 + s, true, wa, va);
+            if (s + 1 >= steps) break;
+            if (s + 2 < steps) fetch(s + 2, wa, va);
+            if (s + 1 < len) gacc<CPL, VEC, IS_MAX>(acc, arg, j0 + s + 1, true, wb, vb);
         }
         if (item >= n_work) continue;
         if (!(r.z & kIvlSplit)) {  // the chunk is the whole interval: store its cell
@@ -151,7 +160,25 @@ pool_ivl_combine_kernel(const PoolParams P) {
         for (int c = lane; c < C; c += 32) {
             float v = pp[c];
             uint32_t a = IS_MAX ? pa[c] : 0u;
-            for (uint32_t k = 1; k < sp.w; ++k) {
+            uint32_t k = 1;
+            // 4 independent loads in flight, added in chunk order
+            for (; k + 4 <= sp.w; k += 4) {
+                float x[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) x[q] = pp[int64_t(k + q) * C + c];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (IS_MAX) {
+                        if (x[q] > v) {
+                            v = x[q];
+                            a = pa[int64_t(k + q) * C + c];
+                        }
+                    } else {
+                        v += x[q];
+                    }
+                }
+            }
+            for (; k < sp.w; ++k) {
                 const float x = pp[int64_t(k) * C + c];
                 if (IS_MAX) {
                     if (x > v) {
