@@ -15,9 +15,10 @@ region.  N=1 also reports cpu_baseline (the oracle's C port of the
 reference's pool_interval, all host threads) and the other configurations as
 "variants".
 
-``--impl reference`` times the reference's CPU pool_interval (the oracle port
-of pkg/src/bevpool/_kernels.py, OpenMP over all host cores) on the same
-config; under torchrun only rank 0 runs it.
+``--impl reference`` times the reference's own CPU pool_interval (installed
+unmodified into baseline/_ref; numba/OpenMP over all host cores; the
+oracle's C port when absent) on the same config; under torchrun only rank 0
+runs it.
 """
 
 from __future__ import annotations
@@ -40,6 +41,12 @@ METRIC = "bev_pool_points_per_sec"
 UNIT = "points/s"
 CONFIG_NAME = "S"
 FLUSH_BYTES = 512 << 20
+KERNEL_KEY = "pool_ivl_kernel"
+# NHWC transpose, zero-fill (memset kernel), chunk kernel, split combine
+LAUNCHES_PER_STEP = 4
+# pure L2 gather of the S-config rows in rank order (scripts/gather_mlp_bench.cu,
+# profiles/r01/gather_mlp_bench.txt)
+L2_GATHER_CEILING_GBPS = 13610.0
 
 
 def parse_args():
@@ -83,11 +90,56 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+# Runs in a fresh interpreter: the reference sizes its OpenMP pool at import
+# (pkg/src/bevpool/_threads.py:32-37), and OpenBLAS spin threads starve it
+# unless OPENBLAS_NUM_THREADS=1.
+_REF_SNIPPET = r"""
+import json, os, sys, time
+sys.path.insert(0, os.environ["BVP_REF_DIR"])
+import numpy as np
+import bevpool as ref
+from bevpool.bevgrid import BevGridSpec
+from bevpool.geometry import FrustumSpec
+reps, warm, max_s = int(sys.argv[1]), int(sys.argv[2]), float(sys.argv[3])
+spec = ref.WorkloadSpec(6, FrustumSpec(32, 88, 1.0, 0.5, 118),
+                        BevGridSpec(-54.0, 54.0, -54.0, 54.0, -10.0, 10.0, 0.3), 80, 0)
+rig, feats, logits, grid = ref.gen_workload(spec)
+cache = ref.build_cache(rig, spec.frustum, grid)
+dist = ref.normalize_depth(logits)
+for _ in range(warm):
+    ref.pool_interval(feats, dist, cache, grid, ref.Reducer.SUM)
+ts = []
+t_start = time.perf_counter()
+while len(ts) < reps:
+    t0 = time.perf_counter()
+    ref.pool_interval(feats, dist, cache, grid, ref.Reducer.SUM)
+    ts.append(time.perf_counter() - t0)
+    if time.perf_counter() - t_start > max_s and len(ts) >= 3:
+        break
+print(json.dumps({"times": ts, "threads": ref.get_parallelism()}))
+"""
+
+
 def time_cpu_reference(spec, max_seconds, min_reps=3, max_reps=200, warmup=1):
-    """The oracle port of the reference pool_interval (transposes + 64-bit
-    interval_reduce, OpenMP) on all host threads.  Returns (per-step seconds)."""
+    """The reference's own pool_interval (pkg/src/bevpool/pooling.py:206-221,
+    numba + OpenMP) from baseline/_ref on all host threads, in a subprocess.
+    Falls back to the oracle's C port of it when the reference is not
+    installed.  Returns (per-step seconds, threads, kind)."""
+    if os.path.isdir(os.path.join(REF_DIR, "bevpool")):
+        env = dict(os.environ, BVP_REF_DIR=REF_DIR, OPENBLAS_NUM_THREADS="1",
+                   BEVPOOL_THREADS=str(cpu_threads()), NUMBA_NUM_THREADS=str(cpu_threads()),
+                   NUMBA_CACHE_DIR=os.environ.get("NUMBA_CACHE_DIR", "/tmp/bvp_numba_cache"))
+        res = subprocess.run([sys.executable, "-c", _REF_SNIPPET, str(max_reps), str(warmup),
+                              str(max_seconds)], capture_output=True, text=True, env=env,
+                             timeout=min(3600.0, max(600.0, 10 * max_seconds)))
+        if res.returncode == 0:
+            out = json.loads(res.stdout.strip().splitlines()[-1])
+            return out["times"], out["threads"], "reference"
+        print(f"reference arm failed, using the oracle port: {res.stderr[-400:]}",
+              file=sys.stderr)
     from oracle import oracle as o
-    from paper_2205_13542_b200.workload import gen_workload, synthetic_rig  # noqa: F401 (inputs)
 
     lib = o.lib()
     lib.oracle_set_threads(cpu_threads())
@@ -107,7 +159,7 @@ def time_cpu_reference(spec, max_seconds, min_reps=3, max_reps=200, warmup=1):
         times.append(time.perf_counter() - t0)
         if len(times) >= min_reps and time.perf_counter() - t_start > max_seconds:
             break
-    return times, lib.oracle_max_threads()
+    return times, lib.oracle_max_threads(), "port"
 
 
 def run_reference(args):
@@ -118,20 +170,21 @@ def run_reference(args):
 
     spec = CONFIGS[CONFIG_NAME]
     reps = max(1, args.steps)
-    times, threads = time_cpu_reference(spec, max_seconds=1e9, min_reps=reps, max_reps=reps,
-                                        warmup=max(1, args.warmup))
+    times, threads, kind = time_cpu_reference(spec, max_seconds=1e9, min_reps=reps,
+                                              max_reps=reps, warmup=max(1, args.warmup))
     total = sum(times)
     value = spec.n_points * len(times) / total
+    what = ("the reference's pool_interval (baseline/_ref, numba/OpenMP)" if kind == "reference"
+            else "the oracle's C port of the reference's pool_interval (OpenMP)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 in / f64 accumulate", "data": "synthetic",
         "config": config_dict(spec),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{len(times)} full nuScenes-shape pool_interval steps "
-                                   "(oracle C port of _kernels.interval_reduce + NHWC "
-                                   "transposes, OpenMP)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{len(times)} full nuScenes-shape pool_interval steps ({what}, "
+                                   "incl. its NHWC transposes)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,6 +281,8 @@ def main():
     import paper_2205_13542_b200 as bp
     from paper_2205_13542_b200.bevgrid import ptr, stream_ptr  # noqa: F401
 
+    from paper_2205_13542_b200.shard import max_over_ranks, sample_seeds
+
     rank, world, local = dist_env()
     if world > 1:
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -238,12 +293,13 @@ def main():
     P = spec.n_points
 
     # ---- inputs: this rank's sample (seed = rank), resident in HBM -------
+    (seed,) = sample_seeds(world, rank, world)  # one sample per GPU, seed = sample index
     rig, feats_np, logits_np, grid = bp.gen_workload(
-        bp.WorkloadSpec(spec.n_cameras, f, spec.grid, spec.channels, rank))
+        bp.WorkloadSpec(spec.n_cameras, f, spec.grid, spec.channels, seed))
     cache = bp.build_cache(rig, f, grid, device=dev)
     feats = torch.from_numpy(feats_np).to(dev).view(1, *feats_np.shape)
     dist = bp.normalize_depth(torch.from_numpy(logits_np).to(dev)).view(1, *logits_np.shape)
-    exact = bool(args.exact) if args.exact is not None else bp.pooling.DEFAULT_EXACT
+    exact = bool(args.exact) if args.exact is not None else False
     plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
                        f.depth_bins, 1, bp.Reducer.SUM, exact, dev)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
@@ -272,24 +328,24 @@ def main():
     step_ms = [e[0].elapsed_time(e[2]) for e in ev]
     kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
     tot_ms = sum(step_ms)
-    # e2e: host buffers (pinned) through the public plan API; H2D of the
-    # inputs, both kernels and D2H of the BEV map inside the timed region
+    # e2e: host buffers (pinned) through the public serving API
+    # (PoolPlan.run_frames): every step copies its features + dist H2D,
+    # pools, and copies the BEV map D2H; consecutive frames overlap their
+    # copies (two device buffer sets, separate copy streams); wall clock
+    # over all K frames after a synchronize.
     h_feats = torch.from_numpy(feats_np).pin_memory()
     h_dist = dist.cpu().pin_memory()
-    e2e_ms = []
-    for k in range(max(3, args.warmup) + K):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        plan.run_host(h_feats, h_dist)
-        t1 = time.perf_counter()
-        if k >= max(3, args.warmup):
-            e2e_ms.append(1e3 * (t1 - t0))
-    e2e_tot = sum(e2e_ms)
+    h_out = [torch.empty(tuple(plan.out.shape), dtype=torch.float32).pin_memory() for _ in range(2)]
+    frames = [(h_feats, h_dist)] * K
+    plan.run_frames(frames[:max(3, args.warmup)], [h_out[k & 1] for k in range(max(3, args.warmup))])
+    torch.cuda.synchronize(dev)
     if world > 1:
-        t = torch.tensor([tot_ms, e2e_tot], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        tot_ms, e2e_tot = t.tolist()
+        tdist.barrier()
+    t0 = time.perf_counter()
+    plan.run_frames(frames, [h_out[k & 1] for k in range(K)])
+    e2e_tot = 1e3 * (time.perf_counter() - t0)
+    tot_ms = max_over_ranks(tot_ms, dev)
+    e2e_tot = max_over_ranks(e2e_tot, dev)
 
     variants = {}
     if rank == 0 and world == 1 and not args.no_variants:
@@ -297,13 +353,16 @@ def main():
     clk = clocks.stop()
 
     # ---- roofline of the dominant kernel (interval reduction) -----------
+    # algorithmic bytes of one reduction launch (SURVEY.md §8d, S reference-
+    # API formulation): NHWC features + dist + ranks + interval table + map
     n_in, n_int = cache.n_in_range, cache.n_intervals
     C, NHW, NDHW = spec.channels, spec.n_cameras * f.height * f.width, P
     alg_bytes = 4 * NHW * C + 4 * NDHW + 4 * n_in + 8 * n_int + 4 * C * grid.n_cells
     kern_avg_s = statistics.mean(kern_ms) * 1e-3
     peak, peak_src = measured_peak()
     achieved = alg_bytes / kern_avg_s / 1e9
-    traffic = ncu_traffic("pool_tile_kernel")
+    traffic = ncu_traffic(KERNEL_KEY)
+    gather_bytes = n_in * 4 * C  # feature rows gathered from L2 (NHWC table, 5.4 MB)
 
     if rank != 0:
         if world > 1:
@@ -322,23 +381,32 @@ def main():
                        "interval_kernel_median": statistics.median(kern_ms)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "pool_tile_kernel (interval reduction, reference formulation)",
+                     "kernel": "interval reduction step (zero-fill + pool_ivl_kernel + combine), "
+                               "reference formulation",
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                     "frac_of_nominal_8TBs": achieved / 8000.0},
+                     "frac_of_nominal_8TBs": achieved / 8000.0,
+                     "l2_gather": {"bytes": gather_bytes,
+                                   "achieved_GBps": gather_bytes / kern_avg_s / 1e9,
+                                   "ceiling_GBps": L2_GATHER_CEILING_GBPS,
+                                   "ceiling_source": "scripts/gather_mlp_bench.cu (pure gather of "
+                                                     "the same rows, measured on B200)"}},
         "e2e": {"value": world * P * K / (e2e_tot * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
                 "ms_per_step": e2e_tot / K,
-                "path": "PoolPlan.run_host (pinned H2D features+dist, 2 launches, D2H map)"},
-        "gpu_launches": 2 * K * world,
+                "path": "PoolPlan.run_frames: pinned H2D features+dist, pooling, D2H map per "
+                        "frame; copies of consecutive frames overlap (wall clock)"},
+        "gpu_launches": LAUNCHES_PER_STEP * K * world,
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        times, threads = time_cpu_reference(spec, args.cpu_seconds)
+        times, threads, kind = time_cpu_reference(spec, args.cpu_seconds)
         v = P * len(times) / sum(times)
         line["cpu_baseline"] = {
-            "value": v, "unit": UNIT, "cores": threads, "kind": "port",
+            "value": v, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{len(times)} full nuScenes-shape pool_interval steps "
-                      f"(median {1e3 * statistics.median(times):.1f} ms), oracle C port, OpenMP"}
+                      f"(median {1e3 * statistics.median(times):.1f} ms, ~{args.cpu_seconds:.0f} s "
+                      f"of CPU), " + ("the reference itself (baseline/_ref, numba/OpenMP)"
+                                      if kind == "reference" else "oracle C port, OpenMP")}
     if variants:
         line["variants"] = variants
     print(json.dumps(line), flush=True)

@@ -32,8 +32,10 @@ from .bevgrid import AssociationCache, BevGridSpec, cuda_device, ptr, stream_ptr
 from .errors import ConfigurationError, StaleCacheError, UnsupportedReducerError, ValidationError
 from .lift import any_nonfinite
 
-#: exact (bit-identical, 64-bit) accumulation by default, like the reference
-DEFAULT_EXACT = True
+#: default accumulation: fp32 (fast; within 1.2e-7 of the reference at the
+#: nuScenes shape, bar 1e-5).  exact=True reproduces the reference's 64-bit
+#: interval_reduce bit for bit.
+DEFAULT_EXACT = False
 
 
 class Reducer(enum.Enum):
@@ -303,6 +305,49 @@ class PoolPlan:
         ho.copy_(self.out, non_blocking=True)
         torch.cuda.current_stream(self.dev).synchronize()
         return ho.numpy().reshape(self.B, self.C, self.grid.nx, self.grid.ny)
+
+    def run_frames(self, frames, outputs) -> None:
+        """Serving loop over host frames: frames[k] = (features, dist) pinned
+        CPU tensors of the planned shapes, outputs[k] a pinned CPU tensor of
+        the map's shape.  Frame k's H2D (copy stream), pooling (current
+        stream) and D2H (second copy stream) overlap frame k-1's D2H and
+        frame k+1's H2D through two device buffer sets; returns when every
+        output has landed."""
+        cur = torch.cuda.current_stream(self.dev)
+        if getattr(self, "_pipe", None) is None:
+            f32 = dict(dtype=torch.float32, device=self.dev)
+            self._pipe = dict(
+                h2d=torch.cuda.Stream(self.dev), d2h=torch.cuda.Stream(self.dev),
+                feats=[torch.empty(self.feature_shape, **f32) for _ in range(2)],
+                dist=[torch.empty(self.dist_shape, **f32) for _ in range(2)],
+                out=[torch.empty(tuple(self.out.shape), **f32) for _ in range(2)])
+        pp = self._pipe
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_free = [None, None]  # D2H of the buffer's previous frame done
+        ev_used = [None, None]  # pooling of the buffer's previous frame done
+        for k, ((hf, hd), ho) in enumerate(zip(frames, outputs)):
+            i = k & 1
+            with torch.cuda.stream(pp["h2d"]):
+                if ev_used[i] is not None:
+                    pp["h2d"].wait_event(ev_used[i])
+                pp["feats"][i].copy_(hf.view(self.feature_shape), non_blocking=True)
+                pp["dist"][i].copy_(hd.view(self.dist_shape), non_blocking=True)
+                ev_in[i].record(pp["h2d"])
+            cur.wait_event(ev_in[i])
+            if ev_free[i] is not None:
+                cur.wait_event(ev_free[i])
+            self.run(pp["feats"][i], pp["dist"][i], pp["out"][i])
+            ev_out[i].record(cur)
+            ev_used[i] = torch.cuda.Event()
+            ev_used[i].record(cur)
+            with torch.cuda.stream(pp["d2h"]):
+                pp["d2h"].wait_event(ev_out[i])
+                ho.view(tuple(self.out.shape)).copy_(pp["out"][i], non_blocking=True)
+                ev_free[i] = torch.cuda.Event()
+                ev_free[i].record(pp["d2h"])
+        pp["d2h"].synchronize()
+        cur.synchronize()
 
     @property
     def h2d_bytes(self) -> int:
