@@ -258,7 +258,7 @@ class AssociationCache:
         pool = self._host.setdefault("scratch", {})
         t = pool.get(key)
         if t is None or t.numel() < n:
-            t = torch.empty(n, dtype=torch.uint8, device=self.device)
+            t = torch.zeros(n, dtype=torch.uint8, device=self.device)  # counters start at 0
             pool[key] = t
         return t
 

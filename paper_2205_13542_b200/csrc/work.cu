@@ -10,8 +10,9 @@
 // was NOT cut writes its cell directly; chunks of a cut ("split") interval
 // write fp32 partials that a second pass adds in chunk order.
 //
-// work[4 w..]:  first sorted point, end, destination, interval.
-//               destination: the cell id, or kSplitDest | partial slot
+// work[4 w..]:  first sorted point, end, destination, interval (split chunks:
+//               split index).  destination: the cell id, or kSplitDest |
+//               partial slot
 // splits[4 s..]: interval, cell, first partial slot, chunk count
 // counts:       n_work, n_splits, n_partials
 //
@@ -50,7 +51,7 @@ __global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
                                  const uint32_t *__restrict__ cbase,
                                  const uint32_t *__restrict__ pbase,
                                  const uint32_t *__restrict__ sbase, uint4 *__restrict__ tmp,
-                                 uint32_t *__restrict__ hist, uint4 *__restrict__ splits) {
+                                 uint32_t *__restrict__ keys, uint4 *__restrict__ splits) {
     const int64_t n_int = counts[1];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_int;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -60,34 +61,29 @@ __global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
         for (uint32_t k = 0; k < nch; ++k) {
             const uint32_t a = lo + k * chunk, e = min(hi, a + chunk);
             const uint32_t dest = split ? (kSplitDest | (pbase[i] + k)) : cell;
-            tmp[cbase[i] + k] = make_uint4(a, e, dest, static_cast<uint32_t>(i));
-            atomicAdd(hist + (chunk - (e - a)), 1u);  // bucket 0 = longest
+            // .w: the interval, or for a chunk of a split interval its split index
+            tmp[cbase[i] + k] = make_uint4(a, e, dest, split ? sbase[i] : static_cast<uint32_t>(i));
+            keys[cbase[i] + k] = chunk - (e - a);  // bucket 0 = longest
         }
         if (split) splits[sbase[i]] = make_uint4(static_cast<uint32_t>(i), cell, pbase[i], nch);
     }
 }
 
-// exclusive scan of the (chunk + 1)-bucket histogram, one block
-__global__ void work_hist_scan_kernel(uint32_t *__restrict__ hist, int nb) {
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int b = 0; b < nb; ++b) {
-            const uint32_t c = hist[b];
-            hist[b] = run;
-            run += c;
-        }
-    }
+// keys of the unused tail: out of range (dropped by the sort)
+__global__ void work_keys_tail_kernel(const uint32_t *__restrict__ n_work_p, int64_t cap,
+                                      uint32_t *__restrict__ keys) {
+    const int64_t n = *n_work_p;
+    for (int64_t w = n + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < cap;
+         w += (int64_t)gridDim.x * blockDim.x)
+        keys[w] = BVP_OUT_OF_RANGE;
 }
 
-__global__ void work_scatter_kernel(const uint4 *__restrict__ tmp,
-                                    const uint32_t *__restrict__ n_work_p, uint32_t chunk,
-                                    uint32_t *__restrict__ cursor, uint4 *__restrict__ work) {
+__global__ void work_gather_kernel(const uint4 *__restrict__ tmp, const uint32_t *__restrict__ order,
+                                   const uint32_t *__restrict__ n_work_p, uint4 *__restrict__ work) {
     const int64_t n = *n_work_p;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < n;
-         w += (int64_t)gridDim.x * blockDim.x) {
-        const uint4 r = tmp[w];
-        work[atomicAdd(cursor + (chunk - (r.y - r.x)), 1u)] = r;
-    }
+         w += (int64_t)gridDim.x * blockDim.x)
+        work[w] = tmp[order[w]];
 }
 
 __global__ void work_counts_kernel(const uint32_t *__restrict__ n_work,
@@ -99,7 +95,8 @@ __global__ void work_counts_kernel(const uint32_t *__restrict__ n_work,
 }
 
 struct WorkLayout {
-    size_t off_nch, off_npart, off_nsplit, off_part, off_tot, off_hist, off_tmp, bytes;
+    size_t off_nch, off_npart, off_nsplit, off_part, off_tot, off_tmp, off_keys, off_order,
+        off_sstarts, off_scells, off_sfirst, off_scounts, off_sws, sort_ws, bytes;
 };
 static int64_t work_cap(int64_t n_int_max, int64_t n_points, int chunk) {
     return chunk > 0 ? n_int_max + n_points / chunk + 1 : 0;
@@ -108,14 +105,22 @@ static WorkLayout work_layout(int64_t n_int_max, int64_t n_points, int chunk) {
     WorkLayout L{};
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t n = size_t(n_int_max);
+    const int64_t cap = work_cap(n_int_max, n_points, chunk);
     size_t o = 0;
     L.off_nch = o; o = al(o + n * 4);
     L.off_npart = o; o = al(o + n * 4);
     L.off_nsplit = o; o = al(o + n * 4);
     L.off_part = o; o = al(o + size_t(scan_partials_len<uint32_t>(n_int_max)) * 4);
     L.off_tot = o; o = al(o + 16);
-    L.off_hist = o; o = al(o + size_t(chunk + 1) * 4);
-    L.off_tmp = o; o = al(o + size_t(work_cap(n_int_max, n_points, chunk)) * 16);
+    L.off_tmp = o; o = al(o + size_t(cap) * 16);
+    L.off_keys = o; o = al(o + size_t(cap) * 4);
+    L.off_order = o; o = al(o + size_t(cap) * 4);
+    L.off_sstarts = o; o = al(o + size_t(chunk + 2) * 4);
+    L.off_scells = o; o = al(o + size_t(chunk + 2) * 4);
+    L.off_sfirst = o; o = al(o + size_t(chunk + 2) * 4);
+    L.off_scounts = o; o = al(o + 16);
+    L.sort_ws = bvp_sort_workspace_bytes(cap, chunk + 1);
+    L.off_sws = o; o = al(o + L.sort_ws);
     L.bytes = o;
     return L;
 }
@@ -152,23 +157,32 @@ int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cell
     auto *nsplit = reinterpret_cast<uint32_t *>(ws + L.off_nsplit);
     auto *part = reinterpret_cast<uint32_t *>(ws + L.off_part);
     auto *tot = reinterpret_cast<uint32_t *>(ws + L.off_tot);  // n_work, n_partials, n_splits
-    auto *hist = reinterpret_cast<uint32_t *>(ws + L.off_hist);
     auto *tmp = reinterpret_cast<uint4 *>(ws + L.off_tmp);
+    auto *keys = reinterpret_cast<uint32_t *>(ws + L.off_keys);
+    auto *order = reinterpret_cast<uint32_t *>(ws + L.off_order);
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_int_max, 256), 4096));
     work_count_kernel<<<blocks, 256, 0, s>>>(interval_starts, counts, n_int_max, uint32_t(chunk),
                                              nch, npart, nsplit);
     device_excl_scan<uint32_t>(nch, nch, n_int_max, part, tot + 0, s);
     device_excl_scan<uint32_t>(npart, npart, n_int_max, part, tot + 1, s);
     device_excl_scan<uint32_t>(nsplit, nsplit, n_int_max, part, tot + 2, s);
-    cudaMemsetAsync(hist, 0, size_t(chunk + 1) * 4, s);
     work_emit_kernel<<<blocks, 256, 0, s>>>(interval_starts, interval_cells, counts,
-                                            uint32_t(chunk), nch, npart, nsplit, tmp, hist,
+                                            uint32_t(chunk), nch, npart, nsplit, tmp, keys,
                                             reinterpret_cast<uint4 *>(splits));
-    work_hist_scan_kernel<<<1, 32, 0, s>>>(hist, chunk + 1);
     const int64_t cap = work_cap(n_int_max, n_points, chunk);
-    work_scatter_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(cap, 256), 4096)), 256,
-                          0, s>>>(tmp, tot + 0, uint32_t(chunk), hist,
-                                  reinterpret_cast<uint4 *>(work));
+    const unsigned cb = static_cast<unsigned>(std::min<int64_t>(ceil_div(cap, 256), 4096));
+    work_keys_tail_kernel<<<cb, 256, 0, s>>>(tot + 0, cap, keys);
+    // stable counting sort by length bucket (the association's own sort):
+    // longest chunks first, cell order within a bucket, so a warp's groups
+    // store to neighbouring cells
+    const int rc = bvp_sort_intervals(keys, cap, chunk + 1, order,
+                                      reinterpret_cast<uint32_t *>(ws + L.off_sstarts),
+                                      reinterpret_cast<uint32_t *>(ws + L.off_scells),
+                                      reinterpret_cast<uint32_t *>(ws + L.off_sfirst), nullptr,
+                                      reinterpret_cast<int64_t *>(ws + L.off_scounts),
+                                      ws + L.off_sws, L.sort_ws, stream);
+    if (rc != BVP_OK) return rc;
+    work_gather_kernel<<<cb, 256, 0, s>>>(tmp, order, tot + 0, reinterpret_cast<uint4 *>(work));
     work_counts_kernel<<<1, 1, 0, s>>>(tot + 0, tot + 2, tot + 1, work_counts);
     return check_launch("make_work");
 }
