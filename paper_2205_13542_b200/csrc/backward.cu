@@ -17,7 +17,7 @@
 // reduction instead of 32 separate butterflies.
 #include <algorithm>
 
-#include "common.cuh"
+#include "pool_group.cuh"
 
 namespace bvp {
 
@@ -153,6 +153,135 @@ pool_backward_kernel(const float *__restrict__ gT, const uint32_t *__restrict__ 
     (void)P;
 }
 
+// SUM / MEAN backward, group layout (measured faster, profiles/): a warp
+// takes 8 consecutive pixels of the flattened (N, H*W) frustum, one per
+// 4-lane group, and walks their D depth points in step.  Per step each group
+// gathers its point's gradient row gT[interval] (5 float4 per lane at C = 80),
+// accumulates grad_f += w * g and reduces <f, g> over its 4 lanes into
+// grad_w.  The 8 groups' grad_w stores (and, at the end, every channel's
+// grad_f stores) are 8 consecutive floats.  Interval ids and weights of a
+// 4-point window are loaded one lane per point and shuffled, a window ahead.
+// Every gradient element is written by exactly one lane: no atomics.
+template <int CPL>
+__global__ void __launch_bounds__(256, 2)
+pool_backward_grp_kernel(const float *__restrict__ gT, const float *__restrict__ feats_nhwc,
+                         const float *__restrict__ dist, const uint32_t *__restrict__ iop, int N,
+                         int C, int HW, int D, int64_t n_int_max, int L, int lg,
+                         float *__restrict__ grad_f, float *__restrict__ grad_w) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane >> lg, li = lane & (L - 1);
+    const int G = 32 >> lg;
+    const int b = blockIdx.y;
+    const int64_t NHW = int64_t(N) * HW;
+    const int nch = C / 4;
+    const int64_t pix = (int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G + g;
+    const bool valid = pix < NHW;
+    const int64_t px = valid ? pix : 0;
+    const int64_t n = px / HW, hw = px - n * HW;
+    float f[CPL][4], af[CPL][4];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+        const int ch = li + k * L;
+        const bool ok = ch < nch;
+        const float4 t = ok ? __ldg(reinterpret_cast<const float4 *>(
+                                  feats_nhwc + (int64_t(b) * NHW + px) * C) + ch)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        f[k][0] = t.x; f[k][1] = t.y; f[k][2] = t.z; f[k][3] = t.w;
+        af[k][0] = af[k][1] = af[k][2] = af[k][3] = 0.f;
+    }
+    const uint32_t *ip = iop + px * D;
+    const float *wp = dist + (int64_t(b) * N + n) * D * HW + hw;
+    float *gw = grad_w ? grad_w + (int64_t(b) * N + n) * D * HW + hw : nullptr;
+    const float *gTb = gT + int64_t(b) * n_int_max * C;
+    // windows of L points: lane li holds point d0 + li's interval and weight;
+    // the current and the next window are kept, the one after is in flight
+    auto load_win = [&](int d0, uint32_t &iv, float &w) {
+        const int d = d0 + li;
+        iv = kOOR;
+        w = 0.f;
+        if (valid && d < D) {
+            iv = __ldg(ip + d);
+            w = __ldg(wp + int64_t(d) * HW);
+        }
+    };
+    uint32_t iv0, iv1, iv2;
+    float w0, w1, w2;
+    load_win(0, iv0, w0);
+    load_win(L, iv1, w1);
+    load_win(2 * L, iv2, w2);
+    int wbase = 0;  // first point of window 0
+    const int gbase = g * L;
+    // point d's (interval, weight): window 0 or 1 (d < wbase + 2L always)
+    auto point = [&](int d, uint32_t &iv, float &w) {
+        const int q = d - wbase;
+        const int src = gbase + (q & (L - 1));
+        const uint32_t a0 = __shfl_sync(0xFFFFFFFFu, iv0, src), a1 = __shfl_sync(0xFFFFFFFFu, iv1, src);
+        const float b0 = __shfl_sync(0xFFFFFFFFu, w0, src), b1 = __shfl_sync(0xFFFFFFFFu, w1, src);
+        iv = q < L ? a0 : a1;
+        w = q < L ? b0 : b1;
+    };
+    // gradient row of point d into registers (zeros when out of range)
+    auto fetch = [&](int d, uint32_t &iv, float &w, float4 (&row)[CPL]) {
+        point(d, iv, w);
+        const float4 *r = reinterpret_cast<const float4 *>(gTb + int64_t(iv == kOOR ? 0u : iv) * C);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int ch = li + k * L;
+            row[k] = (iv != kOOR && ch < nch) ? __ldg(r + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    auto consume = [&](int d, float w, const float4 (&row)[CPL]) {
+        float dot = 0.f;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const float4 t = row[k];
+            af[k][0] = fmaf(w, t.x, af[k][0]);
+            af[k][1] = fmaf(w, t.y, af[k][1]);
+            af[k][2] = fmaf(w, t.z, af[k][2]);
+            af[k][3] = fmaf(w, t.w, af[k][3]);
+            dot = fmaf(f[k][0], t.x, dot);
+            dot = fmaf(f[k][1], t.y, dot);
+            dot = fmaf(f[k][2], t.z, dot);
+            dot = fmaf(f[k][3], t.w, dot);
+        }
+        for (int o = 1; o < L; o <<= 1) dot += __shfl_xor_sync(0xFFFFFFFFu, dot, o);
+        if (gw && valid && li == 0) gw[int64_t(d) * HW] = dot;
+    };
+    // advance the windows so that points d and d + 1 are covered
+    auto cover = [&](int d) {
+        while (d + 1 >= wbase + 2 * L) {
+            iv0 = iv1; w0 = w1;
+            iv1 = iv2; w1 = w2;
+            wbase += L;
+            load_win(wbase + 2 * L, iv2, w2);
+        }
+    };
+    float4 ra[CPL], rb[CPL];
+    uint32_t ia, ib;
+    float wa, wb;
+    fetch(0, ia, wa, ra);
+#pragma unroll 1
+    for (int d = 0; d < D; d += 2) {
+        cover(d);
+        if (d + 1 < D) fetch(d + 1, ib, wb, rb);
+        consume(d, wa, ra);
+        if (d + 1 >= D) break;
+        cover(d + 1);
+        if (d + 2 < D) fetch(d + 2, ia, wa, ra);
+        consume(d + 1, wb, rb);
+    }
+    if (grad_f && valid) {
+        float *gf = grad_f + (int64_t(b) * N + n) * C * HW + hw;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+            const int ch = li + k * L;
+            if (ch < nch)
+#pragma unroll
+                for (int x = 0; x < 4; ++x) gf[int64_t(ch * 4 + x) * HW] = af[k][x];
+        }
+    }
+}
+
 template <bool IS_MAX>
 __global__ void lifted_backward_kernel(const float *__restrict__ gT,
                                        const uint32_t *__restrict__ argT,
@@ -224,6 +353,19 @@ int bvp_pool_backward_f32(const float *grad_out, const float *feats_nhwc, const 
     int rc = launch_grad_rows(grad_out, interval_starts, interval_cells, cell_first, B, C, nx, ny,
                               n_int_max, mode == BVP_MEAN, gT, s);
     if (rc != BVP_OK) return rc;
+    int L, lg, cpl;
+    if (mode != BVP_MAX && C % 4 == 0 && choose_group(C / 4, 4, L, lg, cpl)) {
+        const int64_t NHW = int64_t(N) * H * W;
+        const int G = 32 >> lg;
+        const dim3 grid(static_cast<unsigned>(ceil_div(ceil_div(NHW, G), 8)), static_cast<unsigned>(B));
+#define BVP_BWD_GRP(CPLV)                                                                     \
+        if (cpl == CPLV)                                                                      \
+            pool_backward_grp_kernel<CPLV><<<grid, 256, 0, s>>>(gT, feats_nhwc, dist,         \
+                interval_of_point, N, C, H * W, D, n_int_max, L, lg, grad_features, grad_dist);
+        BVP_BWD_GRP(1) BVP_BWD_GRP(2) BVP_BWD_GRP(3) BVP_BWD_GRP(4) BVP_BWD_GRP(5) BVP_BWD_GRP(6)
+#undef BVP_BWD_GRP
+        return check_launch("pool_backward");
+    }
     const size_t smem = size_t(C + D) * kRowPitch * sizeof(float);
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "C + D too large for the backward");
     const dim3 grid(static_cast<unsigned>((W + 31) / 32), static_cast<unsigned>(N * H),
