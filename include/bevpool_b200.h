@@ -263,7 +263,7 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks,
 /* ---- fused lift + pool, bf16 inputs (config F) ------------------------- */
 
 /* Workspace: per-pixel log-sum-exp (f32) + NHWC bf16 context. */
-size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W);
+size_t bvp_fused_workspace_bytes(int B, int N, int C, int H, int W, int D);
 
 /* logits (B,N,D,H,W) bf16, context (B,N,C,H,W) bf16 -> out (B,C,nx*ny)
  * f32 = pool(softmax_D(logits) (x) context), fp32 accumulation. */

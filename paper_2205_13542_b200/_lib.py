@@ -76,7 +76,7 @@ SIGNATURES = {
     "bvp_any_nonfinite": (_I, [_P, _L, _P, _P]),
     "bvp_lift_f32": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P]),
     "bvp_pool_lifted_f32": (_I, [_P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _P, _P, _S, _P]),
-    "bvp_fused_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
+    "bvp_fused_workspace_bytes": (_S, [_I, _I, _I, _I, _I, _I]),
     "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
                                  _I, _P, _P, _S, _P, _S, _P]),
     "bvp_backward_workspace_bytes": (_S, [_I, _I, _L]),

@@ -34,12 +34,62 @@
 namespace bvp {
 
 constexpr uint32_t kIvlSplit = 0x80000000u;  // work.cu kSplitDest
+
+// A row chunk as loaded (packed) and its fp32 unpacking.
+template <typename Elem, int VEC>
+struct RawChunk;
+template <>
+struct RawChunk<float, 4> {
+    using type = float4;
+    template <bool STREAM>
+    __device__ __forceinline__ static float4 load(const float *p) {
+        return STREAM ? ldg_stream_f4(p) : ldg_f4(p);
+    }
+    __device__ __forceinline__ static float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+    __device__ __forceinline__ static void unpack(const float4 &t, float (&v)[4]) {
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    }
+};
+template <>
+struct RawChunk<float, 1> {
+    using type = float;
+    template <bool STREAM>
+    __device__ __forceinline__ static float load(const float *p) { return __ldg(p); }
+    __device__ __forceinline__ static float zero() { return 0.f; }
+    __device__ __forceinline__ static void unpack(float t, float (&v)[1]) { v[0] = t; }
+};
+template <>
+struct RawChunk<__nv_bfloat16, 8> {
+    using type = uint4;
+    template <bool STREAM>
+    __device__ __forceinline__ static uint4 load(const __nv_bfloat16 *p) {
+        return __ldg(reinterpret_cast<const uint4 *>(p));
+    }
+    __device__ __forceinline__ static uint4 zero() { return make_uint4(0u, 0u, 0u, 0u); }
+    __device__ __forceinline__ static void unpack(const uint4 &t, float (&v)[8]) {
+        const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            v[2 * i] = __uint_as_float(w[i] << 16);
+            v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
+};
+template <>
+struct RawChunk<__nv_bfloat16, 1> {
+    using type = float;
+    template <bool STREAM>
+    __device__ __forceinline__ static float load(const __nv_bfloat16 *p) { return __bfloat162float(p[0]); }
+    __device__ __forceinline__ static float zero() { return 0.f; }
+    __device__ __forceinline__ static void unpack(float t, float (&v)[1]) { v[0] = t; }
+};
 #ifndef BVP_IVL_MIN_BLOCKS
 #define BVP_IVL_MIN_BLOCKS 3
 #endif
 
 template <typename Elem, int VEC, int CPL, bool IS_MAX, int SRC>
-__global__ void __launch_bounds__(kPoolThreads, BVP_IVL_MIN_BLOCKS)
+__global__ void __launch_bounds__(kPoolThreads, sizeof(Elem) == 2 ? BVP_IVL_MIN_BLOCKS + 1
+                                                                  : BVP_IVL_MIN_BLOCKS)
 pool_ivl_kernel(const PoolParams P, int L, int lg) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y;
@@ -83,7 +133,9 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
         // rows of two steps in flight: fetch(s + 1) is issued before the
         // FMAs of step s; each fetch also loads the next step's record
         uint2 m = len > 0 ? rec_of(j0) : make_uint2(0u, 0u);
-        auto fetch = [&](uint32_t s, float &w, float (&v)[CPL][VEC]) {
+        // rows stay packed (bf16: 4 registers per 8 values) until the FMAs
+        using Raw = typename RawChunk<Elem, VEC>::type;
+        auto fetch = [&](uint32_t s, float &w, Raw (&v)[CPL]) {
             const bool ok = s < len;
             w = 1.f;
             if (SRC == kSrcDist) w = ok ? __ldg(wdist + m.y) : 0.f;
@@ -92,22 +144,27 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
                 if (k == 0 || ((live >> k) & 1u))
-                    ChunkLoad<Elem, VEC>::template load<SRC == kSrcX>(rp + k * L * VEC, v[k]);
-                else
-#pragma unroll
-                    for (int x = 0; x < VEC; ++x) v[k][x] = 0.f;
+                    v[k] = RawChunk<Elem, VEC>::template load<SRC == kSrcX>(rp + k * L * VEC);
+                else v[k] = RawChunk<Elem, VEC>::zero();
             }
             if (s + 1 < len) m = rec_of(j0 + s + 1);
         };
-        float wa, wb, va[CPL][VEC], vb[CPL][VEC];
+        auto consume = [&](uint32_t j, float w, const Raw (&raw)[CPL]) {
+            float v[CPL][VEC];
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) RawChunk<Elem, VEC>::unpack(raw[k], v[k]);
+            gacc<CPL, VEC, IS_MAX>(acc, arg, j, true, w, v);
+        };
+        float wa, wb;
+        Raw va[CPL], vb[CPL];
         if (steps > 0) fetch(0, wa, va);
 #pragma unroll 1
         for (uint32_t s = 0; s < steps; s += 2) {
             if (s + 1 < steps) fetch(s + 1, wb, vb);
-            if (s < len) gacc<CPL, VEC, IS_MAX>(acc, arg, j0 + s, true, wa, va);
+            if (s < len) consume(j0 + s, wa, va);
             if (s + 1 >= steps) break;
             if (s + 2 < steps) fetch(s + 2, wa, va);
-            if (s + 1 < len) gacc<CPL, VEC, IS_MAX>(acc, arg, j0 + s + 1, true, wb, vb);
+            if (s + 1 < len) consume(j0 + s + 1, wb, vb);
         }
         if (item >= n_work) continue;
         if (!(r.z & kIvlSplit)) {  // the chunk is the whole interval: store its cell

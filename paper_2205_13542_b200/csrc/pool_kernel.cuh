@@ -577,6 +577,7 @@ BVP_DECLARE_RUN_POOL(double, float, 1, kSrcDist)         // pool_exact.cu
 BVP_DECLARE_RUN_POOL(float, float, 4, kSrcX)             // pool_x.cu
 BVP_DECLARE_RUN_POOL(float, float, 1, kSrcX)             // pool_x.cu
 BVP_DECLARE_RUN_POOL(float, __nv_bfloat16, 8, kSrcFused) // fused.cu
+BVP_DECLARE_RUN_POOL(float, __nv_bfloat16, 8, kSrcDist)  // fused.cu (precomputed softmax)
 BVP_DECLARE_RUN_POOL(float, __nv_bfloat16, 1, kSrcFused) // fused.cu
 #undef BVP_DECLARE_RUN_POOL
 

@@ -447,7 +447,7 @@ def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCa
     cache = cache.for_grid(grid)
     dev = lg.device
     out = torch.empty((B, C, grid.n_cells), dtype=torch.float32, device=dev)
-    ws = torch.empty(_lib.load().bvp_fused_workspace_bytes(B, N, C, H, W), dtype=torch.uint8,
+    ws = torch.empty(_lib.load().bvp_fused_workspace_bytes(B, N, C, H, W, D), dtype=torch.uint8,
                      device=dev)
     _lib.call("bvp_fused_pool_bf16", ptr(lg), ptr(cx), ptr(cache.d_ranks),
               ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_cell_first),
