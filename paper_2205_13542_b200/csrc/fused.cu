@@ -169,7 +169,8 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     // 91 us vs 99 us for exp(logit - lse) per point at the nuScenes shape)
     static const int wmode = [] { const char *e = getenv("BVP_FUSED_W"); return e ? atoi(e) : 1; }();
     float *wsm = reinterpret_cast<float *>(ws + L.off_w);
-    if (wmode) pixel_softmax_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), wsm);
+    const bool use_w = wmode && C % 8 == 0;  // the weight-gather kernel needs 16-byte chunks
+    if (use_w) pixel_softmax_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), wsm);
     else pixel_lse_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), lse);
     launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
                                   int(HW), ctx, s);
@@ -186,7 +187,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     p.scratch = scratch;
     p.scratch_bytes = scratch_bytes;
     const bool is_max = mode == BVP_MAX;
-    if (wmode && C % 8 == 0) {
+    if (use_w) {
         p.wsrc = wsm;
         const int rcw = run_pool<float, __nv_bfloat16, 8, kSrcDist>(p, B, is_max, s);
         if (rcw != BVP_OK) return rcw;

@@ -406,3 +406,83 @@ def test_backward_nuscenes_shape_sum():
         gw = np.einsum("chwd,chw->dhw", gc, features[n].astype(np.float64))
         assert max_rel_dev(gf, gf_got[n]) <= FP32_TOL
         assert max_rel_dev(gw, gw_got[n]) <= FP32_TOL
+
+
+# ---- lane layouts: every channel count the fast kernels instantiate --------
+
+def _sweep_case(C, seed=7):
+    spec = bp.CONFIGS["T"]
+    rng = np.random.default_rng(seed)
+    rig, _, logits, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    features = rng.uniform(-1, 1, size=(1, C, spec.frustum.height, spec.frustum.width)
+                           ).astype(np.float32)
+    return cache, grid, features, logits
+
+
+@pytest.mark.parametrize("C", [1, 3, 4, 8, 12, 20, 33, 64, 80, 96, 128, 200, 256])
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+def test_fast_mode_channel_sweep(C, red):
+    cache, grid, features, logits = _sweep_case(C)
+    dist = o.normalize_depth(logits)
+    want = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
+                           cache.interval_cells, grid.n_cells, red)
+    got = bp.pool_interval(features, dist, cache, grid, red, exact=False).values
+    assert max_rel_dev(want, got.reshape(want.shape)) <= FP32_TOL
+
+
+@pytest.mark.parametrize("C", [8, 16, 24, 40, 80, 7, 13])
+def test_fused_channel_sweep(C):
+    cache, grid, features, logits = _sweep_case(C, seed=11)
+    dev = torch.device("cuda")
+    fb, lb = o.bf16_round(features), o.bf16_round(logits)
+    got = bp.pool_fused(torch.from_numpy(logits).to(dev).to(torch.bfloat16),
+                        torch.from_numpy(features).to(dev).to(torch.bfloat16), cache, grid
+                        ).values.cpu().numpy().reshape(C, -1)
+    want = o.fused_pool(fb, lb, cache.ranks, cache.interval_starts, cache.interval_cells,
+                        grid.n_cells, "sum")
+    assert max_rel_dev(want, got) <= 1e-5
+
+
+@pytest.mark.parametrize("C", [3, 32, 80])
+def test_lifted_channel_sweep(C):
+    cache, grid, features, logits = _sweep_case(C, seed=13)
+    dist = o.normalize_depth(logits)
+    dev = torch.device("cuda")
+    x = bp.lift_features(torch.from_numpy(features).to(dev), torch.from_numpy(dist).to(dev))
+    for red in ("sum", "mean", "max"):
+        got = bp.pool_lifted(x, cache, grid, red).values.cpu().numpy().reshape(C, -1)
+        want = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
+                               cache.interval_cells, grid.n_cells, red)
+        assert max_rel_dev(want, got) <= FP32_TOL, red
+
+
+def test_fast_mode_high_res_config():
+    """Config H (6 x 64 x 176, 720 x 720 grid): fast SUM within 1e-5 of the
+    64-bit oracle, and the uncached builder reproduces the cached build."""
+    spec = bp.CONFIGS["H"]
+    rig, features, logits, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    dist = o.normalize_depth(logits)
+    want = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
+                           cache.interval_cells, grid.n_cells, "sum")
+    got = bp.pool_interval(features, dist, cache, grid, exact=False).values
+    assert max_rel_dev(want, got.reshape(want.shape)) <= FP32_TOL
+    builder = bp.CacheBuilder(spec.n_cameras, spec.frustum, grid)
+    c2 = builder.build(torch.from_numpy(bp.rig_rows(rig)).cuda())
+    got2 = bp.pool_interval(features, dist, c2, grid, exact=False).values
+    assert np.array_equal(got, got2)  # capacity-bounded schedule, same result
+
+
+def test_fast_mode_batched_and_deterministic():
+    spec, features, logits, grid, cache = _S()
+    dev = torch.device("cuda")
+    F = torch.stack([torch.from_numpy(features)] * 3).to(dev)
+    Dd = torch.stack([torch.from_numpy(o.normalize_depth(logits))] * 3).to(dev)
+    F[1] *= -1.0
+    out = bp.pool_interval(F, Dd, cache, grid, exact=False).values
+    for b in range(3):
+        one = bp.pool_interval(F[b], Dd[b], cache, grid, exact=False).values
+        assert torch.equal(out[b], one)
+    again = bp.pool_interval(F, Dd, cache, grid, exact=False).values
+    assert torch.equal(out, again)
