@@ -23,8 +23,10 @@
 //     deterministic, independent of timing and launch shape;
 //   * the map is zero-filled first (cudaMemsetAsync) so the scattered column
 //     stores hit valid L2 lines.  Measured alternatives, both slower: zeroing
-//     only the empty cells in-kernel (+15 us, partial-sector write misses) and
-//     combining split intervals in the last-finishing chunk (+14 us).
+//     only the empty cells in-kernel (+15 us, partial-sector write misses),
+//     combining split intervals in the last-finishing chunk (+14 us), and
+//     walking intervals longer than a chunk with a whole warp (8 slices,
+//     butterfly combine; +9 us).
 #pragma once
 
 #include <algorithm>
