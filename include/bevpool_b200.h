@@ -321,6 +321,26 @@ int bvp_pool_prefixsum_f32(const float *features, const float *dist,
                            void *workspace, size_t workspace_bytes,
                            void *stream);
 
+/* ---- shared-BEV fusion (reference fusion.py) ------------ */
+
+/* Workspace for bvp_lidar_to_bev. */
+size_t bvp_lidar_workspace_bytes(int64_t n_points, int nx, int ny);
+
+/* lidar_to_bev (fusion.py:19-53): points (M, 4) float64 x, y, z, intensity
+ * (device) -> out (3, nx*ny) f32: point count, reduced intensity, reduced
+ * height per cell (mode BVP_SUM / MEAN / MAX; the count ignores it).  grid:
+ * HOST, 7 float64 as bvp_frustum_cells.  Bit-identical to the reference. */
+int bvp_lidar_to_bev(const double *points, int64_t n_points, const double *grid,
+                     int nx, int ny, int mode, float *out, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
+/* grid_resample (fusion.py:70-108): bilinear BEV -> BEV, float64 math,
+ * src (C, src_nx, src_ny) f32 -> dst (C, dst_nx, dst_ny) f32; grids: HOST,
+ * 7 float64 each.  Bit-identical to the reference. */
+int bvp_grid_resample_f32(const float *src, int C, const double *src_grid,
+                          int src_nx, int src_ny, const double *dst_grid,
+                          int dst_nx, int dst_ny, float *dst, void *stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -372,3 +372,67 @@ def max_rel_dev(reference, candidate) -> float:
     if a.size == 0:
         return 0.0
     return float((np.abs(a - b) / np.maximum(1.0, np.abs(a))).max())
+
+
+# --------------------------------------------------------------------------
+# shared-BEV fusion (fusion.py) -- §8f "next" components
+# --------------------------------------------------------------------------
+
+def quantize_points(grid7, nx, ny, xyz):
+    """Restates bevgrid.py:85-98 on float64 (M, 3) points."""
+    x_min, _, y_min, _, z_min, z_max, r = grid7
+    pts = np.asarray(xyz, dtype=np.float64)
+    ix = np.floor((pts[:, 0] - x_min) / r).astype(np.int64)
+    iy = np.floor((pts[:, 1] - y_min) / r).astype(np.int64)
+    z = pts[:, 2]
+    ok = (ix >= 0) & (ix < nx) & (iy >= 0) & (iy < ny) & (z >= z_min) & (z < z_max)
+    return np.where(ok, ix * ny + iy, OUT_OF_RANGE).astype(np.uint32)
+
+
+def lidar_to_bev(points, grid7, nx, ny, mode="sum"):
+    """Restates fusion.py:19-53: (3, nx, ny) float32 count / intensity /
+    height, fp64 bincount sums in input order."""
+    points = np.asarray(points, dtype=np.float64)
+    n_cells = nx * ny
+    out = np.zeros((3, n_cells), dtype=np.float32)
+    if points.shape[0]:
+        cells = quantize_points(grid7, nx, ny, points[:, :3])
+        keep = cells != OUT_OF_RANGE
+        cells = cells[keep].astype(np.int64)
+        counts = np.bincount(cells, minlength=n_cells)
+        out[0] = counts
+        for ch, values in ((1, points[keep, 3]), (2, points[keep, 2])):
+            if mode == "max":
+                best = np.full(n_cells, -np.inf)
+                np.maximum.at(best, cells, values)
+                out[ch] = np.where(np.isneginf(best), 0.0, best)
+            else:
+                acc = np.bincount(cells, weights=values, minlength=n_cells)
+                if mode == "mean":
+                    acc = np.divide(acc, counts, out=np.zeros_like(acc), where=counts > 0)
+                out[ch] = acc
+    return out.reshape(3, nx, ny)
+
+
+def grid_resample(values, src7, src_nx, src_ny, dst7, dst_nx, dst_ny):
+    """Restates fusion.py:70-108 (bilinear between cell centres, fp64)."""
+    eps = 1e-9
+    gx = (dst7[0] + (np.arange(dst_nx) + 0.5) * dst7[6] - src7[0]) / src7[6] - 0.5
+    gy = (dst7[2] + (np.arange(dst_ny) + 0.5) * dst7[6] - src7[2]) / src7[6] - 0.5
+    cov_x = (gx >= -eps) & (gx <= src_nx - 1 + eps)
+    cov_y = (gy >= -eps) & (gy <= src_ny - 1 + eps)
+    gx = np.clip(gx, 0.0, src_nx - 1)
+    gy = np.clip(gy, 0.0, src_ny - 1)
+    x0 = np.floor(gx).astype(np.int64)
+    y0 = np.floor(gy).astype(np.int64)
+    x1 = np.minimum(x0 + 1, src_nx - 1)
+    y1 = np.minimum(y0 + 1, src_ny - 1)
+    fx = np.clip(gx - x0, 0.0, 1.0)[None, :, None]
+    fy = np.clip(gy - y0, 0.0, 1.0)[None, None, :]
+    v = np.asarray(values).astype(np.float64)
+    ix0, ix1 = x0[:, None], x1[:, None]
+    iy0, iy1 = y0[None, :], y1[None, :]
+    interp = (v[:, ix0, iy0] * (1 - fx) * (1 - fy) + v[:, ix1, iy0] * fx * (1 - fy)
+              + v[:, ix0, iy1] * (1 - fx) * fy + v[:, ix1, iy1] * fx * fy)
+    interp *= (cov_x[:, None] & cov_y[None, :])[None, :, :]
+    return interp.astype(np.float32)

@@ -84,6 +84,9 @@ SIGNATURES = {
                                    _I, _L, _I, _P, _P, _P, _S, _P]),
     "bvp_pool_lifted_backward_f32": (_I, [_P, _P, _P, _P, _P, _I, _L, _I, _I, _L, _I, _P, _P,
                                           _S, _P]),
+    "bvp_lidar_workspace_bytes": (_S, [_L, _I, _I]),
+    "bvp_lidar_to_bev": (_I, [_P, _L, _P, _I, _I, _I, _P, _P, _S, _P]),
+    "bvp_grid_resample_f32": (_I, [_P, _I, _P, _I, _I, _P, _I, _I, _P, _P]),
     "bvp_prefixsum_workspace_bytes": (_S, [_L, _I]),
     "bvp_pool_prefixsum_f32": (_I, [_P, _P, _P, _P, _P, _L, _L, _I, _I, _I, _I, _I, _L, _I, _P,
                                     _P, _S, _P]),

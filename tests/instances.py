@@ -90,3 +90,47 @@ GOLDEN_INSTANCES = (
     + [(300 + s, 24, 12, 8) for s in range(6)]
     + [(10_000 + s, 64, 32, 16) for s in range(12)]
 )
+
+
+# ---- shared-BEV fusion inputs (tests/golden/make_golden_fusion.py) ---------
+
+def random_cloud(seed: int, n: int, grid: tuple) -> np.ndarray:
+    """(n, 4) float64 LiDAR-like cloud over and around `grid`: a quarter of
+    the x/y coordinates sit exactly on cell edges, some points fall outside
+    x/y/z, intensities in [0, 1)."""
+    rng = np.random.default_rng(seed)
+    x_min, x_max, y_min, y_max, z_min, z_max, r = grid
+    pts = np.empty((n, 4))
+    pts[:, 0] = rng.uniform(x_min - 2 * r, x_max + 2 * r, n)
+    pts[:, 1] = rng.uniform(y_min - 2 * r, y_max + 2 * r, n)
+    edge = rng.random(n) < 0.25
+    pts[edge, 0] = x_min + r * rng.integers(-1, int(round((x_max - x_min) / r)) + 2, edge.sum())
+    pts[edge, 1] = y_min + r * rng.integers(-1, int(round((y_max - y_min) / r)) + 2, edge.sum())
+    pts[:, 2] = rng.uniform(z_min - 1.0, z_max + 1.0, n)
+    pts[:, 3] = rng.random(n)
+    return pts
+
+
+#: (seed, points, grid) of the pinned LiDAR cases
+LIDAR_CASES = [
+    (1, 20000, (-51.2, 51.2, -51.2, 51.2, -10.0, 10.0, 0.8)),
+    (2, 100000, (-54.0, 54.0, -54.0, 54.0, -10.0, 10.0, 0.3)),
+    (3, 0, (-8.0, 8.0, -8.0, 8.0, -10.0, 10.0, 0.5)),
+    (4, 5000, (-3.0, 4.5, -2.0, 2.0, -1.0, 1.0, 0.25)),
+]
+
+#: (seed, C, src grid, dst grid) of the pinned resampling cases
+RESAMPLE_CASES = [
+    (11, 3, (-51.2, 51.2, -51.2, 51.2, -10.0, 10.0, 0.8), (-54.0, 54.0, -54.0, 54.0, -10.0, 10.0, 0.3)),
+    (12, 5, (-54.0, 54.0, -54.0, 54.0, -10.0, 10.0, 0.3), (-51.2, 51.2, -51.2, 51.2, -10.0, 10.0, 0.4)),
+    (13, 2, (-8.0, 8.0, -8.0, 8.0, -5.0, 5.0, 0.5), (-10.0, 6.0, -7.5, 9.0, -5.0, 5.0, 0.25)),
+    (14, 4, (-4.0, 4.0, -4.0, 4.0, -1.0, 1.0, 1.0), (-4.0, 4.0, -4.0, 4.0, -1.0, 1.0, 1.0)),
+]
+
+
+def random_map(seed: int, C: int, nx: int, ny: int) -> np.ndarray:
+    return np.random.default_rng(seed).uniform(-1, 1, size=(C, nx, ny)).astype(np.float32)
+
+
+def grid_shape(grid: tuple) -> tuple[int, int]:
+    return (int(round((grid[1] - grid[0]) / grid[6])), int(round((grid[3] - grid[2]) / grid[6])))
