@@ -32,9 +32,48 @@ to_nhwc_kernel(const T *__restrict__ src, int A, int HW, T *__restrict__ dst) {
     }
 }
 
+// Whole-row variant (A <= kRowsA): a CTA moves 32 pixels x all A channels;
+// the loads are 128-byte rows of one channel, the stores one contiguous
+// 32 x A block of the NHWC output (A * 128 bytes), written as 16-byte words.
+constexpr int kRowsA = 128;
+template <typename T>
+__global__ void __launch_bounds__(256)
+to_nhwc_rows_kernel(const T *__restrict__ src, int A, int HW, T *__restrict__ dst) {
+    extern __shared__ __align__(16) unsigned char s_raw[];
+    T *t = reinterpret_cast<T *>(s_raw);  // [32][A + pad] (pixel-major)
+    const int pitch = A + (16 / int(sizeof(T)));
+    const int64_t n = blockIdx.y;
+    const int hw0 = blockIdx.x * 32;
+    const int np = min(32, HW - hw0);
+    const T *sb = src + n * int64_t(A) * HW + hw0;
+    for (int a = threadIdx.x >> 5; a < A; a += 8)
+        if ((threadIdx.x & 31) < np) t[(threadIdx.x & 31) * pitch + a] = sb[int64_t(a) * HW + (threadIdx.x & 31)];
+    __syncthreads();
+    T *db = dst + (n * HW + hw0) * int64_t(A);
+    constexpr int V = 16 / sizeof(T);
+    const int total = np * A;  // contiguous in the output
+    if ((A % V) == 0) {
+        for (int e = threadIdx.x * V; e < total; e += 256 * V) {
+            const int px = e / A, a = e - px * A;
+            *reinterpret_cast<uint4 *>(db + e) = *reinterpret_cast<const uint4 *>(t + px * pitch + a);
+        }
+    } else {
+        for (int e = threadIdx.x; e < total; e += 256) {
+            const int px = e / A, a = e - px * A;
+            db[e] = t[px * pitch + a];
+        }
+    }
+}
+
 template <typename T>
 void launch_to_nhwc(const T *src, int64_t NB, int A, int HW, T *dst, cudaStream_t s) {
     if (NB == 0 || A == 0 || HW == 0) return;
+    if (A <= kRowsA) {
+        const size_t smem = size_t(32) * (A + 16 / sizeof(T)) * sizeof(T);
+        const dim3 grid((HW + 31) / 32, static_cast<unsigned>(NB));
+        to_nhwc_rows_kernel<T><<<grid, 256, smem, s>>>(src, A, HW, dst);
+        return;
+    }
     const dim3 grid((HW + 31) / 32, (A + 31) / 32, static_cast<unsigned>(NB));
     to_nhwc_kernel<T><<<grid, dim3(32, 8), 0, s>>>(src, A, HW, dst);
 }

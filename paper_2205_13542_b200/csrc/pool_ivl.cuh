@@ -203,59 +203,48 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
     }
 }
 
-// One warp per split interval: add its chunk partials in chunk order (MAX:
-// the first maximum in rank order), scale (MEAN), store the cell's column.
+// One thread per (split interval, channel): add the interval's chunk
+// partials in chunk order (MAX: the first maximum in rank order), scale
+// (MEAN), store the cell's value.  Loads of up to 8 chunks are issued before
+// the in-order adds, so a thread waits ~2 memory latencies, not one per chunk.
 template <bool IS_MAX>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_ivl_combine_kernel(const PoolParams P) {
-    const int lane = threadIdx.x & 31;
     const int b = blockIdx.y;
     const int C = P.C;
     const int64_t n_split = P.work_counts[1], n_part = P.work_counts[2];
-    const int64_t nwarps = int64_t(gridDim.x) * kPoolWarps;
+    const int64_t total = n_split * C;
 #pragma unroll 1
-    for (int64_t s = int64_t(blockIdx.x) * kPoolWarps + (threadIdx.x >> 5); s < n_split; s += nwarps) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t s = e / C;
+        const int c = static_cast<int>(e - s * C);
         const uint4 sp = __ldg(P.splits + s);  // interval, cell, first slot, chunks
-        const float *pp = P.partials + (int64_t(b) * n_part + sp.z) * C;
-        const uint32_t *pa = IS_MAX ? P.partial_arg + (int64_t(b) * n_part + sp.z) * C : nullptr;
-        float inv = 1.f;
-        if (P.mean) inv = 1.f / float(__ldg(P.starts + sp.x + 1) - __ldg(P.starts + sp.x));
-        float *out = P.out + int64_t(b) * C * P.n_cells + sp.y;
-        for (int c = lane; c < C; c += 32) {
-            float v = pp[c];
-            uint32_t a = IS_MAX ? pa[c] : 0u;
-            uint32_t k = 1;
-            // 4 independent loads in flight, added in chunk order
-            for (; k + 4 <= sp.w; k += 4) {
-                float x[4];
+        const float *pp = P.partials + (int64_t(b) * n_part + sp.z) * C + c;
+        const uint32_t *pa = IS_MAX ? P.partial_arg + (int64_t(b) * n_part + sp.z) * C + c : nullptr;
+        float v = 0.f;
+        uint32_t a = 0u;
+        for (uint32_t k0 = 0; k0 < sp.w; k0 += 8) {
+            float x[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) x[q] = pp[int64_t(k + q) * C + c];
+            for (int q = 0; q < 8; ++q) x[q] = k0 + q < sp.w ? pp[int64_t(k0 + q) * C] : 0.f;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (IS_MAX) {
-                        if (x[q] > v) {
-                            v = x[q];
-                            a = pa[int64_t(k + q) * C + c];
-                        }
-                    } else {
-                        v += x[q];
-                    }
-                }
-            }
-            for (; k < sp.w; ++k) {
-                const float x = pp[int64_t(k) * C + c];
+            for (int q = 0; q < 8; ++q) {
+                if (k0 + q >= sp.w) break;
                 if (IS_MAX) {
-                    if (x > v) {
-                        v = x;
-                        a = pa[int64_t(k) * C + c];
+                    if (k0 + q == 0 || x[q] > v) {
+                        v = x[q];
+                        a = pa[int64_t(k0 + q) * C];
                     }
                 } else {
-                    v += x;
+                    v = (k0 + q == 0) ? x[q] : v + x[q];
                 }
             }
-            out[int64_t(c) * P.n_cells] = v * inv;
-            if (IS_MAX && P.argmax) P.argmax[(b * P.n_int_max + sp.x) * C + c] = __ldg(P.ranks + a);
         }
+        float inv = 1.f;
+        if (P.mean) inv = 1.f / float(__ldg(P.starts + sp.x + 1) - __ldg(P.starts + sp.x));
+        P.out[int64_t(b) * C * P.n_cells + int64_t(c) * P.n_cells + sp.y] = v * inv;
+        if (IS_MAX && P.argmax) P.argmax[(b * P.n_int_max + sp.x) * C + c] = __ldg(P.ranks + a);
     }
 }
 
@@ -301,7 +290,8 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
 #undef BVP_IVL_LAUNCH
     if (p.max_splits > 0) {
         const dim3 cg(static_cast<unsigned>(std::max<int64_t>(
-                          1, std::min<int64_t>(ceil_div(p.max_splits, kPoolWarps), kNumSms * 8))),
+                          1, std::min<int64_t>(ceil_div(p.max_splits * p.C, kPoolThreads),
+                                               kNumSms * 16))),
                       static_cast<unsigned>(B));
         if (is_max) pool_ivl_combine_kernel<true><<<cg, kPoolThreads, 0, s>>>(p);
         else pool_ivl_combine_kernel<false><<<cg, kPoolThreads, 0, s>>>(p);
