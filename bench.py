@@ -284,8 +284,15 @@ def main():
     from paper_2205_13542_b200.shard import max_over_ranks, sample_seeds
 
     rank, world, local = dist_env()
+    # one process per GPU; BVP_BENCH_BACKEND=gloo + more ranks than GPUs is
+    # only for exercising the multi-rank path on a single-GPU box
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BVP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     spec = bp.CONFIGS[CONFIG_NAME]

@@ -40,11 +40,16 @@ def _initialized() -> bool:
     return tdist.is_available() and tdist.is_initialized()
 
 
+def _coll_device(device):
+    """gloo reduces host tensors; NCCL device tensors."""
+    return None if tdist.get_backend() == "gloo" else device
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar (device-timed step time) over all ranks."""
     if not _initialized() or tdist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     return float(t.item())
 
@@ -52,7 +57,7 @@ def max_over_ranks(value: float, device=None) -> float:
 def sum_over_ranks(value: float, device=None) -> float:
     if not _initialized() or tdist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     tdist.all_reduce(t, op=tdist.ReduceOp.SUM)
     return float(t.item())
 
