@@ -180,13 +180,17 @@ int bvp_point_meta(const uint32_t *ranks, const int64_t *counts, int N, int H,
  * cut into chunks of <= chunk points; chunks are listed longest first, so a
  * warp's 8 lane groups (one chunk each) finish together.  An interval cut
  * into several chunks ("split") gets one fp32 partial per chunk, combined in
- * chunk order by a second pass.  Capacities: work n_int + n_in / chunk + 1
- * (bvp_work_capacity), splits n_int.  work_counts: device int64[3] receiving
+ * chunk order by a second pass.  tile: 0 = longest first (cell order within
+ * a length); > 0 = by tile x tile cell blocks, longest first within one;
+ * -1 = cell order, no sort (per-frame rebuilds).  Capacities: work
+ * n_int + n_in / chunk + 1 (bvp_work_capacity), splits n_int.  work_counts: device int64[3] receiving
  * n_work, n_splits, n_partials.  Run after the cache build. */
 int64_t bvp_work_capacity(int64_t n_int_max, int64_t n_points, int chunk);
-size_t bvp_work_workspace_bytes(int64_t n_int_max, int64_t n_points, int chunk);
+size_t bvp_work_workspace_bytes(int64_t n_int_max, int64_t n_points, int chunk,
+                                int nx, int ny, int tile);
 int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cells,
                   const int64_t *counts, int64_t n_int_max, int64_t n_points, int chunk,
+                  int nx, int ny, int tile,
                   uint32_t *work, uint32_t *splits, int64_t *work_counts,
                   void *workspace, size_t workspace_bytes, void *stream);
 

@@ -124,6 +124,9 @@ UNIT_BUDGET = 128
 TASK_BUDGET = 384
 #: chunk length of the fast kernels' work list (csrc/work.cu); 0 disables it
 CHUNK = int(os.environ.get("BVP_CHUNK", "64"))
+#: chunk order: 0 = longest first (cell order within a length); > 0 = by 2D
+#: tiles of WORK_TILE x WORK_TILE cells, longest first within a tile
+WORK_TILE = int(os.environ.get("BVP_WORK_TILE", "0"))
 
 
 def work_bounds(n_points: int, n_int_max: int, chunk: int) -> tuple[int, int, int]:
@@ -311,7 +314,8 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
     cap = int(lib.bvp_units_capacity(nx, ny, n_cells))
     n_int_max = min(n_cells, P)
     ws = max(lib.bvp_sort_workspace_bytes(P, n_cells), lib.bvp_units_workspace_bytes(nx, ny),
-             lib.bvp_work_workspace_bytes(n_int_max, P, CHUNK) if CHUNK > 0 else 0)
+             lib.bvp_work_workspace_bytes(n_int_max, P, CHUNK, nx, ny, WORK_TILE)
+             if CHUNK > 0 else 0)
     work = {}
     if CHUNK > 0:
         mw, ms, mp = work_bounds(P, n_int_max, CHUNK)
@@ -333,7 +337,7 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
 
 
 def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
-                   task_budget: int = TASK_BUDGET) -> None:
+                   task_budget: int = TASK_BUDGET, work_tile: int = WORK_TILE) -> None:
     """Work units and tasks, plus the point gather table when the frustum
     dims are known."""
     N, H, W, D = dims if dims is not None else (1, 1, 1, 1)
@@ -344,7 +348,8 @@ def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
               stream_ptr(dev))
     if "work" in b:
         _lib.call("bvp_make_work", ptr(b["starts"]), ptr(b["icells"]), ptr(b["counts"]),
-                  b["n_int_max"], b["ranks"].numel(), CHUNK, ptr(b["work"]), ptr(b["splits"]),
+                  b["n_int_max"], b["ranks"].numel(), CHUNK, nx, ny, work_tile, ptr(b["work"]),
+                  ptr(b["splits"]),
                   ptr(b["work_counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
 
 
@@ -370,12 +375,15 @@ class CacheBuilder:
     aliases the builder's buffers until the next ``build``."""
 
     def __init__(self, n_cameras: int, frustum: FrustumSpec, grid: BevGridSpec, device=None,
-                 unit_budget: int = UNIT_BUDGET):
+                 unit_budget: int = UNIT_BUDGET, sort_work: bool = False):
         self.dev = cuda_device(device)
         self.n_cameras, self.frustum, self.grid = n_cameras, frustum, grid
         self.P = n_cameras * frustum.points_per_camera
         self.bufs = _alloc(self.P, grid.nx, grid.ny, self.dev)
         self.unit_budget = unit_budget
+        # per-frame rebuilds keep the chunk list in cell order (the length
+        # sort costs more than it saves once per frame); cached builds sort
+        self.work_tile = WORK_TILE if sort_work else -1
         self._grid_arr = grid.as_array()
 
     def build(self, cams: torch.Tensor, fingerprint: int = 0) -> AssociationCache:
@@ -390,7 +398,7 @@ class CacheBuilder:
                   ptr(b["cell_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
                   b["ws"].numel(), stream_ptr(self.dev))
         dims = (self.n_cameras, f.height, f.width, f.depth_bins)
-        _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims)
+        _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims, work_tile=self.work_tile)
         return _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
 
 
@@ -402,7 +410,7 @@ def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
     arrays are bit-identical to the reference's.
     """
     cams = rig_rows(rig)
-    builder = CacheBuilder(len(rig), frustum_spec, grid_spec, device)
+    builder = CacheBuilder(len(rig), frustum_spec, grid_spec, device, sort_work=True)
     cams_d = torch.from_numpy(cams).to(builder.dev)
     cache = builder.build(cams_d, fingerprint_inputs(rig, frustum_spec, grid_spec))
     cache._counts()  # one sync: sizes known on the host from here on

@@ -51,7 +51,9 @@ __global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
                                  const uint32_t *__restrict__ cbase,
                                  const uint32_t *__restrict__ pbase,
                                  const uint32_t *__restrict__ sbase, uint4 *__restrict__ tmp,
-                                 uint32_t *__restrict__ keys, uint4 *__restrict__ splits) {
+                                 uint32_t *__restrict__ keys, uint4 *__restrict__ splits,
+                                 int ny, int tile) {
+    const int tiles_y = tile > 0 ? (ny + tile - 1) / tile : 1;
     const int64_t n_int = counts[1];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_int;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -63,7 +65,14 @@ __global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
             const uint32_t dest = split ? (kSplitDest | (pbase[i] + k)) : cell;
             // .w: the interval, or for a chunk of a split interval its split index
             tmp[cbase[i] + k] = make_uint4(a, e, dest, split ? sbase[i] : static_cast<uint32_t>(i));
-            keys[cbase[i] + k] = chunk - (e - a);  // bucket 0 = longest
+            // bucket 0 = longest; tile > 0: 2D cell tiles first (L1 reuse of
+            // the feature rows shared by neighbouring cells), length within
+            uint32_t key = chunk - (e - a);
+            if (tile > 0) {
+                const uint32_t ix = cell / uint32_t(ny), iy = cell - ix * uint32_t(ny);
+                key += (chunk + 1) * ((ix / tile) * tiles_y + iy / tile);
+            }
+            keys[cbase[i] + k] = key;
         }
         if (split) splits[sbase[i]] = make_uint4(static_cast<uint32_t>(i), cell, pbase[i], nch);
     }
@@ -101,7 +110,12 @@ struct WorkLayout {
 static int64_t work_cap(int64_t n_int_max, int64_t n_points, int chunk) {
     return chunk > 0 ? n_int_max + n_points / chunk + 1 : 0;
 }
-static WorkLayout work_layout(int64_t n_int_max, int64_t n_points, int chunk) {
+static int64_t work_keys(int chunk, int nx, int ny, int tile) {
+    if (tile < 0) return 1;  // unsorted: no sort workspace
+    const int64_t nt = tile > 0 ? int64_t((nx + tile - 1) / tile) * ((ny + tile - 1) / tile) : 1;
+    return nt * (chunk + 1);
+}
+static WorkLayout work_layout(int64_t n_int_max, int64_t n_points, int chunk, int64_t nkeys) {
     WorkLayout L{};
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     const size_t n = size_t(n_int_max);
@@ -115,11 +129,11 @@ static WorkLayout work_layout(int64_t n_int_max, int64_t n_points, int chunk) {
     L.off_tmp = o; o = al(o + size_t(cap) * 16);
     L.off_keys = o; o = al(o + size_t(cap) * 4);
     L.off_order = o; o = al(o + size_t(cap) * 4);
-    L.off_sstarts = o; o = al(o + size_t(chunk + 2) * 4);
-    L.off_scells = o; o = al(o + size_t(chunk + 2) * 4);
-    L.off_sfirst = o; o = al(o + size_t(chunk + 2) * 4);
+    L.off_sstarts = o; o = al(o + size_t(nkeys + 1) * 4);
+    L.off_scells = o; o = al(o + size_t(nkeys + 1) * 4);
+    L.off_sfirst = o; o = al(o + size_t(nkeys + 1) * 4);
     L.off_scounts = o; o = al(o + 16);
-    L.sort_ws = bvp_sort_workspace_bytes(cap, chunk + 1);
+    L.sort_ws = bvp_sort_workspace_bytes(cap, nkeys);
     L.off_sws = o; o = al(o + L.sort_ws);
     L.bytes = o;
     return L;
@@ -135,19 +149,22 @@ int64_t bvp_work_capacity(int64_t n_int_max, int64_t n_points, int chunk) {
     return work_cap(n_int_max, n_points, chunk);
 }
 
-size_t bvp_work_workspace_bytes(int64_t n_int_max, int64_t n_points, int chunk) {
-    return work_layout(n_int_max, n_points, chunk).bytes;
+size_t bvp_work_workspace_bytes(int64_t n_int_max, int64_t n_points, int chunk, int nx, int ny,
+                                int tile) {
+    return work_layout(n_int_max, n_points, chunk, work_keys(chunk, nx, ny, tile)).bytes;
 }
 
 int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cells,
                   const int64_t *counts, int64_t n_int_max, int64_t n_points, int chunk,
-                  uint32_t *work, uint32_t *splits, int64_t *work_counts, void *workspace,
-                  size_t workspace_bytes, void *stream) {
+                  int nx, int ny, int tile, uint32_t *work, uint32_t *splits,
+                  int64_t *work_counts, void *workspace, size_t workspace_bytes, void *stream) {
     BVP_REQUIRE(interval_starts && interval_cells && counts && work && splits && work_counts,
                 BVP_ERR_INVALID, "null pointer argument");
     BVP_REQUIRE(chunk >= 1 && chunk <= 4096 && n_int_max >= 1 && n_points >= 1, BVP_ERR_INVALID,
                 "bad chunk %d or sizes", chunk);
-    const WorkLayout L = work_layout(n_int_max, n_points, chunk);
+    BVP_REQUIRE(nx >= 1 && ny >= 1 && tile >= -1, BVP_ERR_INVALID, "bad grid / tile");
+    const int64_t nkeys = work_keys(chunk, nx, ny, tile);
+    const WorkLayout L = work_layout(n_int_max, n_points, chunk, nkeys);
     BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
                 "work workspace too small: need %zu bytes", L.bytes);
     cudaStream_t s = as_stream(stream);
@@ -168,14 +185,19 @@ int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cell
     device_excl_scan<uint32_t>(nsplit, nsplit, n_int_max, part, tot + 2, s);
     work_emit_kernel<<<blocks, 256, 0, s>>>(interval_starts, interval_cells, counts,
                                             uint32_t(chunk), nch, npart, nsplit, tmp, keys,
-                                            reinterpret_cast<uint4 *>(splits));
+                                            reinterpret_cast<uint4 *>(splits), ny, tile);
     const int64_t cap = work_cap(n_int_max, n_points, chunk);
     const unsigned cb = static_cast<unsigned>(std::min<int64_t>(ceil_div(cap, 256), 4096));
+    if (tile < 0) {  // cell order as emitted (per-frame builds: no sort)
+        cudaMemcpyAsync(work, tmp, size_t(cap) * 16, cudaMemcpyDeviceToDevice, s);
+        work_counts_kernel<<<1, 1, 0, s>>>(tot + 0, tot + 2, tot + 1, work_counts);
+        return check_launch("make_work");
+    }
     work_keys_tail_kernel<<<cb, 256, 0, s>>>(tot + 0, cap, keys);
     // stable counting sort by length bucket (the association's own sort):
     // longest chunks first, cell order within a bucket, so a warp's groups
     // store to neighbouring cells
-    const int rc = bvp_sort_intervals(keys, cap, chunk + 1, order,
+    const int rc = bvp_sort_intervals(keys, cap, nkeys, order,
                                       reinterpret_cast<uint32_t *>(ws + L.off_sstarts),
                                       reinterpret_cast<uint32_t *>(ws + L.off_scells),
                                       reinterpret_cast<uint32_t *>(ws + L.off_sfirst), nullptr,
