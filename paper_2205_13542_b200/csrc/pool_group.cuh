@@ -191,8 +191,9 @@ struct GroupStream {
     }
 };
 
-template <int CPL, int VEC, bool IS_MAX>
-__device__ __forceinline__ void gacc(float (&acc)[CPL][VEC], uint32_t (&arg)[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1],
+// ARG: track the winning point of MAX (autograd); false keeps MAX's value only
+template <int CPL, int VEC, bool IS_MAX, bool ARG = IS_MAX>
+__device__ __forceinline__ void gacc(float (&acc)[CPL][VEC], uint32_t (&arg)[ARG ? CPL : 1][ARG ? VEC : 1],
                                      uint32_t j, bool ok, float w, const float (&v)[CPL][VEC]) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
@@ -200,9 +201,13 @@ __device__ __forceinline__ void gacc(float (&acc)[CPL][VEC], uint32_t (&arg)[IS_
         for (int x = 0; x < VEC; ++x) {
             if (IS_MAX) {
                 const float pv = w * v[k][x];
-                if (ok && pv > acc[k][x]) {
+                if (ARG) {
+                    if (ok && pv > acc[k][x]) {
+                        acc[k][x] = pv;
+                        arg[ARG ? k : 0][ARG ? x : 0] = j;
+                    }
+                } else if (ok && pv > acc[k][x]) {  // first maximum, as the reference
                     acc[k][x] = pv;
-                    arg[IS_MAX ? k : 0][IS_MAX ? x : 0] = j;
                 }
             } else {
                 acc[k][x] = fmaf(w, v[k][x], acc[k][x]);
@@ -210,14 +215,14 @@ __device__ __forceinline__ void gacc(float (&acc)[CPL][VEC], uint32_t (&arg)[IS_
         }
 }
 
-template <int CPL, int VEC, bool IS_MAX>
-__device__ __forceinline__ void greset(float (&acc)[CPL][VEC], uint32_t (&arg)[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1]) {
+template <int CPL, int VEC, bool IS_MAX, bool ARG = IS_MAX>
+__device__ __forceinline__ void greset(float (&acc)[CPL][VEC], uint32_t (&arg)[ARG ? CPL : 1][ARG ? VEC : 1]) {
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
 #pragma unroll
         for (int x = 0; x < VEC; ++x) {
             acc[k][x] = IS_MAX ? -INFINITY : 0.f;
-            if (IS_MAX) arg[IS_MAX ? k : 0][IS_MAX ? x : 0] = 0xFFFFFFFFu;
+            if (ARG) arg[ARG ? k : 0][ARG ? x : 0] = 0xFFFFFFFFu;
         }
 }
 

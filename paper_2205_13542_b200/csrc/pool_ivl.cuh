@@ -89,7 +89,7 @@ struct RawChunk<__nv_bfloat16, 1> {
 #define BVP_IVL_MIN_BLOCKS 3
 #endif
 
-template <typename Elem, int VEC, int CPL, bool IS_MAX, int SRC>
+template <typename Elem, int VEC, int CPL, bool IS_MAX, int SRC, bool ARG = IS_MAX>
 __global__ void __launch_bounds__(kPoolThreads, sizeof(Elem) == 2 ? BVP_IVL_MIN_BLOCKS + 1
                                                                   : BVP_IVL_MIN_BLOCKS)
 pool_ivl_kernel(const PoolParams P, int L, int lg) {
@@ -130,8 +130,8 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
         for (int o = 16; o >= 1; o >>= 1) steps = max(steps, __shfl_xor_sync(0xFFFFFFFFu, steps, o));
 
         float acc[CPL][VEC];
-        uint32_t arg[IS_MAX ? CPL : 1][IS_MAX ? VEC : 1];
-        greset<CPL, VEC, IS_MAX>(acc, arg);
+        uint32_t arg[ARG ? CPL : 1][ARG ? VEC : 1];
+        greset<CPL, VEC, IS_MAX, ARG>(acc, arg);
         // rows of two steps in flight: fetch(s + 1) is issued before the
         // FMAs of step s; each fetch also loads the next step's record
         uint2 m = len > 0 ? rec_of(j0) : make_uint2(0u, 0u);
@@ -155,7 +155,7 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
             float v[CPL][VEC];
 #pragma unroll
             for (int k = 0; k < CPL; ++k) RawChunk<Elem, VEC>::unpack(raw[k], v[k]);
-            gacc<CPL, VEC, IS_MAX>(acc, arg, j, true, w, v);
+            gacc<CPL, VEC, IS_MAX, ARG>(acc, arg, j, true, w, v);
         };
         float wa, wb;
         Raw va[CPL], vb[CPL];
@@ -180,15 +180,15 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
                     for (int x = 0; x < VEC; ++x) {
                         const int c = ch * VEC + x;
                         out[int64_t(c) * P.n_cells] = acc[k][x] * inv;
-                        if (IS_MAX && P.argmax)
+                        if (ARG && P.argmax)
                             P.argmax[(b * P.n_int_max + r.w) * C + c] =
-                                __ldg(P.ranks + arg[IS_MAX ? k : 0][IS_MAX ? x : 0]);
+                                __ldg(P.ranks + arg[ARG ? k : 0][ARG ? x : 0]);
                     }
             }
         } else {  // one chunk of a split interval: its partial
             const int64_t slot = int64_t(b) * n_part + (r.z & ~kIvlSplit);
             float *pp = P.partials + slot * C;
-            uint32_t *pa = IS_MAX ? P.partial_arg + slot * C : nullptr;
+            uint32_t *pa = ARG ? P.partial_arg + slot * C : nullptr;
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
                 const int ch = li + k * L;
@@ -196,7 +196,7 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) {
                         pp[ch * VEC + x] = acc[k][x];
-                        if (IS_MAX) pa[ch * VEC + x] = arg[IS_MAX ? k : 0][IS_MAX ? x : 0];
+                        if (ARG) pa[ch * VEC + x] = arg[ARG ? k : 0][ARG ? x : 0];
                     }
             }
         }
@@ -207,7 +207,7 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
 // partials in chunk order (MAX: the first maximum in rank order), scale
 // (MEAN), store the cell's value.  Loads of up to 8 chunks are issued before
 // the in-order adds, so a thread waits ~2 memory latencies, not one per chunk.
-template <bool IS_MAX>
+template <bool IS_MAX, bool ARG = IS_MAX>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_ivl_combine_kernel(const PoolParams P) {
     const int b = blockIdx.y;
@@ -221,7 +221,7 @@ pool_ivl_combine_kernel(const PoolParams P) {
         const int c = static_cast<int>(e - s * C);
         const uint4 sp = __ldg(P.splits + s);  // interval, cell, first slot, chunks
         const float *pp = P.partials + (int64_t(b) * n_part + sp.z) * C + c;
-        const uint32_t *pa = IS_MAX ? P.partial_arg + (int64_t(b) * n_part + sp.z) * C + c : nullptr;
+        const uint32_t *pa = ARG ? P.partial_arg + (int64_t(b) * n_part + sp.z) * C + c : nullptr;
         float v = 0.f;
         uint32_t a = 0u;
         for (uint32_t k0 = 0; k0 < sp.w; k0 += 8) {
@@ -234,7 +234,7 @@ pool_ivl_combine_kernel(const PoolParams P) {
                 if (IS_MAX) {
                     if (k0 + q == 0 || x[q] > v) {
                         v = x[q];
-                        a = pa[int64_t(k0 + q) * C];
+                        if (ARG) a = pa[int64_t(k0 + q) * C];
                     }
                 } else {
                     v = (k0 + q == 0) ? x[q] : v + x[q];
@@ -244,7 +244,7 @@ pool_ivl_combine_kernel(const PoolParams P) {
         float inv = 1.f;
         if (P.mean) inv = 1.f / float(__ldg(P.starts + sp.x + 1) - __ldg(P.starts + sp.x));
         P.out[int64_t(b) * C * P.n_cells + int64_t(c) * P.n_cells + sp.y] = v * inv;
-        if (IS_MAX && P.argmax) P.argmax[(b * P.n_int_max + sp.x) * C + c] = __ldg(P.ranks + a);
+        if (ARG && P.argmax) P.argmax[(b * P.n_int_max + sp.x) * C + c] = __ldg(P.ranks + a);
     }
 }
 
@@ -269,9 +269,10 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
                 "pool scratch too small: need %zu bytes (bvp_pool_scratch_bytes)", need);
     PoolParams p = p0;
     p.partials = static_cast<float *>(scratch);
-    p.partial_arg = is_max ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
-                                                          size_t(B) * p0.chunk_partials * p0.C)
-                           : nullptr;
+    const bool arg = is_max && p0.argmax;  // MAX winners only for autograd
+    p.partial_arg = arg ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
+                                                       size_t(B) * p0.chunk_partials * p0.C)
+                        : nullptr;
     cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
     const int G = 32 >> lg;
     const int64_t batches = ceil_div(p.max_work, G);
@@ -279,11 +280,12 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
                         1, std::min<int64_t>(ceil_div(batches, kPoolWarps),
                                              int64_t(kNumSms) * BVP_IVL_MIN_BLOCKS * 4))),
                     static_cast<unsigned>(B));
-#define BVP_IVL_LAUNCH(CPLV)                                                     \
-    if (cpl == CPLV) {                                                           \
-        auto k = is_max ? pool_ivl_kernel<Elem, VEC, CPLV, true, SRC>            \
-                        : pool_ivl_kernel<Elem, VEC, CPLV, false, SRC>;          \
-        k<<<grid, kPoolThreads, 0, s>>>(p, L, lg);                               \
+#define BVP_IVL_LAUNCH(CPLV)                                                          \
+    if (cpl == CPLV) {                                                                \
+        auto k = !is_max ? pool_ivl_kernel<Elem, VEC, CPLV, false, SRC>               \
+                 : arg   ? pool_ivl_kernel<Elem, VEC, CPLV, true, SRC, true>          \
+                         : pool_ivl_kernel<Elem, VEC, CPLV, true, SRC, false>;        \
+        k<<<grid, kPoolThreads, 0, s>>>(p, L, lg);                                    \
     }
     BVP_IVL_LAUNCH(1) BVP_IVL_LAUNCH(2) BVP_IVL_LAUNCH(3)
     BVP_IVL_LAUNCH(4) BVP_IVL_LAUNCH(5) BVP_IVL_LAUNCH(6)
@@ -293,7 +295,8 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
                           1, std::min<int64_t>(ceil_div(p.max_splits * p.C, kPoolThreads),
                                                kNumSms * 16))),
                       static_cast<unsigned>(B));
-        if (is_max) pool_ivl_combine_kernel<true><<<cg, kPoolThreads, 0, s>>>(p);
+        if (arg) pool_ivl_combine_kernel<true, true><<<cg, kPoolThreads, 0, s>>>(p);
+        else if (is_max) pool_ivl_combine_kernel<true, false><<<cg, kPoolThreads, 0, s>>>(p);
         else pool_ivl_combine_kernel<false><<<cg, kPoolThreads, 0, s>>>(p);
     }
     return BVP_OK;
