@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import BevPoolError, ConfigurationError, ValidationError
+from .errors import CudaError, ExtensionMissingError, from_status  # noqa: F401
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbevpool_sm100.so")
 
@@ -19,14 +19,6 @@ BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
 TILE_CELLS = 32
 OUT_OF_RANGE = 0xFFFFFFFF
 ABI_VERSION = 5
-
-
-class ExtensionMissingError(BevPoolError, RuntimeError):
-    """libbevpool_sm100.so is not built or cannot be loaded."""
-
-
-class CudaError(BevPoolError, RuntimeError):
-    """A CUDA launch inside the library failed."""
 
 
 _P = ctypes.c_void_p
@@ -122,12 +114,7 @@ def check(rc: int, what: str) -> None:
     """Map a C-ABI status to the reference's exception types."""
     if rc == BVP_OK:
         return
-    msg = f"{what}: {load().bvp_last_error().decode(errors='replace')}"
-    if rc == BVP_ERR_INVALID:
-        raise ValidationError(msg)
-    if rc == BVP_ERR_UNSUPPORTED:
-        raise ConfigurationError(msg)
-    raise CudaError(msg)
+    raise from_status(rc, f"{what}: {load().bvp_last_error().decode(errors='replace')}")
 
 
 def call(name: str, *args) -> None:

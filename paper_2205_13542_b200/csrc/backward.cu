@@ -163,7 +163,10 @@ pool_backward_kernel(const float *__restrict__ gT, const uint32_t *__restrict__ 
 // 4-point window are loaded one lane per point and shuffled, a window ahead.
 // Every gradient element is written by exactly one lane: no atomics.
 template <int CPL>
-__global__ void __launch_bounds__(256, 2)
+#ifndef BVP_BWD_MIN_BLOCKS
+#define BVP_BWD_MIN_BLOCKS 2
+#endif
+__global__ void __launch_bounds__(256, BVP_BWD_MIN_BLOCKS)
 pool_backward_grp_kernel(const float *__restrict__ gT, const float *__restrict__ feats_nhwc,
                          const float *__restrict__ dist, const uint32_t *__restrict__ iop, int N,
                          int C, int HW, int D, int64_t n_int_max, int L, int lg,
