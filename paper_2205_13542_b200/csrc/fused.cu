@@ -84,6 +84,9 @@ pixel_lse_kernel(const __nv_bfloat16 *__restrict__ logits, int64_t NB, int D, in
 __global__ void __launch_bounds__(32 * kLseWarps)
 pixel_softmax_kernel(const __nv_bfloat16 *__restrict__ logits, int64_t NB, int D, int HW,
                      float *__restrict__ wout) {
+    // each thread's depth planes d = warp + 8 q (q < kQ) are loaded at once and
+    // kept in registers: one read of the logits, independent loads in flight
+    constexpr int kQ = 16;  // D <= 128 in registers; larger D re-reads
     __shared__ float s_m[kLseWarps][32], s_s[kLseWarps][32], s_lse[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tiles = (HW + 31) / 32;
@@ -91,13 +94,22 @@ pixel_softmax_kernel(const __nv_bfloat16 *__restrict__ logits, int64_t NB, int D
     const int hw = (blockIdx.x - n * tiles) * 32 + lane;
     const bool ok = hw < HW;
     const __nv_bfloat16 *l = logits + n * D * int64_t(HW) + (ok ? hw : 0);
-    float m = -INFINITY, sum = 0.f;
-    for (int d = warp; d < D; d += kLseWarps) {
-        const float v = __bfloat162float(l[int64_t(d) * HW]);
-        const float nm = fmaxf(m, v);
-        sum = sum * __expf(m - nm) + __expf(v - nm);
-        m = nm;
+    float v[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const int d = warp + q * kLseWarps;
+        v[q] = d < D ? __bfloat162float(l[int64_t(d) * HW]) : -INFINITY;
     }
+    float m = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) m = fmaxf(m, v[q]);
+    for (int d = warp + kQ * kLseWarps; d < D; d += kLseWarps)
+        m = fmaxf(m, __bfloat162float(l[int64_t(d) * HW]));
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) sum += v[q] == -INFINITY ? 0.f : __expf(v[q] - m);
+    for (int d = warp + kQ * kLseWarps; d < D; d += kLseWarps)
+        sum += __expf(__bfloat162float(l[int64_t(d) * HW]) - m);
     s_m[warp][lane] = m;
     s_s[warp][lane] = sum;
     __syncthreads();
@@ -113,7 +125,12 @@ pixel_softmax_kernel(const __nv_bfloat16 *__restrict__ logits, int64_t NB, int D
     if (!ok) return;
     const float lse = s_lse[lane];
     float *wo = wout + n * D * int64_t(HW) + hw;
-    for (int d = warp; d < D; d += kLseWarps)
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const int d = warp + q * kLseWarps;
+        if (d < D) wo[int64_t(d) * HW] = __expf(v[q] - lse);
+    }
+    for (int d = warp + kQ * kLseWarps; d < D; d += kLseWarps)
         wo[int64_t(d) * HW] = __expf(__bfloat162float(l[int64_t(d) * HW]) - lse);
 }
 
