@@ -19,6 +19,7 @@ constexpr int kKeysPerThread = 16;
 constexpr int kSortTile = kSortThreads * kKeysPerThread;  // 4096 keys per CTA
 constexpr int kMaxDigitBits = 10;
 constexpr int kMaxDigits = 1 << kMaxDigitBits;
+constexpr int64_t kCountSortMaxRun = 64;  // counting sort while P <= 64 * n_cells
 
 struct GridParams {
     double x_min, y_min, z_min, z_max, r;
@@ -38,20 +39,9 @@ struct FrustumParams {
 //   e_j = fma(R[j][2],pz, fma(R[j][1],py, R[j][0]*px)) + t_j
 //        (the OpenBLAS dgemm rounding of geometry.py:185-186)
 //   ix = floor((x - x_min)/r) ...                  bevgrid.py:88-96
-__device__ __forceinline__ uint32_t point_cell(const double *__restrict__ cams,
-                                               const FrustumParams &f,
-                                               const GridParams &g, int64_t p) {
-    const int d = static_cast<int>(p % f.D);
-    int64_t rest = p / f.D;
-    const int w = static_cast<int>(rest % f.W);
-    rest /= f.W;
-    const int h = static_cast<int>(rest % f.H);
-    const int n = static_cast<int>(rest / f.H);
-    const double *c = cams + 16 * n;
-    const double fx = __ldg(c + 0), fy = __ldg(c + 1), cx = __ldg(c + 2), cy = __ldg(c + 3);
+__device__ __forceinline__ uint32_t cell_at(const double *__restrict__ c, const FrustumParams &f,
+                                            const GridParams &g, double dx, double dy, int d) {
     const double depth = __dadd_rn(f.d_min, __dmul_rn(f.d_step, static_cast<double>(d)));
-    const double dx = __ddiv_rn(__dsub_rn(static_cast<double>(w), cx), fx);
-    const double dy = __ddiv_rn(__dsub_rn(static_cast<double>(h), cy), fy);
     const double px = __dmul_rn(dx, depth), py = __dmul_rn(dy, depth), pz = depth;
     double e[3];
 #pragma unroll
@@ -67,6 +57,28 @@ __device__ __forceinline__ uint32_t point_cell(const double *__restrict__ cams,
         qy < static_cast<double>(g.ny) && e[2] >= g.z_min && e[2] < g.z_max)
         return static_cast<uint32_t>(static_cast<int64_t>(qx) * g.ny + static_cast<int64_t>(qy));
     return kOOR;
+}
+
+// The ray of pixel (h, w) of a camera: dx = (w - cx)/fx, dy = (h - cy)/fy.
+__device__ __forceinline__ void pixel_ray(const double *__restrict__ c, int h, int w, double &dx,
+                                          double &dy) {
+    dx = __ddiv_rn(__dsub_rn(static_cast<double>(w), __ldg(c + 2)), __ldg(c + 0));
+    dy = __ddiv_rn(__dsub_rn(static_cast<double>(h), __ldg(c + 3)), __ldg(c + 1));
+}
+
+__device__ __forceinline__ uint32_t point_cell(const double *__restrict__ cams,
+                                               const FrustumParams &f,
+                                               const GridParams &g, int64_t p) {
+    const int d = static_cast<int>(p % f.D);
+    int64_t rest = p / f.D;
+    const int w = static_cast<int>(rest % f.W);
+    rest /= f.W;
+    const int h = static_cast<int>(rest % f.H);
+    const int n = static_cast<int>(rest / f.H);
+    const double *c = cams + 16 * n;
+    double dx, dy;
+    pixel_ray(c, h, w, dx, dy);
+    return cell_at(c, f, g, dx, dy, d);
 }
 
 __global__ void frustum_cells_kernel(const double *__restrict__ cams, FrustumParams f,
@@ -247,12 +259,330 @@ __global__ void interval_of_point_kernel(const uint32_t *__restrict__ cells, int
     }
 }
 
+// ---- counting sort (bounded keys, short runs) ------------------------------
+// Used when the mean run per key is short (frustum association: ~15 points per
+// cell).  (1) count_front: cell of every point and an arrival slot in its cell
+// from the per-cell counter (atomicAdd's return value); (2) the per-cell
+// counts are scanned into interval tables (shared with the radix path); (3)
+// count_scatter: ranks[first_rank(cell) + slot] = p; (4) seg_sort: the slots
+// follow atomic arrival order, so every interval's run of point indices is
+// sorted ascending -- which restores the reference's stable order (ties by
+// point index, bevgrid.py:149) exactly.
+
+// Slot of this lane's point among the warp's points of the same cell: one
+// atomic per distinct cell (leader lane), ranks among peers by lane.
+__device__ __forceinline__ uint32_t claim_slot(uint32_t c, uint32_t *__restrict__ cell_count) {
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, c);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (c != kOOR && (threadIdx.x & 31) == leader) base = atomicAdd(&cell_count[c], __popc(peers));
+    base = __shfl_sync(0xFFFFFFFFu, base, leader);
+    return c != kOOR ? base + __popc(peers & lanemask_lt()) : 0u;
+}
+
+constexpr int kFrontPix = 32;    // pixels per tile (one per lane)
+constexpr int kFrontDepth = 64;  // depth bins per shared-memory pass
+
+// Tile t covers 32 consecutive pixels in column-major order q = (n*W + w)*H +
+// h: lanes run down an image column, i.e. along one vertical line in 3-D.
+// For a near-level camera that line projects into one or two BEV cells, so a
+// warp's 32 points at one depth bin mostly share a cell: one atomic claims
+// consecutive slots for all of them (in point order), and count_scatter's
+// stores for them are contiguous.  The sort stays exact for any rig.
+__device__ __forceinline__ uint32_t tile_pixel(const FrustumParams &f, uint32_t q) {
+    const uint32_t h = q % f.H, nw = q / f.H;
+    const uint32_t w = nw % f.W, n = nw / f.W;
+    return (n * f.H + h) * f.W + w;
+}
+
+// Frustum points, tile by tile (warps stride the depth bins).  The ray's two
+// divisions run once per pixel and warp.  Cells and slots are staged in
+// shared memory and written as contiguous per-pixel runs of depth bins.
+__global__ void __launch_bounds__(256)
+count_front_kernel(const double *__restrict__ cams, FrustumParams f, GridParams g,
+                   uint32_t *__restrict__ cells, uint32_t *__restrict__ cell_count,
+                   uint32_t *__restrict__ slot) {
+    __shared__ uint32_t s_cell[kFrontDepth][kFrontPix + 1], s_slot[kFrontDepth][kFrontPix + 1];
+    __shared__ uint32_t s_pix[kFrontPix];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t npix = static_cast<uint32_t>(f.N) * f.H * f.W;
+    const uint32_t ntiles = (npix + kFrontPix - 1) / kFrontPix;
+    const uint32_t D = static_cast<uint32_t>(f.D);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t q = tile * kFrontPix + lane;
+        const bool valid = q < npix;
+        const uint32_t h = q % f.H, nw = q / f.H;
+        const uint32_t w = nw % f.W, n = valid ? nw / f.W : 0;
+        if (warp == 0) s_pix[lane] = (n * f.H + h) * f.W + w;
+        const double *c = cams + 16 * n;
+        double dx, dy;
+        pixel_ray(c, static_cast<int>(h), static_cast<int>(w), dx, dy);
+        const int npx = static_cast<int>(min(npix - tile * kFrontPix, uint32_t(kFrontPix)));
+        for (uint32_t d0 = 0; d0 < D; d0 += kFrontDepth) {
+            const int nd = static_cast<int>(min(D - d0, uint32_t(kFrontDepth)));
+            for (int dd = warp; dd < nd; dd += 8) {
+                const uint32_t cc = valid ? cell_at(c, f, g, dx, dy, static_cast<int>(d0) + dd)
+                                          : kOOR;
+                s_slot[dd][lane] = claim_slot(cc, cell_count);
+                s_cell[dd][lane] = cc;
+            }
+            __syncthreads();
+            for (int i = warp; i < npx; i += 8) {
+                const uint32_t p0 = s_pix[i] * D + d0;
+                for (int dd = lane; dd < nd; dd += 32) {
+                    cells[p0 + dd] = s_cell[dd][i];
+                    slot[p0 + dd] = s_slot[dd][i];
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Given cells (no geometry): points in index order, one aggregated atomic per
+// distinct cell of a warp.
+__global__ void __launch_bounds__(256)
+count_cells_kernel(const uint32_t *__restrict__ cells, int64_t P,
+                   uint32_t *__restrict__ cell_count, uint32_t *__restrict__ slot) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < P; base += stride) {
+        const int64_t p = base + threadIdx.x;
+        const uint32_t cc = p < P ? cells[p] : kOOR;
+        const uint32_t sl = claim_slot(cc, cell_count);
+        if (p < P) slot[p] = sl;
+    }
+}
+
+__device__ __forceinline__ void scatter_point(uint32_t p, uint32_t c, uint32_t sl,
+                                              const unsigned long long *__restrict__ scanned,
+                                              uint32_t *__restrict__ ranks, uint32_t &iv) {
+    iv = kOOR;
+    if (c == kOOR) return;
+    const unsigned long long e = __ldg(scanned + c);
+    ranks[static_cast<uint32_t>(e & 0xFFFFFFFFull) + sl] = p;
+    iv = static_cast<uint32_t>(e >> 32);
+}
+
+// ranks[first(cell) + slot] = p (unsorted within a cell) and the interval of
+// every point.  scanned[c] = (interval index << 32) | first rank.  Frustum
+// layout: the tile of count_front_kernel read as per-pixel runs, then walked
+// depth-major so a warp's stores land on neighbouring cells.
+__global__ void __launch_bounds__(256)
+count_scatter_kernel(const uint32_t *__restrict__ cells, const uint32_t *__restrict__ slot,
+                     FrustumParams f, const unsigned long long *__restrict__ scanned,
+                     uint32_t *__restrict__ ranks, uint32_t *__restrict__ iop) {
+    __shared__ uint32_t s_cell[kFrontDepth][kFrontPix + 1], s_slot[kFrontDepth][kFrontPix + 1];
+    __shared__ uint32_t s_pix[kFrontPix];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t npix = static_cast<uint32_t>(f.N) * f.H * f.W;
+    const uint32_t ntiles = (npix + kFrontPix - 1) / kFrontPix;
+    const uint32_t D = static_cast<uint32_t>(f.D);
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int npx = static_cast<int>(min(npix - tile * kFrontPix, uint32_t(kFrontPix)));
+        if (warp == 0 && lane < npx) s_pix[lane] = tile_pixel(f, tile * kFrontPix + lane);
+        __syncthreads();
+        for (uint32_t d0 = 0; d0 < D; d0 += kFrontDepth) {
+            const int nd = static_cast<int>(min(D - d0, uint32_t(kFrontDepth)));
+            for (int i = warp; i < npx; i += 8) {
+                const uint32_t p0 = s_pix[i] * D + d0;
+                for (int dd = lane; dd < nd; dd += 32) {
+                    s_cell[dd][i] = cells[p0 + dd];
+                    s_slot[dd][i] = slot[p0 + dd];
+                }
+            }
+            __syncthreads();
+            for (int dd = warp; dd < nd; dd += 8) {
+                uint32_t iv = kOOR;
+                if (lane < npx)
+                    scatter_point(s_pix[lane] * D + d0 + dd, s_cell[dd][lane], s_slot[dd][lane],
+                                  scanned, ranks, iv);
+                s_slot[dd][lane] = iv;
+            }
+            __syncthreads();
+            if (iop)
+                for (int i = warp; i < npx; i += 8) {
+                    const uint32_t p0 = s_pix[i] * D + d0;
+                    for (int dd = lane; dd < nd; dd += 32) iop[p0 + dd] = s_slot[dd][i];
+                }
+            __syncthreads();
+        }
+    }
+}
+
+__global__ void count_scatter_flat_kernel(const uint32_t *__restrict__ cells,
+                                          const uint32_t *__restrict__ slot, int64_t P,
+                                          const unsigned long long *__restrict__ scanned,
+                                          uint32_t *__restrict__ ranks,
+                                          uint32_t *__restrict__ iop) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t iv;
+        scatter_point(static_cast<uint32_t>(p), cells[p], slot[p], scanned, ranks, iv);
+        if (iop) iop[p] = iv;
+    }
+}
+
+// Ascending bitonic sort of a run of L <= 32 K values held K per lane
+// (element lane + 32 m); missing elements are +inf.
+template <int K>
+__device__ __forceinline__ void warp_sort_run(uint32_t *r, int L, int lane) {
+    uint32_t v[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) v[m] = lane + 32 * m < L ? r[lane + 32 * m] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int k = 2; k <= 32 * K; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {  // partner in the same lane
+#pragma unroll
+                for (int m = 0; m < K; ++m) {
+                    const int m2 = m ^ (j >> 5);
+                    if (m2 > m) {
+                        const bool up = ((32 * m) & k) == 0;
+                        const uint32_t lo = min(v[m], v[m2]), hi = max(v[m], v[m2]);
+                        v[m] = up ? lo : hi;
+                        v[m2] = up ? hi : lo;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < K; ++m) {
+                    const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v[m], j);
+                    const bool up = ((lane + 32 * m) & k) == 0, lower = (lane & j) == 0;
+                    v[m] = (lower == up) ? min(v[m], o) : max(v[m], o);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < K; ++m)
+        if (lane + 32 * m < L) r[lane + 32 * m] = v[m];
+}
+
+// Ascending bitonic sort of a[0, L) by `nthreads` cooperating threads (the
+// all-ascending form: a mirror compare opens each merge, half-cleaners
+// follow).  Positions >= L act as +inf, so compares reaching past L are
+// skipped and nothing is padded.  `sync` orders the stages.
+template <typename Sync>
+__device__ __forceinline__ void bitonic_sort(uint32_t *a, int L, int tid, int nthreads,
+                                             Sync sync) {
+    int lgn = 0;
+    while ((1 << lgn) < L) ++lgn;
+    const int half = 1 << (lgn - 1);
+    for (int lk = 1; lk <= lgn; ++lk) {
+        for (int lj = lk - 1; lj >= 0; --lj) {
+            const int j = 1 << lj;
+            for (int i = tid; i < half; i += nthreads) {
+                const int blk = i >> lj, off = i & (j - 1);
+                int lo, hi;
+                if (lj == lk - 1) {  // mirror compare within blocks of 2^lk
+                    lo = (blk << lk) + off;
+                    hi = (blk << lk) + (1 << lk) - 1 - off;
+                } else {
+                    lo = (blk << (lj + 1)) + off;
+                    hi = lo + j;
+                }
+                if (hi < L) {
+                    const uint32_t x = a[lo], y = a[hi];
+                    if (x > y) {
+                        a[lo] = y;
+                        a[hi] = x;
+                    }
+                }
+            }
+            sync();
+        }
+    }
+}
+
+constexpr int kSegCtaMax = 8192;   // ... by one CTA: 8 warp-sorted slices, merged by rank
+
+__device__ __forceinline__ void warp_sort_any(uint32_t *r, int L, int lane) {
+    if (L <= 32) warp_sort_run<1>(r, L, lane);
+    else if (L <= 64) warp_sort_run<2>(r, L, lane);
+    else if (L <= 128) warp_sort_run<4>(r, L, lane);
+    else if (L <= 256) warp_sort_run<8>(r, L, lane);
+    else if (L <= 512) warp_sort_run<16>(r, L, lane);
+    else warp_sort_run<32>(r, L, lane);
+}
+
+// One warp per interval, runs of <= 256 points sorted in registers; longer
+// runs are queued for seg_sort_long_kernel (kept out of this kernel so its
+// register budget -- and occupancy -- stays that of the short runs).
+__global__ void __launch_bounds__(256)
+seg_sort_warp_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ starts,
+                     const int64_t *__restrict__ counts, uint32_t *__restrict__ long_list,
+                     uint32_t *__restrict__ n_long) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_int = counts[1];
+    const int64_t nwarps = int64_t(gridDim.x) * 8;
+    for (int64_t iv = int64_t(blockIdx.x) * 8 + warp; iv < n_int; iv += nwarps) {
+        const uint32_t lo = __ldg(starts + iv);
+        const int L = static_cast<int>(__ldg(starts + iv + 1) - lo);
+        if (L <= 1) continue;
+        if (L <= 32) warp_sort_run<1>(ranks + lo, L, lane);
+        else if (L <= 64) warp_sort_run<2>(ranks + lo, L, lane);
+        else if (L <= 128) warp_sort_run<4>(ranks + lo, L, lane);
+        else if (L <= 256) warp_sort_run<8>(ranks + lo, L, lane);
+        else if (lane == 0) long_list[atomicAdd(n_long, 1u)] = static_cast<uint32_t>(iv);
+    }
+}
+
+// One CTA per queued run (> 256 points): up to kSegCtaMax the run is staged
+// in shared memory, each warp sorts one slice in registers, and every value
+// goes straight to its
+// final place = its index in its slice + the number of smaller values in each
+// other slice (binary searches; the values -- point ids -- are distinct);
+// beyond, an in-place bitonic sort in global memory (correct for any length;
+// only degenerate grids with huge cells get there).
+__global__ void __launch_bounds__(256)
+seg_sort_long_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ starts,
+                     const uint32_t *__restrict__ long_list,
+                     const uint32_t *__restrict__ n_long) {
+    __shared__ uint32_t sh[kSegCtaMax];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nl = *n_long;
+    for (uint32_t k = blockIdx.x; k < nl; k += gridDim.x) {
+        const uint32_t iv = long_list[k];
+        const uint32_t lo = starts[iv];
+        const int L = static_cast<int>(starts[iv + 1] - lo);
+        uint32_t *r = ranks + lo;
+        if (L > kSegCtaMax) {
+            bitonic_sort(r, L, threadIdx.x, blockDim.x, []() { __syncthreads(); });
+            continue;
+        }
+        for (int i = threadIdx.x; i < L; i += blockDim.x) sh[i] = r[i];
+        __syncthreads();
+        const int cs = (L + 7) / 8;
+        const int a0 = min(L, warp * cs), a1 = min(L, a0 + cs);
+        if (a1 > a0) warp_sort_any(sh + a0, a1 - a0, lane);
+        __syncthreads();
+        for (int i = threadIdx.x; i < L; i += blockDim.x) {
+            const uint32_t x = sh[i];
+            const int own = i / cs;
+            int pos = i - own * cs;
+            for (int b = 0; b < 8; ++b) {
+                if (b == own) continue;
+                int l = min(L, b * cs), h = min(L, l + cs);
+                while (l < h) {  // first index in slice b with value > x
+                    const int m = (l + h) >> 1;
+                    if (sh[m] < x) l = m + 1;
+                    else h = m;
+                }
+                pos += l - min(L, b * cs);
+            }
+            r[pos] = x;
+        }
+        __syncthreads();
+    }
+}
+
 // ---- workspace layout -------------------------------------------------------
 struct SortLayout {
     int key_bits, passes, digit_bits;
     int64_t n_tiles, hist_len;
     size_t off_count, off_packed, off_keys_a, off_vals_a, off_keys_b, off_vals_b, off_hist,
-        off_part64, off_part32, off_total64, off_total32, bytes;
+        off_part64, off_part32, off_total64, off_total32, off_long, off_nlong, bytes;
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -278,6 +608,8 @@ static SortLayout sort_layout(int64_t P, int64_t n_cells) {
     L.off_part32 = o; o = align256(o + 4 * size_t(scan_partials_len<uint32_t>(L.hist_len)));
     L.off_total64 = o; o = align256(o + 8);
     L.off_total32 = o; o = align256(o + 8);
+    L.off_long = o; o = align256(o + 4 * size_t(n_cells));
+    L.off_nlong = o; o = align256(o + 8);
     L.bytes = o;
     return L;
 }
@@ -307,6 +639,28 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
     auto *total32 = reinterpret_cast<uint32_t *>(w + L.off_total32);
 
     cudaMemsetAsync(cell_count, 0, 4 * size_t(n_cells), s);
+    const unsigned cb = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_cells, 256), 4096));
+    if (P <= kCountSortMaxRun * n_cells) {  // counting sort: short runs per key
+        uint32_t *slot = ka;
+        auto *long_list = reinterpret_cast<uint32_t *>(w + L.off_long);
+        auto *n_long = reinterpret_cast<uint32_t *>(w + L.off_nlong);
+        cudaMemsetAsync(n_long, 0, 8, s);
+        if (cams)
+            count_front_kernel<<<148 * 4, 256, 0, s>>>(cams, *fp, *gp, cells, cell_count, slot);
+        else
+            count_cells_kernel<<<148 * 8, 256, 0, s>>>(cells, P, cell_count, slot);
+        pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
+        device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
+        make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
+                                                 icells, cell_first, counts);
+        if (cams)
+            count_scatter_kernel<<<148 * 4, 256, 0, s>>>(cells, slot, *fp, packed, ranks, iop);
+        else
+            count_scatter_flat_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, P, packed, ranks, iop);
+        seg_sort_warp_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, counts, long_list, n_long);
+        seg_sort_long_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, long_list, n_long);
+        return check_launch("sort_intervals");
+    }
     const unsigned tiles = static_cast<unsigned>(L.n_tiles);
     if (cams)
         pass0_front_kernel<true><<<tiles, kSortThreads, 0, s>>>(
@@ -316,7 +670,6 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
             nullptr, FrustumParams{}, GridParams{}, P, cells, cell_count, L.digit_bits, hist,
             L.n_tiles);
     // interval tables from the per-cell counts (independent of the sort)
-    const unsigned cb = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_cells, 256), 4096));
     pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
     device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
     make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,

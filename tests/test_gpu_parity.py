@@ -486,3 +486,36 @@ def test_fast_mode_batched_and_deterministic():
         assert torch.equal(out[b], one)
     again = bp.pool_interval(F, Dd, cache, grid, exact=False).values
     assert torch.equal(out, again)
+
+
+# ---- the GPU sort against a stable numpy argsort (bevgrid.py:142-158) -------
+@pytest.mark.parametrize("sizes", [
+    (0, 5, 31, 32, 33, 64, 65, 100, 128, 200, 256, 300, 512, 700, 1024),  # warp registers
+    (1025, 3000, 8192),                 # CTA: warp-sorted slices merged by rank
+    (9000, 20000),                      # in-place global fallback
+])
+def test_sort_intervals_every_run_length(sizes):
+    """Counting-sort path (P <= 64 cells): runs of every size class, points
+    shuffled and mixed with out-of-range ids, must come back in stable order."""
+    rng = np.random.default_rng(len(sizes))
+    n_cells = max(64, (sum(sizes) + 63) // 64 + len(sizes))
+    cell_ids = rng.choice(n_cells, size=len(sizes), replace=False)
+    cells = np.concatenate([np.full(n, c, dtype=np.uint32) for n, c in zip(sizes, cell_ids)]
+                           + [np.full(sum(sizes) // 7 + 1, bp.OUT_OF_RANGE, dtype=np.uint32)])
+    cells = cells[rng.permutation(cells.size)]
+    ranks, starts, icells = bp.ranks_and_intervals(cells, n_cells)
+    want = o.ranks_and_intervals(cells, n_cells)
+    np.testing.assert_array_equal(ranks, want[0])
+    np.testing.assert_array_equal(starts, want[1])
+    np.testing.assert_array_equal(icells, want[2])
+
+
+def test_sort_intervals_radix_path():
+    """Few keys, long runs (P > 64 cells): the LSD radix path."""
+    rng = np.random.default_rng(7)
+    cells = rng.integers(0, 50, size=200_000).astype(np.uint32)
+    cells[rng.random(cells.size) < 0.1] = bp.OUT_OF_RANGE
+    ranks, starts, icells = bp.ranks_and_intervals(cells, 50)
+    want = o.ranks_and_intervals(cells, 50)
+    for got, ref in zip((ranks, starts, icells), want):
+        np.testing.assert_array_equal(got, ref)
