@@ -196,6 +196,12 @@ int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cell
 
 /* ---- cached forward ---------------------------------------------------- */
 
+/* 1 when pooling C channels (bf16: the fused path) in this mode launches the
+ * unit / task kernels, i.e. needs the schedule's units, long_units, tasks and
+ * counts; 0 when the chunk schedule (work) alone suffices, so a schedule
+ * built without units (all four NULL) may be passed. */
+int bvp_pool_needs_units(int C, int bf16, int exact);
+
 /* Scratch of the fast kernels (the split intervals' partials) for B samples
  * of C channels in `mode`; 0 when the schedule has no chunk schedule. */
 size_t bvp_pool_scratch_bytes(const bvp_schedule *schedule, int B, int C, int mode);

@@ -58,6 +58,7 @@ SIGNATURES = {
     "bvp_work_workspace_bytes": (_S, [_L, _L, _I, _I, _I, _I]),
     "bvp_make_work": (_I, [_P, _P, _P, _L, _L, _I, _I, _I, _I, _P, _P, _P, _P, _S, _P]),
     "bvp_pool_scratch_bytes": (_S, [_SP, _I, _I, _I]),
+    "bvp_pool_needs_units": (_I, [_I, _I, _I]),
     "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
                                   _L, _I, _I, _P, _P, _P, _P, _S, _P]),
     "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I,

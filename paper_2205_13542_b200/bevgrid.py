@@ -179,6 +179,7 @@ class AssociationCache:
     chunk: int = 0
     _host_counts: tuple | None = field(default=None, repr=False)
     _host: dict = field(default_factory=dict, repr=False)
+    _units_pending: object = field(default=None, repr=False)  # deferred units build
 
     # ---- sizes ----------------------------------------------------------
     @property
@@ -214,47 +215,72 @@ class AssociationCache:
 
     @property
     def n_units(self) -> int:
+        self.ensure_units()
         return int(self.d_sched_counts[0].item())
 
     @property
     def n_long(self) -> int:
+        self.ensure_units()
         return int(self.d_sched_counts[1].item())
 
     def fit_launch(self) -> None:
         """Shrink the launch bounds to the exact unit / chunk counts (one host
         sync)."""
+        self.ensure_units()
         c = self.d_sched_counts.cpu().tolist()
         self.max_units, self.max_long, self.max_tasks = max(1, int(c[0])), int(c[1]), max(1, int(c[2]))
         if self.d_work_counts is not None:
             w = self.d_work_counts.cpu().tolist()
             self.max_work, self.max_splits, self.max_partials = int(w[0]), int(w[1]), int(w[2])
-        self._host.pop("schedules", None)
+        for k in [k for k in self._host if isinstance(k, tuple) and k[0] == "schedules"]:
+            self._host.pop(k)
         self._host.pop("scratch", None)
 
-    def schedule(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1):
+    def schedule(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1, *,
+                 units: bool = True):
         """The bvp_schedule the C ABI takes; the point gather table is
         (re)derived for an (N, H, W, D) frustum (N=None: the caller does not
-        read it, e.g. the materialised path)."""
+        read it, e.g. the materialised path).  units=False: the caller's
+        launch needs only the chunk schedule (bvp_pool_needs_units), so units
+        deferred by a per-frame build are not built for it."""
         if N is not None and self.meta_dims != (N, H, W, D):
             _lib.call("bvp_point_meta", ptr(self.d_ranks), ptr(self.d_counts), N, H, W, D,
                       ptr(self.d_meta), stream_ptr(self.device))
             self.meta_dims = (N, H, W, D)
-        s = self._host.get("schedules")
+        with_units = units or self.d_work is None
+        if with_units:
+            self.ensure_units()
+        key = ("schedules", self._units_pending is None)
+        s = self._host.get(key)
         if s is None:
             work = (None, None, None, 0, 0, 0, 0)
             if self.d_work is not None:
                 work = (ptr(self.d_work), ptr(self.d_splits), ptr(self.d_work_counts),
                         self.max_work, self.max_splits, self.max_partials, self.chunk)
-            s = _lib.Schedule(ptr(self.d_units), ptr(self.d_meta), ptr(self.d_long_units),
-                              ptr(self.d_tasks), ptr(self.d_sched_counts), self.max_units,
-                              self.max_long, self.max_tasks, None, 1, *work)
-            self._host["schedules"] = s
+            if self._units_pending is None:
+                s = _lib.Schedule(ptr(self.d_units), ptr(self.d_meta), ptr(self.d_long_units),
+                                  ptr(self.d_tasks), ptr(self.d_sched_counts), self.max_units,
+                                  self.max_long, self.max_tasks, None, 1, *work)
+            else:  # units not built: the kernels see NULL and refuse to use them
+                s = _lib.Schedule(None, ptr(self.d_meta), None, None, None, 0, 0, 0, None, 1,
+                                  *work)
+            self._host[key] = s
         return s
+
+    def ensure_units(self) -> None:
+        """Build the work units / tasks a per-frame build deferred (stream
+        ordered, no host sync)."""
+        if self._units_pending is not None:
+            build, self._units_pending = self._units_pending, None
+            build()
+
+    def needs_units(self, C: int, bf16: bool = False, exact: bool = False) -> bool:
+        return bool(_lib.load().bvp_pool_needs_units(C, int(bf16), int(exact)))
 
     def scratch(self, B: int, C: int, mode: int) -> torch.Tensor | None:
         """Scratch of the fast kernels (split-interval partials), kept per
         (B, C, mode) shape."""
-        n = int(_lib.load().bvp_pool_scratch_bytes(self.schedule(), B, C, mode))
+        n = int(_lib.load().bvp_pool_scratch_bytes(self.schedule(units=False), B, C, mode))
         if n == 0:
             return None
         key = (B, C, mode == 2)
@@ -337,20 +363,33 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
 
 
 def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
-                   task_budget: int = TASK_BUDGET, work_tile: int = WORK_TILE) -> None:
-    """Work units and tasks, plus the point gather table when the frustum
-    dims are known."""
+                   task_budget: int = TASK_BUDGET, work_tile: int = WORK_TILE,
+                   defer_units: bool = False):
+    """Chunk schedule (work) and point gather table, plus the work units and
+    tasks -- or, defer_units, a closure that builds the units later (only the
+    exact mode and very wide channel counts read them).  Returns the closure
+    or None."""
     N, H, W, D = dims if dims is not None else (1, 1, 1, 1)
-    _lib.call("bvp_make_schedule", ptr(b["ranks"]), ptr(b["starts"]), ptr(b["cell_first"]),
-              ptr(b["counts"]), N, H, W, D, nx, ny, budget, task_budget, ptr(b["units"]),
-              ptr(b["long_units"]), ptr(b["tasks"]), ptr(b["sched_counts"]),
-              ptr(b["meta"]) if dims is not None else None, ptr(b["ws"]), b["ws"].numel(),
-              stream_ptr(dev))
+
+    def units(meta=dims is not None and not defer_units):
+        _lib.call("bvp_make_schedule", ptr(b["ranks"]), ptr(b["starts"]), ptr(b["cell_first"]),
+                  ptr(b["counts"]), N, H, W, D, nx, ny, budget, task_budget, ptr(b["units"]),
+                  ptr(b["long_units"]), ptr(b["tasks"]), ptr(b["sched_counts"]),
+                  ptr(b["meta"]) if meta else None, ptr(b["ws"]), b["ws"].numel(),
+                  stream_ptr(dev))
+
     if "work" in b:
         _lib.call("bvp_make_work", ptr(b["starts"]), ptr(b["icells"]), ptr(b["counts"]),
                   b["n_int_max"], b["ranks"].numel(), CHUNK, nx, ny, work_tile, ptr(b["work"]),
                   ptr(b["splits"]),
                   ptr(b["work_counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
+    if defer_units and "work" in b:
+        if dims is not None:
+            _lib.call("bvp_point_meta", ptr(b["ranks"]), ptr(b["counts"]), N, H, W, D,
+                      ptr(b["meta"]), stream_ptr(dev))
+        return lambda: units(False)
+    units()
+    return None
 
 
 def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, dims=None):
@@ -384,6 +423,8 @@ class CacheBuilder:
         # per-frame rebuilds keep the chunk list in cell order (the length
         # sort costs more than it saves once per frame); cached builds sort
         self.work_tile = WORK_TILE if sort_work else -1
+        # per-frame rebuilds also defer the work units (built on first use)
+        self.defer_units = not sort_work
         self._grid_arr = grid.as_array()
 
     def build(self, cams: torch.Tensor, fingerprint: int = 0) -> AssociationCache:
@@ -398,8 +439,11 @@ class CacheBuilder:
                   ptr(b["cell_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
                   b["ws"].numel(), stream_ptr(self.dev))
         dims = (self.n_cameras, f.height, f.width, f.depth_bins)
-        _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims, work_tile=self.work_tile)
-        return _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
+        pending = _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims,
+                                 work_tile=self.work_tile, defer_units=self.defer_units)
+        cache = _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
+        cache._units_pending = pending
+        return cache
 
 
 def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,

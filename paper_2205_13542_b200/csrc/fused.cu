@@ -172,7 +172,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
                 "fused workspace too small: need %zu bytes", L.bytes);
     BVP_REQUIRE(logits && (C == 0 || (out && context && ranks && interval_starts &&
                                       interval_cells && cell_first && schedule &&
-                                      schedule->units && schedule->counts)),
+                                      ((schedule->units && schedule->counts) || schedule->work))),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     cudaStream_t s = as_stream(stream);

@@ -231,8 +231,8 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
                 H, W, D, nx, ny);
     BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
     BVP_REQUIRE(C == 0 || (out && feats_nhwc && dist && ranks && interval_starts &&
-                           interval_cells && cell_first && schedule && schedule->units &&
-                           schedule->counts),
+                           interval_cells && cell_first && schedule &&
+                           ((schedule->units && schedule->counts) || schedule->work)),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
@@ -335,7 +335,8 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *i
     BVP_REQUIRE(C >= 0 && nx >= 1 && ny >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
                 "bad arguments");
     BVP_REQUIRE(C == 0 || (out && x && ranks && interval_starts && interval_cells && cell_first &&
-                           schedule && schedule->units && schedule->counts),
+                           schedule &&
+                           ((schedule->units && schedule->counts) || schedule->work)),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,

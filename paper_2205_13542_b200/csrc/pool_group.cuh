@@ -471,7 +471,8 @@ int run_pool_group(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
                 "channel count %d too large for the group kernel", p.C);
     BVP_REQUIRE(SRC == kSrcX || p.meta, BVP_ERR_INVALID,
                 "the cache's point gather table (point_meta) is required");
-    BVP_REQUIRE(p.tasks, BVP_ERR_INVALID, "the cache's task table is required");
+    BVP_REQUIRE(p.units && p.tasks && p.sched_counts, BVP_ERR_INVALID,
+                "the schedule's units / tasks are required (built without units?)");
     const size_t smem = std::max(size_t(kPoolWarps) * p.C * kUnitPitch * sizeof(float),
                                  size_t(kPoolWarps) * p.C * 2 * sizeof(float));
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);

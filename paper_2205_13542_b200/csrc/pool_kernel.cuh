@@ -590,7 +590,8 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     BVP_REQUIRE(smem <= 227 * 1024, BVP_ERR_UNSUPPORTED, "channel count %d too large", p.C);
     BVP_REQUIRE(SRC == kSrcX || p.meta, BVP_ERR_INVALID,
                 "the cache's point gather table (point_meta) is required");
-    BVP_REQUIRE(p.tasks, BVP_ERR_INVALID, "the cache's task table is required");
+    BVP_REQUIRE(p.units && p.tasks && p.sched_counts, BVP_ERR_INVALID,
+                "the schedule's units / tasks are required (built without units?)");
     // fast mode: heavy cells are split over a CTA by pool_long_kernel; the
     // exact mode must walk every interval in order and does not split
     constexpr bool kSplit = sizeof(Acc) == sizeof(float);

@@ -519,3 +519,25 @@ def test_sort_intervals_radix_path():
     want = o.ranks_and_intervals(cells, 50)
     for got, ref in zip((ranks, starts, icells), want):
         np.testing.assert_array_equal(got, ref)
+
+
+def test_per_frame_build_defers_units():
+    """A per-frame CacheBuilder build skips the work units; fast pooling runs
+    on the chunk schedule alone, the exact mode builds the units on first use,
+    and both match a cache built eagerly."""
+    spec = bp.CONFIGS["T"]
+    f = spec.frustum
+    rig, feats, logits, grid = bp.gen_workload(spec)
+    dist = bp.normalize_depth(logits)
+    eager = bp.build_cache(rig, f, grid)
+    builder = bp.CacheBuilder(spec.n_cameras, f, grid)
+    lazy = builder.build(torch.from_numpy(bp.rig_rows(rig)).cuda())
+    assert lazy._units_pending is not None
+    fast = bp.pool_interval(feats, dist, lazy, grid, exact=False).values
+    assert lazy._units_pending is not None  # fast path did not need them
+    np.testing.assert_array_equal(fast, bp.pool_interval(feats, dist, eager, grid,
+                                                         exact=False).values)
+    ex = bp.pool_interval(feats, dist, lazy, grid, exact=True).values
+    assert lazy._units_pending is None
+    np.testing.assert_array_equal(ex, bp.pool_interval(feats, dist, eager, grid,
+                                                       exact=True).values)
