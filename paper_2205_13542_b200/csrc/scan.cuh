@@ -1,64 +1,102 @@
 // scan.cuh -- device-wide exclusive scan (reduce / scan partials / downsweep).
+//
+// A block owns a chunk of kScanChunk elements; each of its 8 warps owns a
+// contiguous 512-element slice and walks it 32 elements at a time with warp
+// shuffles only, so a chunk costs one block barrier instead of one per round.
+// T: an integer or floating type, or uint4 (four independent counters scanned
+// together).
 #pragma once
 
 #include "common.cuh"
 
 namespace bvp {
 
-// ---- device-wide exclusive scan (3 phases) ---------------------------------
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanChunk = kScanThreads * kScanItems;
+constexpr int kScanWarps = kScanThreads / 32;
+constexpr int kScanSlice = kScanChunk / kScanWarps;  // elements per warp
+
+__device__ __forceinline__ uint4 operator+(uint4 a, uint4 b) {
+    return make_uint4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ uint4 &operator+=(uint4 &a, uint4 b) { return a = a + b; }
 
 template <typename T>
-__device__ __forceinline__ T block_excl_scan(T v, T *warp_sums, T &total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    T x = v;
+__device__ __forceinline__ T shfl_up_t(T v, int o) { return __shfl_up_sync(0xFFFFFFFFu, v, o); }
+template <>
+__device__ __forceinline__ uint4 shfl_up_t<uint4>(uint4 v, int o) {
+    return make_uint4(__shfl_up_sync(0xFFFFFFFFu, v.x, o), __shfl_up_sync(0xFFFFFFFFu, v.y, o),
+                      __shfl_up_sync(0xFFFFFFFFu, v.z, o), __shfl_up_sync(0xFFFFFFFFu, v.w, o));
+}
+template <typename T>
+__device__ __forceinline__ T shfl_t(T v, int src) { return __shfl_sync(0xFFFFFFFFu, v, src); }
+template <>
+__device__ __forceinline__ uint4 shfl_t<uint4>(uint4 v, int src) {
+    return make_uint4(__shfl_sync(0xFFFFFFFFu, v.x, src), __shfl_sync(0xFFFFFFFFu, v.y, src),
+                      __shfl_sync(0xFFFFFFFFu, v.z, src), __shfl_sync(0xFFFFFFFFu, v.w, src));
+}
+
+// Inclusive warp scan.
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T x, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        T y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        const T y = shfl_up_t(x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) warp_sums[warp] = x;
-    __syncthreads();
-    T wpre = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < kScanThreads / 32; ++w) {
-        const T s = warp_sums[w];
-        if (w < warp) wpre += s;
-        tot += s;
-    }
-    __syncthreads();
-    total = tot;
-    return wpre + x - v;
+    return x;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kScanThreads)
 scan_reduce_kernel(const T *__restrict__ in, int64_t n, T *__restrict__ partials) {
-    __shared__ T ws[kScanThreads / 32];
-    const int64_t base = blockIdx.x * (int64_t)kScanChunk;
-    T s = 0;
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t e = base + k * kScanThreads + threadIdx.x;
+    __shared__ T ws[kScanWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = blockIdx.x * (int64_t)kScanChunk + warp * kScanSlice;
+    T s{};
+#pragma unroll 4
+    for (int k = 0; k < kScanSlice / 32; ++k) {
+        const int64_t e = base + k * 32 + lane;
         if (e < n) s += in[e];
     }
-    T tot;
-    block_excl_scan<T>(s, ws, tot);
-    if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+    s = warp_incl_scan(s, lane);
+    if (lane == 31) ws[warp] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        T t{};
+#pragma unroll
+        for (int w = 0; w < kScanWarps; ++w) t += ws[w];
+        partials[blockIdx.x] = t;
+    }
 }
 
+// Exclusive scan of the block partials (one block; nb is small).
 template <typename T>
 __global__ void __launch_bounds__(kScanThreads)
 scan_partials_kernel(T *__restrict__ partials, int64_t nb, T *__restrict__ total_out) {
-    __shared__ T ws[kScanThreads / 32];
-    T carry = 0;
+    __shared__ T ws[kScanWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T carry{};
     for (int64_t b = 0; b < nb; b += kScanThreads) {
         const int64_t e = b + threadIdx.x;
-        const T v = e < nb ? partials[e] : T(0);
-        T tot;
-        const T ex = block_excl_scan<T>(v, ws, tot);
-        if (e < nb) partials[e] = carry + ex;
+        const T v = e < nb ? partials[e] : T{};
+        const T x = warp_incl_scan(v, lane);
+        if (lane == 31) ws[warp] = x;
+        __syncthreads();
+        T wpre{}, tot{};
+#pragma unroll
+        for (int w = 0; w < kScanWarps; ++w) {
+            const T s = ws[w];
+            if (w < warp) wpre += s;
+            tot += s;
+        }
+        __syncthreads();
+        // exclusive prefix of this thread: carry + wpre + (x - v), with the
+        // warp-exclusive part taken from the neighbouring lane
+        T wex = shfl_up_t(x, 1);
+        if (lane == 0) wex = T{};
+        if (e < nb) partials[e] = carry + wpre + wex;
         carry += tot;
     }
     if (threadIdx.x == 0 && total_out) *total_out = carry;
@@ -68,16 +106,32 @@ template <typename T>
 __global__ void __launch_bounds__(kScanThreads)
 scan_down_kernel(const T *__restrict__ in, int64_t n, const T *__restrict__ partials,
                  T *__restrict__ out) {
-    __shared__ T ws[kScanThreads / 32];
-    const int64_t base = blockIdx.x * (int64_t)kScanChunk;
-    T carry = partials[blockIdx.x];
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t e = base + k * kScanThreads + threadIdx.x;
-        const T v = e < n ? in[e] : T(0);
-        T tot;
-        const T ex = block_excl_scan<T>(v, ws, tot);
-        if (e < n) out[e] = carry + ex;
-        carry += tot;
+    __shared__ T ws[kScanWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = blockIdx.x * (int64_t)kScanChunk + warp * kScanSlice;
+    constexpr int R = kScanSlice / 32;
+    T ex[R];
+    T run{};
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int64_t e = base + k * 32 + lane;
+        const T v = e < n ? in[e] : T{};
+        const T x = warp_incl_scan(v, lane);
+        T wex = shfl_up_t(x, 1);
+        if (lane == 0) wex = T{};
+        ex[k] = run + wex;
+        run += shfl_t(x, 31);
+    }
+    if (lane == 0) ws[warp] = run;
+    __syncthreads();
+    T pre = partials[blockIdx.x];
+#pragma unroll
+    for (int w = 0; w < kScanWarps; ++w)
+        if (w < warp) pre += ws[w];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int64_t e = base + k * 32 + lane;
+        if (e < n) out[e] = pre + ex[k];
     }
 }
 

@@ -27,19 +27,17 @@ namespace bvp {
 
 constexpr uint32_t kSplitDest = 0x80000000u;
 
-// per interval: chunk count, partial count (chunks if split), split flag
+// per interval: (chunk count, partial count (chunks if split), split flag, 0)
+// -- one uint4 so a single scan yields all three bases
 __global__ void work_count_kernel(const uint32_t *__restrict__ starts,
                                   const int64_t *__restrict__ counts, int64_t n_int_max,
-                                  uint32_t chunk, uint32_t *__restrict__ nch,
-                                  uint32_t *__restrict__ npart, uint32_t *__restrict__ nsplit) {
+                                  uint32_t chunk, uint4 *__restrict__ cnt) {
     const int64_t n_int = counts[1];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_int_max;
          i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t c = 0;
         if (i < n_int) c = (starts[i + 1] - starts[i] + chunk - 1) / chunk;
-        nch[i] = c;
-        npart[i] = c > 1 ? c : 0u;
-        nsplit[i] = c > 1 ? 1u : 0u;
+        cnt[i] = make_uint4(c, c > 1 ? c : 0u, c > 1 ? 1u : 0u, 0u);
     }
 }
 
@@ -48,9 +46,7 @@ __global__ void work_count_kernel(const uint32_t *__restrict__ starts,
 __global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
                                  const uint32_t *__restrict__ icells,
                                  const int64_t *__restrict__ counts, uint32_t chunk,
-                                 const uint32_t *__restrict__ cbase,
-                                 const uint32_t *__restrict__ pbase,
-                                 const uint32_t *__restrict__ sbase, uint4 *__restrict__ tmp,
+                                 const uint4 *__restrict__ base, uint4 *__restrict__ tmp,
                                  uint32_t *__restrict__ keys, uint4 *__restrict__ splits,
                                  int ny, int tile) {
     const int tiles_y = tile > 0 ? (ny + tile - 1) / tile : 1;
@@ -59,12 +55,13 @@ __global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t lo = starts[i], hi = starts[i + 1], cell = icells[i];
         const uint32_t nch = (hi - lo + chunk - 1) / chunk;
+        const uint4 b = base[i];  // exclusive: chunk, partial, split bases
         const bool split = nch > 1;
         for (uint32_t k = 0; k < nch; ++k) {
             const uint32_t a = lo + k * chunk, e = min(hi, a + chunk);
-            const uint32_t dest = split ? (kSplitDest | (pbase[i] + k)) : cell;
+            const uint32_t dest = split ? (kSplitDest | (b.y + k)) : cell;
             // .w: the interval, or for a chunk of a split interval its split index
-            tmp[cbase[i] + k] = make_uint4(a, e, dest, split ? sbase[i] : static_cast<uint32_t>(i));
+            tmp[b.x + k] = make_uint4(a, e, dest, split ? b.z : static_cast<uint32_t>(i));
             // bucket 0 = longest; tile > 0: 2D cell tiles first (L1 reuse of
             // the feature rows shared by neighbouring cells), length within
             uint32_t key = chunk - (e - a);
@@ -72,9 +69,9 @@ __global__ void work_emit_kernel(const uint32_t *__restrict__ starts,
                 const uint32_t ix = cell / uint32_t(ny), iy = cell - ix * uint32_t(ny);
                 key += (chunk + 1) * ((ix / tile) * tiles_y + iy / tile);
             }
-            keys[cbase[i] + k] = key;
+            if (keys) keys[b.x + k] = key;
         }
-        if (split) splits[sbase[i]] = make_uint4(static_cast<uint32_t>(i), cell, pbase[i], nch);
+        if (split) splits[b.z] = make_uint4(static_cast<uint32_t>(i), cell, b.y, nch);
     }
 }
 
@@ -95,16 +92,15 @@ __global__ void work_gather_kernel(const uint4 *__restrict__ tmp, const uint32_t
         work[w] = tmp[order[w]];
 }
 
-__global__ void work_counts_kernel(const uint32_t *__restrict__ n_work,
-                                   const uint32_t *__restrict__ n_split,
-                                   const uint32_t *__restrict__ n_part, int64_t *__restrict__ out) {
-    out[0] = *n_work;
-    out[1] = *n_split;
-    out[2] = *n_part;
+__global__ void work_counts_kernel(const uint4 *__restrict__ tot, int64_t *__restrict__ out) {
+    const uint4 t = *tot;
+    out[0] = t.x;  // chunks
+    out[1] = t.z;  // split intervals
+    out[2] = t.y;  // partials
 }
 
 struct WorkLayout {
-    size_t off_nch, off_npart, off_nsplit, off_part, off_tot, off_tmp, off_keys, off_order,
+    size_t off_cnt, off_part, off_tot, off_tmp, off_keys, off_order,
         off_sstarts, off_scells, off_sfirst, off_scounts, off_sws, sort_ws, bytes;
 };
 static int64_t work_cap(int64_t n_int_max, int64_t n_points, int chunk) {
@@ -121,10 +117,8 @@ static WorkLayout work_layout(int64_t n_int_max, int64_t n_points, int chunk, in
     const size_t n = size_t(n_int_max);
     const int64_t cap = work_cap(n_int_max, n_points, chunk);
     size_t o = 0;
-    L.off_nch = o; o = al(o + n * 4);
-    L.off_npart = o; o = al(o + n * 4);
-    L.off_nsplit = o; o = al(o + n * 4);
-    L.off_part = o; o = al(o + size_t(scan_partials_len<uint32_t>(n_int_max)) * 4);
+    L.off_cnt = o; o = al(o + n * 16);
+    L.off_part = o; o = al(o + size_t(scan_partials_len<uint4>(n_int_max)) * 16);
     L.off_tot = o; o = al(o + 16);
     L.off_tmp = o; o = al(o + size_t(cap) * 16);
     L.off_keys = o; o = al(o + size_t(cap) * 4);
@@ -169,31 +163,32 @@ int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cell
                 "work workspace too small: need %zu bytes", L.bytes);
     cudaStream_t s = as_stream(stream);
     char *ws = static_cast<char *>(workspace);
-    auto *nch = reinterpret_cast<uint32_t *>(ws + L.off_nch);
-    auto *npart = reinterpret_cast<uint32_t *>(ws + L.off_npart);
-    auto *nsplit = reinterpret_cast<uint32_t *>(ws + L.off_nsplit);
-    auto *part = reinterpret_cast<uint32_t *>(ws + L.off_part);
-    auto *tot = reinterpret_cast<uint32_t *>(ws + L.off_tot);  // n_work, n_partials, n_splits
+    auto *cnt = reinterpret_cast<uint4 *>(ws + L.off_cnt);
+    auto *part = reinterpret_cast<uint4 *>(ws + L.off_part);
+    auto *tot = reinterpret_cast<uint4 *>(ws + L.off_tot);  // n_work, n_partials, n_splits
     auto *tmp = reinterpret_cast<uint4 *>(ws + L.off_tmp);
     auto *keys = reinterpret_cast<uint32_t *>(ws + L.off_keys);
     auto *order = reinterpret_cast<uint32_t *>(ws + L.off_order);
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_int_max, 256), 4096));
     work_count_kernel<<<blocks, 256, 0, s>>>(interval_starts, counts, n_int_max, uint32_t(chunk),
-                                             nch, npart, nsplit);
-    device_excl_scan<uint32_t>(nch, nch, n_int_max, part, tot + 0, s);
-    device_excl_scan<uint32_t>(npart, npart, n_int_max, part, tot + 1, s);
-    device_excl_scan<uint32_t>(nsplit, nsplit, n_int_max, part, tot + 2, s);
+                                             cnt);
+    device_excl_scan<uint4>(cnt, cnt, n_int_max, part, tot, s);
+    // tile < 0: cell order as emitted (per-frame builds: no sort), straight
+    // into the work list
+    const bool sorted = tile >= 0;
     work_emit_kernel<<<blocks, 256, 0, s>>>(interval_starts, interval_cells, counts,
-                                            uint32_t(chunk), nch, npart, nsplit, tmp, keys,
+                                            uint32_t(chunk), cnt,
+                                            sorted ? tmp : reinterpret_cast<uint4 *>(work),
+                                            sorted ? keys : nullptr,
                                             reinterpret_cast<uint4 *>(splits), ny, tile);
     const int64_t cap = work_cap(n_int_max, n_points, chunk);
     const unsigned cb = static_cast<unsigned>(std::min<int64_t>(ceil_div(cap, 256), 4096));
-    if (tile < 0) {  // cell order as emitted (per-frame builds: no sort)
-        cudaMemcpyAsync(work, tmp, size_t(cap) * 16, cudaMemcpyDeviceToDevice, s);
-        work_counts_kernel<<<1, 1, 0, s>>>(tot + 0, tot + 2, tot + 1, work_counts);
+    const uint32_t *n_work = reinterpret_cast<const uint32_t *>(tot);
+    if (!sorted) {
+        work_counts_kernel<<<1, 1, 0, s>>>(tot, work_counts);
         return check_launch("make_work");
     }
-    work_keys_tail_kernel<<<cb, 256, 0, s>>>(tot + 0, cap, keys);
+    work_keys_tail_kernel<<<cb, 256, 0, s>>>(n_work, cap, keys);
     // stable counting sort by length bucket (the association's own sort):
     // longest chunks first, cell order within a bucket, so a warp's groups
     // store to neighbouring cells
@@ -204,8 +199,8 @@ int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cell
                                       reinterpret_cast<int64_t *>(ws + L.off_scounts),
                                       ws + L.off_sws, L.sort_ws, stream);
     if (rc != BVP_OK) return rc;
-    work_gather_kernel<<<cb, 256, 0, s>>>(tmp, order, tot + 0, reinterpret_cast<uint4 *>(work));
-    work_counts_kernel<<<1, 1, 0, s>>>(tot + 0, tot + 2, tot + 1, work_counts);
+    work_gather_kernel<<<cb, 256, 0, s>>>(tmp, order, n_work, reinterpret_cast<uint4 *>(work));
+    work_counts_kernel<<<1, 1, 0, s>>>(tot, work_counts);
     return check_launch("make_work");
 }
 
