@@ -24,7 +24,12 @@ constexpr int64_t kCountSortMaxRun = 64;  // counting sort while P <= 64 * n_cel
 struct GridParams {
     double x_min, y_min, z_min, z_max, r;
     int nx, ny;
+    double rinv;  // RN(1/r): the quantiser's fast path (exact fallback below)
 };
+
+inline GridParams grid_params(const double *grid, int nx, int ny) {
+    return GridParams{grid[0], grid[2], grid[4], grid[5], grid[6], nx, ny, 1.0 / grid[6]};
+}
 
 struct FrustumParams {
     int N, H, W, D;
@@ -39,6 +44,18 @@ struct FrustumParams {
 //   e_j = fma(R[j][2],pz, fma(R[j][1],py, R[j][0]*px)) + t_j
 //        (the OpenBLAS dgemm rounding of geometry.py:185-186)
 //   ix = floor((x - x_min)/r) ...                  bevgrid.py:88-96
+// floor(RN(a / r)) -- numpy's floor((x - x_min) / r) -- without a division
+// when possible: t = RN(a * RN(1/r)) lies within 2^-51 |t| of RN(a/r), so
+// unless t is that close to an integer both floors agree; otherwise (e.g.
+// quotients that are exactly integral) the IEEE division decides.
+__device__ __forceinline__ double floor_div(double a, const GridParams &g) {
+    const double t = __dmul_rn(a, g.rinv);
+    const double k = floor(t);
+    const double margin = fabs(t) * 0x1p-50 + 0x1p-1000;
+    if (t - k > margin && (k + 1.0) - t > margin) return k;
+    return floor(__ddiv_rn(a, g.r));
+}
+
 __device__ __forceinline__ uint32_t cell_at(const double *__restrict__ c, const FrustumParams &f,
                                             const GridParams &g, double dx, double dy, int d) {
     const double depth = __dadd_rn(f.d_min, __dmul_rn(f.d_step, static_cast<double>(d)));
@@ -51,10 +68,11 @@ __device__ __forceinline__ uint32_t cell_at(const double *__restrict__ c, const 
         acc = __fma_rn(__ldg(c + 6 + 3 * j), pz, acc);
         e[j] = __dadd_rn(acc, __ldg(c + 13 + j));
     }
-    const double qx = floor(__ddiv_rn(__dsub_rn(e[0], g.x_min), g.r));
-    const double qy = floor(__ddiv_rn(__dsub_rn(e[1], g.y_min), g.r));
+    if (!(e[2] >= g.z_min && e[2] < g.z_max)) return kOOR;
+    const double qx = floor_div(__dsub_rn(e[0], g.x_min), g);
+    const double qy = floor_div(__dsub_rn(e[1], g.y_min), g);
     if (qx >= 0.0 && qx < static_cast<double>(g.nx) && qy >= 0.0 &&
-        qy < static_cast<double>(g.ny) && e[2] >= g.z_min && e[2] < g.z_max)
+        qy < static_cast<double>(g.ny))
         return static_cast<uint32_t>(static_cast<int64_t>(qx) * g.ny + static_cast<int64_t>(qy));
     return kOOR;
 }
@@ -646,7 +664,7 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         auto *n_long = reinterpret_cast<uint32_t *>(w + L.off_nlong);
         cudaMemsetAsync(n_long, 0, 8, s);
         if (cams)
-            count_front_kernel<<<148 * 4, 256, 0, s>>>(cams, *fp, *gp, cells, cell_count, slot);
+            count_front_kernel<<<148 * 8, 256, 0, s>>>(cams, *fp, *gp, cells, cell_count, slot);
         else
             count_cells_kernel<<<148 * 8, 256, 0, s>>>(cells, P, cell_count, slot);
         pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
@@ -654,7 +672,7 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
                                                  icells, cell_first, counts);
         if (cams)
-            count_scatter_kernel<<<148 * 4, 256, 0, s>>>(cells, slot, *fp, packed, ranks, iop);
+            count_scatter_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, *fp, packed, ranks, iop);
         else
             count_scatter_flat_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, P, packed, ranks, iop);
         seg_sort_warp_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, counts, long_list, n_long);
@@ -716,7 +734,7 @@ int bvp_frustum_cells(const double *cams, int N, int H, int W, int D, double dep
     BVP_REQUIRE(N > 0 && H > 0 && W > 0 && D > 0 && nx > 0 && ny > 0, BVP_ERR_INVALID,
                 "frustum/grid dims must be positive");
     const FrustumParams f{N, H, W, D, depth_min, depth_step};
-    const GridParams g{grid[0], grid[2], grid[4], grid[5], grid[6], nx, ny};
+    const GridParams g = grid_params(grid, nx, ny);
     const int64_t P = int64_t(N) * H * W * D;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), 148 * 64));
     frustum_cells_kernel<<<blocks, 256, 0, as_stream(stream)>>>(cams, f, g, P, cell_of_point);
@@ -750,7 +768,7 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D, double depth
     BVP_REQUIRE(N > 0 && H > 0 && W > 0 && D > 0 && nx > 0 && ny > 0, BVP_ERR_INVALID,
                 "frustum/grid dims must be positive");
     const FrustumParams f{N, H, W, D, depth_min, depth_step};
-    const GridParams g{grid[0], grid[2], grid[4], grid[5], grid[6], nx, ny};
+    const GridParams g = grid_params(grid, nx, ny);
     return sort_impl(cams, &f, &g, cell_of_point, int64_t(N) * H * W * D, int64_t(nx) * ny,
                      ranks, interval_starts, interval_cells, cell_first, interval_of_point,
                      counts, workspace, workspace_bytes, as_stream(stream));
