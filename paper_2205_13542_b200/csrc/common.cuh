@@ -31,6 +31,36 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Fork / join with this thread's side stream of the current device: work
+// launched on `side` is ordered after what was queued on `main` before the
+// fork, and `main` waits for it at join() -- by events, so a captured CUDA
+// graph gets two parallel branches.
+struct SideFork {
+    cudaStream_t main, side = nullptr;
+    cudaEvent_t fork = nullptr, joined = nullptr;
+    explicit SideFork(cudaStream_t s) : main(s), side(s) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        static thread_local cudaStream_t streams[64] = {};
+        if (dev < 0 || dev >= 64) return;  // run inline
+        if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+        side = streams[dev];
+        cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&joined, cudaEventDisableTiming);
+        cudaEventRecord(fork, main);
+        cudaStreamWaitEvent(side, fork, 0);
+    }
+    void join() {
+        if (side == main) return;
+        cudaEventRecord(joined, side);
+        cudaStreamWaitEvent(main, joined, 0);
+        cudaEventDestroy(fork);
+        cudaEventDestroy(joined);
+        side = main;
+    }
+    ~SideFork() { join(); }
+};
+
 // ---- device helpers --------------------------------------------------------
 __host__ __device__ inline int64_t ceil_div_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

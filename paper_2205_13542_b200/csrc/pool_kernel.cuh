@@ -35,6 +35,8 @@
 //   kSrcFused : rows = NHWC context (bf16), weight = exp(logit - lse[pixel])
 #pragma once
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bvp {
@@ -548,6 +550,114 @@ pool_long_kernel(const PoolParams P) {
     }
 }
 
+// Exact mode: one CTA per heavy cell (a long unit), summed in rank order
+// like every other cell -- but with the gathers batched.  The cell's points
+// are walked in tiles of T = kExactTile / C rows: all 256 threads load the
+// next tile's rows (and weights) into registers while the channel threads
+// run the current tile's sequential fp64 FMAs out of shared memory, so the
+// cell costs ~L / T gather latencies instead of ~L / 4.
+constexpr int kExactTile = 8192;                  // floats per staged tile
+constexpr int kExactRegs = kExactTile / kPoolThreads;  // per thread (32)
+
+template <int VEC, bool IS_MAX>
+__global__ void __launch_bounds__(kPoolThreads)
+pool_exact_long_kernel(const PoolParams P) {
+    extern __shared__ float s_ex[];  // [T][C] rows, [T] weights
+    const int C = P.C, tid = threadIdx.x;
+    const int b = blockIdx.y;
+    if (int64_t(blockIdx.x) >= P.sched_counts[1]) return;
+    const int T = min(128, kExactTile / C);
+    float *s_rows = s_ex, *s_w = s_ex + T * C;
+    const uint32_t k = __ldg(P.long_units + blockIdx.x);
+    const int64_t cell = __ldg(P.units + 4 * size_t(k));
+    const uint32_t iv = __ldg(P.cell_first + cell);
+    const uint32_t lo = __ldg(P.starts + iv), hi = __ldg(P.starts + iv + 1);
+    const float *rows = static_cast<const float *>(P.rows) + b * P.rows_bstride;
+    const float *wd = static_cast<const float *>(P.wsrc) + b * P.w_bstride;
+    const int cv = C / VEC;          // vectors per row
+    constexpr int R = kExactRegs / VEC;  // vectors per thread per tile
+
+    float buf[R][VEC];
+    float wbuf = 0.f;
+    auto load = [&](uint32_t j0) {  // tile starting at sorted point j0 -> registers
+        const int n = static_cast<int>(min(uint32_t(T), hi - j0));
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int e = tid + q * kPoolThreads;
+            const int t = e / cv;
+            if (t < n) {
+                const uint2 m = __ldg(P.meta + j0 + t);
+                const float *src = rows + size_t(m.x) * C + (e - t * cv) * VEC;
+                if (VEC == 4) {
+                    const float4 v = ldg_f4(src);
+                    buf[q][0] = v.x; buf[q][VEC > 1 ? 1 : 0] = v.y;
+                    buf[q][VEC > 2 ? 2 : 0] = v.z; buf[q][VEC > 3 ? 3 : 0] = v.w;
+                } else {
+                    buf[q][0] = __ldg(src);
+                }
+            }
+        }
+        if (tid < n) wbuf = __ldg(wd + __ldg(P.meta + j0 + tid).y);
+    };
+    auto stash = [&](uint32_t j0) {
+        const int n = static_cast<int>(min(uint32_t(T), hi - j0));
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int e = tid + q * kPoolThreads;
+            if (e / cv < n)
+#pragma unroll
+                for (int x = 0; x < VEC; ++x) s_rows[e * VEC + x] = buf[q][x];
+        }
+        if (tid < n) s_w[tid] = wbuf;
+    };
+
+    constexpr int A = 1024 / kPoolThreads;  // channels per thread (C <= 1024)
+    double acc[A];
+    uint32_t arg[A];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        acc[a] = IS_MAX ? -INFINITY : 0.0;
+        arg[a] = lo;
+    }
+    load(lo);
+    for (uint32_t j0 = lo; j0 < hi; j0 += T) {
+        __syncthreads();  // the previous tile is consumed
+        stash(j0);
+        __syncthreads();
+        if (j0 + T < hi) load(j0 + T);  // in flight during the sums below
+        const int n = static_cast<int>(min(uint32_t(T), hi - j0));
+#pragma unroll
+        for (int a = 0; a < A; ++a) {
+            const int c = tid + a * kPoolThreads;
+            if (c >= C) break;
+            double r = acc[a];
+            uint32_t ra = arg[a];
+            for (int t = 0; t < n; ++t) {
+                const double pv = double(s_w[t]) * double(s_rows[t * C + c]);
+                if (IS_MAX) {
+                    if (pv > r) {
+                        r = pv;
+                        ra = j0 + t;
+                    }
+                } else {
+                    r += pv;
+                }
+            }
+            acc[a] = r;
+            arg[a] = ra;
+        }
+    }
+    float *out = P.out + int64_t(b) * C * P.n_cells + cell;
+    const double inv = P.mean ? 1.0 / double(hi - lo) : 1.0;
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+        const int c = tid + a * kPoolThreads;
+        if (c >= C) break;
+        out[int64_t(c) * P.n_cells] = static_cast<float>(acc[a] * inv);
+        if (IS_MAX && P.argmax) P.argmax[(b * P.n_int_max + iv) * C + c] = __ldg(P.ranks + arg[a]);
+    }
+}
+
 // Channel chunks per lane for a row of `nchunks` VEC-element chunks.
 inline int choose_ch(int nchunks) {
     for (int ch : {1, 2, 4, 8})
@@ -592,9 +702,11 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
                 "the cache's point gather table (point_meta) is required");
     BVP_REQUIRE(p.units && p.tasks && p.sched_counts, BVP_ERR_INVALID,
                 "the schedule's units / tasks are required (built without units?)");
-    // fast mode: heavy cells are split over a CTA by pool_long_kernel; the
-    // exact mode must walk every interval in order and does not split
-    constexpr bool kSplit = sizeof(Acc) == sizeof(float);
+    // heavy cells go to a CTA each: split over its warps in the fast mode
+    // (pool_long_kernel), walked in order with batched gathers in the exact
+    // mode (pool_exact_long_kernel)
+    constexpr bool kSplit = true;
+    constexpr bool kExact = sizeof(Acc) == sizeof(double);
     const dim3 grid(static_cast<unsigned>(ceil_div(p.max_units, kPoolWarps * p.order_rep)),
                     static_cast<unsigned>(B));
     const size_t lsmem = size_t(kPoolWarps) * p.C * 2 * sizeof(float);
@@ -604,8 +716,25 @@ int run_pool_impl(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
                         : pool_unit_kernel<Acc, Elem, VEC, CHV, false, SRC, kSplit>;         \
         if (smem > 48 * 1024)                                                                \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)); \
+        if (kExact && p.max_long > 0) {                                                      \
+            /* heavy cells on a side stream, overlapping the unit kernel */                  \
+            auto ke = is_max ? pool_exact_long_kernel<VEC, true>                             \
+                             : pool_exact_long_kernel<VEC, false>;                           \
+            const int T = std::min(128, kExactTile / p.C);                                   \
+            const size_t esmem = size_t(T) * (p.C + 1) * sizeof(float);                      \
+            if (esmem > 48 * 1024)                                                           \
+                cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                     int(esmem));                                            \
+            SideFork fork(s);                                                                \
+            ke<<<dim3(static_cast<unsigned>(p.max_long), static_cast<unsigned>(B)),          \
+                 kPoolThreads, esmem, fork.side>>>(p);                                       \
+            k<<<grid, kPoolThreads, smem, s>>>(p);                                           \
+            fork.join();                                                                     \
+            return BVP_OK;                                                                   \
+        }                                                                                    \
         k<<<grid, kPoolThreads, smem, s>>>(p);                                               \
-        if (kSplit && p.max_long > 0) {                                                      \
+        if (kExact) {                                                                        \
+        } else if (kSplit && p.max_long > 0) {                                               \
             auto kl = is_max ? pool_long_kernel<Elem, VEC, CHV, true, SRC>                   \
                              : pool_long_kernel<Elem, VEC, CHV, false, SRC>;                 \
             if (lsmem > 48 * 1024)                                                           \
