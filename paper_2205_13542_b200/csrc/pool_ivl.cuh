@@ -30,6 +30,7 @@
 #pragma once
 
 #include <algorithm>
+#include <type_traits>
 
 #include "pool_group.cuh"
 
@@ -89,10 +90,41 @@ struct RawChunk<__nv_bfloat16, 1> {
 #define BVP_IVL_MIN_BLOCKS 3
 #endif
 
-template <typename Elem, int VEC, int CPL, bool IS_MAX, int SRC, bool ARG = IS_MAX>
-__global__ void __launch_bounds__(kPoolThreads, sizeof(Elem) == 2 ? BVP_IVL_MIN_BLOCKS + 1
-                                                                  : BVP_IVL_MIN_BLOCKS)
+// Accumulation of one point into a lane's channel slices.  EXACT: fp64, the
+// fp32 x fp32 product exact, one rounding per add -- the reference's
+// arithmetic, so a chunk that is a whole interval reproduces its sum bit for
+// bit.
+template <bool EXACT, int CPL, int VEC, bool IS_MAX, bool ARG>
+__device__ __forceinline__ void ivl_acc(std::conditional_t<EXACT, double, float> (&acc)[CPL][VEC],
+                                        uint32_t (&arg)[ARG ? CPL : 1][ARG ? VEC : 1],
+                                        uint32_t j, float w, const float (&v)[CPL][VEC]) {
+    if constexpr (!EXACT) {
+        gacc<CPL, VEC, IS_MAX, ARG>(acc, arg, j, true, w, v);
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+#pragma unroll
+        for (int x = 0; x < VEC; ++x) {
+            const double pv = double(w) * double(v[k][x]);
+            if (IS_MAX) {
+                if (pv > acc[k][x]) {
+                    acc[k][x] = pv;
+                    if (ARG) arg[ARG ? k : 0][ARG ? x : 0] = j;
+                }
+            } else {
+                acc[k][x] += pv;
+            }
+        }
+}
+
+template <typename Elem, int VEC, int CPL, bool IS_MAX, int SRC, bool ARG = IS_MAX,
+          bool EXACT = false>
+__global__ void __launch_bounds__(kPoolThreads, EXACT ? 2
+                                                : sizeof(Elem) == 2 ? BVP_IVL_MIN_BLOCKS + 1
+                                                                    : BVP_IVL_MIN_BLOCKS)
 pool_ivl_kernel(const PoolParams P, int L, int lg) {
+    using Acc = std::conditional_t<EXACT, double, float>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int b = blockIdx.y;
     const int C = P.C;
@@ -124,14 +156,22 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
         const int64_t item = batch * G + g;
         uint4 r = make_uint4(0u, 0u, 0u, 0u);
         if (item < n_work) r = __ldg(P.work + item);
-        const uint32_t j0 = r.x, len = r.y - r.x;
+        const uint32_t j0 = r.x;
+        // EXACT: chunks of split intervals belong to pool_exact_long_kernel
+        const uint32_t len = (EXACT && (r.z & kIvlSplit)) ? 0u : r.y - r.x;
         uint32_t steps = len;
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) steps = max(steps, __shfl_xor_sync(0xFFFFFFFFu, steps, o));
 
-        float acc[CPL][VEC];
+        Acc acc[CPL][VEC];
         uint32_t arg[ARG ? CPL : 1][ARG ? VEC : 1];
-        greset<CPL, VEC, IS_MAX, ARG>(acc, arg);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+#pragma unroll
+            for (int x = 0; x < VEC; ++x) {
+                acc[k][x] = IS_MAX ? Acc(-INFINITY) : Acc(0);
+                if (ARG) arg[ARG ? k : 0][ARG ? x : 0] = 0xFFFFFFFFu;
+            }
         // rows of two steps in flight: fetch(s + 1) is issued before the
         // FMAs of step s; each fetch also loads the next step's record
         uint2 m = len > 0 ? rec_of(j0) : make_uint2(0u, 0u);
@@ -155,7 +195,7 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
             float v[CPL][VEC];
 #pragma unroll
             for (int k = 0; k < CPL; ++k) RawChunk<Elem, VEC>::unpack(raw[k], v[k]);
-            gacc<CPL, VEC, IS_MAX, ARG>(acc, arg, j, true, w, v);
+            ivl_acc<EXACT, CPL, VEC, IS_MAX, ARG>(acc, arg, j, w, v);
         };
         float wa, wb;
         Raw va[CPL], vb[CPL];
@@ -168,9 +208,9 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
             if (s + 2 < steps) fetch(s + 2, wa, va);
             if (s + 1 < len) consume(j0 + s + 1, wb, vb);
         }
-        if (item >= n_work) continue;
+        if (item >= n_work || (EXACT && (r.z & kIvlSplit))) continue;
         if (!(r.z & kIvlSplit)) {  // the chunk is the whole interval: store its cell
-            const float inv = P.mean ? 1.f / float(len) : 1.f;
+            const Acc inv = P.mean ? Acc(1) / Acc(len) : Acc(1);
             float *out = P.out + int64_t(b) * C * P.n_cells + r.z;
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
@@ -179,7 +219,7 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) {
                         const int c = ch * VEC + x;
-                        out[int64_t(c) * P.n_cells] = acc[k][x] * inv;
+                        out[int64_t(c) * P.n_cells] = static_cast<float>(acc[k][x] * inv);
                         if (ARG && P.argmax)
                             P.argmax[(b * P.n_int_max + r.w) * C + c] =
                                 __ldg(P.ranks + arg[ARG ? k : 0][ARG ? x : 0]);
@@ -195,7 +235,7 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
                 if (ch < nch)
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) {
-                        pp[ch * VEC + x] = acc[k][x];
+                        pp[ch * VEC + x] = static_cast<float>(acc[k][x]);
                         if (ARG) pa[ch * VEC + x] = arg[ARG ? k : 0][ARG ? x : 0];
                     }
             }
@@ -256,7 +296,10 @@ inline size_t ivl_scratch_bytes(int64_t n_partials, int B, int C, bool is_max) {
 
 // Zero-fill + chunk kernel + combine.  BVP_ERR_UNSUPPORTED: shape not covered
 // (the caller falls back).
-template <typename Elem, int VEC, int SRC>
+// EXACT: fp64 accumulation; chunks that are whole intervals here, the split
+// intervals (longer than a chunk) walked in order by pool_exact_long_kernel
+// on a forked stream -- every cell bit-identical to the reference.
+template <typename Elem, int VEC, int SRC, bool EXACT = false>
 int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
     void *scratch = p0.scratch;
     const size_t scratch_bytes = p0.scratch_bytes;
@@ -264,15 +307,16 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
     if (!p0.work || !choose_group(p0.C / VEC, VEC, L, lg, cpl)) return BVP_ERR_UNSUPPORTED;
     BVP_REQUIRE(SRC == kSrcX || p0.meta, BVP_ERR_INVALID,
                 "the cache's point gather table (point_meta) is required");
-    const size_t need = ivl_scratch_bytes(p0.max_splits > 0 ? p0.chunk_partials : 0, B, p0.C, is_max);
+    const size_t need =
+        EXACT ? 0 : ivl_scratch_bytes(p0.max_splits > 0 ? p0.chunk_partials : 0, B, p0.C, is_max);
     BVP_REQUIRE(scratch_bytes >= need, BVP_ERR_INVALID,
                 "pool scratch too small: need %zu bytes (bvp_pool_scratch_bytes)", need);
     PoolParams p = p0;
     p.partials = static_cast<float *>(scratch);
     const bool arg = is_max && p0.argmax;  // MAX winners only for autograd
-    p.partial_arg = arg ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
-                                                       size_t(B) * p0.chunk_partials * p0.C)
-                        : nullptr;
+    p.partial_arg = arg && !EXACT ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
+                                                                 size_t(B) * p0.chunk_partials * p0.C)
+                                  : nullptr;
     cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
     const int G = 32 >> lg;
     const int64_t batches = ceil_div(p.max_work, G);
@@ -280,17 +324,29 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
                         1, std::min<int64_t>(ceil_div(batches, kPoolWarps),
                                              int64_t(kNumSms) * BVP_IVL_MIN_BLOCKS * 4))),
                     static_cast<unsigned>(B));
+    SideFork fork(s);
+    if (EXACT && p.max_splits > 0) {  // the split intervals, in order, meanwhile
+        auto ke = is_max ? pool_exact_long_kernel<VEC, true, true>
+                         : pool_exact_long_kernel<VEC, false, true>;
+        const int T = std::min(128, kExactTile / p.C);
+        const size_t esmem = size_t(T) * (p.C + 1) * sizeof(float);
+        if (esmem > 48 * 1024)
+            cudaFuncSetAttribute(ke, cudaFuncAttributeMaxDynamicSharedMemorySize, int(esmem));
+        ke<<<dim3(static_cast<unsigned>(p.max_splits), static_cast<unsigned>(B)), kPoolThreads,
+             esmem, fork.side>>>(p);
+    }
 #define BVP_IVL_LAUNCH(CPLV)                                                          \
     if (cpl == CPLV) {                                                                \
-        auto k = !is_max ? pool_ivl_kernel<Elem, VEC, CPLV, false, SRC>               \
-                 : arg   ? pool_ivl_kernel<Elem, VEC, CPLV, true, SRC, true>          \
-                         : pool_ivl_kernel<Elem, VEC, CPLV, true, SRC, false>;        \
+        auto k = !is_max ? pool_ivl_kernel<Elem, VEC, CPLV, false, SRC, false, EXACT> \
+                 : arg   ? pool_ivl_kernel<Elem, VEC, CPLV, true, SRC, true, EXACT>   \
+                         : pool_ivl_kernel<Elem, VEC, CPLV, true, SRC, false, EXACT>; \
         k<<<grid, kPoolThreads, 0, s>>>(p, L, lg);                                    \
     }
     BVP_IVL_LAUNCH(1) BVP_IVL_LAUNCH(2) BVP_IVL_LAUNCH(3)
     BVP_IVL_LAUNCH(4) BVP_IVL_LAUNCH(5) BVP_IVL_LAUNCH(6)
 #undef BVP_IVL_LAUNCH
-    if (p.max_splits > 0) {
+    fork.join();
+    if (!EXACT && p.max_splits > 0) {
         const dim3 cg(static_cast<unsigned>(std::max<int64_t>(
                           1, std::min<int64_t>(ceil_div(p.max_splits * p.C, kPoolThreads),
                                                kNumSms * 16))),

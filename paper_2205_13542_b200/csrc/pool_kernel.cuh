@@ -559,18 +559,28 @@ pool_long_kernel(const PoolParams P) {
 constexpr int kExactTile = 8192;                  // floats per staged tile
 constexpr int kExactRegs = kExactTile / kPoolThreads;  // per thread (32)
 
-template <int VEC, bool IS_MAX>
+// SPLITS: the cells are the chunk schedule's split intervals (work.cu),
+// else the long units (units.cu).
+template <int VEC, bool IS_MAX, bool SPLITS = false>
 __global__ void __launch_bounds__(kPoolThreads)
 pool_exact_long_kernel(const PoolParams P) {
     extern __shared__ float s_ex[];  // [T][C] rows, [T] weights
     const int C = P.C, tid = threadIdx.x;
     const int b = blockIdx.y;
-    if (int64_t(blockIdx.x) >= P.sched_counts[1]) return;
+    if (int64_t(blockIdx.x) >= (SPLITS ? P.work_counts[1] : P.sched_counts[1])) return;
     const int T = min(128, kExactTile / C);
     float *s_rows = s_ex, *s_w = s_ex + T * C;
-    const uint32_t k = __ldg(P.long_units + blockIdx.x);
-    const int64_t cell = __ldg(P.units + 4 * size_t(k));
-    const uint32_t iv = __ldg(P.cell_first + cell);
+    int64_t cell;
+    uint32_t iv;
+    if (SPLITS) {
+        const uint4 sp = __ldg(P.splits + blockIdx.x);  // interval, cell, slot, chunks
+        iv = sp.x;
+        cell = sp.y;
+    } else {
+        const uint32_t k = __ldg(P.long_units + blockIdx.x);
+        cell = __ldg(P.units + 4 * size_t(k));
+        iv = __ldg(P.cell_first + cell);
+    }
     const uint32_t lo = __ldg(P.starts + iv), hi = __ldg(P.starts + iv + 1);
     const float *rows = static_cast<const float *>(P.rows) + b * P.rows_bstride;
     const float *wd = static_cast<const float *>(P.wsrc) + b * P.w_bstride;

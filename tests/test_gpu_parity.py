@@ -522,9 +522,10 @@ def test_sort_intervals_radix_path():
 
 
 def test_per_frame_build_defers_units():
-    """A per-frame CacheBuilder build skips the work units; fast pooling runs
-    on the chunk schedule alone, the exact mode builds the units on first use,
-    and both match a cache built eagerly."""
+    """A per-frame CacheBuilder build skips the work units; fast and exact
+    pooling both run on the chunk schedule alone, a launch that needs the
+    units (here: reading the unit count) builds them on first use, and every
+    result matches a cache built eagerly."""
     spec = bp.CONFIGS["T"]
     f = spec.frustum
     rig, feats, logits, grid = bp.gen_workload(spec)
@@ -538,6 +539,7 @@ def test_per_frame_build_defers_units():
     np.testing.assert_array_equal(fast, bp.pool_interval(feats, dist, eager, grid,
                                                          exact=False).values)
     ex = bp.pool_interval(feats, dist, lazy, grid, exact=True).values
-    assert lazy._units_pending is None
+    assert lazy._units_pending is not None
     np.testing.assert_array_equal(ex, bp.pool_interval(feats, dist, eager, grid,
                                                        exact=True).values)
+    assert lazy.n_units == eager.n_units and lazy._units_pending is None
