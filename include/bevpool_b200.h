@@ -70,6 +70,9 @@ extern "C" {
 #define BVP_SUM 0
 #define BVP_MEAN 1
 #define BVP_MAX 2
+/* or-ed into mode of bvp_pool_forward_nhwc_f32: `out` was zero-filled by
+ * bvp_pool_prepare_f32 since it was last written, so the zero fill is skipped */
+#define BVP_OUT_ZEROED 0x100
 
 /* Work schedule of the interval kernels (device pointers; built once per
  * cache by bvp_make_schedule).
@@ -230,6 +233,12 @@ int bvp_pool_forward_f32(const float *features, const float *dist,
  * bvp_pool_forward_f32 performs first; pooling.py:215). */
 int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst,
                     void *stream);
+
+/* The first half of bvp_pool_forward_f32: the features' NHWC staging and the
+ * zero fill of out (B, C, n_cells), side by side on a forked stream.  Follow
+ * with bvp_pool_forward_nhwc_f32(..., mode | BVP_OUT_ZEROED, ...). */
+int bvp_pool_prepare_f32(const float *features, int B, int N, int C, int H, int W,
+                         float *feats_nhwc, float *out, int64_t n_cells, void *stream);
 
 /* Same as bvp_pool_forward_f32 with the features already NHWC (B,N,H,W,C). */
 int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,

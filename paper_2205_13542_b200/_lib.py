@@ -18,6 +18,7 @@ BVP_OK, BVP_ERR_INVALID, BVP_ERR_UNSUPPORTED, BVP_ERR_CUDA = 0, 1, 2, 3
 BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
 TILE_CELLS = 32
 OUT_OF_RANGE = 0xFFFFFFFF
+BVP_OUT_ZEROED = 0x100  # include/bevpool_b200.h
 ABI_VERSION = 5
 
 
@@ -64,6 +65,7 @@ SIGNATURES = {
     "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I,
                                        _I, _L, _I, _I, _P, _P, _P, _S, _P]),
     "bvp_to_nhwc_f32": (_I, [_P, _I, _I, _I, _P, _P]),
+    "bvp_pool_prepare_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _L, _P]),
     "bvp_reorder_weights": (_I, [_P, _P, _L, _I, _I, _I, _I, _P, _P]),
     "bvp_normalize_depth": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "bvp_any_nonfinite": (_I, [_P, _L, _P, _P]),

@@ -46,8 +46,20 @@ to_nhwc_rows_kernel(const T *__restrict__ src, int A, int HW, T *__restrict__ ds
     const int hw0 = blockIdx.x * 32;
     const int np = min(32, HW - hw0);
     const T *sb = src + n * int64_t(A) * HW + hw0;
-    for (int a = threadIdx.x >> 5; a < A; a += 8)
-        if ((threadIdx.x & 31) < np) t[(threadIdx.x & 31) * pitch + a] = sb[int64_t(a) * HW + (threadIdx.x & 31)];
+    // every load of the tile issued before the first shared store (A <= 128:
+    // <= 16 per thread), so a block waits one memory latency, not A / 8
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    T v[kRowsA / 8];
+#pragma unroll
+    for (int i = 0; i < kRowsA / 8; ++i) {
+        const int a = w + 8 * i;
+        if (a < A && lane < np) v[i] = sb[int64_t(a) * HW + lane];
+    }
+#pragma unroll
+    for (int i = 0; i < kRowsA / 8; ++i) {
+        const int a = w + 8 * i;
+        if (a < A && lane < np) t[lane * pitch + a] = v[i];
+    }
     __syncthreads();
     T *db = dst + (n * HW + hw0) * int64_t(A);
     constexpr int V = 16 / sizeof(T);
@@ -219,13 +231,16 @@ int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst, void *s
     return check_launch("to_nhwc");
 }
 
-int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const uint32_t *ranks,
+}  // extern "C"
+
+namespace bvp {
+static int pool_forward_nhwc(const float *feats_nhwc, const float *dist, const uint32_t *ranks,
                               const uint32_t *interval_starts, const uint32_t *interval_cells,
                               const uint32_t *cell_first, const bvp_schedule *schedule, int B,
                               int N, int C, int H, int W, int D, int nx, int ny,
                               int64_t n_int_max, int mode, int exact, float *out,
                               uint32_t *argmax, void *scratch, size_t scratch_bytes,
-                              void *stream) {
+                              void *stream, bool zeroed) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims B=%d N=%d C=%d H=%d W=%d D=%d nx=%d ny=%d", B, N, C,
                 H, W, D, nx, ny);
@@ -248,6 +263,7 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
     p.w_bstride = int64_t(N) * D * H * W;
     p.scratch = scratch;
     p.scratch_bytes = scratch_bytes;
+    p.out_zeroed = zeroed ? 1 : 0;
     const bool is_max = mode == BVP_MAX, v4 = (C % 4) == 0;
     cudaStream_t s = as_stream(stream);
     int rc;
@@ -260,6 +276,39 @@ int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const 
     if (rc != BVP_OK) return rc;
     return check_launch("pool_forward");
 }
+}  // namespace bvp
+
+extern "C" {
+
+int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist, const uint32_t *ranks,
+                              const uint32_t *interval_starts, const uint32_t *interval_cells,
+                              const uint32_t *cell_first, const bvp_schedule *schedule, int B,
+                              int N, int C, int H, int W, int D, int nx, int ny,
+                              int64_t n_int_max, int mode, int exact, float *out,
+                              uint32_t *argmax, void *scratch, size_t scratch_bytes,
+                              void *stream) {
+    return pool_forward_nhwc(feats_nhwc, dist, ranks, interval_starts, interval_cells,
+                             cell_first, schedule, B, N, C, H, W, D, nx, ny, n_int_max,
+                             mode & ~BVP_OUT_ZEROED, exact, out, argmax, scratch, scratch_bytes,
+                             stream, (mode & BVP_OUT_ZEROED) != 0);
+}
+
+int bvp_pool_prepare_f32(const float *features, int B, int N, int C, int H, int W,
+                         float *feats_nhwc, float *out, int64_t n_cells, void *stream) {
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && n_cells >= 1,
+                BVP_ERR_INVALID, "bad dims");
+    BVP_REQUIRE(C == 0 || (features && feats_nhwc && out), BVP_ERR_INVALID,
+                "null pointer argument");
+    if (C == 0) return BVP_OK;
+    // the map's zero fill (for the chunk kernel's scattered column stores)
+    // runs beside the features' NHWC transpose: two graph branches
+    cudaStream_t s = as_stream(stream);
+    SideFork fork(s);
+    cudaMemsetAsync(out, 0, size_t(B) * C * n_cells * sizeof(float), fork.side);
+    launch_to_nhwc<float>(features, int64_t(B) * N, C, H * W, feats_nhwc, s);
+    fork.join();
+    return check_launch("pool_prepare");
+}
 
 int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_t *ranks,
                          const uint32_t *interval_starts, const uint32_t *interval_cells,
@@ -268,11 +317,15 @@ int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_
                          int exact, float *out, float *feats_nhwc, uint32_t *argmax,
                          void *scratch, size_t scratch_bytes, void *stream) {
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1, BVP_ERR_INVALID, "bad dims");
-    BVP_REQUIRE(C == 0 || (features && feats_nhwc), BVP_ERR_INVALID, "null pointer argument");
-    launch_to_nhwc<float>(features, int64_t(B) * N, C, H * W, feats_nhwc, as_stream(stream));
-    return bvp_pool_forward_nhwc_f32(feats_nhwc, dist, ranks, interval_starts, interval_cells,
-                                     cell_first, schedule, B, N, C, H, W, D, nx, ny, n_int_max,
-                                     mode, exact, out, argmax, scratch, scratch_bytes, stream);
+    BVP_REQUIRE(C == 0 || (features && feats_nhwc && out), BVP_ERR_INVALID,
+                "null pointer argument");
+    if (C == 0) return BVP_OK;
+    const int rc = bvp_pool_prepare_f32(features, B, N, C, H, W, feats_nhwc, out,
+                                        int64_t(nx) * ny, stream);
+    if (rc != BVP_OK) return rc;
+    return pool_forward_nhwc(feats_nhwc, dist, ranks, interval_starts, interval_cells, cell_first,
+                             schedule, B, N, C, H, W, D, nx, ny, n_int_max, mode, exact, out,
+                             argmax, scratch, scratch_bytes, stream, true);
 }
 
 int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in, int N, int D,

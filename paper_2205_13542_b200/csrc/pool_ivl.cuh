@@ -317,7 +317,7 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
     p.partial_arg = arg && !EXACT ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
                                                                  size_t(B) * p0.chunk_partials * p0.C)
                                   : nullptr;
-    cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
+    if (!p.out_zeroed) cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
     const int G = 32 >> lg;
     const int64_t batches = ceil_div(p.max_work, G);
     const dim3 grid(static_cast<unsigned>(std::max<int64_t>(

@@ -80,6 +80,7 @@ struct PoolParams {
     size_t scratch_bytes;
     int long_only;           // group kernel: long cells only
     int debug;               // experiment switches (BVP_IVL_DEBUG), 0 in production
+    int out_zeroed;          // the caller already zero-filled out (chunk kernel skips it)
     float *partials;         // split intervals: [B][n_chunks of splits][C] (workspace)
     uint32_t *partial_arg;   // MAX: sorted position of each partial's max
     int64_t rows_bstride;    // elements of rows per batch sample

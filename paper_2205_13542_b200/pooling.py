@@ -229,9 +229,9 @@ class PoolPlan:
     """Pre-planned cached forward for fixed shapes (the serving loop).
 
     Output, NHWC staging and pinned host buffers are allocated once; ``run``
-    is exactly two kernel launches on the current stream (features -> NHWC
-    transpose, interval reduction) with no validation and no host sync, so
-    it can be captured in a CUDA graph.  ``run_host`` is the end-to-end
+    is one C call on the current stream (features -> NHWC transpose beside the
+    map's zero fill, then the interval reduction) with no validation and no
+    host sync, so it can be captured in a CUDA graph.  ``run_host`` is the end-to-end
     drop-in for host (numpy) buffers: pinned H2D of features + dist, run,
     D2H of the (C, nx, ny) map.
     """
@@ -267,21 +267,41 @@ class PoolPlan:
         _lib.call("bvp_to_nhwc_f32", ptr(features), self.B * self.N, self.C, self.H * self.W,
                   ptr(self.nhwc), stream_ptr(self.dev))
 
-    def reduce(self, dist: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def prepare(self, features: torch.Tensor) -> None:
+        """NHWC staging of the features beside the zero fill of the plan's
+        output map (forked stream); follow with reduce(dist, zeroed=True)."""
+        _lib.call("bvp_pool_prepare_f32", ptr(features), self.B, self.N, self.C, self.H, self.W,
+                  ptr(self.nhwc), ptr(self.out), self.grid.n_cells, stream_ptr(self.dev))
+
+    def reduce(self, dist: torch.Tensor, out: torch.Tensor | None = None,
+               zeroed: bool = False) -> torch.Tensor:
+        """The interval reduction on the staged features.  zeroed=True: the
+        plan's output was zero-filled by prepare() since it was last written
+        (the reduction then skips its own zero fill)."""
+        mode = self.mode | (_lib.BVP_OUT_ZEROED if zeroed and out is None else 0)
         out = self.out if out is None else out
         c = self.cache
         _lib.call("bvp_pool_forward_nhwc_f32", ptr(self.nhwc), ptr(dist), ptr(c.d_ranks),
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
                   c.schedule(self.N, self.H, self.W, self.D, units=self._units), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
-                  self.mode, self.exact, ptr(out), None, *self._scratch, stream_ptr(self.dev))
+                  mode, self.exact, ptr(out), None, *self._scratch, stream_ptr(self.dev))
         return out
 
     def run(self, features: torch.Tensor, dist: torch.Tensor,
             out: torch.Tensor | None = None) -> torch.Tensor:
-        """features (B,N,C,H,W) / dist (B,N,D,H,W) contiguous float32 CUDA."""
-        self.transpose(features)
-        return self.reduce(dist, out)
+        """features (B,N,C,H,W) / dist (B,N,D,H,W) contiguous float32 CUDA.
+        One C call: the NHWC transpose and the map's zero fill run side by
+        side (forked stream), then the interval reduction."""
+        out = self.out if out is None else out
+        c = self.cache
+        _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(c.d_ranks),
+                  ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
+                  c.schedule(self.N, self.H, self.W, self.D, units=self._units), self.B,
+                  self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
+                  self.mode, self.exact, ptr(out), ptr(self.nhwc), None, *self._scratch,
+                  stream_ptr(self.dev))
+        return out
 
     def graphed(self, fn, *tensors):
         """A CUDA graph of ``fn(*tensors)`` (the plan's launches on these

@@ -52,3 +52,12 @@ g.replay()
 torch.cuda.synchronize()
 print(f"eager {eager:.1f} us  graph {graph:.1f} us  (warm L2: eager {warm_e:.1f} graph {warm_g:.1f})"
       f"  same={bool(torch.equal(ref, plan.out))}")
+
+# the bench's split: staging graph | reduction graph
+gt = plan.graphed(plan.prepare, feats)
+import functools  # noqa: E402
+gr = plan.graphed(functools.partial(plan.reduce, zeroed=True), dist)
+gtr = lambda: (gt.replay(), gr.replay())  # noqa: E731
+print(f"staging graph {t(lambda: gt.replay()):.1f} us  reduction graph "
+      f"{t(lambda: gr.replay()):.1f} us  both {t(gtr):.1f} us  "
+      f"transpose only {t(lambda: plan.transpose(feats)):.1f} us")
