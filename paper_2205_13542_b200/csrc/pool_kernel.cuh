@@ -371,116 +371,6 @@ pool_unit_kernel(const PoolParams P) {
     }
 }
 
-// One warp per task.  SPLIT: long tasks are left to pool_long_kernel (fast
-// mode); the exact mode walks them here, in order.
-template <typename Acc, typename Elem, int VEC, int CH, bool IS_MAX, int SRC, bool SPLIT>
-__global__ void __launch_bounds__(kPoolThreads)
-pool_stream_kernel(const PoolParams P) {
-    using G = Gather<Elem, VEC, CH, SRC>;
-    constexpr int U = G::U;
-    extern __shared__ float s_all[];  // per warp: [C][kUnitPitch]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int b = blockIdx.y;
-
-    const int64_t t = int64_t(blockIdx.x) * kPoolWarps + warp;
-    if (t >= P.sched_counts[2]) return;
-    const uint4 ta = __ldg(P.tasks + 2 * t), tb = __ldg(P.tasks + 2 * t + 1);
-    if (SPLIT && (ta.y & kLongUnit)) return;
-    const uint32_t u_end = ta.x + (ta.y & 0xFFFFu);
-    const uint32_t J0 = ta.z, J1 = ta.w;
-    const int C = P.C;
-    const int64_t n_cells = P.n_cells;
-    const uint32_t *starts = P.starts;
-    const uint32_t *icells = P.icells;
-    float *s_tile = s_all + warp * C * kUnitPitch;
-    float *out_b = P.out + int64_t(b) * C * n_cells;
-
-    // current unit
-    uint32_t u = ta.x;
-    uint2 ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + 2 * size_t(u));
-    int64_t cell0 = ur.x;
-    auto flush_unit = [&]() {  // write the current unit's columns, advance
-        const int ncell = static_cast<int>(ur.y & 0xFFu);
-        const uint32_t has = (ur.y >> 8) & 0xFFu;
-        __syncwarp();
-        float *o = out_b + cell0;
-        for (int idx = lane; idx < C * ncell; idx += 32) {
-            const int c = idx / ncell, x = idx - c * ncell;
-            o[int64_t(c) * n_cells + x] = ((has >> x) & 1u) ? s_tile[c * kUnitPitch + x] : 0.f;
-        }
-        __syncwarp();
-        ++u;
-        if (u < u_end) {
-            ur = __ldg(reinterpret_cast<const uint2 *>(P.units) + 2 * size_t(u));
-            cell0 = ur.x;
-        }
-    };
-
-    const G g(P, b);
-    Acc acc[CH][VEC];
-    uint32_t arg[IS_MAX ? CH : 1][IS_MAX ? VEC : 1];
-    acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
-    // current interval [lo, hi) with its cell; the next one prefetched
-    uint32_t iv = tb.x;
-    uint32_t lo = J0, hi = __ldg(starts + iv + 1);
-    uint32_t cell = __ldg(icells + iv);
-    uint32_t nhi = __ldg(starts + iv + 2), ncell_id = __ldg(icells + iv + 1);
-    auto enter_interval = [&]() {  // make the unit containing `cell` current
-        while (int64_t(cell) >= cell0 + int64_t(ur.y & 0xFFu)) flush_unit();
-    };
-    auto park = [&]() {  // interval iv = [lo, hi) complete
-        const int lc = static_cast<int>(int64_t(cell) - cell0);
-        const Acc inv = P.mean ? Acc(1) / Acc(hi - lo) : Acc(1);
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-            const int ch = lane + 32 * q;
-            if (ch < g.nchunks)
-#pragma unroll
-                for (int x = 0; x < VEC; ++x) {
-                    const int c = ch * VEC + x;
-                    s_tile[c * kUnitPitch + lc] = static_cast<float>(acc[q][x] * inv);
-                    if (IS_MAX && P.argmax)
-                        P.argmax[(b * P.n_int_max + iv) * C + c] =
-                            __ldg(P.ranks + arg[IS_MAX ? q : 0][IS_MAX ? x : 0]);
-                }
-        }
-    };
-
-    if (J1 > J0) {
-        enter_interval();
-        float v[2][U][CH][VEC];
-        gather_stream(g, J0, J1, v, [&](uint32_t js, const float (&ws)[U],
-                                        const float (&vb)[U][CH][VEC]) {
-            if (js + U <= hi) {  // whole step inside the current interval
-#pragma unroll
-                for (int k = 0; k < U; ++k)
-                    acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, js + k, ws[k], vb[k]);
-            } else {
-#pragma unroll
-                for (int k = 0; k < U; ++k) {
-                    const uint32_t jj = js + k;
-                    if (jj >= J1) break;
-                    if (jj == hi) {  // interval boundary (warp-uniform)
-                        park();
-                        acc_reset<Acc, CH, VEC, IS_MAX>(acc, arg);
-                        ++iv;
-                        lo = hi;
-                        hi = nhi;
-                        cell = ncell_id;
-                        nhi = __ldg(starts + iv + 2);
-                        ncell_id = __ldg(icells + iv + 1);
-                        enter_interval();
-                    }
-                    acc_point<Acc, CH, VEC, IS_MAX>(acc, arg, jj, ws[k], vb[k]);
-                }
-            }
-        });
-        park();
-    }
-    // the last unit with an interval and every empty unit after it
-    while (u < u_end) flush_unit();
-}
-
 // Fast mode: one CTA per heavy cell (a single interval above the unit point
 // budget).  Its 8 warps walk equal slices of the interval; the slices'
 // partial results are combined in slice order in shared memory, so the sum

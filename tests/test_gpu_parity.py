@@ -543,3 +543,23 @@ def test_per_frame_build_defers_units():
     np.testing.assert_array_equal(ex, bp.pool_interval(feats, dist, eager, grid,
                                                        exact=True).values)
     assert lazy.n_units == eager.n_units and lazy._units_pending is None
+
+
+def test_plan_staging_split_matches_run():
+    """PoolPlan.prepare (NHWC staging beside the zero fill) + reduce(zeroed)
+    equals run(); a caller-provided output buffer is always zero-filled."""
+    spec = bp.CONFIGS["T"]
+    f = spec.frustum
+    rig, feats_np, logits_np, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, f, grid)
+    feats = torch.from_numpy(feats_np).cuda()[None]
+    dist = bp.normalize_depth(torch.from_numpy(logits_np).cuda())[None]
+    plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
+                       f.depth_bins, 1, bp.Reducer.SUM)
+    want = plan.run(feats, dist).clone()
+    plan.out.fill_(7.0)
+    plan.prepare(feats)
+    np.testing.assert_array_equal(plan.reduce(dist, zeroed=True).cpu().numpy(), want.cpu().numpy())
+    mine = torch.full_like(want, 3.0)
+    plan.reduce(dist, out=mine, zeroed=True)  # not the plan's buffer: zero-filled anyway
+    np.testing.assert_array_equal(mine.cpu().numpy(), want.cpu().numpy())
