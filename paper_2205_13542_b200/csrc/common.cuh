@@ -38,13 +38,15 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct SideFork {
     cudaStream_t main, side = nullptr;
     cudaEvent_t fork = nullptr, joined = nullptr;
-    explicit SideFork(cudaStream_t s) : main(s), side(s) {
+    // which: one of two side streams (two concurrent forks need distinct ones)
+    explicit SideFork(cudaStream_t s, int which = 0) : main(s), side(s) {
         int dev = 0;
         cudaGetDevice(&dev);
-        static thread_local cudaStream_t streams[64] = {};
-        if (dev < 0 || dev >= 64) return;  // run inline
-        if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-        side = streams[dev];
+        static thread_local cudaStream_t streams[64][2] = {};
+        if (dev < 0 || dev >= 64 || which < 0 || which > 1) return;  // run inline
+        cudaStream_t &st = streams[dev][which];
+        if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        side = st;
         cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&joined, cudaEventDisableTiming);
         cudaEventRecord(fork, main);

@@ -187,10 +187,16 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     static const int wmode = [] { const char *e = getenv("BVP_FUSED_W"); return e ? atoi(e) : 1; }();
     float *wsm = reinterpret_cast<float *>(ws + L.off_w);
     const bool use_w = wmode && C % 8 == 0;  // the weight-gather kernel needs 16-byte chunks
-    if (use_w) pixel_softmax_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), wsm);
-    else pixel_lse_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), lse);
-    launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
-                                  int(HW), ctx, s);
+    // three independent prologue branches (forked streams): the depth
+    // softmax, the context's NHWC staging, the map's zero fill
+    {
+        SideFork f1(s, 0), f2(s, 1);
+        if (use_w) pixel_softmax_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), wsm);
+        else pixel_lse_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), lse);
+        launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
+                                      int(HW), ctx, f1.side);
+        cudaMemsetAsync(out, 0, size_t(B) * C * nx * ny * sizeof(float), f2.side);
+    }
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
                                     C, nx, ny, out, mode);
     p.rows = ctx;
@@ -203,6 +209,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     p.w_bstride = int64_t(N) * D * HW;
     p.scratch = scratch;
     p.scratch_bytes = scratch_bytes;
+    p.out_zeroed = 1;
     const bool is_max = mode == BVP_MAX;
     if (use_w) {
         p.wsrc = wsm;
