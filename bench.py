@@ -544,9 +544,8 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
     hplan = bp.PoolPlan(hc, hgrid, hs.n_cameras, hs.channels, hs.frustum.height, hs.frustum.width,
                         hs.frustum.depth_bins, 1, bp.Reducer.SUM, False, dev)
 
-    def hframe():
-        hb.build(hcams)
-        hplan.run(hfe, hd)
+    def hframe():  # association beside the feature staging, then the pooling
+        hplan.run_uncached(hb, hcams, hfe, hd)
     ms = _timeit(torch, hframe, flush)
     hP = hs.n_points
     hn_in, hn_int = hc.n_in_range, hc.n_intervals

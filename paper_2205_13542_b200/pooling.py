@@ -303,6 +303,23 @@ class PoolPlan:
                   stream_ptr(self.dev))
         return out
 
+    def run_uncached(self, builder, cams: torch.Tensor, features: torch.Tensor,
+                     dist: torch.Tensor) -> torch.Tensor:
+        """One frame with the geometry rebuilt (config H): ``builder`` (the
+        CacheBuilder whose buffers this plan's cache aliases) reassociates
+        the rig ``cams`` while the features' staging and the map's zero fill
+        run beside it on a side stream; then the reduction."""
+        cur = torch.cuda.current_stream(self.dev)
+        side = self.__dict__.get("_side")
+        if side is None:
+            side = self._side = torch.cuda.Stream(self.dev)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            self.prepare(features)
+        builder.build(cams)
+        cur.wait_stream(side)
+        return self.reduce(dist, zeroed=True)
+
     def graphed(self, fn, *tensors):
         """A CUDA graph of ``fn(*tensors)`` (the plan's launches on these
         buffers), captured once per buffer set and replayed after that: the

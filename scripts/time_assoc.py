@@ -44,6 +44,5 @@ for name in sys.argv[1:] or ["S", "H"]:
     tp = t(lambda: plan.run(feats, dist))
 
     def frame():
-        builder.build(cams)
-        plan.run(feats, dist)
+        plan.run_uncached(builder, cams, feats, dist)
     print(f"{name}: association {tb:8.1f} us  pool step {tp:8.1f} us  frame {t(frame):8.1f} us")

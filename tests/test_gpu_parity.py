@@ -563,3 +563,21 @@ def test_plan_staging_split_matches_run():
     mine = torch.full_like(want, 3.0)
     plan.reduce(dist, out=mine, zeroed=True)  # not the plan's buffer: zero-filled anyway
     np.testing.assert_array_equal(mine.cpu().numpy(), want.cpu().numpy())
+
+
+def test_run_uncached_matches_cached_pool():
+    """Config-H style frame (association rebuilt beside the feature staging)
+    equals pooling with an eagerly built cache."""
+    spec = bp.CONFIGS["T"]
+    f = spec.frustum
+    rig, feats_np, logits_np, grid = bp.gen_workload(spec)
+    feats = torch.from_numpy(feats_np).cuda()[None]
+    dist = bp.normalize_depth(torch.from_numpy(logits_np).cuda())[None]
+    builder = bp.CacheBuilder(spec.n_cameras, f, grid)
+    cams = torch.from_numpy(bp.rig_rows(rig)).cuda()
+    plan = bp.PoolPlan(builder.build(cams), grid, spec.n_cameras, spec.channels, f.height,
+                       f.width, f.depth_bins, 1, bp.Reducer.SUM)
+    got = plan.run_uncached(builder, cams, feats, dist).cpu().numpy()
+    want = bp.pool_interval(feats_np, bp.normalize_depth(logits_np),
+                            bp.build_cache(rig, f, grid), grid).values
+    np.testing.assert_array_equal(got.reshape(want.shape), want)
