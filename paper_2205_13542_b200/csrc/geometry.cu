@@ -524,13 +524,24 @@ __device__ __forceinline__ void warp_sort_any(uint32_t *r, int L, int lane) {
     else warp_sort_run<32>(r, L, lane);
 }
 
+// The intervals whose runs are longer than 256 points (seg_sort_long_kernel's).
+__global__ void pick_long_runs_kernel(const uint32_t *__restrict__ starts,
+                                      const int64_t *__restrict__ counts,
+                                      uint32_t *__restrict__ long_list,
+                                      uint32_t *__restrict__ n_long) {
+    const int64_t n_int = counts[1];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_int;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (__ldg(starts + i + 1) - __ldg(starts + i) > 256u)
+            long_list[atomicAdd(n_long, 1u)] = static_cast<uint32_t>(i);
+}
+
 // One warp per interval, runs of <= 256 points sorted in registers; longer
-// runs are queued for seg_sort_long_kernel (kept out of this kernel so its
-// register budget -- and occupancy -- stays that of the short runs).
+// runs are seg_sort_long_kernel's (a separate kernel on a forked stream, so
+// this one keeps the short runs' register budget and occupancy).
 __global__ void __launch_bounds__(256)
 seg_sort_warp_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ starts,
-                     const int64_t *__restrict__ counts, uint32_t *__restrict__ long_list,
-                     uint32_t *__restrict__ n_long) {
+                     const int64_t *__restrict__ counts) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_int = counts[1];
     const int64_t nwarps = int64_t(gridDim.x) * 8;
@@ -542,7 +553,7 @@ seg_sort_warp_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ 
         else if (L <= 64) warp_sort_run<2>(ranks + lo, L, lane);
         else if (L <= 128) warp_sort_run<4>(ranks + lo, L, lane);
         else if (L <= 256) warp_sort_run<8>(ranks + lo, L, lane);
-        else if (lane == 0) long_list[atomicAdd(n_long, 1u)] = static_cast<uint32_t>(iv);
+        // longer runs: seg_sort_long_kernel, concurrently
     }
 }
 
@@ -675,8 +686,12 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
             count_scatter_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, *fp, packed, ranks, iop);
         else
             count_scatter_flat_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, P, packed, ranks, iop);
-        seg_sort_warp_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, counts, long_list, n_long);
-        seg_sort_long_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, long_list, n_long);
+        pick_long_runs_kernel<<<cb, 256, 0, s>>>(starts, counts, long_list, n_long);
+        {  // short runs and long runs side by side
+            SideFork fork(s);
+            seg_sort_long_kernel<<<148 * 4, 256, 0, fork.side>>>(ranks, starts, long_list, n_long);
+            seg_sort_warp_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, counts);
+        }
         return check_launch("sort_intervals");
     }
     const unsigned tiles = static_cast<unsigned>(L.n_tiles);
