@@ -41,8 +41,18 @@ grad_rows_kernel(const float *__restrict__ grad_out, const uint32_t *__restrict_
     const uint32_t i0 = cell_first[cell0], i1 = cell_first[cell0 + rem];
     if (i0 == i1) return;
     const float *g = grad_out + int64_t(b) * C * n_cells + cell0;
-    for (int c = warp; c < C; c += 4)
-        s[c * kRowPitch + lane] = lane < rem ? __ldg(g + int64_t(c) * n_cells + lane) : 0.f;
+    // 8 channel rows per warp in flight at a time
+    for (int c0 = warp; c0 < C; c0 += 32) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int c = c0 + 4 * q;
+            v[q] = (c < C && lane < rem) ? __ldg(g + int64_t(c) * n_cells + lane) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (c0 + 4 * q < C) s[(c0 + 4 * q) * kRowPitch + lane] = v[q];
+    }
     __syncthreads();
     for (uint32_t i = i0 + warp; i < i1; i += 4) {
         const int lc = static_cast<int>(icells[i] - cell0);
