@@ -154,6 +154,23 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D,
                     int64_t *counts, void *workspace, size_t workspace_bytes,
                     void *stream);
 
+/* One call per frame (CacheBuilder, config H): bvp_build_cache, with the
+ * chunk list (bvp_make_work, cell order, tile -1) built on a forked stream
+ * as soon as the interval tables exist -- beside the rank scatter and run
+ * sorts -- and the point gather table (bvp_point_meta) after the ranks.
+ * work_workspace: bvp_work_workspace_bytes(min(n_cells, P), P, chunk, nx, ny,
+ * -1) bytes, distinct from workspace. */
+int bvp_build_association(const double *cams, int N, int H, int W, int D,
+                          double depth_min, double depth_step, const double *grid,
+                          int nx, int ny, uint32_t *cell_of_point, uint32_t *ranks,
+                          uint32_t *interval_starts, uint32_t *interval_cells,
+                          uint32_t *cell_first, uint32_t *interval_of_point,
+                          int64_t *counts, int chunk, uint32_t *work,
+                          uint32_t *splits, int64_t *work_counts,
+                          uint32_t *point_meta, void *workspace,
+                          size_t workspace_bytes, void *work_workspace,
+                          size_t work_workspace_bytes, void *stream);
+
 /* ---- work schedule (cached with the association) ---------------------- */
 
 /* Capacities of the schedule arrays and the builder's workspace. */

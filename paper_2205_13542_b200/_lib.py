@@ -49,6 +49,8 @@ SIGNATURES = {
     "bvp_sort_intervals": (_I, [_P, _L, _L, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
     "bvp_build_cache": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _I, _I, _P, _P, _P, _P, _P, _P,
                              _P, _P, _S, _P]),
+    "bvp_build_association": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _I, _I, _P, _P, _P, _P, _P, _P,
+                                   _P, _I, _P, _P, _P, _P, _P, _S, _P, _S, _P]),
     "bvp_pool_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
     "bvp_units_capacity": (_L, [_I, _I, _L]),
     "bvp_units_workspace_bytes": (_S, [_I, _I]),

@@ -364,7 +364,7 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
 
 def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
                    task_budget: int = TASK_BUDGET, work_tile: int = WORK_TILE,
-                   defer_units: bool = False):
+                   defer_units: bool = False, work_done: bool = False):
     """Chunk schedule (work) and point gather table, plus the work units and
     tasks -- or, defer_units, a closure that builds the units later (only the
     exact mode and very wide channel counts read them).  Returns the closure
@@ -378,13 +378,13 @@ def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
                   ptr(b["meta"]) if meta else None, ptr(b["ws"]), b["ws"].numel(),
                   stream_ptr(dev))
 
-    if "work" in b:
+    if "work" in b and not work_done:
         _lib.call("bvp_make_work", ptr(b["starts"]), ptr(b["icells"]), ptr(b["counts"]),
                   b["n_int_max"], b["ranks"].numel(), CHUNK, nx, ny, work_tile, ptr(b["work"]),
                   ptr(b["splits"]),
                   ptr(b["work_counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
     if defer_units and "work" in b:
-        if dims is not None:
+        if dims is not None and not work_done:
             _lib.call("bvp_point_meta", ptr(b["ranks"]), ptr(b["counts"]), N, H, W, D,
                       ptr(b["meta"]), stream_ptr(dev))
         return lambda: units(False)
@@ -424,8 +424,15 @@ class CacheBuilder:
         # sort costs more than it saves once per frame); cached builds sort
         self.work_tile = WORK_TILE if sort_work else -1
         # per-frame rebuilds also defer the work units (built on first use)
+        # and build the chunk list beside the rank sort (own workspace)
         self.defer_units = not sort_work
         self._grid_arr = grid.as_array()
+        self._one_call = self.defer_units and CHUNK > 0
+        if self._one_call:
+            b = self.bufs
+            n = int(_lib.load().bvp_work_workspace_bytes(b["n_int_max"], self.P, CHUNK, grid.nx,
+                                                         grid.ny, -1))
+            b["wws"] = torch.empty(n, dtype=torch.uint8, device=self.dev)
 
     def build(self, cams: torch.Tensor, fingerprint: int = 0) -> AssociationCache:
         """cams: (N, 16) float64 CUDA tensor (see geometry.rig_rows)."""
@@ -433,12 +440,24 @@ class CacheBuilder:
         if cams.dtype != torch.float64 or cams.shape != (self.n_cameras, 16) or not cams.is_cuda:
             raise ConfigurationError("cams must be a CUDA float64 (N, 16) tensor")
         cams = cams.contiguous()
+        dims = (self.n_cameras, f.height, f.width, f.depth_bins)
+        if self._one_call:
+            _lib.call("bvp_build_association", ptr(cams), *dims, f.depth_min, f.depth_step,
+                      self._grid_arr.ctypes.data, g.nx, g.ny, ptr(b["cells"]), ptr(b["ranks"]),
+                      ptr(b["starts"]), ptr(b["icells"]), ptr(b["cell_first"]), ptr(b["iop"]),
+                      ptr(b["counts"]), CHUNK, ptr(b["work"]), ptr(b["splits"]),
+                      ptr(b["work_counts"]), ptr(b["meta"]), ptr(b["ws"]), b["ws"].numel(),
+                      ptr(b["wws"]), b["wws"].numel(), stream_ptr(self.dev))
+            pending = _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims,
+                                     defer_units=True, work_done=True)
+            cache = _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
+            cache._units_pending = pending
+            return cache
         _lib.call("bvp_build_cache", ptr(cams), self.n_cameras, f.height, f.width, f.depth_bins,
                   f.depth_min, f.depth_step, self._grid_arr.ctypes.data, g.nx, g.ny,
                   ptr(b["cells"]), ptr(b["ranks"]), ptr(b["starts"]), ptr(b["icells"]),
                   ptr(b["cell_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
                   b["ws"].numel(), stream_ptr(self.dev))
-        dims = (self.n_cameras, f.height, f.width, f.depth_bins)
         pending = _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims,
                                  work_tile=self.work_tile, defer_units=self.defer_units)
         cache = _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)

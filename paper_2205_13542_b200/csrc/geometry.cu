@@ -7,6 +7,7 @@
 // bevgrid.py:183-203 (build_cache).  Paths relative to pkg/src/bevpool/.
 #include <algorithm>
 #include <cstdio>
+#include <functional>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -643,10 +644,16 @@ static SortLayout sort_layout(int64_t P, int64_t n_cells) {
     return L;
 }
 
+// Optional work a caller hangs on the sort: `on_tables` runs (on a forked
+// stream) as soon as the interval tables exist, beside the rank scatter and
+// run sorts; `on_ranks` follows the final ranks on the main stream.
+using SortHook = std::function<int(cudaStream_t)>;
+
 static int sort_impl(const double *cams, const FrustumParams *fp, const GridParams *gp,
                      uint32_t *cells, int64_t P, int64_t n_cells, uint32_t *ranks,
                      uint32_t *starts, uint32_t *icells, uint32_t *cell_first, uint32_t *iop,
-                     int64_t *counts, void *ws, size_t ws_bytes, cudaStream_t s) {
+                     int64_t *counts, void *ws, size_t ws_bytes, cudaStream_t s,
+                     const SortHook *on_tables = nullptr, const SortHook *on_ranks = nullptr) {
     const SortLayout L = sort_layout(P, n_cells);
     BVP_REQUIRE(ws != nullptr && ws_bytes >= L.bytes, BVP_ERR_INVALID,
                 "sort workspace too small: need %zu bytes, got %zu", L.bytes, ws_bytes);
@@ -682,6 +689,8 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
         make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
                                                  icells, cell_first, counts);
+        SideFork tables(s, 1);
+        const int rc_t = on_tables ? (*on_tables)(tables.side) : BVP_OK;
         if (cams)
             count_scatter_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, *fp, packed, ranks, iop);
         else
@@ -692,6 +701,10 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
             seg_sort_long_kernel<<<148 * 4, 256, 0, fork.side>>>(ranks, starts, long_list, n_long);
             seg_sort_warp_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, counts);
         }
+        const int rc_r = on_ranks ? (*on_ranks)(s) : BVP_OK;
+        tables.join();
+        if (rc_t != BVP_OK) return rc_t;
+        if (rc_r != BVP_OK) return rc_r;
         return check_launch("sort_intervals");
     }
     const unsigned tiles = static_cast<unsigned>(L.n_tiles);
@@ -732,6 +745,14 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
                 kin, vin, P, counts, shift, L.digit_bits, hist, L.n_tiles, kout, vout);
         kin = kout;
         vin = vout;
+    }
+    if (on_tables) {
+        const int rc = (*on_tables)(s);
+        if (rc != BVP_OK) return rc;
+    }
+    if (on_ranks) {
+        const int rc = (*on_ranks)(s);
+        if (rc != BVP_OK) return rc;
     }
     return check_launch("sort_intervals");
 }
@@ -787,6 +808,36 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D, double depth
     return sort_impl(cams, &f, &g, cell_of_point, int64_t(N) * H * W * D, int64_t(nx) * ny,
                      ranks, interval_starts, interval_cells, cell_first, interval_of_point,
                      counts, workspace, workspace_bytes, as_stream(stream));
+}
+
+int bvp_build_association(const double *cams, int N, int H, int W, int D, double depth_min,
+                          double depth_step, const double *grid, int nx, int ny,
+                          uint32_t *cell_of_point, uint32_t *ranks, uint32_t *interval_starts,
+                          uint32_t *interval_cells, uint32_t *cell_first,
+                          uint32_t *interval_of_point, int64_t *counts, int chunk,
+                          uint32_t *work, uint32_t *splits, int64_t *work_counts,
+                          uint32_t *point_meta, void *workspace, size_t workspace_bytes,
+                          void *work_workspace, size_t work_workspace_bytes, void *stream) {
+    BVP_REQUIRE(cams && grid && cell_of_point && ranks && interval_starts && interval_cells &&
+                    cell_first && counts && work && splits && work_counts && point_meta,
+                BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(N > 0 && H > 0 && W > 0 && D > 0 && nx > 0 && ny > 0, BVP_ERR_INVALID,
+                "frustum/grid dims must be positive");
+    const FrustumParams f{N, H, W, D, depth_min, depth_step};
+    const GridParams g = grid_params(grid, nx, ny);
+    const int64_t P = int64_t(N) * H * W * D, n_cells = int64_t(nx) * ny;
+    const int64_t n_int_max = std::min(n_cells, P);
+    const SortHook tables = [&](cudaStream_t side) {
+        return bvp_make_work(interval_starts, interval_cells, counts, n_int_max, P, chunk, nx, ny,
+                             -1, work, splits, work_counts, work_workspace, work_workspace_bytes,
+                             side);
+    };
+    const SortHook sorted = [&](cudaStream_t main) {
+        return bvp_point_meta(ranks, counts, N, H, W, D, point_meta, main);
+    };
+    return sort_impl(cams, &f, &g, cell_of_point, P, n_cells, ranks, interval_starts,
+                     interval_cells, cell_first, interval_of_point, counts, workspace,
+                     workspace_bytes, as_stream(stream), &tables, &sorted);
 }
 
 }  // extern "C"
