@@ -581,3 +581,17 @@ def test_run_uncached_matches_cached_pool():
     want = bp.pool_interval(feats_np, bp.normalize_depth(logits_np),
                             bp.build_cache(rig, f, grid), grid).values
     np.testing.assert_array_equal(got.reshape(want.shape), want)
+
+
+@pytest.mark.parametrize("C", [1, 3, 20, 80, 200, 250, 256, 512])
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+def test_exact_mode_channel_sweep(C, red):
+    """exact=True is bit-identical to the fp64 restatement for every lane
+    layout: the chunk-schedule path and (C = 250, 512: too wide for it) the
+    work-unit path, both with their in-order walks of the long intervals."""
+    cache, grid, features, logits = _sweep_case(C, seed=5)
+    dist = o.normalize_depth(logits)
+    want = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
+                           cache.interval_cells, grid.n_cells, red)
+    got = bp.pool_interval(features, dist, cache, grid, red, exact=True).values
+    np.testing.assert_array_equal(got.reshape(want.shape), want)
