@@ -128,6 +128,7 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
 }
 
 // ---- depth softmax (lift.py:17-31), 64-bit math ------------------------------
+// Thread per pixel, the depth bins in order (any D).
 __global__ void normalize_depth_kernel(const float *__restrict__ logits, int64_t NB, int D,
                                        int HW, float *__restrict__ dist) {
     const int64_t total = NB * HW;
@@ -143,6 +144,55 @@ __global__ void normalize_depth_kernel(const float *__restrict__ logits, int64_t
         for (int d = 0; d < D; ++d)
             o[int64_t(d) * HW] = float(exp(double(l[int64_t(d) * HW]) - double(m)) / sum);
     }
+}
+
+// D <= 8 * kSoftSlice: CTA per 32 pixels (lane = pixel, coalesced), warp w
+// owns the contiguous depth slice [w*S, (w+1)*S): its logits and their fp64
+// exponentials stay in registers (one exp per point), the slice sums are
+// added in slice order -- so every pixel's sum runs over d in order, in 8
+// sequential pieces.
+constexpr int kSoftSlice = 16;
+__global__ void __launch_bounds__(256)
+normalize_depth_tile_kernel(const float *__restrict__ logits, int64_t NB, int D, int HW,
+                            float *__restrict__ dist) {
+    __shared__ float s_m[8][32];
+    __shared__ double s_s[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tiles = (HW + 31) / 32;
+    const int64_t n = blockIdx.x / tiles;
+    const int hw = int(blockIdx.x - n * tiles) * 32 + lane;
+    const bool ok = hw < HW;
+    const int S = (D + 7) / 8, d0 = warp * S, d1 = min(D, d0 + S);
+    const float *l = logits + n * D * int64_t(HW) + (ok ? hw : 0);
+    float v[kSoftSlice];
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kSoftSlice; ++i) {
+        v[i] = (d0 + i < d1) ? l[int64_t(d0 + i) * HW] : -INFINITY;
+        m = fmaxf(m, v[i]);
+    }
+    s_m[warp][lane] = m;
+    __syncthreads();
+    float M = s_m[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) M = fmaxf(M, s_m[w][lane]);
+    double e[kSoftSlice];
+    double part = 0.0;
+#pragma unroll
+    for (int i = 0; i < kSoftSlice; ++i) {
+        e[i] = (d0 + i < d1) ? exp(double(v[i]) - double(M)) : 0.0;
+        part += e[i];
+    }
+    s_s[warp][lane] = part;
+    __syncthreads();
+    double sum = s_s[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) sum += s_s[w][lane];
+    if (!ok) return;
+    float *o = dist + n * D * int64_t(HW) + hw;
+#pragma unroll
+    for (int i = 0; i < kSoftSlice; ++i)
+        if (d0 + i < d1) o[int64_t(d0 + i) * HW] = float(e[i] / sum);
 }
 
 __global__ void any_nonfinite_kernel(const float *__restrict__ x, int64_t n, int *flag) {
@@ -345,6 +395,12 @@ int bvp_normalize_depth(const float *logits, int NB, int D, int H, int W, float 
                 "bad arguments");
     const int64_t total = int64_t(NB) * H * W;
     if (total == 0) return BVP_OK;
+    if (D <= 8 * kSoftSlice) {
+        const int64_t tiles = int64_t(NB) * ceil_div(int64_t(H) * W, 32);
+        normalize_depth_tile_kernel<<<static_cast<unsigned>(tiles), 256, 0, as_stream(stream)>>>(
+            logits, NB, D, H * W, dist);
+        return check_launch("normalize_depth");
+    }
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(total, 128), 148 * 16));
     normalize_depth_kernel<<<blocks, 128, 0, as_stream(stream)>>>(logits, NB, D, H * W, dist);
     return check_launch("normalize_depth");

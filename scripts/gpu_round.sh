@@ -14,3 +14,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/gmlp scripts/gather_mlp
 ls -la $OUT
 timeout 300 python scripts/time_train.py 4 > $OUT/train.txt 2>&1
 timeout 300 python scripts/time_assoc.py S H > $OUT/assoc.txt 2>&1
+timeout 900 python scripts/stage_compare.py > $OUT/stages.txt 2>&1
