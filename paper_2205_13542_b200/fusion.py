@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .bevgrid import BevGridSpec, cuda_device, ptr, stream_ptr
+from .bevgrid import BevGridSpec, cuda_device, ptr, stream_ptr, to_numpy
 from .errors import ValidationError
 from .pooling import _MODE, BevFeatureMap, Reducer, _reducer
 
@@ -47,7 +47,7 @@ def lidar_to_bev(points, grid: BevGridSpec, reducer=Reducer.SUM) -> BevFeatureMa
     _lib.call("bvp_lidar_to_bev", ptr(t) if M else None, M, g.ctypes.data, grid.nx, grid.ny,
               _MODE[reducer], ptr(out), ptr(ws), ws.numel(), stream_ptr(dev))
     v = out.view(3, grid.nx, grid.ny)
-    return BevFeatureMap(v.cpu().numpy() if host else v, grid)
+    return BevFeatureMap(to_numpy(v) if host else v, grid)
 
 
 def fuse_concat(a: BevFeatureMap, b: BevFeatureMap) -> BevFeatureMap:
@@ -82,7 +82,7 @@ def grid_resample(src: BevFeatureMap, dst_grid: BevGridSpec) -> BevFeatureMap:
     sa, da = sg.as_array(), dst_grid.as_array()
     _lib.call("bvp_grid_resample_f32", ptr(t), C, sa.ctypes.data, sg.nx, sg.ny, da.ctypes.data,
               dst_grid.nx, dst_grid.ny, ptr(out), stream_ptr(dev))
-    return BevFeatureMap(out.cpu().numpy() if host else out, dst_grid)
+    return BevFeatureMap(to_numpy(out) if host else out, dst_grid)
 
 
 def bev_encoder(fused: BevFeatureMap) -> BevFeatureMap:

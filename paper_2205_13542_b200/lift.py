@@ -6,7 +6,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .bevgrid import cuda_device, ptr, stream_ptr
+from .bevgrid import cuda_device, ptr, stream_ptr, to_numpy
 from .errors import ValidationError
 
 
@@ -44,7 +44,7 @@ def normalize_depth(logits, check_finite: bool = True):
     out = torch.empty_like(t)
     if t.numel():
         _lib.call("bvp_normalize_depth", ptr(t), NB, D, H, W, ptr(out), stream_ptr(t.device))
-    return out.cpu().numpy() if host else out
+    return to_numpy(out) if host else out
 
 
 def point_weight(dist, n: int, h: int, w: int, d: int) -> float:

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .bevgrid import AssociationCache, BevGridSpec, cuda_device, ptr, stream_ptr
+from .bevgrid import AssociationCache, BevGridSpec, cuda_device, ptr, stream_ptr, to_numpy
 from .errors import ConfigurationError, StaleCacheError, UnsupportedReducerError, ValidationError
 from .lift import any_nonfinite
 
@@ -171,7 +171,7 @@ def _finish(out: torch.Tensor, inp: _Inputs, grid: BevGridSpec) -> BevFeatureMap
     if not inp.batched:
         v = v[0]
     if inp.host:
-        v = v.cpu().numpy()
+        v = to_numpy(v)
     return BevFeatureMap(v, grid)
 
 
@@ -455,7 +455,7 @@ def reorder_weights(dist, cache: AssociationCache):
     w = torch.empty(n_in, dtype=torch.float32, device=dev)
     _lib.call("bvp_reorder_weights", ptr(dt), ptr(cache.d_ranks), n_in, nd, d_, hd, wd, ptr(w),
               stream_ptr(dev))
-    return w.cpu().numpy() if host else w
+    return to_numpy(w) if host else w
 
 
 # --------------------------------------------------------------------------
