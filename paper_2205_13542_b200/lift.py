@@ -10,12 +10,23 @@ from .bevgrid import cuda_device, ptr, stream_ptr, to_numpy
 from .errors import ValidationError
 
 
+def nonfinite_flags(*tensors: torch.Tensor) -> list:
+    """Device finiteness scans of float32 CUDA tensors, one flag each, read
+    back with a single host sync."""
+    if not tensors:
+        return []
+    flags = torch.zeros(len(tensors), dtype=torch.int32, device=tensors[0].device)
+    for k, t in enumerate(tensors):
+        t = t.contiguous()
+        if t.numel():
+            _lib.call("bvp_any_nonfinite", ptr(t), t.numel(), ptr(flags[k:]),
+                      stream_ptr(t.device))
+    return [bool(v) for v in flags.tolist()]
+
+
 def any_nonfinite(t: torch.Tensor) -> bool:
     """Device finiteness scan of a float32 CUDA tensor (one host sync)."""
-    flag = torch.zeros(1, dtype=torch.int32, device=t.device)
-    t = t.contiguous()
-    _lib.call("bvp_any_nonfinite", ptr(t), t.numel(), ptr(flag), stream_ptr(t.device))
-    return bool(flag.item())
+    return nonfinite_flags(t)[0]
 
 
 def normalize_depth(logits, check_finite: bool = True):

@@ -30,7 +30,7 @@ import torch
 from . import _lib
 from .bevgrid import AssociationCache, BevGridSpec, cuda_device, ptr, stream_ptr, to_numpy
 from .errors import ConfigurationError, StaleCacheError, UnsupportedReducerError, ValidationError
-from .lift import any_nonfinite
+from .lift import nonfinite_flags
 
 #: default accumulation: fp32 (fast; within 1.2e-7 of the reference at the
 #: nuScenes shape, bar 1e-5).  exact=True reproduces the reference's 64-bit
@@ -145,9 +145,10 @@ def _check_inputs(features, dist, cache: AssociationCache, grid: BevGridSpec,
         ft = features.contiguous().view(fs)
         dt = dist.contiguous().view(ds)
     if check_finite:
-        if ft.numel() and any_nonfinite(ft):
+        bad_f, bad_d = nonfinite_flags(ft, dt)  # one host sync for both
+        if bad_f:
             raise ValidationError("features contain non-finite values")
-        if dt.numel() and any_nonfinite(dt):
+        if bad_d:
             raise ValidationError("dist contains non-finite values")
     if cache.n_points != n * h * w * d:
         raise StaleCacheError(
