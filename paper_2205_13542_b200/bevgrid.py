@@ -139,6 +139,10 @@ CHUNK = int(os.environ.get("BVP_CHUNK", "64"))
 #: chunk order: 0 = longest first (cell order within a length); > 0 = by 2D
 #: tiles of WORK_TILE x WORK_TILE cells, longest first within a tile
 WORK_TILE = int(os.environ.get("BVP_WORK_TILE", "0"))
+#: chunk length of the exact mode's own chunk list: its lane groups sum whole
+#: intervals up to this length in fp64; longer ones are walked in order by a
+#: CTA each (pool_exact_long_kernel), so fewer, longer chunks suit it
+EXACT_CHUNK = int(os.environ.get("BVP_EXACT_CHUNK", "128"))
 
 
 def work_bounds(n_points: int, n_int_max: int, chunk: int) -> tuple[int, int, int]:
@@ -249,12 +253,13 @@ class AssociationCache:
         self._host.pop("scratch", None)
 
     def schedule(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1, *,
-                 units: bool = True):
+                 units: bool = True, exact: bool = False):
         """The bvp_schedule the C ABI takes; the point gather table is
         (re)derived for an (N, H, W, D) frustum (N=None: the caller does not
         read it, e.g. the materialised path).  units=False: the caller's
         launch needs only the chunk schedule (bvp_pool_needs_units), so units
-        deferred by a per-frame build are not built for it."""
+        deferred by a per-frame build are not built for it.  exact=True: the
+        exact mode's own chunk list (EXACT_CHUNK), built on first use."""
         if N is not None and self.meta_dims != (N, H, W, D):
             _lib.call("bvp_point_meta", ptr(self.d_ranks), ptr(self.d_counts), N, H, W, D,
                       ptr(self.d_meta), stream_ptr(self.device))
@@ -262,11 +267,15 @@ class AssociationCache:
         with_units = units or self.d_work is None
         if with_units:
             self.ensure_units()
-        key = ("schedules", self._units_pending is None)
+        xw = self.exact_work() if exact and self.d_work is not None else None
+        key = ("schedules", self._units_pending is None, xw is not None)
         s = self._host.get(key)
         if s is None:
             work = (None, None, None, 0, 0, 0, 0)
-            if self.d_work is not None:
+            if xw is not None:
+                work = (ptr(xw["work"]), ptr(xw["splits"]), ptr(xw["counts"]), *xw["bounds"],
+                        EXACT_CHUNK)
+            elif self.d_work is not None:
                 work = (ptr(self.d_work), ptr(self.d_splits), ptr(self.d_work_counts),
                         self.max_work, self.max_splits, self.max_partials, self.chunk)
             if self._units_pending is None:
@@ -278,6 +287,26 @@ class AssociationCache:
                                   *work)
             self._host[key] = s
         return s
+
+    def exact_work(self) -> dict:
+        """The exact mode's chunk list: intervals of <= EXACT_CHUNK points as
+        single chunks, longest first (one build per cache, stream ordered)."""
+        xw = self._host.get("exact_work")
+        if xw is None:
+            dev, i32 = self.device, dict(dtype=torch.int32, device=self.device)
+            n_int_max, P = self.n_int_max, int(self.d_ranks.numel())
+            mw, ms, mp = work_bounds(P, n_int_max, EXACT_CHUNK)
+            xw = dict(work=torch.empty(4 * mw, **i32), splits=torch.empty(4 * ms, **i32),
+                      counts=torch.zeros(3, dtype=torch.int64, device=dev), bounds=(mw, ms, mp))
+            ws = torch.empty(int(_lib.load().bvp_work_workspace_bytes(
+                n_int_max, P, EXACT_CHUNK, self.nx, self.ny, 0)), dtype=torch.uint8, device=dev)
+            _lib.call("bvp_make_work", ptr(self.d_interval_starts), ptr(self.d_interval_cells),
+                      ptr(self.d_counts), n_int_max, P, EXACT_CHUNK, self.nx, self.ny, 0,
+                      ptr(xw["work"]), ptr(xw["splits"]), ptr(xw["counts"]), ptr(ws), ws.numel(),
+                      stream_ptr(dev))
+            xw["ws"] = ws  # kept until the build has run (stream ordered)
+            self._host["exact_work"] = xw
+        return xw
 
     def ensure_units(self) -> None:
         """Build the work units / tasks a per-frame build deferred (stream

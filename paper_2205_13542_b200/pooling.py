@@ -195,7 +195,7 @@ def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
                   ptr(cache.d_cell_first),
                   cache.schedule(inp.N, inp.H, inp.W, inp.D,
-                                 units=cache.needs_units(inp.C, exact=exact)),
+                                 units=cache.needs_units(inp.C, exact=exact), exact=bool(exact)),
                   inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
                   grid.nx, grid.ny, cache.n_int_max, _MODE[reducer],
                   exact, ptr(out), ptr(nhwc), None,
@@ -284,7 +284,8 @@ class PoolPlan:
         c = self.cache
         _lib.call("bvp_pool_forward_nhwc_f32", ptr(self.nhwc), ptr(dist), ptr(c.d_ranks),
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
-                  c.schedule(self.N, self.H, self.W, self.D, units=self._units), self.B,
+                  c.schedule(self.N, self.H, self.W, self.D, units=self._units,
+                             exact=bool(self.exact)), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
                   mode, self.exact, ptr(out), None, *self._scratch, stream_ptr(self.dev))
         return out
@@ -298,7 +299,8 @@ class PoolPlan:
         c = self.cache
         _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(c.d_ranks),
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
-                  c.schedule(self.N, self.H, self.W, self.D, units=self._units), self.B,
+                  c.schedule(self.N, self.H, self.W, self.D, units=self._units,
+                             exact=bool(self.exact)), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
                   self.mode, self.exact, ptr(out), ptr(self.nhwc), None, *self._scratch,
                   stream_ptr(self.dev))
