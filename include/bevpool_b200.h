@@ -253,9 +253,20 @@ int bvp_to_nhwc_f32(const float *src, int NB, int C, int HW, float *dst,
 
 /* The first half of bvp_pool_forward_f32: the features' NHWC staging and the
  * zero fill of out (B, C, n_cells), side by side on a forked stream.  Follow
- * with bvp_pool_forward_nhwc_f32(..., mode | BVP_OUT_ZEROED, ...). */
+ * with bvp_pool_forward_nhwc_f32(..., mode | BVP_OUT_ZEROED, ...).  out = NULL:
+ * the staging alone (the fast reduction then zeroes the empty cells beside
+ * its kernels). */
 int bvp_pool_prepare_f32(const float *features, int B, int N, int C, int H, int W,
                          float *feats_nhwc, float *out, int64_t n_cells, void *stream);
+
+/* Zero fill of the cells of out (B, C, n_cells) that no interval covers
+ * (cell_first[c] == cell_first[c+1]); occupied cells are untouched.  The fast
+ * reduction runs it beside its kernels when out was not zero-filled
+ * (bvp_pool_prepare_f32 with out = NULL stages the features alone).  No
+ * reference counterpart: the reference's pool_interval allocates a zeroed
+ * map (pooling.py:213). */
+int bvp_zero_empty_cells(const uint32_t *cell_first, int64_t n_cells, int C, int B, float *out,
+                         void *stream);
 
 /* Same as bvp_pool_forward_f32 with the features already NHWC (B,N,H,W,C). */
 int bvp_pool_forward_nhwc_f32(const float *feats_nhwc, const float *dist,

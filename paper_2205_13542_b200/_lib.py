@@ -68,6 +68,7 @@ SIGNATURES = {
                                        _I, _L, _I, _I, _P, _P, _P, _S, _P]),
     "bvp_to_nhwc_f32": (_I, [_P, _I, _I, _I, _P, _P]),
     "bvp_pool_prepare_f32": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _L, _P]),
+    "bvp_zero_empty_cells": (_I, [_P, _L, _I, _I, _P, _P]),
     "bvp_reorder_weights": (_I, [_P, _P, _L, _I, _I, _I, _I, _P, _P]),
     "bvp_normalize_depth": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "bvp_any_nonfinite": (_I, [_P, _L, _P, _P]),

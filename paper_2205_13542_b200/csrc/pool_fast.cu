@@ -24,3 +24,16 @@ extern "C" int bvp_pool_needs_units(int C, int bf16, int exact) {
     int L, lg, cpl;
     return choose_group(C / vec, vec, L, lg, cpl) ? 0 : 1;
 }
+
+// Zero fill of the empty cells of out (B, C, n_cells): the cells no interval
+// covers (cell_first[c] == cell_first[c+1]).  Occupied cells are left as they are.
+extern "C" int bvp_zero_empty_cells(const uint32_t *cell_first, int64_t n_cells, int C, int B,
+                                    float *out, void *stream) {
+    BVP_REQUIRE(n_cells >= 0 && C >= 0 && B >= 0, BVP_ERR_INVALID, "bad dims");
+    if (n_cells == 0 || C == 0 || B == 0) return BVP_OK;
+    BVP_REQUIRE(cell_first && out, BVP_ERR_INVALID, "null pointer argument");
+    bvp::zero_empty_cells_kernel<<<bvp::kNumSms, bvp::kZeroThreads, 0,
+                                   static_cast<cudaStream_t>(stream)>>>(cell_first, n_cells, C, B,
+                                                                         out);
+    return bvp::check_launch("zero_empty_cells");
+}

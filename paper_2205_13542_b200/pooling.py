@@ -268,11 +268,14 @@ class PoolPlan:
         _lib.call("bvp_to_nhwc_f32", ptr(features), self.B * self.N, self.C, self.H * self.W,
                   ptr(self.nhwc), stream_ptr(self.dev))
 
-    def prepare(self, features: torch.Tensor) -> None:
+    def prepare(self, features: torch.Tensor, zero: bool = True) -> None:
         """NHWC staging of the features beside the zero fill of the plan's
-        output map (forked stream); follow with reduce(dist, zeroed=True)."""
+        output map (forked stream); follow with reduce(dist, zeroed=True).
+        zero=False: the staging alone; reduce(dist) then zeroes the empty
+        cells beside its kernels."""
         _lib.call("bvp_pool_prepare_f32", ptr(features), self.B, self.N, self.C, self.H, self.W,
-                  ptr(self.nhwc), ptr(self.out), self.grid.n_cells, stream_ptr(self.dev))
+                  ptr(self.nhwc), ptr(self.out) if zero else None, self.grid.n_cells,
+                  stream_ptr(self.dev))
 
     def reduce(self, dist: torch.Tensor, out: torch.Tensor | None = None,
                zeroed: bool = False) -> torch.Tensor:
