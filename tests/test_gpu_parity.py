@@ -595,3 +595,35 @@ def test_exact_mode_channel_sweep(C, red):
                            cache.interval_cells, grid.n_cells, red)
     got = bp.pool_interval(features, dist, cache, grid, red, exact=True).values
     np.testing.assert_array_equal(got.reshape(want.shape), want)
+
+
+@pytest.mark.parametrize("name", ["T", "S"])
+def test_empty_cells_zeroed_beside_reduction(name):
+    """PoolPlan.run zeroes only the empty cells, beside the chunk kernel
+    (bvp_zero_empty_cells on a forked stream): a NaN-poisoned map comes out
+    equal to the oracle for every reducer, batch 2 included; the bare entry
+    point zeroes exactly the cells no interval covers."""
+    spec = bp.CONFIGS[name]
+    f = spec.frustum
+    rig, feats_np, logits_np, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, f, grid)
+    dist_np = o.normalize_depth(logits_np)
+    feats = torch.from_numpy(np.stack([feats_np, -feats_np])).cuda()
+    dist = torch.from_numpy(np.stack([dist_np, dist_np])).cuda()
+    for red in bp.Reducer:
+        plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
+                           f.depth_bins, 2, red)
+        plan.out.fill_(float("nan"))
+        got = plan.run(feats, dist).cpu().numpy()
+        for b, fb in enumerate((feats_np, -feats_np)):
+            want = o.pool_interval(fb, dist_np, cache.ranks, cache.interval_starts,
+                                   cache.interval_cells, grid.n_cells, red.value)
+            assert max_rel_dev(want, got[b].reshape(want.shape)) <= FP32_TOL, (red, b)
+    out = torch.full((2, spec.channels, grid.n_cells), float("nan"), device="cuda")
+    bp._lib.call("bvp_zero_empty_cells", cache.d_cell_first.data_ptr(), grid.n_cells,
+                 spec.channels, 2, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    occupied = np.zeros(grid.n_cells, bool)
+    occupied[np.asarray(cache.interval_cells)] = True
+    o_np = out.cpu().numpy()
+    assert np.isnan(o_np[:, :, occupied]).all()
+    assert (o_np[:, :, ~occupied] == 0).all()
