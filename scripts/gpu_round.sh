@@ -15,3 +15,4 @@ ls -la $OUT
 timeout 300 python scripts/time_train.py 4 > $OUT/train.txt 2>&1
 timeout 300 python scripts/time_assoc.py S H > $OUT/assoc.txt 2>&1
 timeout 900 python scripts/stage_compare.py > $OUT/stages.txt 2>&1
+timeout 300 python scripts/time_zero.py > $OUT/zero_fill.txt 2>&1
