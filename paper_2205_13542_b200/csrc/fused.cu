@@ -187,6 +187,10 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     static const int wmode = [] { const char *e = getenv("BVP_FUSED_W"); return e ? atoi(e) : 1; }();
     float *wsm = reinterpret_cast<float *>(ws + L.off_w);
     const bool use_w = wmode && C % 8 == 0;  // the weight-gather kernel needs 16-byte chunks
+    // BVP_FUSED_ZERO=1: no memset branch; the reduction zeroes the empty cells
+    // beside its kernels (as the fp32 fast path does)
+    static const int zmode = [] { const char *e = getenv("BVP_FUSED_ZERO"); return e ? atoi(e) : 0; }();
+    const bool zero_beside = zmode && schedule->work;
     // three independent prologue branches (forked streams): the depth
     // softmax, the context's NHWC staging, the map's zero fill
     {
@@ -195,7 +199,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
         else pixel_lse_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), lse);
         launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
                                       int(HW), ctx, f1.side);
-        cudaMemsetAsync(out, 0, size_t(B) * C * nx * ny * sizeof(float), f2.side);
+        if (!zero_beside) cudaMemsetAsync(out, 0, size_t(B) * C * nx * ny * sizeof(float), f2.side);
     }
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
                                     C, nx, ny, out, mode);
@@ -209,7 +213,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     p.w_bstride = int64_t(N) * D * HW;
     p.scratch = scratch;
     p.scratch_bytes = scratch_bytes;
-    p.out_zeroed = 1;
+    p.out_zeroed = zero_beside ? 0 : 1;
     const bool is_max = mode == BVP_MAX;
     if (use_w) {
         p.wsrc = wsm;

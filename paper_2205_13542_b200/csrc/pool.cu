@@ -373,11 +373,11 @@ int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_
     BVP_REQUIRE(C == 0 || (features && feats_nhwc && out), BVP_ERR_INVALID,
                 "null pointer argument");
     if (C == 0) return BVP_OK;
-    // fast mode with a chunk schedule: the staging alone, then the reduction
-    // zeroes the empty cells beside its kernels (one graph: 71.7-73.7 us
-    // against 75.8-78.5 us with the full memset beside the transpose,
-    // scripts/time_zero.py); exact mode: the memset beside the transpose
-    const bool zero_beside = !exact && cell_first && schedule && schedule->work;
+    // fast mode with a chunk schedule, under graph capture: the staging
+    // alone, then the reduction zeroes the empty cells beside its kernels
+    // (zero_empty_beside); otherwise the memset beside the transpose
+    const bool zero_beside = !exact && cell_first && schedule && schedule->work &&
+                             zero_empty_beside(as_stream(stream));
     const int rc = bvp_pool_prepare_f32(features, B, N, C, H, W, feats_nhwc,
                                         zero_beside ? nullptr : out, int64_t(nx) * ny, stream);
     if (rc != BVP_OK) return rc;

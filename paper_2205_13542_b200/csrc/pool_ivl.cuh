@@ -30,6 +30,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "pool_group.cuh"
@@ -352,10 +353,12 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
     p.partial_arg = arg && !EXACT ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
                                                                  size_t(B) * p0.chunk_partials * p0.C)
                                   : nullptr;
-    // fast mode: the empty cells' zero fill runs beside the kernels (forked
-    // stream, joined after the combine); exact mode keeps the up-front memset
-    // (its fp64 chunk kernel leaves no registers for a co-resident block)
-    const bool zero_beside = !p.out_zeroed && !EXACT && p.cell_first;
+    // fast mode under graph capture: the empty cells' zero fill runs beside
+    // the kernels (forked stream, joined after the combine); eager launches
+    // and exact mode (its fp64 chunk kernel leaves no registers for a
+    // co-resident block) keep the up-front memset
+    const bool zero_beside = !p.out_zeroed && !EXACT && p.cell_first &&
+                             zero_empty_beside(s);
     if (!p.out_zeroed && !zero_beside)
         cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
     SideFork zfork(s, zero_beside ? 1 : -1);  // -1: inline, no events

@@ -599,8 +599,9 @@ def test_exact_mode_channel_sweep(C, red):
 
 @pytest.mark.parametrize("name", ["T", "S"])
 def test_empty_cells_zeroed_beside_reduction(name):
-    """PoolPlan.run zeroes only the empty cells, beside the chunk kernel
-    (bvp_zero_empty_cells on a forked stream): a NaN-poisoned map comes out
+    """PoolPlan.run replayed from a graph zeroes only the empty cells, beside
+    the chunk kernel (bvp_zero_empty_cells on a forked stream); launched
+    eagerly it memsets the map first.  Either way a NaN-poisoned map comes out
     equal to the oracle for every reducer, batch 2 included; the bare entry
     point zeroes exactly the cells no interval covers."""
     spec = bp.CONFIGS[name]
@@ -613,12 +614,15 @@ def test_empty_cells_zeroed_beside_reduction(name):
     for red in bp.Reducer:
         plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
                            f.depth_bins, 2, red)
-        plan.out.fill_(float("nan"))
-        got = plan.run(feats, dist).cpu().numpy()
-        for b, fb in enumerate((feats_np, -feats_np)):
-            want = o.pool_interval(fb, dist_np, cache.ranks, cache.interval_starts,
-                                   cache.interval_cells, grid.n_cells, red.value)
-            assert max_rel_dev(want, got[b].reshape(want.shape)) <= FP32_TOL, (red, b)
+        g = plan.graphed(plan.run, feats, dist)  # captured: zero fill beside the kernels
+        for run in (lambda: plan.run(feats, dist), g.replay):  # eager: memset first
+            plan.out.fill_(float("nan"))
+            run()
+            got = plan.out.cpu().numpy()
+            for b, fb in enumerate((feats_np, -feats_np)):
+                want = o.pool_interval(fb, dist_np, cache.ranks, cache.interval_starts,
+                                       cache.interval_cells, grid.n_cells, red.value)
+                assert max_rel_dev(want, got[b].reshape(want.shape)) <= FP32_TOL, (red, b)
     out = torch.full((2, spec.channels, grid.n_cells), float("nan"), device="cuda")
     bp._lib.call("bvp_zero_empty_cells", cache.d_cell_first.data_ptr(), grid.n_cells,
                  spec.channels, 2, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
