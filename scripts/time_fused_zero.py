@@ -32,8 +32,29 @@ if len(sys.argv) > 1:
         if i >= 3:
             ts.append(a.elapsed_time(b) * 1e3)
     out = torch.as_tensor(out.values if hasattr(out, "values") else out)
-    print(f"BVP_FUSED_ZERO={os.environ.get('BVP_FUSED_ZERO', '0')}: "
-          f"{statistics.median(ts):6.1f} us  same={bool(torch.equal(out, ref))}")
+    # graph-replayed
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        bp.pool_fused(lg, cx, cache, grid)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        gout = bp.pool_fused(lg, cx, cache, grid)
+    tg = []
+    for i in range(43):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        if i >= 3:
+            tg.append(a.elapsed_time(b) * 1e3)
+    gout = torch.as_tensor(gout.values if hasattr(gout, "values") else gout)
+    print(f"BVP_FUSED_ZERO={os.environ.get('BVP_FUSED_ZERO', '0')}: eager "
+          f"{statistics.median(ts):6.1f} us  graph {statistics.median(tg):6.1f} us  "
+          f"same={bool(torch.equal(out, ref))} graph_same={bool(torch.equal(gout, ref))}")
     torch.save(out.cpu(), f"/tmp/fz{os.environ.get('BVP_FUSED_ZERO', '0')}.pt")
 else:
     for z in ("0", "1", "0", "1"):
