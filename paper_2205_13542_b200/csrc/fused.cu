@@ -187,8 +187,11 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     static const int wmode = [] { const char *e = getenv("BVP_FUSED_W"); return e ? atoi(e) : 1; }();
     float *wsm = reinterpret_cast<float *>(ws + L.off_w);
     const bool use_w = wmode && C % 8 == 0;  // the weight-gather kernel needs 16-byte chunks
-    // BVP_FUSED_ZERO=1: no memset branch; the reduction zeroes the empty cells
-    // beside its kernels (as the fp32 fast path does)
+    // BVP_FUSED_ZERO=1 (measurement only): no memset branch; the reduction
+    // zeroes the empty cells beside its kernels, as the captured fp32 path
+    // does.  Slower here (80 / 94 us eager / captured against 76 / 78 us,
+    // scripts/time_fused_zero.py): the bf16 chunk kernel's four blocks per SM
+    // leave no registers for the zero-fill block.
     static const int zmode = [] { const char *e = getenv("BVP_FUSED_ZERO"); return e ? atoi(e) : 0; }();
     const bool zero_beside = zmode && schedule->work;
     // three independent prologue branches (forked streams): the depth
