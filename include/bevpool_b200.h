@@ -57,7 +57,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BVP_ABI_VERSION 5
+#define BVP_ABI_VERSION 6
 
 #define BVP_OK 0
 #define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
@@ -73,6 +73,11 @@ extern "C" {
 /* or-ed into mode of bvp_pool_forward_nhwc_f32: `out` was zero-filled by
  * bvp_pool_prepare_f32 since it was last written, so the zero fill is skipped */
 #define BVP_OUT_ZEROED 0x100
+/* or-ed into mode of bvp_tile_pool_*: launch only the tile reduction (phase 1,
+ * segment rows) or only the per-cell combine into the map (phase 2); for
+ * per-kernel timing.  Neither flag: both, in order. */
+#define BVP_TILE_PHASE1 0x200
+#define BVP_TILE_PHASE2 0x400
 
 /* Work schedule of the interval kernels (device pointers; built once per
  * cache by bvp_make_schedule).
@@ -352,6 +357,58 @@ int bvp_pool_lifted_backward_f32(const float *grad_out,
                                  int64_t n_int_max, int mode, float *grad_x,
                                  void *workspace, size_t workspace_bytes,
                                  void *stream);
+
+/* ---- pixel-column tiled pooling (the fast SUM / MEAN path) -------------- */
+
+/* Plan of the tiled reduction (csrc/tile.cu), built on the device from
+ * cell_of_point alone.  A tile is one camera column segment (n, w, up to 64
+ * rows); its points are grouped by cell ("segments", 8 per group).  All
+ * arrays live in one caller-allocated buffer `base` of bvp_tile_plan_bytes();
+ * bvp_tile_plan_init fills the struct, bvp_build_tile_plan the buffer.
+ *   n_seg           device int64: number of segments ((tile, cell) pairs),
+ *                   -1 if a tile overflowed the record encoding
+ *   cell_seg_first  device uint32[n_cells + 1]: first segment row of a cell
+ *   cell_points     device uint32[n_cells]: in-range points per cell
+ *   max_seg         host bound on n_seg: rows of the segment-row scratch */
+typedef struct bvp_tile_plan {
+    int N, H, W, D;
+    int64_t n_cells;
+    void *base;
+    size_t bytes;
+    int64_t max_seg;
+    int tile_rows;
+    int64_t n_tiles;
+    const int64_t *n_seg;
+    const uint32_t *cell_seg_first;
+    const uint32_t *cell_points;
+} bvp_tile_plan;
+
+/* 1 when the tiled path takes this frustum / grid (D <= 8192, ...). */
+int bvp_tile_plan_supported(int N, int H, int W, int D, int64_t n_cells);
+size_t bvp_tile_plan_bytes(int N, int H, int W, int D, int64_t n_cells);
+size_t bvp_tile_plan_workspace_bytes(int N, int H, int W, int D, int64_t n_cells);
+int bvp_tile_plan_init(bvp_tile_plan *plan, int N, int H, int W, int D, int64_t n_cells,
+                       void *base, size_t bytes, int64_t max_seg);
+/* cell_of_point[N*H*W*D] (bevgrid.py:85-98's output) -> the plan; stream
+ * ordered, no host sync.  Deterministic. */
+int bvp_build_tile_plan(const uint32_t *cell_of_point, bvp_tile_plan *plan,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* pool_interval SUM / MEAN (pooling.py:206-221) through the plan: features
+ * (B,N,C,H,W) f32, dist (B,N,D,H,W) f32 -> out (B,C,n_cells) f32, every
+ * element written (empty cells 0).  fp32 accumulation (<= ~1e-6 relative of
+ * the reference's fp64).  rows: scratch of B * max_seg * C floats.  C <= 128. */
+int bvp_tile_pool_f32(const float *features, const float *dist, const bvp_tile_plan *plan,
+                      int B, int C, int mode, float *rows, size_t rows_bytes, float *out,
+                      void *stream);
+
+/* Fused lift + pool (config F): logits (B,N,D,H,W) bf16 and context
+ * (B,N,C,H,W) bf16 -> out (B,C,n_cells) f32 = pool(softmax_D(logits) (x)
+ * context); the depth softmax of a tile's pixels is formed in shared memory
+ * (fp32), nothing else is materialised. */
+int bvp_tile_pool_fused_bf16(const uint16_t *logits, const uint16_t *context,
+                             const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
+                             size_t rows_bytes, float *out, void *stream);
 
 /* ---- the paper's "before": LSS prefix-sum pooling --------- */
 

@@ -19,7 +19,9 @@ BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
 TILE_CELLS = 32
 OUT_OF_RANGE = 0xFFFFFFFF
 BVP_OUT_ZEROED = 0x100  # include/bevpool_b200.h
-ABI_VERSION = 5
+BVP_TILE_PHASE1 = 0x200
+BVP_TILE_PHASE2 = 0x400
+ABI_VERSION = 6
 
 
 _P = ctypes.c_void_p
@@ -39,6 +41,16 @@ class Schedule(ctypes.Structure):
 
 
 _SP = ctypes.POINTER(Schedule)
+
+
+class TilePlanStruct(ctypes.Structure):
+    """struct bvp_tile_plan (include/bevpool_b200.h)."""
+    _fields_ = [("N", _I), ("H", _I), ("W", _I), ("D", _I), ("n_cells", _L), ("base", _P),
+                ("bytes", _S), ("max_seg", _L), ("tile_rows", _I), ("n_tiles", _L),
+                ("n_seg", _P), ("cell_seg_first", _P), ("cell_points", _P)]
+
+
+_TP = ctypes.POINTER(TilePlanStruct)
 
 #: name -> (restype, argtypes); mirrors include/bevpool_b200.h one to one
 SIGNATURES = {
@@ -85,6 +97,13 @@ SIGNATURES = {
     "bvp_lidar_workspace_bytes": (_S, [_L, _I, _I]),
     "bvp_lidar_to_bev": (_I, [_P, _L, _P, _I, _I, _I, _P, _P, _S, _P]),
     "bvp_grid_resample_f32": (_I, [_P, _I, _P, _I, _I, _P, _I, _I, _P, _P]),
+    "bvp_tile_plan_supported": (_I, [_I, _I, _I, _I, _L]),
+    "bvp_tile_plan_bytes": (_S, [_I, _I, _I, _I, _L]),
+    "bvp_tile_plan_workspace_bytes": (_S, [_I, _I, _I, _I, _L]),
+    "bvp_tile_plan_init": (_I, [_TP, _I, _I, _I, _I, _L, _P, _S, _L]),
+    "bvp_build_tile_plan": (_I, [_P, _TP, _P, _S, _P]),
+    "bvp_tile_pool_f32": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
+    "bvp_tile_pool_fused_bf16": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
     "bvp_prefixsum_workspace_bytes": (_S, [_L, _I]),
     "bvp_pool_prefixsum_f32": (_I, [_P, _P, _P, _P, _P, _L, _L, _I, _I, _I, _I, _I, _L, _I, _P,
                                     _P, _S, _P]),

@@ -20,6 +20,7 @@ on first access.
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import os
 import struct
@@ -151,6 +152,83 @@ def work_bounds(n_points: int, n_int_max: int, chunk: int) -> tuple[int, int, in
     their partial slots <= 2 n_in / chunk."""
     return (n_int_max + n_points // chunk + 1, n_points // (chunk + 1) + 1,
             2 * n_points // chunk + 1)
+
+
+class TilePlan:
+    """Device plan of the pixel-column tiled reduction (csrc/tile.cu): the
+    in-range points of every camera column tile grouped by cell, built on the
+    GPU from cell_of_point (no host round trip).  ``exact_count``: read the
+    segment count back once (one sync) and size the segment-row scratch to
+    it; otherwise the scratch is sized for the worst case (one segment per
+    point), which per-frame rebuilds use."""
+
+    def __init__(self, N: int, H: int, W: int, D: int, n_cells: int, device):
+        lib = _lib.load()
+        self.dims = (N, H, W, D)
+        self.n_cells = n_cells
+        self.device = device
+        nbytes = int(lib.bvp_tile_plan_bytes(N, H, W, D, n_cells))
+        if nbytes == 0:
+            raise ConfigurationError(f"frustum {self.dims} not supported by the tile plan")
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.ws = torch.empty(int(lib.bvp_tile_plan_workspace_bytes(N, H, W, D, n_cells)),
+                              dtype=torch.uint8, device=device)
+        self.st = _lib.TilePlanStruct()
+        self.bound = N * H * W * D
+        _lib.call("bvp_tile_plan_init", ctypes.byref(self.st), N, H, W, D, n_cells,
+                  ptr(self.buf), nbytes, self.bound)
+        self._rows = {}
+
+    @staticmethod
+    def supported(N: int, H: int, W: int, D: int, n_cells: int) -> bool:
+        return bool(_lib.load().bvp_tile_plan_supported(N, H, W, D, n_cells))
+
+    def build(self, cell_of_point: torch.Tensor, exact_count: bool = False) -> "TilePlan":
+        _lib.call("bvp_build_tile_plan", ptr(cell_of_point), ctypes.byref(self.st), ptr(self.ws),
+                  self.ws.numel(), stream_ptr(self.device))
+        if exact_count:
+            self.fit()
+        return self
+
+    @property
+    def max_seg(self) -> int:
+        return int(self.st.max_seg)
+
+    @property
+    def n_seg(self) -> int:
+        """Segment count of the last build (one host sync)."""
+        off = self.st.n_seg - self.buf.data_ptr()
+        n = int(self.buf[off:off + 8].view(torch.int64).item())
+        if n < 0:
+            raise ConfigurationError("tile plan overflow (a tile's weight window is too large)")
+        return n
+
+    def fit(self) -> "TilePlan":
+        """Shrink the segment-row scratch to the built plan (one sync)."""
+        self.st.max_seg = max(1, self.n_seg)
+        self._rows.clear()
+        return self
+
+    def rows(self, B: int, C: int) -> torch.Tensor:
+        """Segment-row scratch for B samples of C channels (kept per shape)."""
+        key = (B, C)
+        t = self._rows.get(key)
+        if t is None:
+            t = torch.empty(B * self.max_seg * max(C, 1), dtype=torch.float32, device=self.device)
+            self._rows[key] = t
+        return t
+
+    def pool_f32(self, features: torch.Tensor, dist: torch.Tensor, B: int, C: int, mode: int,
+                 out: torch.Tensor) -> None:
+        rows = self.rows(B, C)
+        _lib.call("bvp_tile_pool_f32", ptr(features), ptr(dist), ctypes.byref(self.st), B, C,
+                  mode, ptr(rows), 4 * rows.numel(), ptr(out), stream_ptr(self.device))
+
+    def pool_fused_bf16(self, logits: torch.Tensor, context: torch.Tensor, B: int, C: int,
+                        mode: int, out: torch.Tensor) -> None:
+        rows = self.rows(B, C)
+        _lib.call("bvp_tile_pool_fused_bf16", ptr(logits), ptr(context), ctypes.byref(self.st),
+                  B, C, mode, ptr(rows), 4 * rows.numel(), ptr(out), stream_ptr(self.device))
 
 
 @dataclass(eq=False)
@@ -287,6 +365,19 @@ class AssociationCache:
                                   *work)
             self._host[key] = s
         return s
+
+    def tile_plan(self, N: int, H: int, W: int, D: int) -> "TilePlan | None":
+        """The tiled reduction's plan for an (N, H, W, D) frustum (built on
+        first use, one sync to size its scratch); None when the frustum is
+        outside the tiled path's limits."""
+        key = ("tile", N, H, W, D)
+        if key not in self._host:
+            plan = None
+            if TilePlan.supported(N, H, W, D, self.n_cells) and self.n_points == N * H * W * D:
+                plan = TilePlan(N, H, W, D, self.n_cells, self.device).build(
+                    self.d_cell_of_point, exact_count=True)
+            self._host[key] = plan
+        return self._host[key]
 
     def exact_work(self) -> dict:
         """The exact mode's chunk list: intervals of <= EXACT_CHUNK points as
@@ -469,6 +560,9 @@ class CacheBuilder:
         self.defer_units = not sort_work
         self._grid_arr = grid.as_array()
         self._one_call = self.defer_units and CHUNK > 0
+        self.dims = (n_cameras, frustum.height, frustum.width, frustum.depth_bins)
+        self.tplan = (TilePlan(*self.dims, grid.n_cells, self.dev)
+                      if TilePlan.supported(*self.dims, grid.n_cells) else None)
         if self._one_call:
             b = self.bufs
             n = int(_lib.load().bvp_work_workspace_bytes(b["n_int_max"], self.P, CHUNK, grid.nx,
@@ -493,7 +587,7 @@ class CacheBuilder:
                                      defer_units=True, work_done=True)
             cache = _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
             cache._units_pending = pending
-            return cache
+            return self._with_tiles(cache)
         _lib.call("bvp_build_cache", ptr(cams), self.n_cameras, f.height, f.width, f.depth_bins,
                   f.depth_min, f.depth_step, self._grid_arr.ctypes.data, g.nx, g.ny,
                   ptr(b["cells"]), ptr(b["ranks"]), ptr(b["starts"]), ptr(b["icells"]),
@@ -503,6 +597,14 @@ class CacheBuilder:
                                  work_tile=self.work_tile, defer_units=self.defer_units)
         cache = _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
         cache._units_pending = pending
+        return self._with_tiles(cache)
+
+    def _with_tiles(self, cache: AssociationCache) -> AssociationCache:
+        """Rebuild the tiled reduction's plan from this frame's cells (stream
+        ordered, no sync; scratch sized for the worst case) and attach it."""
+        if self.tplan is not None:
+            self.tplan.build(self.bufs["cells"])
+        cache._host[("tile", *self.dims)] = self.tplan
         return cache
 
 
@@ -519,6 +621,8 @@ def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
     cache = builder.build(cams_d, fingerprint_inputs(rig, frustum_spec, grid_spec))
     cache._counts()  # one sync: sizes known on the host from here on
     cache.fit_launch()
+    if builder.tplan is not None:
+        builder.tplan.fit()
     return cache
 
 

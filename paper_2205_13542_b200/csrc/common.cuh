@@ -98,6 +98,20 @@ __device__ __forceinline__ void st_stream_f4(float *p, float4 v) {
                  : "memory");
 }
 
+// Read-only loads that ask L2 to fetch the surrounding 256 bytes: strided
+// gathers of neighbouring columns by different CTAs then hit L2 instead of
+// each pulling its own 32-byte sector from DRAM.
+__device__ __forceinline__ float ldg_l2pf(const float *p) {
+    float r;
+    asm volatile("ld.global.nc.L2::256B.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint16_t ldg_l2pf(const uint16_t *p) {
+    uint16_t r;
+    asm volatile("ld.global.nc.L2::256B.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    return r;
+}
+
 __device__ __forceinline__ float bf16_to_f32(uint16_t v) {
     return __uint_as_float(static_cast<uint32_t>(v) << 16);
 }

@@ -1,0 +1,920 @@
+// tile.cu -- pixel-column tiled BEV pooling (SUM / MEAN, fp32 accumulate).
+//
+// The reference reduces interval by interval: every in-range point of a
+// cell gathers its pixel's feature row (_kernels.py:34-55).  A pixel's row is
+// used by every depth bin of its ray (~103 points at the nuScenes shape), so
+// the interval formulation re-reads each 320-byte row ~100 times from L2.
+// Here the work is tiled by PIXELS instead of by cells:
+//
+//   tile t = one camera column segment (n, w, rows h0..h0+TH): its TH feature
+//   rows are staged in shared memory ONCE; every point of the tile is one
+//   (h, d) of those rows.  Within the tile the points are sorted by cell
+//   (then h, d); a run of equal cells is a "segment".  8 consecutive
+//   segments form a group, and a group is a small dense product
+//
+//       seg_row[k, c] = sum_{h in union(g)} A[k, h] * F[h, c],   k < 8
+//       A[k, h]       = sum_{d : cell(h, d) = cell_k} w[h, d]
+//
+//   (the union is the set of rows any of the 8 cells sees; for a level rig
+//   all rows of a column hit the same cells, so A is ~97% dense at S).
+//   One warp computes a group with lanes over channels, 8 x ceil(C/32)
+//   accumulators per lane, the row of F read once per (group, h) for all 8
+//   cells.
+//
+// Phase 1 (tile_pool_kernel, one CTA per (tile, sample)) writes one 4C-byte
+// row per segment; phase 2 (tile_finalize_kernel, one CTA per 32 cells)
+// sums each cell's segment rows in tile order (~22% of cells at S see more
+// than one tile), applies MEAN's 1/len, transposes through shared memory and
+// writes the channel-major map (C, n_cells) with full 128-byte lines -- every
+// element exactly once, empty cells as zeros (pooling.py:213).  No atomics
+// touch values: the result is deterministic and independent of launch shape.
+//
+// The plan (tile_plan_kernel and friends) is built once per association
+// from cell_of_point alone (bevgrid.py:85-98's output), on the GPU.
+//
+// Reference: pooling.py:206-221 (pool_interval), _kernels.py:22-63
+// (interval_reduce), bevgrid.py:142-158 (the association it consumes).
+#include <algorithm>
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace bvp {
+
+constexpr int kTileGroup = 8;         // segments (cells) per group
+constexpr int kTileMaxRows = 64;      // rows per tile (one u64 mask per group)
+constexpr int kTileMaxPoints = 8192;  // points per tile (smem sort capacity)
+constexpr int kPlanThreads = 512;
+constexpr int kPoolThreads = 256;
+constexpr int kFinCells = 32;         // cells per finalize CTA
+
+struct TileGeom {
+    int N, H, W, D, TH, n_hb;
+    int64_t T, tpc, gcap;
+    int hl_bits, d_bits;
+};
+
+inline int bits_for(int64_t v) {  // bits to hold values in [0, v]
+    int b = 0;
+    while (b < 62 && (int64_t(1) << b) <= v) ++b;
+    return b;
+}
+
+inline int tile_rows_for(int H, int D) {
+    int th = std::min(H, kTileMaxRows);
+    th = std::min(th, std::max(1, kTileMaxPoints / std::max(D, 1)));
+    return th;
+}
+
+inline TileGeom tile_geom(int N, int H, int W, int D) {
+    TileGeom g{};
+    g.N = N; g.H = H; g.W = W; g.D = D;
+    g.TH = tile_rows_for(H, D);
+    g.n_hb = int((H + g.TH - 1) / g.TH);
+    g.T = int64_t(N) * g.n_hb * W;
+    g.tpc = int64_t(g.TH) * D;
+    g.gcap = (g.tpc + kTileGroup - 1) / kTileGroup + 1;  // + sentinel
+    g.hl_bits = bits_for(g.TH - 1);
+    g.d_bits = bits_for(D - 1);
+    return g;
+}
+
+// tile index t = (n * n_hb + hb) * W + w: neighbouring columns are
+// neighbouring tiles, so concurrently running CTAs share the 32-byte sectors
+// of the strided (N, C, H, W) / (N, D, H, W) inputs through L2.
+struct TileId {
+    int n, hb, w, h0, th;
+};
+__device__ __forceinline__ TileId tile_id(int64_t t64, int W, int n_hb, int TH, int H) {
+    TileId r;
+    const int t = int(t64);  // T < 2^31 (plan_supported)
+    r.w = t % W;
+    const int rest = t / W;
+    r.hb = rest % n_hb;
+    r.n = rest / n_hb;
+    r.h0 = r.hb * TH;
+    r.th = min(TH, H - r.h0);
+    return r;
+}
+
+// ---- block helpers ---------------------------------------------------------
+// Exclusive scan of one value per thread across the block (blockDim.x <= 1024).
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp,
+                                                    uint32_t *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t y = lane < nw ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
+            if (lane >= o) y += z;
+        }
+        if (lane < nw) s_warp[lane] = y;  // inclusive warp totals
+    }
+    __syncthreads();
+    const uint32_t pre = warp ? s_warp[warp - 1] : 0u;
+    if (total) *total = s_warp[nw - 1];
+    __syncthreads();
+    return pre + x - v;
+}
+
+// ---- plan build -------------------------------------------------------------
+// One CTA per tile.  Keys (cell << 16 | hl << d_bits | d), sorted ascending
+// in shared memory (bitonic); the low bits order the points of a cell by
+// (h, d), which is their rank order within the tile (bevgrid.py:149's stable
+// tie-break restricted to one column).
+__global__ void __launch_bounds__(kPlanThreads)
+tile_plan_kernel(const uint32_t *__restrict__ cells, TileGeom g, uint4 *__restrict__ hdr,
+                 uint32_t *__restrict__ rec, uint32_t *__restrict__ seg_cell,
+                 uint32_t *__restrict__ seg_start, uint4 *__restrict__ groups,
+                 int *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long *keys = reinterpret_cast<unsigned long long *>(smem);
+    __shared__ unsigned long long gmask[kTileMaxPoints / kTileGroup + 1];
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_tot[2];
+
+    const int64_t t = blockIdx.x;
+    const TileId id = tile_id(t, g.W, g.n_hb, g.TH, g.H);
+    const int np_all = id.th * g.D;
+    int cap = 1;
+    while (cap < np_all) cap <<= 1;
+    const uint32_t *cbase = cells + ((int64_t(id.n) * g.H + id.h0) * g.W + id.w) * g.D;
+    const int64_t hstride = int64_t(g.W) * g.D;
+    uint32_t nvalid = 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int hl = warp; hl < id.th; hl += nw)
+        for (int d = lane; d < g.D; d += 32) {
+            const uint32_t c = __ldg(cbase + hl * hstride + d);
+            unsigned long long k = ~0ull;
+            if (c != kOOR) {
+                k = (static_cast<unsigned long long>(c) << 16) |
+                    static_cast<unsigned>((hl << g.d_bits) | d);
+                ++nvalid;
+            }
+            keys[hl * g.D + d] = k;
+        }
+    for (int i = np_all + threadIdx.x; i < cap; i += blockDim.x) keys[i] = ~0ull;
+    for (int i = threadIdx.x; i < kTileMaxPoints / kTileGroup + 1; i += blockDim.x) gmask[i] = 0;
+    block_excl_scan(nvalid, s_warp, &s_tot[0]);
+    const int n_pts = int(s_tot[0]);
+    const int hmask = (1 << g.hl_bits) - 1, dmask = (1 << g.d_bits) - 1;
+    // bitonic sort of keys[0, cap)
+    for (int k = 2; k <= cap; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < (cap >> 1); i += blockDim.x) {
+                const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
+                const unsigned long long a = keys[lo], b = keys[hi];
+                const bool up = (lo & k) == 0;
+                if ((a > b) == up) {
+                    keys[lo] = b;
+                    keys[hi] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // segments: thread owns the contiguous points [k0, k1)
+    const int per = (n_pts + blockDim.x - 1) / blockDim.x;
+    const int k0 = min(n_pts, int(threadIdx.x) * per), k1 = min(n_pts, k0 + per);
+    uint32_t heads = 0;
+    for (int k = k0; k < k1; ++k)
+        heads += (k == 0 || (keys[k] >> 16) != (keys[k - 1] >> 16)) ? 1u : 0u;
+    uint32_t seg = block_excl_scan(heads, s_warp, &s_tot[1]);
+    const int n_segs = int(s_tot[1]);
+    const int n_groups = (n_segs + kTileGroup - 1) / kTileGroup;
+    // union masks of the groups
+    {
+        uint32_t sg = seg;
+        for (int k = k0; k < k1; ++k) {
+            const bool head = (k == 0 || (keys[k] >> 16) != (keys[k - 1] >> 16));
+            if (head) ++sg;
+            const int hl = int(keys[k] >> g.d_bits) & hmask;
+            atomicOr(&gmask[(sg - 1) / kTileGroup], 1ull << hl);
+        }
+    }
+    __syncthreads();
+    // group offsets into the weight window: 8 floats per union row
+    __shared__ uint32_t s_woff[kTileMaxPoints / kTileGroup + 1];
+    {
+        const int gper = (n_groups + blockDim.x - 1) / blockDim.x;
+        const int g0 = min(n_groups, int(threadIdx.x) * gper), g1 = min(n_groups, g0 + gper);
+        uint32_t sum = 0;
+        for (int q = g0; q < g1; ++q) sum += kTileGroup * __popcll(gmask[q]);
+        uint32_t off = block_excl_scan(sum, s_warp, &s_tot[0]);
+        for (int q = g0; q < g1; ++q) {
+            s_woff[q] = off;
+            off += kTileGroup * __popcll(gmask[q]);
+        }
+    }
+    __syncthreads();
+    const uint32_t total_w = s_tot[0];
+    const int shift = g.hl_bits + g.d_bits;
+    const uint32_t wmax = 1u << (31 - shift);
+    if (threadIdx.x == 0 && total_w > wmax) atomicExch(err, 1);
+    uint4 *gt = groups + t * g.gcap;
+    uint32_t *rt = rec + t * g.tpc;
+    uint32_t *sc = seg_cell + t * g.tpc;
+    uint32_t *sn = seg_start + t * g.tpc;
+    {
+        uint32_t sg = seg;  // segments started before k0
+        for (int k = k0; k < k1; ++k) {
+            const uint32_t c = uint32_t(keys[k] >> 16);
+            const bool head = (k == 0 || c != uint32_t(keys[k - 1] >> 16));
+            if (head) ++sg;
+            const uint32_t s = sg - 1;
+            const int hl = int(keys[k] >> g.d_bits) & hmask, d = int(keys[k]) & dmask;
+            const int q = int(s / kTileGroup), kk = int(s % kTileGroup);
+            const int prev_hl = k > 0 ? int(keys[k - 1] >> g.d_bits) & hmask : -1;
+            const bool run_head = head || hl != prev_hl;
+            const unsigned long long m = gmask[q];
+            const uint32_t upos = __popcll(m & ((1ull << hl) - 1ull));
+            const uint32_t widx = s_woff[q] + upos * kTileGroup + kk;
+            rt[k] = (run_head ? 0x80000000u : 0u) | ((widx & (wmax - 1)) << shift) |
+                    (uint32_t(hl) << g.d_bits) | uint32_t(d);
+            if (head) {
+                sc[s] = c;
+                sn[s] = uint32_t(k);  // first point of the segment
+                if (kk == 0)
+                    gt[q] = make_uint4(uint32_t(m), uint32_t(m >> 32), s_woff[q], uint32_t(k));
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        gt[n_groups] = make_uint4(0u, 0u, total_w, uint32_t(n_pts));
+        hdr[t] = make_uint4(uint32_t(n_pts), uint32_t(n_segs), uint32_t(n_groups), total_w);
+    }
+}
+
+// Segments per cell (and in-range points per cell, for MEAN).
+__global__ void tile_seg_count_kernel(const uint4 *__restrict__ hdr, TileGeom g,
+                                      const uint32_t *__restrict__ seg_cell,
+                                      const uint32_t *__restrict__ seg_start,
+                                      uint32_t *__restrict__ cell_nseg,
+                                      uint32_t *__restrict__ cell_npts) {
+    const int64_t t = blockIdx.x;
+    const int n_segs = int(hdr[t].y);
+    for (int s = threadIdx.x; s < n_segs; s += blockDim.x) {
+        const uint32_t c = seg_cell[t * g.tpc + s];
+        const uint32_t first = seg_start[t * g.tpc + s];
+        const uint32_t end = s + 1 < n_segs ? seg_start[t * g.tpc + s + 1] : hdr[t].x;
+        atomicAdd(&cell_nseg[c], 1u);
+        atomicAdd(&cell_npts[c], end - first);
+    }
+}
+
+// Slots in arrival order; tile_seg_fix_kernel reorders them by tile.
+__global__ void tile_seg_assign_kernel(const uint4 *__restrict__ hdr, TileGeom g,
+                                       const uint32_t *__restrict__ seg_cell,
+                                       const uint32_t *__restrict__ cell_seg_first,
+                                       uint32_t *__restrict__ cell_fill,
+                                       unsigned long long *__restrict__ owner) {
+    const int64_t t = blockIdx.x;
+    const int n_segs = int(hdr[t].y);
+    for (int s = threadIdx.x; s < n_segs; s += blockDim.x) {
+        const uint32_t c = seg_cell[t * g.tpc + s];
+        const uint32_t slot = atomicAdd(&cell_fill[c], 1u);
+        owner[cell_seg_first[c] + slot] = (static_cast<unsigned long long>(t) << 32) | uint32_t(s);
+    }
+}
+
+// Per cell: order its segments by tile (deterministic), record each
+// segment's row index.
+__global__ void tile_seg_fix_kernel(const uint32_t *__restrict__ cell_seg_first, int64_t n_cells,
+                                    TileGeom g, unsigned long long *__restrict__ owner,
+                                    uint32_t *__restrict__ seg_row) {
+    for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < n_cells;
+         c += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t s0 = cell_seg_first[c], s1 = cell_seg_first[c + 1];
+        if (s1 - s0 > 1) {  // insertion sort (a few entries)
+            for (uint32_t a = s0 + 1; a < s1; ++a) {
+                const unsigned long long v = owner[a];
+                uint32_t b = a;
+                while (b > s0 && owner[b - 1] > v) {
+                    owner[b] = owner[b - 1];
+                    --b;
+                }
+                owner[b] = v;
+            }
+        }
+        for (uint32_t a = s0; a < s1; ++a) {
+            const unsigned long long v = owner[a];
+            seg_row[int64_t(v >> 32) * g.tpc + uint32_t(v)] = a;
+        }
+    }
+}
+
+// ---- phase 1: tile reduction -------------------------------------------------
+enum TileSrc { kTileF32 = 0, kTileBF16Fused = 1 };
+
+struct TilePoolArgs {
+    const void *feats;       // (B, N, C, H, W) f32 | bf16
+    const void *weights;     // dist (B, N, D, H, W) f32 | logits bf16
+    const uint4 *hdr;
+    const uint32_t *rec;
+    const uint4 *groups;
+    const uint32_t *seg_row;
+    float *rows;             // (B, max_seg, C)
+    int64_t max_seg;
+    TileGeom g;
+    int C, wbudget;
+    int dbg;  // ablation (profiling builds): 1 stop after staging, 2 after aggregation
+};
+
+// acc.x += w.x * f, acc.y += w.y * f in one FFMA2 (Blackwell packed fp32;
+// the scalar f is a broadcast operand, no move).
+__device__ __forceinline__ void ffma2(float2 &acc, float2 w, float f) {
+    unsigned long long a = *reinterpret_cast<unsigned long long *>(&acc);
+    const unsigned long long wv = *reinterpret_cast<const unsigned long long *>(&w);
+    unsigned long long fv;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(fv) : "f"(f));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(wv), "l"(fv));
+    acc = *reinterpret_cast<float2 *>(&a);
+}
+
+// One union row of a group: acc[m][j] += (w[2m], w[2m+1]) * F[hl][lane + 32 j].
+template <int CS, int FS>
+__device__ __forceinline__ void group_row(float2 (&acc)[kTileGroup / 2][CS], const float *wq,
+                                          const float *fs, int hl, int lane) {
+    const float4 w0 = *reinterpret_cast<const float4 *>(wq);
+    const float4 w1 = *reinterpret_cast<const float4 *>(wq + 4);
+#pragma unroll
+    for (int j = 0; j < CS; ++j) {
+        const float f = fs[hl * FS + lane + 32 * j];
+        ffma2(acc[0][j], make_float2(w0.x, w0.y), f);
+        ffma2(acc[1][j], make_float2(w0.z, w0.w), f);
+        ffma2(acc[2][j], make_float2(w1.x, w1.y), f);
+        ffma2(acc[3][j], make_float2(w1.z, w1.w), f);
+    }
+}
+
+// Every global load of a tile is independent of the others (the addresses
+// follow from the tile index alone), so a CTA waits about one memory latency
+// per stage: (1) the feature rows F[hl][c] and the depth weights w[hl][d] of
+// the tile's pixels into shared memory -- for the fused variant the logits,
+// soft-maxed in place -- (2) the records, which only index shared memory,
+// aggregate the weights per (cell, row), (3) the group products.
+template <int CS, int SRC, int CL>
+__global__ void __launch_bounds__(kPoolThreads)
+tile_pool_kernel(TilePoolArgs a) {
+    constexpr int CP = CS * 32;
+    constexpr int FS = CP + 4;  // row stride: 16-byte aligned rows of channel quads
+    constexpr int NW = kPoolThreads / 32;
+    extern __shared__ __align__(16) float sm[];
+    const TileGeom &g = a.g;
+    const int64_t t = blockIdx.x;
+    const int b = blockIdx.y;
+    const TileId id = tile_id(t, g.W, g.n_hb, g.TH, g.H);
+    const uint4 h = a.hdr[t];
+    const int n_segs = int(h.y), n_groups = int(h.z);
+    const int HW = g.H * g.W, C = a.C, D = g.D, PD = (D + 3) & ~3;
+    float *ws = sm;                                           // weight window [wbudget]
+    float *fs = ws + a.wbudget;                               // [TH][FS] feature rows
+    float *pw = fs + g.TH * FS;                               // [TH][PD] depth weights
+    const int64_t nb = int64_t(b) * g.N + id.n;
+    const int64_t pix0 = int64_t(id.h0) * g.W + id.w;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // (1) stage: F[hl][c] = features[n, c, h0 + hl, w]; w[hl][d] = dist[n, d, h0 + hl, w].
+    // The CL tiles of a cluster are CL adjacent columns of one camera.  CTA
+    // `rank` loads channel quads (and depth-bin quads) rank, rank + CL, ... for
+    // all CL columns -- a warp's load covers CL neighbouring columns x 32/CL
+    // rows, 32/CL lines instead of 32 -- and stores each quad as one 16-byte
+    // word into the shared memory of the CTA owning its column (distributed
+    // shared memory).  A warp issues the loads of up to U items before their
+    // stores, so it waits about one memory latency per U items.
+    {
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        const int rank = CL > 1 ? int(cluster.block_rank()) : 0;
+        const int j = lane % CL, r0 = lane / CL;
+        constexpr int RS = 32 / CL;  // rows per load instruction
+        constexpr int U = 4;
+        float *rfs = CL > 1 ? cluster.map_shared_rank(fs, j) : fs;
+        float *rpw = CL > 1 ? cluster.map_shared_rank(pw, j) : pw;
+        const int64_t col = pix0 - rank + j;  // (h0, w_base + j)
+        const int n_rb = (id.th + RS - 1) / RS;
+        auto stage = [&](const void *src, int n_ch, int64_t base, float *dst, int stride) {
+            const int n_q = (((n_ch + 3) >> 2) - rank + CL - 1) / CL;  // this CTA's quads
+            const int items = n_q * n_rb;
+            for (int i0 = warp; i0 < items; i0 += NW * U) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int it = i0 + NW * u;
+                    const int qi = it / n_rb, m = it - qi * n_rb;
+                    const int c0 = 4 * (rank + CL * qi), hl = r0 + RS * m;
+                    float x[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (it < items && hl < id.th) {
+                        const int64_t off = base + int64_t(c0) * HW + int64_t(hl) * g.W;
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            if (c0 + e < n_ch) {
+                                if (SRC == kTileF32)
+                                    x[e] = ldg_l2pf(static_cast<const float *>(src) + off + int64_t(e) * HW);
+                                else
+                                    x[e] = bf16_to_f32(ldg_l2pf(static_cast<const uint16_t *>(src) + off + int64_t(e) * HW));
+                            }
+                    }
+                    v[u] = make_float4(x[0], x[1], x[2], x[3]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int it = i0 + NW * u;
+                    const int qi = it / n_rb, m = it - qi * n_rb;
+                    const int c0 = 4 * (rank + CL * qi), hl = r0 + RS * m;
+                    if (it < items && hl < id.th)
+                        *reinterpret_cast<float4 *>(dst + hl * stride + c0) = v[u];
+                }
+            }
+        };
+        stage(a.feats, C, nb * C * HW + col, rfs, FS);
+        stage(a.weights, D, nb * D * HW + col, rpw, PD);
+        // channel quads past C up to CP: zero (no quad holds both)
+        for (int i = threadIdx.x; i < id.th * (CP - ((C + 3) & ~3)); i += kPoolThreads) {
+            const int w4 = CP - ((C + 3) & ~3);
+            fs[(i / w4) * FS + ((C + 3) & ~3) + i % w4] = 0.f;
+        }
+        if (CL > 1)
+            cluster.sync();
+    }
+    if (n_segs == 0 || a.dbg == 1) return;
+    const uint4 *gt = a.groups + t * g.gcap;
+    const uint32_t total_w = __ldg(&gt[n_groups].z);
+    if (SRC == kTileBF16Fused) {
+        __syncthreads();
+        // depth softmax of the tile's pixels (lift.py:17-31 semantics, fp32
+        // from bf16 logits): one warp per pixel, lanes over depth bins
+        for (int hl = warp; hl < id.th; hl += NW) {
+            float *row = pw + hl * PD;
+            float m = -INFINITY;
+            for (int d = lane; d < D; d += 32) m = fmaxf(m, row[d]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+            float sum = 0.f;
+            for (int d = lane; d < D; d += 32) {
+                const float e = expf(row[d] - m);
+                row[d] = e;
+                sum += e;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            const float inv = 1.f / sum;
+            for (int d = lane; d < D; d += 32) row[d] *= inv;
+        }
+    }
+    const uint32_t *rt = a.rec + t * g.tpc;
+    const uint32_t *srow = a.seg_row + t * g.tpc;
+    float *rows = a.rows + int64_t(b) * a.max_seg * C;
+    const int shift = g.hl_bits + g.d_bits;
+    const uint32_t dmask = (1u << g.d_bits) - 1u, hmask = (1u << g.hl_bits) - 1u;
+    const uint32_t wmask = (1u << (31 - shift)) - 1u;
+    for (int q0 = 0; q0 < n_groups;) {
+        // a window of groups whose weights fit the budget (one, for nearly
+        // every tile: then no search)
+        const uint4 G0 = q0 ? gt[q0] : make_uint4(0u, 0u, 0u, 0u);
+        int q1 = n_groups;
+        if (total_w - G0.z > uint32_t(a.wbudget)) {
+            int lo = q0 + 1, hi = n_groups - 1;
+            q1 = q0 + 1;  // one group always fits (8 x TH <= budget)
+            while (lo <= hi) {
+                const int mid = (lo + hi) >> 1;
+                if (gt[mid].z - G0.z <= uint32_t(a.wbudget)) {
+                    q1 = mid;
+                    lo = mid + 1;
+                } else {
+                    hi = mid - 1;
+                }
+            }
+        }
+        const uint32_t r_end = q1 == n_groups ? h.x : gt[q1].w;
+        const uint32_t w_end = q1 == n_groups ? total_w : gt[q1].z;
+        const uint32_t wlen = w_end - G0.z;
+        __syncthreads();  // staging done; previous window consumed
+        for (uint32_t i = threadIdx.x; i < wlen; i += kPoolThreads) ws[i] = 0.f;
+        __syncthreads();
+        // (2) aggregate: each run of one (cell, row) summed in depth order;
+        // a thread's records are loaded U at a time
+        {
+            constexpr int U = 4;
+            for (uint32_t k0 = G0.w + threadIdx.x; k0 < r_end; k0 += kPoolThreads * U) {
+                uint32_t rr[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t k = k0 + kPoolThreads * u;
+                    rr[u] = k < r_end ? __ldg(rt + k) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t k = k0 + kPoolThreads * u;
+                    uint32_t r = rr[u];
+                    if (k >= r_end || !(r >> 31)) continue;
+                    const uint32_t widx = (r >> shift) & wmask;
+                    float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+                    for (uint32_t kk = k + 1; kk < r_end; ++kk) {
+                        r = __ldg(rt + kk);
+                        if (r >> 31) break;
+                        sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+                    }
+                    ws[widx - G0.z] = sum;
+                }
+            }
+        }
+        __syncthreads();
+        if (a.dbg == 2) return;
+        // (3) one warp per group of 8 cells
+        for (int q = q0 + warp; q < q1; q += NW) {
+            const uint4 G = gt[q];
+            const float *wq = ws + (G.z - G0.z);
+            float2 acc[kTileGroup / 2][CS];
+#pragma unroll
+            for (int m = 0; m < kTileGroup / 2; ++m)
+#pragma unroll
+                for (int j = 0; j < CS; ++j) acc[m][j] = make_float2(0.f, 0.f);
+            for (uint32_t m = G.x; m; m &= m - 1, wq += kTileGroup)
+                group_row<CS, FS>(acc, wq, fs, __ffs(m) - 1, lane);
+            for (uint32_t m = G.y; m; m &= m - 1, wq += kTileGroup)
+                group_row<CS, FS>(acc, wq, fs, 31 + __ffs(m), lane);
+            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
+            const uint32_t my_row = lane < nk ? __ldg(srow + q * kTileGroup + lane) : 0u;
+#pragma unroll
+            for (int k = 0; k < kTileGroup; ++k) {
+                const uint32_t row = __shfl_sync(0xFFFFFFFFu, my_row, k);
+                if (k < nk) {
+                    float *dst = rows + int64_t(row) * C;
+#pragma unroll
+                    for (int j = 0; j < CS; ++j) {
+                        const int c = lane + 32 * j;
+                        if (c < C) dst[c] = (k & 1) ? acc[k >> 1][j].y : acc[k >> 1][j].x;
+                    }
+                }
+            }
+        }
+        q0 = q1;
+    }
+}
+
+// ---- phase 2: per-cell combine + transpose into the channel-major map -------
+// Persistent CTAs walk blocks of 32 consecutive cells.  In a block, warp w
+// combines cells w, w+8, w+16, w+24 (lanes over channels; a cell's segment
+// rows are contiguous, the first row of all four cells is loaded before any
+// is summed), then warp w writes channels w, w+8, ... of the 32 cells as full
+// 128-byte lines.  The next block's cell_seg_first entries are loaded while
+// this block's rows are in flight, so a block costs one memory latency.
+template <int CS>
+__global__ void __launch_bounds__(kPoolThreads)
+tile_finalize_kernel(const float *__restrict__ rows, int64_t max_seg,
+                     const uint32_t *__restrict__ cell_seg_first,
+                     const uint32_t *__restrict__ cell_npts, int64_t n_cells, int C, int B,
+                     int mean, float *__restrict__ out) {
+    constexpr int CP = CS * 32;
+    constexpr int NW = kPoolThreads / 32, CPW = kFinCells / NW;
+    __shared__ float tile[kFinCells][CP + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_blk = int((n_cells + kFinCells - 1) / kFinCells), total = n_blk * B;
+    auto load_first = [&](int it, uint32_t &f, uint32_t &f32) {
+        if (it < total) {
+            const int bb = it / n_blk;
+            const int64_t c0 = int64_t(it - bb * n_blk) * kFinCells;
+            const int64_t nc = n_cells - c0 < kFinCells ? n_cells - c0 : int64_t(kFinCells);
+            f = __ldg(cell_seg_first + c0 + (lane < nc ? lane : nc));
+            f32 = __ldg(cell_seg_first + c0 + nc);
+        }
+    };
+    uint32_t first = 0, first32 = 0;
+    load_first(blockIdx.x, first, first32);
+    for (int it = blockIdx.x; it < total; it += gridDim.x) {
+        uint32_t nfirst = 0, nfirst32 = 0;
+        load_first(it + gridDim.x, nfirst, nfirst32);
+        const int b = it / n_blk;
+        const int64_t c0 = int64_t(it - b * n_blk) * kFinCells;
+        const int nc = int(n_cells - c0 < kFinCells ? n_cells - c0 : int64_t(kFinCells));
+        const float *rb = rows + int64_t(b) * max_seg * C;
+        float acc[CPW][CS];
+        uint32_t s0[CPW], s1[CPW];
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+            const int cl = warp + NW * u;
+            s0[u] = __shfl_sync(0xFFFFFFFFu, first, cl);
+            s1[u] = cl + 1 < 32 ? __shfl_sync(0xFFFFFFFFu, first, (cl + 1) & 31) : first32;
+            if (cl >= nc) s1[u] = s0[u];
+#pragma unroll
+            for (int j = 0; j < CS; ++j)
+                acc[u][j] = (s1[u] > s0[u] && lane + 32 * j < C)
+                                ? __ldg(rb + int64_t(s0[u]) * C + lane + 32 * j)
+                                : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+            const int cl = warp + NW * u;
+            for (uint32_t s = s0[u] + 1; s < s1[u]; ++s)
+#pragma unroll
+                for (int j = 0; j < CS; ++j)
+                    if (lane + 32 * j < C) acc[u][j] += __ldg(rb + int64_t(s) * C + lane + 32 * j);
+            if (mean && s1[u] > s0[u]) {
+                const float inv = 1.f / float(__ldg(cell_npts + c0 + cl));
+#pragma unroll
+                for (int j = 0; j < CS; ++j) acc[u][j] *= inv;
+            }
+#pragma unroll
+            for (int j = 0; j < CS; ++j) tile[cl][lane + 32 * j] = acc[u][j];
+        }
+        __syncthreads();
+        float *ob = out + int64_t(b) * C * n_cells + c0 + lane;
+        if (lane < nc)
+            for (int ch = warp; ch < C; ch += NW) ob[int64_t(ch) * n_cells] = tile[lane][ch];
+        __syncthreads();
+        first = nfirst;
+        first32 = nfirst32;
+    }
+}
+
+// ---- plan layout -------------------------------------------------------------
+static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct PlanLayout {
+    size_t hdr, rec, seg_cell, seg_start, seg_row, groups, csf, npts, nseg, bytes;
+};
+static PlanLayout plan_layout(const TileGeom &g, int64_t n_cells) {
+    PlanLayout L{};
+    size_t o = 0;
+    const size_t pts = size_t(g.T) * g.tpc;
+    L.hdr = o; o = a256(o + 16 * size_t(g.T));
+    L.rec = o; o = a256(o + 4 * pts);
+    L.seg_cell = o; o = a256(o + 4 * pts);
+    L.seg_start = o; o = a256(o + 4 * pts);
+    L.seg_row = o; o = a256(o + 4 * pts);
+    L.groups = o; o = a256(o + 16 * size_t(g.T) * g.gcap);
+    L.csf = o; o = a256(o + 4 * size_t(n_cells + 1));
+    L.npts = o; o = a256(o + 4 * size_t(n_cells));
+    L.nseg = o; o = a256(o + 8);
+    L.bytes = o;
+    return L;
+}
+
+struct PlanWs {
+    size_t fill, owner, part, total, err, bytes;
+};
+static PlanWs plan_ws(const TileGeom &g, int64_t n_cells) {
+    PlanWs L{};
+    size_t o = 0;
+    L.fill = o; o = a256(o + 4 * size_t(n_cells + 1));
+    L.owner = o; o = a256(o + 8 * size_t(g.T) * g.tpc);
+    L.part = o; o = a256(o + 4 * size_t(scan_partials_len<uint32_t>(n_cells + 1)));
+    L.total = o; o = a256(o + 8);
+    L.err = o; o = a256(o + 8);
+    L.bytes = o;
+    return L;
+}
+
+__global__ void tile_plan_count_kernel(const uint32_t *__restrict__ total, int64_t n_cells,
+                                       uint32_t *__restrict__ csf, int64_t *__restrict__ nseg,
+                                       const int *__restrict__ err) {
+    csf[n_cells] = *total;
+    nseg[0] = *err ? -1 : int64_t(*total);
+}
+
+static bool plan_supported(int N, int H, int W, int D, int64_t n_cells) {
+    if (N < 1 || H < 1 || W < 1 || D < 1 || D > kTileMaxPoints) return false;
+    if (n_cells < 1 || n_cells >= (int64_t(1) << 32) - 1) return false;
+    const TileGeom g = tile_geom(N, H, W, D);
+    return g.T < (int64_t(1) << 31) && g.tpc <= kTileMaxPoints &&
+           g.hl_bits + g.d_bits <= 16;
+}
+
+static int plan_dims_from(const bvp_tile_plan *p, TileGeom &g) {
+    BVP_REQUIRE(p && p->base, BVP_ERR_INVALID, "null tile plan");
+    BVP_REQUIRE(plan_supported(p->N, p->H, p->W, p->D, p->n_cells), BVP_ERR_UNSUPPORTED,
+                "frustum %dx%dx%dx%d not supported by the tile plan", p->N, p->H, p->W, p->D);
+    g = tile_geom(p->N, p->H, p->W, p->D);
+    return BVP_OK;
+}
+
+template <typename T>
+static T *at(const bvp_tile_plan *p, size_t off) {
+    return reinterpret_cast<T *>(static_cast<char *>(p->base) + off);
+}
+
+template <int CS, int SRC, int CL>
+static int launch_phase1(const TilePoolArgs &a, int B, size_t smem, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tile_pool_kernel<CS, SRC, CL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(a.g.T), unsigned(B));
+    cfg.blockDim = dim3(kPoolThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_c[1];
+    attr_c[0].id = cudaLaunchAttributeClusterDimension;
+    attr_c[0].val.clusterDim.x = CL;
+    attr_c[0].val.clusterDim.y = 1;
+    attr_c[0].val.clusterDim.z = 1;
+    cfg.attrs = attr_c;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, tile_pool_kernel<CS, SRC, CL>, a);
+    BVP_REQUIRE(e == cudaSuccess, BVP_ERR_CUDA, "tile_pool launch: %s", cudaGetErrorString(e));
+    return BVP_OK;
+}
+
+template <int CS, int SRC>
+static int run_tile_pool(const void *feats, const void *weights, const bvp_tile_plan *p,
+                         const TileGeom &g, int B, int C, int mean, int phases, float *rows,
+                         float *out, cudaStream_t s) {
+    const PlanLayout L = plan_layout(g, p->n_cells);
+    TilePoolArgs a{};
+    a.feats = feats;
+    a.weights = weights;
+    a.hdr = at<const uint4>(p, L.hdr);
+    a.rec = at<const uint32_t>(p, L.rec);
+    a.groups = at<const uint4>(p, L.groups);
+    a.seg_row = at<const uint32_t>(p, L.seg_row);
+    a.rows = rows;
+    a.max_seg = p->max_seg;
+    a.g = g;
+    a.C = C;
+    a.wbudget = std::max(2048, 128 * g.TH);
+#ifdef BVP_TILE_ABLATION  // profiling builds only: stop phase 1 after a stage
+    a.dbg = BVP_TILE_ABLATION;
+#endif
+    const int CP = CS * 32;
+    const size_t smem =
+        sizeof(float) * (size_t(g.TH) * (CP + 4) + size_t(g.TH) * ((g.D + 3) & ~3) + a.wbudget);
+    // clusters of CL adjacent columns (CL | W keeps a cluster inside one row
+    // of tiles)
+    int CL = (g.W % 8 == 0) ? 8 : (g.W % 4 == 0) ? 4 : (g.W % 2 == 0) ? 2 : 1;
+    if (phases & 1) {
+        int rc = BVP_OK;
+        switch (CL) {
+            case 8: rc = launch_phase1<CS, SRC, 8>(a, B, smem, s); break;
+            case 4: rc = launch_phase1<CS, SRC, 4>(a, B, smem, s); break;
+            case 2: rc = launch_phase1<CS, SRC, 2>(a, B, smem, s); break;
+            default: rc = launch_phase1<CS, SRC, 1>(a, B, smem, s); break;
+        }
+        if (rc != BVP_OK) return rc;
+    }
+    const int64_t nblk = ceil_div(p->n_cells, kFinCells) * B;
+    static int fin_per_sm[5] = {};
+    if (!fin_per_sm[CS]) {
+        int dev = 0, n = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tile_finalize_kernel<CS>, kPoolThreads, 0);
+        fin_per_sm[CS] = std::max(1, n) * sms;
+    }
+    if (phases & 2)
+        tile_finalize_kernel<CS><<<unsigned(std::min<int64_t>(nblk, fin_per_sm[CS])), kPoolThreads, 0, s>>>(
+            rows, p->max_seg, at<const uint32_t>(p, L.csf), at<const uint32_t>(p, L.npts),
+            p->n_cells, C, B, mean, out);
+    return check_launch("tile_pool");
+}
+
+template <int SRC>
+static int tile_pool_dispatch(const void *feats, const void *weights, const bvp_tile_plan *p,
+                              int B, int C, int mode, float *rows, size_t rows_bytes, float *out,
+                              cudaStream_t s) {
+    TileGeom g;
+    const int rc = plan_dims_from(p, g);
+    if (rc != BVP_OK) return rc;
+    BVP_REQUIRE(B >= 1 && C >= 0, BVP_ERR_INVALID, "bad dims B=%d C=%d", B, C);
+    int phases = 3;
+    if (mode & (BVP_TILE_PHASE1 | BVP_TILE_PHASE2))
+        phases = ((mode & BVP_TILE_PHASE1) ? 1 : 0) | ((mode & BVP_TILE_PHASE2) ? 2 : 0);
+    mode &= ~(BVP_TILE_PHASE1 | BVP_TILE_PHASE2);
+    BVP_REQUIRE(mode == BVP_SUM || mode == BVP_MEAN, BVP_ERR_UNSUPPORTED,
+                "the tile path reduces SUM and MEAN only (mode %d)", mode);
+    BVP_REQUIRE(C <= 128, BVP_ERR_UNSUPPORTED, "the tile path takes C <= 128 (C=%d)", C);
+    if (C == 0) return BVP_OK;
+    BVP_REQUIRE(feats && weights && out && rows, BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(rows_bytes >= size_t(B) * p->max_seg * C * sizeof(float), BVP_ERR_INVALID,
+                "segment-row scratch too small: need %zu bytes, got %zu",
+                size_t(B) * p->max_seg * C * sizeof(float), rows_bytes);
+    const int mean = mode == BVP_MEAN;
+    switch ((C + 31) / 32) {
+        case 1: return run_tile_pool<1, SRC>(feats, weights, p, g, B, C, mean, phases, rows, out, s);
+        case 2: return run_tile_pool<2, SRC>(feats, weights, p, g, B, C, mean, phases, rows, out, s);
+        case 3: return run_tile_pool<3, SRC>(feats, weights, p, g, B, C, mean, phases, rows, out, s);
+        default: return run_tile_pool<4, SRC>(feats, weights, p, g, B, C, mean, phases, rows, out, s);
+    }
+}
+
+}  // namespace bvp
+
+using namespace bvp;
+
+extern "C" {
+
+int bvp_tile_plan_supported(int N, int H, int W, int D, int64_t n_cells) {
+    return plan_supported(N, H, W, D, n_cells) ? 1 : 0;
+}
+
+size_t bvp_tile_plan_bytes(int N, int H, int W, int D, int64_t n_cells) {
+    if (!plan_supported(N, H, W, D, n_cells)) return 0;
+    return plan_layout(tile_geom(N, H, W, D), n_cells).bytes;
+}
+
+size_t bvp_tile_plan_workspace_bytes(int N, int H, int W, int D, int64_t n_cells) {
+    if (!plan_supported(N, H, W, D, n_cells)) return 0;
+    return plan_ws(tile_geom(N, H, W, D), n_cells).bytes;
+}
+
+int bvp_build_tile_plan(const uint32_t *cell_of_point, bvp_tile_plan *plan, void *workspace,
+                        size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(cell_of_point, BVP_ERR_INVALID, "null cell_of_point");
+    TileGeom g;
+    int rc = plan_dims_from(plan, g);
+    if (rc != BVP_OK) return rc;
+    const int64_t n_cells = plan->n_cells;
+    const PlanLayout L = plan_layout(g, n_cells);
+    const PlanWs WL = plan_ws(g, n_cells);
+    BVP_REQUIRE(plan->bytes >= L.bytes, BVP_ERR_INVALID, "tile plan buffer too small");
+    BVP_REQUIRE(workspace && workspace_bytes >= WL.bytes, BVP_ERR_INVALID,
+                "tile plan workspace too small: need %zu bytes, got %zu", WL.bytes,
+                workspace_bytes);
+    cudaStream_t s = as_stream(stream);
+    char *w = static_cast<char *>(workspace);
+    auto *fill = reinterpret_cast<uint32_t *>(w + WL.fill);
+    auto *owner = reinterpret_cast<unsigned long long *>(w + WL.owner);
+    auto *part = reinterpret_cast<uint32_t *>(w + WL.part);
+    auto *total = reinterpret_cast<uint32_t *>(w + WL.total);
+    auto *err = reinterpret_cast<int *>(w + WL.err);
+    auto *csf = at<uint32_t>(plan, L.csf);
+    auto *npts = at<uint32_t>(plan, L.npts);
+    cudaMemsetAsync(err, 0, 8, s);
+    cudaMemsetAsync(csf, 0, 4 * size_t(n_cells + 1), s);
+    cudaMemsetAsync(npts, 0, 4 * size_t(n_cells), s);
+    cudaMemsetAsync(fill, 0, 4 * size_t(n_cells + 1), s);
+    int cap = 1;
+    while (cap < g.tpc) cap <<= 1;
+    const size_t smem = 8 * size_t(cap);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(tile_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             8 * kTileMaxPoints);
+        attr = true;
+    }
+    tile_plan_kernel<<<unsigned(g.T), kPlanThreads, smem, s>>>(
+        cell_of_point, g, at<uint4>(plan, L.hdr), at<uint32_t>(plan, L.rec),
+        at<uint32_t>(plan, L.seg_cell), at<uint32_t>(plan, L.seg_start), at<uint4>(plan, L.groups),
+        err);
+    tile_seg_count_kernel<<<unsigned(g.T), 256, 0, s>>>(
+        at<const uint4>(plan, L.hdr), g, at<const uint32_t>(plan, L.seg_cell),
+        at<const uint32_t>(plan, L.seg_start), csf, npts);
+    device_excl_scan<uint32_t>(csf, csf, n_cells, part, total, s);
+    tile_plan_count_kernel<<<1, 1, 0, s>>>(total, n_cells, csf, at<int64_t>(plan, L.nseg), err);
+    tile_seg_assign_kernel<<<unsigned(g.T), 256, 0, s>>>(at<const uint4>(plan, L.hdr), g,
+                                                          at<const uint32_t>(plan, L.seg_cell),
+                                                          csf, fill, owner);
+    const unsigned cb = unsigned(std::min<int64_t>(ceil_div(n_cells, 256), 148 * 16));
+    tile_seg_fix_kernel<<<cb, 256, 0, s>>>(csf, n_cells, g, owner, at<uint32_t>(plan, L.seg_row));
+    return check_launch("build_tile_plan");
+}
+
+int bvp_tile_plan_init(bvp_tile_plan *plan, int N, int H, int W, int D, int64_t n_cells,
+                       void *base, size_t bytes, int64_t max_seg) {
+    BVP_REQUIRE(plan, BVP_ERR_INVALID, "null plan");
+    BVP_REQUIRE(plan_supported(N, H, W, D, n_cells), BVP_ERR_UNSUPPORTED,
+                "frustum %dx%dx%dx%d / %lld cells not supported by the tile plan", N, H, W, D,
+                (long long)n_cells);
+    const TileGeom g = tile_geom(N, H, W, D);
+    const PlanLayout L = plan_layout(g, n_cells);
+    BVP_REQUIRE(base && bytes >= L.bytes, BVP_ERR_INVALID, "tile plan buffer too small");
+    plan->N = N; plan->H = H; plan->W = W; plan->D = D;
+    plan->n_cells = n_cells;
+    plan->base = base;
+    plan->bytes = bytes;
+    plan->max_seg = max_seg;
+    plan->tile_rows = g.TH;
+    plan->n_tiles = g.T;
+    plan->n_seg = reinterpret_cast<const int64_t *>(static_cast<char *>(base) + L.nseg);
+    plan->cell_seg_first = reinterpret_cast<const uint32_t *>(static_cast<char *>(base) + L.csf);
+    plan->cell_points = reinterpret_cast<const uint32_t *>(static_cast<char *>(base) + L.npts);
+    return BVP_OK;
+}
+
+int bvp_tile_pool_f32(const float *features, const float *dist, const bvp_tile_plan *plan, int B,
+                      int C, int mode, float *rows, size_t rows_bytes, float *out, void *stream) {
+    return tile_pool_dispatch<kTileF32>(features, dist, plan, B, C, mode, rows, rows_bytes, out,
+                                        as_stream(stream));
+}
+
+int bvp_tile_pool_fused_bf16(const uint16_t *logits, const uint16_t *context,
+                             const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
+                             size_t rows_bytes, float *out, void *stream) {
+    return tile_pool_dispatch<kTileBF16Fused>(context, logits, plan, B, C, mode, rows, rows_bytes,
+                                              out, as_stream(stream));
+}
+
+}  // extern "C"

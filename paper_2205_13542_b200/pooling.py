@@ -62,6 +62,18 @@ def _scratch(cache: AssociationCache, B: int, C: int, mode: int) -> tuple:
 
 BACKENDS = ("prefixsum", "interval")
 
+#: widest channel count of the tiled path (csrc/tile.cu: 4 x 32 lanes)
+TILE_MAX_C = 128
+
+
+def _tile_plan(cache: AssociationCache, N: int, H: int, W: int, D: int, C: int, mode: int,
+               exact: int):
+    """The pixel-column tiled reduction (csrc/tile.cu) pools SUM / MEAN in
+    fast mode; MAX and exact mode use the interval kernels."""
+    if exact or mode == _lib.BVP_MAX or C == 0 or C > TILE_MAX_C:
+        return None
+    return cache.tile_plan(N, H, W, D)
+
 
 def _reducer(r) -> Reducer:
     return r if isinstance(r, Reducer) else Reducer.parse(str(r))
@@ -188,8 +200,11 @@ def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
     inp = _check_inputs(features, dist, cache, grid, check_finite)
     cache = cache.for_grid(grid)
     out = torch.empty((inp.B, inp.C, grid.n_cells), dtype=torch.float32, device=inp.feats.device)
-    if inp.C:
-        exact = int(DEFAULT_EXACT if exact is None else exact)
+    exact = int(DEFAULT_EXACT if exact is None else exact)
+    tp = _tile_plan(cache, inp.N, inp.H, inp.W, inp.D, inp.C, _MODE[reducer], exact)
+    if tp is not None:
+        tp.pool_f32(inp.feats, inp.dist, inp.B, inp.C, _MODE[reducer], out)
+    elif inp.C:
         nhwc = torch.empty(inp.feats.numel(), dtype=torch.float32, device=inp.feats.device)
         _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
@@ -226,6 +241,19 @@ def pool_prefixsum(features, dist, cache: AssociationCache, grid: BevGridSpec,
     return _finish(out, inp, grid)
 
 
+def _fn_key(fn):
+    """Stable cache key of a callable: bound methods by (object, name),
+    functools.partials by their function and arguments, else the object."""
+    import functools
+    if isinstance(fn, functools.partial):
+        return ("partial", _fn_key(fn.func), tuple(map(repr, fn.args)),
+                tuple(sorted((k, repr(v)) for k, v in fn.keywords.items())))
+    owner = getattr(fn, "__self__", None)
+    if owner is not None:
+        return ("method", id(owner), fn.__name__)
+    return ("fn", fn)
+
+
 class PoolPlan:
     """Pre-planned cached forward for fixed shapes (the serving loop).
 
@@ -249,6 +277,8 @@ class PoolPlan:
                                                           width, depth_bins)
         self.mode = _MODE[_reducer(reducer)]
         self.exact = int(DEFAULT_EXACT if exact is None else exact)
+        self._tile = _tile_plan(self.cache, n_cameras, height, width, depth_bins, channels,
+                                self.mode, self.exact)
         self._units = self.cache.needs_units(channels, exact=self.exact)
         f32 = dict(dtype=torch.float32, device=self.dev)
         self.out = torch.empty((batch, channels, grid.n_cells), **f32)
@@ -267,6 +297,20 @@ class PoolPlan:
     def transpose(self, features: torch.Tensor) -> None:
         _lib.call("bvp_to_nhwc_f32", ptr(features), self.B * self.N, self.C, self.H * self.W,
                   ptr(self.nhwc), stream_ptr(self.dev))
+
+    @property
+    def tiled(self) -> bool:
+        """True when this plan pools through the pixel-column tiled path."""
+        return self._tile is not None
+
+    def phase(self, features: torch.Tensor, dist: torch.Tensor, which: int,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+        """One launch of the tiled path alone (which = 1: the tile reduction
+        into segment rows, 2: the per-cell combine into the map), for timing."""
+        out = self.out if out is None else out
+        flag = _lib.BVP_TILE_PHASE1 if which == 1 else _lib.BVP_TILE_PHASE2
+        self._tile.pool_f32(features, dist, self.B, self.C, self.mode | flag, out)
+        return out
 
     def prepare(self, features: torch.Tensor, zero: bool = True) -> None:
         """NHWC staging of the features beside the zero fill of the plan's
@@ -299,6 +343,9 @@ class PoolPlan:
         One C call: the NHWC transpose and the map's zero fill run side by
         side (forked stream), then the interval reduction."""
         out = self.out if out is None else out
+        if self._tile is not None:
+            self._tile.pool_f32(features, dist, self.B, self.C, self.mode, out)
+            return out
         c = self.cache
         _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(c.d_ranks),
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
@@ -315,6 +362,12 @@ class PoolPlan:
         CacheBuilder whose buffers this plan's cache aliases) reassociates
         the rig ``cams`` while the features' staging and the map's zero fill
         run beside it on a side stream; then the reduction."""
+        if self._tile is not None:
+            # the builder rebuilds the tile plan this plan pools through
+            self.cache = builder.build(cams).for_grid(self.grid)
+            self._tile = _tile_plan(self.cache, self.N, self.H, self.W, self.D, self.C,
+                                    self.mode, self.exact)
+            return self.run(features, dist)
         cur = torch.cuda.current_stream(self.dev)
         side = self.__dict__.get("_side")
         if side is None:
@@ -322,7 +375,9 @@ class PoolPlan:
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             self.prepare(features)
-        builder.build(cams)
+        # pool with the cache of THIS frame (its deferred units and exact
+        # chunk list belong to it, not to the first frame's cache)
+        self.cache = builder.build(cams).for_grid(self.grid)
         cur.wait_stream(side)
         return self.reduce(dist, zeroed=True)
 
@@ -330,7 +385,7 @@ class PoolPlan:
         """A CUDA graph of ``fn(*tensors)`` (the plan's launches on these
         buffers), captured once per buffer set and replayed after that: the
         frame loop then costs one host call instead of one per kernel."""
-        key = (getattr(fn, "__name__", id(fn)),) + tuple(t.data_ptr() for t in tensors)
+        key = (_fn_key(fn),) + tuple(t.data_ptr() for t in tensors)
         graphs = self.__dict__.setdefault("_graphs", {})
         g = graphs.get(key)
         if g is None:
@@ -342,6 +397,7 @@ class PoolPlan:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn(*tensors)
+            g.fn = fn  # keeps fn (and so its identity) alive with the graph
             graphs[key] = g
         return g
 
@@ -520,6 +576,11 @@ def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCa
     cache = cache.for_grid(grid)
     dev = lg.device
     out = torch.empty((B, C, grid.n_cells), dtype=torch.float32, device=dev)
+    tp = _tile_plan(cache, N, H, W, D, C, _MODE[reducer], 0)
+    if tp is not None:  # softmax formed per tile in shared memory (csrc/tile.cu)
+        tp.pool_fused_bf16(lg, cx, B, C, _MODE[reducer], out)
+        v = out.view(B, C, grid.nx, grid.ny)
+        return BevFeatureMap(v if batched else v[0], grid)
     ws = torch.empty(_lib.load().bvp_fused_workspace_bytes(B, N, C, H, W, D), dtype=torch.uint8,
                      device=dev)
     _lib.call("bvp_fused_pool_bf16", ptr(lg), ptr(cx), ptr(cache.d_ranks),

@@ -546,8 +546,9 @@ def test_per_frame_build_defers_units():
 
 
 def test_plan_staging_split_matches_run():
-    """PoolPlan.prepare (NHWC staging beside the zero fill) + reduce(zeroed)
-    equals run(); a caller-provided output buffer is always zero-filled."""
+    """Interval path (MAX): PoolPlan.prepare (NHWC staging beside the zero
+    fill) + reduce(zeroed) equals run(); a caller-provided output buffer is
+    always zero-filled.  Tiled path (SUM): phase 1 then phase 2 equals run()."""
     spec = bp.CONFIGS["T"]
     f = spec.frustum
     rig, feats_np, logits_np, grid = bp.gen_workload(spec)
@@ -555,7 +556,8 @@ def test_plan_staging_split_matches_run():
     feats = torch.from_numpy(feats_np).cuda()[None]
     dist = bp.normalize_depth(torch.from_numpy(logits_np).cuda())[None]
     plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
-                       f.depth_bins, 1, bp.Reducer.SUM)
+                       f.depth_bins, 1, bp.Reducer.MAX)
+    assert not plan.tiled
     want = plan.run(feats, dist).clone()
     plan.out.fill_(7.0)
     plan.prepare(feats)
@@ -563,6 +565,13 @@ def test_plan_staging_split_matches_run():
     mine = torch.full_like(want, 3.0)
     plan.reduce(dist, out=mine, zeroed=True)  # not the plan's buffer: zero-filled anyway
     np.testing.assert_array_equal(mine.cpu().numpy(), want.cpu().numpy())
+    tplan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
+                        f.depth_bins, 1, bp.Reducer.SUM)
+    assert tplan.tiled
+    want = tplan.run(feats, dist).clone()
+    tplan.out.fill_(7.0)
+    tplan.phase(feats, dist, 1)
+    np.testing.assert_array_equal(tplan.phase(feats, dist, 2).cpu().numpy(), want.cpu().numpy())
 
 
 def test_run_uncached_matches_cached_pool():
@@ -581,6 +590,34 @@ def test_run_uncached_matches_cached_pool():
     want = bp.pool_interval(feats_np, bp.normalize_depth(logits_np),
                             bp.build_cache(rig, f, grid), grid).values
     np.testing.assert_array_equal(got.reshape(want.shape), want)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_run_uncached_follows_rig_changes(exact):
+    """A per-frame plan pools every frame with THAT frame's association
+    (exact mode's chunk list and the tile plan included) when the rig
+    changes between frames."""
+    spec = bp.CONFIGS["T"]
+    f = spec.frustum
+    rig, feats_np, logits_np, grid = bp.gen_workload(spec)
+    rig2 = [bp.CameraCalibration(c.fx * 1.1, c.fy * 1.1, c.cx + 1.5, c.cy - 0.5, c.rotation,
+                                 c.translation + np.array([0.7, -0.4, 0.1]), c.camera_id)
+            for c in rig]
+    feats = torch.from_numpy(feats_np).cuda()[None]
+    dist = bp.normalize_depth(torch.from_numpy(logits_np).cuda())[None]
+    builder = bp.CacheBuilder(spec.n_cameras, f, grid)
+    cams = [torch.from_numpy(bp.rig_rows(r)).cuda() for r in (rig, rig2)]
+    plan = bp.PoolPlan(builder.build(cams[0]), grid, spec.n_cameras, spec.channels, f.height,
+                       f.width, f.depth_bins, 1, bp.Reducer.SUM, exact=exact)
+    for r, c in ((rig, cams[0]), (rig2, cams[1]), (rig, cams[0])):
+        got = plan.run_uncached(builder, c, feats, dist).cpu().numpy()
+        cache = bp.build_cache(r, f, grid)
+        want = o.pool_interval(feats_np, dist[0].cpu().numpy(), cache.ranks,
+                               cache.interval_starts, cache.interval_cells, grid.n_cells, "sum")
+        if exact:
+            np.testing.assert_array_equal(got.reshape(want.shape), want)
+        else:
+            assert max_rel_dev(want, got.reshape(want.shape)) <= FP32_TOL
 
 
 @pytest.mark.parametrize("C", [1, 3, 20, 80, 200, 250, 256, 512])
