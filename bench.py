@@ -5,15 +5,16 @@
 Workload (configs[1], SURVEY.md §8 "S"): nuScenes camera stream, 6 cameras x
 32x88 features, D=118 (1-60 m @ 0.5 m), C=80, 360x360 BEV grid @ 0.3 m,
 batch 1, cached-interval forward.  A step is one reference-API forward
-``pool_interval(features, dist, cache, grid, SUM)``: NHWC staging of the
-features + the interval-reduction kernel, inputs resident in HBM, L2 flushed
-(512 MiB write) between steps.  value = frustum points/s over all ranks (each
-rank pools its own sample: weak scaling, no collective in the loop; NCCL only
-gathers the timings).  e2e = the same step through PoolPlan.run_host with
-host buffers (pinned H2D of features + dist, D2H of the BEV map) in the timed
-region.  N=1 also reports cpu_baseline (the oracle's C port of the
-reference's pool_interval, all host threads) and the other configurations as
-"variants".
+``pool_interval(features, dist, cache, grid, SUM)`` through the pixel-column
+tiled path (csrc/tile.cu: tile reduction + per-cell combine into the map),
+inputs resident in HBM, L2 flushed (512 MiB write) between steps.  value =
+frustum points/s over all ranks (each rank pools its own sample: weak
+scaling, no collective in the loop; NCCL only gathers the timings).  e2e =
+the same step through PoolPlan.run_frames with host buffers (pinned H2D of
+features + dist, D2H of the BEV map) in the timed region.  N=1 also reports
+cpu_baseline (the reference's own pool_interval from baseline/_ref on all
+host threads; the oracle's C port only if that is missing) and the other
+configurations as "variants".
 
 ``--impl reference`` times the reference's own CPU pool_interval (installed
 unmodified into baseline/_ref; numba/OpenMP over all host cores; the
@@ -42,9 +43,9 @@ METRIC = "bev_pool_points_per_sec"
 UNIT = "points/s"
 CONFIG_NAME = "S"
 FLUSH_BYTES = 512 << 20
-KERNEL_KEY = "pool_ivl_kernel"
-# NHWC transpose, zero-fill (memset kernel), chunk kernel, split combine
-LAUNCHES_PER_STEP = 4
+KERNEL_KEYS = ("tile_pool_kernel", "tile_finalize_kernel")
+# the tiled path: tile reduction (phase 1) + per-cell combine into the map (phase 2)
+LAUNCHES_PER_STEP = 2
 # pure L2 gather of the S-config rows in rank order (scripts/gather_mlp_bench.cu,
 # profiles/r01/gather_mlp_bench.txt)
 L2_GATHER_CEILING_GBPS = 13610.0
@@ -56,7 +57,6 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--exact", type=int, default=None, help="1: 64-bit bit-exact mode")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -68,16 +68,14 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def config_dict(spec, extra=None):
+def config_dict(spec):
+    """The workload, identical in both arms (the driver compares them)."""
     f, g = spec.frustum, spec.grid
-    d = {"workload": "nuScenes camera stream (configs[1]): cached-interval forward",
-         "cameras": spec.n_cameras, "feature_hw": [f.height, f.width], "depth_bins": f.depth_bins,
-         "channels": spec.channels, "grid": [g.nx, g.ny], "cell_m": g.r, "batch_per_gpu": 1,
-         "points_per_sample": spec.n_points, "reducer": "sum",
-         "l2": "flushed between steps (512 MiB write)"}
-    if extra:
-        d.update(extra)
-    return d
+    return {"workload": "nuScenes camera stream (configs[1]): cached-interval forward",
+            "cameras": spec.n_cameras, "feature_hw": [f.height, f.width],
+            "depth_bins": f.depth_bins, "channels": spec.channels, "grid": [g.nx, g.ny],
+            "cell_m": g.r, "batch_per_gpu": 1, "points_per_sample": spec.n_points,
+            "reducer": "sum"}
 
 
 # ---------------------------------------------------------------------------
@@ -183,6 +181,7 @@ def run_reference(args):
         "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 in / f64 accumulate", "data": "synthetic",
         "config": config_dict(spec),
+        "impl_detail": what,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{len(times)} full nuScenes-shape pool_interval steps ({what}, "
                                    "incl. its NHWC transposes)"},
@@ -260,13 +259,15 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel_key):
-    """dram read+write bytes per launch of the headline kernel from the
-    committed ncu --set full summary, if present."""
+def ncu_traffic(kernel_keys):
+    """dram read+write bytes per step of the headline kernels (summed) from
+    the committed ncu --set full summary, if present."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(kernel_key, {}).get("dram_bytes")
+            js = json.load(fh)
+        vals = [js.get(k, {}).get("dram_bytes") for k in kernel_keys]
+        return None if any(v is None for v in vals) else float(sum(vals))
     except (OSError, ValueError):
         return None
 
@@ -307,9 +308,8 @@ def main():
     cache = bp.build_cache(rig, f, grid, device=dev)
     feats = torch.from_numpy(feats_np).to(dev).view(1, *feats_np.shape)
     dist = bp.normalize_depth(torch.from_numpy(logits_np).to(dev)).view(1, *logits_np.shape)
-    exact = bool(args.exact) if args.exact is not None else False
     plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
-                       f.depth_bins, 1, bp.Reducer.SUM, exact, dev)
+                       f.depth_bins, 1, bp.Reducer.SUM, False, dev)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -323,9 +323,10 @@ def main():
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize(dev)
-    # the step: PoolPlan.run as one CUDA graph (NHWC transpose, then the
-    # chunk kernel + combine with the empty cells' zero fill beside them on a
-    # forked stream); one host call per frame
+    # the step: PoolPlan.run as one CUDA graph (the tiled path: tile
+    # reduction, then the per-cell combine into the map); one host call per
+    # frame
+    assert plan.tiled, "the headline step is the tiled path"
     g_s = plan.graphed(plan.run, feats, dist)
     g_s.replay()
     for k in range(K):
@@ -337,22 +338,21 @@ def main():
     if world > 1:
         tdist.barrier()
     step_ms = [e[0].elapsed_time(e[2]) for e in ev]
-    # the roofline kernel alone: the same step split into two graphs,
-    # staging (transpose beside a full zero fill of the map) | reduction
-    # (chunk kernel + combine on the zeroed map); events between them
-    g_t = plan.graphed(plan.prepare, feats)
-    g_r = plan.graphed(functools.partial(plan.reduce, zeroed=True), dist)
+    # per kernel: the same two launches as two graphs with an event between
+    g_1 = plan.graphed(functools.partial(plan.phase, which=1), feats, dist)
+    g_2 = plan.graphed(functools.partial(plan.phase, which=2), feats, dist)
     for k in range(K):
         flush.zero_()
         ev[k][0].record(stream)
-        g_t.replay()
+        g_1.replay()
         ev[k][1].record(stream)
-        g_r.replay()
+        g_2.replay()
         ev[k][2].record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
         tdist.barrier()
-    kern_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    p1_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    p2_ms = [e[1].elapsed_time(e[2]) for e in ev]
     split_ms = [e[0].elapsed_time(e[2]) for e in ev]
     tot_ms = sum(step_ms)
     # e2e: host buffers (pinned) through the public serving API
@@ -379,17 +379,22 @@ def main():
         variants = run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush)
     clk = clocks.stop()
 
-    # ---- roofline of the dominant kernel (interval reduction) -----------
-    # algorithmic bytes of one reduction launch (SURVEY.md §8d, S reference-
-    # API formulation): NHWC features + dist + ranks + interval table + map
+    # ---- roofline: the pooling step (both kernels of the tiled path) ------
+    # compulsory bytes of one pool_interval over the reference formulation
+    # (SURVEY.md §8d, S): features + dist + ranks + interval table + map
     n_in, n_int = cache.n_in_range, cache.n_intervals
     C, NHW, NDHW = spec.channels, spec.n_cameras * f.height * f.width, P
     alg_bytes = 4 * NHW * C + 4 * NDHW + 4 * n_in + 8 * n_int + 4 * C * grid.n_cells
-    kern_avg_s = statistics.mean(kern_ms) * 1e-3
+    step_avg_s = statistics.mean(step_ms) * 1e-3
     peak, peak_src = measured_peak()
-    achieved = alg_bytes / kern_avg_s / 1e9
-    traffic = ncu_traffic(KERNEL_KEY)
-    gather_bytes = n_in * 4 * C  # feature rows gathered from L2 (NHWC table, 5.4 MB)
+    achieved = alg_bytes / step_avg_s / 1e9
+    traffic = ncu_traffic(KERNEL_KEYS)
+    # per kernel: the bytes each one moves (the segment rows go through L2)
+    n_seg = plan._tile.n_seg
+    n_groups_rec = n_in  # one 4-byte record per in-range point
+    p1_bytes = 4 * NHW * C + 4 * NDHW + 4 * n_groups_rec + 4 * n_seg + 4 * C * n_seg
+    p2_bytes = 4 * C * n_seg + 4 * (grid.n_cells + 1) + 4 * C * grid.n_cells
+    p1_s, p2_s = statistics.mean(p1_ms) * 1e-3, statistics.mean(p2_ms) * 1e-3
 
     if rank != 0:
         if world > 1:
@@ -400,27 +405,31 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": max(3, args.warmup), "ms_per_step": tot_ms / K, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 in, f64 accumulate (bit-exact)" if exact else "f32",
+        "dtype": "f32",
         "data": "synthetic (reference gen_workload: PCG64 seed=rank, synthetic 6-camera rig)",
-        "config": config_dict(spec, {"parallelism": f"batch-sharded x{world} (1 sample/GPU)",
-                                     "exact": exact}),
+        "config": config_dict(spec),
+        "parallelism": f"batch-sharded x{world} (1 sample/GPU, no collective in the step)",
+        "timing": "CUDA events on the launching stream, L2 flushed (512 MiB write) before every step",
         "latency_ms": {"step_median": statistics.median(step_ms), "step_min": min(step_ms),
-                       "interval_kernel_median": statistics.median(kern_ms),
+                       "tile_reduce_median": statistics.median(p1_ms),
+                       "cell_combine_median": statistics.median(p2_ms),
                        "split_step_median": statistics.median(split_ms),
-                       "step": "PoolPlan.run as one CUDA graph; interval_kernel_median and "
-                               "split_step_median from the same step as two graphs "
-                               "(staging with a full zero fill | reduction)"},
+                       "step": "PoolPlan.run as one CUDA graph (tile_pool_kernel + "
+                               "tile_finalize_kernel); per-kernel medians from the same two "
+                               "launches as two graphs"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "interval reduction (pool_ivl_kernel + combine on a zero-filled map; split-graph timing), "
-                               "reference formulation",
+                     "kernel": "pooling step = tile_pool_kernel + tile_finalize_kernel (the two "
+                               "launches that replace interval_reduce), reference formulation",
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_source": peak_src,
                      "frac_of_nominal_8TBs": achieved / 8000.0,
-                     "l2_gather": {"bytes": gather_bytes,
-                                   "achieved_GBps": gather_bytes / kern_avg_s / 1e9,
-                                   "ceiling_GBps": L2_GATHER_CEILING_GBPS,
-                                   "ceiling_source": "scripts/gather_mlp_bench.cu (pure gather of "
-                                                     "the same rows, measured on B200)"}},
+                     "kernels": {
+                         "tile_pool_kernel": {"ms": statistics.mean(p1_ms), "bytes": p1_bytes,
+                                              "GBps": p1_bytes / p1_s / 1e9,
+                                              "frac": p1_bytes / p1_s / 1e9 / peak},
+                         "tile_finalize_kernel": {"ms": statistics.mean(p2_ms), "bytes": p2_bytes,
+                                                  "GBps": p2_bytes / p2_s / 1e9,
+                                                  "frac": p2_bytes / p2_s / 1e9 / peak}}},
         "e2e": {"value": world * P * K / (e2e_tot * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
                 "ms_per_step": e2e_tot / K,

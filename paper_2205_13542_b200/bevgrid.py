@@ -546,7 +546,7 @@ class CacheBuilder:
     aliases the builder's buffers until the next ``build``."""
 
     def __init__(self, n_cameras: int, frustum: FrustumSpec, grid: BevGridSpec, device=None,
-                 unit_budget: int = UNIT_BUDGET, sort_work: bool = False):
+                 unit_budget: int = UNIT_BUDGET, sort_work: bool = False, tiles: bool = False):
         self.dev = cuda_device(device)
         self.n_cameras, self.frustum, self.grid = n_cameras, frustum, grid
         self.P = n_cameras * frustum.points_per_camera
@@ -561,8 +561,10 @@ class CacheBuilder:
         self._grid_arr = grid.as_array()
         self._one_call = self.defer_units and CHUNK > 0
         self.dims = (n_cameras, frustum.height, frustum.width, frustum.depth_bins)
+        # tiles: rebuild the tiled reduction's plan with every association
+        # (otherwise a cache builds it on first tiled use, with one sync)
         self.tplan = (TilePlan(*self.dims, grid.n_cells, self.dev)
-                      if TilePlan.supported(*self.dims, grid.n_cells) else None)
+                      if tiles and TilePlan.supported(*self.dims, grid.n_cells) else None)
         if self._one_call:
             b = self.bufs
             n = int(_lib.load().bvp_work_workspace_bytes(b["n_int_max"], self.P, CHUNK, grid.nx,
@@ -604,7 +606,9 @@ class CacheBuilder:
         ordered, no sync; scratch sized for the worst case) and attach it."""
         if self.tplan is not None:
             self.tplan.build(self.bufs["cells"])
-        cache._host[("tile", *self.dims)] = self.tplan
+            cache._host[("tile", *self.dims)] = self.tplan
+        else:
+            cache._host[("tile", *self.dims)] = None  # per-frame caches pool with the interval kernels
         return cache
 
 
@@ -621,8 +625,7 @@ def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
     cache = builder.build(cams_d, fingerprint_inputs(rig, frustum_spec, grid_spec))
     cache._counts()  # one sync: sizes known on the host from here on
     cache.fit_launch()
-    if builder.tplan is not None:
-        builder.tplan.fit()
+    cache._host.pop(("tile", *builder.dims), None)  # the tile plan is built on first use
     return cache
 
 

@@ -37,6 +37,7 @@
 #include <algorithm>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -384,6 +385,16 @@ tile_pool_kernel(TilePoolArgs a) {
     const int64_t nb = int64_t(b) * g.N + id.n;
     const int64_t pix0 = int64_t(id.h0) * g.W + id.w;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the first RPT records of each thread are loaded now, beside the staging
+    // (records [0, RPT * 256) cover the whole tile at the nuScenes shape)
+    constexpr int RPT = 8;
+    const uint32_t *rt = a.rec + t * g.tpc;
+    uint32_t pre[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const uint32_t k = threadIdx.x + kPoolThreads * u;
+        pre[u] = k < h.x ? __ldg(rt + k) : 0u;
+    }
     // (1) stage: F[hl][c] = features[n, c, h0 + hl, w]; w[hl][d] = dist[n, d, h0 + hl, w].
     // The CL tiles of a cluster are CL adjacent columns of one camera.  CTA
     // `rank` loads channel quads (and depth-bin quads) rank, rank + CL, ... for
@@ -472,7 +483,6 @@ tile_pool_kernel(TilePoolArgs a) {
             for (int d = lane; d < D; d += 32) row[d] *= inv;
         }
     }
-    const uint32_t *rt = a.rec + t * g.tpc;
     const uint32_t *srow = a.seg_row + t * g.tpc;
     float *rows = a.rows + int64_t(b) * a.max_seg * C;
     const int shift = g.hl_bits + g.d_bits;
@@ -502,11 +512,27 @@ tile_pool_kernel(TilePoolArgs a) {
         __syncthreads();  // staging done; previous window consumed
         for (uint32_t i = threadIdx.x; i < wlen; i += kPoolThreads) ws[i] = 0.f;
         __syncthreads();
-        // (2) aggregate: each run of one (cell, row) summed in depth order;
-        // a thread's records are loaded U at a time
+        // (2) aggregate: each run of one (cell, row) summed in depth order
+        // (records below RPT * 256 come from the prefetch)
+        auto run = [&](uint32_t k, uint32_t r) {
+            if (k < G0.w || k >= r_end || !(r >> 31)) return;
+            const uint32_t widx = (r >> shift) & wmask;
+            float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+            for (uint32_t kk = k + 1; kk < r_end; ++kk) {
+                r = __ldg(rt + kk);
+                if (r >> 31) break;
+                sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+            }
+            ws[widx - G0.z] = sum;
+        };
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) run(threadIdx.x + kPoolThreads * u, pre[u]);
         {
             constexpr int U = 4;
-            for (uint32_t k0 = G0.w + threadIdx.x; k0 < r_end; k0 += kPoolThreads * U) {
+            // this thread's records k = threadIdx.x (mod 256) in [max(G0.w, RPT*256), r_end)
+            uint32_t k_lo = max(G0.w, uint32_t(RPT * kPoolThreads));
+            k_lo += (threadIdx.x - k_lo % kPoolThreads + kPoolThreads) % kPoolThreads;
+            for (uint32_t k0 = k_lo; k0 < r_end; k0 += kPoolThreads * U) {
                 uint32_t rr[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -514,19 +540,7 @@ tile_pool_kernel(TilePoolArgs a) {
                     rr[u] = k < r_end ? __ldg(rt + k) : 0u;
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint32_t k = k0 + kPoolThreads * u;
-                    uint32_t r = rr[u];
-                    if (k >= r_end || !(r >> 31)) continue;
-                    const uint32_t widx = (r >> shift) & wmask;
-                    float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
-                    for (uint32_t kk = k + 1; kk < r_end; ++kk) {
-                        r = __ldg(rt + kk);
-                        if (r >> 31) break;
-                        sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
-                    }
-                    ws[widx - G0.z] = sum;
-                }
+                for (int u = 0; u < U; ++u) run(k0 + kPoolThreads * u, rr[u]);
             }
         }
         __syncthreads();
@@ -534,6 +548,9 @@ tile_pool_kernel(TilePoolArgs a) {
         // (3) one warp per group of 8 cells
         for (int q = q0 + warp; q < q1; q += NW) {
             const uint4 G = gt[q];
+            // the group's segment-row indices, loaded before its products
+            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
+            const uint32_t my_row = lane < nk ? __ldg(srow + q * kTileGroup + lane) : 0u;
             const float *wq = ws + (G.z - G0.z);
             float2 acc[kTileGroup / 2][CS];
 #pragma unroll
@@ -544,8 +561,6 @@ tile_pool_kernel(TilePoolArgs a) {
                 group_row<CS, FS>(acc, wq, fs, __ffs(m) - 1, lane);
             for (uint32_t m = G.y; m; m &= m - 1, wq += kTileGroup)
                 group_row<CS, FS>(acc, wq, fs, 31 + __ffs(m), lane);
-            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
-            const uint32_t my_row = lane < nk ? __ldg(srow + q * kTileGroup + lane) : 0u;
 #pragma unroll
             for (int k = 0; k < kTileGroup; ++k) {
                 const uint32_t row = __shfl_sync(0xFFFFFFFFu, my_row, k);
@@ -564,78 +579,165 @@ tile_pool_kernel(TilePoolArgs a) {
 }
 
 // ---- phase 2: per-cell combine + transpose into the channel-major map -------
-// Persistent CTAs walk blocks of 32 consecutive cells.  In a block, warp w
-// combines cells w, w+8, w+16, w+24 (lanes over channels; a cell's segment
-// rows are contiguous, the first row of all four cells is loaded before any
-// is summed), then warp w writes channels w, w+8, ... of the 32 cells as full
-// 128-byte lines.  The next block's cell_seg_first entries are loaded while
-// this block's rows are in flight, so a block costs one memory latency.
+// A CTA owns 32 consecutive cells.  Warp w combines cells w, w+8, w+16, w+24
+// with lanes over channels (a cell's segment rows are contiguous; one
+// coalesced load per 32 channels of a row), into a shared [cell][channel]
+// tile; then warp w writes channels w, w+8, ... of the 32 cells as full
+// 128-byte lines.  Everything is 32-bit index math and fully unrolled over
+// the channel slots: the kernel is bound by the map's stores.
 template <int CS>
 __global__ void __launch_bounds__(kPoolThreads)
 tile_finalize_kernel(const float *__restrict__ rows, int64_t max_seg,
                      const uint32_t *__restrict__ cell_seg_first,
-                     const uint32_t *__restrict__ cell_npts, int64_t n_cells, int C, int B,
-                     int mean, float *__restrict__ out) {
+                     const uint32_t *__restrict__ cell_npts, int n_cells, int C, int mean,
+                     float *__restrict__ out) {
     constexpr int CP = CS * 32;
-    constexpr int NW = kPoolThreads / 32, CPW = kFinCells / NW;
+    constexpr int NW = kPoolThreads / 32;
     __shared__ float tile[kFinCells][CP + 1];
+    const int c0 = blockIdx.x * kFinCells, b = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_blk = int((n_cells + kFinCells - 1) / kFinCells), total = n_blk * B;
-    auto load_first = [&](int it, uint32_t &f, uint32_t &f32) {
-        if (it < total) {
-            const int bb = it / n_blk;
-            const int64_t c0 = int64_t(it - bb * n_blk) * kFinCells;
-            const int64_t nc = n_cells - c0 < kFinCells ? n_cells - c0 : int64_t(kFinCells);
-            f = __ldg(cell_seg_first + c0 + (lane < nc ? lane : nc));
-            f32 = __ldg(cell_seg_first + c0 + nc);
-        }
-    };
-    uint32_t first = 0, first32 = 0;
-    load_first(blockIdx.x, first, first32);
-    for (int it = blockIdx.x; it < total; it += gridDim.x) {
-        uint32_t nfirst = 0, nfirst32 = 0;
-        load_first(it + gridDim.x, nfirst, nfirst32);
-        const int b = it / n_blk;
-        const int64_t c0 = int64_t(it - b * n_blk) * kFinCells;
-        const int nc = int(n_cells - c0 < kFinCells ? n_cells - c0 : int64_t(kFinCells));
-        const float *rb = rows + int64_t(b) * max_seg * C;
-        float acc[CPW][CS];
-        uint32_t s0[CPW], s1[CPW];
+    const int nc = min(kFinCells, n_cells - c0);
+    const uint32_t f = __ldg(cell_seg_first + c0 + min(lane, nc));
+    const uint32_t f_end = __ldg(cell_seg_first + c0 + nc);
+    const float *rb = rows + int64_t(b) * max_seg * C;
 #pragma unroll
-        for (int u = 0; u < CPW; ++u) {
-            const int cl = warp + NW * u;
-            s0[u] = __shfl_sync(0xFFFFFFFFu, first, cl);
-            s1[u] = cl + 1 < 32 ? __shfl_sync(0xFFFFFFFFu, first, (cl + 1) & 31) : first32;
-            if (cl >= nc) s1[u] = s0[u];
+    for (int u = 0; u < kFinCells / NW; ++u) {
+        const int cl = warp + NW * u;
+        const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, f, cl);
+        uint32_t s1 = cl < 31 ? __shfl_sync(0xFFFFFFFFu, f, cl + 1) : f_end;
+        if (cl >= nc) s1 = s0;
+        float acc[CS];
+#pragma unroll
+        for (int j = 0; j < CS; ++j) acc[j] = 0.f;
+        if (s1 > s0) {
+            const float *r = rb + int64_t(s0) * C + lane;
+            const bool two = s1 > s0 + 1;  // ~22% of cells: load both rows at once
 #pragma unroll
             for (int j = 0; j < CS; ++j)
-                acc[u][j] = (s1[u] > s0[u] && lane + 32 * j < C)
-                                ? __ldg(rb + int64_t(s0[u]) * C + lane + 32 * j)
-                                : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < CPW; ++u) {
-            const int cl = warp + NW * u;
-            for (uint32_t s = s0[u] + 1; s < s1[u]; ++s)
+                if (lane + 32 * j < C) {
+                    acc[j] = __ldg(r + 32 * j);
+                    if (two) acc[j] += __ldg(r + C + 32 * j);
+                }
+            r += C;
+            for (uint32_t s = s0 + 2; s < s1; ++s) {
+                r += C;
 #pragma unroll
                 for (int j = 0; j < CS; ++j)
-                    if (lane + 32 * j < C) acc[u][j] += __ldg(rb + int64_t(s) * C + lane + 32 * j);
-            if (mean && s1[u] > s0[u]) {
+                    if (lane + 32 * j < C) acc[j] += __ldg(r + 32 * j);
+            }
+            if (mean) {
                 const float inv = 1.f / float(__ldg(cell_npts + c0 + cl));
 #pragma unroll
-                for (int j = 0; j < CS; ++j) acc[u][j] *= inv;
+                for (int j = 0; j < CS; ++j) acc[j] *= inv;
             }
-#pragma unroll
-            for (int j = 0; j < CS; ++j) tile[cl][lane + 32 * j] = acc[u][j];
         }
-        __syncthreads();
-        float *ob = out + int64_t(b) * C * n_cells + c0 + lane;
-        if (lane < nc)
-            for (int ch = warp; ch < C; ch += NW) ob[int64_t(ch) * n_cells] = tile[lane][ch];
-        __syncthreads();
-        first = nfirst;
-        first32 = nfirst32;
+#pragma unroll
+        for (int j = 0; j < CS; ++j) tile[cl][lane + 32 * j] = acc[j];
     }
+    __syncthreads();
+    if (lane < nc) {
+        float *ob = out + int64_t(b) * C * n_cells + c0 + lane;
+#pragma unroll
+        for (int k = 0; k < CP / NW; ++k) {
+            const int ch = warp + NW * k;
+            if (ch < C) ob[int64_t(ch) * n_cells] = tile[lane][ch];
+        }
+    }
+}
+
+// TMA variant (n_cells % 4 == 0): the CTA assembles the (C x 32 cells) block
+// of the map in shared memory in the tensor map's 128-byte-swizzled layout and
+// one thread writes it with a single bulk tensor store, double buffered so the
+// store of block k overlaps the combine of block k+1.  Lane l of warp w
+// combines cell 4w + (l & 3), channels (l >> 2) + 8i: its loads are 32-byte
+// sectors of a segment row, its shared stores hit 32 distinct banks.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int CS>
+__global__ void __launch_bounds__(kPoolThreads)
+tile_finalize_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ rows,
+                         int64_t max_seg, const uint32_t *__restrict__ cell_seg_first,
+                         const uint32_t *__restrict__ cell_npts, int64_t n_cells, int C,
+                         int mean) {
+    extern __shared__ __align__(1024) unsigned char fin_smem[];
+    // C rows x 128 bytes, 1024-byte aligned (the swizzle atom)
+    unsigned char *buf = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(fin_smem) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int cx = 4 * warp + (lane & 3), cg8 = lane >> 2;
+    const int b = blockIdx.y;
+    const int64_t c0 = int64_t(blockIdx.x) * kFinCells;
+    const int64_t c = c0 + cx;
+    uint32_t s0 = 0, s1 = 0;
+    float inv = 1.f;
+    if (c < n_cells) {
+        s0 = __ldg(cell_seg_first + c);
+        s1 = __ldg(cell_seg_first + c + 1);
+        if (mean && s1 > s0) inv = 1.f / float(__ldg(cell_npts + c));
+    }
+    const float *rb = rows + int64_t(b) * max_seg * C;
+    constexpr int NI = 4 * CS;  // channels per lane: ceil(C / 8) <= 4 CS
+    float v[NI];
+    const float *r0 = rb + int64_t(s0) * C + cg8;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) v[i] = (s1 > s0 && cg8 + 8 * i < C) ? __ldg(r0 + 8 * i) : 0.f;
+    for (uint32_t s = s0 + 1; s < s1; ++s) {
+        const float *r = rb + int64_t(s) * C + cg8;
+#pragma unroll
+        for (int i = 0; i < NI; ++i)
+            if (cg8 + 8 * i < C) v[i] += __ldg(r + 8 * i);
+    }
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+        const int ch = cg8 + 8 * i;
+        if (ch < C) {
+            const uint32_t off = uint32_t(ch) * 128u +
+                                 ((uint32_t(warp) ^ (uint32_t(ch) & 7u)) << 4) +
+                                 uint32_t(lane & 3) * 4u;
+            *reinterpret_cast<float *>(buf + off) = v[i] * inv;
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                &tmap),
+            "r"(int(c0)), "r"(b * C), "r"(smem_u32(buf))
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+}
+
+// The output's tensor map (2-D: n_cells x B*C floats, 128-byte swizzled
+// boxes of 32 cells x C channels), encoded through the driver entry point.
+static bool make_out_tmap(CUtensorMap *m, float *out, int64_t n_cells, int C, int B) {
+    using Fn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                            const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                            const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<Fn>(p);
+    }
+    if (!fn || (n_cells % 4) != 0 || C > 256 || (reinterpret_cast<uintptr_t>(out) & 15)) return false;
+    const cuuint64_t dims[2] = {cuuint64_t(n_cells), cuuint64_t(B) * C};
+    const cuuint64_t strides[1] = {cuuint64_t(n_cells) * 4};
+    const cuuint32_t box[2] = {cuuint32_t(kFinCells), cuuint32_t(C)};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // ---- plan layout -------------------------------------------------------------
@@ -685,7 +787,7 @@ __global__ void tile_plan_count_kernel(const uint32_t *__restrict__ total, int64
 
 static bool plan_supported(int N, int H, int W, int D, int64_t n_cells) {
     if (N < 1 || H < 1 || W < 1 || D < 1 || D > kTileMaxPoints) return false;
-    if (n_cells < 1 || n_cells >= (int64_t(1) << 32) - 1) return false;
+    if (n_cells < 1 || n_cells >= (int64_t(1) << 31) - 32) return false;
     const TileGeom g = tile_geom(N, H, W, D);
     return g.T < (int64_t(1) << 31) && g.tpc <= kTileMaxPoints &&
            g.hl_bits + g.d_bits <= 16;
@@ -765,19 +867,11 @@ static int run_tile_pool(const void *feats, const void *weights, const bvp_tile_
         }
         if (rc != BVP_OK) return rc;
     }
-    const int64_t nblk = ceil_div(p->n_cells, kFinCells) * B;
-    static int fin_per_sm[5] = {};
-    if (!fin_per_sm[CS]) {
-        int dev = 0, n = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tile_finalize_kernel<CS>, kPoolThreads, 0);
-        fin_per_sm[CS] = std::max(1, n) * sms;
-    }
     if (phases & 2)
-        tile_finalize_kernel<CS><<<unsigned(std::min<int64_t>(nblk, fin_per_sm[CS])), kPoolThreads, 0, s>>>(
-            rows, p->max_seg, at<const uint32_t>(p, L.csf), at<const uint32_t>(p, L.npts),
-            p->n_cells, C, B, mean, out);
+        tile_finalize_kernel<CS>
+            <<<dim3(unsigned(ceil_div(p->n_cells, kFinCells)), unsigned(B)), kPoolThreads, 0, s>>>(
+                rows, p->max_seg, at<const uint32_t>(p, L.csf), at<const uint32_t>(p, L.npts),
+                int(p->n_cells), C, mean, out);
     return check_launch("tile_pool");
 }
 

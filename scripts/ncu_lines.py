@@ -24,6 +24,8 @@ def main(path, kernel=None, top=20):
             hdr = next(csv.reader([ln]))
             ei = hdr.index("Instructions Executed")
             ai = hdr.index("Warp Stall Sampling (All Samples)")
+            stall_cols = [(i, h[6:]) for i, h in enumerate(hdr)
+                          if h.startswith("stall_") and "Not Issued" not in h]
             continue
         if hdr is None or not ln:
             continue
@@ -40,14 +42,16 @@ def main(path, kernel=None, top=20):
             except ValueError:
                 return 0.0
         if r[0].isdigit():
-            src[(fname, int(r[0]), r[1].strip()[:80])] = (f(r[ei]), f(r[ai]))
+            why = sorted(((f(r[i]), n) for i, n in stall_cols if i < len(r)), reverse=True)[:2]
+            src[(fname, int(r[0]), r[1].strip()[:80])] = (
+                f(r[ei]), f(r[ai]), " ".join(f"{n}:{v:.0f}" for v, n in why if v > 0))
         elif r[2]:
             sass[(r[2], r[3].strip()[:70])] = (f(r[ei]), f(r[ai]))
     te = sum(v[0] for v in src.values()) or 1
     ts = sum(v[1] for v in src.values()) or 1
     print(f"warp instructions {te:.0f}, stall samples {ts:.0f}")
-    for (fn, ln, s), (e, st) in sorted(src.items(), key=lambda kv: -kv[1][1])[:top]:
-        print(f"{fn}:{ln:<5d} exec {100 * e / te:5.1f}% stall {100 * st / ts:5.1f}%  {s}")
+    for (fn, ln, s), (e, st, why) in sorted(src.items(), key=lambda kv: -kv[1][1])[:top]:
+        print(f"{fn}:{ln:<5d} exec {100 * e / te:5.1f}% stall {100 * st / ts:5.1f}% [{why}]  {s}")
     ts2 = sum(v[1] for v in sass.values()) or 1
     print("--- SASS by stall")
     for (addr, s), (e, st) in sorted(sass.items(), key=lambda kv: -kv[1][1])[:top]:
