@@ -7,8 +7,13 @@
  *
  * Reference interfaces replaced (paths relative to the reference's
  * pkg/src/bevpool/):
- *   bvp_frustum_cells     generate_frustum + quantize_points
+ *   bvp_frustum_points    generate_frustum (geometry.py:162-191)
+ *   bvp_quantize_points   quantize_points (bevgrid.py:85-98)
+ *   bvp_frustum_cells     generate_frustum + quantize_points fused
  *                         (geometry.py:162-191, bevgrid.py:85-98)
+ *   bvp_interval_reduce_f32  _kernels.interval_reduce (_kernels.py:22-63),
+ *                         same arguments and bit-identical results
+ *   bvp_depth_distribution_check  check_depth_distribution (lift.py:52-63)
  *   bvp_sort_intervals    ranks_and_intervals (bevgrid.py:142-158)
  *   bvp_build_cache       build_cache minus the host fingerprint
  *                         (bevgrid.py:183-203)
@@ -70,6 +75,10 @@ extern "C" {
 #define BVP_SUM 0
 #define BVP_MEAN 1
 #define BVP_MAX 2
+/* MEAN as the reference's pool_naive computes it: the fp64 sum divided by the
+ * point count (pooling.py:152-156) instead of multiplied by 1/count
+ * (_kernels.py:57-60); exact mode only. */
+#define BVP_MEAN_DIV 3
 /* or-ed into mode of bvp_pool_forward_nhwc_f32: `out` was zero-filled by
  * bvp_pool_prepare_f32 since it was last written, so the zero fill is skipped */
 #define BVP_OUT_ZEROED 0x100
@@ -136,6 +145,17 @@ const char *bvp_last_error(void);
 int bvp_frustum_cells(const double *cams, int N, int H, int W, int D,
                       double depth_min, double depth_step, const double *grid,
                       int nx, int ny, uint32_t *cell_of_point, void *stream);
+
+/* generate_frustum (geometry.py:162-191): coords (N*H*W*D, 3) float64,
+ * device, row ((n*H + h)*W + w)*D + d, the reference's rounding (the
+ * OpenBLAS dgemm FMA chain of SURVEY §8c). */
+int bvp_frustum_points(const double *cams, int N, int H, int W, int D,
+                       double depth_min, double depth_step, double *coords, void *stream);
+
+/* quantize_points (bevgrid.py:85-98): coords (M, 3) float64 -> cells[M]
+ * uint32 (0xFFFFFFFF out of range).  grid: HOST, 7 float64. */
+int bvp_quantize_points(const double *coords, int64_t M, const double *grid, int nx, int ny,
+                        uint32_t *cells, void *stream);
 
 /* Workspace for bvp_sort_intervals / bvp_build_cache. */
 size_t bvp_sort_workspace_bytes(int64_t n_points, int64_t n_cells);
@@ -357,6 +377,28 @@ int bvp_pool_lifted_backward_f32(const float *grad_out,
                                  int64_t n_int_max, int mode, float *grad_x,
                                  void *workspace, size_t workspace_bytes,
                                  void *stream);
+
+/* ---- the reference's native kernel, as it is called ----------------------- */
+
+/* interval_reduce (_kernels.py:22-63) with the reference's own arguments:
+ * ranks[n_in], interval_starts[n_int], interval_cells[n_int] (the
+ * AssociationCache arrays), dist_t (N, H, W, D) f32 and feats_t (N, H, W, C)
+ * f32 (the transposes pooling.py:215-216 makes), out (C, n_cells) f32 --
+ * every interval's cell is written; other cells are left as they are (the
+ * reference pre-zeroes out, pooling.py:213).  mode BVP_SUM / MEAN / MAX.
+ * fp64 accumulation in rank order: bit-identical to the reference.  No
+ * workspace, no schedule; stream ordered. */
+int bvp_interval_reduce_f32(const uint32_t *ranks, const uint32_t *interval_starts,
+                            const uint32_t *interval_cells, int64_t n_in, int64_t n_int,
+                            const float *dist_t, const float *feats_t, float *out,
+                            int64_t n_cells, int H, int W, int D, int C, int mode,
+                            void *stream);
+
+/* check_depth_distribution (lift.py:52-63) statistics of dist (NB, D, H, W)
+ * f32: stats[0] = 1 if any entry is negative, stats[1] = the bits of the
+ * worst |sum_d p - 1| as a float64 (device, 2 x uint64). */
+int bvp_depth_distribution_check(const float *dist, int NB, int D, int H, int W,
+                                 unsigned long long *stats, void *stream);
 
 /* ---- pixel-column tiled pooling (the fast SUM / MEAN path) -------------- */
 

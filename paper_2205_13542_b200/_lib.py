@@ -15,7 +15,7 @@ from .errors import CudaError, ExtensionMissingError, from_status  # noqa: F401
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbevpool_sm100.so")
 
 BVP_OK, BVP_ERR_INVALID, BVP_ERR_UNSUPPORTED, BVP_ERR_CUDA = 0, 1, 2, 3
-BVP_SUM, BVP_MEAN, BVP_MAX = 0, 1, 2
+BVP_SUM, BVP_MEAN, BVP_MAX, BVP_MEAN_DIV = 0, 1, 2, 3
 TILE_CELLS = 32
 OUT_OF_RANGE = 0xFFFFFFFF
 BVP_OUT_ZEROED = 0x100  # include/bevpool_b200.h
@@ -57,6 +57,10 @@ SIGNATURES = {
     "bvp_abi_version": (_I, []),
     "bvp_last_error": (ctypes.c_char_p, []),
     "bvp_frustum_cells": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _I, _I, _P, _P]),
+    "bvp_frustum_points": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _P]),
+    "bvp_quantize_points": (_I, [_P, _L, _P, _I, _I, _P, _P]),
+    "bvp_interval_reduce_f32": (_I, [_P, _P, _P, _L, _L, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P]),
+    "bvp_depth_distribution_check": (_I, [_P, _I, _I, _I, _I, _P, _P]),
     "bvp_sort_workspace_bytes": (_S, [_L, _L]),
     "bvp_sort_intervals": (_I, [_P, _L, _L, _P, _P, _P, _P, _P, _P, _P, _S, _P]),
     "bvp_build_cache": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _I, _I, _P, _P, _P, _P, _P, _P,
@@ -142,5 +146,27 @@ def check(rc: int, what: str) -> None:
     raise from_status(rc, f"{what}: {load().bvp_last_error().decode(errors='replace')}")
 
 
+#: per-entry-point call counts while a ``counting()`` block is active (the
+#: analogue of the reference's debug.counting, debug.py:23-32: it proves the
+#: cached forward launches no geometry)
+_counts: dict | None = None
+
+
+class counting:
+    """Context manager: record how often each C entry point is called."""
+
+    def __enter__(self) -> dict:
+        global _counts
+        self._prev = _counts
+        _counts = {}
+        return _counts
+
+    def __exit__(self, *exc) -> None:
+        global _counts
+        _counts = self._prev
+
+
 def call(name: str, *args) -> None:
+    if _counts is not None:
+        _counts[name] = _counts.get(name, 0) + 1
     check(getattr(load(), name)(*args), name)

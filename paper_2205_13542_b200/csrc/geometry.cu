@@ -57,11 +57,12 @@ __device__ __forceinline__ double floor_div(double a, const GridParams &g) {
     return floor(__ddiv_rn(a, g.r));
 }
 
-__device__ __forceinline__ uint32_t cell_at(const double *__restrict__ c, const FrustumParams &f,
-                                            const GridParams &g, double dx, double dy, int d) {
+// Ego coordinates of frustum point (pixel ray dx, dy; depth bin d) --
+// generate_frustum's rounding (geometry.py:184-186 through OpenBLAS dgemm).
+__device__ __forceinline__ void ego_at(const double *__restrict__ c, const FrustumParams &f,
+                                       double dx, double dy, int d, double (&e)[3]) {
     const double depth = __dadd_rn(f.d_min, __dmul_rn(f.d_step, static_cast<double>(d)));
     const double px = __dmul_rn(dx, depth), py = __dmul_rn(dy, depth), pz = depth;
-    double e[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
         double acc = __dmul_rn(__ldg(c + 4 + 3 * j), px);
@@ -69,6 +70,10 @@ __device__ __forceinline__ uint32_t cell_at(const double *__restrict__ c, const 
         acc = __fma_rn(__ldg(c + 6 + 3 * j), pz, acc);
         e[j] = __dadd_rn(acc, __ldg(c + 13 + j));
     }
+}
+
+// quantize_points (bevgrid.py:85-98): flat cell id of an ego point.
+__device__ __forceinline__ uint32_t quantize_ego(const double (&e)[3], const GridParams &g) {
     if (!(e[2] >= g.z_min && e[2] < g.z_max)) return kOOR;
     const double qx = floor_div(__dsub_rn(e[0], g.x_min), g);
     const double qy = floor_div(__dsub_rn(e[1], g.y_min), g);
@@ -76,6 +81,13 @@ __device__ __forceinline__ uint32_t cell_at(const double *__restrict__ c, const 
         qy < static_cast<double>(g.ny))
         return static_cast<uint32_t>(static_cast<int64_t>(qx) * g.ny + static_cast<int64_t>(qy));
     return kOOR;
+}
+
+__device__ __forceinline__ uint32_t cell_at(const double *__restrict__ c, const FrustumParams &f,
+                                            const GridParams &g, double dx, double dy, int d) {
+    double e[3];
+    ego_at(c, f, dx, dy, d, e);
+    return quantize_ego(e, g);
 }
 
 // The ray of pixel (h, w) of a camera: dx = (w - cx)/fx, dy = (h - cy)/fy.
@@ -98,6 +110,36 @@ __device__ __forceinline__ uint32_t point_cell(const double *__restrict__ cams,
     double dx, dy;
     pixel_ray(c, h, w, dx, dy);
     return cell_at(c, f, g, dx, dy, d);
+}
+
+// generate_frustum: coords[p] = ego (x, y, z) of point p, (P, 3) fp64.
+__global__ void frustum_points_kernel(const double *__restrict__ cams, FrustumParams f, int64_t P,
+                                      double *__restrict__ coords) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int d = static_cast<int>(p % f.D);
+        int64_t rest = p / f.D;
+        const int w = static_cast<int>(rest % f.W);
+        rest /= f.W;
+        const int h = static_cast<int>(rest % f.H);
+        const int n = static_cast<int>(rest / f.H);
+        const double *c = cams + 16 * n;
+        double dx, dy, e[3];
+        pixel_ray(c, h, w, dx, dy);
+        ego_at(c, f, dx, dy, d, e);
+        coords[3 * p] = e[0];
+        coords[3 * p + 1] = e[1];
+        coords[3 * p + 2] = e[2];
+    }
+}
+
+__global__ void quantize_points_kernel(const double *__restrict__ coords, int64_t M, GridParams g,
+                                       uint32_t *__restrict__ cells) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double e[3] = {coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]};
+        cells[i] = quantize_ego(e, g);
+    }
 }
 
 __global__ void frustum_cells_kernel(const double *__restrict__ cams, FrustumParams f,
@@ -775,6 +817,28 @@ int bvp_frustum_cells(const double *cams, int N, int H, int W, int D, double dep
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), 148 * 64));
     frustum_cells_kernel<<<blocks, 256, 0, as_stream(stream)>>>(cams, f, g, P, cell_of_point);
     return check_launch("frustum_cells");
+}
+
+int bvp_frustum_points(const double *cams, int N, int H, int W, int D, double depth_min,
+                       double depth_step, double *coords, void *stream) {
+    BVP_REQUIRE(cams && coords, BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(N > 0 && H > 0 && W > 0 && D > 0, BVP_ERR_INVALID, "frustum dims must be positive");
+    const FrustumParams f{N, H, W, D, depth_min, depth_step};
+    const int64_t P = int64_t(N) * H * W * D;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), 148 * 64));
+    frustum_points_kernel<<<blocks, 256, 0, as_stream(stream)>>>(cams, f, P, coords);
+    return check_launch("frustum_points");
+}
+
+int bvp_quantize_points(const double *coords, int64_t M, const double *grid, int nx, int ny,
+                        uint32_t *cells, void *stream) {
+    BVP_REQUIRE(M == 0 || (coords && cells), BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(grid && nx > 0 && ny > 0, BVP_ERR_INVALID, "bad grid");
+    if (M == 0) return BVP_OK;
+    const GridParams g = grid_params(grid, nx, ny);
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ceil_div(M, 256), 148 * 64));
+    quantize_points_kernel<<<blocks, 256, 0, as_stream(stream)>>>(coords, M, g, cells);
+    return check_launch("quantize_points");
 }
 
 size_t bvp_sort_workspace_bytes(int64_t n_points, int64_t n_cells) {

@@ -123,7 +123,7 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
     p.nx = nx;
     p.ny = ny;
     p.n_cells = int64_t(nx) * ny;
-    p.mean = mode == BVP_MEAN;
+    p.mean = mode == BVP_MEAN ? 1 : mode == BVP_MEAN_DIV ? 2 : 0;
     return p;
 }
 
@@ -294,7 +294,8 @@ static int pool_forward_nhwc(const float *feats_nhwc, const float *dist, const u
     BVP_REQUIRE(B >= 1 && N >= 1 && C >= 0 && H >= 1 && W >= 1 && D >= 1 && nx >= 1 && ny >= 1,
                 BVP_ERR_INVALID, "bad dims B=%d N=%d C=%d H=%d W=%d D=%d nx=%d ny=%d", B, N, C,
                 H, W, D, nx, ny);
-    BVP_REQUIRE(mode >= 0 && mode <= 2, BVP_ERR_INVALID, "bad mode %d", mode);
+    BVP_REQUIRE(mode >= 0 && mode <= 2 || (mode == BVP_MEAN_DIV && exact), BVP_ERR_INVALID,
+                "bad mode %d", mode);
     BVP_REQUIRE(C == 0 || (out && feats_nhwc && dist && ranks && interval_starts &&
                            interval_cells && cell_first && schedule &&
                            ((schedule->units && schedule->counts) || schedule->work)),

@@ -220,7 +220,8 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
 #pragma unroll
                     for (int x = 0; x < VEC; ++x) {
                         const int c = ch * VEC + x;
-                        out[int64_t(c) * P.n_cells] = static_cast<float>(acc[k][x] * inv);
+                        out[int64_t(c) * P.n_cells] = static_cast<float>(
+                            P.mean == 2 ? acc[k][x] / Acc(len) : acc[k][x] * inv);
                         if (ARG && P.argmax)
                             P.argmax[(b * P.n_int_max + r.w) * C + c] =
                                 __ldg(P.ranks + arg[ARG ? k : 0][ARG ? x : 0]);

@@ -332,7 +332,8 @@ pool_unit_kernel(const PoolParams P) {
 #pragma unroll
                 for (int x = 0; x < VEC; ++x) {
                     const int c = ch * VEC + x;
-                    s_tile[c * kUnitPitch + lc] = static_cast<float>(acc[q][x] * inv);
+                    s_tile[c * kUnitPitch + lc] = static_cast<float>(
+                        P.mean == 2 ? acc[q][x] / Acc(hi - lo) : acc[q][x] * inv);
                     if (IS_MAX && P.argmax)
                         P.argmax[(b * P.n_int_max + iv) * C + c] =
                             __ldg(P.ranks + arg[IS_MAX ? q : 0][IS_MAX ? x : 0]);
@@ -573,7 +574,8 @@ pool_exact_long_kernel(const PoolParams P) {
     for (int a = 0; a < A; ++a) {
         const int c = tid + a * kPoolThreads;
         if (c >= C) break;
-        out[int64_t(c) * P.n_cells] = static_cast<float>(acc[a] * inv);
+        out[int64_t(c) * P.n_cells] =
+            static_cast<float>(P.mean == 2 ? acc[a] / double(hi - lo) : acc[a] * inv);
         if (IS_MAX && P.argmax) P.argmax[(b * P.n_int_max + iv) * C + c] = __ldg(P.ranks + arg[a]);
     }
 }

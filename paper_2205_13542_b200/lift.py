@@ -66,3 +66,27 @@ def point_weight(dist, n: int, h: int, w: int, d: int) -> float:
         if not 0 <= value < bound:
             raise IndexError(f"{name} index {value} out of range [0, {bound})")
     return float(dist[n, d, h, w])
+
+
+def check_depth_distribution(dist, tol: float = 1e-6) -> None:
+    """Raise ValidationError unless ``dist`` (N, D, H, W) holds per-pixel
+    distributions: no negative entry, every pixel's D probabilities summing
+    to 1 within ``tol`` (reference lift.py:52-63).  The scan runs on the
+    GPU (bvp_depth_distribution_check, fp64 sums)."""
+    if len(dist.shape) != 4:
+        raise ValidationError(f"distribution must be (N, D, H, W), got {tuple(dist.shape)}")
+    host = isinstance(dist, np.ndarray)
+    t = (torch.from_numpy(np.ascontiguousarray(dist, dtype=np.float32)).to(cuda_device()) if host
+         else dist.float().contiguous())
+    N, D, H, W = (int(v) for v in t.shape)
+    if t.numel() == 0:
+        return
+    stats = torch.zeros(2, dtype=torch.int64, device=t.device)
+    _lib.call("bvp_depth_distribution_check", ptr(t), N, D, H, W, ptr(stats), stream_ptr(t.device))
+    neg, dev_bits = stats.tolist()
+    worst = float(np.array([dev_bits], dtype=np.int64).view(np.float64)[0])
+    if neg:
+        raise ValidationError("distribution has negative entries")
+    if worst > tol:
+        raise ValidationError(
+            f"per-pixel depth probabilities must sum to 1 (worst deviation {worst:.3e})")

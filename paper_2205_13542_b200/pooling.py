@@ -60,7 +60,7 @@ def _scratch(cache: AssociationCache, B: int, C: int, mode: int) -> tuple:
     t = cache.scratch(B, C, mode)
     return (None, 0) if t is None else (ptr(t), t.numel())
 
-BACKENDS = ("prefixsum", "interval")
+BACKENDS = ("naive", "prefixsum", "interval")
 
 #: widest channel count of the tiled path (csrc/tile.cu: 4 x 32 lanes)
 TILE_MAX_C = 128
@@ -486,7 +486,61 @@ class PoolPlan:
         return 4 * self.out.numel()
 
 
-_BACKEND_FN = {"prefixsum": pool_prefixsum, "interval": pool_interval}
+def pool_naive(features, dist, cache: AssociationCache, grid: BevGridSpec,
+               reducer=Reducer.SUM, *, check_finite: bool = True) -> BevFeatureMap:
+    """The reference's scatter backend (pooling.py:135-159) -- its results,
+    on the GPU: every cell sums its points' fp64 products in original point
+    order (which is rank order within a cell), MEAN divides by the count,
+    MAX keeps the largest product.  Runs the exact-mode interval kernels;
+    bit-identical to the reference's pool_naive."""
+    reducer = _reducer(reducer)
+    inp = _check_inputs(features, dist, cache, grid, check_finite)
+    cache = cache.for_grid(grid)
+    out = torch.empty((inp.B, inp.C, grid.n_cells), dtype=torch.float32, device=inp.feats.device)
+    if inp.C:
+        mode = _lib.BVP_MEAN_DIV if reducer is Reducer.MEAN else _MODE[reducer]
+        nhwc = torch.empty(inp.feats.numel(), dtype=torch.float32, device=inp.feats.device)
+        _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
+                  ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
+                  ptr(cache.d_cell_first),
+                  cache.schedule(inp.N, inp.H, inp.W, inp.D,
+                                 units=cache.needs_units(inp.C, exact=True), exact=True),
+                  inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
+                  grid.nx, grid.ny, cache.n_int_max, mode, 1, ptr(out), ptr(nhwc), None,
+                  *_scratch(cache, inp.B, inp.C, _MODE[reducer]), stream_ptr(inp.feats.device))
+    return _finish(out, inp, grid)
+
+
+_BACKEND_FN = {"naive": pool_naive, "prefixsum": pool_prefixsum, "interval": pool_interval}
+
+_PARALLELISM = [0]
+
+
+def set_parallelism(n: int | None = None) -> int:
+    """The reference sizes its CPU worker pool here (_threads.py:42-53).  The
+    CUDA path has no host worker pool, so the count only records the
+    request; it returns the count in effect like the reference (None reads
+    BEVPOOL_THREADS, 0 = one per CPU)."""
+    import os
+    if n is None:
+        raw = os.environ.get("BEVPOOL_THREADS", "0")
+        try:
+            n = int(raw)
+        except ValueError:
+            raise ConfigurationError(
+                f"BEVPOOL_THREADS must be a non-negative integer, got {raw!r}") from None
+        if n < 0:
+            raise ConfigurationError(f"BEVPOOL_THREADS must be >= 0, got {n}")
+    if n == 0:
+        n = os.cpu_count() or 1
+    _PARALLELISM[0] = max(1, int(n))
+    return _PARALLELISM[0]
+
+
+def get_parallelism() -> int:
+    if not _PARALLELISM[0]:
+        set_parallelism()
+    return _PARALLELISM[0]
 
 
 def pool(features, dist, cache, grid, reducer=Reducer.SUM, backend: str = "interval",

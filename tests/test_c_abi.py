@@ -60,3 +60,54 @@ def test_c_host_pipeline_matches_oracle(tmp_path):
     want = o.pool_interval(feats, dist, ranks, starts, icells, NX * NY, "sum")
     np.testing.assert_array_equal(load("out_exact", np.float32).reshape(want.shape), want)
     assert o.max_rel_dev(want, load("out_fast", np.float32).reshape(want.shape)) <= 1e-5
+
+
+def build_interval_reduce(tmp_path):
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    lib_dir = os.path.join(ROOT, "paper_2205_13542_b200")
+    exe = str(tmp_path / "c_abi_interval_reduce")
+    cmd = ["gcc", "-O2", "-std=c11", os.path.join(ROOT, "examples", "c_abi_interval_reduce.c"),
+           "-I", os.path.join(ROOT, "include"), "-I", f"{CUDA}/include",
+           "-L", lib_dir, "-lbevpool_sm100", "-L", f"{CUDA}/lib64", "-lcudart",
+           f"-Wl,-rpath,{lib_dir}", f"-Wl,-rpath,{CUDA}/lib64", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_interval_reduce_host_compiles(tmp_path):
+    if not os.path.exists(os.path.join(ROOT, "paper_2205_13542_b200", "libbevpool_sm100.so")):
+        pytest.skip("library not built")
+    assert os.path.exists(build_interval_reduce(tmp_path))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["T", "S"])
+def test_c_interval_reduce_with_reference_arrays(tmp_path, name):
+    """bvp_interval_reduce_f32 called from C with nothing but the
+    reference's cache arrays and its transposed inputs is bit-identical to
+    the reference's interval_reduce (the oracle restatement, itself pinned
+    to the reference's digests) for SUM, MEAN and MAX."""
+    exe = build_interval_reduce(tmp_path)
+    cfg = o.CONFIGS[name]
+    cache = o.build_cache(cfg)
+    feats, logits = o.gen_inputs(cfg.n_cameras, cfg.channels, cfg.height, cfg.width,
+                                 cfg.depth_bins, 0)
+    dist = o.normalize_depth(logits)
+    arrays = {"ranks": cache["ranks"], "starts": cache["interval_starts"],
+              "icells": cache["interval_cells"],
+              "dist_t": np.ascontiguousarray(dist.transpose(0, 2, 3, 1)),
+              "feats_t": np.ascontiguousarray(feats.transpose(0, 2, 3, 1))}
+    for k, v in arrays.items():
+        v.tofile(tmp_path / f"{k}.bin")
+    n_cells = cfg.n_cells
+    res = subprocess.run([exe, str(tmp_path), str(len(cache["ranks"])),
+                          str(len(cache["interval_starts"])), str(n_cells), str(cfg.height),
+                          str(cfg.width), str(cfg.depth_bins), str(cfg.channels),
+                          str(cfg.n_cameras)], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
+    for red in ("sum", "mean", "max"):
+        want = o.pool_interval(feats, dist, cache["ranks"], cache["interval_starts"],
+                               cache["interval_cells"], n_cells, red)
+        got = np.fromfile(tmp_path / f"out_{red}.bin", dtype=np.float32).reshape(want.shape)
+        np.testing.assert_array_equal(got, want)

@@ -468,10 +468,15 @@ def test_fast_mode_high_res_config():
                            cache.interval_cells, grid.n_cells, "sum")
     got = bp.pool_interval(features, dist, cache, grid, exact=False).values
     assert max_rel_dev(want, got.reshape(want.shape)) <= FP32_TOL
-    builder = bp.CacheBuilder(spec.n_cameras, spec.frustum, grid)
+    builder = bp.CacheBuilder(spec.n_cameras, spec.frustum, grid, tiles=True)
     c2 = builder.build(torch.from_numpy(bp.rig_rows(rig)).cuda())
     got2 = bp.pool_interval(features, dist, c2, grid, exact=False).values
-    assert np.array_equal(got, got2)  # capacity-bounded schedule, same result
+    assert np.array_equal(got, got2)  # per-frame tile plan (capacity-bounded), same result
+    # per-frame caches without a tile plan pool with the interval kernels
+    c3 = bp.CacheBuilder(spec.n_cameras, spec.frustum, grid).build(
+        torch.from_numpy(bp.rig_rows(rig)).cuda())
+    got3 = bp.pool_interval(features, dist, c3, grid, exact=False).values
+    assert max_rel_dev(want, got3.reshape(want.shape)) <= FP32_TOL
 
 
 def test_fast_mode_batched_and_deterministic():
@@ -536,8 +541,9 @@ def test_per_frame_build_defers_units():
     assert lazy._units_pending is not None
     fast = bp.pool_interval(feats, dist, lazy, grid, exact=False).values
     assert lazy._units_pending is not None  # fast path did not need them
-    np.testing.assert_array_equal(fast, bp.pool_interval(feats, dist, eager, grid,
-                                                         exact=False).values)
+    # (the eager cache pools through the tile plan: a different fp32 order)
+    assert max_rel_dev(bp.pool_interval(feats, dist, eager, grid, exact=True).values,
+                       fast) <= FP32_TOL
     ex = bp.pool_interval(feats, dist, lazy, grid, exact=True).values
     assert lazy._units_pending is not None
     np.testing.assert_array_equal(ex, bp.pool_interval(feats, dist, eager, grid,
@@ -582,10 +588,11 @@ def test_run_uncached_matches_cached_pool():
     rig, feats_np, logits_np, grid = bp.gen_workload(spec)
     feats = torch.from_numpy(feats_np).cuda()[None]
     dist = bp.normalize_depth(torch.from_numpy(logits_np).cuda())[None]
-    builder = bp.CacheBuilder(spec.n_cameras, f, grid)
+    builder = bp.CacheBuilder(spec.n_cameras, f, grid, tiles=True)
     cams = torch.from_numpy(bp.rig_rows(rig)).cuda()
     plan = bp.PoolPlan(builder.build(cams), grid, spec.n_cameras, spec.channels, f.height,
                        f.width, f.depth_bins, 1, bp.Reducer.SUM)
+    assert plan.tiled
     got = plan.run_uncached(builder, cams, feats, dist).cpu().numpy()
     want = bp.pool_interval(feats_np, bp.normalize_depth(logits_np),
                             bp.build_cache(rig, f, grid), grid).values
