@@ -57,6 +57,10 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="S", choices=["S", "B", "H"],
+                    help="S: cached forward, 1 sample/GPU (the headline); B: training step "
+                         "(forward + backward), batch 4/GPU; H: high-res frame with the "
+                         "association rebuilt every step, 1 sample/GPU")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -283,7 +287,8 @@ def main():
     import paper_2205_13542_b200 as bp
     from paper_2205_13542_b200.bevgrid import ptr, stream_ptr  # noqa: F401
 
-    from paper_2205_13542_b200.shard import max_over_ranks, sample_seeds
+    from paper_2205_13542_b200.shard import (gather_maps, gather_scalars, max_over_ranks,
+                                             sample_seeds)
 
     rank, world, local = dist_env()
     # one process per GPU; BVP_BENCH_BACKEND=gloo + more ranks than GPUs is
@@ -297,6 +302,9 @@ def main():
             tdist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.config != "S":
+        run_config_bh(args, bp, torch, tdist, dev, rank, world, local)
+        return
     spec = bp.CONFIGS[CONFIG_NAME]
     f = spec.frustum
     P = spec.n_points
@@ -371,6 +379,26 @@ def main():
     t0 = time.perf_counter()
     plan.run_frames(frames, [h_out[k & 1] for k in range(K)])
     e2e_tot = 1e3 * (time.perf_counter() - t0)
+    per_rank_ms = [t / K for t in gather_scalars(tot_ms, dev)]
+    multi = None
+    if world > 1:
+        # verification outside the timed region: every rank's map to rank 0,
+        # which recomputes each sample in one process and compares the bits
+        plan.run(feats, dist)
+        full = gather_maps(plan.out.view(1, spec.channels, grid.nx, grid.ny).clone(), world)
+        if rank == 0:
+            same = []
+            for r in range(world):
+                (sd,) = sample_seeds(world, r, world)
+                _, fr, lr, _ = bp.gen_workload(
+                    bp.WorkloadSpec(spec.n_cameras, f, spec.grid, spec.channels, sd))
+                ft = torch.from_numpy(fr).to(dev)[None]
+                dt = bp.normalize_depth(torch.from_numpy(lr).to(dev))[None]
+                want = plan.run(ft, dt).view(spec.channels, grid.nx, grid.ny)
+                same.append(bool(torch.equal(full[r].to(dev), want)))
+            multi = {"per_rank_step_ms": per_rank_ms,
+                     "gathered_maps_bit_identical_to_single_process": all(same),
+                     "collective_backend": tdist.get_backend()}
     tot_ms = max_over_ranks(tot_ms, dev)
     e2e_tot = max_over_ranks(e2e_tot, dev)
 
@@ -438,6 +466,8 @@ def main():
         "gpu_launches": LAUNCHES_PER_STEP * K * world,
         "clocks": clk,
     }
+    if multi is not None:
+        line["multi_rank"] = multi
     if world == 1 and not args.no_cpu_baseline:
         times, threads, kind = time_cpu_reference(spec, args.cpu_seconds)
         v = P * len(times) / sum(times)
@@ -450,6 +480,98 @@ def main():
     if variants:
         line["variants"] = variants
     print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# configs B and H under the same launcher (batch-sharded, weak scaling)
+# ---------------------------------------------------------------------------
+
+def run_config_bh(args, bp, torch, tdist, dev, rank, world, local):
+    """B: the training step -- forward + gather backward through the
+    autograd op, batch 4 per GPU (samples rank*4 .. rank*4+3).  H: one
+    high-res sample per GPU with the association rebuilt every step
+    (CacheBuilder + PoolPlan.run_uncached).  Inputs resident in HBM, L2
+    flushed before every step, CUDA events, max over ranks."""
+    from paper_2205_13542_b200.shard import gather_scalars, max_over_ranks, sample_seeds
+
+    name = args.config
+    spec = bp.CONFIGS["S" if name == "B" else "H"]
+    f = spec.frustum
+    B_local = 4 if name == "B" else 1
+    seeds = sample_seeds(world * B_local, rank, world)
+    rig, _, _, grid = bp.gen_workload(spec)
+    feats, dists = [], []
+    for sd in seeds:
+        _, fr, lr, _ = bp.gen_workload(bp.WorkloadSpec(spec.n_cameras, f, spec.grid,
+                                                       spec.channels, sd))
+        feats.append(torch.from_numpy(fr))
+        dists.append(bp.normalize_depth(torch.from_numpy(lr).to(dev)).cpu())
+    F = torch.stack(feats).to(dev)
+    Dd = torch.stack(dists).to(dev)
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    if name == "B":
+        cache = bp.build_cache(rig, f, grid, device=dev)
+        Fg = F.clone().requires_grad_(True)
+        Dg = Dd.clone().requires_grad_(True)
+        g = torch.randn((B_local, spec.channels, grid.nx, grid.ny), device=dev)
+
+        def step():
+            Fg.grad = None
+            Dg.grad = None
+            bp.bev_pool(Fg, Dg, cache, grid).backward(g)
+        launches = None
+    else:
+        builder = bp.CacheBuilder(spec.n_cameras, f, grid, dev)
+        cams = torch.from_numpy(bp.rig_rows(rig)).to(dev)
+        plan = bp.PoolPlan(builder.build(cams), grid, spec.n_cameras, spec.channels, f.height,
+                           f.width, f.depth_bins, 1, bp.Reducer.SUM, False, dev)
+
+        def step():
+            plan.run_uncached(builder, cams, F, Dd)
+        launches = None
+    stream = torch.cuda.current_stream(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step()
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize(dev)
+    for k in range(K):
+        flush.zero_()
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        tdist.barrier()
+    step_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    clk = clocks.stop()
+    per_rank = [t / K for t in gather_scalars(sum(step_ms), dev)]
+    tot_ms = max_over_ranks(sum(step_ms), dev)
+    if rank == 0:
+        P = spec.n_points
+        what = ("training step: forward + gather backward (autograd), batch 4 per GPU"
+                if name == "B" else
+                "high-res frame: association rebuilt every step + forward, 1 sample per GPU")
+        cfg = config_dict(spec)
+        cfg.update({"workload": f"config {name} ({what})", "batch_per_gpu": B_local})
+        line = {"metric": METRIC, "value": world * B_local * P * K / (tot_ms * 1e-3),
+                "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, args.warmup),
+                "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference gen_workload)",
+                "config": cfg,
+                "parallelism": f"batch-sharded x{world}, no collective in the step",
+                "timing": "CUDA events, L2 flushed (512 MiB write) before every step, max over ranks",
+                "latency_ms": {"step_median": statistics.median(step_ms),
+                               "per_rank_step_ms": per_rank},
+                "e2e": None, "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
 

@@ -387,6 +387,9 @@ tile_pool_kernel(TilePoolArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // the first RPT records of each thread are loaded now, beside the staging
     // (records [0, RPT * 256) cover the whole tile at the nuScenes shape)
+    // distributed shared memory may be written only once every CTA of the
+    // cluster is running: arrive now, wait just before the first remote store
+    if (CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     constexpr int RPT = 8;
     const uint32_t *rt = a.rec + t * g.tpc;
     uint32_t pre[RPT];
@@ -448,6 +451,7 @@ tile_pool_kernel(TilePoolArgs a) {
                 }
             }
         };
+        if (CL > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
         stage(a.feats, C, nb * C * HW + col, rfs, FS);
         stage(a.weights, D, nb * D * HW + col, rpw, PD);
         // channel quads past C up to CP: zero (no quad holds both)

@@ -54,6 +54,16 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def gather_scalars(value: float, device=None) -> list[float]:
+    """Every rank's scalar (e.g. its device-timed step), in rank order."""
+    if not _initialized() or tdist.get_world_size() == 1:
+        return [float(value)]
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
+    bufs = [torch.empty_like(t) for _ in range(tdist.get_world_size())]
+    tdist.all_gather(bufs, t)
+    return [float(b.item()) for b in bufs]
+
+
 def sum_over_ranks(value: float, device=None) -> float:
     if not _initialized() or tdist.get_world_size() == 1:
         return float(value)
@@ -69,6 +79,8 @@ def gather_maps(local: torch.Tensor, n_samples: int) -> torch.Tensor | None:
     if not _initialized() or tdist.get_world_size() == 1:
         return local
     world, rank = tdist.get_world_size(), tdist.get_rank()
+    if tdist.get_backend() == "gloo":
+        local = local.cpu()  # gloo gathers host tensors
     sizes = [shard_range(n_samples, r, world) for r in range(world)]
     cap = max(hi - lo for lo, hi in sizes)
     pad = torch.zeros((cap, *local.shape[1:]), dtype=local.dtype, device=local.device)

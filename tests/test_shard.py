@@ -65,14 +65,28 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank: int, world: int, port: int, n_samples: int, out_path: str):
+def _pool_sample_cuda(seed: int) -> np.ndarray:
+    """The same sample pooled by the CUDA path (exact mode: the reference's
+    bits, so the oracle's single-process result must match exactly)."""
+    import paper_2205_13542_b200 as bp
+    spec = bp.CONFIGS["T"]
+    rig, f, lg, grid = bp.gen_workload(bp.WorkloadSpec(spec.n_cameras, spec.frustum, spec.grid,
+                                                       spec.channels, seed))
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    return bp.pool_interval(f, o.normalize_depth(lg), cache, grid, exact=True).values
+
+
+def _worker(rank: int, world: int, port: int, n_samples: int, out_path: str,
+            cuda: bool = False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cfg = o.CONFIGS["T"]
         cache = o.build_cache(cfg)  # deterministic: identical on every rank
-        local = [_pool_sample(s, cache) for s in sample_seeds(n_samples, rank, world)]
+        seeds = sample_seeds(n_samples, rank, world)
+        local = ([_pool_sample_cuda(s) for s in seeds] if cuda else
+                 [_pool_sample(s, cache) for s in seeds])
         block = torch.from_numpy(np.stack(local)).reshape(len(local), cfg.channels, cfg.nx, cfg.ny)
         full = gather_maps(block, n_samples)
         t_max = max_over_ranks(1.0 + rank)
@@ -97,6 +111,19 @@ def test_two_rank_gather_matches_single_process(tmp_path, n_samples):
     want = np.stack([_pool_sample(s, cache) for s in range(n_samples)])
     assert full.shape == (n_samples, cfg.channels, cfg.nx, cfg.ny)
     assert np.array_equal(full.reshape(want.shape), want)  # bit-identical: shards are independent
+
+
+@pytest.mark.gpu
+def test_two_rank_cuda_pooling_gather_matches_single_process(tmp_path):
+    """Both ranks pool through the CUDA path (sharing the one GPU), gloo
+    gathers the maps: bit-identical to the single-process oracle."""
+    out_path = str(tmp_path / "full.npy")
+    mp.spawn(_worker, args=(2, _free_port(), 4, out_path, True), nprocs=2, join=True)
+    full = np.load(out_path)
+    cfg = o.CONFIGS["T"]
+    cache = o.build_cache(cfg)
+    want = np.stack([_pool_sample(s, cache) for s in range(4)])
+    assert np.array_equal(full.reshape(want.shape), want)
 
 
 def test_single_process_helpers_are_identity():
