@@ -348,6 +348,21 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context,
                         float *out, void *workspace, size_t workspace_bytes,
                         void *scratch, size_t scratch_bytes, void *stream);
 
+/* Backward of the fused path (SUM / MEAN): grad_out (B,C,nx*ny) f32 ->
+ * grad_logits (B,N,D,H,W) and grad_context (B,N,C,H,W), bf16 like the
+ * inputs.  The softmax is recomputed from the logits (fp32), the gather
+ * backward gives grad_context and dL/dw, the softmax Jacobian gives
+ * dL/dlogits.  No atomics; deterministic.  workspace:
+ * bvp_fused_backward_workspace_bytes. */
+size_t bvp_fused_backward_workspace_bytes(int B, int N, int C, int H, int W, int D,
+                                          int64_t n_int_max);
+int bvp_fused_backward_bf16(const float *grad_out, const uint16_t *logits, const uint16_t *context,
+                            const uint32_t *interval_starts, const uint32_t *interval_cells,
+                            const uint32_t *cell_first, const uint32_t *interval_of_point, int B,
+                            int N, int C, int H, int W, int D, int nx, int ny, int64_t n_int_max,
+                            int mode, uint16_t *grad_logits, uint16_t *grad_context,
+                            void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- gather backward (config B) ---------------------------------------- */
 
 /* Workspace: per-interval gradient rows (B, n_int_max, C) f32. */

@@ -364,6 +364,22 @@ def fused_pool(features_bf16_as_f32, logits_bf16_as_f32, ranks, starts,
                          n_cells, mode)
 
 
+def fused_backward(ctx_bf16_as_f32, logits_bf16_as_f32, cell_of_point, grad_out, ranks,
+                   starts, icells, mode="sum"):
+    """fp64 gradient of pool(softmax_D(logits) (x) context) (the fused path)
+    w.r.t. logits and context: the pooling adjoint (pool_backward) on the
+    fp64 softmax, then the softmax Jacobian
+    dL/dl[d] = w[d] (dL/dw[d] - sum_d' w[d'] dL/dw[d']).
+    Returns (grad_logits (N,D,H,W), grad_context (N,C,H,W)) as float64."""
+    x = np.asarray(logits_bf16_as_f32, dtype=np.float64)
+    e = np.exp(x - x.max(axis=1, keepdims=True))
+    w = e / e.sum(axis=1, keepdims=True)
+    gc, gw = pool_backward(ctx_bf16_as_f32, w, cell_of_point, grad_out, ranks, starts, icells,
+                           mode)
+    s = (w * gw).sum(axis=1, keepdims=True)
+    return w * (gw - s), gc
+
+
 def max_rel_dev(reference, candidate) -> float:
     """max |a-b| / max(1, |a|) -- the reference suite's metric
     (tests/conftest.py:68-74 of the reference)."""

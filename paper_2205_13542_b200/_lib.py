@@ -94,6 +94,9 @@ SIGNATURES = {
     "bvp_fused_pool_bf16": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
                                  _I, _P, _P, _S, _P, _S, _P]),
     "bvp_backward_workspace_bytes": (_S, [_I, _I, _L]),
+    "bvp_fused_backward_workspace_bytes": (_S, [_I, _I, _I, _I, _I, _I, _L]),
+    "bvp_fused_backward_bf16": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I,
+                                     _L, _I, _P, _P, _P, _S, _P]),
     "bvp_pool_backward_f32": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I,
                                    _I, _L, _I, _P, _P, _P, _S, _P]),
     "bvp_pool_lifted_backward_f32": (_I, [_P, _P, _P, _P, _P, _I, _L, _I, _I, _L, _I, _P, _P,

@@ -82,3 +82,55 @@ def bev_pool(features: torch.Tensor, dist: torch.Tensor, cache: AssociationCache
 
 def bev_pool_map(features, dist, cache, grid, reducer=Reducer.SUM) -> BevFeatureMap:
     return BevFeatureMap(bev_pool(features, dist, cache, grid, reducer), grid)
+
+
+class _FusedPoolFn(torch.autograd.Function):
+    """pool(softmax_D(logits) (x) context), bf16 in: the tiled fused forward
+    (csrc/tile.cu, softmax in shared memory) and the fused backward
+    (bvp_fused_backward_bf16)."""
+
+    @staticmethod
+    def forward(ctx, logits, context, cache: AssociationCache, grid: BevGridSpec,
+                reducer: Reducer):
+        from .pooling import pool_fused
+        out = pool_fused(logits, context, cache, grid, reducer).values
+        ctx.cache, ctx.grid, ctx.reducer = cache, grid, reducer
+        ctx.save_for_backward(logits, context)
+        return out.view(logits.shape[0], context.shape[2], grid.n_cells)
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        logits, context = ctx.saved_tensors
+        cache, grid = ctx.cache, ctx.grid
+        B, N, D, H, W = logits.shape
+        C = context.shape[2]
+        dev = grad_out.device
+        g = grad_out.float().contiguous()
+        gl = torch.empty_like(logits)
+        gc = torch.empty_like(context)
+        ws = torch.empty(int(_lib.load().bvp_fused_backward_workspace_bytes(
+            B, N, C, H, W, D, cache.n_int_max)), dtype=torch.uint8, device=dev)
+        _lib.call("bvp_fused_backward_bf16", ptr(g), ptr(logits), ptr(context),
+                  ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
+                  ptr(cache.d_cell_first), ptr(cache.d_interval_of_point), B, N, C, H, W, D,
+                  grid.nx, grid.ny, cache.n_int_max, _MODE[ctx.reducer], ptr(gl), ptr(gc),
+                  ptr(ws), ws.numel(), stream_ptr(dev))
+        return gl, gc, None, None, None
+
+
+def bev_pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCache,
+                   grid: BevGridSpec, reducer=Reducer.SUM) -> torch.Tensor:
+    """Differentiable fused lift+pool (config F): logits (N,D,H,W) /
+    (B,N,D,H,W) and context (N,C,H,W) / (B,N,C,H,W), bf16 CUDA -> fp32
+    (C,nx,ny) / (B,C,nx,ny).  Gradients flow to both (bf16).  SUM / MEAN."""
+    reducer = _reducer(reducer)
+    if reducer is Reducer.MAX:
+        from .errors import UnsupportedReducerError
+        raise UnsupportedReducerError("the fused path is differentiable for SUM and MEAN")
+    batched = logits.dim() == 5
+    lg = (logits if batched else logits[None]).to(torch.bfloat16).contiguous()
+    cx = (context if batched else context[None]).to(torch.bfloat16).contiguous()
+    cache = cache.for_grid(grid)
+    out = _FusedPoolFn.apply(lg, cx, cache, grid, reducer)
+    out = out.view(lg.shape[0], cx.shape[2], grid.nx, grid.ny)
+    return out if batched else out[0]

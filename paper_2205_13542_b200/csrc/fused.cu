@@ -231,3 +231,112 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
 }
 
 }  // extern "C"
+
+// ---- fused backward (config F training) -------------------------------------
+// out[c, cell] = sum_{p in cell} w_p ctx[pix(p), c],  w = softmax_D(logits)
+// (SUM / MEAN).  Given g = dL/dout:
+//   grad_ctx[pix, c]   = sum_d w[pix, d] g'[c, cell(pix, d)]
+//   grad_w[pix, d]     = <ctx[pix, :], g'[:, cell(pix, d)]>     (0 off the grid)
+//   grad_logit[pix, d] = w[pix, d] (grad_w[pix, d] - sum_d' w[pix, d'] grad_w[pix, d'])
+// with g' = g (SUM) or g / len(cell) (MEAN).  The first two are the gather
+// backward of backward.cu on the fp32 softmax and an fp32 NHWC copy of the
+// context; the softmax Jacobian and the bf16 casts are one kernel per pixel.
+namespace bvp {
+
+__global__ void __launch_bounds__(256)
+bf16_to_nhwc_f32_kernel(const __nv_bfloat16 *__restrict__ src, int64_t NB, int C, int HW,
+                        float *__restrict__ dst) {
+    const int64_t total = NB * C * int64_t(HW);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int c = int(i % C);
+        const int64_t pix = i / C;  // n * HW + hw
+        const int64_t n = pix / HW, hw = pix - n * HW;
+        dst[i] = __bfloat162float(src[(n * C + c) * HW + hw]);
+    }
+}
+
+// one warp per pixel: the softmax Jacobian, then bf16 stores of grad_logits
+__global__ void __launch_bounds__(256)
+softmax_backward_kernel(const float *__restrict__ w, const float *__restrict__ gw, int64_t NB,
+                        int D, int HW, __nv_bfloat16 *__restrict__ grad_logits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t npix = NB * HW;
+    for (int64_t pix = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); pix < npix;
+         pix += int64_t(gridDim.x) * (blockDim.x >> 5)) {
+        const int64_t n = pix / HW, hw = pix - n * HW;
+        const int64_t base = n * D * int64_t(HW) + hw;
+        float s = 0.f;
+        for (int d = lane; d < D; d += 32) s += w[base + int64_t(d) * HW] * gw[base + int64_t(d) * HW];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        for (int d = lane; d < D; d += 32) {
+            const int64_t k = base + int64_t(d) * HW;
+            grad_logits[k] = __float2bfloat16(w[k] * (gw[k] - s));
+        }
+    }
+}
+
+__global__ void f32_to_bf16_kernel(const float *__restrict__ src, int64_t n,
+                                   __nv_bfloat16 *__restrict__ dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = __float2bfloat16(src[i]);
+}
+
+static size_t a256f(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace bvp
+
+extern "C" {
+
+size_t bvp_fused_backward_workspace_bytes(int B, int N, int C, int H, int W, int D,
+                                          int64_t n_int_max) {
+    const size_t pix = size_t(B) * N * H * W;
+    return a256f(4 * pix * D) * 2 + a256f(4 * pix * C) * 2 +
+           a256f(bvp_backward_workspace_bytes(B, C, n_int_max));
+}
+
+int bvp_fused_backward_bf16(const float *grad_out, const uint16_t *logits, const uint16_t *context,
+                            const uint32_t *interval_starts, const uint32_t *interval_cells,
+                            const uint32_t *cell_first, const uint32_t *interval_of_point, int B,
+                            int N, int C, int H, int W, int D, int nx, int ny, int64_t n_int_max,
+                            int mode, uint16_t *grad_logits, uint16_t *grad_context,
+                            void *workspace, size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(mode == BVP_SUM || mode == BVP_MEAN, BVP_ERR_UNSUPPORTED,
+                "the fused backward takes SUM and MEAN (mode %d)", mode);
+    BVP_REQUIRE(B >= 1 && N >= 1 && C >= 1 && H >= 1 && W >= 1 && D >= 1, BVP_ERR_INVALID,
+                "bad dims");
+    const size_t need = bvp_fused_backward_workspace_bytes(B, N, C, H, W, D, n_int_max);
+    BVP_REQUIRE(workspace && workspace_bytes >= need, BVP_ERR_INVALID,
+                "fused backward workspace too small: need %zu bytes", need);
+    BVP_REQUIRE(grad_out && logits && context && grad_logits && grad_context, BVP_ERR_INVALID,
+                "null pointer argument");
+    cudaStream_t s = as_stream(stream);
+    const int64_t NB = int64_t(B) * N, HW = int64_t(H) * W, pix = NB * HW;
+    char *ws = static_cast<char *>(workspace);
+    float *w = reinterpret_cast<float *>(ws);
+    float *gw = reinterpret_cast<float *>(ws + a256f(4 * size_t(pix) * D));
+    float *ctx = reinterpret_cast<float *>(ws + 2 * a256f(4 * size_t(pix) * D));
+    float *gctx = reinterpret_cast<float *>(reinterpret_cast<char *>(ctx) + a256f(4 * size_t(pix) * C));
+    void *bws = reinterpret_cast<char *>(gctx) + a256f(4 * size_t(pix) * C);
+    const unsigned lb = static_cast<unsigned>(NB * ((HW + 31) / 32));
+    pixel_softmax_kernel<<<lb, 32 * kLseWarps, 0, s>>>(
+        reinterpret_cast<const __nv_bfloat16 *>(logits), NB, D, int(HW), w);
+    const unsigned eb = static_cast<unsigned>(std::min<int64_t>(ceil_div(pix * C, 256), 148 * 32));
+    bf16_to_nhwc_f32_kernel<<<eb, 256, 0, s>>>(reinterpret_cast<const __nv_bfloat16 *>(context),
+                                               NB, C, int(HW), ctx);
+    int rc = bvp_pool_backward_f32(grad_out, ctx, w, interval_starts, interval_cells, cell_first,
+                                   interval_of_point, nullptr, B, N, C, H, W, D, nx, ny, n_int_max,
+                                   mode, gctx, gw, bws, bvp_backward_workspace_bytes(B, C, n_int_max),
+                                   stream);
+    if (rc != BVP_OK) return rc;
+    const unsigned sb = static_cast<unsigned>(std::min<int64_t>(ceil_div(pix, 8), 148 * 32));
+    softmax_backward_kernel<<<sb, 256, 0, s>>>(w, gw, NB, D, int(HW),
+                                               reinterpret_cast<__nv_bfloat16 *>(grad_logits));
+    f32_to_bf16_kernel<<<eb, 256, 0, s>>>(gctx, pix * C,
+                                          reinterpret_cast<__nv_bfloat16 *>(grad_context));
+    return check_launch("fused_backward_bf16");
+}
+
+}  // extern "C"

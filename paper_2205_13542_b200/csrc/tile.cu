@@ -359,6 +359,35 @@ __device__ __forceinline__ void group_row(float2 (&acc)[kTileGroup / 2][CS], con
     }
 }
 
+template <int CS, int FS>
+__device__ __forceinline__ void group_row2(float2 (&acc)[kTileGroup / 2][CS], const float *wq,
+                                           const float *fs, int h0, int h1, int lane) {
+    const float4 a0 = *reinterpret_cast<const float4 *>(wq);
+    const float4 a1 = *reinterpret_cast<const float4 *>(wq + 4);
+    const float4 b0 = *reinterpret_cast<const float4 *>(wq + kTileGroup);
+    const float4 b1 = *reinterpret_cast<const float4 *>(wq + kTileGroup + 4);
+    float fa[CS], fb[CS];
+#pragma unroll
+    for (int j = 0; j < CS; ++j) {
+        fa[j] = fs[h0 * FS + lane + 32 * j];
+        fb[j] = fs[h1 * FS + lane + 32 * j];
+    }
+#pragma unroll
+    for (int j = 0; j < CS; ++j) {
+        ffma2(acc[0][j], make_float2(a0.x, a0.y), fa[j]);
+        ffma2(acc[1][j], make_float2(a0.z, a0.w), fa[j]);
+        ffma2(acc[2][j], make_float2(a1.x, a1.y), fa[j]);
+        ffma2(acc[3][j], make_float2(a1.z, a1.w), fa[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < CS; ++j) {
+        ffma2(acc[0][j], make_float2(b0.x, b0.y), fb[j]);
+        ffma2(acc[1][j], make_float2(b0.z, b0.w), fb[j]);
+        ffma2(acc[2][j], make_float2(b1.x, b1.y), fb[j]);
+        ffma2(acc[3][j], make_float2(b1.z, b1.w), fb[j]);
+    }
+}
+
 // Every global load of a tile is independent of the others (the addresses
 // follow from the tile index alone), so a CTA waits about one memory latency
 // per stage: (1) the feature rows F[hl][c] and the depth weights w[hl][d] of
@@ -366,7 +395,7 @@ __device__ __forceinline__ void group_row(float2 (&acc)[kTileGroup / 2][CS], con
 // soft-maxed in place -- (2) the records, which only index shared memory,
 // aggregate the weights per (cell, row), (3) the group products.
 template <int CS, int SRC, int CL>
-__global__ void __launch_bounds__(kPoolThreads)
+__global__ void __launch_bounds__(kPoolThreads, 4)
 tile_pool_kernel(TilePoolArgs a) {
     constexpr int CP = CS * 32;
     constexpr int FS = CP + 4;  // row stride: 16-byte aligned rows of channel quads
@@ -561,10 +590,25 @@ tile_pool_kernel(TilePoolArgs a) {
             for (int m = 0; m < kTileGroup / 2; ++m)
 #pragma unroll
                 for (int j = 0; j < CS; ++j) acc[m][j] = make_float2(0.f, 0.f);
-            for (uint32_t m = G.x; m; m &= m - 1, wq += kTileGroup)
-                group_row<CS, FS>(acc, wq, fs, __ffs(m) - 1, lane);
-            for (uint32_t m = G.y; m; m &= m - 1, wq += kTileGroup)
-                group_row<CS, FS>(acc, wq, fs, 31 + __ffs(m), lane);
+            // rows two at a time: the second row's loads are in flight while
+            // the first row's products issue
+            for (int half = 0; half < 2; ++half) {
+                uint32_t m = half ? G.y : G.x;
+                const int base = half ? 31 : -1;
+                while (m) {
+                    const int h0 = base + __ffs(m);
+                    m &= m - 1;
+                    if (m) {
+                        const int h1 = base + __ffs(m);
+                        m &= m - 1;
+                        group_row2<CS, FS>(acc, wq, fs, h0, h1, lane);
+                        wq += 2 * kTileGroup;
+                    } else {
+                        group_row<CS, FS>(acc, wq, fs, h0, lane);
+                        wq += kTileGroup;
+                    }
+                }
+            }
 #pragma unroll
             for (int k = 0; k < kTileGroup; ++k) {
                 const uint32_t row = __shfl_sync(0xFFFFFFFFu, my_row, k);

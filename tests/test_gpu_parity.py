@@ -675,3 +675,53 @@ def test_empty_cells_zeroed_beside_reduction(name):
     o_np = out.cpu().numpy()
     assert np.isnan(o_np[:, :, occupied]).all()
     assert (o_np[:, :, ~occupied] == 0).all()
+
+
+# ---- the fused path's backward (config F training) vs the fp64 restatement ----
+
+def _fused_grads(name, red, seed=3):
+    spec = bp.CONFIGS[name]
+    rig, features, logits, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, spec.frustum, grid)
+    dev = torch.device("cuda")
+    lg = torch.from_numpy(logits).to(dev).to(torch.bfloat16).requires_grad_(True)
+    cx = torch.from_numpy(features).to(dev).to(torch.bfloat16).requires_grad_(True)
+    out = bp.bev_pool_fused(lg, cx, cache, grid, red)
+    g = torch.randn(out.shape, device=dev, generator=torch.Generator(dev).manual_seed(seed))
+    out.backward(g)
+    assert lg.grad.dtype == torch.bfloat16 and cx.grad.dtype == torch.bfloat16
+    return (spec, features, logits, grid, cache, out.detach(), g.cpu().numpy().reshape(out.shape[0], -1),
+            lg.grad.float().cpu().numpy(), cx.grad.float().cpu().numpy())
+
+
+@pytest.mark.parametrize("red", ["sum", "mean"])
+def test_fused_backward_matches_fp64_restatement(red):
+    spec, features, logits, grid, cache, out, g, gl, gc = _fused_grads("T", red)
+    want_l, want_c = o.fused_backward(o.bf16_round(features), o.bf16_round(logits),
+                                      cache.cell_of_point, g, cache.ranks,
+                                      cache.interval_starts, cache.interval_cells, red)
+    assert max_rel_dev(want_l, gl) <= BF16_TOL
+    assert max_rel_dev(want_c, gc) <= BF16_TOL
+    want = o.fused_pool(o.bf16_round(features), o.bf16_round(logits), cache.ranks,
+                        cache.interval_starts, cache.interval_cells, grid.n_cells, red)
+    assert max_rel_dev(want, out.cpu().numpy().reshape(want.shape)) <= 1e-5
+
+
+def test_fused_backward_nuscenes_shape_sum():
+    """S shape, restated per camera in fp64 (as test_backward_nuscenes_shape_sum)."""
+    spec, features, logits, grid, cache, out, g, gl_got, gc_got = _fused_grads("S", "sum")
+    fb, lb = o.bf16_round(features).astype(np.float64), o.bf16_round(logits).astype(np.float64)
+    N, C, H, W = features.shape
+    D = logits.shape[1]
+    cells = cache.cell_of_point.reshape(N, H, W, D)
+    g64 = np.concatenate([g.astype(np.float64), np.zeros((C, 1))], axis=1)
+    for n in range(N):
+        e = np.exp(lb[n] - lb[n].max(axis=0, keepdims=True))
+        w = e / e.sum(axis=0, keepdims=True)                      # D, H, W
+        idx = np.where(cells[n] == bp.OUT_OF_RANGE, grid.n_cells, cells[n]).astype(np.int64)
+        gcol = g64[:, idx]                                        # C, H, W, D
+        gc = np.einsum("chwd,dhw->chw", gcol, w)
+        gw = np.einsum("chwd,chw->dhw", gcol, fb[n])
+        gl = w * (gw - (w * gw).sum(axis=0, keepdims=True))
+        assert max_rel_dev(gc, gc_got[n]) <= BF16_TOL
+        assert max_rel_dev(gl, gl_got[n]) <= BF16_TOL
