@@ -645,11 +645,23 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
     rec("materialised_pool", ms, n_in * (4 * C + 4) + 8 * n_int + 4 * C * n_cells)
     del x
 
-    # fused bf16 lift+pool
-    lg = torch.randn(dist.shape, device=dev).to(torch.bfloat16)[0]
-    cx = feats[0].to(torch.bfloat16)
-    ms = _timeit(torch, lambda: bp.pool_fused(lg, cx, cache, grid), flush)
-    rec("fused_bf16", ms, 2 * P + 2 * NHW * C + 4 * NHW + 4 * n_in + 8 * n_int + 4 * C * n_cells)
+    # fused bf16 lift+pool: the tiled kernels with the depth softmax formed
+    # per tile in shared memory (one CUDA graph, like the headline step)
+    lg = torch.randn(dist.shape, device=dev).to(torch.bfloat16)
+    cx = feats.to(torch.bfloat16)
+    tp = cache.tile_plan(spec.n_cameras, f.height, f.width, f.depth_bins)
+    fout = torch.empty((1, C, n_cells), dtype=torch.float32, device=dev)
+    fused_fn = lambda: tp.pool_fused_bf16(lg, cx, 1, C, 0, fout)  # noqa: E731  (SUM)
+    fused_fn()
+    gf = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gf):
+        fused_fn()
+    ms = _timeit(torch, gf.replay, flush)
+    rec("fused_bf16", ms, 2 * P + 2 * NHW * C + 4 * n_in + 8 * n_int + 4 * C * n_cells,
+        path="tile_pool_kernel<bf16 fused> + tile_finalize_kernel (graph)")
+    ms = _timeit(torch, lambda: bp.pool_fused(lg[0], cx[0], cache, grid), flush)
+    rec("fused_bf16_api", ms, 2 * P + 2 * NHW * C + 4 * n_in + 8 * n_int + 4 * C * n_cells,
+        path="bp.pool_fused (allocates its output every call)")
 
     # cold association (geometry + sort + tables), no host sync
     builder = bp.CacheBuilder(spec.n_cameras, f, grid, dev)

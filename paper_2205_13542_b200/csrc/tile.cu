@@ -494,26 +494,31 @@ tile_pool_kernel(TilePoolArgs a) {
     if (n_segs == 0 || a.dbg == 1) return;
     const uint4 *gt = a.groups + t * g.gcap;
     const uint32_t total_w = __ldg(&gt[n_groups].z);
+    // fused: 1 / sum_d exp(l - max) of each pixel; the weights are left
+    // unnormalised (exp2 of the scaled logits) and the aggregation scales
+    // each (cell, row) sum by its row's factor
+    __shared__ float s_inv[kTileMaxRows];
     if (SRC == kTileBF16Fused) {
         __syncthreads();
         // depth softmax of the tile's pixels (lift.py:17-31 semantics, fp32
         // from bf16 logits): one warp per pixel, lanes over depth bins
+        constexpr float kLog2e = 1.4426950408889634f;
         for (int hl = warp; hl < id.th; hl += NW) {
             float *row = pw + hl * PD;
             float m = -INFINITY;
             for (int d = lane; d < D; d += 32) m = fmaxf(m, row[d]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+            const float ms = m * kLog2e;
             float sum = 0.f;
             for (int d = lane; d < D; d += 32) {
-                const float e = expf(row[d] - m);
+                const float e = exp2f(fmaf(row[d], kLog2e, -ms));
                 row[d] = e;
                 sum += e;
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-            const float inv = 1.f / sum;
-            for (int d = lane; d < D; d += 32) row[d] *= inv;
+            if (lane == 0) s_inv[hl] = 1.f / sum;
         }
     }
     const uint32_t *srow = a.seg_row + t * g.tpc;
@@ -549,13 +554,14 @@ tile_pool_kernel(TilePoolArgs a) {
         // (records below RPT * 256 come from the prefetch)
         auto run = [&](uint32_t k, uint32_t r) {
             if (k < G0.w || k >= r_end || !(r >> 31)) return;
-            const uint32_t widx = (r >> shift) & wmask;
+            const uint32_t widx = (r >> shift) & wmask, r0 = r;
             float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
             for (uint32_t kk = k + 1; kk < r_end; ++kk) {
                 r = __ldg(rt + kk);
                 if (r >> 31) break;
                 sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
             }
+            if (SRC == kTileBF16Fused) sum *= s_inv[(r0 >> g.d_bits) & hmask];
             ws[widx - G0.z] = sum;
         };
 #pragma unroll
@@ -856,12 +862,16 @@ static T *at(const bvp_tile_plan *p, size_t off) {
 
 template <int CS, int SRC, int CL>
 static int launch_phase1(const TilePoolArgs &a, int B, size_t smem, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static int max_dyn = -1;
+    if (max_dyn < 0) {  // opt in to the full shared memory, less the static part
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, tile_pool_kernel<CS, SRC, CL>);
+        max_dyn = 227 * 1024 - int(fa.sharedSizeBytes);
         cudaFuncSetAttribute(tile_pool_kernel<CS, SRC, CL>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
     }
+    BVP_REQUIRE(smem <= size_t(max_dyn), BVP_ERR_UNSUPPORTED,
+                "tile needs %zu bytes of shared memory (max %d)", smem, max_dyn);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(a.g.T), unsigned(B));
     cfg.blockDim = dim3(kPoolThreads);
