@@ -136,14 +136,14 @@ UNIT_BUDGET = 128
 #: points per warp task (a run of consecutive units walked as one stream)
 TASK_BUDGET = 384
 #: chunk length of the fast kernels' work list (csrc/work.cu); 0 disables it
-CHUNK = int(os.environ.get("BVP_CHUNK", "64"))
+CHUNK = 64
 #: chunk order: 0 = longest first (cell order within a length); > 0 = by 2D
 #: tiles of WORK_TILE x WORK_TILE cells, longest first within a tile
-WORK_TILE = int(os.environ.get("BVP_WORK_TILE", "0"))
+WORK_TILE = 0
 #: chunk length of the exact mode's own chunk list: its lane groups sum whole
 #: intervals up to this length in fp64; longer ones are walked in order by a
 #: CTA each (pool_exact_long_kernel), so fewer, longer chunks suit it
-EXACT_CHUNK = int(os.environ.get("BVP_EXACT_CHUNK", "128"))
+EXACT_CHUNK = 128
 
 
 def work_bounds(n_points: int, n_int_max: int, chunk: int) -> tuple[int, int, int]:

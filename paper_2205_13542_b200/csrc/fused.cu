@@ -182,18 +182,12 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     const int64_t NB = int64_t(B) * N, HW = int64_t(H) * W;
     auto *lg = reinterpret_cast<const __nv_bfloat16 *>(logits);
     const unsigned lb = static_cast<unsigned>(NB * ceil_div(HW, 32));
-    // 1: softmax weights precomputed per (n, d, h, w) by the prologue (measured
-    // 91 us vs 99 us for exp(logit - lse) per point at the nuScenes shape)
-    static const int wmode = [] { const char *e = getenv("BVP_FUSED_W"); return e ? atoi(e) : 1; }();
+    // the softmax weights are precomputed per (n, d, h, w) by the prologue
+    // (measured 91 us vs 99 us for exp(logit - lse) per point at the
+    // nuScenes shape); the weight-gather kernel needs 16-byte chunks
     float *wsm = reinterpret_cast<float *>(ws + L.off_w);
-    const bool use_w = wmode && C % 8 == 0;  // the weight-gather kernel needs 16-byte chunks
-    // BVP_FUSED_ZERO=1 (measurement only): no memset branch; the reduction
-    // zeroes the empty cells beside its kernels, as the captured fp32 path
-    // does.  Slower here (80 / 94 us eager / captured against 76 / 78 us,
-    // scripts/time_fused_zero.py): the bf16 chunk kernel's four blocks per SM
-    // leave no registers for the zero-fill block.
-    static const int zmode = [] { const char *e = getenv("BVP_FUSED_ZERO"); return e ? atoi(e) : 0; }();
-    const bool zero_beside = zmode && schedule->work;
+    const bool use_w = C % 8 == 0;
+    const bool zero_beside = false;  // the map is zero-filled beside the prologue
     // three independent prologue branches (forked streams): the depth
     // softmax, the context's NHWC staging, the map's zero fill
     {

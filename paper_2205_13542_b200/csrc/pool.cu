@@ -374,17 +374,13 @@ int bvp_pool_forward_f32(const float *features, const float *dist, const uint32_
     BVP_REQUIRE(C == 0 || (features && feats_nhwc && out), BVP_ERR_INVALID,
                 "null pointer argument");
     if (C == 0) return BVP_OK;
-    // fast mode with a chunk schedule, under graph capture: the staging
-    // alone, then the reduction zeroes the empty cells beside its kernels
-    // (zero_empty_beside); otherwise the memset beside the transpose
-    const bool zero_beside = !exact && cell_first && schedule && schedule->work &&
-                             zero_empty_beside(as_stream(stream));
-    const int rc = bvp_pool_prepare_f32(features, B, N, C, H, W, feats_nhwc,
-                                        zero_beside ? nullptr : out, int64_t(nx) * ny, stream);
+    // the memset of the map beside the NHWC transpose, then the reduction
+    const int rc = bvp_pool_prepare_f32(features, B, N, C, H, W, feats_nhwc, out,
+                                        int64_t(nx) * ny, stream);
     if (rc != BVP_OK) return rc;
     return pool_forward_nhwc(feats_nhwc, dist, ranks, interval_starts, interval_cells, cell_first,
                              schedule, B, N, C, H, W, D, nx, ny, n_int_max, mode, exact, out,
-                             argmax, scratch, scratch_bytes, stream, !zero_beside);
+                             argmax, scratch, scratch_bytes, stream, true);
 }
 
 int bvp_reorder_weights(const float *dist, const uint32_t *ranks, int64_t n_in, int N, int D,

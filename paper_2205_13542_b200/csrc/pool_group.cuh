@@ -451,11 +451,7 @@ pool_group_kernel(const PoolParams P, int L, int lg) {
 // lanes per point group and chunks per lane for a row of nch chunks:
 // the smallest power-of-two L with ceil(nch / L) * VEC <= budget floats.
 inline bool choose_group(int nch, int vec, int &L, int &lg, int &cpl) {
-    static const int env_budget = [] {
-        const char *e = getenv("BVP_GROUP_BUDGET");
-        return e ? atoi(e) : 0;
-    }();
-    const int budget = env_budget > 0 ? env_budget : (vec == 8 ? 24 : 20);
+    const int budget = vec == 8 ? 24 : 20;
     for (lg = 0, L = 1; L <= 32; L <<= 1, ++lg) {
         cpl = (nch + L - 1) / L;
         if (cpl * vec <= budget && cpl <= kGroupMaxCpl) return true;

@@ -354,18 +354,8 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
     p.partial_arg = arg && !EXACT ? reinterpret_cast<uint32_t *>(static_cast<float *>(scratch) +
                                                                  size_t(B) * p0.chunk_partials * p0.C)
                                   : nullptr;
-    // fast mode under graph capture: the empty cells' zero fill runs beside
-    // the kernels (forked stream, joined after the combine); eager launches
-    // and exact mode (its fp64 chunk kernel leaves no registers for a
-    // co-resident block) keep the up-front memset
-    const bool zero_beside = !p.out_zeroed && !EXACT && p.cell_first &&
-                             zero_empty_beside(s);
-    if (!p.out_zeroed && !zero_beside)
-        cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
-    SideFork zfork(s, zero_beside ? 1 : -1);  // -1: inline, no events
-    if (zero_beside)
-        zero_empty_cells_kernel<<<kNumSms, kZeroThreads, 0, zfork.side>>>(p.cell_first, p.n_cells,
-                                                                          p.C, B, p.out);
+    // the scattered column stores need a zero-filled map
+    if (!p.out_zeroed) cudaMemsetAsync(p.out, 0, size_t(B) * p.C * p.n_cells * sizeof(float), s);
     const int G = 32 >> lg;
     const int64_t batches = ceil_div(p.max_work, G);
     const dim3 grid(static_cast<unsigned>(std::max<int64_t>(
@@ -403,7 +393,6 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
         else if (is_max) pool_ivl_combine_kernel<true, false><<<cg, kPoolThreads, 0, s>>>(p);
         else pool_ivl_combine_kernel<false><<<cg, kPoolThreads, 0, s>>>(p);
     }
-    zfork.join();
     return BVP_OK;
 }
 

@@ -46,22 +46,8 @@ namespace bvp {
 constexpr int kPoolWarps = 8;
 constexpr int kPoolThreads = 32 * kPoolWarps;
 
-// Whether the fast path zeroes the empty cells beside its kernels (else a
-// memset of the whole map beside the feature staging): only when the launches
-// are being captured into a CUDA graph.  Measured at config S
-// (scripts/time_zero_modes.py, profiles/r01/zero_modes.txt): graph-replayed,
-// beside is faster (batch 1: 71.7 vs 75.7 us, batch 4: 232 vs 273 us);
-// launched eagerly it is slower (89 vs 74 us, 380 vs 266 us).
-// BVP_ZERO_BESIDE=0/1 overrides (measurement).
-inline bool zero_empty_beside(cudaStream_t s) {
-    static const int env = [] {
-        const char *e = getenv("BVP_ZERO_BESIDE");
-        return e ? atoi(e) : -1;
-    }();
-    if (env >= 0) return env != 0;
-    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-    return cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive;
-}
+// The interval kernels' map is zero-filled by a memset beside the feature
+// staging (bvp_pool_prepare_f32) before their scattered column stores.
 constexpr int kUnitPitch = kUnitCells + 1;
 constexpr uint32_t kLongUnit = 0x80000000u;  // unit / task flag: split by pool_long_kernel
 

@@ -37,7 +37,6 @@
 #include <algorithm>
 
 #include <cooperative_groups.h>
-#include <cuda.h>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -329,7 +328,6 @@ struct TilePoolArgs {
     int64_t max_seg;
     TileGeom g;
     int C, wbudget;
-    int dbg;  // ablation (profiling builds): 1 stop after staging, 2 after aggregation
 };
 
 // acc.x += w.x * f, acc.y += w.y * f in one FFMA2 (Blackwell packed fp32;
@@ -491,7 +489,7 @@ tile_pool_kernel(TilePoolArgs a) {
         if (CL > 1)
             cluster.sync();
     }
-    if (n_segs == 0 || a.dbg == 1) return;
+    if (n_segs == 0) return;
     const uint4 *gt = a.groups + t * g.gcap;
     const uint32_t total_w = __ldg(&gt[n_groups].z);
     // fused: 1 / sum_d exp(l - max) of each pixel; the weights are left
@@ -583,7 +581,6 @@ tile_pool_kernel(TilePoolArgs a) {
             }
         }
         __syncthreads();
-        if (a.dbg == 2) return;
         // (3) one warp per group of 8 cells
         for (int q = q0 + warp; q < q1; q += NW) {
             const uint4 G = gt[q];
@@ -699,101 +696,6 @@ tile_finalize_kernel(const float *__restrict__ rows, int64_t max_seg,
     }
 }
 
-// TMA variant (n_cells % 4 == 0): the CTA assembles the (C x 32 cells) block
-// of the map in shared memory in the tensor map's 128-byte-swizzled layout and
-// one thread writes it with a single bulk tensor store, double buffered so the
-// store of block k overlaps the combine of block k+1.  Lane l of warp w
-// combines cell 4w + (l & 3), channels (l >> 2) + 8i: its loads are 32-byte
-// sectors of a segment row, its shared stores hit 32 distinct banks.
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-template <int CS>
-__global__ void __launch_bounds__(kPoolThreads)
-tile_finalize_tma_kernel(const __grid_constant__ CUtensorMap tmap, const float *__restrict__ rows,
-                         int64_t max_seg, const uint32_t *__restrict__ cell_seg_first,
-                         const uint32_t *__restrict__ cell_npts, int64_t n_cells, int C,
-                         int mean) {
-    extern __shared__ __align__(1024) unsigned char fin_smem[];
-    // C rows x 128 bytes, 1024-byte aligned (the swizzle atom)
-    unsigned char *buf = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(fin_smem) + 1023) & ~uintptr_t(1023));
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int cx = 4 * warp + (lane & 3), cg8 = lane >> 2;
-    const int b = blockIdx.y;
-    const int64_t c0 = int64_t(blockIdx.x) * kFinCells;
-    const int64_t c = c0 + cx;
-    uint32_t s0 = 0, s1 = 0;
-    float inv = 1.f;
-    if (c < n_cells) {
-        s0 = __ldg(cell_seg_first + c);
-        s1 = __ldg(cell_seg_first + c + 1);
-        if (mean && s1 > s0) inv = 1.f / float(__ldg(cell_npts + c));
-    }
-    const float *rb = rows + int64_t(b) * max_seg * C;
-    constexpr int NI = 4 * CS;  // channels per lane: ceil(C / 8) <= 4 CS
-    float v[NI];
-    const float *r0 = rb + int64_t(s0) * C + cg8;
-#pragma unroll
-    for (int i = 0; i < NI; ++i) v[i] = (s1 > s0 && cg8 + 8 * i < C) ? __ldg(r0 + 8 * i) : 0.f;
-    for (uint32_t s = s0 + 1; s < s1; ++s) {
-        const float *r = rb + int64_t(s) * C + cg8;
-#pragma unroll
-        for (int i = 0; i < NI; ++i)
-            if (cg8 + 8 * i < C) v[i] += __ldg(r + 8 * i);
-    }
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-        const int ch = cg8 + 8 * i;
-        if (ch < C) {
-            const uint32_t off = uint32_t(ch) * 128u +
-                                 ((uint32_t(warp) ^ (uint32_t(ch) & 7u)) << 4) +
-                                 uint32_t(lane & 3) * 4u;
-            *reinterpret_cast<float *>(buf + off) = v[i] * inv;
-        }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile(
-            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                &tmap),
-            "r"(int(c0)), "r"(b * C), "r"(smem_u32(buf))
-            : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
-}
-
-// The output's tensor map (2-D: n_cells x B*C floats, 128-byte swizzled
-// boxes of 32 cells x C channels), encoded through the driver entry point.
-static bool make_out_tmap(CUtensorMap *m, float *out, int64_t n_cells, int C, int B) {
-    using Fn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                            const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                            const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                            CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static Fn fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<Fn>(p);
-    }
-    if (!fn || (n_cells % 4) != 0 || C > 256 || (reinterpret_cast<uintptr_t>(out) & 15)) return false;
-    const cuuint64_t dims[2] = {cuuint64_t(n_cells), cuuint64_t(B) * C};
-    const cuuint64_t strides[1] = {cuuint64_t(n_cells) * 4};
-    const cuuint32_t box[2] = {cuuint32_t(kFinCells), cuuint32_t(C)};
-    const cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 // ---- plan layout -------------------------------------------------------------
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -906,9 +808,6 @@ static int run_tile_pool(const void *feats, const void *weights, const bvp_tile_
     a.g = g;
     a.C = C;
     a.wbudget = std::max(2048, 128 * g.TH);
-#ifdef BVP_TILE_ABLATION  // profiling builds only: stop phase 1 after a stage
-    a.dbg = BVP_TILE_ABLATION;
-#endif
     const int CP = CS * 32;
     const size_t smem =
         sizeof(float) * (size_t(g.TH) * (CP + 4) + size_t(g.TH) * ((g.D + 3) & ~3) + a.wbudget);
