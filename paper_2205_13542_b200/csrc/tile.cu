@@ -49,6 +49,7 @@ constexpr int kTileMaxPoints = 8192;  // points per tile (smem sort capacity)
 constexpr int kPlanThreads = 512;
 constexpr int kPoolThreads = 256;
 constexpr int kFinCells = 32;         // cells per finalize CTA
+constexpr int kGtCache = 32;          // group headers cached in shared memory
 
 struct TileGeom {
     int N, H, W, D, TH, n_hb;
@@ -220,7 +221,7 @@ tile_plan_kernel(const uint32_t *__restrict__ cells, TileGeom g, uint4 *__restri
     __syncthreads();
     const uint32_t total_w = s_tot[0];
     const int shift = g.hl_bits + g.d_bits;
-    const uint32_t wmax = 1u << (31 - shift);
+    const uint32_t wmax = 1u << (30 - shift);
     if (threadIdx.x == 0 && total_w > wmax) atomicExch(err, 1);
     uint4 *gt = groups + t * g.gcap;
     uint32_t *rt = rec + t * g.tpc;
@@ -240,8 +241,13 @@ tile_plan_kernel(const uint32_t *__restrict__ cells, TileGeom g, uint4 *__restri
             const unsigned long long m = gmask[q];
             const uint32_t upos = __popcll(m & ((1ull << hl) - 1ull));
             const uint32_t widx = s_woff[q] + upos * kTileGroup + kk;
-            rt[k] = (run_head ? 0x80000000u : 0u) | ((widx & (wmax - 1)) << shift) |
-                    (uint32_t(hl) << g.d_bits) | uint32_t(d);
+            // bit 31: first point of a (cell, row) run; bit 30: the run goes on
+            // with the next record (most runs are single points: their
+            // aggregation then reads no other record)
+            const bool more = k + 1 < n_pts && uint32_t(keys[k + 1] >> 16) == c &&
+                              (int(keys[k + 1] >> g.d_bits) & hmask) == hl;
+            rt[k] = (run_head ? 0x80000000u : 0u) | (more ? 0x40000000u : 0u) |
+                    ((widx & (wmax - 1)) << shift) | (uint32_t(hl) << g.d_bits) | uint32_t(d);
             if (head) {
                 sc[s] = c;
                 sn[s] = uint32_t(k);  // first point of the segment
@@ -329,7 +335,6 @@ struct TilePoolArgs {
     TileGeom g;
     int C, wbudget;
 };
-
 // acc.x += w.x * f, acc.y += w.y * f in one FFMA2 (Blackwell packed fp32;
 // the scalar f is a broadcast operand, no move).
 __device__ __forceinline__ void ffma2(float2 &acc, float2 w, float f) {
@@ -414,10 +419,29 @@ tile_pool_kernel(TilePoolArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // the first RPT records of each thread are loaded now, beside the staging
     // (records [0, RPT * 256) cover the whole tile at the nuScenes shape)
+    // the tile's group headers and segment-row indices (when they fit the
+    // small caches) are copied to shared memory asynchronously now, so the
+    // group products never wait on a global load
+    __shared__ __align__(16) uint4 s_gt[kGtCache + 1];
+    __shared__ uint32_t s_srow[kGtCache * kTileGroup];
+    const bool gt_cached = n_groups <= kGtCache;
+    if (gt_cached) {
+        const uint4 *gsrc = a.groups + t * g.gcap;
+        const uint32_t *ssrc = a.seg_row + t * g.tpc;
+        for (int i = threadIdx.x; i <= n_groups; i += kPoolThreads)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(&s_gt[i]))),
+                         "l"(gsrc + i));
+        for (int i = threadIdx.x; i < n_segs; i += kPoolThreads)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(&s_srow[i]))),
+                         "l"(ssrc + i));
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     // distributed shared memory may be written only once every CTA of the
     // cluster is running: arrive now, wait just before the first remote store
     if (CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    constexpr int RPT = 8;
+    constexpr int RPT = 16;
     const uint32_t *rt = a.rec + t * g.tpc;
     uint32_t pre[RPT];
 #pragma unroll
@@ -489,9 +513,10 @@ tile_pool_kernel(TilePoolArgs a) {
         if (CL > 1)
             cluster.sync();
     }
+    asm volatile("griddepcontrol.launch_dependents;");
     if (n_segs == 0) return;
-    const uint4 *gt = a.groups + t * g.gcap;
-    const uint32_t total_w = __ldg(&gt[n_groups].z);
+    const uint4 *gt = gt_cached ? s_gt : a.groups + t * g.gcap;
+    const uint32_t total_w = h.w;
     // fused: 1 / sum_d exp(l - max) of each pixel; the weights are left
     // unnormalised (exp2 of the scaled logits) and the aggregation scales
     // each (cell, row) sum by its row's factor
@@ -519,11 +544,13 @@ tile_pool_kernel(TilePoolArgs a) {
             if (lane == 0) s_inv[hl] = 1.f / sum;
         }
     }
-    const uint32_t *srow = a.seg_row + t * g.tpc;
+    if (gt_cached) asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // every thread's copies visible (and the staging done)
+    const uint32_t *srow = gt_cached ? s_srow : a.seg_row + t * g.tpc;
     float *rows = a.rows + int64_t(b) * a.max_seg * C;
     const int shift = g.hl_bits + g.d_bits;
     const uint32_t dmask = (1u << g.d_bits) - 1u, hmask = (1u << g.hl_bits) - 1u;
-    const uint32_t wmask = (1u << (31 - shift)) - 1u;
+    const uint32_t wmask = (1u << (30 - shift)) - 1u;
     for (int q0 = 0; q0 < n_groups;) {
         // a window of groups whose weights fit the budget (one, for nearly
         // every tile: then no search)
@@ -554,9 +581,8 @@ tile_pool_kernel(TilePoolArgs a) {
             if (k < G0.w || k >= r_end || !(r >> 31)) return;
             const uint32_t widx = (r >> shift) & wmask, r0 = r;
             float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
-            for (uint32_t kk = k + 1; kk < r_end; ++kk) {
+            for (uint32_t kk = k + 1; (r >> 30) & 1u; ++kk) {  // the run's later points
                 r = __ldg(rt + kk);
-                if (r >> 31) break;
                 sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
             }
             if (SRC == kTileBF16Fused) sum *= s_inv[(r0 >> g.d_bits) & hmask];
@@ -586,7 +612,7 @@ tile_pool_kernel(TilePoolArgs a) {
             const uint4 G = gt[q];
             // the group's segment-row indices, loaded before its products
             const int nk = min(kTileGroup, n_segs - q * kTileGroup);
-            const uint32_t my_row = lane < nk ? __ldg(srow + q * kTileGroup + lane) : 0u;
+            const uint32_t my_row = lane < nk ? srow[q * kTileGroup + lane] : 0u;
             const float *wq = ws + (G.z - G0.z);
             float2 acc[kTileGroup / 2][CS];
 #pragma unroll
@@ -627,6 +653,7 @@ tile_pool_kernel(TilePoolArgs a) {
         }
         q0 = q1;
     }
+    __syncthreads();
 }
 
 // ---- phase 2: per-cell combine + transpose into the channel-major map -------
@@ -650,6 +677,7 @@ tile_finalize_kernel(const float *__restrict__ rows, int64_t max_seg,
     const int nc = min(kFinCells, n_cells - c0);
     const uint32_t f = __ldg(cell_seg_first + c0 + min(lane, nc));
     const uint32_t f_end = __ldg(cell_seg_first + c0 + nc);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // phase 1's rows (PDL)
     const float *rb = rows + int64_t(b) * max_seg * C;
 #pragma unroll
     for (int u = 0; u < kFinCells / NW; ++u) {
@@ -824,11 +852,26 @@ static int run_tile_pool(const void *feats, const void *weights, const bvp_tile_
         }
         if (rc != BVP_OK) return rc;
     }
-    if (phases & 2)
-        tile_finalize_kernel<CS>
-            <<<dim3(unsigned(ceil_div(p->n_cells, kFinCells)), unsigned(B)), kPoolThreads, 0, s>>>(
-                rows, p->max_seg, at<const uint32_t>(p, L.csf), at<const uint32_t>(p, L.npts),
-                int(p->n_cells), C, mean, out);
+    if (phases & 2) {
+        // programmatic dependent launch: the combine's CTAs take the slots
+        // phase-1 CTAs free, read their cell tables, and wait in
+        // griddepcontrol.wait until phase 1's rows are complete
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(ceil_div(p->n_cells, kFinCells)), unsigned(B));
+        cfg.blockDim = dim3(kPoolThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at1[1];
+        at1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at1[0].val.programmaticStreamSerializationAllowed = (phases & 1) ? 1 : 0;
+        cfg.attrs = at1;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(
+            &cfg, tile_finalize_kernel<CS>, static_cast<const float *>(rows), p->max_seg,
+            at<const uint32_t>(p, L.csf), at<const uint32_t>(p, L.npts), int(p->n_cells), C, mean,
+            out);
+        BVP_REQUIRE(e == cudaSuccess, BVP_ERR_CUDA, "tile_finalize launch: %s",
+                    cudaGetErrorString(e));
+    }
     return check_launch("tile_pool");
 }
 
