@@ -318,11 +318,12 @@ class AssociationCache:
         return int(self.d_sched_counts[1].item())
 
     def fit_launch(self) -> None:
-        """Shrink the launch bounds to the exact unit / chunk counts (one host
-        sync)."""
-        self.ensure_units()
-        c = self.d_sched_counts.cpu().tolist()
-        self.max_units, self.max_long, self.max_tasks = max(1, int(c[0])), int(c[1]), max(1, int(c[2]))
+        """Shrink the launch bounds to the exact chunk (and, when built, unit)
+        counts (one host sync).  Deferred units keep their capacity bounds."""
+        if self._units_pending is None:  # units already built: their exact counts
+            c = self.d_sched_counts.cpu().tolist()
+            self.max_units, self.max_long, self.max_tasks = (max(1, int(c[0])), int(c[1]),
+                                                             max(1, int(c[2])))
         if self.d_work_counts is not None:
             w = self.d_work_counts.cpu().tolist()
             self.max_work, self.max_splits, self.max_partials = int(w[0]), int(w[1]), int(w[2])
@@ -557,9 +558,9 @@ class CacheBuilder:
         self.work_tile = WORK_TILE if sort_work else -1
         # per-frame rebuilds also defer the work units (built on first use)
         # and build the chunk list beside the rank sort (own workspace)
-        self.defer_units = not sort_work
+        self.defer_units = True  # units only for the wide-channel fallbacks: built on first use
         self._grid_arr = grid.as_array()
-        self._one_call = self.defer_units and CHUNK > 0
+        self._one_call = not sort_work and CHUNK > 0
         self.dims = (n_cameras, frustum.height, frustum.width, frustum.depth_bins)
         # tiles: rebuild the tiled reduction's plan with every association
         # (otherwise a cache builds it on first tiled use, with one sync)

@@ -105,3 +105,31 @@ def test_cli_stale_cache_and_verify(tmp_path, capsys):
     assert "PASS" in capsys.readouterr().out
     assert cli.main(["verify", *small, "--corrupt-backend", "interval"]) == 1
     assert "FAIL" in capsys.readouterr().out
+
+
+@pytest.mark.gpu
+def test_cli_pool_naive_is_byte_identical(tmp_path):
+    """The reference CLI's `pool --backend naive` file (bev_naive.bvpt, made by
+    the reference itself) is reproduced byte for byte."""
+    assert cli.main(_pool_args(tmp_path, "--backend", "naive")) == 0
+    assert filecmp.cmp(tmp_path / "bev.bvpt", os.path.join(GOLD, "bev_naive.bvpt"),
+                       shallow=False)
+
+
+@pytest.mark.gpu
+def test_cli_bench_and_csv(tmp_path, capsys):
+    """`bench` (reference cli.py:135-156): stage table and the reference's
+    CSV columns; --sweep runs the three resolutions."""
+    small = ["--cameras", "2", "--height", "8", "--width", "12", "--depth-bins", "9",
+             "--channels", "8", "--grid-extent", "16", "--cell-size", "0.5"]
+    csv_path = tmp_path / "bench.csv"
+    assert cli.main(["bench", *small, "--reps", "2", "--warmups", "1", "--csv", str(csv_path)]) == 0
+    out = capsys.readouterr().out
+    assert "association_cold" in out and "association_cached" in out and "interval" in out
+    lines = csv_path.read_text().splitlines()
+    assert lines[0] == "backend,n_points,channels,stage,median_ms,min_ms,speedup_vs_baseline"
+    stages = {ln.split(",")[3] for ln in lines[1:]}
+    assert stages == {"association_cold", "association_cached", "pool"}
+    assert cli.main(["bench", *small, "--reps", "1", "--warmups", "1", "--sweep",
+                     "--backend", "interval"]) == 0
+    assert capsys.readouterr().out.count("workload:") == 3

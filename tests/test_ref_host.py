@@ -149,3 +149,30 @@ print(json.dumps(res))
         assert equal, red
         assert dev <= 1e-5, (red, dev)
         assert kernel_equal, red
+
+
+def test_reference_cli_with_cuda_backend(host_ref, tmp_path):
+    """The reference's own CLI (cli.py:195-243) with `--backend cuda_exact`
+    writes the same file as its `--backend interval`; `bench --backend cuda`
+    and `verify` run (examples/ref_cli_cuda.py)."""
+    gold = os.path.join(HERE, "golden", "cli")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([REF, ROOT]), OPENBLAS_NUM_THREADS="1",
+               NUMBA_CACHE_DIR=os.environ.get("NUMBA_CACHE_DIR", "/tmp/bvp_numba_cache"))
+
+    def cli(*args):
+        return subprocess.run([sys.executable, "-m", "examples.ref_cli_cuda", *args], env=env,
+                              cwd=ROOT, capture_output=True, text=True, timeout=900)
+
+    files = ["--calib", os.path.join(gold, "calibration.json"),
+             "--features", os.path.join(gold, "features.bvpt"),
+             "--logits", os.path.join(gold, "logits.bvpt"),
+             "--grid-extent", "8.0", "--cell-size", "0.5"]
+    for backend in ("interval", "cuda_exact", "cuda"):
+        r = cli("pool", *files, "--backend", backend, "--out", str(tmp_path / f"{backend}.bvpt"))
+        assert r.returncode == 0, r.stderr
+    a = (tmp_path / "interval.bvpt").read_bytes()
+    assert a == (tmp_path / "cuda_exact.bvpt").read_bytes()
+    small = ["--cameras", "2", "--height", "8", "--width", "12", "--depth-bins", "9",
+             "--channels", "8", "--grid-extent", "16", "--cell-size", "0.5"]
+    r = cli("bench", *small, "--backend", "cuda", "--reps", "2", "--warmups", "1")
+    assert r.returncode == 0 and "cuda" in r.stdout, r.stderr
