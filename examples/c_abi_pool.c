@@ -123,14 +123,9 @@ int main(int argc, char **argv) {
     int64_t host_counts[2], host_wc[3];
     CHECK_CUDA(cudaMemcpy(host_counts, counts, sizeof host_counts, cudaMemcpyDeviceToHost));
     CHECK_CUDA(cudaMemcpy(host_wc, work_counts, sizeof host_wc, cudaMemcpyDeviceToHost));
-    if (bvp_pool_needs_units(C, 0, 0) || bvp_pool_needs_units(C, 0, 1)) {
-        fprintf(stderr, "C = %d needs work units; this example builds only the chunk list\n", C);
-        return 1;
-    }
     bvp_schedule sched;
     memset(&sched, 0, sizeof sched);
     sched.point_meta = meta;
-    sched.order_rep = 1;
     sched.work = work;
     sched.splits = splits;
     sched.work_counts = work_counts;

@@ -43,9 +43,9 @@
  *                           of any run of cells in O(1)
  *   interval_of_point[P]    interval index per point or 0xFFFFFFFF
  *   counts[2] (int64)       n_in, n_int
- * and from bvp_make_schedule the work schedule of the interval kernels
- * (bvp_schedule below).  A whole frame can be rebuilt and pooled without a
- * host round trip.
+ * and from bvp_make_work / bvp_point_meta the chunk schedule of the interval
+ * kernels (bvp_schedule below).  A whole frame can be rebuilt and pooled
+ * without a host round trip.
  */
 #ifndef BEVPOOL_B200_H
 #define BEVPOOL_B200_H
@@ -62,7 +62,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BVP_ABI_VERSION 6
+#define BVP_ABI_VERSION 7
 
 #define BVP_OK 0
 #define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
@@ -88,43 +88,21 @@ extern "C" {
 #define BVP_TILE_PHASE1 0x200
 #define BVP_TILE_PHASE2 0x400
 
-/* Work schedule of the interval kernels (device pointers; built once per
- * cache by bvp_make_schedule).
- *   units       2 x uint32 per unit: first flat cell, cell count (<= 8) with
- *               bit 31 set for a "long" unit (one cell holding more than the
- *               point budget; the fast kernels split it over a CTA)
+/* Chunk schedule of the interval kernels (device pointers; built with the
+ * cache by bvp_make_work / bvp_point_meta).
  *   point_meta  2 x uint32 per sorted point j: feature row n*H*W + h*W + w
  *               and weight index (n*D + d)*H*W + h*W + w of ranks[j]
- *   long_units  unit indices of the long units
- *   tasks       8 x uint32 per task (a run of consecutive units one warp
- *               walks as one point stream): first unit, unit count (bit 31:
- *               long), first and end sorted point, first and end interval
- *   counts      device int64[3]: n_units, n_long, n_tasks
- *   max_units, max_long, max_tasks  host launch sizes (>= the device counts)
- *   order       optional (may be NULL): launch order of the units, a
- *               permutation of [0, n_units) grouping units of one 2D block
- *               of BEV cells so a CTA's warps share feature rows in L1
- *   order_rep   units per warp of the unit kernel (>= 1)
- *   work, splits, work_counts, max_work, max_splits, chunk
- *               optional chunk schedule of the fast kernels from
- *               bvp_make_work (work NULL: none): work = 4 x uint32 per
- *               chunk (first sorted point, end, destination, interval),
- *               chunks of <= `chunk` points sorted by length; splits = 4 x
- *               uint32 per interval cut into several chunks (interval, cell,
- *               first partial slot, chunk count); work_counts = device
- *               int64[3] n_work, n_splits, n_partials; max_work, max_splits,
- *               max_partials host bounds (>= the device counts) */
+ *   work, splits, work_counts, max_work, max_splits, max_partials, chunk
+ *               the chunk list from bvp_make_work (work NULL: none -- the
+ *               reference-order kernel then pools every interval): work = 4 x
+ *               uint32 per chunk (first sorted point, end, destination,
+ *               interval), chunks of <= `chunk` points sorted by length;
+ *               splits = 4 x uint32 per interval cut into several chunks
+ *               (interval, cell, first partial slot, chunk count);
+ *               work_counts = device int64[3] n_work, n_splits, n_partials;
+ *               max_* host bounds (>= the device counts) */
 typedef struct bvp_schedule {
-    const uint32_t *units;
     const uint32_t *point_meta;
-    const uint32_t *long_units;
-    const uint32_t *tasks;
-    const int64_t *counts;
-    int64_t max_units;
-    int64_t max_long;
-    int64_t max_tasks;
-    const uint32_t *order;
-    int64_t order_rep;
     const uint32_t *work;
     const uint32_t *splits;
     const int64_t *work_counts;
@@ -198,24 +176,6 @@ int bvp_build_association(const double *cams, int N, int H, int W, int D,
 
 /* ---- work schedule (cached with the association) ---------------------- */
 
-/* Capacities of the schedule arrays and the builder's workspace. */
-int64_t bvp_units_capacity(int nx, int ny, int64_t n_int_max);
-size_t bvp_units_workspace_bytes(int nx, int ny);
-
-/* Cut the grid into work units (runs of <= 8 cells of one BEV row holding
- * <= budget in-range points, cell order), list the long units, group the
- * units into tasks of ~task_budget points, and fill the point gather table
- * (skipped when point_meta is NULL).  Capacities: units and tasks
- * bvp_units_capacity(), long_units n_cells.  sched_counts: device int64[3]
- * receiving n_units, n_long, n_tasks.  Run after the cache build. */
-int bvp_make_schedule(const uint32_t *ranks, const uint32_t *interval_starts,
-                      const uint32_t *cell_first, const int64_t *counts, int N,
-                      int H, int W, int D, int nx, int ny, int budget,
-                      int task_budget, uint32_t *units, uint32_t *long_units,
-                      uint32_t *tasks, int64_t *sched_counts,
-                      uint32_t *point_meta, void *workspace,
-                      size_t workspace_bytes, void *stream);
-
 /* The point gather table alone (e.g. when a loaded cache's frustum shape is
  * only known at pooling time). */
 int bvp_point_meta(const uint32_t *ranks, const int64_t *counts, int N, int H,
@@ -240,12 +200,6 @@ int bvp_make_work(const uint32_t *interval_starts, const uint32_t *interval_cell
                   void *workspace, size_t workspace_bytes, void *stream);
 
 /* ---- cached forward ---------------------------------------------------- */
-
-/* 1 when pooling C channels (bf16: the fused path) in this mode launches the
- * unit / task kernels, i.e. needs the schedule's units, long_units, tasks and
- * counts; 0 when the chunk schedule (work) alone suffices, so a schedule
- * built without units (all four NULL) may be passed. */
-int bvp_pool_needs_units(int C, int bf16, int exact);
 
 /* Scratch of the fast kernels (the split intervals' partials) for B samples
  * of C channels in `mode`; 0 when the schedule has no chunk schedule. */

@@ -21,7 +21,7 @@ OUT_OF_RANGE = 0xFFFFFFFF
 BVP_OUT_ZEROED = 0x100  # include/bevpool_b200.h
 BVP_TILE_PHASE1 = 0x200
 BVP_TILE_PHASE2 = 0x400
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 
 _P = ctypes.c_void_p
@@ -33,11 +33,8 @@ _S = ctypes.c_size_t
 
 class Schedule(ctypes.Structure):
     """struct bvp_schedule (include/bevpool_b200.h)."""
-    _fields_ = [("units", _P), ("point_meta", _P), ("long_units", _P), ("tasks", _P),
-                ("counts", _P), ("max_units", _L), ("max_long", _L), ("max_tasks", _L),
-                ("order", _P), ("order_rep", _L), ("work", _P), ("splits", _P),
-                ("work_counts", _P), ("max_work", _L), ("max_splits", _L), ("max_partials", _L),
-                ("chunk", _L)]
+    _fields_ = [("point_meta", _P), ("work", _P), ("splits", _P), ("work_counts", _P),
+                ("max_work", _L), ("max_splits", _L), ("max_partials", _L), ("chunk", _L)]
 
 
 _SP = ctypes.POINTER(Schedule)
@@ -68,16 +65,11 @@ SIGNATURES = {
     "bvp_build_association": (_I, [_P, _I, _I, _I, _I, _D, _D, _P, _I, _I, _P, _P, _P, _P, _P, _P,
                                    _P, _I, _P, _P, _P, _P, _P, _S, _P, _S, _P]),
     "bvp_pool_workspace_bytes": (_S, [_I, _I, _I, _I, _I]),
-    "bvp_units_capacity": (_L, [_I, _I, _L]),
-    "bvp_units_workspace_bytes": (_S, [_I, _I]),
-    "bvp_make_schedule": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _P, _P, _P,
-                               _P, _P, _S, _P]),
     "bvp_point_meta": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "bvp_work_capacity": (_L, [_L, _L, _I]),
     "bvp_work_workspace_bytes": (_S, [_L, _L, _I, _I, _I, _I]),
     "bvp_make_work": (_I, [_P, _P, _P, _L, _L, _I, _I, _I, _I, _P, _P, _P, _P, _S, _P]),
     "bvp_pool_scratch_bytes": (_S, [_SP, _I, _I, _I]),
-    "bvp_pool_needs_units": (_I, [_I, _I, _I]),
     "bvp_pool_forward_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I, _I,
                                   _L, _I, _I, _P, _P, _P, _P, _S, _P]),
     "bvp_pool_forward_nhwc_f32": (_I, [_P, _P, _P, _P, _P, _P, _SP, _I, _I, _I, _I, _I, _I, _I,

@@ -35,8 +35,7 @@ class _BevPoolFn(torch.autograd.Function):
         _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
                   ptr(cache.d_cell_first),
-                  cache.schedule(N, H, W, D, units=cache.needs_units(C, exact=bool(exact)),
-                                 exact=bool(exact)),
+                  cache.schedule(N, H, W, D, exact=bool(exact)),
                   B, N, C, H, W, D, nx, ny,
                   cache.n_int_max,
                   _MODE[reducer], int(exact), ptr(out), ptr(nhwc), ptr(argmax),

@@ -131,10 +131,6 @@ def _u32(t: torch.Tensor) -> np.ndarray:
     return to_numpy(t).view(np.uint32)
 
 
-#: points per work unit of the interval kernels (csrc/units.cu)
-UNIT_BUDGET = 128
-#: points per warp task (a run of consecutive units walked as one stream)
-TASK_BUDGET = 384
 #: chunk length of the fast kernels' work list (csrc/work.cu); 0 disables it
 CHUNK = 64
 #: chunk order: 0 = longest first (cell order within a length); > 0 = by 2D
@@ -238,7 +234,7 @@ class AssociationCache:
     ``ranks`` lists the in-range point ids sorted by cell (stable); interval
     i covers ranks[interval_starts[i] : interval_starts[i+1]] and all its
     points share cell interval_cells[i].  Immutable after build.  ``nx, ny``
-    is the grid shape the work units were cut for.
+    is the grid shape the cell tables were cut for.
     """
 
     d_cell_of_point: torch.Tensor          # (P,)
@@ -248,14 +244,7 @@ class AssociationCache:
     d_cell_first: torch.Tensor             # (n_cells + 1,)
     d_interval_of_point: torch.Tensor      # (P,)
     d_counts: torch.Tensor                 # (2,) int64: n_in, n_int
-    d_units: torch.Tensor                  # (2 * max_units,) (first cell, count | long)
-    d_long_units: torch.Tensor             # (max_long,) unit ids of split cells
-    d_tasks: torch.Tensor                  # (8 * max_tasks,) warp tasks
-    d_sched_counts: torch.Tensor           # (3,) int64: n_units, n_long, n_tasks
     d_meta: torch.Tensor                   # (2 * P,) per sorted point: row, weight index
-    max_units: int                         # launch bounds (>= the device counts)
-    max_long: int
-    max_tasks: int
     fingerprint: int
     nx: int
     ny: int
@@ -273,7 +262,6 @@ class AssociationCache:
     chunk: int = 0
     _host_counts: tuple | None = field(default=None, repr=False)
     _host: dict = field(default_factory=dict, repr=False)
-    _units_pending: object = field(default=None, repr=False)  # deferred units build
 
     # ---- sizes ----------------------------------------------------------
     @property
@@ -307,23 +295,8 @@ class AssociationCache:
         """Capacity of the interval tables (no host sync)."""
         return int(self.d_interval_cells.shape[0])
 
-    @property
-    def n_units(self) -> int:
-        self.ensure_units()
-        return int(self.d_sched_counts[0].item())
-
-    @property
-    def n_long(self) -> int:
-        self.ensure_units()
-        return int(self.d_sched_counts[1].item())
-
     def fit_launch(self) -> None:
-        """Shrink the launch bounds to the exact chunk (and, when built, unit)
-        counts (one host sync).  Deferred units keep their capacity bounds."""
-        if self._units_pending is None:  # units already built: their exact counts
-            c = self.d_sched_counts.cpu().tolist()
-            self.max_units, self.max_long, self.max_tasks = (max(1, int(c[0])), int(c[1]),
-                                                             max(1, int(c[2])))
+        """Shrink the launch bounds to the exact chunk counts (one host sync)."""
         if self.d_work_counts is not None:
             w = self.d_work_counts.cpu().tolist()
             self.max_work, self.max_splits, self.max_partials = int(w[0]), int(w[1]), int(w[2])
@@ -332,22 +305,17 @@ class AssociationCache:
         self._host.pop("scratch", None)
 
     def schedule(self, N: int | None = None, H: int = 1, W: int = 1, D: int = 1, *,
-                 units: bool = True, exact: bool = False):
+                 exact: bool = False):
         """The bvp_schedule the C ABI takes; the point gather table is
         (re)derived for an (N, H, W, D) frustum (N=None: the caller does not
-        read it, e.g. the materialised path).  units=False: the caller's
-        launch needs only the chunk schedule (bvp_pool_needs_units), so units
-        deferred by a per-frame build are not built for it.  exact=True: the
-        exact mode's own chunk list (EXACT_CHUNK), built on first use."""
+        read it, e.g. the materialised path).  exact=True: the exact mode's
+        own chunk list (EXACT_CHUNK), built on first use."""
         if N is not None and self.meta_dims != (N, H, W, D):
             _lib.call("bvp_point_meta", ptr(self.d_ranks), ptr(self.d_counts), N, H, W, D,
                       ptr(self.d_meta), stream_ptr(self.device))
             self.meta_dims = (N, H, W, D)
-        with_units = units or self.d_work is None
-        if with_units:
-            self.ensure_units()
         xw = self.exact_work() if exact and self.d_work is not None else None
-        key = ("schedules", self._units_pending is None, xw is not None)
+        key = ("schedules", xw is not None)
         s = self._host.get(key)
         if s is None:
             work = (None, None, None, 0, 0, 0, 0)
@@ -357,13 +325,7 @@ class AssociationCache:
             elif self.d_work is not None:
                 work = (ptr(self.d_work), ptr(self.d_splits), ptr(self.d_work_counts),
                         self.max_work, self.max_splits, self.max_partials, self.chunk)
-            if self._units_pending is None:
-                s = _lib.Schedule(ptr(self.d_units), ptr(self.d_meta), ptr(self.d_long_units),
-                                  ptr(self.d_tasks), ptr(self.d_sched_counts), self.max_units,
-                                  self.max_long, self.max_tasks, None, 1, *work)
-            else:  # units not built: the kernels see NULL and refuse to use them
-                s = _lib.Schedule(None, ptr(self.d_meta), None, None, None, 0, 0, 0, None, 1,
-                                  *work)
+            s = _lib.Schedule(ptr(self.d_meta), *work)
             self._host[key] = s
         return s
 
@@ -400,20 +362,10 @@ class AssociationCache:
             self._host["exact_work"] = xw
         return xw
 
-    def ensure_units(self) -> None:
-        """Build the work units / tasks a per-frame build deferred (stream
-        ordered, no host sync)."""
-        if self._units_pending is not None:
-            build, self._units_pending = self._units_pending, None
-            build()
-
-    def needs_units(self, C: int, bf16: bool = False, exact: bool = False) -> bool:
-        return bool(_lib.load().bvp_pool_needs_units(C, int(bf16), int(exact)))
-
     def scratch(self, B: int, C: int, mode: int) -> torch.Tensor | None:
         """Scratch of the fast kernels (split-interval partials), kept per
         (B, C, mode) shape."""
-        n = int(_lib.load().bvp_pool_scratch_bytes(self.schedule(units=False), B, C, mode))
+        n = int(_lib.load().bvp_pool_scratch_bytes(self.schedule(), B, C, mode))
         if n == 0:
             return None
         key = (B, C, mode == 2)
@@ -453,7 +405,7 @@ class AssociationCache:
         return self._view("interval_of_point", self.d_interval_of_point, self.n_points)
 
     def for_grid(self, grid: BevGridSpec) -> "AssociationCache":
-        """This cache with cell tables / work units cut for ``grid``'s shape.
+        """This cache with cell tables / chunk list cut for ``grid``'s shape.
         Caches loaded from disk carry no grid (reference bevgrid.py:110-113);
         their tables are re-derived once per pooling grid shape."""
         if (grid.nx, grid.ny) == (self.nx, self.ny):
@@ -470,9 +422,8 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
     i32 = dict(dtype=torch.int32, device=dev)
     lib = _lib.load()
     n_cells = nx * ny
-    cap = int(lib.bvp_units_capacity(nx, ny, n_cells))
     n_int_max = min(n_cells, P)
-    ws = max(lib.bvp_sort_workspace_bytes(P, n_cells), lib.bvp_units_workspace_bytes(nx, ny),
+    ws = max(lib.bvp_sort_workspace_bytes(P, n_cells),
              lib.bvp_work_workspace_bytes(n_int_max, P, CHUNK, nx, ny, WORK_TILE)
              if CHUNK > 0 else 0)
     work = {}
@@ -487,51 +438,32 @@ def _alloc(P: int, nx: int, ny: int, dev) -> dict:
         starts=torch.empty(n_cells + 1, **i32), icells=torch.empty(n_cells, **i32),
         cell_first=torch.empty(n_cells + 1, **i32), iop=torch.empty(P, **i32),
         counts=torch.zeros(2, dtype=torch.int64, device=dev),
-        units=torch.empty(4 * (cap + 1), **i32), long_units=torch.empty(n_cells, **i32),
-        tasks=torch.empty(8 * cap, **i32),
-        sched_counts=torch.zeros(3, dtype=torch.int64, device=dev),
         meta=torch.empty(2 * P, **i32),
-        cap=cap, ws=torch.empty(ws, dtype=torch.uint8, device=dev),
+        ws=torch.empty(ws, dtype=torch.uint8, device=dev),
     )
 
 
-def _make_schedule(b: dict, nx: int, ny: int, budget: int, dev, dims=None,
-                   task_budget: int = TASK_BUDGET, work_tile: int = WORK_TILE,
-                   defer_units: bool = False, work_done: bool = False):
-    """Chunk schedule (work) and point gather table, plus the work units and
-    tasks -- or, defer_units, a closure that builds the units later (only the
-    exact mode and very wide channel counts read them).  Returns the closure
-    or None."""
-    N, H, W, D = dims if dims is not None else (1, 1, 1, 1)
-
-    def units(meta=dims is not None and not defer_units):
-        _lib.call("bvp_make_schedule", ptr(b["ranks"]), ptr(b["starts"]), ptr(b["cell_first"]),
-                  ptr(b["counts"]), N, H, W, D, nx, ny, budget, task_budget, ptr(b["units"]),
-                  ptr(b["long_units"]), ptr(b["tasks"]), ptr(b["sched_counts"]),
-                  ptr(b["meta"]) if meta else None, ptr(b["ws"]), b["ws"].numel(),
-                  stream_ptr(dev))
-
+def _make_schedule(b: dict, nx: int, ny: int, dev, dims=None, work_tile: int = WORK_TILE,
+                   work_done: bool = False) -> None:
+    """The chunk schedule (work) of the interval kernels and the point gather
+    table (stream ordered, no sync)."""
     if "work" in b and not work_done:
         _lib.call("bvp_make_work", ptr(b["starts"]), ptr(b["icells"]), ptr(b["counts"]),
                   b["n_int_max"], b["ranks"].numel(), CHUNK, nx, ny, work_tile, ptr(b["work"]),
-                  ptr(b["splits"]),
-                  ptr(b["work_counts"]), ptr(b["ws"]), b["ws"].numel(), stream_ptr(dev))
-    if defer_units and "work" in b:
-        if dims is not None and not work_done:
-            _lib.call("bvp_point_meta", ptr(b["ranks"]), ptr(b["counts"]), N, H, W, D,
-                      ptr(b["meta"]), stream_ptr(dev))
-        return lambda: units(False)
-    units()
-    return None
+                  ptr(b["splits"]), ptr(b["work_counts"]), ptr(b["ws"]), b["ws"].numel(),
+                  stream_ptr(dev))
+    if dims is not None and not work_done:
+        N, H, W, D = dims
+        _lib.call("bvp_point_meta", ptr(b["ranks"]), ptr(b["counts"]), N, H, W, D,
+                  ptr(b["meta"]), stream_ptr(dev))
 
 
 def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, dims=None):
     """A cache over the buffers b; launch bounds are the capacities until
     fit_launch() (no host sync needed to pool)."""
     cache = AssociationCache(b["cells"], b["ranks"], b["starts"], b["icells"], b["cell_first"],
-                             b["iop"], b["counts"], b["units"], b["long_units"], b["tasks"],
-                             b["sched_counts"], b["meta"], b["cap"], int(b["long_units"].numel()),
-                             b["cap"], fingerprint, nx, ny, n_cameras, frustum, grid, dims)
+                             b["iop"], b["counts"], b["meta"], fingerprint, nx, ny, n_cameras,
+                             frustum, grid, dims)
     if "work" in b:
         cache.d_work, cache.d_splits, cache.d_work_counts = b["work"], b["splits"], b["work_counts"]
         cache.max_work, cache.max_splits, cache.max_partials = b["work_bounds"]
@@ -542,23 +474,20 @@ def _cache_of(b: dict, fingerprint, nx, ny, n_cameras, frustum, grid, dims=None)
 class CacheBuilder:
     """Re-usable GPU association builder: buffers and workspace are allocated
     once for a (frustum, grid) shape and every ``build`` reruns geometry +
-    sort + interval tables + work units on the current stream with no host
+    sort + interval tables + chunk list on the current stream with no host
     round trip (config H: uncached geometry every frame).  The returned cache
     aliases the builder's buffers until the next ``build``."""
 
     def __init__(self, n_cameras: int, frustum: FrustumSpec, grid: BevGridSpec, device=None,
-                 unit_budget: int = UNIT_BUDGET, sort_work: bool = False, tiles: bool = False):
+                 sort_work: bool = False, tiles: bool = False):
         self.dev = cuda_device(device)
         self.n_cameras, self.frustum, self.grid = n_cameras, frustum, grid
         self.P = n_cameras * frustum.points_per_camera
         self.bufs = _alloc(self.P, grid.nx, grid.ny, self.dev)
-        self.unit_budget = unit_budget
         # per-frame rebuilds keep the chunk list in cell order (the length
-        # sort costs more than it saves once per frame); cached builds sort
+        # sort costs more than it saves once per frame) and build it beside
+        # the rank sort (own workspace); cached builds sort it
         self.work_tile = WORK_TILE if sort_work else -1
-        # per-frame rebuilds also defer the work units (built on first use)
-        # and build the chunk list beside the rank sort (own workspace)
-        self.defer_units = True  # units only for the wide-channel fallbacks: built on first use
         self._grid_arr = grid.as_array()
         self._one_call = not sort_work and CHUNK > 0
         self.dims = (n_cameras, frustum.height, frustum.width, frustum.depth_bins)
@@ -586,20 +515,15 @@ class CacheBuilder:
                       ptr(b["counts"]), CHUNK, ptr(b["work"]), ptr(b["splits"]),
                       ptr(b["work_counts"]), ptr(b["meta"]), ptr(b["ws"]), b["ws"].numel(),
                       ptr(b["wws"]), b["wws"].numel(), stream_ptr(self.dev))
-            pending = _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims,
-                                     defer_units=True, work_done=True)
             cache = _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
-            cache._units_pending = pending
             return self._with_tiles(cache)
         _lib.call("bvp_build_cache", ptr(cams), self.n_cameras, f.height, f.width, f.depth_bins,
                   f.depth_min, f.depth_step, self._grid_arr.ctypes.data, g.nx, g.ny,
                   ptr(b["cells"]), ptr(b["ranks"]), ptr(b["starts"]), ptr(b["icells"]),
                   ptr(b["cell_first"]), ptr(b["iop"]), ptr(b["counts"]), ptr(b["ws"]),
                   b["ws"].numel(), stream_ptr(self.dev))
-        pending = _make_schedule(b, g.nx, g.ny, self.unit_budget, self.dev, dims,
-                                 work_tile=self.work_tile, defer_units=self.defer_units)
+        _make_schedule(b, g.nx, g.ny, self.dev, dims, work_tile=self.work_tile)
         cache = _cache_of(b, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
-        cache._units_pending = pending
         return self._with_tiles(cache)
 
     def _with_tiles(self, cache: AssociationCache) -> AssociationCache:
@@ -631,11 +555,10 @@ def build_cache(rig: list[CameraCalibration], frustum_spec: FrustumSpec,
 
 
 def cache_from_cells(cell_of_point, nx: int, ny: int, fingerprint: int = 0, n_cameras=None,
-                     frustum=None, grid=None, device=None,
-                     unit_budget: int = UNIT_BUDGET) -> AssociationCache:
+                     frustum=None, grid=None, device=None) -> AssociationCache:
     """Association cache from given cell ids (a loaded file, a synthetic test
     cache) for an nx x ny grid: GPU stable sort + interval tables
-    (bevgrid.py:142-158) + work units."""
+    (bevgrid.py:142-158) + the chunk list."""
     dev = cuda_device(device)
     cells = np.ascontiguousarray(cell_of_point, dtype=np.uint32)
     P = int(cells.shape[0])
@@ -653,7 +576,7 @@ def cache_from_cells(cell_of_point, nx: int, ny: int, fingerprint: int = 0, n_ca
     dims = None
     if frustum is not None and n_cameras is not None:
         dims = (n_cameras, frustum.height, frustum.width, frustum.depth_bins)
-    _make_schedule(b, nx, ny, unit_budget, dev, dims)
+    _make_schedule(b, nx, ny, dev, dims)
     cache = _cache_of(b, fingerprint, nx, ny, n_cameras, frustum, grid, dims)
     cache._counts()
     cache.fit_launch()

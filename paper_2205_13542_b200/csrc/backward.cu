@@ -17,7 +17,7 @@
 // reduction instead of 32 separate butterflies.
 #include <algorithm>
 
-#include "pool_group.cuh"
+#include "pool_kernel.cuh"
 
 namespace bvp {
 

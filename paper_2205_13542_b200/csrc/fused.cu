@@ -1,11 +1,11 @@
 // fused.cu -- config F: lift + pool fused, bf16 inputs, fp32 accumulation.
 //
-// The frustum tensor x = softmax_D(logits) (x) context is never formed: a
-// small prologue computes each pixel's log-sum-exp over D (N*H*W floats) and
-// the NHWC bf16 copy of the context; the interval kernel then forms
-// exp(logit - lse) * context[c] in registers per point (pool_kernel.cuh,
-// kSrcFused).  Reference semantics: normalize_depth (lift.py:17-31) followed
-// by pool_interval (pooling.py:206-221).
+// The fast path is the tiled kernel (tile.cu, the softmax formed in shared
+// memory); this file holds its fallback for MAX and channel counts above 128
+// -- a prologue writes the fp32 softmax weights and the NHWC bf16 copy of the
+// context, the interval kernels pool them -- and the fused backward.
+// Reference semantics: normalize_depth (lift.py:17-31) followed by
+// pool_interval (pooling.py:206-221).
 #include <algorithm>
 #include <cstdlib>
 
@@ -14,70 +14,18 @@
 namespace bvp {
 
 template <>
-int run_pool<float, __nv_bfloat16, 8, kSrcFused>(const PoolParams &p, int B, bool is_max,
-                                                 cudaStream_t s) {
-    return run_pool_fast<__nv_bfloat16, 8, kSrcFused>(p, B, is_max, s);
-}
-template <>
 int run_pool<float, __nv_bfloat16, 8, kSrcDist>(const PoolParams &p, int B, bool is_max,
                                                 cudaStream_t s) {
     return run_pool_fast<__nv_bfloat16, 8, kSrcDist>(p, B, is_max, s);
 }
 template <>
-int run_pool<float, __nv_bfloat16, 1, kSrcFused>(const PoolParams &p, int B, bool is_max,
-                                                 cudaStream_t s) {
-    return run_pool_fast<__nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);
+int run_pool<float, __nv_bfloat16, 1, kSrcDist>(const PoolParams &p, int B, bool is_max,
+                                                cudaStream_t s) {
+    return run_pool_fast<__nv_bfloat16, 1, kSrcDist>(p, B, is_max, s);
 }
 
-// lse[pix] = max_d l + log(sum_d exp(l - max)).  A CTA covers 32 consecutive
-// pixels of one camera; its 8 warps split the D depth planes (warp w takes
-// d = w, w+8, ...), so each warp's loads are 64 contiguous bytes of one
-// plane and every thread keeps ~D/8 independent loads in flight.  Partial
-// (max, sum) pairs are merged in shared memory.
-constexpr int kLseWarps = 8;
-__global__ void __launch_bounds__(32 * kLseWarps)
-pixel_lse_kernel(const __nv_bfloat16 *__restrict__ logits, int64_t NB, int D, int HW,
-                 float *__restrict__ lse) {
-    __shared__ float s_m[kLseWarps][32], s_s[kLseWarps][32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tiles = (HW + 31) / 32;
-    const int64_t n = blockIdx.x / tiles;
-    const int hw = (blockIdx.x - n * tiles) * 32 + lane;
-    const bool ok = hw < HW;
-    const __nv_bfloat16 *l = logits + n * D * int64_t(HW) + (ok ? hw : 0);
-    float m = -INFINITY, sum = 0.f;
-    int d = warp;
-#pragma unroll 1
-    for (; d + 3 * kLseWarps < D; d += 4 * kLseWarps) {
-        float v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = __bfloat162float(l[int64_t(d + k * kLseWarps) * HW]);
-        const float mm = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-        const float nm = fmaxf(m, mm);
-        sum = sum * __expf(m - nm) + __expf(v[0] - nm) + __expf(v[1] - nm) + __expf(v[2] - nm) +
-              __expf(v[3] - nm);
-        m = nm;
-    }
-    for (; d < D; d += kLseWarps) {
-        const float v = __bfloat162float(l[int64_t(d) * HW]);
-        const float nm = fmaxf(m, v);
-        sum = sum * __expf(m - nm) + __expf(v - nm);
-        m = nm;
-    }
-    s_m[warp][lane] = m;
-    s_s[warp][lane] = sum;
-    __syncthreads();
-    if (warp == 0 && ok) {
-        float M = s_m[0][lane];
-        for (int w = 1; w < kLseWarps; ++w) M = fmaxf(M, s_m[w][lane]);
-        float S = 0.f;
-        for (int w = 0; w < kLseWarps; ++w)
-            if (s_m[w][lane] != -INFINITY) S += s_s[w][lane] * __expf(s_m[w][lane] - M);
-        lse[n * HW + hw] = M + __logf(S);
-    }
-}
+constexpr int kLseWarps = 8;  // warps per CTA of the softmax prologue (32 pixels each)
 
-// The same per-pixel log-sum-exp, then every depth weight
 // w[n,d,h,w] = exp(l - lse) written once (fp32, N x D x H x W -- the depth
 // distribution, not the N x D x H x W x C frustum): the pooling kernel then
 // gathers one weight per point instead of a logit and a log-sum-exp.
@@ -171,8 +119,7 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     BVP_REQUIRE(workspace && workspace_bytes >= L.bytes, BVP_ERR_INVALID,
                 "fused workspace too small: need %zu bytes", L.bytes);
     BVP_REQUIRE(logits && (C == 0 || (out && context && ranks && interval_starts &&
-                                      interval_cells && cell_first && schedule &&
-                                      ((schedule->units && schedule->counts) || schedule->work))),
+                                      interval_cells && cell_first && schedule)),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     cudaStream_t s = as_stream(stream);
@@ -184,25 +131,22 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     const unsigned lb = static_cast<unsigned>(NB * ceil_div(HW, 32));
     // the softmax weights are precomputed per (n, d, h, w) by the prologue
     // (measured 91 us vs 99 us for exp(logit - lse) per point at the
-    // nuScenes shape); the weight-gather kernel needs 16-byte chunks
+    // nuScenes shape); this path is the fallback of the tiled fused kernel
+    // (MAX, channel counts above 128)
     float *wsm = reinterpret_cast<float *>(ws + L.off_w);
-    const bool use_w = C % 8 == 0;
-    const bool zero_beside = false;  // the map is zero-filled beside the prologue
     // three independent prologue branches (forked streams): the depth
     // softmax, the context's NHWC staging, the map's zero fill
     {
         SideFork f1(s, 0), f2(s, 1);
-        if (use_w) pixel_softmax_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), wsm);
-        else pixel_lse_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), lse);
+        pixel_softmax_kernel<<<lb, 32 * kLseWarps, 0, s>>>(lg, NB, D, int(HW), wsm);
         launch_to_nhwc<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16 *>(context), NB, C,
                                       int(HW), ctx, f1.side);
-        if (!zero_beside) cudaMemsetAsync(out, 0, size_t(B) * C * nx * ny * sizeof(float), f2.side);
+        cudaMemsetAsync(out, 0, size_t(B) * C * nx * ny * sizeof(float), f2.side);
     }
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
                                     C, nx, ny, out, mode);
     p.rows = ctx;
-    p.wsrc = lg;
-    p.lse = lse;
+    p.wsrc = wsm;
     p.D = D;
     p.HW = int(HW);
     p.NHW = int(N * HW);
@@ -210,16 +154,10 @@ int bvp_fused_pool_bf16(const uint16_t *logits, const uint16_t *context, const u
     p.w_bstride = int64_t(N) * D * HW;
     p.scratch = scratch;
     p.scratch_bytes = scratch_bytes;
-    p.out_zeroed = zero_beside ? 0 : 1;
+    p.out_zeroed = 1;
     const bool is_max = mode == BVP_MAX;
-    if (use_w) {
-        p.wsrc = wsm;
-        const int rcw = run_pool<float, __nv_bfloat16, 8, kSrcDist>(p, B, is_max, s);
-        if (rcw != BVP_OK) return rcw;
-        return check_launch("fused_pool_bf16");
-    }
-    const int rc = (C % 8 == 0) ? run_pool<float, __nv_bfloat16, 8, kSrcFused>(p, B, is_max, s)
-                                : run_pool<float, __nv_bfloat16, 1, kSrcFused>(p, B, is_max, s);
+    const int rc = (C % 8 == 0) ? run_pool<float, __nv_bfloat16, 8, kSrcDist>(p, B, is_max, s)
+                                : run_pool<float, __nv_bfloat16, 1, kSrcDist>(p, B, is_max, s);
     if (rc != BVP_OK) return rc;
     return check_launch("fused_pool_bf16");
 }

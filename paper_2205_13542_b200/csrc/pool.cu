@@ -101,16 +101,7 @@ PoolParams make_pool_params(const uint32_t *ranks, const uint32_t *starts, const
     p.starts = starts;
     p.icells = icells;
     p.cell_first = cell_first;
-    p.units = sched->units;
     p.meta = reinterpret_cast<const uint2 *>(sched->point_meta);
-    p.long_units = sched->long_units;
-    p.tasks = reinterpret_cast<const uint4 *>(sched->tasks);
-    p.sched_counts = sched->counts;
-    p.max_units = sched->max_units;
-    p.max_long = sched->max_long;
-    p.max_tasks = sched->max_tasks;
-    p.order = sched->order;
-    p.order_rep = sched->order_rep > 0 ? sched->order_rep : 1;
     p.work = reinterpret_cast<const uint4 *>(sched->work);
     p.splits = reinterpret_cast<const uint4 *>(sched->splits);
     p.work_counts = sched->work_counts;
@@ -297,8 +288,7 @@ static int pool_forward_nhwc(const float *feats_nhwc, const float *dist, const u
     BVP_REQUIRE(mode >= 0 && mode <= 2 || (mode == BVP_MEAN_DIV && exact), BVP_ERR_INVALID,
                 "bad mode %d", mode);
     BVP_REQUIRE(C == 0 || (out && feats_nhwc && dist && ranks && interval_starts &&
-                           interval_cells && cell_first && schedule &&
-                           ((schedule->units && schedule->counts) || schedule->work)),
+                           interval_cells && cell_first && schedule),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,
@@ -449,8 +439,7 @@ int bvp_pool_lifted_f32(const float *x, const uint32_t *ranks, const uint32_t *i
     BVP_REQUIRE(C >= 0 && nx >= 1 && ny >= 1 && mode >= 0 && mode <= 2, BVP_ERR_INVALID,
                 "bad arguments");
     BVP_REQUIRE(C == 0 || (out && x && ranks && interval_starts && interval_cells && cell_first &&
-                           schedule &&
-                           ((schedule->units && schedule->counts) || schedule->work)),
+                           schedule),
                 BVP_ERR_INVALID, "null pointer argument");
     if (C == 0) return BVP_OK;
     PoolParams p = make_pool_params(ranks, interval_starts, interval_cells, cell_first, schedule,

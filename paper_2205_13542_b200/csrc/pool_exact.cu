@@ -7,13 +7,13 @@ namespace bvp {
 template <>
 int run_pool<double, float, 4, kSrcDist>(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     const int rc = run_pool_ivl<float, 4, kSrcDist, true>(p, B, is_max, s);
-    return rc != BVP_ERR_UNSUPPORTED ? rc : run_pool_impl<double, float, 4, kSrcDist>(p, B, is_max, s);
+    return rc != BVP_ERR_UNSUPPORTED ? rc : run_pool_ref<float, kSrcDist>(p, B, is_max, s);
 }
 
 template <>
 int run_pool<double, float, 1, kSrcDist>(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     const int rc = run_pool_ivl<float, 1, kSrcDist, true>(p, B, is_max, s);
-    return rc != BVP_ERR_UNSUPPORTED ? rc : run_pool_impl<double, float, 1, kSrcDist>(p, B, is_max, s);
+    return rc != BVP_ERR_UNSUPPORTED ? rc : run_pool_ref<float, kSrcDist>(p, B, is_max, s);
 }
 
 }  // namespace bvp

@@ -18,13 +18,6 @@ int run_pool<float, float, 1, kSrcDist>(const PoolParams &p, int B, bool is_max,
 
 using namespace bvp;
 
-extern "C" int bvp_pool_needs_units(int C, int bf16, int exact) {
-    (void)exact;  // both modes run on the chunk schedule when the width fits
-    const int vec = bf16 ? (C % 8 == 0 ? 8 : 1) : (C % 4 == 0 ? 4 : 1);
-    int L, lg, cpl;
-    return choose_group(C / vec, vec, L, lg, cpl) ? 0 : 1;
-}
-
 // Zero fill of the empty cells of out (B, C, n_cells): the cells no interval
 // covers (cell_first[c] == cell_first[c+1]).  Occupied cells are left as they are.
 extern "C" int bvp_zero_empty_cells(const uint32_t *cell_first, int64_t n_cells, int C, int B,

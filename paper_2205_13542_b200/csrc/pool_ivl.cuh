@@ -33,7 +33,8 @@
 #include <cstdlib>
 #include <type_traits>
 
-#include "pool_group.cuh"
+#include "pool_kernel.cuh"
+#include "pool_ref.cuh"
 
 namespace bvp {
 
@@ -138,9 +139,6 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
         if (li + k * L < nch) live |= 1u << k;
     const Elem *rows = static_cast<const Elem *>(P.rows) + b * P.rows_bstride + li * VEC;
     const float *wdist = static_cast<const float *>(P.wsrc) + (SRC == kSrcDist ? b * P.w_bstride : 0);
-    const __nv_bfloat16 *wlog =
-        static_cast<const __nv_bfloat16 *>(P.wsrc) + (SRC == kSrcFused ? b * P.w_bstride : 0);
-    const float *lse = P.lse + (SRC == kSrcFused ? int64_t(b) * P.NHW : 0);
     const uint32_t Cu = static_cast<uint32_t>(C);
     const int64_t n_work = P.work_counts[0];
     const int64_t n_part = P.max_splits > 0 ? P.work_counts[2] : 0;
@@ -182,7 +180,6 @@ pool_ivl_kernel(const PoolParams P, int L, int lg) {
             const bool ok = s < len;
             w = 1.f;
             if (SRC == kSrcDist) w = ok ? __ldg(wdist + m.y) : 0.f;
-            else if (SRC == kSrcFused) w = ok ? __expf(__bfloat162float(wlog[m.y]) - __ldg(lse + m.x)) : 0.f;
             const Elem *rp = rows + m.x * Cu;
 #pragma unroll
             for (int k = 0; k < CPL; ++k) {
@@ -402,10 +399,7 @@ template <typename Elem, int VEC, int SRC>
 int run_pool_fast(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     const int rc = run_pool_ivl<Elem, VEC, SRC>(p, B, is_max, s);
     if (rc != BVP_ERR_UNSUPPORTED) return rc;
-    int L, lg, cpl;
-    if (p.tasks && choose_group(p.C / VEC, VEC, L, lg, cpl))
-        return run_pool_group<Elem, VEC, SRC>(p, B, is_max, s);
-    return run_pool_impl<float, Elem, VEC, SRC>(p, B, is_max, s);
+    return run_pool_ref<Elem, SRC>(p, B, is_max, s);  // channel widths the chunk kernel lacks
 }
 
 }  // namespace bvp

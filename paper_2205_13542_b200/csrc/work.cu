@@ -19,6 +19,9 @@
 // The order of chunks of equal length is whatever the atomics produce; it
 // changes no output bit (every chunk is summed by one group in rank order and
 // partials are combined in slot order).
+//
+// The point gather table (point_meta) turns every sorted point's id into its
+// feature row and weight index once, so the interval kernels never divide.
 #include <algorithm>
 
 #include "scan.cuh"
@@ -99,6 +102,20 @@ __global__ void work_counts_kernel(const uint4 *__restrict__ tot, int64_t *__res
     out[2] = t.y;  // partials
 }
 
+// Per sorted point: (feature row = pixel, weight index into (N,D,H,W)).
+__global__ void point_meta_kernel(const uint32_t *__restrict__ ranks,
+                                  const int64_t *__restrict__ counts, int64_t P, int D, int HW,
+                                  uint2 *__restrict__ meta) {
+    const int64_t n_in = counts[0];
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n_in && j < P;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = ranks[j];
+        const uint32_t pix = p / D, d = p - pix * D;
+        const uint32_t n = pix / HW, hw = pix - n * HW;
+        meta[j] = make_uint2(pix, (n * D + d) * HW + hw);
+    }
+}
+
 struct WorkLayout {
     size_t off_cnt, off_part, off_tot, off_tmp, off_keys, off_order,
         off_sstarts, off_scells, off_sfirst, off_scounts, off_sws, sort_ws, bytes;
@@ -138,6 +155,17 @@ static WorkLayout work_layout(int64_t n_int_max, int64_t n_points, int chunk, in
 using namespace bvp;
 
 extern "C" {
+
+int bvp_point_meta(const uint32_t *ranks, const int64_t *counts, int N, int H, int W, int D,
+                   uint32_t *point_meta, void *stream) {
+    BVP_REQUIRE(ranks && counts && point_meta, BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(N >= 1 && H >= 1 && W >= 1 && D >= 1, BVP_ERR_INVALID, "bad dims");
+    const int64_t P = int64_t(N) * H * W * D;
+    const unsigned mb = static_cast<unsigned>(std::min<int64_t>(ceil_div(P, 256), int64_t(148) * 32));
+    point_meta_kernel<<<mb, 256, 0, as_stream(stream)>>>(ranks, counts, P, D, H * W,
+                                                         reinterpret_cast<uint2 *>(point_meta));
+    return check_launch("point_meta");
+}
 
 int64_t bvp_work_capacity(int64_t n_int_max, int64_t n_points, int chunk) {
     return work_cap(n_int_max, n_points, chunk);

@@ -209,8 +209,7 @@ def pool_interval(features, dist, cache: AssociationCache, grid: BevGridSpec,
         _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
                   ptr(cache.d_cell_first),
-                  cache.schedule(inp.N, inp.H, inp.W, inp.D,
-                                 units=cache.needs_units(inp.C, exact=exact), exact=bool(exact)),
+                  cache.schedule(inp.N, inp.H, inp.W, inp.D, exact=bool(exact)),
                   inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
                   grid.nx, grid.ny, cache.n_int_max, _MODE[reducer],
                   exact, ptr(out), ptr(nhwc), None,
@@ -279,7 +278,6 @@ class PoolPlan:
         self.exact = int(DEFAULT_EXACT if exact is None else exact)
         self._tile = _tile_plan(self.cache, n_cameras, height, width, depth_bins, channels,
                                 self.mode, self.exact)
-        self._units = self.cache.needs_units(channels, exact=self.exact)
         f32 = dict(dtype=torch.float32, device=self.dev)
         self.out = torch.empty((batch, channels, grid.n_cells), **f32)
         self.nhwc = torch.empty(batch * n_cameras * height * width * channels, **f32)
@@ -331,8 +329,7 @@ class PoolPlan:
         c = self.cache
         _lib.call("bvp_pool_forward_nhwc_f32", ptr(self.nhwc), ptr(dist), ptr(c.d_ranks),
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
-                  c.schedule(self.N, self.H, self.W, self.D, units=self._units,
-                             exact=bool(self.exact)), self.B,
+                  c.schedule(self.N, self.H, self.W, self.D, exact=bool(self.exact)), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
                   mode, self.exact, ptr(out), None, *self._scratch, stream_ptr(self.dev))
         return out
@@ -349,8 +346,7 @@ class PoolPlan:
         c = self.cache
         _lib.call("bvp_pool_forward_f32", ptr(features), ptr(dist), ptr(c.d_ranks),
                   ptr(c.d_interval_starts), ptr(c.d_interval_cells), ptr(c.d_cell_first),
-                  c.schedule(self.N, self.H, self.W, self.D, units=self._units,
-                             exact=bool(self.exact)), self.B,
+                  c.schedule(self.N, self.H, self.W, self.D, exact=bool(self.exact)), self.B,
                   self.N, self.C, self.H, self.W, self.D, self.grid.nx, self.grid.ny, c.n_int_max,
                   self.mode, self.exact, ptr(out), ptr(self.nhwc), None, *self._scratch,
                   stream_ptr(self.dev))
@@ -503,8 +499,7 @@ def pool_naive(features, dist, cache: AssociationCache, grid: BevGridSpec,
         _lib.call("bvp_pool_forward_f32", ptr(inp.feats), ptr(inp.dist), ptr(cache.d_ranks),
                   ptr(cache.d_interval_starts), ptr(cache.d_interval_cells),
                   ptr(cache.d_cell_first),
-                  cache.schedule(inp.N, inp.H, inp.W, inp.D,
-                                 units=cache.needs_units(inp.C, exact=True), exact=True),
+                  cache.schedule(inp.N, inp.H, inp.W, inp.D, exact=True),
                   inp.B, inp.N, inp.C, inp.H, inp.W, inp.D,
                   grid.nx, grid.ny, cache.n_int_max, mode, 1, ptr(out), ptr(nhwc), None,
                   *_scratch(cache, inp.B, inp.C, _MODE[reducer]), stream_ptr(inp.feats.device))
@@ -604,7 +599,7 @@ def pool_lifted(x: torch.Tensor, cache: AssociationCache, grid: BevGridSpec,
     out = torch.empty((C, grid.n_cells), dtype=torch.float32, device=x.device)
     _lib.call("bvp_pool_lifted_f32", ptr(x), ptr(cache.d_ranks), ptr(cache.d_interval_starts),
               ptr(cache.d_interval_cells), ptr(cache.d_cell_first),
-              cache.schedule(units=cache.needs_units(C)), C,
+              cache.schedule(), C,
               grid.nx, grid.ny,
               _MODE[reducer], ptr(out), *_scratch(cache, 1, C, _MODE[reducer]),
               stream_ptr(x.device))
@@ -639,7 +634,7 @@ def pool_fused(logits: torch.Tensor, context: torch.Tensor, cache: AssociationCa
                      device=dev)
     _lib.call("bvp_fused_pool_bf16", ptr(lg), ptr(cx), ptr(cache.d_ranks),
               ptr(cache.d_interval_starts), ptr(cache.d_interval_cells), ptr(cache.d_cell_first),
-              cache.schedule(N, H, W, D, units=cache.needs_units(C, bf16=True)),
+              cache.schedule(N, H, W, D),
               B, N, C, H, W, D, grid.nx, grid.ny, _MODE[reducer], ptr(out), ptr(ws), ws.numel(),
               *_scratch(cache, B, C, _MODE[reducer]), stream_ptr(dev))
     v = out.view(B, C, grid.nx, grid.ny)
