@@ -668,6 +668,9 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
     cams = torch.from_numpy(bp.rig_rows(rig)).to(dev)
     ms = _timeit(torch, lambda: builder.build(cams), flush)
     rec("association_cold", ms, 12 * P + 4 * n_in + 8 * n_cells + 8 * n_int)
+    gbuilder = bp.CacheBuilder(spec.n_cameras, f, grid, dev, graph=True)
+    ms = _timeit(torch, lambda: gbuilder.build(cams), flush)
+    rec("association_cold_graph", ms, 12 * P + 4 * n_in + 8 * n_cells + 8 * n_int)
     ms = _timeit(torch, lambda: bp.reorder_weights(dist[0], cache), flush)
     rec("association_cached_reorder", ms, 4 * n_in + 4 * n_in + 4 * n_in)
 

@@ -479,8 +479,13 @@ class CacheBuilder:
     aliases the builder's buffers until the next ``build``."""
 
     def __init__(self, n_cameras: int, frustum: FrustumSpec, grid: BevGridSpec, device=None,
-                 sort_work: bool = False, tiles: bool = False):
+                 sort_work: bool = False, tiles: bool = False, graph: bool = False):
         self.dev = cuda_device(device)
+        # graph: the build's launches are captured once into a CUDA graph
+        # and replayed (one host call per frame instead of ~20 launches)
+        self.use_graph = graph
+        self._graph = None
+        self._cams = None
         self.n_cameras, self.frustum, self.grid = n_cameras, frustum, grid
         self.P = n_cameras * frustum.points_per_camera
         self.bufs = _alloc(self.P, grid.nx, grid.ny, self.dev)
@@ -503,10 +508,32 @@ class CacheBuilder:
 
     def build(self, cams: torch.Tensor, fingerprint: int = 0) -> AssociationCache:
         """cams: (N, 16) float64 CUDA tensor (see geometry.rig_rows)."""
-        b, f, g = self.bufs, self.frustum, self.grid
+        f, g = self.frustum, self.grid
         if cams.dtype != torch.float64 or cams.shape != (self.n_cameras, 16) or not cams.is_cuda:
             raise ConfigurationError("cams must be a CUDA float64 (N, 16) tensor")
-        cams = cams.contiguous()
+        dims = (self.n_cameras, f.height, f.width, f.depth_bins)
+        if not self.use_graph:
+            return self._launch(cams.contiguous(), fingerprint)
+        if self._graph is None:
+            self._cams = torch.empty_like(cams, memory_format=torch.contiguous_format)
+            self._cams.copy_(cams)
+            side = torch.cuda.Stream(self.dev)
+            side.wait_stream(torch.cuda.current_stream(self.dev))
+            with torch.cuda.stream(side):  # warm-up (lazy attributes) outside the capture
+                self._launch(self._cams, fingerprint)
+            torch.cuda.current_stream(self.dev).wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                self._launch(self._cams, fingerprint)
+            self._graph = graph
+        self._cams.copy_(cams)
+        self._graph.replay()
+        cache = _cache_of(self.bufs, fingerprint, g.nx, g.ny, self.n_cameras, f, g, dims)
+        cache._host[("tile", *self.dims)] = self.tplan
+        return cache
+
+    def _launch(self, cams: torch.Tensor, fingerprint: int) -> AssociationCache:
+        b, f, g = self.bufs, self.frustum, self.grid
         dims = (self.n_cameras, f.height, f.width, f.depth_bins)
         if self._one_call:
             _lib.call("bvp_build_association", ptr(cams), *dims, f.depth_min, f.depth_step,

@@ -1,48 +1,45 @@
-"""Cold association (uncached geometry) and pooling at configs S and H: CUDA
-events, cold L2, median of 20; plus a launch breakdown target for ncu."""
+"""Cold association (CacheBuilder.build) eager vs graph-replayed, configs S
+and H: flush L2 (512 MiB write) before each rep, CUDA events, mean of 50."""
+import json
 import os
 import statistics
 import sys
 
+import torch
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-
-import torch  # noqa: E402
-
 import paper_2205_13542_b200 as bp  # noqa: E402
 
-flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
-
-def t(fn, n=20):
-    for _ in range(3):
-        flush.zero_()
-        fn()
+def timeit(fn, flush, reps=50):
+    st = torch.cuda.current_stream()
     ts = []
-    for _ in range(n):
+    for i in range(reps + 5):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+        a.record(st)
         fn()
-        b.record()
+        b.record(st)
         b.synchronize()
-        ts.append(a.elapsed_time(b) * 1e3)
-    return statistics.median(ts)
+        if i >= 5:
+            ts.append(a.elapsed_time(b) * 1e3)
+    return round(statistics.fmean(ts), 1)
 
 
-for name in sys.argv[1:] or ["S", "H"]:
-    spec = bp.CONFIGS[name]
-    f = spec.frustum
-    rig, feats_np, logits_np, grid = bp.gen_workload(spec)
-    builder = bp.CacheBuilder(spec.n_cameras, f, grid)
-    cams = torch.from_numpy(bp.rig_rows(rig)).cuda()
-    cache = builder.build(cams)
-    feats = torch.from_numpy(feats_np).cuda()[None]
-    dist = bp.normalize_depth(torch.from_numpy(logits_np).cuda())[None]
-    plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width,
-                       f.depth_bins, 1, bp.Reducer.SUM)
-    tb = t(lambda: builder.build(cams))
-    tp = t(lambda: plan.run(feats, dist))
+def main():
+    dev = torch.device("cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    res = {}
+    for name in sys.argv[1:] or ["S", "H"]:
+        spec = bp.CONFIGS[name]
+        rig, _, _, grid = bp.gen_workload(spec)
+        cams = torch.from_numpy(bp.rig_rows(rig)).to(dev)
+        for label, kw in (("eager", {}), ("graph", {"graph": True}),
+                          ("graph_tiles", {"graph": True, "tiles": True})):
+            b = bp.CacheBuilder(spec.n_cameras, spec.frustum, grid, dev, **kw)
+            res[f"{name}_{label}_us"] = timeit(lambda: b.build(cams), flush)
+    print(json.dumps(res))
 
-    def frame():
-        plan.run_uncached(builder, cams, feats, dist)
-    print(f"{name}: association {tb:8.1f} us  pool step {tp:8.1f} us  frame {t(frame):8.1f} us")
+
+if __name__ == "__main__":
+    main()

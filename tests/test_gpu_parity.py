@@ -621,12 +621,39 @@ def test_run_uncached_follows_rig_changes(exact):
             assert max_rel_dev(want, got.reshape(want.shape)) <= FP32_TOL
 
 
+@pytest.mark.parametrize("tiles", [False, True])
+def test_graphed_builder_follows_rig_changes(tiles):
+    """CacheBuilder(graph=True) replays one captured build per frame: its
+    association arrays equal build_cache's for every rig it is fed, in any
+    order, and pooling through it matches the eager builder bit for bit."""
+    spec = bp.CONFIGS["S"]
+    f = spec.frustum
+    rig, feats_np, logits_np, grid = bp.gen_workload(spec)
+    rig2 = [bp.CameraCalibration(c.fx * 0.9, c.fy * 0.9, c.cx - 2.0, c.cy + 1.0, c.rotation,
+                                 c.translation + np.array([-0.3, 0.5, 0.05]), c.camera_id)
+            for c in rig]
+    feats = torch.from_numpy(feats_np).cuda()
+    dist = bp.normalize_depth(torch.from_numpy(logits_np).cuda())
+    gb = bp.CacheBuilder(spec.n_cameras, f, grid, tiles=tiles, graph=True)
+    eb = bp.CacheBuilder(spec.n_cameras, f, grid, tiles=tiles)
+    for r in (rig, rig2, rig2, rig):
+        cams = torch.from_numpy(bp.rig_rows(r)).cuda()
+        c = gb.build(cams)
+        want = bp.build_cache(r, f, grid)
+        for name in ("cell_of_point", "ranks", "interval_starts", "interval_cells"):
+            np.testing.assert_array_equal(getattr(c, name), getattr(want, name), err_msg=name)
+        got = bp.pool_interval(feats, dist, c, grid, exact=False).values
+        ref = bp.pool_interval(feats, dist, eb.build(cams), grid, exact=False).values
+        assert torch.equal(got, ref)
+
+
 @pytest.mark.parametrize("C", [1, 3, 20, 80, 200, 250, 256, 512])
 @pytest.mark.parametrize("red", ["sum", "mean", "max"])
 def test_exact_mode_channel_sweep(C, red):
     """exact=True is bit-identical to the fp64 restatement for every lane
-    layout: the chunk-schedule path and (C = 250, 512: too wide for it) the
-    work-unit path, both with their in-order walks of the long intervals."""
+    layout: the chunk-schedule path (with its in-order walk of the long
+    intervals) and, for C = 250, 512 (too wide for it), the reference-order
+    kernel pool_ref.cuh."""
     cache, grid, features, logits = _sweep_case(C, seed=5)
     dist = o.normalize_depth(logits)
     want = o.pool_interval(features, dist, cache.ranks, cache.interval_starts,
