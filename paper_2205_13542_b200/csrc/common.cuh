@@ -101,14 +101,17 @@ __device__ __forceinline__ void st_stream_f4(float *p, float4 v) {
 // Read-only loads that ask L2 to fetch the surrounding 256 bytes: strided
 // gathers of neighbouring columns by different CTAs then hit L2 instead of
 // each pulling its own 32-byte sector from DRAM.
-__device__ __forceinline__ float ldg_l2pf(const float *p) {
-    float r;
-    asm volatile("ld.global.nc.L2::256B.f32 %0, [%1];" : "=f"(r) : "l"(p));
+// Read-only loads with a 256-byte L2 prefetch hint, as raw bits.  Not
+// volatile: the compiler may batch and predicate them, and a value is only
+// waited for where it is used (the staging loops convert at the store).
+__device__ __forceinline__ uint32_t ldg_l2pf_b32(const void *p) {
+    uint32_t r;
+    asm("ld.global.nc.L2::256B.b32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
-__device__ __forceinline__ uint16_t ldg_l2pf(const uint16_t *p) {
+__device__ __forceinline__ uint32_t ldg_l2pf_u16(const void *p) {
     uint16_t r;
-    asm volatile("ld.global.nc.L2::256B.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    asm("ld.global.nc.L2::256B.u16 %0, [%1];" : "=h"(r) : "l"(p));
     return r;
 }
 

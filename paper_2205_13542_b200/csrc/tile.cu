@@ -472,25 +472,26 @@ tile_pool_kernel(TilePoolArgs a) {
             const int n_q = (((n_ch + 3) >> 2) - rank + CL - 1) / CL;  // this CTA's quads
             const int items = n_q * n_rb;
             for (int i0 = warp; i0 < items; i0 += NW * U) {
-                float4 v[U];
+                // all U x 4 loads issue before any value is used (raw bits;
+                // bf16 widened at the store)
+                uint32_t x[U][4];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int it = i0 + NW * u;
                     const int qi = it / n_rb, m = it - qi * n_rb;
                     const int c0 = 4 * (rank + CL * qi), hl = r0 + RS * m;
-                    float x[4] = {0.f, 0.f, 0.f, 0.f};
-                    if (it < items && hl < id.th) {
-                        const int64_t off = base + int64_t(c0) * HW + int64_t(hl) * g.W;
+                    const bool ok = it < items && hl < id.th;
+                    const int64_t off = base + int64_t(c0) * HW + int64_t(hl) * g.W;
 #pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            if (c0 + e < n_ch) {
-                                if (SRC == kTileF32)
-                                    x[e] = ldg_l2pf(static_cast<const float *>(src) + off + int64_t(e) * HW);
-                                else
-                                    x[e] = bf16_to_f32(ldg_l2pf(static_cast<const uint16_t *>(src) + off + int64_t(e) * HW));
-                            }
+                    for (int e = 0; e < 4; ++e) {
+                        x[u][e] = 0u;
+                        if (ok && c0 + e < n_ch) {
+                            if (SRC == kTileF32)
+                                x[u][e] = ldg_l2pf_b32(static_cast<const float *>(src) + off + int64_t(e) * HW);
+                            else
+                                x[u][e] = ldg_l2pf_u16(static_cast<const uint16_t *>(src) + off + int64_t(e) * HW) << 16;
+                        }
                     }
-                    v[u] = make_float4(x[0], x[1], x[2], x[3]);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -498,7 +499,9 @@ tile_pool_kernel(TilePoolArgs a) {
                     const int qi = it / n_rb, m = it - qi * n_rb;
                     const int c0 = 4 * (rank + CL * qi), hl = r0 + RS * m;
                     if (it < items && hl < id.th)
-                        *reinterpret_cast<float4 *>(dst + hl * stride + c0) = v[u];
+                        *reinterpret_cast<float4 *>(dst + hl * stride + c0) =
+                            make_float4(__uint_as_float(x[u][0]), __uint_as_float(x[u][1]),
+                                        __uint_as_float(x[u][2]), __uint_as_float(x[u][3]));
                 }
             }
         };
