@@ -160,7 +160,8 @@ int bvp_build_cache(const double *cams, int N, int H, int W, int D,
 /* One call per frame (CacheBuilder, config H): bvp_build_cache, with the
  * chunk list (bvp_make_work, cell order, tile -1) built on a forked stream
  * as soon as the interval tables exist -- beside the rank scatter and run
- * sorts -- and the point gather table (bvp_point_meta) after the ranks.
+ * sorts -- and the point gather table (bvp_point_meta's output) written by the
+ * run sorts as each cell's run is ordered (no pass of its own).
  * work_workspace: bvp_work_workspace_bytes(min(n_cells, P), P, chunk, nx, ny,
  * -1) bytes, distinct from workspace. */
 int bvp_build_association(const double *cams, int N, int H, int W, int D,

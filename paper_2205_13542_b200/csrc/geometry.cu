@@ -483,10 +483,26 @@ __global__ void count_scatter_flat_kernel(const uint32_t *__restrict__ cells,
     }
 }
 
+// The point gather table of the interval kernels (work.cu point_meta_kernel),
+// written by the run sorts as each run's final order is known: per sorted
+// point its feature row (pixel) and weight index into (N, D, H, W).
+struct MetaOut {
+    uint2 *meta;  // null: not wanted
+    uint32_t D, HW;
+    __device__ __forceinline__ void put(uint32_t j, uint32_t p) const {
+        const uint32_t pix = p / D, d = p - pix * D;
+        const uint32_t n = pix / HW, hw = pix - n * HW;
+        meta[j] = make_uint2(pix, (n * D + d) * HW + hw);
+    }
+};
+
 // Ascending bitonic sort of a run of L <= 32 K values held K per lane
-// (element lane + 32 m); missing elements are +inf.
+// (element lane + 32 m); missing elements are +inf.  mo.meta: also the run's
+// gather-table entries (r's offset in ranks is lo).
 template <int K>
-__device__ __forceinline__ void warp_sort_run(uint32_t *r, int L, int lane) {
+__device__ __forceinline__ void warp_sort_run(uint32_t *r, int L, int lane,
+                                              MetaOut mo = MetaOut{nullptr, 1u, 1u},
+                                              uint32_t lo = 0u) {
     uint32_t v[K];
 #pragma unroll
     for (int m = 0; m < K; ++m) v[m] = lane + 32 * m < L ? r[lane + 32 * m] : 0xFFFFFFFFu;
@@ -517,7 +533,10 @@ __device__ __forceinline__ void warp_sort_run(uint32_t *r, int L, int lane) {
     }
 #pragma unroll
     for (int m = 0; m < K; ++m)
-        if (lane + 32 * m < L) r[lane + 32 * m] = v[m];
+        if (lane + 32 * m < L) {
+            r[lane + 32 * m] = v[m];
+            if (mo.meta) mo.put(lo + lane + 32 * m, v[m]);
+        }
 }
 
 // Ascending bitonic sort of a[0, L) by `nthreads` cooperating threads (the
@@ -584,18 +603,21 @@ __global__ void pick_long_runs_kernel(const uint32_t *__restrict__ starts,
 // this one keeps the short runs' register budget and occupancy).
 __global__ void __launch_bounds__(256)
 seg_sort_warp_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ starts,
-                     const int64_t *__restrict__ counts) {
+                     const int64_t *__restrict__ counts, MetaOut mo) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_int = counts[1];
     const int64_t nwarps = int64_t(gridDim.x) * 8;
     for (int64_t iv = int64_t(blockIdx.x) * 8 + warp; iv < n_int; iv += nwarps) {
         const uint32_t lo = __ldg(starts + iv);
         const int L = static_cast<int>(__ldg(starts + iv + 1) - lo);
-        if (L <= 1) continue;
-        if (L <= 32) warp_sort_run<1>(ranks + lo, L, lane);
-        else if (L <= 64) warp_sort_run<2>(ranks + lo, L, lane);
-        else if (L <= 128) warp_sort_run<4>(ranks + lo, L, lane);
-        else if (L <= 256) warp_sort_run<8>(ranks + lo, L, lane);
+        if (L <= 1) {
+            if (L == 1 && mo.meta && lane == 0) mo.put(lo, ranks[lo]);
+            continue;
+        }
+        if (L <= 32) warp_sort_run<1>(ranks + lo, L, lane, mo, lo);
+        else if (L <= 64) warp_sort_run<2>(ranks + lo, L, lane, mo, lo);
+        else if (L <= 128) warp_sort_run<4>(ranks + lo, L, lane, mo, lo);
+        else if (L <= 256) warp_sort_run<8>(ranks + lo, L, lane, mo, lo);
         // longer runs: seg_sort_long_kernel, concurrently
     }
 }
@@ -610,7 +632,7 @@ seg_sort_warp_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ 
 __global__ void __launch_bounds__(256)
 seg_sort_long_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ starts,
                      const uint32_t *__restrict__ long_list,
-                     const uint32_t *__restrict__ n_long) {
+                     const uint32_t *__restrict__ n_long, MetaOut mo) {
     __shared__ uint32_t sh[kSegCtaMax];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t nl = *n_long;
@@ -621,6 +643,9 @@ seg_sort_long_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ 
         uint32_t *r = ranks + lo;
         if (L > kSegCtaMax) {
             bitonic_sort(r, L, threadIdx.x, blockDim.x, []() { __syncthreads(); });
+            __syncthreads();
+            if (mo.meta)
+                for (int i = threadIdx.x; i < L; i += blockDim.x) mo.put(lo + i, r[i]);
             continue;
         }
         for (int i = threadIdx.x; i < L; i += blockDim.x) sh[i] = r[i];
@@ -644,6 +669,7 @@ seg_sort_long_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ 
                 pos += l - min(L, b * cs);
             }
             r[pos] = x;
+            if (mo.meta) mo.put(lo + pos, x);
         }
         __syncthreads();
     }
@@ -695,7 +721,8 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
                      uint32_t *cells, int64_t P, int64_t n_cells, uint32_t *ranks,
                      uint32_t *starts, uint32_t *icells, uint32_t *cell_first, uint32_t *iop,
                      int64_t *counts, void *ws, size_t ws_bytes, cudaStream_t s,
-                     const SortHook *on_tables = nullptr, const SortHook *on_ranks = nullptr) {
+                     const SortHook *on_tables = nullptr, const SortHook *on_ranks = nullptr,
+                     uint32_t *point_meta = nullptr) {
     const SortLayout L = sort_layout(P, n_cells);
     BVP_REQUIRE(ws != nullptr && ws_bytes >= L.bytes, BVP_ERR_INVALID,
                 "sort workspace too small: need %zu bytes, got %zu", L.bytes, ws_bytes);
@@ -740,8 +767,13 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         pick_long_runs_kernel<<<cb, 256, 0, s>>>(starts, counts, long_list, n_long);
         {  // short runs and long runs side by side
             SideFork fork(s);
-            seg_sort_long_kernel<<<148 * 4, 256, 0, fork.side>>>(ranks, starts, long_list, n_long);
-            seg_sort_warp_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, counts);
+            // the point gather table comes with the sorted runs (cams: the
+            // frustum's N, H, W, D)
+            const MetaOut mo{point_meta && fp ? reinterpret_cast<uint2 *>(point_meta) : nullptr,
+                             fp ? uint32_t(fp->D) : 1u, fp ? uint32_t(fp->H) * fp->W : 1u};
+            seg_sort_long_kernel<<<148 * 4, 256, 0, fork.side>>>(ranks, starts, long_list, n_long,
+                                                                  mo);
+            seg_sort_warp_kernel<<<148 * 4, 256, 0, s>>>(ranks, starts, counts, mo);
         }
         const int rc_r = on_ranks ? (*on_ranks)(s) : BVP_OK;
         tables.join();
@@ -790,6 +822,10 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
     }
     if (on_tables) {
         const int rc = (*on_tables)(s);
+        if (rc != BVP_OK) return rc;
+    }
+    if (point_meta && fp) {  // radix path: the gather table from the final ranks
+        const int rc = bvp_point_meta(ranks, counts, fp->N, fp->H, fp->W, fp->D, point_meta, s);
         if (rc != BVP_OK) return rc;
     }
     if (on_ranks) {
@@ -896,12 +932,10 @@ int bvp_build_association(const double *cams, int N, int H, int W, int D, double
                              -1, work, splits, work_counts, work_workspace, work_workspace_bytes,
                              side);
     };
-    const SortHook sorted = [&](cudaStream_t main) {
-        return bvp_point_meta(ranks, counts, N, H, W, D, point_meta, main);
-    };
+    // the point gather table is written by the run sorts themselves
     return sort_impl(cams, &f, &g, cell_of_point, P, n_cells, ranks, interval_starts,
                      interval_cells, cell_first, interval_of_point, counts, workspace,
-                     workspace_bytes, as_stream(stream), &tables, &sorted);
+                     workspace_bytes, as_stream(stream), &tables, nullptr, point_meta);
 }
 
 }  // extern "C"
