@@ -627,6 +627,14 @@ tile_pool_kernel(TilePoolArgs a) {
             for (int half = 0; half < 2; ++half) {
                 uint32_t m = half ? G.y : G.x;
                 const int base = half ? 31 : -1;
+                if (m == 0xFFFFFFFFu) {  // all 32 rows (a level rig: most groups)
+#pragma unroll 8
+                    for (int h = base + 1; h < base + 33; h += 2) {
+                        group_row2<CS, FS>(acc, wq, fs, h, h + 1, lane);
+                        wq += 2 * kTileGroup;
+                    }
+                    continue;
+                }
                 while (m) {
                     const int h0 = base + __ffs(m);
                     m &= m - 1;
