@@ -468,18 +468,38 @@ tile_pool_kernel(TilePoolArgs a) {
         float *rpw = CL > 1 ? cluster.map_shared_rank(pw, j) : pw;
         const int64_t col = pix0 - rank + j;  // (h0, w_base + j)
         const int n_rb = (id.th + RS - 1) / RS;
-        auto stage = [&](const void *src, int n_ch, int64_t base, float *dst, int stride) {
-            const int n_q = (((n_ch + 3) >> 2) - rank + CL - 1) / CL;  // this CTA's quads
+        // n_quads >= ceil(n_ch / 4): the quads past n_ch are stored as zeros
+        // wait_first: the cluster barrier's wait (every CTA of the cluster
+        // running, so its shared memory may be written) sits between the
+        // first round's loads and its stores -- every warp runs that round
+        auto stage = [&](const void *src, int n_ch, int n_quads, int64_t base, float *dst,
+                         int stride, bool wait_first) {
+            const int n_q = (n_quads - rank + CL - 1) / CL;  // this CTA's quads
             const int items = n_q * n_rb;
-            for (int i0 = warp; i0 < items; i0 += NW * U) {
+            for (int i0 = warp; i0 < items || (wait_first && i0 == warp); i0 += NW * U) {
+                // item it = (quad qi, row block m); the U items of a round are
+                // NW apart, so one division per round and carries after it
+                int qs[U], ms[U];
+                {
+                    int qi = i0 / n_rb, m = i0 - qi * n_rb;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        qs[u] = qi;
+                        ms[u] = m;
+                        m += NW;
+                        while (m >= n_rb) {
+                            m -= n_rb;
+                            ++qi;
+                        }
+                    }
+                }
                 // all U x 4 loads issue before any value is used (raw bits;
                 // bf16 widened at the store)
                 uint32_t x[U][4];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int it = i0 + NW * u;
-                    const int qi = it / n_rb, m = it - qi * n_rb;
-                    const int c0 = 4 * (rank + CL * qi), hl = r0 + RS * m;
+                    const int c0 = 4 * (rank + CL * qs[u]), hl = r0 + RS * ms[u];
                     const bool ok = it < items && hl < id.th;
                     const int64_t off = base + int64_t(c0) * HW + int64_t(hl) * g.W;
 #pragma unroll
@@ -493,11 +513,12 @@ tile_pool_kernel(TilePoolArgs a) {
                         }
                     }
                 }
+                if (CL > 1 && wait_first && i0 == warp)
+                    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int it = i0 + NW * u;
-                    const int qi = it / n_rb, m = it - qi * n_rb;
-                    const int c0 = 4 * (rank + CL * qi), hl = r0 + RS * m;
+                    const int c0 = 4 * (rank + CL * qs[u]), hl = r0 + RS * ms[u];
                     if (it < items && hl < id.th)
                         *reinterpret_cast<float4 *>(dst + hl * stride + c0) =
                             make_float4(__uint_as_float(x[u][0]), __uint_as_float(x[u][1]),
@@ -505,14 +526,10 @@ tile_pool_kernel(TilePoolArgs a) {
                 }
             }
         };
-        if (CL > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-        stage(a.feats, C, nb * C * HW + col, rfs, FS);
-        stage(a.weights, D, nb * D * HW + col, rpw, PD);
-        // channel quads past C up to CP: zero (no quad holds both)
-        for (int i = threadIdx.x; i < id.th * (CP - ((C + 3) & ~3)); i += kPoolThreads) {
-            const int w4 = CP - ((C + 3) & ~3);
-            fs[(i / w4) * FS + ((C + 3) & ~3) + i % w4] = 0.f;
-        }
+        // feature rows padded with zero channels up to CP (the products read
+        // CS full channel slots)
+        stage(a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
+        stage(a.weights, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
         if (CL > 1)
             cluster.sync();
     }
