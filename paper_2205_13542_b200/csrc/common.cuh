@@ -101,17 +101,24 @@ __device__ __forceinline__ void st_stream_f4(float *p, float4 v) {
 // Read-only loads that ask L2 to fetch the surrounding 256 bytes: strided
 // gathers of neighbouring columns by different CTAs then hit L2 instead of
 // each pulling its own 32-byte sector from DRAM.
-// Read-only loads with a 256-byte L2 prefetch hint, as raw bits.  Not
-// volatile: the compiler may batch and predicate them, and a value is only
-// waited for where it is used (the staging loops convert at the store).
-__device__ __forceinline__ uint32_t ldg_l2pf_b32(const void *p) {
+// Read-only loads with a 256-byte L2 prefetch hint, as raw bits, predicated
+// in PTX (no branch around each load; 0 when off).  Not volatile: the
+// compiler may batch them, and a value is only waited for where it is used
+// (the staging loops convert at the store).
+__device__ __forceinline__ uint32_t ldg_l2pf_b32(const void *p, bool on) {
     uint32_t r;
-    asm("ld.global.nc.L2::256B.b32 %0, [%1];" : "=r"(r) : "l"(p));
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, 0;\n\t"
+        "@q ld.global.nc.L2::256B.b32 %0, [%1];\n\t}"
+        : "=r"(r)
+        : "l"(p), "r"(int(on)));
     return r;
 }
-__device__ __forceinline__ uint32_t ldg_l2pf_u16(const void *p) {
+__device__ __forceinline__ uint32_t ldg_l2pf_u16(const void *p, bool on) {
     uint16_t r;
-    asm("ld.global.nc.L2::256B.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b16 %0, 0;\n\t"
+        "@q ld.global.nc.L2::256B.u16 %0, [%1];\n\t}"
+        : "=h"(r)
+        : "l"(p), "r"(int(on)));
     return r;
 }
 

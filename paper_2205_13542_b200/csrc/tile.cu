@@ -474,6 +474,11 @@ tile_pool_kernel(TilePoolArgs a) {
         // first round's loads and its stores -- every warp runs that round
         auto stage = [&](const void *src, int n_ch, int n_quads, int64_t base, float *dst,
                          int stride, bool wait_first) {
+            // byte addresses: the tile's column once, then one 32-bit offset
+            // per item and one add per channel of the quad
+            constexpr int ES = SRC == kTileF32 ? 4 : 2;
+            const char *sb = static_cast<const char *>(src) + base * ES;
+            const uint32_t plane = uint32_t(HW) * ES, rowb = uint32_t(g.W) * ES;
             const int n_q = (n_quads - rank + CL - 1) / CL;  // this CTA's quads
             const int items = n_q * n_rb;
             for (int i0 = warp; i0 < items || (wait_first && i0 == warp); i0 += NW * U) {
@@ -501,16 +506,14 @@ tile_pool_kernel(TilePoolArgs a) {
                     const int it = i0 + NW * u;
                     const int c0 = 4 * (rank + CL * qs[u]), hl = r0 + RS * ms[u];
                     const bool ok = it < items && hl < id.th;
-                    const int64_t off = base + int64_t(c0) * HW + int64_t(hl) * g.W;
+                    const char *pi = sb + (uint64_t(uint32_t(c0)) * plane + uint32_t(hl) * rowb);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
-                        x[u][e] = 0u;
-                        if (ok && c0 + e < n_ch) {
-                            if (SRC == kTileF32)
-                                x[u][e] = ldg_l2pf_b32(static_cast<const float *>(src) + off + int64_t(e) * HW);
-                            else
-                                x[u][e] = ldg_l2pf_u16(static_cast<const uint16_t *>(src) + off + int64_t(e) * HW) << 16;
-                        }
+                        const bool on = ok && c0 + e < n_ch;
+                        if (SRC == kTileF32)
+                            x[u][e] = ldg_l2pf_b32(pi + uint64_t(e) * plane, on);
+                        else
+                            x[u][e] = ldg_l2pf_u16(pi + uint64_t(e) * plane, on) << 16;
                     }
                 }
                 if (CL > 1 && wait_first && i0 == warp)
