@@ -62,7 +62,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BVP_ABI_VERSION 7
+#define BVP_ABI_VERSION 8
 
 #define BVP_OK 0
 #define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
@@ -405,6 +405,14 @@ int bvp_tile_plan_init(bvp_tile_plan *plan, int N, int H, int W, int D, int64_t 
  * ordered, no host sync.  Deterministic. */
 int bvp_build_tile_plan(const uint32_t *cell_of_point, bvp_tile_plan *plan,
                         void *workspace, size_t workspace_bytes, void *stream);
+/* The same plan from an association: its ranks (in-range point ids by cell,
+ * ties by id; bevgrid.py:142-158) are stably sorted by tile, which lists
+ * every tile's points in the plan's (cell, h, d) order without a per-tile
+ * sort.  counts[0] = the number of in-range points (device).  Identical
+ * plan; ~5x faster than bvp_build_tile_plan at config S. */
+int bvp_build_tile_plan_ranks(const uint32_t *cell_of_point, const uint32_t *ranks,
+                              const int64_t *counts, bvp_tile_plan *plan,
+                              void *workspace, size_t workspace_bytes, void *stream);
 
 /* pool_interval SUM / MEAN (pooling.py:206-221) through the plan: features
  * (B,N,C,H,W) f32, dist (B,N,D,H,W) f32 -> out (B,C,n_cells) f32, every

@@ -21,7 +21,7 @@ OUT_OF_RANGE = 0xFFFFFFFF
 BVP_OUT_ZEROED = 0x100  # include/bevpool_b200.h
 BVP_TILE_PHASE1 = 0x200
 BVP_TILE_PHASE2 = 0x400
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 
 _P = ctypes.c_void_p
@@ -101,6 +101,7 @@ SIGNATURES = {
     "bvp_tile_plan_workspace_bytes": (_S, [_I, _I, _I, _I, _L]),
     "bvp_tile_plan_init": (_I, [_TP, _I, _I, _I, _I, _L, _P, _S, _L]),
     "bvp_build_tile_plan": (_I, [_P, _TP, _P, _S, _P]),
+    "bvp_build_tile_plan_ranks": (_I, [_P, _P, _P, _TP, _P, _S, _P]),
     "bvp_tile_pool_f32": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
     "bvp_tile_pool_fused_bf16": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
     "bvp_prefixsum_workspace_bytes": (_S, [_L, _I]),

@@ -179,9 +179,17 @@ class TilePlan:
     def supported(N: int, H: int, W: int, D: int, n_cells: int) -> bool:
         return bool(_lib.load().bvp_tile_plan_supported(N, H, W, D, n_cells))
 
-    def build(self, cell_of_point: torch.Tensor, exact_count: bool = False) -> "TilePlan":
-        _lib.call("bvp_build_tile_plan", ptr(cell_of_point), ctypes.byref(self.st), ptr(self.ws),
-                  self.ws.numel(), stream_ptr(self.device))
+    def build(self, cell_of_point: torch.Tensor, exact_count: bool = False, ranks=None,
+              counts=None) -> "TilePlan":
+        """ranks / counts: the association's (device), whose stable sort by
+        tile replaces the per-tile sort (same plan, faster)."""
+        if ranks is not None:
+            _lib.call("bvp_build_tile_plan_ranks", ptr(cell_of_point), ptr(ranks), ptr(counts),
+                      ctypes.byref(self.st), ptr(self.ws), self.ws.numel(),
+                      stream_ptr(self.device))
+        else:
+            _lib.call("bvp_build_tile_plan", ptr(cell_of_point), ctypes.byref(self.st),
+                      ptr(self.ws), self.ws.numel(), stream_ptr(self.device))
         if exact_count:
             self.fit()
         return self
@@ -338,7 +346,8 @@ class AssociationCache:
             plan = None
             if TilePlan.supported(N, H, W, D, self.n_cells) and self.n_points == N * H * W * D:
                 plan = TilePlan(N, H, W, D, self.n_cells, self.device).build(
-                    self.d_cell_of_point, exact_count=True)
+                    self.d_cell_of_point, exact_count=True, ranks=self.d_ranks,
+                    counts=self.d_counts)
             self._host[key] = plan
         return self._host[key]
 
@@ -557,7 +566,8 @@ class CacheBuilder:
         """Rebuild the tiled reduction's plan from this frame's cells (stream
         ordered, no sync; scratch sized for the worst case) and attach it."""
         if self.tplan is not None:
-            self.tplan.build(self.bufs["cells"])
+            self.tplan.build(self.bufs["cells"], ranks=self.bufs["ranks"],
+                             counts=self.bufs["counts"])
             cache._host[("tile", *self.dims)] = self.tplan
         else:
             cache._host[("tile", *self.dims)] = None  # per-frame caches pool with the interval kernels

@@ -10,6 +10,7 @@
 #include <functional>
 
 #include "common.cuh"
+#include "partition.cuh"
 #include "scan.cuh"
 
 namespace bvp {
@@ -833,6 +834,63 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         if (rc != BVP_OK) return rc;
     }
     return check_launch("sort_intervals");
+}
+
+// ---- stable partition (partition.cuh) ----------------------------------------
+struct PartLayout {
+    int passes, digit_bits;
+    int64_t n_tiles, hist_len;
+    size_t keys_a, vals_a, keys_b, vals_b, hist, part, total, bytes;
+};
+static PartLayout part_layout(int64_t n_max, int key_bits) {
+    PartLayout L{};
+    key_bits = std::max(1, key_bits);
+    L.passes = (key_bits + kMaxDigitBits - 1) / kMaxDigitBits;
+    L.digit_bits = (key_bits + L.passes - 1) / L.passes;
+    L.n_tiles = std::max<int64_t>(1, ceil_div(n_max, kSortTile));
+    L.hist_len = (int64_t(1) << L.digit_bits) * L.n_tiles;
+    size_t o = 0;
+    L.keys_a = o; o = align256(o + 4 * size_t(n_max));
+    L.vals_a = o; o = align256(o + 4 * size_t(n_max));
+    L.keys_b = o; o = align256(o + 4 * size_t(n_max));
+    L.vals_b = o; o = align256(o + 4 * size_t(n_max));
+    L.hist = o; o = align256(o + 4 * size_t(L.hist_len));
+    L.part = o; o = align256(o + 4 * size_t(scan_partials_len<uint32_t>(L.hist_len)));
+    L.total = o; o = align256(o + 8);
+    L.bytes = o;
+    return L;
+}
+
+size_t stable_partition_ws_bytes(int64_t n_max, int key_bits) {
+    return part_layout(n_max, key_bits).bytes;
+}
+
+int stable_partition(const uint32_t *keys, const uint32_t *vals, const int64_t *count,
+                     int64_t n_max, int key_bits, uint32_t *vals_out, void *ws,
+                     size_t ws_bytes, cudaStream_t s) {
+    const PartLayout L = part_layout(n_max, key_bits);
+    BVP_REQUIRE(ws && ws_bytes >= L.bytes, BVP_ERR_INVALID,
+                "partition workspace too small: need %zu bytes, got %zu", L.bytes, ws_bytes);
+    char *w = static_cast<char *>(ws);
+    auto *hist = reinterpret_cast<uint32_t *>(w + L.hist);
+    auto *part = reinterpret_cast<uint32_t *>(w + L.part);
+    auto *total = reinterpret_cast<uint32_t *>(w + L.total);
+    const unsigned tiles = static_cast<unsigned>(L.n_tiles);
+    const uint32_t *kin = keys, *vin = vals;
+    for (int pass = 0; pass < L.passes; ++pass) {
+        const int shift = pass * L.digit_bits;
+        const bool last = pass == L.passes - 1;
+        uint32_t *kout = last ? nullptr : reinterpret_cast<uint32_t *>(w + ((pass & 1) ? L.keys_b : L.keys_a));
+        uint32_t *vout = last ? vals_out : reinterpret_cast<uint32_t *>(w + ((pass & 1) ? L.vals_b : L.vals_a));
+        radix_upsweep_kernel<<<tiles, kSortThreads, 0, s>>>(kin, count, shift, L.digit_bits, hist,
+                                                            L.n_tiles);
+        device_excl_scan<uint32_t>(hist, hist, L.hist_len, part, total, s);
+        radix_scatter_kernel<false><<<tiles, kSortThreads, 0, s>>>(
+            kin, vin, n_max, count, shift, L.digit_bits, hist, L.n_tiles, kout, vout);
+        kin = kout;
+        vin = vout;
+    }
+    return check_launch("stable_partition");
 }
 
 }  // namespace bvp

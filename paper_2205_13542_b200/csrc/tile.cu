@@ -39,6 +39,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "partition.cuh"
 #include "scan.cuh"
 
 namespace bvp {
@@ -130,15 +131,58 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp
 }
 
 // ---- plan build -------------------------------------------------------------
-// One CTA per tile.  Keys (cell << 16 | hl << d_bits | d), sorted ascending
-// in shared memory (bitonic); the low bits order the points of a cell by
-// (h, d), which is their rank order within the tile (bevgrid.py:149's stable
-// tie-break restricted to one column).
+// Tile of a frustum point id p = ((n H + h) W + w) D + d.
+__device__ __forceinline__ uint32_t tile_of_point(uint32_t p, const TileGeom &g) {
+    const uint32_t pix = p / uint32_t(g.D);
+    const uint32_t w = pix % uint32_t(g.W), nh = pix / uint32_t(g.W);
+    const uint32_t h = nh % uint32_t(g.H), n = nh / uint32_t(g.H);
+    return (n * uint32_t(g.n_hb) + h / uint32_t(g.TH)) * uint32_t(g.W) + w;
+}
+
+// The association's ranks (in-range point ids, by cell, ties by id) keyed by
+// their tile, and the points per tile (block histogram in shared memory,
+// one global add per tile and block).  A stable partition of the ranks by
+// these keys lists every tile's points by (cell, h, d): the tile's own order.
+__global__ void tile_key_kernel(const uint32_t *__restrict__ ranks,
+                                const int64_t *__restrict__ counts, TileGeom g, int64_t P,
+                                uint32_t *__restrict__ keys, uint32_t *__restrict__ tile_count) {
+    extern __shared__ uint32_t s_hist[];  // [T]
+    const uint32_t T = uint32_t(g.T);
+    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x) s_hist[i] = 0u;
+    __syncthreads();
+    const int64_t n_in = counts[0];
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < P;
+         j += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t k = kOOR;
+        if (j < n_in) {
+            k = tile_of_point(__ldg(ranks + j), g);
+            atomicAdd(&s_hist[k], 1u);
+        }
+        keys[j] = k;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < T; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(tile_count + i, s_hist[i]);
+}
+
+// The tile's points from the association, in order (SORTED plan build):
+// pts[start[t], start[t + 1]) are tile t's point ids by (cell, h, d).
+struct TileSorted {
+    const uint32_t *pts;
+    const uint32_t *start;
+};
+
+// One CTA per tile.  Keys (cell << 16 | hl << d_bits | d), ascending; the
+// low bits order the points of a cell by (h, d), which is their rank order
+// within the tile (bevgrid.py:149's stable tie-break restricted to one
+// column).  SORTED: read in that order from the association (TileSorted);
+// otherwise sorted in shared memory (bitonic) from cell_of_point alone.
+template <bool SORTED>
 __global__ void __launch_bounds__(kPlanThreads)
 tile_plan_kernel(const uint32_t *__restrict__ cells, TileGeom g, uint4 *__restrict__ hdr,
                  uint32_t *__restrict__ rec, uint32_t *__restrict__ seg_cell,
                  uint32_t *__restrict__ seg_start, uint4 *__restrict__ groups,
-                 int *__restrict__ err) {
+                 int *__restrict__ err, TileSorted ts) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *keys = reinterpret_cast<unsigned long long *>(smem);
     __shared__ unsigned long long gmask[kTileMaxPoints / kTileGroup + 1];
@@ -154,35 +198,51 @@ tile_plan_kernel(const uint32_t *__restrict__ cells, TileGeom g, uint4 *__restri
     const int64_t hstride = int64_t(g.W) * g.D;
     uint32_t nvalid = 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int hl = warp; hl < id.th; hl += nw)
-        for (int d = lane; d < g.D; d += 32) {
-            const uint32_t c = __ldg(cbase + hl * hstride + d);
-            unsigned long long k = ~0ull;
-            if (c != kOOR) {
-                k = (static_cast<unsigned long long>(c) << 16) |
-                    static_cast<unsigned>((hl << g.d_bits) | d);
-                ++nvalid;
-            }
-            keys[hl * g.D + d] = k;
-        }
-    for (int i = np_all + threadIdx.x; i < cap; i += blockDim.x) keys[i] = ~0ull;
     for (int i = threadIdx.x; i < kTileMaxPoints / kTileGroup + 1; i += blockDim.x) gmask[i] = 0;
-    block_excl_scan(nvalid, s_warp, &s_tot[0]);
-    const int n_pts = int(s_tot[0]);
     const int hmask = (1 << g.hl_bits) - 1, dmask = (1 << g.d_bits) - 1;
-    // bitonic sort of keys[0, cap)
-    for (int k = 2; k <= cap; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < (cap >> 1); i += blockDim.x) {
-                const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
-                const unsigned long long a = keys[lo], b = keys[hi];
-                const bool up = (lo & k) == 0;
-                if ((a > b) == up) {
-                    keys[lo] = b;
-                    keys[hi] = a;
+    int n_pts;
+    if (SORTED) {
+        const uint32_t lo = __ldg(ts.start + t), hi = __ldg(ts.start + t + 1);
+        n_pts = int(hi - lo);
+        for (int k = threadIdx.x; k < n_pts; k += blockDim.x) {
+            const uint32_t p = __ldg(ts.pts + lo + k);
+            const uint32_t pix = p / uint32_t(g.D), d = p - pix * uint32_t(g.D);
+            const uint32_t hl = (pix / uint32_t(g.W)) % uint32_t(g.H) - uint32_t(id.h0);
+            keys[k] = (static_cast<unsigned long long>(__ldg(cells + p)) << 16) |
+                      ((hl << g.d_bits) | d);
+        }
+        __syncthreads();
+    } else {
+        for (int hl = warp; hl < id.th; hl += nw)
+            for (int d = lane; d < g.D; d += 32) {
+                const uint32_t c = __ldg(cbase + hl * hstride + d);
+                unsigned long long k = ~0ull;
+                if (c != kOOR) {
+                    k = (static_cast<unsigned long long>(c) << 16) |
+                        static_cast<unsigned>((hl << g.d_bits) | d);
+                    ++nvalid;
                 }
+                keys[hl * g.D + d] = k;
             }
-            __syncthreads();
+        for (int i = np_all + threadIdx.x; i < cap; i += blockDim.x) keys[i] = ~0ull;
+        block_excl_scan(nvalid, s_warp, &s_tot[0]);
+        n_pts = int(s_tot[0]);
+    }
+    // bitonic sort of keys[0, cap)
+    if (!SORTED) {
+        for (int k = 2; k <= cap; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < (cap >> 1); i += blockDim.x) {
+                    const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
+                    const unsigned long long a = keys[lo], b = keys[hi];
+                    const bool up = (lo & k) == 0;
+                    if ((a > b) == up) {
+                        keys[lo] = b;
+                        keys[hi] = a;
+                    }
+                }
+                __syncthreads();
+            }
         }
     }
     // segments: thread owns the contiguous points [k0, k1)
@@ -779,16 +839,26 @@ static PlanLayout plan_layout(const TileGeom &g, int64_t n_cells) {
 }
 
 struct PlanWs {
-    size_t fill, owner, part, total, err, bytes;
+    size_t fill, owner, part, total, err;
+    // the by-tile partition of the association's ranks (bvp_build_tile_plan_ranks)
+    size_t tkeys, tpts, tstart, tpart, ttotal, tsort, tsort_bytes, bytes;
 };
 static PlanWs plan_ws(const TileGeom &g, int64_t n_cells) {
     PlanWs L{};
+    const int64_t P = int64_t(g.N) * g.H * g.W * g.D;
     size_t o = 0;
     L.fill = o; o = a256(o + 4 * size_t(n_cells + 1));
     L.owner = o; o = a256(o + 8 * size_t(g.T) * g.tpc);
     L.part = o; o = a256(o + 4 * size_t(scan_partials_len<uint32_t>(n_cells + 1)));
     L.total = o; o = a256(o + 8);
     L.err = o; o = a256(o + 8);
+    L.tkeys = o; o = a256(o + 4 * size_t(P));
+    L.tpts = o; o = a256(o + 4 * size_t(P));
+    L.tstart = o; o = a256(o + 4 * size_t(g.T + 1));
+    L.tpart = o; o = a256(o + 4 * size_t(scan_partials_len<uint32_t>(g.T + 1)));
+    L.ttotal = o; o = a256(o + 8);
+    L.tsort_bytes = stable_partition_ws_bytes(P, bits_for(g.T - 1));
+    L.tsort = o; o = a256(o + L.tsort_bytes);
     L.bytes = o;
     return L;
 }
@@ -955,9 +1025,12 @@ size_t bvp_tile_plan_workspace_bytes(int N, int H, int W, int D, int64_t n_cells
     return plan_ws(tile_geom(N, H, W, D), n_cells).bytes;
 }
 
-int bvp_build_tile_plan(const uint32_t *cell_of_point, bvp_tile_plan *plan, void *workspace,
-                        size_t workspace_bytes, void *stream) {
+static int build_tile_plan(const uint32_t *cell_of_point, const uint32_t *ranks,
+                           const int64_t *counts, bvp_tile_plan *plan, void *workspace,
+                           size_t workspace_bytes, void *stream) {
     BVP_REQUIRE(cell_of_point, BVP_ERR_INVALID, "null cell_of_point");
+    BVP_REQUIRE((ranks == nullptr) == (counts == nullptr), BVP_ERR_INVALID,
+                "ranks and counts go together");
     TileGeom g;
     int rc = plan_dims_from(plan, g);
     if (rc != BVP_OK) return rc;
@@ -986,14 +1059,39 @@ int bvp_build_tile_plan(const uint32_t *cell_of_point, bvp_tile_plan *plan, void
     const size_t smem = 8 * size_t(cap);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(tile_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(tile_plan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             8 * kTileMaxPoints);
+        cudaFuncSetAttribute(tile_plan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              8 * kTileMaxPoints);
         attr = true;
     }
-    tile_plan_kernel<<<unsigned(g.T), kPlanThreads, smem, s>>>(
-        cell_of_point, g, at<uint4>(plan, L.hdr), at<uint32_t>(plan, L.rec),
-        at<uint32_t>(plan, L.seg_cell), at<uint32_t>(plan, L.seg_start), at<uint4>(plan, L.groups),
-        err);
+    TileSorted ts{};
+    // (the per-tile histogram lives in shared memory: up to 12288 tiles)
+    if (ranks && g.T * 4 > 48 * 1024) ranks = nullptr;
+    if (ranks) {  // the tiles' points in order from the association: a stable partition
+        const int64_t P = int64_t(g.N) * g.H * g.W * g.D;
+        auto *tkeys = reinterpret_cast<uint32_t *>(w + WL.tkeys);
+        auto *tpts = reinterpret_cast<uint32_t *>(w + WL.tpts);
+        auto *tstart = reinterpret_cast<uint32_t *>(w + WL.tstart);
+        cudaMemsetAsync(tstart, 0, 4 * size_t(g.T + 1), s);
+        const unsigned kb = unsigned(std::min<int64_t>(ceil_div(P, 256), 148 * 4));
+        tile_key_kernel<<<kb, 256, 4 * size_t(g.T), s>>>(ranks, counts, g, P, tkeys, tstart);
+        device_excl_scan<uint32_t>(tstart, tstart, g.T + 1, reinterpret_cast<uint32_t *>(w + WL.tpart),
+                                   reinterpret_cast<uint32_t *>(w + WL.ttotal), s);
+        rc = stable_partition(tkeys, ranks, counts, P, bits_for(g.T - 1), tpts, w + WL.tsort,
+                              WL.tsort_bytes, s);
+        if (rc != BVP_OK) return rc;
+        ts = TileSorted{tpts, tstart};
+        tile_plan_kernel<true><<<unsigned(g.T), kPlanThreads, smem, s>>>(
+            cell_of_point, g, at<uint4>(plan, L.hdr), at<uint32_t>(plan, L.rec),
+            at<uint32_t>(plan, L.seg_cell), at<uint32_t>(plan, L.seg_start),
+            at<uint4>(plan, L.groups), err, ts);
+    } else {
+        tile_plan_kernel<false><<<unsigned(g.T), kPlanThreads, smem, s>>>(
+            cell_of_point, g, at<uint4>(plan, L.hdr), at<uint32_t>(plan, L.rec),
+            at<uint32_t>(plan, L.seg_cell), at<uint32_t>(plan, L.seg_start),
+            at<uint4>(plan, L.groups), err, ts);
+    }
     tile_seg_count_kernel<<<unsigned(g.T), 256, 0, s>>>(
         at<const uint4>(plan, L.hdr), g, at<const uint32_t>(plan, L.seg_cell),
         at<const uint32_t>(plan, L.seg_start), csf, npts);
@@ -1005,6 +1103,20 @@ int bvp_build_tile_plan(const uint32_t *cell_of_point, bvp_tile_plan *plan, void
     const unsigned cb = unsigned(std::min<int64_t>(ceil_div(n_cells, 256), 148 * 16));
     tile_seg_fix_kernel<<<cb, 256, 0, s>>>(csf, n_cells, g, owner, at<uint32_t>(plan, L.seg_row));
     return check_launch("build_tile_plan");
+}
+
+int bvp_build_tile_plan(const uint32_t *cell_of_point, bvp_tile_plan *plan, void *workspace,
+                        size_t workspace_bytes, void *stream) {
+    return build_tile_plan(cell_of_point, nullptr, nullptr, plan, workspace, workspace_bytes,
+                           stream);
+}
+
+int bvp_build_tile_plan_ranks(const uint32_t *cell_of_point, const uint32_t *ranks,
+                              const int64_t *counts, bvp_tile_plan *plan, void *workspace,
+                              size_t workspace_bytes, void *stream) {
+    BVP_REQUIRE(ranks && counts, BVP_ERR_INVALID, "null ranks / counts");
+    return build_tile_plan(cell_of_point, ranks, counts, plan, workspace, workspace_bytes,
+                           stream);
 }
 
 int bvp_tile_plan_init(bvp_tile_plan *plan, int N, int H, int W, int D, int64_t n_cells,

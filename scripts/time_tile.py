@@ -73,6 +73,13 @@ def main(name="S"):
     if builder.tplan is not None:
         res["tile_plan_build_us"] = timeit(lambda: builder.tplan.build(builder.bufs["cells"]),
                                            flush, reps=10)
+    from paper_2205_13542_b200.bevgrid import TilePlan
+    tp2 = TilePlan(spec.n_cameras, f.height, f.width, f.depth_bins, grid.n_cells, dev)
+    res["tile_plan_build_sort_us"] = timeit(lambda: tp2.build(cache.d_cell_of_point), flush,
+                                            reps=10)
+    res["tile_plan_build_ranks_us"] = timeit(
+        lambda: tp2.build(cache.d_cell_of_point, ranks=cache.d_ranks, counts=cache.d_counts),
+        flush, reps=10)
     print(json.dumps(res))
 
 
