@@ -687,6 +687,8 @@ def deserialize_cache(data: bytes, n_cells: int | None = None, device=None) -> A
     if pos != len(data):
         raise FileFormatError("trailing bytes after cache payload", offset=pos)
     cells, ranks, starts, icells = arrays
+    if cells.size == 0:  # no frustum has zero points; the device tables need one
+        raise FileFormatError("empty association (cell_of_point has no entries)", offset=14)
     if n_cells is None:
         n_cells = int(icells.max()) + 1 if icells.size else 1
     cache = cache_from_cells(cells, 1, n_cells, fingerprint, device=device)

@@ -1,9 +1,10 @@
 // pool_ivl.cuh -- the fast (fp32-accumulating) interval-reduction kernel over
 // the chunk schedule (work.cu), sm_100a.
 //
-// Restates the reference's interval_reduce (_kernels.py:22-63) in fast mode
-// (fp32 accumulation; tolerance 1e-5 against the fp64 reference -- the
-// bit-exact fp64 mode is pool_kernel.cuh's).
+// Restates the reference's interval_reduce (_kernels.py:22-63): fast mode
+// (fp32 accumulation; tolerance 1e-5 against the fp64 reference) and, with
+// EXACT, the bit-exact fp64 mode (whole intervals here, the intervals longer
+// than a chunk in order by pool_exact_long_kernel, pool_kernel.cuh).
 //
 // Design (measured, profiles/ + scripts/gather_mlp_bench.cu): the path is a
 // gather of 320-byte feature rows from an L2-resident table; B200 sustains
@@ -394,7 +395,8 @@ int run_pool_ivl(const PoolParams &p0, int B, bool is_max, cudaStream_t s) {
 }
 
 // Fast-mode dispatch: the chunk kernel when the cache carries a chunk
-// schedule, else the group kernel, else the one-point-per-warp kernel.
+// schedule and a lane layout fits C, else the reference-order kernel
+// (pool_ref.cuh).
 template <typename Elem, int VEC, int SRC>
 int run_pool_fast(const PoolParams &p, int B, bool is_max, cudaStream_t s) {
     const int rc = run_pool_ivl<Elem, VEC, SRC>(p, B, is_max, s);

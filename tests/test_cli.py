@@ -4,6 +4,7 @@ reference's own CLI (tests/golden/cli/, tests/golden/make_golden_cli.py)."""
 
 import filecmp
 import os
+import re
 
 import numpy as np
 import pytest
@@ -41,6 +42,21 @@ def test_tensor_round_trip_and_errors():
         serialize_tensor(a.astype(np.float64))
     g = load_tensor(os.path.join(GOLD, "features.bvpt"))
     assert g.shape == (2, 3, 4, 6) and g.dtype == np.float32
+
+
+def test_tensor_truncation_reports_the_field_being_read():
+    """Every truncation of a BVPT blob names the field being read and its
+    start offset, as the reference's take() does (tensorio.py:39-71): magic
+    [0, 4), header [4, 8), shape[i] [8 + 4i, 12 + 4i), payload after."""
+    a = np.arange(12, dtype=np.float32).reshape(3, 4)
+    blob = serialize_tensor(a)
+    fields = [(0, 4, "magic"), (4, 8, "header"), (8, 12, "shape[0]"), (12, 16, "shape[1]"),
+              (16, len(blob), "payload")]
+    for n in range(len(blob)):
+        start, what = next((lo, w) for lo, hi, w in fields if lo <= n < hi)
+        with pytest.raises(FileFormatError, match=rf"truncated while reading {re.escape(what)}") as ei:
+            deserialize_tensor(blob[:n])
+        assert ei.value.offset == start, (n, what)
 
 
 def test_calibration_round_trip_and_field_errors():
