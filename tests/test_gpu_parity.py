@@ -781,3 +781,32 @@ def test_tile_plan_from_ranks_matches_per_tile_sort(name):
     a.pool_fused_bf16(lg, cx, 1, C, bp._lib.BVP_SUM, oa)
     b.pool_fused_bf16(lg, cx, 1, C, bp._lib.BVP_SUM, ob)
     assert torch.equal(oa, ob)
+
+
+@pytest.mark.parametrize("seed", [20_000 + s for s in range(8)])
+def test_tile_path_random_wide_instances(seed):
+    """Random rigs with up to 96 rows (several 64-row tiles per column), up to
+    130 depth bins (depth-weight quads past 32) and odd widths (clusters of
+    8 / 4 / 2 / 1 columns): the tiled reduction (SUM, MEAN) and its fused
+    bf16 variant against the 64-bit oracle."""
+    inst = random_instance(seed, 96, 130, 40)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    dist = o.normalize_depth(inst.logits)
+    C = inst.features.shape[1]
+    n_cam = inst.cams.shape[0]
+    assert cache.tile_plan(n_cam, frustum.height, frustum.width, frustum.depth_bins) is not None
+    for red in (bp.Reducer.SUM, bp.Reducer.MEAN):
+        want = o.pool_naive(inst.features, dist, cache.cell_of_point, grid.n_cells, red.value)
+        got = bp.pool_interval(inst.features, dist, cache, grid, red, exact=False)
+        assert max_rel_dev(want, got.values.reshape(want.shape)) <= FP32_TOL, red
+    if C == 0:
+        return
+    dev = torch.device("cuda")
+    fb, lb = o.bf16_round(inst.features), o.bf16_round(inst.logits)
+    got = bp.pool_fused(torch.from_numpy(inst.logits).to(dev).to(torch.bfloat16),
+                        torch.from_numpy(inst.features).to(dev).to(torch.bfloat16), cache, grid
+                        ).values.cpu().numpy().reshape(C, -1)
+    want = o.fused_pool(fb, lb, cache.ranks, cache.interval_starts, cache.interval_cells,
+                        grid.n_cells, "sum")
+    assert max_rel_dev(want, got) <= 1e-5
