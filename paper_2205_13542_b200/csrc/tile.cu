@@ -46,6 +46,7 @@ namespace bvp {
 
 constexpr int kTileGroup = 8;         // segments (cells) per group
 constexpr int kTileMaxRows = 64;      // rows per tile (one u64 mask per group)
+constexpr int kTileRows = 32;         // rows per tile chosen (tile_rows_for)
 constexpr int kTileMaxPoints = 8192;  // points per tile (smem sort capacity)
 constexpr int kPlanThreads = 512;
 constexpr int kPoolThreads = 256;
@@ -64,10 +65,15 @@ inline int bits_for(int64_t v) {  // bits to hold values in [0, v]
     return b;
 }
 
+// Rows per tile: at most kTileRows (measured at config H, 64 rows: 32-row
+// tiles take the step from 203 to 178 us -- four 45 KB CTAs per SM instead
+// of two 88 KB ones outweigh twice the segment rows; 16 or 24 rows are
+// slower), balanced over the fewest row blocks, and at most kTileMaxPoints
+// points per tile.
 inline int tile_rows_for(int H, int D) {
-    int th = std::min(H, kTileMaxRows);
-    th = std::min(th, std::max(1, kTileMaxPoints / std::max(D, 1)));
-    return th;
+    const int cap = std::min(kTileRows, std::max(1, kTileMaxPoints / std::max(D, 1)));
+    const int n_hb = (H + cap - 1) / cap;
+    return (H + n_hb - 1) / n_hb;
 }
 
 inline TileGeom tile_geom(int N, int H, int W, int D) {
