@@ -426,6 +426,18 @@ int bvp_tile_pool_f32(const float *features, const float *dist, const bvp_tile_p
  * (B,N,C,H,W) bf16 -> out (B,C,n_cells) f32 = pool(softmax_D(logits) (x)
  * context); the depth softmax of a tile's pixels is formed in shared memory
  * (fp32), nothing else is materialised. */
+/* The adjoint of bvp_tile_pool_f32 (config B training, SUM / MEAN): from
+ * grad_out (B,C,n_cells) and the forward's features / dist, grad_features
+ * (B,N,C,H,W) and grad_dist (B,N,D,H,W) (either may be NULL: not computed),
+ * every element written once (points out of range and pixels no point of
+ * which is in range get 0).  rows: the same scratch as the forward's.
+ * Deterministic; fp32 (<= ~1e-6 relative of the fp64 adjoint).  Tiles of
+ * <= 32 rows (every plan bvp_tile_plan_init makes). */
+int bvp_tile_backward_f32(const float *grad_out, const float *features, const float *dist,
+                          const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
+                          size_t rows_bytes, float *grad_features, float *grad_dist,
+                          void *stream);
+
 int bvp_tile_pool_fused_bf16(const uint16_t *logits, const uint16_t *context,
                              const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
                              size_t rows_bytes, float *out, void *stream);

@@ -102,6 +102,7 @@ SIGNATURES = {
     "bvp_tile_plan_init": (_I, [_TP, _I, _I, _I, _I, _L, _P, _S, _L]),
     "bvp_build_tile_plan": (_I, [_P, _TP, _P, _S, _P]),
     "bvp_build_tile_plan_ranks": (_I, [_P, _P, _P, _TP, _P, _S, _P]),
+    "bvp_tile_backward_f32": (_I, [_P, _P, _P, _TP, _I, _I, _I, _P, _S, _P, _P, _P]),
     "bvp_tile_pool_f32": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
     "bvp_tile_pool_fused_bf16": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
     "bvp_prefixsum_workspace_bytes": (_S, [_L, _I]),

@@ -1,11 +1,14 @@
 """Training: the interval pooling as a differentiable torch op (config B).
 
-Forward is the cached interval reduction (bvp_pool_forward_f32); backward is
-the atomic-free gather backward (bvp_pool_backward_f32, csrc/backward.cu)
-producing gradients for both the context features and the depth
-distribution.  MAX routes each output gradient to the first point (rank
-order) attaining the max, recorded by the forward.  The reference has no
-backward; tests/ check this one against an fp64 restatement
+SUM / MEAN in fast mode run the pixel-column tiled reduction forward
+(bvp_tile_pool_f32) and its adjoint backward (bvp_tile_backward_f32: the
+same tiles and weight windows, every gradient row read once per segment);
+MAX and exact mode run the cached interval reduction (bvp_pool_forward_f32)
+and the atomic-free gather backward (bvp_pool_backward_f32,
+csrc/backward.cu).  Both produce gradients for the context features and the
+depth distribution.  MAX routes each output gradient to the first point
+(rank order) attaining the max, recorded by the forward.  The reference has
+no backward; tests/ check these against an fp64 restatement
 that is itself checked against finite differences.
 """
 
@@ -15,7 +18,7 @@ import torch
 
 from . import _lib
 from .bevgrid import AssociationCache, BevGridSpec, ptr, stream_ptr
-from .pooling import _MODE, BevFeatureMap, Reducer, _reducer, _scratch
+from .pooling import _MODE, BevFeatureMap, Reducer, _reducer, _scratch, _tile_plan
 
 
 class _BevPoolFn(torch.autograd.Function):
@@ -28,6 +31,12 @@ class _BevPoolFn(torch.autograd.Function):
         features = features.contiguous()
         dist = dist.contiguous()
         out = torch.empty((B, C, nx * ny), dtype=torch.float32, device=dev)
+        tp = _tile_plan(cache, N, H, W, D, C, _MODE[reducer], int(exact))
+        if tp is not None:  # the tiled path, forward and backward
+            tp.pool_f32(features, dist, B, C, _MODE[reducer], out)
+            ctx.cache, ctx.reducer, ctx.dims, ctx.tile = cache, reducer, (B, N, C, H, W, D, nx, ny), tp
+            ctx.save_for_backward(features, dist)
+            return out
         nhwc = torch.empty(features.numel(), dtype=torch.float32, device=dev)
         argmax = None
         if reducer is Reducer.MAX:
@@ -40,13 +49,12 @@ class _BevPoolFn(torch.autograd.Function):
                   cache.n_int_max,
                   _MODE[reducer], int(exact), ptr(out), ptr(nhwc), ptr(argmax),
                   *_scratch(cache, B, C, _MODE[reducer]), stream_ptr(dev))
-        ctx.cache, ctx.reducer, ctx.dims = cache, reducer, (B, N, C, H, W, D, nx, ny)
+        ctx.cache, ctx.reducer, ctx.dims, ctx.tile = cache, reducer, (B, N, C, H, W, D, nx, ny), None
         ctx.save_for_backward(nhwc, dist, argmax)
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
-        nhwc, dist, argmax = ctx.saved_tensors
         cache, reducer = ctx.cache, ctx.reducer
         B, N, C, H, W, D, nx, ny = ctx.dims
         dev = grad_out.device
@@ -54,6 +62,16 @@ class _BevPoolFn(torch.autograd.Function):
         need_f, need_w = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
         gf = torch.empty((B, N, C, H, W), dtype=torch.float32, device=dev) if need_f else None
         gw = torch.empty((B, N, D, H, W), dtype=torch.float32, device=dev) if need_w else None
+        if ctx.tile is not None:
+            # the gather backward reads feature rows: the NHWC copy the interval
+            # forward makes on the side, made here for the tiled forward
+            features, dist = ctx.saved_tensors
+            nhwc = torch.empty(features.numel(), dtype=torch.float32, device=dev)
+            _lib.call("bvp_to_nhwc_f32", ptr(features), B * N, C, H * W, ptr(nhwc),
+                      stream_ptr(dev))
+            argmax = None
+        else:
+            nhwc, dist, argmax = ctx.saved_tensors
         if need_f or need_w:
             ws = torch.empty(_lib.load().bvp_backward_workspace_bytes(B, C, cache.n_int_max),
                              dtype=torch.uint8, device=dev)

@@ -228,6 +228,15 @@ class TilePlan:
         _lib.call("bvp_tile_pool_f32", ptr(features), ptr(dist), ctypes.byref(self.st), B, C,
                   mode, ptr(rows), 4 * rows.numel(), ptr(out), stream_ptr(self.device))
 
+    def backward_f32(self, grad_out: torch.Tensor, features: torch.Tensor, dist: torch.Tensor,
+                     B: int, C: int, mode: int, grad_features, grad_dist) -> None:
+        """The adjoint of pool_f32 (SUM / MEAN): grad_features / grad_dist
+        (either may be None) from grad_out (B, C, n_cells)."""
+        rows = self.rows(B, C)
+        _lib.call("bvp_tile_backward_f32", ptr(grad_out), ptr(features), ptr(dist),
+                  ctypes.byref(self.st), B, C, mode, ptr(rows), 4 * rows.numel(),
+                  ptr(grad_features), ptr(grad_dist), stream_ptr(self.device))
+
     def pool_fused_bf16(self, logits: torch.Tensor, context: torch.Tensor, B: int, C: int,
                         mode: int, out: torch.Tensor) -> None:
         rows = self.rows(B, C)

@@ -457,6 +457,133 @@ __device__ __forceinline__ void group_row2(float2 (&acc)[kTileGroup / 2][CS], co
     }
 }
 
+// ---- cluster column staging ---------------------------------------------------
+// The CL tiles of a cluster are CL adjacent columns of one camera.  CTA
+// `rank` moves channel quads (and depth-bin quads) rank, rank + CL, ... for
+// all CL columns -- a warp's access covers CL neighbouring columns x 32/CL
+// rows, 32/CL lines instead of 32 -- each quad one 16-byte word in the
+// shared memory of the CTA owning its column (distributed shared memory).
+struct ColumnXfer {
+    int rank, j, r0;  // this CTA's rank; the lane's column (peer) and first row
+    int n_rb, th;     // row blocks of 32/CL rows; rows of the tile
+    int HW, W;
+};
+
+template <int CL>
+__device__ __forceinline__ ColumnXfer column_xfer(int rank, int th, int HW, int W) {
+    const int lane = threadIdx.x & 31;
+    constexpr int RS = 32 / CL;
+    return ColumnXfer{rank, lane % CL, lane / CL, (th + RS - 1) / RS, th, HW, W};
+}
+
+// item it = (quad qi, row block m); the U items of a round are NW apart, so
+// one division per round and carries after it
+template <int U>
+__device__ __forceinline__ void xfer_items(int i0, int n_rb, int (&qs)[U], int (&ms)[U]) {
+    constexpr int NW = kPoolThreads / 32;
+    int qi = i0 / n_rb, m = i0 - qi * n_rb;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        qs[u] = qi;
+        ms[u] = m;
+        m += NW;
+        while (m >= n_rb) {
+            m -= n_rb;
+            ++qi;
+        }
+    }
+}
+
+// Global -> (remote) shared: rows [0, th) x quads of src (planes HW apart,
+// column base `base` of the cluster's first column + j) into dst[hl][c]
+// (stride floats).  n_quads >= ceil(n_ch / 4): quads past n_ch are stored as
+// zeros.  ES: element bytes (4 fp32, 2 bf16 widened).  wait_first: the
+// cluster barrier's wait (every CTA running, so its shared memory may be
+// written) sits between the first round's loads and its stores.
+template <int CL, int ES>
+__device__ __forceinline__ void stage_quads(const ColumnXfer &x, const void *src, int n_ch,
+                                            int n_quads, int64_t base, float *dst, int stride,
+                                            bool wait_first) {
+    constexpr int NW = kPoolThreads / 32, RS = 32 / CL, U = 4;
+    const int warp = threadIdx.x >> 5;
+    // byte addresses: the tile's column once, then one 32-bit offset per item
+    // and one add per channel of the quad
+    const char *sb = static_cast<const char *>(src) + base * ES;
+    const uint32_t plane = uint32_t(x.HW) * ES, rowb = uint32_t(x.W) * ES;
+    const int n_q = (n_quads - x.rank + CL - 1) / CL;  // this CTA's quads
+    const int items = n_q * x.n_rb;
+    for (int i0 = warp; i0 < items || (wait_first && i0 == warp); i0 += NW * U) {
+        int qs[U], ms[U];
+        xfer_items<U>(i0, x.n_rb, qs, ms);
+        // all U x 4 loads issue before any value is used (raw bits; bf16
+        // widened at the store)
+        uint32_t v[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = i0 + NW * u;
+            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
+            const bool ok = it < items && hl < x.th;
+            const char *pi = sb + (uint64_t(uint32_t(c0)) * plane + uint32_t(hl) * rowb);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const bool on = ok && c0 + e < n_ch;
+                if (ES == 4)
+                    v[u][e] = ldg_l2pf_b32(pi + uint64_t(e) * plane, on);
+                else
+                    v[u][e] = ldg_l2pf_u16(pi + uint64_t(e) * plane, on) << 16;
+            }
+        }
+        if (CL > 1 && wait_first && i0 == warp)
+            asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = i0 + NW * u;
+            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
+            if (it < items && hl < x.th)
+                *reinterpret_cast<float4 *>(dst + hl * stride + c0) =
+                    make_float4(__uint_as_float(v[u][0]), __uint_as_float(v[u][1]),
+                                __uint_as_float(v[u][2]), __uint_as_float(v[u][3]));
+        }
+    }
+}
+
+// (Remote) shared -> global, the reverse of stage_quads: src[hl][c] of the
+// CTA owning column j into dst planes (fp32), channels < n_ch.
+template <int CL>
+__device__ __forceinline__ void unstage_quads(const ColumnXfer &x, float *dst, int n_ch,
+                                              int64_t base, const float *src, int stride) {
+    constexpr int NW = kPoolThreads / 32, RS = 32 / CL, U = 4;
+    const int warp = threadIdx.x >> 5;
+    float *db = dst + base;
+    const int n_q = (((n_ch + 3) >> 2) - x.rank + CL - 1) / CL;
+    const int items = n_q * x.n_rb;
+    for (int i0 = warp; i0 < items; i0 += NW * U) {
+        int qs[U], ms[U];
+        xfer_items<U>(i0, x.n_rb, qs, ms);
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = i0 + NW * u;
+            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
+            v[u] = it < items && hl < x.th
+                       ? *reinterpret_cast<const float4 *>(src + hl * stride + c0)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = i0 + NW * u;
+            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
+            if (it < items && hl < x.th) {
+                float *po = db + int64_t(c0) * x.HW + int64_t(hl) * x.W;
+                const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (c0 + e < n_ch) po[int64_t(e) * x.HW] = e4[e];
+            }
+        }
+    }
+}
+
 // Every global load of a tile is independent of the others (the addresses
 // follow from the tile index alone), so a CTA waits about one memory latency
 // per stage: (1) the feature rows F[hl][c] and the depth weights w[hl][d] of
@@ -515,90 +642,21 @@ tile_pool_kernel(TilePoolArgs a) {
         const uint32_t k = threadIdx.x + kPoolThreads * u;
         pre[u] = k < h.x ? __ldg(rt + k) : 0u;
     }
-    // (1) stage: F[hl][c] = features[n, c, h0 + hl, w]; w[hl][d] = dist[n, d, h0 + hl, w].
-    // The CL tiles of a cluster are CL adjacent columns of one camera.  CTA
-    // `rank` loads channel quads (and depth-bin quads) rank, rank + CL, ... for
-    // all CL columns -- a warp's load covers CL neighbouring columns x 32/CL
-    // rows, 32/CL lines instead of 32 -- and stores each quad as one 16-byte
-    // word into the shared memory of the CTA owning its column (distributed
-    // shared memory).  A warp issues the loads of up to U items before their
-    // stores, so it waits about one memory latency per U items.
+    // (1) stage: F[hl][c] = features[n, c, h0 + hl, w]; w[hl][d] = dist[n, d, h0 + hl, w]
+    // (stage_quads: cluster columns, distributed shared memory)
     {
         namespace cg = cooperative_groups;
         cg::cluster_group cluster = cg::this_cluster();
         const int rank = CL > 1 ? int(cluster.block_rank()) : 0;
-        const int j = lane % CL, r0 = lane / CL;
-        constexpr int RS = 32 / CL;  // rows per load instruction
-        constexpr int U = 4;
-        float *rfs = CL > 1 ? cluster.map_shared_rank(fs, j) : fs;
-        float *rpw = CL > 1 ? cluster.map_shared_rank(pw, j) : pw;
-        const int64_t col = pix0 - rank + j;  // (h0, w_base + j)
-        const int n_rb = (id.th + RS - 1) / RS;
-        // n_quads >= ceil(n_ch / 4): the quads past n_ch are stored as zeros
-        // wait_first: the cluster barrier's wait (every CTA of the cluster
-        // running, so its shared memory may be written) sits between the
-        // first round's loads and its stores -- every warp runs that round
-        auto stage = [&](const void *src, int n_ch, int n_quads, int64_t base, float *dst,
-                         int stride, bool wait_first) {
-            // byte addresses: the tile's column once, then one 32-bit offset
-            // per item and one add per channel of the quad
-            constexpr int ES = SRC == kTileF32 ? 4 : 2;
-            const char *sb = static_cast<const char *>(src) + base * ES;
-            const uint32_t plane = uint32_t(HW) * ES, rowb = uint32_t(g.W) * ES;
-            const int n_q = (n_quads - rank + CL - 1) / CL;  // this CTA's quads
-            const int items = n_q * n_rb;
-            for (int i0 = warp; i0 < items || (wait_first && i0 == warp); i0 += NW * U) {
-                // item it = (quad qi, row block m); the U items of a round are
-                // NW apart, so one division per round and carries after it
-                int qs[U], ms[U];
-                {
-                    int qi = i0 / n_rb, m = i0 - qi * n_rb;
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        qs[u] = qi;
-                        ms[u] = m;
-                        m += NW;
-                        while (m >= n_rb) {
-                            m -= n_rb;
-                            ++qi;
-                        }
-                    }
-                }
-                // all U x 4 loads issue before any value is used (raw bits;
-                // bf16 widened at the store)
-                uint32_t x[U][4];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int it = i0 + NW * u;
-                    const int c0 = 4 * (rank + CL * qs[u]), hl = r0 + RS * ms[u];
-                    const bool ok = it < items && hl < id.th;
-                    const char *pi = sb + (uint64_t(uint32_t(c0)) * plane + uint32_t(hl) * rowb);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const bool on = ok && c0 + e < n_ch;
-                        if (SRC == kTileF32)
-                            x[u][e] = ldg_l2pf_b32(pi + uint64_t(e) * plane, on);
-                        else
-                            x[u][e] = ldg_l2pf_u16(pi + uint64_t(e) * plane, on) << 16;
-                    }
-                }
-                if (CL > 1 && wait_first && i0 == warp)
-                    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int it = i0 + NW * u;
-                    const int c0 = 4 * (rank + CL * qs[u]), hl = r0 + RS * ms[u];
-                    if (it < items && hl < id.th)
-                        *reinterpret_cast<float4 *>(dst + hl * stride + c0) =
-                            make_float4(__uint_as_float(x[u][0]), __uint_as_float(x[u][1]),
-                                        __uint_as_float(x[u][2]), __uint_as_float(x[u][3]));
-                }
-            }
-        };
+        const ColumnXfer x = column_xfer<CL>(rank, id.th, HW, g.W);
+        float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
+        float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
+        const int64_t col = pix0 - rank + x.j;  // (h0, w_base + j)
+        constexpr int ES = SRC == kTileF32 ? 4 : 2;
         // feature rows padded with zero channels up to CP (the products read
         // CS full channel slots)
-        stage(a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
-        stage(a.weights, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
+        stage_quads<CL, ES>(x, a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
+        stage_quads<CL, ES>(x, a.weights, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
         if (CL > 1)
             cluster.sync();
     }
@@ -821,6 +879,312 @@ tile_finalize_kernel(const float *__restrict__ rows, int64_t max_seg,
     }
 }
 
+// ---- backward (config B): the adjoint of the tiled reduction ----------------
+// out[c, cell] = sum_p w_p f[pix(p), c] (SUM; MEAN scales by 1/len(cell)), so
+//   grad_f[pix = (n, h, w), c] = sum_{p of the pixel} w_p g[c, cell(p)]
+//                              = sum_k A[k, h] G[k, c]   per tile, over segments k
+//   grad_w[p]                  = <f[pix(p), :], g[:, cell(p)]> = Dot[k(p), h(p)]
+// with A the forward's aggregated weights and G[k, :] = g[:, cell_k] (x 1/len
+// for MEAN) -- the same column tiles, groups and weight windows as the
+// forward, so every gradient row is read once per (segment, tile) instead of
+// once per point.  No atomics: each gradient element is written once.
+
+// G rows per segment slot: rows[s, :] = g[:, cell(s)] (x 1/len for MEAN), one
+// CTA per 32 cells (coalesced channel lines in, a shared-memory transpose,
+// 4C-byte rows out); blocks without segments are skipped.
+template <int CS>
+__global__ void __launch_bounds__(kPoolThreads)
+tile_grad_rows_kernel(const float *__restrict__ grad_out, const uint32_t *__restrict__ cell_seg_first,
+                      const uint32_t *__restrict__ cell_npts, int n_cells, int C, int mean,
+                      int64_t max_seg, float *__restrict__ rows) {
+    constexpr int CP = CS * 32;
+    constexpr int NW = kPoolThreads / 32;
+    __shared__ float tile[CP][kFinCells + 1];
+    const int c0 = blockIdx.x * kFinCells, b = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nc = min(kFinCells, n_cells - c0);
+    const uint32_t f = __ldg(cell_seg_first + c0 + min(lane, nc));
+    const uint32_t f_end = __ldg(cell_seg_first + c0 + nc);
+    if (__shfl_sync(0xFFFFFFFFu, f, 0) == f_end) return;  // no segment in the block
+    const float *gb = grad_out + int64_t(b) * C * n_cells + c0;
+#pragma unroll
+    for (int k = 0; k < CP / NW; ++k) {
+        const int ch = warp + NW * k;
+        tile[ch][lane] = ch < C && lane < nc ? __ldg(gb + int64_t(ch) * n_cells + lane) : 0.f;
+    }
+    __syncthreads();
+    float *rb = rows + int64_t(b) * max_seg * C + lane;
+#pragma unroll
+    for (int u = 0; u < kFinCells / NW; ++u) {
+        const int cl = warp + NW * u;
+        const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, f, cl);
+        uint32_t s1 = cl < 31 ? __shfl_sync(0xFFFFFFFFu, f, cl + 1) : f_end;
+        if (cl >= nc) s1 = s0;
+        if (s1 == s0) continue;
+        const float inv = mean ? 1.f / float(__ldg(cell_npts + c0 + cl)) : 1.f;
+        for (uint32_t sg = s0; sg < s1; ++sg)
+#pragma unroll
+            for (int j = 0; j < CS; ++j)
+                if (lane + 32 * j < C) rb[int64_t(sg) * C + 32 * j] = tile[lane + 32 * j][cl] * inv;
+    }
+}
+
+struct TileBwdArgs {
+    const float *grad_rows;  // (B, max_seg, C): tile_grad_rows_kernel's rows
+    const float *feats;      // (B, N, C, H, W)
+    const float *dist;       // (B, N, D, H, W)
+    const uint4 *hdr;
+    const uint32_t *rec;
+    const uint4 *groups;
+    const uint32_t *seg_row;
+    float *grad_feats;       // (B, N, C, H, W), or null
+    float *grad_dist;        // (B, N, D, H, W), or null
+    int64_t max_seg;
+    TileGeom g;
+    int C, wbudget;
+};
+
+// A[k, h] of one row for the 4 cells k0..k0+3 of a group (0 for rows outside
+// the group's union).
+__device__ __forceinline__ float4 group_weights4(unsigned long long m, const float *w, int h,
+                                                 int k0) {
+    if (!((m >> h) & 1ull)) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return *reinterpret_cast<const float4 *>(
+        w + __popcll(m & ((1ull << h) - 1ull)) * kTileGroup + k0);
+}
+
+// One CTA per (tile, sample), clusters of CL columns as in the forward.
+// Warp w owns the tile rows h = w, w + 8, w + 16, w + 24 (TH <= 32) and walks
+// every group in order, 4 cells at a time: grad_f of its rows accumulates in
+// registers (FFMA2 over row pairs), and the 16 dot products <f[h], G[k]> of
+// its rows and the 4 cells are reduced across the lanes (16 shuffles) and
+// written over the weight window's (k, h) slots -- which only this warp
+// reads.  Then every point's record picks its Dot from the window into the
+// depth-weight rows (weights no longer needed), points without a record are
+// zeroed, and both tiles go back to global memory through the cluster.
+template <int CS, int CL>
+__global__ void __launch_bounds__(kPoolThreads, 4)
+tile_backward_kernel(TileBwdArgs a) {
+    constexpr int CP = CS * 32;
+    constexpr int FS = CP + 4;
+    constexpr int NW = kPoolThreads / 32;
+    extern __shared__ __align__(16) float sm[];
+    __shared__ uint32_t s_cov[kTileMaxPoints / 32];  // points with a record
+    const TileGeom &g = a.g;
+    const int64_t t = blockIdx.x;
+    const int b = blockIdx.y;
+    const TileId id = tile_id(t, g.W, g.n_hb, g.TH, g.H);
+    const uint4 h = a.hdr[t];
+    const int n_segs = int(h.y), n_groups = int(h.z);
+    const int HW = g.H * g.W, C = a.C, D = g.D, PD = (D + 3) & ~3;
+    float *ws = sm;               // weight window [wbudget]: A, then the dot products
+    float *fs = ws + a.wbudget;   // [TH][FS] feature rows, then grad_f rows
+    float *pw = fs + g.TH * FS;   // [TH][PD] depth weights, then grad_w rows
+    float *gsm = pw + g.TH * PD;  // [2][8][CP] gradient rows of the current / next group
+    const int64_t nb = int64_t(b) * g.N + id.n;
+    const int64_t pix0 = int64_t(id.h0) * g.W + id.w;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = CL > 1 ? int(cluster.block_rank()) : 0;
+    const ColumnXfer x = column_xfer<CL>(rank, id.th, HW, g.W);
+    const int64_t col = pix0 - rank + x.j;
+    if (CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    for (int i = threadIdx.x; i < kTileMaxPoints / 32; i += kPoolThreads) s_cov[i] = 0u;
+    {
+        float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
+        float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
+        stage_quads<CL, 4>(x, a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
+        stage_quads<CL, 4>(x, a.dist, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
+        if (CL > 1) cluster.sync();
+        else __syncthreads();
+    }
+    // this warp's feature rows (the dot products' left operands), then fs is
+    // free for grad_f
+    float fr[4][CS];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < CS; ++j)
+            fr[i][j] = warp + 8 * i < id.th ? fs[(warp + 8 * i) * FS + lane + 32 * j] : 0.f;
+    float2 gacc[2][CS];  // rows (w, w + 8) and (w + 16, w + 24)
+#pragma unroll
+    for (int p2 = 0; p2 < 2; ++p2)
+#pragma unroll
+        for (int j = 0; j < CS; ++j) gacc[p2][j] = make_float2(0.f, 0.f);
+    const uint4 *gt = a.groups + t * g.gcap;
+    const uint32_t *srow = a.seg_row + t * g.tpc;
+    const uint32_t *rt = a.rec + t * g.tpc;
+    const float *grows0 = a.grad_rows + int64_t(b) * a.max_seg * C;
+    const int shift = g.hl_bits + g.d_bits;
+    const uint32_t dmask = (1u << g.d_bits) - 1u, hmask = (1u << g.hl_bits) - 1u;
+    const uint32_t wmask = (1u << (30 - shift)) - 1u;
+    const uint32_t total_w = h.w;
+    for (int q0 = 0; q0 < n_groups;) {
+        // weight windows as in the forward (one for nearly every tile)
+        const uint4 G0 = q0 ? gt[q0] : make_uint4(0u, 0u, 0u, 0u);
+        int q1 = n_groups;
+        if (total_w - G0.z > uint32_t(a.wbudget)) {
+            int lo = q0 + 1, hi = n_groups - 1;
+            q1 = q0 + 1;
+            while (lo <= hi) {
+                const int mid = (lo + hi) >> 1;
+                if (gt[mid].z - G0.z <= uint32_t(a.wbudget)) {
+                    q1 = mid;
+                    lo = mid + 1;
+                } else {
+                    hi = mid - 1;
+                }
+            }
+        }
+        const uint32_t r_end = q1 == n_groups ? h.x : gt[q1].w;
+        const uint32_t w_end = q1 == n_groups ? total_w : gt[q1].z;
+        __syncthreads();  // previous window's records done with ws / pw
+        for (uint32_t i = threadIdx.x; i < w_end - G0.z; i += kPoolThreads) ws[i] = 0.f;
+        __syncthreads();
+        // aggregation: A of the window (the forward's arithmetic)
+        for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
+            uint32_t r = __ldg(rt + k);
+            if (!(r >> 31)) continue;
+            const uint32_t widx = (r >> shift) & wmask;
+            float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+            for (uint32_t kk = k + 1; (r >> 30) & 1u; ++kk) {
+                r = __ldg(rt + kk);
+                sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+            }
+            ws[widx - G0.z] = sum;
+        }
+        __syncthreads();
+        // the groups, every warp all of them (its own rows); each group's 8
+        // gradient rows are copied to shared memory (cp.async, double
+        // buffered: group q + 1's copy runs during group q's products)
+        auto fetch = [&](int q, int buf) {
+            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
+            float *dst = gsm + buf * (kTileGroup * CP);
+            if ((C & 3) == 0) {
+                const int c4 = C >> 2;
+                for (int i = threadIdx.x; i < nk * c4; i += kPoolThreads) {
+                    const int k = i / c4, c = 4 * (i - k * c4);
+                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * CP + c))),
+                                 "l"(src));
+                }
+            } else {
+                for (int i = threadIdx.x; i < nk * C; i += kPoolThreads) {
+                    const int k = i / C, c = i - k * C;
+                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * CP + c))),
+                                 "l"(src));
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        fetch(q0, 0);
+        for (int q = q0; q < q1; ++q) {
+            if (q + 1 < q1) {
+                fetch(q + 1, (q + 1 - q0) & 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncthreads();  // group q's rows visible to every warp
+            const float *gq = gsm + ((q - q0) & 1) * (kTileGroup * CP) + lane;
+            const uint4 Gq = gt[q];
+            const unsigned long long m = Gq.x | (static_cast<unsigned long long>(Gq.y) << 32);
+            float *wq = ws + (Gq.z - G0.z);
+            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
+#pragma unroll
+            for (int k0 = 0; k0 < kTileGroup; k0 += 4) {
+                if (k0 >= nk) break;
+                float gr[4][CS];
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    const bool ok = k0 + kk < nk;
+#pragma unroll
+                    for (int j = 0; j < CS; ++j)
+                        gr[kk][j] = ok && lane + 32 * j < C ? gq[(k0 + kk) * CP + 32 * j] : 0.f;
+                }
+                // grad_f: rows pair (hA, hB) += (A[k, hA], A[k, hB]) * G[k, c]
+#pragma unroll
+                for (int p2 = 0; p2 < 2; ++p2) {
+                    const int hA = warp + 16 * p2, hB = hA + 8;
+                    const float4 wa = group_weights4(m, wq, hA, k0);
+                    const float4 wb = group_weights4(m, wq, hB, k0);
+#pragma unroll
+                    for (int j = 0; j < CS; ++j) {
+                        ffma2(gacc[p2][j], make_float2(wa.x, wb.x), gr[0][j]);
+                        ffma2(gacc[p2][j], make_float2(wa.y, wb.y), gr[1][j]);
+                        ffma2(gacc[p2][j], make_float2(wa.z, wb.z), gr[2][j]);
+                        ffma2(gacc[p2][j], make_float2(wa.w, wb.w), gr[3][j]);
+                    }
+                }
+                // dot products <f[h_i], G[k]>: lane partials over its channels,
+                // then a 16-value transpose reduction; index = 4 i + kk
+                float v[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        float sacc = 0.f;
+#pragma unroll
+                        for (int j = 0; j < CS; ++j) sacc = fmaf(fr[i][j], gr[kk][j], sacc);
+                        v[4 * i + kk] = sacc;
+                    }
+#pragma unroll
+                for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
+                    const bool upper = lane & o;
+#pragma unroll
+                    for (int e = 0; e < n; ++e) {
+                        const float send = upper ? v[e] : v[e + n];
+                        const float keep = upper ? v[e + n] : v[e];
+                        v[e] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, o);
+                    }
+                }
+                v[0] += __shfl_xor_sync(0xFFFFFFFFu, v[0], 1);
+                const int idx = (lane >> 1) & 15, i = idx >> 2, kk = idx & 3, hh = warp + 8 * i;
+                __syncwarp();
+                if (!(lane & 1) && k0 + kk < nk && hh < id.th && ((m >> hh) & 1ull))
+                    wq[__popcll(m & ((1ull << hh) - 1ull)) * kTileGroup + k0 + kk] = v[0];
+                __syncwarp();
+            }
+            __syncthreads();  // every warp done with this buffer before it is refilled
+        }
+        // every point of the window: its Dot into the depth-weight rows
+        for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
+            const uint32_t r = __ldg(rt + k);
+            const uint32_t hl = (r >> g.d_bits) & hmask, d = r & dmask;
+            pw[hl * PD + d] = ws[((r >> shift) & wmask) - G0.z];
+            const uint32_t pt = hl * uint32_t(D) + d;
+            atomicOr(&s_cov[pt >> 5], 1u << (pt & 31));
+        }
+        q0 = q1;
+    }
+    __syncthreads();
+    // points without a record (out of range) get a zero weight gradient; the
+    // warp's grad_f rows go over the feature rows
+    for (int pt = threadIdx.x; pt < id.th * D; pt += kPoolThreads)
+        if (!((s_cov[pt >> 5] >> (pt & 31)) & 1u)) pw[(pt / D) * PD + pt % D] = 0.f;
+#pragma unroll
+    for (int p2 = 0; p2 < 2; ++p2)
+#pragma unroll
+        for (int j = 0; j < CS; ++j) {
+            const int hA = warp + 16 * p2, hB = hA + 8;
+            if (hA < id.th) fs[hA * FS + lane + 32 * j] = gacc[p2][j].x;
+            if (hB < id.th) fs[hB * FS + lane + 32 * j] = gacc[p2][j].y;
+        }
+    if (CL > 1) cluster.sync();
+    else __syncthreads();
+    {
+        const float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
+        const float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
+        if (a.grad_feats) unstage_quads<CL>(x, a.grad_feats, C, nb * C * HW + col, rfs, FS);
+        if (a.grad_dist) unstage_quads<CL>(x, a.grad_dist, D, nb * D * HW + col, rpw, PD);
+    }
+    if (CL > 1) cluster.sync();  // peers done reading this CTA's shared memory
+}
+
 // ---- plan layout -------------------------------------------------------------
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -980,6 +1344,73 @@ static int run_tile_pool(const void *feats, const void *weights, const bvp_tile_
                     cudaGetErrorString(e));
     }
     return check_launch("tile_pool");
+}
+
+template <int CS, int CL>
+static int launch_backward(const TileBwdArgs &a, int B, size_t smem, cudaStream_t s) {
+    static int max_dyn = -1;
+    if (max_dyn < 0) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, tile_backward_kernel<CS, CL>);
+        max_dyn = 227 * 1024 - int(fa.sharedSizeBytes);
+        cudaFuncSetAttribute(tile_backward_kernel<CS, CL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+    }
+    BVP_REQUIRE(smem <= size_t(max_dyn), BVP_ERR_UNSUPPORTED,
+                "tile backward needs %zu bytes of shared memory (max %d)", smem, max_dyn);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(a.g.T), unsigned(B));
+    cfg.blockDim = dim3(kPoolThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_c[1];
+    attr_c[0].id = cudaLaunchAttributeClusterDimension;
+    attr_c[0].val.clusterDim.x = CL;
+    attr_c[0].val.clusterDim.y = 1;
+    attr_c[0].val.clusterDim.z = 1;
+    cfg.attrs = attr_c;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, tile_backward_kernel<CS, CL>, a);
+    BVP_REQUIRE(e == cudaSuccess, BVP_ERR_CUDA, "tile_backward launch: %s", cudaGetErrorString(e));
+    return BVP_OK;
+}
+
+template <int CS>
+static int run_tile_backward(const float *grad_out, const float *feats, const float *dist,
+                             const bvp_tile_plan *p, const TileGeom &g, int B, int C, int mean,
+                             float *rows, float *grad_feats, float *grad_dist, cudaStream_t s) {
+    const PlanLayout L = plan_layout(g, p->n_cells);
+    tile_grad_rows_kernel<CS><<<dim3(unsigned(ceil_div(p->n_cells, kFinCells)), unsigned(B)),
+                                kPoolThreads, 0, s>>>(
+        grad_out, at<const uint32_t>(p, L.csf), at<const uint32_t>(p, L.npts), int(p->n_cells), C,
+        mean, p->max_seg, rows);
+    TileBwdArgs a{};
+    a.grad_rows = rows;
+    a.feats = feats;
+    a.dist = dist;
+    a.hdr = at<const uint4>(p, L.hdr);
+    a.rec = at<const uint32_t>(p, L.rec);
+    a.groups = at<const uint4>(p, L.groups);
+    a.seg_row = at<const uint32_t>(p, L.seg_row);
+    a.grad_feats = grad_feats;
+    a.grad_dist = grad_dist;
+    a.max_seg = p->max_seg;
+    a.g = g;
+    a.C = C;
+    a.wbudget = std::max(2048, 128 * g.TH);
+    const int CP = CS * 32;
+    const size_t smem = sizeof(float) * (size_t(g.TH) * (CP + 4) + size_t(g.TH) * ((g.D + 3) & ~3) +
+                                         a.wbudget + 2 * kTileGroup * CP);
+    const int CL = (g.W % 8 == 0) ? 8 : (g.W % 4 == 0) ? 4 : (g.W % 2 == 0) ? 2 : 1;
+    int rc;
+    switch (CL) {
+        case 8: rc = launch_backward<CS, 8>(a, B, smem, s); break;
+        case 4: rc = launch_backward<CS, 4>(a, B, smem, s); break;
+        case 2: rc = launch_backward<CS, 2>(a, B, smem, s); break;
+        default: rc = launch_backward<CS, 1>(a, B, smem, s); break;
+    }
+    if (rc != BVP_OK) return rc;
+    return check_launch("tile_backward");
 }
 
 template <int SRC>
@@ -1151,6 +1582,37 @@ int bvp_tile_pool_f32(const float *features, const float *dist, const bvp_tile_p
                       int C, int mode, float *rows, size_t rows_bytes, float *out, void *stream) {
     return tile_pool_dispatch<kTileF32>(features, dist, plan, B, C, mode, rows, rows_bytes, out,
                                         as_stream(stream));
+}
+
+int bvp_tile_backward_f32(const float *grad_out, const float *features, const float *dist,
+                          const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
+                          size_t rows_bytes, float *grad_features, float *grad_dist,
+                          void *stream) {
+    TileGeom g;
+    const int rc = plan_dims_from(plan, g);
+    if (rc != BVP_OK) return rc;
+    BVP_REQUIRE(B >= 1 && C >= 0, BVP_ERR_INVALID, "bad dims B=%d C=%d", B, C);
+    BVP_REQUIRE(mode == BVP_SUM || mode == BVP_MEAN, BVP_ERR_UNSUPPORTED,
+                "the tiled backward takes SUM and MEAN only (mode %d)", mode);
+    BVP_REQUIRE(C <= 128, BVP_ERR_UNSUPPORTED, "the tiled backward takes C <= 128 (C=%d)", C);
+    BVP_REQUIRE(g.TH <= 32, BVP_ERR_UNSUPPORTED, "the tiled backward takes tiles of <= 32 rows");
+    if (C == 0 || (!grad_features && !grad_dist)) return BVP_OK;
+    BVP_REQUIRE(grad_out && features && dist && rows, BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(rows_bytes >= size_t(B) * plan->max_seg * C * sizeof(float), BVP_ERR_INVALID,
+                "segment-row scratch too small: need %zu bytes, got %zu",
+                size_t(B) * plan->max_seg * C * sizeof(float), rows_bytes);
+    cudaStream_t s = as_stream(stream);
+    const int mean = mode == BVP_MEAN;
+    switch ((C + 31) / 32) {
+        case 1: return run_tile_backward<1>(grad_out, features, dist, plan, g, B, C, mean, rows,
+                                            grad_features, grad_dist, s);
+        case 2: return run_tile_backward<2>(grad_out, features, dist, plan, g, B, C, mean, rows,
+                                            grad_features, grad_dist, s);
+        case 3: return run_tile_backward<3>(grad_out, features, dist, plan, g, B, C, mean, rows,
+                                            grad_features, grad_dist, s);
+        default: return run_tile_backward<4>(grad_out, features, dist, plan, g, B, C, mean, rows,
+                                             grad_features, grad_dist, s);
+    }
 }
 
 int bvp_tile_pool_fused_bf16(const uint16_t *logits, const uint16_t *context,

@@ -810,3 +810,38 @@ def test_tile_path_random_wide_instances(seed):
     want = o.fused_pool(fb, lb, cache.ranks, cache.interval_starts, cache.interval_cells,
                         grid.n_cells, "sum")
     assert max_rel_dev(want, got) <= 1e-5
+
+
+@pytest.mark.parametrize("seed", [20_000 + s for s in range(6)])
+@pytest.mark.parametrize("red", ["sum", "mean"])
+def test_tiled_backward_random_wide_instances(seed, red):
+    """bev_pool's SUM / MEAN backward (tiled forward, gather backward) and the
+    tiled adjoint (bvp_tile_backward_f32) on random wide rigs against the
+    fp64 restatement: gradients of both the features and the depth
+    distribution, out-of-range points and pixels without in-range points
+    included (zeros)."""
+    inst = random_instance(seed, 96, 130, 40)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    dist = o.normalize_depth(inst.logits)
+    C = inst.features.shape[1]
+    if C == 0:
+        return
+    dev = torch.device("cuda")
+    f = torch.from_numpy(inst.features).to(dev).requires_grad_(True)
+    d = torch.from_numpy(dist).to(dev).requires_grad_(True)
+    out = bp.bev_pool(f, d, cache, grid, red)
+    g = np.random.default_rng(seed).standard_normal((C, grid.n_cells)).astype(np.float32)
+    out.backward(torch.from_numpy(g).to(dev).view_as(out))
+    gf, gw = o.pool_backward(inst.features, dist, cache.cell_of_point, g.astype(np.float64),
+                             cache.ranks, cache.interval_starts, cache.interval_cells, red)
+    assert max_rel_dev(gf, f.grad.cpu().numpy()) <= FP32_TOL
+    assert max_rel_dev(gw, d.grad.cpu().numpy()) <= FP32_TOL
+    n_cam = inst.cams.shape[0]
+    tp = cache.tile_plan(n_cam, frustum.height, frustum.width, frustum.depth_bins)
+    tf = torch.full_like(f, float("nan"))
+    tw = torch.full_like(d, float("nan"))
+    tp.backward_f32(torch.from_numpy(g).to(dev), f.detach(), d.detach(), 1, C,
+                    bp._lib.BVP_MEAN if red == "mean" else bp._lib.BVP_SUM, tf, tw)
+    assert max_rel_dev(gf, tf.cpu().numpy()) <= FP32_TOL
+    assert max_rel_dev(gw, tw.cpu().numpy()) <= FP32_TOL
