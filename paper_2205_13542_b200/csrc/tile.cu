@@ -944,32 +944,60 @@ struct TileBwdArgs {
     int C, wbudget;
 };
 
-// A[k, h] of one row for the 4 cells k0..k0+3 of a group (0 for rows outside
-// the group's union).
-__device__ __forceinline__ float4 group_weights4(unsigned long long m, const float *w, int h,
-                                                 int k0) {
-    if (!((m >> h) & 1ull)) return make_float4(0.f, 0.f, 0.f, 0.f);
-    return *reinterpret_cast<const float4 *>(
-        w + __popcll(m & ((1ull << h) - 1ull)) * kTileGroup + k0);
+// ---- tensor-core pieces of the backward (mma.sync m16n8k8, tf32 operands) ---
+// fp32 accuracy from tf32 operands: x = hi + lo, hi = tf32(x), lo the exact
+// fp32 remainder; a*b ~ hi*hi + hi*lo + lo*hi (the dropped lo*lo is 2^-22
+// relative).  Measured 278 TFLOP/s for tf32 mma.sync on this GPU
+// (scripts/mma_vs_ffma2.cu): the backward's two products per group -- the
+// (row, segment) dot products over C channels and grad_f's 8-segment sums --
+// are GEMM-shaped with K = C and N = C, where FFMA lanes-over-channels need a
+// cross-lane reduction per dot product.
+__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    lo = __float_as_uint(x - __uint_as_float(hi));
+}
+// d += a * b three ways (lo*hi, hi*lo, hi*hi: small terms first)
+__device__ __forceinline__ void mma3_tf32(float (&d)[4], const uint32_t (&ah)[4],
+                                          const uint32_t (&al)[4], uint32_t bh0, uint32_t bh1,
+                                          uint32_t bl0, uint32_t bl1) {
+#define BVP_MMA_TF32(A, B0, B1)                                                        \
+    asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, "       \
+        "{%4, %5, %6, %7}, {%8, %9}, {%0, %1, %2, %3};"                                \
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])                               \
+        : "r"(A[0]), "r"(A[1]), "r"(A[2]), "r"(A[3]), "r"(B0), "r"(B1))
+    BVP_MMA_TF32(al, bh0, bh1);
+    BVP_MMA_TF32(ah, bl0, bl1);
+    BVP_MMA_TF32(ah, bh0, bh1);
+#undef BVP_MMA_TF32
 }
 
-// One CTA per (tile, sample), clusters of CL columns as in the forward.
-// Warp w owns the tile rows h = w, w + 8, w + 16, w + 24 (TH <= 32) and walks
-// every group in order, 4 cells at a time: grad_f of its rows accumulates in
-// registers (FFMA2 over row pairs), and the 16 dot products <f[h], G[k]> of
-// its rows and the 4 cells are reduced across the lanes (16 shuffles) and
-// written over the weight window's (k, h) slots -- which only this warp
-// reads.  Then every point's record picks its Dot from the window into the
-// depth-weight rows (weights no longer needed), points without a record are
-// zeroed, and both tiles go back to global memory through the cluster.
+// One CTA per (tile, sample), clusters of CL columns as in the forward.  Per
+// group (every warp every group; the group's 8 gradient rows copied to
+// shared memory, double buffered):
+//   Dot[h, k] = sum_c F[h, c] G[k, c]   -- M = 32 rows, N = 8 segments, K = C:
+//     warp w takes m-tile w & 1 and k-steps w >> 1 (+4, +8) with its F
+//     fragments held in registers; the 4 K-partials are added in a fixed
+//     order through shared memory and written over the weight window's
+//     (k, h) slots (A is read before);
+//   grad_f[h, c] += sum_k A[k, h] G[k, c] -- M = 32 rows, N = C, K = 8:
+//     warp w accumulates m-tile w & 1 x n-tiles w >> 1 (+4, +8) in registers
+//     over all groups, in order.
+// Then every point's record picks its Dot from the window into the
+// depth-weight rows (weights no longer needed), points without a record
+// are zeroed, grad_f goes over the feature rows, and both tiles go back to
+// global memory through the cluster.  Deterministic (fixed sums, no atomics
+// on values); tiles of <= 32 rows, C <= 128.
 template <int CS, int CL>
 __global__ void __launch_bounds__(kPoolThreads, 4)
 tile_backward_kernel(TileBwdArgs a) {
     constexpr int CP = CS * 32;
-    constexpr int FS = CP + 4;
-    constexpr int NW = kPoolThreads / 32;
+    constexpr int FS = CP + 4;   // = 4 (mod 32): conflict-free fragment loads
+    constexpr int GS = CP + 4;
+    constexpr int NKS = (CP + 7) / 8;
     extern __shared__ __align__(16) float sm[];
     __shared__ uint32_t s_cov[kTileMaxPoints / 32];  // points with a record
+    __shared__ float s_dpart[4][32][kTileGroup];      // Dot K-partials of a group
+    __shared__ float s_a[32][kTileGroup + 1];          // the group's A, dense [row][segment]
     const TileGeom &g = a.g;
     const int64_t t = blockIdx.x;
     const int b = blockIdx.y;
@@ -980,10 +1008,13 @@ tile_backward_kernel(TileBwdArgs a) {
     float *ws = sm;               // weight window [wbudget]: A, then the dot products
     float *fs = ws + a.wbudget;   // [TH][FS] feature rows, then grad_f rows
     float *pw = fs + g.TH * FS;   // [TH][PD] depth weights, then grad_w rows
-    float *gsm = pw + g.TH * PD;  // [2][8][CP] gradient rows of the current / next group
+    float *gsm = pw + g.TH * PD;  // [2][8][GS] gradient rows of the current / next group
     const int64_t nb = int64_t(b) * g.N + id.n;
     const int64_t pix0 = int64_t(id.h0) * g.W + id.w;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int mt = warp & 1, wq4 = warp >> 1;  // m-tile; k-step / n-tile quarter
+    const int NT = (C + 7) >> 3;               // n-tiles (and k-steps) over C
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = CL > 1 ? int(cluster.block_rank()) : 0;
@@ -991,6 +1022,8 @@ tile_backward_kernel(TileBwdArgs a) {
     const int64_t col = pix0 - rank + x.j;
     if (CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     for (int i = threadIdx.x; i < kTileMaxPoints / 32; i += kPoolThreads) s_cov[i] = 0u;
+    // gradient-row buffers: channels past C stay zero (the copies stop at C)
+    for (int i = threadIdx.x; i < 2 * kTileGroup * GS; i += kPoolThreads) gsm[i] = 0.f;
     {
         float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
         float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
@@ -999,19 +1032,22 @@ tile_backward_kernel(TileBwdArgs a) {
         if (CL > 1) cluster.sync();
         else __syncthreads();
     }
-    // this warp's feature rows (the dot products' left operands), then fs is
-    // free for grad_f
-    float fr[4][CS];
+    // this warp's F fragments (A operand of Dot): rows mt*16 + g (+8),
+    // channels 8 ks + t (+4), k-steps ks = wq4, wq4 + 4, wq4 + 8
+    uint32_t fh[3][4], fl[3][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 3; ++i) {
+        const int ks = wq4 + 4 * i;
 #pragma unroll
-        for (int j = 0; j < CS; ++j)
-            fr[i][j] = warp + 8 * i < id.th ? fs[(warp + 8 * i) * FS + lane + 32 * j] : 0.f;
-    float2 gacc[2][CS];  // rows (w, w + 8) and (w + 16, w + 24)
+        for (int e = 0; e < 4; ++e) {
+            const int r = mt * 16 + g8 + 8 * (e & 1), c = 8 * ks + t4 + 4 * (e >> 1);
+            const float v = ks < NT && r < id.th ? fs[r * FS + c] : 0.f;
+            split_tf32(v, fh[i][e], fl[i][e]);
+        }
+    }
+    float gacc[3][4];  // grad_f: m-tile mt x n-tiles wq4 (+4, +8)
 #pragma unroll
-    for (int p2 = 0; p2 < 2; ++p2)
-#pragma unroll
-        for (int j = 0; j < CS; ++j) gacc[p2][j] = make_float2(0.f, 0.f);
+    for (int i = 0; i < 3; ++i) gacc[i][0] = gacc[i][1] = gacc[i][2] = gacc[i][3] = 0.f;
     const uint4 *gt = a.groups + t * g.gcap;
     const uint32_t *srow = a.seg_row + t * g.tpc;
     const uint32_t *rt = a.rec + t * g.tpc;
@@ -1020,6 +1056,37 @@ tile_backward_kernel(TileBwdArgs a) {
     const uint32_t dmask = (1u << g.d_bits) - 1u, hmask = (1u << g.hl_bits) - 1u;
     const uint32_t wmask = (1u << (30 - shift)) - 1u;
     const uint32_t total_w = h.w;
+    auto fetch = [&](int q, int buf) {  // group q's gradient rows -> gsm[buf]
+        const int nk = min(kTileGroup, n_segs - q * kTileGroup);
+        float *dst = gsm + buf * (kTileGroup * GS);
+        if ((C & 3) == 0) {
+            const int c4 = C >> 2;
+            for (int i = threadIdx.x; i < kTileGroup * c4; i += kPoolThreads) {
+                const int k = i / c4, c = 4 * (i - k * c4);
+                if (k < nk) {
+                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * GS + c))),
+                                 "l"(src));
+                } else {  // rows past the group's cells: zero (their A is 0)
+                    *reinterpret_cast<float4 *>(dst + k * GS + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        } else {
+            for (int i = threadIdx.x; i < kTileGroup * C; i += kPoolThreads) {
+                const int k = i / C, c = i - k * C;
+                if (k < nk) {
+                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * GS + c))),
+                                 "l"(src));
+                } else {
+                    dst[k * GS + c] = 0.f;
+                }
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     for (int q0 = 0; q0 < n_groups;) {
         // weight windows as in the forward (one for nearly every tile)
         const uint4 G0 = q0 ? gt[q0] : make_uint4(0u, 0u, 0u, 0u);
@@ -1041,6 +1108,7 @@ tile_backward_kernel(TileBwdArgs a) {
         const uint32_t w_end = q1 == n_groups ? total_w : gt[q1].z;
         __syncthreads();  // previous window's records done with ws / pw
         for (uint32_t i = threadIdx.x; i < w_end - G0.z; i += kPoolThreads) ws[i] = 0.f;
+        fetch(q0, 0);
         __syncthreads();
         // aggregation: A of the window (the forward's arithmetic)
         for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
@@ -1054,34 +1122,6 @@ tile_backward_kernel(TileBwdArgs a) {
             }
             ws[widx - G0.z] = sum;
         }
-        __syncthreads();
-        // the groups, every warp all of them (its own rows); each group's 8
-        // gradient rows are copied to shared memory (cp.async, double
-        // buffered: group q + 1's copy runs during group q's products)
-        auto fetch = [&](int q, int buf) {
-            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
-            float *dst = gsm + buf * (kTileGroup * CP);
-            if ((C & 3) == 0) {
-                const int c4 = C >> 2;
-                for (int i = threadIdx.x; i < nk * c4; i += kPoolThreads) {
-                    const int k = i / c4, c = 4 * (i - k * c4);
-                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * CP + c))),
-                                 "l"(src));
-                }
-            } else {
-                for (int i = threadIdx.x; i < nk * C; i += kPoolThreads) {
-                    const int k = i / C, c = i - k * C;
-                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * CP + c))),
-                                 "l"(src));
-                }
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        fetch(q0, 0);
         for (int q = q0; q < q1; ++q) {
             if (q + 1 < q1) {
                 fetch(q + 1, (q + 1 - q0) & 1);
@@ -1089,68 +1129,63 @@ tile_backward_kernel(TileBwdArgs a) {
             } else {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
             }
-            __syncthreads();  // group q's rows visible to every warp
-            const float *gq = gsm + ((q - q0) & 1) * (kTileGroup * CP) + lane;
             const uint4 Gq = gt[q];
             const unsigned long long m = Gq.x | (static_cast<unsigned long long>(Gq.y) << 32);
             float *wq = ws + (Gq.z - G0.z);
             const int nk = min(kTileGroup, n_segs - q * kTileGroup);
+            // this thread's (row, segment) of the group: its window slot
+            const int ar = threadIdx.x >> 3, ak = threadIdx.x & 7;
+            const bool a_in = ak < nk && ar < id.th && ((m >> ar) & 1ull);
+            const int a_slot = a_in ? __popcll(m & ((1ull << ar) - 1ull)) * kTileGroup + ak : 0;
+            __syncthreads();  // group q's rows (and, first time, A) visible; s_a free
+            s_a[ar][ak] = a_in ? wq[a_slot] : 0.f;
+            __syncthreads();
+            const float *gq = gsm + ((q - q0) & 1) * (kTileGroup * GS);
+            // Dot K-partial: this warp's k-steps
+            {
+                float dacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int k0 = 0; k0 < kTileGroup; k0 += 4) {
-                if (k0 >= nk) break;
-                float gr[4][CS];
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const bool ok = k0 + kk < nk;
-#pragma unroll
-                    for (int j = 0; j < CS; ++j)
-                        gr[kk][j] = ok && lane + 32 * j < C ? gq[(k0 + kk) * CP + 32 * j] : 0.f;
-                }
-                // grad_f: rows pair (hA, hB) += (A[k, hA], A[k, hB]) * G[k, c]
-#pragma unroll
-                for (int p2 = 0; p2 < 2; ++p2) {
-                    const int hA = warp + 16 * p2, hB = hA + 8;
-                    const float4 wa = group_weights4(m, wq, hA, k0);
-                    const float4 wb = group_weights4(m, wq, hB, k0);
-#pragma unroll
-                    for (int j = 0; j < CS; ++j) {
-                        ffma2(gacc[p2][j], make_float2(wa.x, wb.x), gr[0][j]);
-                        ffma2(gacc[p2][j], make_float2(wa.y, wb.y), gr[1][j]);
-                        ffma2(gacc[p2][j], make_float2(wa.z, wb.z), gr[2][j]);
-                        ffma2(gacc[p2][j], make_float2(wa.w, wb.w), gr[3][j]);
+                for (int i = 0; i < 3; ++i) {
+                    const int ks = wq4 + 4 * i;
+                    if (ks < NT) {  // B = G^T: b0 = G[g][8 ks + t], b1 = G[g][8 ks + t + 4]
+                        uint32_t bh0, bl0, bh1, bl1;
+                        split_tf32(gq[g8 * GS + 8 * ks + t4], bh0, bl0);
+                        split_tf32(gq[g8 * GS + 8 * ks + t4 + 4], bh1, bl1);
+                        mma3_tf32(dacc, fh[i], fl[i], bh0, bh1, bl0, bl1);
                     }
                 }
-                // dot products <f[h_i], G[k]>: lane partials over its channels,
-                // then a 16-value transpose reduction; index = 4 i + kk
-                float v[16];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        float sacc = 0.f;
-#pragma unroll
-                        for (int j = 0; j < CS; ++j) sacc = fmaf(fr[i][j], gr[kk][j], sacc);
-                        v[4 * i + kk] = sacc;
-                    }
-#pragma unroll
-                for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
-                    const bool upper = lane & o;
-#pragma unroll
-                    for (int e = 0; e < n; ++e) {
-                        const float send = upper ? v[e] : v[e + n];
-                        const float keep = upper ? v[e + n] : v[e];
-                        v[e] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, o);
-                    }
-                }
-                v[0] += __shfl_xor_sync(0xFFFFFFFFu, v[0], 1);
-                const int idx = (lane >> 1) & 15, i = idx >> 2, kk = idx & 3, hh = warp + 8 * i;
-                __syncwarp();
-                if (!(lane & 1) && k0 + kk < nk && hh < id.th && ((m >> hh) & 1ull))
-                    wq[__popcll(m & ((1ull << hh) - 1ull)) * kTileGroup + k0 + kk] = v[0];
-                __syncwarp();
+                // rows mt*16 + g (+8), segments 2t, 2t+1
+                s_dpart[wq4][mt * 16 + g8][2 * t4] = dacc[0];
+                s_dpart[wq4][mt * 16 + g8][2 * t4 + 1] = dacc[1];
+                s_dpart[wq4][mt * 16 + g8 + 8][2 * t4] = dacc[2];
+                s_dpart[wq4][mt * 16 + g8 + 8][2 * t4 + 1] = dacc[3];
             }
-            __syncthreads();  // every warp done with this buffer before it is refilled
+            // grad_f: A^T (rows x segments) . G (segments x channels)
+            {
+                const int r0 = mt * 16 + g8;
+                const float a4[4] = {s_a[r0][t4], s_a[r0 + 8][t4], s_a[r0][t4 + 4],
+                                     s_a[r0 + 8][t4 + 4]};
+                uint32_t ah[4], al[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) split_tf32(a4[e], ah[e], al[e]);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    const int nt = wq4 + 4 * i;
+                    if (nt < NT) {  // b0 = G[t][8 nt + g], b1 = G[t + 4][8 nt + g]
+                        uint32_t bh0, bl0, bh1, bl1;
+                        split_tf32(gq[t4 * GS + 8 * nt + g8], bh0, bl0);
+                        split_tf32(gq[(t4 + 4) * GS + 8 * nt + g8], bh1, bl1);
+                        mma3_tf32(gacc[i], ah, al, bh0, bh1, bl0, bl1);
+                    }
+                }
+            }
+            __syncthreads();  // partials complete; every warp done with A and this buffer
+            // Dot = the 4 K-partials in order, over the window's (k, h) slots
+            if (a_in)
+                wq[a_slot] = ((s_dpart[0][ar][ak] + s_dpart[1][ar][ak]) + s_dpart[2][ar][ak]) +
+                             s_dpart[3][ar][ak];
         }
+        __syncthreads();
         // every point of the window: its Dot into the depth-weight rows
         for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
             const uint32_t r = __ldg(rt + k);
@@ -1163,17 +1198,26 @@ tile_backward_kernel(TileBwdArgs a) {
     }
     __syncthreads();
     // points without a record (out of range) get a zero weight gradient; the
-    // warp's grad_f rows go over the feature rows
-    for (int pt = threadIdx.x; pt < id.th * D; pt += kPoolThreads)
-        if (!((s_cov[pt >> 5] >> (pt & 31)) & 1u)) pw[(pt / D) * PD + pt % D] = 0.f;
-#pragma unroll
-    for (int p2 = 0; p2 < 2; ++p2)
-#pragma unroll
-        for (int j = 0; j < CS; ++j) {
-            const int hA = warp + 16 * p2, hB = hA + 8;
-            if (hA < id.th) fs[hA * FS + lane + 32 * j] = gacc[p2][j].x;
-            if (hB < id.th) fs[hB * FS + lane + 32 * j] = gacc[p2][j].y;
+    // grad_f fragments go over the feature rows
+    for (int hl = warp; hl < id.th; hl += kPoolThreads / 32)
+        for (int d = lane; d < D; d += 32) {
+            const int pt = hl * D + d;
+            if (!((s_cov[pt >> 5] >> (pt & 31)) & 1u)) pw[hl * PD + d] = 0.f;
         }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const int nt = wq4 + 4 * i;
+        if (nt >= NT) continue;
+        const int r0 = mt * 16 + g8, c0 = 8 * nt + 2 * t4;
+        if (r0 < id.th) {
+            fs[r0 * FS + c0] = gacc[i][0];
+            fs[r0 * FS + c0 + 1] = gacc[i][1];
+        }
+        if (r0 + 8 < id.th) {
+            fs[(r0 + 8) * FS + c0] = gacc[i][2];
+            fs[(r0 + 8) * FS + c0 + 1] = gacc[i][3];
+        }
+    }
     if (CL > 1) cluster.sync();
     else __syncthreads();
     {
@@ -1400,7 +1444,7 @@ static int run_tile_backward(const float *grad_out, const float *feats, const fl
     a.wbudget = std::max(2048, 128 * g.TH);
     const int CP = CS * 32;
     const size_t smem = sizeof(float) * (size_t(g.TH) * (CP + 4) + size_t(g.TH) * ((g.D + 3) & ~3) +
-                                         a.wbudget + 2 * kTileGroup * CP);
+                                         a.wbudget + 2 * kTileGroup * (CP + 4));
     const int CL = (g.W % 8 == 0) ? 8 : (g.W % 4 == 0) ? 4 : (g.W % 2 == 0) ? 2 : 1;
     int rc;
     switch (CL) {
