@@ -7,6 +7,9 @@
  *                                       point gather table; one call)
  *               bvp_normalize_depth    (fp64 softmax over D)
  *               bvp_pool_forward_f32   (fast fp32 and exact fp64)
+ *   per rig:    bvp_build_tile_plan_ranks (the tiled reduction's plan, from
+ *                                       the association)
+ *               bvp_tile_pool_f32      (the tiled reduction: the fast path)
  *
  * Writes the inputs, the cache's ranks / interval table and both maps to
  * <out_dir>/*.bin so tests/test_c_abi.py can check them against the oracle.
@@ -141,6 +144,23 @@ int main(int argc, char **argv) {
     CHECK_BVP(bvp_pool_forward_f32(feat, dist, ranks, starts, icells, cell_first, &sched, 1, N, C,
                                    H, W, D, nx, ny, n_int_max, BVP_SUM, 1, out_exact, nhwc, NULL,
                                    scratch, scratch_bytes, NULL));
+    /* the tiled reduction (csrc/tile.cu): plan from the association, then
+     * the pooling; the plan is per rig, the pooling per frame */
+    const size_t plan_bytes = bvp_tile_plan_bytes(N, H, W, D, n_cells);
+    const size_t plan_ws_bytes = bvp_tile_plan_workspace_bytes(N, H, W, D, n_cells);
+    if (plan_bytes == 0) {
+        fprintf(stderr, "frustum not supported by the tile plan\n");
+        return 1;
+    }
+    void *plan_buf = dev_alloc(plan_bytes), *plan_ws = dev_alloc(plan_ws_bytes);
+    bvp_tile_plan plan;
+    CHECK_BVP(bvp_tile_plan_init(&plan, N, H, W, D, n_cells, plan_buf, plan_bytes, P));
+    CHECK_BVP(bvp_build_tile_plan_ranks(cells, ranks, counts, &plan, plan_ws, plan_ws_bytes, NULL));
+    const size_t rows_bytes = sizeof(float) * (size_t)plan.max_seg * C;
+    void *rows = dev_alloc(rows_bytes);
+    float *out_tiled = dev_alloc(sizeof(float) * C * n_cells);
+    CHECK_BVP(bvp_tile_pool_f32(feat, dist, &plan, 1, C, BVP_SUM, rows, rows_bytes, out_tiled,
+                                NULL));
     CHECK_CUDA(cudaDeviceSynchronize());
 
     /* fast vs exact, the reference's tolerance metric max|a-b| / max(1,|a|) */
@@ -164,7 +184,8 @@ int main(int argc, char **argv) {
         dump(out_dir, "interval_starts", starts, 4 * host_counts[1]) ||
         dump(out_dir, "interval_cells", icells, 4 * host_counts[1]) ||
         dump(out_dir, "out_exact", out_exact, map_bytes) ||
-        dump(out_dir, "out_fast", out_fast, map_bytes)) {
+        dump(out_dir, "out_fast", out_fast, map_bytes) ||
+        dump(out_dir, "out_tiled", out_tiled, map_bytes)) {
         fprintf(stderr, "writing %s failed\n", out_dir);
         return 1;
     }

@@ -60,6 +60,7 @@ def test_c_host_pipeline_matches_oracle(tmp_path):
     want = o.pool_interval(feats, dist, ranks, starts, icells, NX * NY, "sum")
     np.testing.assert_array_equal(load("out_exact", np.float32).reshape(want.shape), want)
     assert o.max_rel_dev(want, load("out_fast", np.float32).reshape(want.shape)) <= 1e-5
+    assert o.max_rel_dev(want, load("out_tiled", np.float32).reshape(want.shape)) <= 1e-5
 
 
 def build_interval_reduce(tmp_path):
