@@ -1056,13 +1056,15 @@ tile_backward_kernel(TileBwdArgs a) {
     const uint32_t dmask = (1u << g.d_bits) - 1u, hmask = (1u << g.hl_bits) - 1u;
     const uint32_t wmask = (1u << (30 - shift)) - 1u;
     const uint32_t total_w = h.w;
+    // the copy's 16-byte item of this thread (8 x C/4 <= 256 items: at most one)
+    const int f_c4 = C >> 2, f_k = threadIdx.x / max(f_c4, 1);
+    const int f_c = 4 * (threadIdx.x - f_k * f_c4);
     auto fetch = [&](int q, int buf) {  // group q's gradient rows -> gsm[buf]
         const int nk = min(kTileGroup, n_segs - q * kTileGroup);
         float *dst = gsm + buf * (kTileGroup * GS);
         if ((C & 3) == 0) {
-            const int c4 = C >> 2;
-            for (int i = threadIdx.x; i < kTileGroup * c4; i += kPoolThreads) {
-                const int k = i / c4, c = 4 * (i - k * c4);
+            if (f_k < kTileGroup) {
+                const int k = f_k, c = f_c;
                 if (k < nk) {
                     const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
@@ -1122,6 +1124,21 @@ tile_backward_kernel(TileBwdArgs a) {
             }
             ws[widx - G0.z] = sum;
         }
+        // this thread's (row, segment) of a group: its window slot; the
+        // group's A goes dense into s_a for the fragments
+        const int ar = threadIdx.x >> 3, ak = threadIdx.x & 7;
+        int a_slot = 0;
+        bool a_in = false;
+        auto load_a = [&](int q) {
+            const uint4 Gq = gt[q];
+            const unsigned long long m = Gq.x | (static_cast<unsigned long long>(Gq.y) << 32);
+            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
+            a_in = ak < nk && ar < id.th && ((m >> ar) & 1ull);
+            a_slot = (Gq.z - G0.z) + (a_in ? __popcll(m & ((1ull << ar) - 1ull)) * kTileGroup + ak : 0);
+            s_a[ar][ak] = a_in ? ws[a_slot] : 0.f;
+        };
+        __syncthreads();  // A of the window complete
+        load_a(q0);
         for (int q = q0; q < q1; ++q) {
             if (q + 1 < q1) {
                 fetch(q + 1, (q + 1 - q0) & 1);
@@ -1129,17 +1146,7 @@ tile_backward_kernel(TileBwdArgs a) {
             } else {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
             }
-            const uint4 Gq = gt[q];
-            const unsigned long long m = Gq.x | (static_cast<unsigned long long>(Gq.y) << 32);
-            float *wq = ws + (Gq.z - G0.z);
-            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
-            // this thread's (row, segment) of the group: its window slot
-            const int ar = threadIdx.x >> 3, ak = threadIdx.x & 7;
-            const bool a_in = ak < nk && ar < id.th && ((m >> ar) & 1ull);
-            const int a_slot = a_in ? __popcll(m & ((1ull << ar) - 1ull)) * kTileGroup + ak : 0;
-            __syncthreads();  // group q's rows (and, first time, A) visible; s_a free
-            s_a[ar][ak] = a_in ? wq[a_slot] : 0.f;
-            __syncthreads();
+            __syncthreads();  // group q's rows and s_a visible; s_dpart free
             const float *gq = gsm + ((q - q0) & 1) * (kTileGroup * GS);
             // Dot K-partial: this warp's k-steps
             {
@@ -1179,11 +1186,13 @@ tile_backward_kernel(TileBwdArgs a) {
                     }
                 }
             }
-            __syncthreads();  // partials complete; every warp done with A and this buffer
-            // Dot = the 4 K-partials in order, over the window's (k, h) slots
+            __syncthreads();  // partials complete; every warp done with s_a and this buffer
+            // Dot = the 4 K-partials in order, over the window's (k, h) slots;
+            // then the next group's A
             if (a_in)
-                wq[a_slot] = ((s_dpart[0][ar][ak] + s_dpart[1][ar][ak]) + s_dpart[2][ar][ak]) +
+                ws[a_slot] = ((s_dpart[0][ar][ak] + s_dpart[1][ar][ak]) + s_dpart[2][ar][ak]) +
                              s_dpart[3][ar][ak];
+            if (q + 1 < q1) load_a(q + 1);
         }
         __syncthreads();
         // every point of the window: its Dot into the depth-weight rows
