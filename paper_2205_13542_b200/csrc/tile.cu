@@ -671,24 +671,30 @@ tile_pool_kernel(TilePoolArgs a) {
     if (SRC == kTileBF16Fused) {
         __syncthreads();
         // depth softmax of the tile's pixels (lift.py:17-31 semantics, fp32
-        // from bf16 logits): one warp per pixel, lanes over depth bins
+        // from bf16 logits): 8 lanes per pixel, 4 pixels per warp at once
+        // (pixel rows PD apart fall in distinct banks), lanes over depth bins
         constexpr float kLog2e = 1.4426950408889634f;
-        for (int hl = warp; hl < id.th; hl += NW) {
-            float *row = pw + hl * PD;
+        const int sub = lane & 7;
+        for (int hl0 = 4 * warp; hl0 < id.th; hl0 += 4 * NW) {
+            const int hl = hl0 + (lane >> 3);
+            const bool on = hl < id.th;
+            float *row = pw + (on ? hl : 0) * PD;
             float m = -INFINITY;
-            for (int d = lane; d < D; d += 32) m = fmaxf(m, row[d]);
+            if (on)
+                for (int d = sub; d < D; d += 8) m = fmaxf(m, row[d]);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+            for (int o = 4; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
             const float ms = m * kLog2e;
             float sum = 0.f;
-            for (int d = lane; d < D; d += 32) {
-                const float e = exp2f(fmaf(row[d], kLog2e, -ms));
-                row[d] = e;
-                sum += e;
-            }
+            if (on)
+                for (int d = sub; d < D; d += 8) {
+                    const float e = exp2f(fmaf(row[d], kLog2e, -ms));
+                    row[d] = e;
+                    sum += e;
+                }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-            if (lane == 0) s_inv[hl] = 1.f / sum;
+            for (int o = 4; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            if (on && sub == 0) s_inv[hl] = 1.f / sum;
         }
     }
     if (gt_cached) asm volatile("cp.async.wait_all;" ::: "memory");
