@@ -726,7 +726,9 @@ tile_pool_kernel(TilePoolArgs a) {
         const uint32_t w_end = q1 == n_groups ? total_w : gt[q1].z;
         const uint32_t wlen = w_end - G0.z;
         __syncthreads();  // staging done; previous window consumed
-        for (uint32_t i = threadIdx.x; i < wlen; i += kPoolThreads) ws[i] = 0.f;
+        // (window offsets and lengths are multiples of 8 floats: 16-byte stores)
+        for (uint32_t i = 4 * threadIdx.x; i < wlen; i += 4 * kPoolThreads)
+            *reinterpret_cast<float4 *>(ws + i) = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
         // (2) aggregate: each run of one (cell, row) summed in depth order
         // (records below RPT * 256 come from the prefetch)
