@@ -663,6 +663,23 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
     rec("fused_bf16_api", ms, 2 * P + 2 * NHW * C + 4 * n_in + 8 * n_int + 4 * C * n_cells,
         path="bp.pool_fused (allocates its output every call)")
 
+    # the reference's own calling convention: numpy in, numpy out, through
+    # the drop-in pool_interval (pageable host arrays staged through pinned
+    # buffers, the map copied back) -- wall clock per call, mean of 10
+    import time
+    fe_np = feats[0].cpu().numpy()
+    di_np = dist[0].cpu().numpy()
+    for _ in range(3):
+        bp.pool_interval(fe_np, di_np, cache, grid)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(10):
+        bp.pool_interval(fe_np, di_np, cache, grid)
+    ms = 1e3 * (time.perf_counter() - t0) / 10
+    rec("e2e_numpy_pool_interval", ms, ref_bytes,
+        path="bp.pool_interval(numpy features, numpy dist) -> numpy map (the reference's "
+             "convention; wall clock, pageable host arrays)")
+
     # cold association (geometry + sort + tables), no host sync
     builder = bp.CacheBuilder(spec.n_cameras, f, grid, dev)
     cams = torch.from_numpy(bp.rig_rows(rig)).to(dev)
