@@ -289,14 +289,19 @@ __global__ void make_intervals_kernel(const uint32_t *__restrict__ cell_count,
                                       int64_t n_cells, uint32_t *__restrict__ starts,
                                       uint32_t *__restrict__ icells,
                                       uint32_t *__restrict__ cell_first,
-                                      int64_t *__restrict__ counts) {
+                                      int64_t *__restrict__ counts,
+                                      uint32_t *__restrict__ long_list = nullptr,
+                                      uint32_t *__restrict__ n_long = nullptr) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cells;
          c += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long ex = scanned[c];
         const uint32_t iv = static_cast<uint32_t>(ex >> 32);
-        if (cell_count[c] > 0) {
+        const uint32_t k = cell_count[c];
+        if (k > 0) {
             starts[iv] = static_cast<uint32_t>(ex & 0xFFFFFFFFull);
             icells[iv] = static_cast<uint32_t>(c);
+            // runs longer than 256 points: seg_sort_long_kernel's
+            if (long_list && k > 256u) long_list[atomicAdd(n_long, 1u)] = iv;
         }
         cell_first[c] = iv;
     }
@@ -587,17 +592,6 @@ __device__ __forceinline__ void warp_sort_any(uint32_t *r, int L, int lane) {
     else warp_sort_run<32>(r, L, lane);
 }
 
-// The intervals whose runs are longer than 256 points (seg_sort_long_kernel's).
-__global__ void pick_long_runs_kernel(const uint32_t *__restrict__ starts,
-                                      const int64_t *__restrict__ counts,
-                                      uint32_t *__restrict__ long_list,
-                                      uint32_t *__restrict__ n_long) {
-    const int64_t n_int = counts[1];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_int;
-         i += (int64_t)gridDim.x * blockDim.x)
-        if (__ldg(starts + i + 1) - __ldg(starts + i) > 256u)
-            long_list[atomicAdd(n_long, 1u)] = static_cast<uint32_t>(i);
-}
 
 // One warp per interval, runs of <= 256 points sorted in registers; longer
 // runs are seg_sort_long_kernel's (a separate kernel on a forked stream, so
@@ -758,14 +752,13 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
         device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
         make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
-                                                 icells, cell_first, counts);
+                                                 icells, cell_first, counts, long_list, n_long);
         SideFork tables(s, 1);
         const int rc_t = on_tables ? (*on_tables)(tables.side) : BVP_OK;
         if (cams)
             count_scatter_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, *fp, packed, ranks, iop);
         else
             count_scatter_flat_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, P, packed, ranks, iop);
-        pick_long_runs_kernel<<<cb, 256, 0, s>>>(starts, counts, long_list, n_long);
         {  // short runs and long runs side by side
             SideFork fork(s);
             // the point gather table comes with the sorted runs (cams: the
