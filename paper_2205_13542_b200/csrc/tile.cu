@@ -34,107 +34,9 @@
 //
 // Reference: pooling.py:206-221 (pool_interval), _kernels.py:22-63
 // (interval_reduce), bevgrid.py:142-158 (the association it consumes).
-#include <algorithm>
-
-#include <cooperative_groups.h>
-
-#include "common.cuh"
-#include "partition.cuh"
-#include "scan.cuh"
+#include "tile.cuh"
 
 namespace bvp {
-
-constexpr int kTileGroup = 8;         // segments (cells) per group
-constexpr int kTileMaxRows = 64;      // rows per tile (one u64 mask per group)
-constexpr int kTileRows = 32;         // rows per tile chosen (tile_rows_for)
-constexpr int kTileMaxPoints = 8192;  // points per tile (smem sort capacity)
-constexpr int kPlanThreads = 512;
-constexpr int kPoolThreads = 256;
-constexpr int kFinCells = 32;         // cells per finalize CTA
-constexpr int kGtCache = 32;          // group headers cached in shared memory
-
-struct TileGeom {
-    int N, H, W, D, TH, n_hb;
-    int64_t T, tpc, gcap;
-    int hl_bits, d_bits;
-};
-
-inline int bits_for(int64_t v) {  // bits to hold values in [0, v]
-    int b = 0;
-    while (b < 62 && (int64_t(1) << b) <= v) ++b;
-    return b;
-}
-
-// Rows per tile: at most kTileRows (measured at config H, 64 rows: 32-row
-// tiles take the step from 203 to 178 us -- four 45 KB CTAs per SM instead
-// of two 88 KB ones outweigh twice the segment rows; 16 or 24 rows are
-// slower), balanced over the fewest row blocks, and at most kTileMaxPoints
-// points per tile.
-inline int tile_rows_for(int H, int D) {
-    const int cap = std::min(kTileRows, std::max(1, kTileMaxPoints / std::max(D, 1)));
-    const int n_hb = (H + cap - 1) / cap;
-    return (H + n_hb - 1) / n_hb;
-}
-
-inline TileGeom tile_geom(int N, int H, int W, int D) {
-    TileGeom g{};
-    g.N = N; g.H = H; g.W = W; g.D = D;
-    g.TH = tile_rows_for(H, D);
-    g.n_hb = int((H + g.TH - 1) / g.TH);
-    g.T = int64_t(N) * g.n_hb * W;
-    g.tpc = int64_t(g.TH) * D;
-    g.gcap = (g.tpc + kTileGroup - 1) / kTileGroup + 1;  // + sentinel
-    g.hl_bits = bits_for(g.TH - 1);
-    g.d_bits = bits_for(D - 1);
-    return g;
-}
-
-// tile index t = (n * n_hb + hb) * W + w: neighbouring columns are
-// neighbouring tiles, so concurrently running CTAs share the 32-byte sectors
-// of the strided (N, C, H, W) / (N, D, H, W) inputs through L2.
-struct TileId {
-    int n, hb, w, h0, th;
-};
-__device__ __forceinline__ TileId tile_id(int64_t t64, int W, int n_hb, int TH, int H) {
-    TileId r;
-    const int t = int(t64);  // T < 2^31 (plan_supported)
-    r.w = t % W;
-    const int rest = t / W;
-    r.hb = rest % n_hb;
-    r.n = rest / n_hb;
-    r.h0 = r.hb * TH;
-    r.th = min(TH, H - r.h0);
-    return r;
-}
-
-// ---- block helpers ---------------------------------------------------------
-// Exclusive scan of one value per thread across the block (blockDim.x <= 1024).
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *s_warp,
-                                                    uint32_t *total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t y = lane < nw ? s_warp[lane] : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t z = __shfl_up_sync(0xFFFFFFFFu, y, o);
-            if (lane >= o) y += z;
-        }
-        if (lane < nw) s_warp[lane] = y;  // inclusive warp totals
-    }
-    __syncthreads();
-    const uint32_t pre = warp ? s_warp[warp - 1] : 0u;
-    if (total) *total = s_warp[nw - 1];
-    __syncthreads();
-    return pre + x - v;
-}
 
 // ---- plan build -------------------------------------------------------------
 // Tile of a frustum point id p = ((n H + h) W + w) D + d.
@@ -401,16 +303,6 @@ struct TilePoolArgs {
     TileGeom g;
     int C, wbudget;
 };
-// acc.x += w.x * f, acc.y += w.y * f in one FFMA2 (Blackwell packed fp32;
-// the scalar f is a broadcast operand, no move).
-__device__ __forceinline__ void ffma2(float2 &acc, float2 w, float f) {
-    unsigned long long a = *reinterpret_cast<unsigned long long *>(&acc);
-    const unsigned long long wv = *reinterpret_cast<const unsigned long long *>(&w);
-    unsigned long long fv;
-    asm("mov.b64 %0, {%1, %1};" : "=l"(fv) : "f"(f));
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a) : "l"(wv), "l"(fv));
-    acc = *reinterpret_cast<float2 *>(&a);
-}
 
 // One union row of a group: acc[m][j] += (w[2m], w[2m+1]) * F[hl][lane + 32 j].
 template <int CS, int FS>
@@ -454,133 +346,6 @@ __device__ __forceinline__ void group_row2(float2 (&acc)[kTileGroup / 2][CS], co
         ffma2(acc[1][j], make_float2(b0.z, b0.w), fb[j]);
         ffma2(acc[2][j], make_float2(b1.x, b1.y), fb[j]);
         ffma2(acc[3][j], make_float2(b1.z, b1.w), fb[j]);
-    }
-}
-
-// ---- cluster column staging ---------------------------------------------------
-// The CL tiles of a cluster are CL adjacent columns of one camera.  CTA
-// `rank` moves channel quads (and depth-bin quads) rank, rank + CL, ... for
-// all CL columns -- a warp's access covers CL neighbouring columns x 32/CL
-// rows, 32/CL lines instead of 32 -- each quad one 16-byte word in the
-// shared memory of the CTA owning its column (distributed shared memory).
-struct ColumnXfer {
-    int rank, j, r0;  // this CTA's rank; the lane's column (peer) and first row
-    int n_rb, th;     // row blocks of 32/CL rows; rows of the tile
-    int HW, W;
-};
-
-template <int CL>
-__device__ __forceinline__ ColumnXfer column_xfer(int rank, int th, int HW, int W) {
-    const int lane = threadIdx.x & 31;
-    constexpr int RS = 32 / CL;
-    return ColumnXfer{rank, lane % CL, lane / CL, (th + RS - 1) / RS, th, HW, W};
-}
-
-// item it = (quad qi, row block m); the U items of a round are NW apart, so
-// one division per round and carries after it
-template <int U>
-__device__ __forceinline__ void xfer_items(int i0, int n_rb, int (&qs)[U], int (&ms)[U]) {
-    constexpr int NW = kPoolThreads / 32;
-    int qi = i0 / n_rb, m = i0 - qi * n_rb;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        qs[u] = qi;
-        ms[u] = m;
-        m += NW;
-        while (m >= n_rb) {
-            m -= n_rb;
-            ++qi;
-        }
-    }
-}
-
-// Global -> (remote) shared: rows [0, th) x quads of src (planes HW apart,
-// column base `base` of the cluster's first column + j) into dst[hl][c]
-// (stride floats).  n_quads >= ceil(n_ch / 4): quads past n_ch are stored as
-// zeros.  ES: element bytes (4 fp32, 2 bf16 widened).  wait_first: the
-// cluster barrier's wait (every CTA running, so its shared memory may be
-// written) sits between the first round's loads and its stores.
-template <int CL, int ES>
-__device__ __forceinline__ void stage_quads(const ColumnXfer &x, const void *src, int n_ch,
-                                            int n_quads, int64_t base, float *dst, int stride,
-                                            bool wait_first) {
-    constexpr int NW = kPoolThreads / 32, RS = 32 / CL, U = 4;
-    const int warp = threadIdx.x >> 5;
-    // byte addresses: the tile's column once, then one 32-bit offset per item
-    // and one add per channel of the quad
-    const char *sb = static_cast<const char *>(src) + base * ES;
-    const uint32_t plane = uint32_t(x.HW) * ES, rowb = uint32_t(x.W) * ES;
-    const int n_q = (n_quads - x.rank + CL - 1) / CL;  // this CTA's quads
-    const int items = n_q * x.n_rb;
-    for (int i0 = warp; i0 < items || (wait_first && i0 == warp); i0 += NW * U) {
-        int qs[U], ms[U];
-        xfer_items<U>(i0, x.n_rb, qs, ms);
-        // all U x 4 loads issue before any value is used (raw bits; bf16
-        // widened at the store)
-        uint32_t v[U][4];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int it = i0 + NW * u;
-            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
-            const bool ok = it < items && hl < x.th;
-            const char *pi = sb + (uint64_t(uint32_t(c0)) * plane + uint32_t(hl) * rowb);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const bool on = ok && c0 + e < n_ch;
-                if (ES == 4)
-                    v[u][e] = ldg_l2pf_b32(pi + uint64_t(e) * plane, on);
-                else
-                    v[u][e] = ldg_l2pf_u16(pi + uint64_t(e) * plane, on) << 16;
-            }
-        }
-        if (CL > 1 && wait_first && i0 == warp)
-            asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int it = i0 + NW * u;
-            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
-            if (it < items && hl < x.th)
-                *reinterpret_cast<float4 *>(dst + hl * stride + c0) =
-                    make_float4(__uint_as_float(v[u][0]), __uint_as_float(v[u][1]),
-                                __uint_as_float(v[u][2]), __uint_as_float(v[u][3]));
-        }
-    }
-}
-
-// (Remote) shared -> global, the reverse of stage_quads: src[hl][c] of the
-// CTA owning column j into dst planes (fp32), channels < n_ch.
-template <int CL>
-__device__ __forceinline__ void unstage_quads(const ColumnXfer &x, float *dst, int n_ch,
-                                              int64_t base, const float *src, int stride) {
-    constexpr int NW = kPoolThreads / 32, RS = 32 / CL, U = 4;
-    const int warp = threadIdx.x >> 5;
-    float *db = dst + base;
-    const int n_q = (((n_ch + 3) >> 2) - x.rank + CL - 1) / CL;
-    const int items = n_q * x.n_rb;
-    for (int i0 = warp; i0 < items; i0 += NW * U) {
-        int qs[U], ms[U];
-        xfer_items<U>(i0, x.n_rb, qs, ms);
-        float4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int it = i0 + NW * u;
-            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
-            v[u] = it < items && hl < x.th
-                       ? *reinterpret_cast<const float4 *>(src + hl * stride + c0)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int it = i0 + NW * u;
-            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
-            if (it < items && hl < x.th) {
-                float *po = db + int64_t(c0) * x.HW + int64_t(hl) * x.W;
-                const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    if (c0 + e < n_ch) po[int64_t(e) * x.HW] = e4[e];
-            }
-        }
     }
 }
 
@@ -887,439 +652,11 @@ tile_finalize_kernel(const float *__restrict__ rows, int64_t max_seg,
     }
 }
 
-// ---- backward (config B): the adjoint of the tiled reduction ----------------
-// out[c, cell] = sum_p w_p f[pix(p), c] (SUM; MEAN scales by 1/len(cell)), so
-//   grad_f[pix = (n, h, w), c] = sum_{p of the pixel} w_p g[c, cell(p)]
-//                              = sum_k A[k, h] G[k, c]   per tile, over segments k
-//   grad_w[p]                  = <f[pix(p), :], g[:, cell(p)]> = Dot[k(p), h(p)]
-// with A the forward's aggregated weights and G[k, :] = g[:, cell_k] (x 1/len
-// for MEAN) -- the same column tiles, groups and weight windows as the
-// forward, so every gradient row is read once per (segment, tile) instead of
-// once per point.  No atomics: each gradient element is written once.
-
-// G rows per segment slot: rows[s, :] = g[:, cell(s)] (x 1/len for MEAN), one
-// CTA per 32 cells (coalesced channel lines in, a shared-memory transpose,
-// 4C-byte rows out); blocks without segments are skipped.
-template <int CS>
-__global__ void __launch_bounds__(kPoolThreads)
-tile_grad_rows_kernel(const float *__restrict__ grad_out, const uint32_t *__restrict__ cell_seg_first,
-                      const uint32_t *__restrict__ cell_npts, int n_cells, int C, int mean,
-                      int64_t max_seg, float *__restrict__ rows) {
-    constexpr int CP = CS * 32;
-    constexpr int NW = kPoolThreads / 32;
-    __shared__ float tile[CP][kFinCells + 1];
-    const int c0 = blockIdx.x * kFinCells, b = blockIdx.y;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nc = min(kFinCells, n_cells - c0);
-    const uint32_t f = __ldg(cell_seg_first + c0 + min(lane, nc));
-    const uint32_t f_end = __ldg(cell_seg_first + c0 + nc);
-    if (__shfl_sync(0xFFFFFFFFu, f, 0) == f_end) return;  // no segment in the block
-    const float *gb = grad_out + int64_t(b) * C * n_cells + c0;
-#pragma unroll
-    for (int k = 0; k < CP / NW; ++k) {
-        const int ch = warp + NW * k;
-        tile[ch][lane] = ch < C && lane < nc ? __ldg(gb + int64_t(ch) * n_cells + lane) : 0.f;
-    }
-    __syncthreads();
-    float *rb = rows + int64_t(b) * max_seg * C + lane;
-#pragma unroll
-    for (int u = 0; u < kFinCells / NW; ++u) {
-        const int cl = warp + NW * u;
-        const uint32_t s0 = __shfl_sync(0xFFFFFFFFu, f, cl);
-        uint32_t s1 = cl < 31 ? __shfl_sync(0xFFFFFFFFu, f, cl + 1) : f_end;
-        if (cl >= nc) s1 = s0;
-        if (s1 == s0) continue;
-        const float inv = mean ? 1.f / float(__ldg(cell_npts + c0 + cl)) : 1.f;
-        for (uint32_t sg = s0; sg < s1; ++sg)
-#pragma unroll
-            for (int j = 0; j < CS; ++j)
-                if (lane + 32 * j < C) rb[int64_t(sg) * C + 32 * j] = tile[lane + 32 * j][cl] * inv;
-    }
-}
-
-struct TileBwdArgs {
-    const float *grad_rows;  // (B, max_seg, C): tile_grad_rows_kernel's rows
-    const float *feats;      // (B, N, C, H, W)
-    const float *dist;       // (B, N, D, H, W)
-    const uint4 *hdr;
-    const uint32_t *rec;
-    const uint4 *groups;
-    const uint32_t *seg_row;
-    float *grad_feats;       // (B, N, C, H, W), or null
-    float *grad_dist;        // (B, N, D, H, W), or null
-    int64_t max_seg;
-    TileGeom g;
-    int C, wbudget;
-};
-
-// ---- tensor-core pieces of the backward (mma.sync m16n8k8, tf32 operands) ---
-// fp32 accuracy from tf32 operands: x = hi + lo, hi = tf32(x), lo the exact
-// fp32 remainder; a*b ~ hi*hi + hi*lo + lo*hi (the dropped lo*lo is 2^-22
-// relative).  Measured 278 TFLOP/s for tf32 mma.sync on this GPU
-// (scripts/mma_vs_ffma2.cu): the backward's two products per group -- the
-// (row, segment) dot products over C channels and grad_f's 8-segment sums --
-// are GEMM-shaped with K = C and N = C, where FFMA lanes-over-channels need a
-// cross-lane reduction per dot product.
-__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
-    lo = __float_as_uint(x - __uint_as_float(hi));
-}
-// d += a * b three ways (lo*hi, hi*lo, hi*hi: small terms first)
-__device__ __forceinline__ void mma3_tf32(float (&d)[4], const uint32_t (&ah)[4],
-                                          const uint32_t (&al)[4], uint32_t bh0, uint32_t bh1,
-                                          uint32_t bl0, uint32_t bl1) {
-#define BVP_MMA_TF32(A, B0, B1)                                                        \
-    asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0, %1, %2, %3}, "       \
-        "{%4, %5, %6, %7}, {%8, %9}, {%0, %1, %2, %3};"                                \
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])                               \
-        : "r"(A[0]), "r"(A[1]), "r"(A[2]), "r"(A[3]), "r"(B0), "r"(B1))
-    BVP_MMA_TF32(al, bh0, bh1);
-    BVP_MMA_TF32(ah, bl0, bl1);
-    BVP_MMA_TF32(ah, bh0, bh1);
-#undef BVP_MMA_TF32
-}
-
-// One CTA per (tile, sample), clusters of CL columns as in the forward.  Per
-// group (every warp every group; the group's 8 gradient rows copied to
-// shared memory, double buffered):
-//   Dot[h, k] = sum_c F[h, c] G[k, c]   -- M = 32 rows, N = 8 segments, K = C:
-//     warp w takes m-tile w & 1 and k-steps w >> 1 (+4, +8) with its F
-//     fragments held in registers; the 4 K-partials are added in a fixed
-//     order through shared memory and written over the weight window's
-//     (k, h) slots (A is read before);
-//   grad_f[h, c] += sum_k A[k, h] G[k, c] -- M = 32 rows, N = C, K = 8:
-//     warp w accumulates m-tile w & 1 x n-tiles w >> 1 (+4, +8) in registers
-//     over all groups, in order.
-// Then every point's record picks its Dot from the window into the
-// depth-weight rows (weights no longer needed), points without a record
-// are zeroed, grad_f goes over the feature rows, and both tiles go back to
-// global memory through the cluster.  Deterministic (fixed sums, no atomics
-// on values); tiles of <= 32 rows, C <= 128.
-template <int CS, int CL>
-__global__ void __launch_bounds__(kPoolThreads, 4)
-tile_backward_kernel(TileBwdArgs a) {
-    constexpr int CP = CS * 32;
-    constexpr int FS = CP + 4;   // = 4 (mod 32): conflict-free fragment loads
-    constexpr int GS = CP + 4;
-    constexpr int NKS = (CP + 7) / 8;
-    extern __shared__ __align__(16) float sm[];
-    __shared__ uint32_t s_cov[kTileMaxPoints / 32];  // points with a record
-    __shared__ float s_dpart[4][32][kTileGroup];      // Dot K-partials of a group
-    __shared__ float s_a[32][kTileGroup + 1];          // the group's A, dense [row][segment]
-    const TileGeom &g = a.g;
-    const int64_t t = blockIdx.x;
-    const int b = blockIdx.y;
-    const TileId id = tile_id(t, g.W, g.n_hb, g.TH, g.H);
-    const uint4 h = a.hdr[t];
-    const int n_segs = int(h.y), n_groups = int(h.z);
-    const int HW = g.H * g.W, C = a.C, D = g.D, PD = (D + 3) & ~3;
-    float *ws = sm;               // weight window [wbudget]: A, then the dot products
-    float *fs = ws + a.wbudget;   // [TH][FS] feature rows, then grad_f rows
-    float *pw = fs + g.TH * FS;   // [TH][PD] depth weights, then grad_w rows
-    float *gsm = pw + g.TH * PD;  // [2][8][GS] gradient rows of the current / next group
-    const int64_t nb = int64_t(b) * g.N + id.n;
-    const int64_t pix0 = int64_t(id.h0) * g.W + id.w;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g8 = lane >> 2, t4 = lane & 3;
-    const int mt = warp & 1, wq4 = warp >> 1;  // m-tile; k-step / n-tile quarter
-    const int NT = (C + 7) >> 3;               // n-tiles (and k-steps) over C
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    const int rank = CL > 1 ? int(cluster.block_rank()) : 0;
-    const ColumnXfer x = column_xfer<CL>(rank, id.th, HW, g.W);
-    const int64_t col = pix0 - rank + x.j;
-    if (CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    for (int i = threadIdx.x; i < kTileMaxPoints / 32; i += kPoolThreads) s_cov[i] = 0u;
-    // gradient-row buffers: channels past C stay zero (the copies stop at C)
-    for (int i = threadIdx.x; i < 2 * kTileGroup * GS; i += kPoolThreads) gsm[i] = 0.f;
-    {
-        float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
-        float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
-        stage_quads<CL, 4>(x, a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
-        stage_quads<CL, 4>(x, a.dist, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
-        if (CL > 1) cluster.sync();
-        else __syncthreads();
-    }
-    // this warp's F fragments (A operand of Dot): rows mt*16 + g (+8),
-    // channels 8 ks + t (+4), k-steps ks = wq4, wq4 + 4, wq4 + 8
-    uint32_t fh[3][4], fl[3][4];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const int ks = wq4 + 4 * i;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int r = mt * 16 + g8 + 8 * (e & 1), c = 8 * ks + t4 + 4 * (e >> 1);
-            const float v = ks < NT && r < id.th ? fs[r * FS + c] : 0.f;
-            split_tf32(v, fh[i][e], fl[i][e]);
-        }
-    }
-    float gacc[3][4];  // grad_f: m-tile mt x n-tiles wq4 (+4, +8)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) gacc[i][0] = gacc[i][1] = gacc[i][2] = gacc[i][3] = 0.f;
-    const uint4 *gt = a.groups + t * g.gcap;
-    const uint32_t *srow = a.seg_row + t * g.tpc;
-    const uint32_t *rt = a.rec + t * g.tpc;
-    const float *grows0 = a.grad_rows + int64_t(b) * a.max_seg * C;
-    const int shift = g.hl_bits + g.d_bits;
-    const uint32_t dmask = (1u << g.d_bits) - 1u, hmask = (1u << g.hl_bits) - 1u;
-    const uint32_t wmask = (1u << (30 - shift)) - 1u;
-    const uint32_t total_w = h.w;
-    // the copy's 16-byte item of this thread (8 x C/4 <= 256 items: at most one)
-    const int f_c4 = C >> 2, f_k = threadIdx.x / max(f_c4, 1);
-    const int f_c = 4 * (threadIdx.x - f_k * f_c4);
-    auto fetch = [&](int q, int buf) {  // group q's gradient rows -> gsm[buf]
-        const int nk = min(kTileGroup, n_segs - q * kTileGroup);
-        float *dst = gsm + buf * (kTileGroup * GS);
-        if ((C & 3) == 0) {
-            if (f_k < kTileGroup) {
-                const int k = f_k, c = f_c;
-                if (k < nk) {
-                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * GS + c))),
-                                 "l"(src));
-                } else {  // rows past the group's cells: zero (their A is 0)
-                    *reinterpret_cast<float4 *>(dst + k * GS + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
-        } else {
-            for (int i = threadIdx.x; i < kTileGroup * C; i += kPoolThreads) {
-                const int k = i / C, c = i - k * C;
-                if (k < nk) {
-                    const float *src = grows0 + int64_t(srow[q * kTileGroup + k]) * C + c;
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + k * GS + c))),
-                                 "l"(src));
-                } else {
-                    dst[k * GS + c] = 0.f;
-                }
-            }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    for (int q0 = 0; q0 < n_groups;) {
-        // weight windows as in the forward (one for nearly every tile)
-        const uint4 G0 = q0 ? gt[q0] : make_uint4(0u, 0u, 0u, 0u);
-        int q1 = n_groups;
-        if (total_w - G0.z > uint32_t(a.wbudget)) {
-            int lo = q0 + 1, hi = n_groups - 1;
-            q1 = q0 + 1;
-            while (lo <= hi) {
-                const int mid = (lo + hi) >> 1;
-                if (gt[mid].z - G0.z <= uint32_t(a.wbudget)) {
-                    q1 = mid;
-                    lo = mid + 1;
-                } else {
-                    hi = mid - 1;
-                }
-            }
-        }
-        const uint32_t r_end = q1 == n_groups ? h.x : gt[q1].w;
-        const uint32_t w_end = q1 == n_groups ? total_w : gt[q1].z;
-        __syncthreads();  // previous window's records done with ws / pw
-        for (uint32_t i = threadIdx.x; i < w_end - G0.z; i += kPoolThreads) ws[i] = 0.f;
-        fetch(q0, 0);
-        __syncthreads();
-        // aggregation: A of the window (the forward's arithmetic)
-        for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
-            uint32_t r = __ldg(rt + k);
-            if (!(r >> 31)) continue;
-            const uint32_t widx = (r >> shift) & wmask;
-            float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
-            for (uint32_t kk = k + 1; (r >> 30) & 1u; ++kk) {
-                r = __ldg(rt + kk);
-                sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
-            }
-            ws[widx - G0.z] = sum;
-        }
-        // this thread's (row, segment) of a group: its window slot; the
-        // group's A goes dense into s_a for the fragments
-        const int ar = threadIdx.x >> 3, ak = threadIdx.x & 7;
-        int a_slot = 0;
-        bool a_in = false;
-        auto load_a = [&](int q) {
-            const uint4 Gq = gt[q];
-            const unsigned long long m = Gq.x | (static_cast<unsigned long long>(Gq.y) << 32);
-            const int nk = min(kTileGroup, n_segs - q * kTileGroup);
-            a_in = ak < nk && ar < id.th && ((m >> ar) & 1ull);
-            a_slot = (Gq.z - G0.z) + (a_in ? __popcll(m & ((1ull << ar) - 1ull)) * kTileGroup + ak : 0);
-            s_a[ar][ak] = a_in ? ws[a_slot] : 0.f;
-        };
-        __syncthreads();  // A of the window complete
-        load_a(q0);
-        for (int q = q0; q < q1; ++q) {
-            if (q + 1 < q1) {
-                fetch(q + 1, (q + 1 - q0) & 1);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");
-            } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            }
-            __syncthreads();  // group q's rows and s_a visible; s_dpart free
-            const float *gq = gsm + ((q - q0) & 1) * (kTileGroup * GS);
-            // Dot K-partial: this warp's k-steps
-            {
-                float dacc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const int ks = wq4 + 4 * i;
-                    if (ks < NT) {  // B = G^T: b0 = G[g][8 ks + t], b1 = G[g][8 ks + t + 4]
-                        uint32_t bh0, bl0, bh1, bl1;
-                        split_tf32(gq[g8 * GS + 8 * ks + t4], bh0, bl0);
-                        split_tf32(gq[g8 * GS + 8 * ks + t4 + 4], bh1, bl1);
-                        mma3_tf32(dacc, fh[i], fl[i], bh0, bh1, bl0, bl1);
-                    }
-                }
-                // rows mt*16 + g (+8), segments 2t, 2t+1
-                s_dpart[wq4][mt * 16 + g8][2 * t4] = dacc[0];
-                s_dpart[wq4][mt * 16 + g8][2 * t4 + 1] = dacc[1];
-                s_dpart[wq4][mt * 16 + g8 + 8][2 * t4] = dacc[2];
-                s_dpart[wq4][mt * 16 + g8 + 8][2 * t4 + 1] = dacc[3];
-            }
-            // grad_f: A^T (rows x segments) . G (segments x channels)
-            {
-                const int r0 = mt * 16 + g8;
-                const float a4[4] = {s_a[r0][t4], s_a[r0 + 8][t4], s_a[r0][t4 + 4],
-                                     s_a[r0 + 8][t4 + 4]};
-                uint32_t ah[4], al[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) split_tf32(a4[e], ah[e], al[e]);
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    const int nt = wq4 + 4 * i;
-                    if (nt < NT) {  // b0 = G[t][8 nt + g], b1 = G[t + 4][8 nt + g]
-                        uint32_t bh0, bl0, bh1, bl1;
-                        split_tf32(gq[t4 * GS + 8 * nt + g8], bh0, bl0);
-                        split_tf32(gq[(t4 + 4) * GS + 8 * nt + g8], bh1, bl1);
-                        mma3_tf32(gacc[i], ah, al, bh0, bh1, bl0, bl1);
-                    }
-                }
-            }
-            __syncthreads();  // partials complete; every warp done with s_a and this buffer
-            // Dot = the 4 K-partials in order, over the window's (k, h) slots;
-            // then the next group's A
-            if (a_in)
-                ws[a_slot] = ((s_dpart[0][ar][ak] + s_dpart[1][ar][ak]) + s_dpart[2][ar][ak]) +
-                             s_dpart[3][ar][ak];
-            if (q + 1 < q1) load_a(q + 1);
-        }
-        __syncthreads();
-        // every point of the window: its Dot into the depth-weight rows
-        for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
-            const uint32_t r = __ldg(rt + k);
-            const uint32_t hl = (r >> g.d_bits) & hmask, d = r & dmask;
-            pw[hl * PD + d] = ws[((r >> shift) & wmask) - G0.z];
-            const uint32_t pt = hl * uint32_t(D) + d;
-            atomicOr(&s_cov[pt >> 5], 1u << (pt & 31));
-        }
-        q0 = q1;
-    }
-    __syncthreads();
-    // points without a record (out of range) get a zero weight gradient; the
-    // grad_f fragments go over the feature rows
-    for (int hl = warp; hl < id.th; hl += kPoolThreads / 32)
-        for (int d = lane; d < D; d += 32) {
-            const int pt = hl * D + d;
-            if (!((s_cov[pt >> 5] >> (pt & 31)) & 1u)) pw[hl * PD + d] = 0.f;
-        }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const int nt = wq4 + 4 * i;
-        if (nt >= NT) continue;
-        const int r0 = mt * 16 + g8, c0 = 8 * nt + 2 * t4;
-        if (r0 < id.th) {
-            fs[r0 * FS + c0] = gacc[i][0];
-            fs[r0 * FS + c0 + 1] = gacc[i][1];
-        }
-        if (r0 + 8 < id.th) {
-            fs[(r0 + 8) * FS + c0] = gacc[i][2];
-            fs[(r0 + 8) * FS + c0 + 1] = gacc[i][3];
-        }
-    }
-    if (CL > 1) cluster.sync();
-    else __syncthreads();
-    {
-        const float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
-        const float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
-        if (a.grad_feats) unstage_quads<CL>(x, a.grad_feats, C, nb * C * HW + col, rfs, FS);
-        if (a.grad_dist) unstage_quads<CL>(x, a.grad_dist, D, nb * D * HW + col, rpw, PD);
-    }
-    if (CL > 1) cluster.sync();  // peers done reading this CTA's shared memory
-}
-
-// ---- plan layout -------------------------------------------------------------
-static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
-
-struct PlanLayout {
-    size_t hdr, rec, seg_cell, seg_start, seg_row, groups, csf, npts, nseg, bytes;
-};
-static PlanLayout plan_layout(const TileGeom &g, int64_t n_cells) {
-    PlanLayout L{};
-    size_t o = 0;
-    const size_t pts = size_t(g.T) * g.tpc;
-    L.hdr = o; o = a256(o + 16 * size_t(g.T));
-    L.rec = o; o = a256(o + 4 * pts);
-    L.seg_cell = o; o = a256(o + 4 * pts);
-    L.seg_start = o; o = a256(o + 4 * pts);
-    L.seg_row = o; o = a256(o + 4 * pts);
-    L.groups = o; o = a256(o + 16 * size_t(g.T) * g.gcap);
-    L.csf = o; o = a256(o + 4 * size_t(n_cells + 1));
-    L.npts = o; o = a256(o + 4 * size_t(n_cells));
-    L.nseg = o; o = a256(o + 8);
-    L.bytes = o;
-    return L;
-}
-
-struct PlanWs {
-    size_t fill, owner, part, total, err;
-    // the by-tile partition of the association's ranks (bvp_build_tile_plan_ranks)
-    size_t tkeys, tpts, tstart, tpart, ttotal, tsort, tsort_bytes, bytes;
-};
-static PlanWs plan_ws(const TileGeom &g, int64_t n_cells) {
-    PlanWs L{};
-    const int64_t P = int64_t(g.N) * g.H * g.W * g.D;
-    size_t o = 0;
-    L.fill = o; o = a256(o + 4 * size_t(n_cells + 1));
-    L.owner = o; o = a256(o + 8 * size_t(g.T) * g.tpc);
-    L.part = o; o = a256(o + 4 * size_t(scan_partials_len<uint32_t>(n_cells + 1)));
-    L.total = o; o = a256(o + 8);
-    L.err = o; o = a256(o + 8);
-    L.tkeys = o; o = a256(o + 4 * size_t(P));
-    L.tpts = o; o = a256(o + 4 * size_t(P));
-    L.tstart = o; o = a256(o + 4 * size_t(g.T + 1));
-    L.tpart = o; o = a256(o + 4 * size_t(scan_partials_len<uint32_t>(g.T + 1)));
-    L.ttotal = o; o = a256(o + 8);
-    L.tsort_bytes = stable_partition_ws_bytes(P, bits_for(g.T - 1));
-    L.tsort = o; o = a256(o + L.tsort_bytes);
-    L.bytes = o;
-    return L;
-}
-
 __global__ void tile_plan_count_kernel(const uint32_t *__restrict__ total, int64_t n_cells,
                                        uint32_t *__restrict__ csf, int64_t *__restrict__ nseg,
                                        const int *__restrict__ err) {
     csf[n_cells] = *total;
     nseg[0] = *err ? -1 : int64_t(*total);
-}
-
-static bool plan_supported(int N, int H, int W, int D, int64_t n_cells) {
-    if (N < 1 || H < 1 || W < 1 || D < 1 || D > kTileMaxPoints) return false;
-    if (n_cells < 1 || n_cells >= (int64_t(1) << 31) - 32) return false;
-    const TileGeom g = tile_geom(N, H, W, D);
-    return g.T < (int64_t(1) << 31) && g.tpc <= kTileMaxPoints &&
-           g.hl_bits + g.d_bits <= 16;
-}
-
-static int plan_dims_from(const bvp_tile_plan *p, TileGeom &g) {
-    BVP_REQUIRE(p && p->base, BVP_ERR_INVALID, "null tile plan");
-    BVP_REQUIRE(plan_supported(p->N, p->H, p->W, p->D, p->n_cells), BVP_ERR_UNSUPPORTED,
-                "frustum %dx%dx%dx%d not supported by the tile plan", p->N, p->H, p->W, p->D);
-    g = tile_geom(p->N, p->H, p->W, p->D);
-    return BVP_OK;
-}
-
-template <typename T>
-static T *at(const bvp_tile_plan *p, size_t off) {
-    return reinterpret_cast<T *>(static_cast<char *>(p->base) + off);
 }
 
 template <int CS, int SRC, int CL>
@@ -1405,73 +742,6 @@ static int run_tile_pool(const void *feats, const void *weights, const bvp_tile_
                     cudaGetErrorString(e));
     }
     return check_launch("tile_pool");
-}
-
-template <int CS, int CL>
-static int launch_backward(const TileBwdArgs &a, int B, size_t smem, cudaStream_t s) {
-    static int max_dyn = -1;
-    if (max_dyn < 0) {
-        cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, tile_backward_kernel<CS, CL>);
-        max_dyn = 227 * 1024 - int(fa.sharedSizeBytes);
-        cudaFuncSetAttribute(tile_backward_kernel<CS, CL>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-    }
-    BVP_REQUIRE(smem <= size_t(max_dyn), BVP_ERR_UNSUPPORTED,
-                "tile backward needs %zu bytes of shared memory (max %d)", smem, max_dyn);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(a.g.T), unsigned(B));
-    cfg.blockDim = dim3(kPoolThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr_c[1];
-    attr_c[0].id = cudaLaunchAttributeClusterDimension;
-    attr_c[0].val.clusterDim.x = CL;
-    attr_c[0].val.clusterDim.y = 1;
-    attr_c[0].val.clusterDim.z = 1;
-    cfg.attrs = attr_c;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, tile_backward_kernel<CS, CL>, a);
-    BVP_REQUIRE(e == cudaSuccess, BVP_ERR_CUDA, "tile_backward launch: %s", cudaGetErrorString(e));
-    return BVP_OK;
-}
-
-template <int CS>
-static int run_tile_backward(const float *grad_out, const float *feats, const float *dist,
-                             const bvp_tile_plan *p, const TileGeom &g, int B, int C, int mean,
-                             float *rows, float *grad_feats, float *grad_dist, cudaStream_t s) {
-    const PlanLayout L = plan_layout(g, p->n_cells);
-    tile_grad_rows_kernel<CS><<<dim3(unsigned(ceil_div(p->n_cells, kFinCells)), unsigned(B)),
-                                kPoolThreads, 0, s>>>(
-        grad_out, at<const uint32_t>(p, L.csf), at<const uint32_t>(p, L.npts), int(p->n_cells), C,
-        mean, p->max_seg, rows);
-    TileBwdArgs a{};
-    a.grad_rows = rows;
-    a.feats = feats;
-    a.dist = dist;
-    a.hdr = at<const uint4>(p, L.hdr);
-    a.rec = at<const uint32_t>(p, L.rec);
-    a.groups = at<const uint4>(p, L.groups);
-    a.seg_row = at<const uint32_t>(p, L.seg_row);
-    a.grad_feats = grad_feats;
-    a.grad_dist = grad_dist;
-    a.max_seg = p->max_seg;
-    a.g = g;
-    a.C = C;
-    a.wbudget = std::max(2048, 128 * g.TH);
-    const int CP = CS * 32;
-    const size_t smem = sizeof(float) * (size_t(g.TH) * (CP + 4) + size_t(g.TH) * ((g.D + 3) & ~3) +
-                                         a.wbudget + 2 * kTileGroup * (CP + 4));
-    const int CL = (g.W % 8 == 0) ? 8 : (g.W % 4 == 0) ? 4 : (g.W % 2 == 0) ? 2 : 1;
-    int rc;
-    switch (CL) {
-        case 8: rc = launch_backward<CS, 8>(a, B, smem, s); break;
-        case 4: rc = launch_backward<CS, 4>(a, B, smem, s); break;
-        case 2: rc = launch_backward<CS, 2>(a, B, smem, s); break;
-        default: rc = launch_backward<CS, 1>(a, B, smem, s); break;
-    }
-    if (rc != BVP_OK) return rc;
-    return check_launch("tile_backward");
 }
 
 template <int SRC>
@@ -1645,36 +915,6 @@ int bvp_tile_pool_f32(const float *features, const float *dist, const bvp_tile_p
                                         as_stream(stream));
 }
 
-int bvp_tile_backward_f32(const float *grad_out, const float *features, const float *dist,
-                          const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
-                          size_t rows_bytes, float *grad_features, float *grad_dist,
-                          void *stream) {
-    TileGeom g;
-    const int rc = plan_dims_from(plan, g);
-    if (rc != BVP_OK) return rc;
-    BVP_REQUIRE(B >= 1 && C >= 0, BVP_ERR_INVALID, "bad dims B=%d C=%d", B, C);
-    BVP_REQUIRE(mode == BVP_SUM || mode == BVP_MEAN, BVP_ERR_UNSUPPORTED,
-                "the tiled backward takes SUM and MEAN only (mode %d)", mode);
-    BVP_REQUIRE(C <= 128, BVP_ERR_UNSUPPORTED, "the tiled backward takes C <= 128 (C=%d)", C);
-    BVP_REQUIRE(g.TH <= 32, BVP_ERR_UNSUPPORTED, "the tiled backward takes tiles of <= 32 rows");
-    if (C == 0 || (!grad_features && !grad_dist)) return BVP_OK;
-    BVP_REQUIRE(grad_out && features && dist && rows, BVP_ERR_INVALID, "null pointer argument");
-    BVP_REQUIRE(rows_bytes >= size_t(B) * plan->max_seg * C * sizeof(float), BVP_ERR_INVALID,
-                "segment-row scratch too small: need %zu bytes, got %zu",
-                size_t(B) * plan->max_seg * C * sizeof(float), rows_bytes);
-    cudaStream_t s = as_stream(stream);
-    const int mean = mode == BVP_MEAN;
-    switch ((C + 31) / 32) {
-        case 1: return run_tile_backward<1>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                            grad_features, grad_dist, s);
-        case 2: return run_tile_backward<2>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                            grad_features, grad_dist, s);
-        case 3: return run_tile_backward<3>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                            grad_features, grad_dist, s);
-        default: return run_tile_backward<4>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                             grad_features, grad_dist, s);
-    }
-}
 
 int bvp_tile_pool_fused_bf16(const uint16_t *logits, const uint16_t *context,
                              const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
