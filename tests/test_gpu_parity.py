@@ -845,3 +845,12 @@ def test_tiled_backward_random_wide_instances(seed, red):
                     bp._lib.BVP_MEAN if red == "mean" else bp._lib.BVP_SUM, tf, tw)
     assert max_rel_dev(gf, tf.cpu().numpy()) <= FP32_TOL
     assert max_rel_dev(gw, tw.cpu().numpy()) <= FP32_TOL
+    # either gradient alone: the same bits (deterministic, independent parts)
+    tw2 = torch.full_like(d, float("nan"))
+    tp.backward_f32(torch.from_numpy(g).to(dev), f.detach(), d.detach(), 1, C,
+                    bp._lib.BVP_MEAN if red == "mean" else bp._lib.BVP_SUM, None, tw2)
+    assert torch.equal(tw, tw2)
+    tf2 = torch.full_like(f, float("nan"))
+    tp.backward_f32(torch.from_numpy(g).to(dev), f.detach(), d.detach(), 1, C,
+                    bp._lib.BVP_MEAN if red == "mean" else bp._lib.BVP_SUM, tf2, None)
+    assert torch.equal(tf, tf2)
