@@ -29,8 +29,11 @@
 // element exactly once, empty cells as zeros (pooling.py:213).  No atomics
 // touch values: the result is deterministic and independent of launch shape.
 //
-// The plan (tile_plan_kernel and friends) is built once per association
-// from cell_of_point alone (bevgrid.py:85-98's output), on the GPU.
+// The plan (tile_plan_kernel and friends) is built once per association on
+// the GPU: from the association's ranks by a stable partition by tile
+// (bvp_build_tile_plan_ranks), or from cell_of_point alone (bevgrid.py:85-98's
+// output) by a per-tile sort (bvp_build_tile_plan); the two plans are equal.
+// The adjoint is tile_backward.cu; shared pieces are in tile.cuh.
 //
 // Reference: pooling.py:206-221 (pool_interval), _kernels.py:22-63
 // (interval_reduce), bevgrid.py:142-158 (the association it consumes).
