@@ -274,14 +274,11 @@ radix_scatter_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
 
 // packed[c] = (count > 0) << 32 | count: one scan yields both the first
 // rank of every cell (low word) and its interval index (high word).
-__global__ void pack_counts_kernel(const uint32_t *__restrict__ cell_count, int64_t n_cells,
-                                   unsigned long long *__restrict__ packed) {
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_cells;
-         c += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t k = cell_count[c];
-        packed[c] = (static_cast<unsigned long long>(k > 0) << 32) | k;
+struct PackCount {  // applied as the scan loads each cell's count
+    __device__ __forceinline__ unsigned long long operator()(uint32_t k) const {
+        return (static_cast<unsigned long long>(k > 0) << 32) | k;
     }
-}
+};
 
 __global__ void make_intervals_kernel(const uint32_t *__restrict__ cell_count,
                                       const unsigned long long *__restrict__ scanned,
@@ -749,8 +746,8 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
             count_front_kernel<<<148 * 8, 256, 0, s>>>(cams, *fp, *gp, cells, cell_count, slot);
         else
             count_cells_kernel<<<148 * 8, 256, 0, s>>>(cells, P, cell_count, slot);
-        pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
-        device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
+        device_excl_scan_xf<unsigned long long>(cell_count, packed, n_cells, part64, total64,
+                                                PackCount{}, s);
         make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
                                                  icells, cell_first, counts, long_list, n_long);
         SideFork tables(s, 1);
@@ -784,8 +781,8 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
             nullptr, FrustumParams{}, GridParams{}, P, cells, cell_count, L.digit_bits, hist,
             L.n_tiles);
     // interval tables from the per-cell counts (independent of the sort)
-    pack_counts_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, packed);
-    device_excl_scan<unsigned long long>(packed, packed, n_cells, part64, total64, s);
+    device_excl_scan_xf<unsigned long long>(cell_count, packed, n_cells, part64, total64,
+                                            PackCount{}, s);
     make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
                                              icells, cell_first, counts);
     if (iop) {

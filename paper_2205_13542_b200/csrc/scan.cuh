@@ -164,9 +164,14 @@ __device__ __forceinline__ uint4 ld_cg<uint4>(const uint4 *p) { return __ldcg(p)
 
 // part: [agg: nb][incl: nb] T, then [flags: nb][ticket] uint32 (zeroed by the caller)
 template <typename T>
+struct ScanIdentity {
+    __device__ __forceinline__ T operator()(T v) const { return v; }
+};
+
+template <typename T, typename In = T, typename Xf = ScanIdentity<T>>
 __global__ void __launch_bounds__(kScanThreads)
-scan_onepass_kernel(const T *__restrict__ in, int64_t n, T *out, T *part, int64_t nb,
-                    T *__restrict__ total) {
+scan_onepass_kernel(const In *__restrict__ in, int64_t n, T *out, T *part, int64_t nb,
+                    T *__restrict__ total, Xf xf = Xf{}) {
     __shared__ T ws[kScanWarps];
     __shared__ T s_excl;
     __shared__ uint32_t s_tile;
@@ -183,7 +188,7 @@ scan_onepass_kernel(const T *__restrict__ in, int64_t n, T *out, T *part, int64_
 #pragma unroll
     for (int k = 0; k < R; ++k) {
         const int64_t e = base + k * 32 + lane;
-        const T v = e < n ? in[e] : T{};
+        const T v = e < n ? xf(in[e]) : T{};
         const T x = warp_incl_scan(v, lane);
         T wex = shfl_up_t(x, 1);
         if (lane == 0) wex = T{};
@@ -259,6 +264,21 @@ static int64_t scan_partials_len(int64_t n) {
     const int64_t nb = ceil_div(n, kScanChunk);
     // three-pass: nb + 1 partials; single pass: 2 nb values + nb + 1 flags
     return 2 * nb + ceil_div((nb + 1) * int64_t(sizeof(uint32_t)), int64_t(sizeof(T))) + 1;
+}
+
+// Exclusive scan of xf(in[i]) (integer T, one pass): out[i] = sum_{j<i} xf(in[j]).
+template <typename T, typename In, typename Xf>
+static void device_excl_scan_xf(const In *in, T *out, int64_t n, T *partials, T *total, Xf xf,
+                                cudaStream_t s) {
+    static_assert(is_exact_scan<T>::value, "the transformed scan is the one-pass form");
+    const int64_t nb = ceil_div(n, kScanChunk);
+    if (nb == 0) {
+        cudaMemsetAsync(total, 0, sizeof(T), s);
+        return;
+    }
+    cudaMemsetAsync(partials + 2 * nb, 0, size_t(nb + 1) * sizeof(uint32_t), s);
+    scan_onepass_kernel<T, In, Xf><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, out, partials, nb,
+                                                                        total, xf);
 }
 
 // Exclusive scan of n elements (in may equal out).  partials must hold
