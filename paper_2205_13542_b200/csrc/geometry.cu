@@ -742,20 +742,35 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         auto *long_list = reinterpret_cast<uint32_t *>(w + L.off_long);
         auto *n_long = reinterpret_cast<uint32_t *>(w + L.off_nlong);
         cudaMemsetAsync(n_long, 0, 8, s);
+        size_t flag_bytes = 0;
+        void *flags = scan_flags(part64, n_cells, &flag_bytes);
+        cudaMemsetAsync(flags, 0, flag_bytes, s);  // the scan's flags, before the front end
         if (cams)
             count_front_kernel<<<148 * 8, 256, 0, s>>>(cams, *fp, *gp, cells, cell_count, slot);
         else
             count_cells_kernel<<<148 * 8, 256, 0, s>>>(cells, P, cell_count, slot);
         device_excl_scan_xf<unsigned long long>(cell_count, packed, n_cells, part64, total64,
-                                                PackCount{}, s);
-        make_intervals_kernel<<<cb, 256, 0, s>>>(cell_count, packed, total64, n_cells, starts,
-                                                 icells, cell_first, counts, long_list, n_long);
+                                                PackCount{}, s, true);
+        // the interval tables (and what hangs on them) on a side stream, beside
+        // the rank scatter; the run sorts need both
         SideFork tables(s, 1);
+        make_intervals_kernel<<<cb, 256, 0, tables.side>>>(cell_count, packed, total64, n_cells,
+                                                           starts, icells, cell_first, counts,
+                                                           long_list, n_long);
+        cudaEvent_t tables_done = nullptr;
+        if (tables.side != s) {
+            cudaEventCreateWithFlags(&tables_done, cudaEventDisableTiming);
+            cudaEventRecord(tables_done, tables.side);
+        }
         const int rc_t = on_tables ? (*on_tables)(tables.side) : BVP_OK;
         if (cams)
             count_scatter_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, *fp, packed, ranks, iop);
         else
             count_scatter_flat_kernel<<<148 * 8, 256, 0, s>>>(cells, slot, P, packed, ranks, iop);
+        if (tables_done) {
+            cudaStreamWaitEvent(s, tables_done, 0);
+            cudaEventDestroy(tables_done);
+        }
         {  // short runs and long runs side by side
             SideFork fork(s);
             // the point gather table comes with the sorted runs (cams: the

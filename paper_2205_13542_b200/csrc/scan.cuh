@@ -267,16 +267,26 @@ static int64_t scan_partials_len(int64_t n) {
 }
 
 // Exclusive scan of xf(in[i]) (integer T, one pass): out[i] = sum_{j<i} xf(in[j]).
+// flags_zeroed: the caller already zeroed scan_flags(partials, n) earlier on
+// the stream (e.g. beside other resets), so the scan follows its producer
+// directly.
+template <typename T>
+static void *scan_flags(T *partials, int64_t n, size_t *bytes) {
+    const int64_t nb = ceil_div(n, kScanChunk);
+    *bytes = size_t(nb + 1) * sizeof(uint32_t);
+    return partials + 2 * nb;
+}
+
 template <typename T, typename In, typename Xf>
 static void device_excl_scan_xf(const In *in, T *out, int64_t n, T *partials, T *total, Xf xf,
-                                cudaStream_t s) {
+                                cudaStream_t s, bool flags_zeroed = false) {
     static_assert(is_exact_scan<T>::value, "the transformed scan is the one-pass form");
     const int64_t nb = ceil_div(n, kScanChunk);
     if (nb == 0) {
         cudaMemsetAsync(total, 0, sizeof(T), s);
         return;
     }
-    cudaMemsetAsync(partials + 2 * nb, 0, size_t(nb + 1) * sizeof(uint32_t), s);
+    if (!flags_zeroed) cudaMemsetAsync(partials + 2 * nb, 0, size_t(nb + 1) * sizeof(uint32_t), s);
     scan_onepass_kernel<T, In, Xf><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, out, partials, nb,
                                                                         total, xf);
 }
