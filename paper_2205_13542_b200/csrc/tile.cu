@@ -405,11 +405,6 @@ tile_pool_kernel(TilePoolArgs a) {
     constexpr int RPT = 16;
     const uint32_t *rt = a.rec + t * g.tpc;
     uint32_t pre[RPT];
-#pragma unroll
-    for (int u = 0; u < RPT; ++u) {
-        const uint32_t k = threadIdx.x + kPoolThreads * u;
-        pre[u] = k < h.x ? __ldg(rt + k) : 0u;
-    }
     // (1) stage: F[hl][c] = features[n, c, h0 + hl, w]; w[hl][d] = dist[n, d, h0 + hl, w]
     // (stage_quads: cluster columns, distributed shared memory)
     {
@@ -425,6 +420,12 @@ tile_pool_kernel(TilePoolArgs a) {
         // CS full channel slots)
         stage_quads<CL, ES>(x, a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
         stage_quads<CL, ES>(x, a.weights, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
+        // the first RPT records of each thread, in flight across the barrier
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const uint32_t k = threadIdx.x + kPoolThreads * u;
+            pre[u] = k < h.x ? __ldg(rt + k) : 0u;
+        }
         if (CL > 1)
             cluster.sync();
     }
