@@ -402,6 +402,10 @@ tile_pool_kernel(TilePoolArgs a) {
     // distributed shared memory may be written only once every CTA of the
     // cluster is running: arrive now, wait just before the first remote store
     if (CL > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    // the first weight window's zeros (it is at most wbudget long; windows
+    // are multiples of 8 floats: 16-byte stores), beside the staging
+    for (uint32_t i = 4 * threadIdx.x; i < min(h.w, uint32_t(a.wbudget)); i += 4 * kPoolThreads)
+        *reinterpret_cast<float4 *>(ws + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     constexpr int RPT = 16;
     const uint32_t *rt = a.rec + t * g.tpc;
     uint32_t pre[RPT];
@@ -494,11 +498,12 @@ tile_pool_kernel(TilePoolArgs a) {
         const uint32_t r_end = q1 == n_groups ? h.x : gt[q1].w;
         const uint32_t w_end = q1 == n_groups ? total_w : gt[q1].z;
         const uint32_t wlen = w_end - G0.z;
-        __syncthreads();  // staging done; previous window consumed
-        // (window offsets and lengths are multiples of 8 floats: 16-byte stores)
-        for (uint32_t i = 4 * threadIdx.x; i < wlen; i += 4 * kPoolThreads)
-            *reinterpret_cast<float4 *>(ws + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncthreads();
+        if (q0 > 0) {  // (the single / first window was zeroed before the staging)
+            __syncthreads();  // previous window consumed
+            for (uint32_t i = 4 * threadIdx.x; i < wlen; i += 4 * kPoolThreads)
+                *reinterpret_cast<float4 *>(ws + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();  // staging done (first window) / window zeroed
         // (2) aggregate: each run of one (cell, row) summed in depth order
         // (records below RPT * 256 come from the prefetch)
         auto run = [&](uint32_t k, uint32_t r) {
