@@ -854,3 +854,29 @@ def test_tiled_backward_random_wide_instances(seed, red):
     tp.backward_f32(torch.from_numpy(g).to(dev), f.detach(), d.detach(), 1, C,
                     bp._lib.BVP_MEAN if red == "mean" else bp._lib.BVP_SUM, tf2, None)
     assert torch.equal(tf, tf2)
+
+
+@pytest.mark.parametrize("seed", [30_000 + s for s in range(4)])
+def test_tile_path_random_deep_instances(seed):
+    """Up to 600 depth bins (tiles of fewer rows, several rounds of depth
+    quads per CTA, the fused softmax over long rays): the tiled reduction
+    and its fused variant against the 64-bit oracle."""
+    inst = random_instance(seed, 24, 600, 12)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    dist = o.normalize_depth(inst.logits)
+    C = inst.features.shape[1]
+    for red in (bp.Reducer.SUM, bp.Reducer.MEAN):
+        want = o.pool_naive(inst.features, dist, cache.cell_of_point, grid.n_cells, red.value)
+        got = bp.pool_interval(inst.features, dist, cache, grid, red, exact=False)
+        assert max_rel_dev(want, got.values.reshape(want.shape)) <= FP32_TOL, red
+    if C == 0:
+        return
+    dev = torch.device("cuda")
+    fb, lb = o.bf16_round(inst.features), o.bf16_round(inst.logits)
+    got = bp.pool_fused(torch.from_numpy(inst.logits).to(dev).to(torch.bfloat16),
+                        torch.from_numpy(inst.features).to(dev).to(torch.bfloat16), cache, grid
+                        ).values.cpu().numpy().reshape(C, -1)
+    want = o.fused_pool(fb, lb, cache.ranks, cache.interval_starts, cache.interval_cells,
+                        grid.n_cells, "sum")
+    assert max_rel_dev(want, got) <= 1e-5
