@@ -148,6 +148,9 @@ tile_backward_kernel(TileBwdArgs a) {
     for (int i = threadIdx.x; i < kTileMaxPoints / 32; i += kPoolThreads) s_cov[i] = 0u;
     // gradient-row buffers: channels past C stay zero (the copies stop at C)
     for (int i = threadIdx.x; i < 2 * kTileGroup * GS; i += kPoolThreads) gsm[i] = 0.f;
+    // the first weight window's zeros (windows are multiples of 8 floats)
+    for (uint32_t i = 4 * threadIdx.x; i < min(h.w, uint32_t(a.wbudget)); i += 4 * kPoolThreads)
+        *reinterpret_cast<float4 *>(ws + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     {
         float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
         float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
@@ -232,21 +235,34 @@ tile_backward_kernel(TileBwdArgs a) {
         }
         const uint32_t r_end = q1 == n_groups ? h.x : gt[q1].w;
         const uint32_t w_end = q1 == n_groups ? total_w : gt[q1].z;
-        __syncthreads();  // previous window's records done with ws / pw
-        for (uint32_t i = threadIdx.x; i < w_end - G0.z; i += kPoolThreads) ws[i] = 0.f;
+        if (q0 > 0) {  // (the first window was zeroed beside the staging)
+            __syncthreads();  // previous window's records done with ws / pw
+            for (uint32_t i = 4 * threadIdx.x; i < w_end - G0.z; i += 4 * kPoolThreads)
+                *reinterpret_cast<float4 *>(ws + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         fetch(q0, 0);
         __syncthreads();
-        // aggregation: A of the window (the forward's arithmetic)
-        for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
-            uint32_t r = __ldg(rt + k);
-            if (!(r >> 31)) continue;
-            const uint32_t widx = (r >> shift) & wmask;
-            float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
-            for (uint32_t kk = k + 1; (r >> 30) & 1u; ++kk) {
-                r = __ldg(rt + kk);
-                sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+        // aggregation: A of the window (the forward's arithmetic); each
+        // thread's records 8 at a time, all loaded before any is used
+        for (uint32_t k0 = G0.w + threadIdx.x; k0 < r_end; k0 += 8 * kPoolThreads) {
+            uint32_t rr[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t k = k0 + u * kPoolThreads;
+                rr[u] = k < r_end ? __ldg(rt + k) : 0u;
             }
-            ws[widx - G0.z] = sum;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                uint32_t r = rr[u];
+                if (!(r >> 31)) continue;
+                const uint32_t widx = (r >> shift) & wmask;
+                float sum = pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+                for (uint32_t kk = k0 + u * kPoolThreads + 1; (r >> 30) & 1u; ++kk) {
+                    r = __ldg(rt + kk);
+                    sum += pw[((r >> g.d_bits) & hmask) * PD + (r & dmask)];
+                }
+                ws[widx - G0.z] = sum;
+            }
         }
         // this thread's (row, segment) of a group: its window slot; the
         // group's A goes dense into s_a for the fragments
@@ -319,13 +335,24 @@ tile_backward_kernel(TileBwdArgs a) {
             if (q + 1 < q1) load_a(q + 1);
         }
         __syncthreads();
-        // every point of the window: its Dot into the depth-weight rows
-        for (uint32_t k = G0.w + threadIdx.x; k < r_end; k += kPoolThreads) {
-            const uint32_t r = __ldg(rt + k);
-            const uint32_t hl = (r >> g.d_bits) & hmask, d = r & dmask;
-            pw[hl * PD + d] = ws[((r >> shift) & wmask) - G0.z];
-            const uint32_t pt = hl * uint32_t(D) + d;
-            atomicOr(&s_cov[pt >> 5], 1u << (pt & 31));
+        // every point of the window: its Dot into the depth-weight rows (the
+        // records 8 at a time, as above)
+        for (uint32_t k0 = G0.w + threadIdx.x; k0 < r_end; k0 += 8 * kPoolThreads) {
+            uint32_t rr[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t k = k0 + u * kPoolThreads;
+                rr[u] = k < r_end ? __ldg(rt + k) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (k0 + u * kPoolThreads >= r_end) break;
+                const uint32_t r = rr[u];
+                const uint32_t hl = (r >> g.d_bits) & hmask, d = r & dmask;
+                pw[hl * PD + d] = ws[((r >> shift) & wmask) - G0.z];
+                const uint32_t pt = hl * uint32_t(D) + d;
+                atomicOr(&s_cov[pt >> 5], 1u << (pt & 31));
+            }
         }
         q0 = q1;
     }
