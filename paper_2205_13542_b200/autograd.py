@@ -62,16 +62,12 @@ class _BevPoolFn(torch.autograd.Function):
         need_f, need_w = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
         gf = torch.empty((B, N, C, H, W), dtype=torch.float32, device=dev) if need_f else None
         gw = torch.empty((B, N, D, H, W), dtype=torch.float32, device=dev) if need_w else None
-        if ctx.tile is not None:
-            # the gather backward reads feature rows: the NHWC copy the interval
-            # forward makes on the side, made here for the tiled forward
+        if ctx.tile is not None:  # the tiled adjoint, on the forward's tiles
             features, dist = ctx.saved_tensors
-            nhwc = torch.empty(features.numel(), dtype=torch.float32, device=dev)
-            _lib.call("bvp_to_nhwc_f32", ptr(features), B * N, C, H * W, ptr(nhwc),
-                      stream_ptr(dev))
-            argmax = None
-        else:
-            nhwc, dist, argmax = ctx.saved_tensors
+            if need_f or need_w:
+                ctx.tile.backward_f32(g, features, dist, B, C, _MODE[reducer], gf, gw)
+            return gf, gw, None, None, None, None, None
+        nhwc, dist, argmax = ctx.saved_tensors
         if need_f or need_w:
             ws = torch.empty(_lib.load().bvp_backward_workspace_bytes(B, C, cache.n_int_max),
                              dtype=torch.uint8, device=dev)
