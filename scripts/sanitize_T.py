@@ -4,7 +4,8 @@
     compute-sanitizer --tool racecheck python scripts/sanitize_T.py
 
 fast (tiled) SUM / MEAN, MAX and exact (interval kernels), pool_naive,
-the fused bf16 path, the gather backward, a graph-captured PoolPlan step,
+the fused bf16 path, the tiled adjoint (SUM / MEAN) and the gather backward
+(MAX), a graph-captured PoolPlan step,
 a per-frame CacheBuilder frame (association + tile plan), the reference-
 shaped interval_reduce, the prefix-sum baseline, and the frustum / quantize
 / depth-check entry points.
@@ -35,7 +36,10 @@ lg = torch.from_numpy(logits_np).to(dev).to(torch.bfloat16)
 bp.pool_fused(lg, feats.to(torch.bfloat16), cache, grid)
 F = feats[None].clone().requires_grad_(True)
 D = dist[None].clone().requires_grad_(True)
-bp.bev_pool(F, D, cache, grid).backward(torch.ones((1, spec.channels, grid.nx, grid.ny), device=dev))
+for red in ("sum", "max"):  # tiled adjoint; gather backward
+    F.grad = D.grad = None
+    bp.bev_pool(F, D, cache, grid, red).backward(
+        torch.ones((1, spec.channels, grid.nx, grid.ny), device=dev))
 plan = bp.PoolPlan(cache, grid, spec.n_cameras, spec.channels, f.height, f.width, f.depth_bins)
 plan.run_graphed(feats[None], dist[None])
 builder = bp.CacheBuilder(spec.n_cameras, f, grid, tiles=True)
