@@ -62,7 +62,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define BVP_ABI_VERSION 8
+#define BVP_ABI_VERSION 9
 
 #define BVP_OK 0
 #define BVP_ERR_INVALID 1      /* bad argument            -> ValidationError     */
@@ -422,10 +422,6 @@ int bvp_tile_pool_f32(const float *features, const float *dist, const bvp_tile_p
                       int B, int C, int mode, float *rows, size_t rows_bytes, float *out,
                       void *stream);
 
-/* Fused lift + pool (config F): logits (B,N,D,H,W) bf16 and context
- * (B,N,C,H,W) bf16 -> out (B,C,n_cells) f32 = pool(softmax_D(logits) (x)
- * context); the depth softmax of a tile's pixels is formed in shared memory
- * (fp32), nothing else is materialised. */
 /* The adjoint of bvp_tile_pool_f32 (config B training, SUM / MEAN): from
  * grad_out (B,C,n_cells) and the forward's features / dist, grad_features
  * (B,N,C,H,W) and grad_dist (B,N,D,H,W) (either may be NULL: not computed),
@@ -438,9 +434,25 @@ int bvp_tile_backward_f32(const float *grad_out, const float *features, const fl
                           size_t rows_bytes, float *grad_features, float *grad_dist,
                           void *stream);
 
+/* Fused lift + pool (config F): logits (B,N,D,H,W) bf16 and context
+ * (B,N,C,H,W) bf16 -> out (B,C,n_cells) f32 = pool(softmax_D(logits) (x)
+ * context); the depth softmax of a tile's pixels is formed in shared memory
+ * (fp32), nothing else is materialised. */
 int bvp_tile_pool_fused_bf16(const uint16_t *logits, const uint16_t *context,
                              const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
                              size_t rows_bytes, float *out, void *stream);
+
+/* Its adjoint (config F training, SUM / MEAN): grad_logits (B,N,D,H,W) bf16
+ * and grad_context (B,N,C,H,W) bf16 (either may be NULL) from grad_out
+ * (B,C,n_cells) f32.  One pass per tile: the softmax is re-formed in shared
+ * memory, grad_w = <context, g'> per point, grad_context = sum_d w g' per
+ * pixel, and grad_logit = w (grad_w - sum_d w grad_w) -- no fp32 copy of the
+ * softmax, the context or a gradient goes through global memory.  fp32
+ * arithmetic, bf16 results; deterministic.  rows: as the forward's. */
+int bvp_tile_fused_backward_bf16(const float *grad_out, const uint16_t *logits,
+                                 const uint16_t *context, const bvp_tile_plan *plan, int B, int C,
+                                 int mode, float *rows, size_t rows_bytes, uint16_t *grad_logits,
+                                 uint16_t *grad_context, void *stream);
 
 /* ---- the paper's "before": LSS prefix-sum pooling --------- */
 

@@ -21,7 +21,7 @@ OUT_OF_RANGE = 0xFFFFFFFF
 BVP_OUT_ZEROED = 0x100  # include/bevpool_b200.h
 BVP_TILE_PHASE1 = 0x200
 BVP_TILE_PHASE2 = 0x400
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 
 _P = ctypes.c_void_p
@@ -105,6 +105,7 @@ SIGNATURES = {
     "bvp_tile_backward_f32": (_I, [_P, _P, _P, _TP, _I, _I, _I, _P, _S, _P, _P, _P]),
     "bvp_tile_pool_f32": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
     "bvp_tile_pool_fused_bf16": (_I, [_P, _P, _TP, _I, _I, _I, _P, _S, _P, _P]),
+    "bvp_tile_fused_backward_bf16": (_I, [_P, _P, _P, _TP, _I, _I, _I, _P, _S, _P, _P, _P]),
     "bvp_prefixsum_workspace_bytes": (_S, [_L, _I]),
     "bvp_pool_prefixsum_f32": (_I, [_P, _P, _P, _P, _P, _L, _L, _I, _I, _I, _I, _I, _L, _I, _P,
                                     _P, _S, _P]),

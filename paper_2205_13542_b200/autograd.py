@@ -99,8 +99,9 @@ def bev_pool_map(features, dist, cache, grid, reducer=Reducer.SUM) -> BevFeature
 
 class _FusedPoolFn(torch.autograd.Function):
     """pool(softmax_D(logits) (x) context), bf16 in: the tiled fused forward
-    (csrc/tile.cu, softmax in shared memory) and the fused backward
-    (bvp_fused_backward_bf16)."""
+    (csrc/tile.cu, softmax in shared memory) and its tiled adjoint
+    (bvp_tile_fused_backward_bf16, csrc/tile_backward.cu); MAX and C > 128
+    take the interval forward and bvp_fused_backward_bf16."""
 
     @staticmethod
     def forward(ctx, logits, context, cache: AssociationCache, grid: BevGridSpec,
@@ -119,6 +120,14 @@ class _FusedPoolFn(torch.autograd.Function):
         C = context.shape[2]
         dev = grad_out.device
         g = grad_out.float().contiguous()
+        tp = _tile_plan(cache, N, H, W, D, C, _MODE[ctx.reducer], 0)
+        if tp is not None:  # one pass per tile, bf16 gradients out
+            need_l, need_c = ctx.needs_input_grad[0], ctx.needs_input_grad[1]
+            gl = torch.empty_like(logits) if need_l else None
+            gc = torch.empty_like(context) if need_c else None
+            if need_l or need_c:
+                tp.fused_backward_bf16(g, logits, context, B, C, _MODE[ctx.reducer], gl, gc)
+            return gl, gc, None, None, None
         gl = torch.empty_like(logits)
         gc = torch.empty_like(context)
         ws = torch.empty(int(_lib.load().bvp_fused_backward_workspace_bytes(

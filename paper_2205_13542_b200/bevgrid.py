@@ -243,6 +243,16 @@ class TilePlan:
         _lib.call("bvp_tile_pool_fused_bf16", ptr(logits), ptr(context), ctypes.byref(self.st),
                   B, C, mode, ptr(rows), 4 * rows.numel(), ptr(out), stream_ptr(self.device))
 
+    def fused_backward_bf16(self, grad_out: torch.Tensor, logits: torch.Tensor,
+                            context: torch.Tensor, B: int, C: int, mode: int, grad_logits,
+                            grad_context) -> None:
+        """The adjoint of pool_fused_bf16 (SUM / MEAN): bf16 grad_logits /
+        grad_context (either may be None) from grad_out (B, C, n_cells) f32."""
+        rows = self.rows(B, C)
+        _lib.call("bvp_tile_fused_backward_bf16", ptr(grad_out), ptr(logits), ptr(context),
+                  ctypes.byref(self.st), B, C, mode, ptr(rows), 4 * rows.numel(),
+                  ptr(grad_logits), ptr(grad_context), stream_ptr(self.device))
+
 
 @dataclass(eq=False)
 class AssociationCache:

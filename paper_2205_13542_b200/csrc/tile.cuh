@@ -207,13 +207,16 @@ __device__ __forceinline__ void stage_quads(const ColumnXfer &x, const void *src
 }
 
 // (Remote) shared -> global, the reverse of stage_quads: src[hl][c] of the
-// CTA owning column j into dst planes (fp32), channels < n_ch.
-template <int CL>
-__device__ __forceinline__ void unstage_quads(const ColumnXfer &x, float *dst, int n_ch,
+// CTA owning column j into dst planes (fp32, or bf16 rounded to nearest),
+// channels < n_ch.
+__device__ __forceinline__ void store_as(float *p, float v) { *p = v; }
+__device__ __forceinline__ void store_as(__nv_bfloat16 *p, float v) { *p = __float2bfloat16(v); }
+template <int CL, typename OT = float>
+__device__ __forceinline__ void unstage_quads(const ColumnXfer &x, OT *dst, int n_ch,
                                               int64_t base, const float *src, int stride) {
     constexpr int NW = kPoolThreads / 32, RS = 32 / CL, U = 4;
     const int warp = threadIdx.x >> 5;
-    float *db = dst + base;
+    OT *db = dst + base;
     const int n_q = (((n_ch + 3) >> 2) - x.rank + CL - 1) / CL;
     const int items = n_q * x.n_rb;
     for (int i0 = warp; i0 < items; i0 += NW * U) {
@@ -233,11 +236,11 @@ __device__ __forceinline__ void unstage_quads(const ColumnXfer &x, float *dst, i
             const int it = i0 + NW * u;
             const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * ms[u];
             if (it < items && hl < x.th) {
-                float *po = db + int64_t(c0) * x.HW + int64_t(hl) * x.W;
+                OT *po = db + int64_t(c0) * x.HW + int64_t(hl) * x.W;
                 const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    if (c0 + e < n_ch) po[int64_t(e) * x.HW] = e4[e];
+                    if (c0 + e < n_ch) store_as(po + int64_t(e) * x.HW, e4[e]);
             }
         }
     }

@@ -56,14 +56,14 @@ tile_grad_rows_kernel(const float *__restrict__ grad_out, const uint32_t *__rest
 
 struct TileBwdArgs {
     const float *grad_rows;  // (B, max_seg, C): tile_grad_rows_kernel's rows
-    const float *feats;      // (B, N, C, H, W)
-    const float *dist;       // (B, N, D, H, W)
+    const void *feats;       // (B, N, C, H, W) f32; fused: the bf16 context
+    const void *dist;        // (B, N, D, H, W) f32; fused: the bf16 depth logits
     const uint4 *hdr;
     const uint32_t *rec;
     const uint4 *groups;
     const uint32_t *seg_row;
-    float *grad_feats;       // (B, N, C, H, W), or null
-    float *grad_dist;        // (B, N, D, H, W), or null
+    void *grad_feats;        // (B, N, C, H, W) f32 / bf16 (fused), or null
+    void *grad_dist;         // (B, N, D, H, W) f32 / grad logits bf16 (fused), or null
     int64_t max_seg;
     TileGeom g;
     int C, wbudget;
@@ -112,7 +112,72 @@ __device__ __forceinline__ void mma3_tf32(float (&d)[4], const uint32_t (&ah)[4]
 // are zeroed, grad_f goes over the feature rows, and both tiles go back to
 // global memory through the cluster.  Deterministic (fixed sums, no atomics
 // on values); tiles of <= 32 rows, C <= 128.
-template <int CS, int CL>
+//
+// FU (config F training, bvp_tile_fused_backward_bf16): the staging reads the
+// bf16 context and depth logits and forms each pixel's depth softmax w in
+// shared memory, as the fused forward does (its max and 1/sum kept per row);
+// the records leave P = w grad_w in the weight rows, and each pixel row goes
+// out as
+//   grad_logit[d] = w[d] (grad_w[d] - sum_d' w[d'] grad_w[d'])
+//                 = P[d] - w[d] sum_d' P[d']
+// with w re-formed bit for bit from the (L2-resident) logits on the way out,
+// so the shared footprint -- and 4 CTAs per SM -- is the fp32 variant's.
+// Both gradients are rounded to bf16; no fp32 copy of the softmax, the
+// context or a gradient touches global memory.
+// FU's write-out of grad_logits (unstage_quads' item walk): for point
+// (d, hl) of column j, P from column j's weight rows and the logit from
+// global memory (read by the staging moments before: L2), then
+//   w = exp2(l log2e - ms) inv  (the staging's arithmetic, the same bits)
+//   grad_logit = P - w psum
+template <int CL>
+__device__ __forceinline__ void unstage_logit_grad(const ColumnXfer &x, __nv_bfloat16 *dst,
+                                                   const __nv_bfloat16 *logits, int D,
+                                                   int64_t base, const float *P, int stride,
+                                                   const float *ms, const float *inv,
+                                                   const float *psum) {
+    constexpr int NW = kPoolThreads / 32, RS = 32 / CL, U = 4;
+    constexpr float kLog2e = 1.4426950408889634f;
+    const int warp = threadIdx.x >> 5;
+    const int n_q = (((D + 3) >> 2) - x.rank + CL - 1) / CL;
+    const int items = n_q * x.n_rb;
+    for (int i0 = warp; i0 < items; i0 += NW * U) {
+        int qs[U], mr[U];
+        xfer_items<U>(i0, x.n_rb, qs, mr);
+        float4 v[U];
+        uint32_t l[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = i0 + NW * u;
+            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * mr[u];
+            const bool ok = it < items && hl < x.th;
+            v[u] = ok ? *reinterpret_cast<const float4 *>(P + hl * stride + c0)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            const char *pl = reinterpret_cast<const char *>(
+                logits + base + int64_t(c0) * x.HW + int64_t(hl) * x.W);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                l[u][e] = ldg_l2pf_u16(pl + 2 * int64_t(e) * x.HW, ok && c0 + e < D) << 16;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int it = i0 + NW * u;
+            const int c0 = 4 * (x.rank + CL * qs[u]), hl = x.r0 + RS * mr[u];
+            if (it < items && hl < x.th) {
+                const float m = ms[hl], iv = inv[hl], s = psum[hl];
+                __nv_bfloat16 *po = dst + base + int64_t(c0) * x.HW + int64_t(hl) * x.W;
+                const float e4[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (c0 + e < D) {
+                        const float w = exp2f(fmaf(__uint_as_float(l[u][e]), kLog2e, -m)) * iv;
+                        po[int64_t(e) * x.HW] = __float2bfloat16(e4[e] - w * s);
+                    }
+            }
+        }
+    }
+}
+
+template <int CS, int CL, bool FU>
 __global__ void __launch_bounds__(kPoolThreads, 4)
 tile_backward_kernel(TileBwdArgs a) {
     constexpr int CP = CS * 32;
@@ -133,6 +198,7 @@ tile_backward_kernel(TileBwdArgs a) {
     float *fs = ws + a.wbudget;   // [TH][FS] feature rows, then grad_f rows
     float *pw = fs + g.TH * FS;   // [TH][PD] depth weights, then grad_w rows
     float *gsm = pw + g.TH * PD;  // [2][8][GS] gradient rows of the current / next group
+    __shared__ float s_ms[FU ? 32 : 1], s_inv[FU ? 32 : 1], s_psum[FU ? 32 : 1];  // FU, per row
     const int64_t nb = int64_t(b) * g.N + id.n;
     const int64_t pix0 = int64_t(id.h0) * g.W + id.w;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,10 +220,45 @@ tile_backward_kernel(TileBwdArgs a) {
     {
         float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
         float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
-        stage_quads<CL, 4>(x, a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
-        stage_quads<CL, 4>(x, a.dist, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
+        constexpr int ES = FU ? 2 : 4;
+        stage_quads<CL, ES>(x, a.feats, C, CP / 4, nb * C * HW + col, rfs, FS, true);
+        stage_quads<CL, ES>(x, a.dist, D, (D + 3) >> 2, nb * D * HW + col, rpw, PD, false);
         if (CL > 1) cluster.sync();
         else __syncthreads();
+    }
+    if (FU) {
+        // w = softmax_D of each pixel row in place (lift.py:17-31, fp32 from
+        // bf16 logits), 8 lanes per pixel as in the fused forward; the
+        // aggregation below reads it after its barrier
+        constexpr float kLog2e = 1.4426950408889634f;
+        const int sub = lane & 7;
+        for (int hl0 = 4 * warp; hl0 < id.th; hl0 += 4 * (kPoolThreads / 32)) {
+            const int hl = hl0 + (lane >> 3);
+            const bool on = hl < id.th;
+            float *row = pw + (on ? hl : 0) * PD;
+            float m = -INFINITY;
+            if (on)
+                for (int d = sub; d < D; d += 8) m = fmaxf(m, row[d]);
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+            const float ms = m * kLog2e;
+            float sum = 0.f;
+            if (on)
+                for (int d = sub; d < D; d += 8) {
+                    const float e = exp2f(fmaf(row[d], kLog2e, -ms));
+                    row[d] = e;
+                    sum += e;
+                }
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+            const float inv = 1.f / sum;
+            if (on)
+                for (int d = sub; d < D; d += 8) row[d] *= inv;
+            if (on && sub == 0) {
+                s_ms[hl] = ms;
+                s_inv[hl] = inv;
+            }
+        }
     }
     // this warp's F fragments (A operand of Dot): rows mt*16 + g (+8),
     // channels 8 ks + t (+4), k-steps ks = wq4, wq4 + 4, wq4 + 8
@@ -349,7 +450,9 @@ tile_backward_kernel(TileBwdArgs a) {
                 if (k0 + u * kPoolThreads >= r_end) break;
                 const uint32_t r = rr[u];
                 const uint32_t hl = (r >> g.d_bits) & hmask, d = r & dmask;
-                pw[hl * PD + d] = ws[((r >> shift) & wmask) - G0.z];
+                const float dot = ws[((r >> shift) & wmask) - G0.z];
+                if (FU) pw[hl * PD + d] *= dot;  // P = w grad_w
+                else pw[hl * PD + d] = dot;
                 const uint32_t pt = hl * uint32_t(D) + d;
                 atomicOr(&s_cov[pt >> 5], 1u << (pt & 31));
             }
@@ -359,11 +462,27 @@ tile_backward_kernel(TileBwdArgs a) {
     __syncthreads();
     // points without a record (out of range) get a zero weight gradient; the
     // grad_f fragments go over the feature rows
-    for (int hl = warp; hl < id.th; hl += kPoolThreads / 32)
+    for (int hl = warp; hl < id.th; hl += kPoolThreads / 32) {
+        if (!FU) {
+            for (int d = lane; d < D; d += 32) {
+                const int pt = hl * D + d;
+                if (!((s_cov[pt >> 5] >> (pt & 31)) & 1u)) pw[hl * PD + d] = 0.f;
+            }
+            continue;
+        }
+        // FU: P of points without a record is 0; the row's sum of P (lane
+        // partials, then a fixed butterfly: deterministic)
+        float *pr = pw + hl * PD;
+        float s = 0.f;
         for (int d = lane; d < D; d += 32) {
             const int pt = hl * D + d;
-            if (!((s_cov[pt >> 5] >> (pt & 31)) & 1u)) pw[hl * PD + d] = 0.f;
+            if ((s_cov[pt >> 5] >> (pt & 31)) & 1u) s += pr[d];
+            else pr[d] = 0.f;
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+        if (lane == 0) s_psum[hl] = s;
+    }
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const int nt = wq4 + 4 * i;
@@ -381,22 +500,36 @@ tile_backward_kernel(TileBwdArgs a) {
     if (CL > 1) cluster.sync();
     else __syncthreads();
     {
+        using OT = typename std::conditional<FU, __nv_bfloat16, float>::type;
         const float *rfs = CL > 1 ? cluster.map_shared_rank(fs, x.j) : fs;
         const float *rpw = CL > 1 ? cluster.map_shared_rank(pw, x.j) : pw;
-        if (a.grad_feats) unstage_quads<CL>(x, a.grad_feats, C, nb * C * HW + col, rfs, FS);
-        if (a.grad_dist) unstage_quads<CL>(x, a.grad_dist, D, nb * D * HW + col, rpw, PD);
+        if (a.grad_feats)
+            unstage_quads<CL>(x, static_cast<OT *>(a.grad_feats), C, nb * C * HW + col, rfs, FS);
+        if (a.grad_dist) {
+            if (FU) {
+                const float *rms = CL > 1 ? cluster.map_shared_rank(s_ms, x.j) : s_ms;
+                const float *rinv = CL > 1 ? cluster.map_shared_rank(s_inv, x.j) : s_inv;
+                const float *rps = CL > 1 ? cluster.map_shared_rank(s_psum, x.j) : s_psum;
+                unstage_logit_grad<CL>(x, static_cast<__nv_bfloat16 *>(a.grad_dist),
+                                       static_cast<const __nv_bfloat16 *>(a.dist), D,
+                                       nb * D * HW + col, rpw, PD, rms, rinv, rps);
+            } else {
+                unstage_quads<CL>(x, static_cast<float *>(a.grad_dist), D, nb * D * HW + col,
+                                  rpw, PD);
+            }
+        }
     }
     if (CL > 1) cluster.sync();  // peers done reading this CTA's shared memory
 }
 
-template <int CS, int CL>
+template <int CS, int CL, bool FU>
 static int launch_backward(const TileBwdArgs &a, int B, size_t smem, cudaStream_t s) {
     static int max_dyn = -1;
     if (max_dyn < 0) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, tile_backward_kernel<CS, CL>);
+        cudaFuncGetAttributes(&fa, tile_backward_kernel<CS, CL, FU>);
         max_dyn = 227 * 1024 - int(fa.sharedSizeBytes);
-        cudaFuncSetAttribute(tile_backward_kernel<CS, CL>,
+        cudaFuncSetAttribute(tile_backward_kernel<CS, CL, FU>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
     }
     BVP_REQUIRE(smem <= size_t(max_dyn), BVP_ERR_UNSUPPORTED,
@@ -413,15 +546,15 @@ static int launch_backward(const TileBwdArgs &a, int B, size_t smem, cudaStream_
     attr_c[0].val.clusterDim.z = 1;
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, tile_backward_kernel<CS, CL>, a);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, tile_backward_kernel<CS, CL, FU>, a);
     BVP_REQUIRE(e == cudaSuccess, BVP_ERR_CUDA, "tile_backward launch: %s", cudaGetErrorString(e));
     return BVP_OK;
 }
 
-template <int CS>
-static int run_tile_backward(const float *grad_out, const float *feats, const float *dist,
+template <int CS, bool FU>
+static int run_tile_backward(const float *grad_out, const void *feats, const void *dist,
                              const bvp_tile_plan *p, const TileGeom &g, int B, int C, int mean,
-                             float *rows, float *grad_feats, float *grad_dist, cudaStream_t s) {
+                             float *rows, void *grad_feats, void *grad_dist, cudaStream_t s) {
     const PlanLayout L = plan_layout(g, p->n_cells);
     tile_grad_rows_kernel<CS><<<dim3(unsigned(ceil_div(p->n_cells, kFinCells)), unsigned(B)),
                                 kPoolThreads, 0, s>>>(
@@ -447,13 +580,45 @@ static int run_tile_backward(const float *grad_out, const float *feats, const fl
     const int CL = (g.W % 8 == 0) ? 8 : (g.W % 4 == 0) ? 4 : (g.W % 2 == 0) ? 2 : 1;
     int rc;
     switch (CL) {
-        case 8: rc = launch_backward<CS, 8>(a, B, smem, s); break;
-        case 4: rc = launch_backward<CS, 4>(a, B, smem, s); break;
-        case 2: rc = launch_backward<CS, 2>(a, B, smem, s); break;
-        default: rc = launch_backward<CS, 1>(a, B, smem, s); break;
+        case 8: rc = launch_backward<CS, 8, FU>(a, B, smem, s); break;
+        case 4: rc = launch_backward<CS, 4, FU>(a, B, smem, s); break;
+        case 2: rc = launch_backward<CS, 2, FU>(a, B, smem, s); break;
+        default: rc = launch_backward<CS, 1, FU>(a, B, smem, s); break;
     }
     if (rc != BVP_OK) return rc;
-    return check_launch("tile_backward");
+    return check_launch(FU ? "tile_fused_backward" : "tile_backward");
+}
+
+template <bool FU>
+static int tile_backward_dispatch(const float *grad_out, const void *feats, const void *dist,
+                                  const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
+                                  size_t rows_bytes, void *grad_feats, void *grad_dist,
+                                  void *stream) {
+    TileGeom g;
+    const int rc = plan_dims_from(plan, g);
+    if (rc != BVP_OK) return rc;
+    BVP_REQUIRE(B >= 1 && C >= 0, BVP_ERR_INVALID, "bad dims B=%d C=%d", B, C);
+    BVP_REQUIRE(mode == BVP_SUM || mode == BVP_MEAN, BVP_ERR_UNSUPPORTED,
+                "the tiled backward takes SUM and MEAN only (mode %d)", mode);
+    BVP_REQUIRE(C <= 128, BVP_ERR_UNSUPPORTED, "the tiled backward takes C <= 128 (C=%d)", C);
+    BVP_REQUIRE(g.TH <= 32, BVP_ERR_UNSUPPORTED, "the tiled backward takes tiles of <= 32 rows");
+    if (C == 0 || (!grad_feats && !grad_dist)) return BVP_OK;
+    BVP_REQUIRE(grad_out && feats && dist && rows, BVP_ERR_INVALID, "null pointer argument");
+    BVP_REQUIRE(rows_bytes >= size_t(B) * plan->max_seg * C * sizeof(float), BVP_ERR_INVALID,
+                "segment-row scratch too small: need %zu bytes, got %zu",
+                size_t(B) * plan->max_seg * C * sizeof(float), rows_bytes);
+    cudaStream_t s = as_stream(stream);
+    const int mean = mode == BVP_MEAN;
+    switch ((C + 31) / 32) {
+        case 1: return run_tile_backward<1, FU>(grad_out, feats, dist, plan, g, B, C, mean, rows,
+                                                grad_feats, grad_dist, s);
+        case 2: return run_tile_backward<2, FU>(grad_out, feats, dist, plan, g, B, C, mean, rows,
+                                                grad_feats, grad_dist, s);
+        case 3: return run_tile_backward<3, FU>(grad_out, feats, dist, plan, g, B, C, mean, rows,
+                                                grad_feats, grad_dist, s);
+        default: return run_tile_backward<4, FU>(grad_out, feats, dist, plan, g, B, C, mean, rows,
+                                                 grad_feats, grad_dist, s);
+    }
 }
 
 }  // namespace bvp
@@ -466,31 +631,16 @@ int bvp_tile_backward_f32(const float *grad_out, const float *features, const fl
                           const bvp_tile_plan *plan, int B, int C, int mode, float *rows,
                           size_t rows_bytes, float *grad_features, float *grad_dist,
                           void *stream) {
-    TileGeom g;
-    const int rc = plan_dims_from(plan, g);
-    if (rc != BVP_OK) return rc;
-    BVP_REQUIRE(B >= 1 && C >= 0, BVP_ERR_INVALID, "bad dims B=%d C=%d", B, C);
-    BVP_REQUIRE(mode == BVP_SUM || mode == BVP_MEAN, BVP_ERR_UNSUPPORTED,
-                "the tiled backward takes SUM and MEAN only (mode %d)", mode);
-    BVP_REQUIRE(C <= 128, BVP_ERR_UNSUPPORTED, "the tiled backward takes C <= 128 (C=%d)", C);
-    BVP_REQUIRE(g.TH <= 32, BVP_ERR_UNSUPPORTED, "the tiled backward takes tiles of <= 32 rows");
-    if (C == 0 || (!grad_features && !grad_dist)) return BVP_OK;
-    BVP_REQUIRE(grad_out && features && dist && rows, BVP_ERR_INVALID, "null pointer argument");
-    BVP_REQUIRE(rows_bytes >= size_t(B) * plan->max_seg * C * sizeof(float), BVP_ERR_INVALID,
-                "segment-row scratch too small: need %zu bytes, got %zu",
-                size_t(B) * plan->max_seg * C * sizeof(float), rows_bytes);
-    cudaStream_t s = as_stream(stream);
-    const int mean = mode == BVP_MEAN;
-    switch ((C + 31) / 32) {
-        case 1: return run_tile_backward<1>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                            grad_features, grad_dist, s);
-        case 2: return run_tile_backward<2>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                            grad_features, grad_dist, s);
-        case 3: return run_tile_backward<3>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                            grad_features, grad_dist, s);
-        default: return run_tile_backward<4>(grad_out, features, dist, plan, g, B, C, mean, rows,
-                                             grad_features, grad_dist, s);
-    }
+    return tile_backward_dispatch<false>(grad_out, features, dist, plan, B, C, mode, rows,
+                                         rows_bytes, grad_features, grad_dist, stream);
+}
+
+int bvp_tile_fused_backward_bf16(const float *grad_out, const uint16_t *logits,
+                                 const uint16_t *context, const bvp_tile_plan *plan, int B, int C,
+                                 int mode, float *rows, size_t rows_bytes, uint16_t *grad_logits,
+                                 uint16_t *grad_context, void *stream) {
+    return tile_backward_dispatch<true>(grad_out, context, logits, plan, B, C, mode, rows,
+                                        rows_bytes, grad_context, grad_logits, stream);
 }
 
 }  // extern "C"

@@ -4,7 +4,7 @@
     compute-sanitizer --tool racecheck python scripts/sanitize_T.py
 
 fast (tiled) SUM / MEAN, MAX and exact (interval kernels), pool_naive,
-the fused bf16 path, the tiled adjoint (SUM / MEAN) and the gather backward
+the fused bf16 path and its tiled adjoint, the tiled adjoint (SUM / MEAN) and the gather backward
 (MAX), a graph-captured PoolPlan step,
 a per-frame CacheBuilder frame (association + tile plan), the reference-
 shaped interval_reduce, the prefix-sum baseline, and the frustum / quantize
@@ -34,6 +34,10 @@ feats = torch.from_numpy(feats_np).to(dev)
 dist = torch.from_numpy(dist_np).to(dev)
 lg = torch.from_numpy(logits_np).to(dev).to(torch.bfloat16)
 bp.pool_fused(lg, feats.to(torch.bfloat16), cache, grid)
+LG = lg[None].clone().requires_grad_(True)  # the fused path's tiled adjoint
+CX = feats[None].to(torch.bfloat16).requires_grad_(True)
+bp.bev_pool_fused(LG, CX, cache, grid).backward(
+    torch.ones((1, spec.channels, grid.nx, grid.ny), device=dev))
 F = feats[None].clone().requires_grad_(True)
 D = dist[None].clone().requires_grad_(True)
 for red in ("sum", "max"):  # tiled adjoint; gather backward

@@ -856,6 +856,55 @@ def test_tiled_backward_random_wide_instances(seed, red):
     assert torch.equal(tf, tf2)
 
 
+@pytest.mark.parametrize("seed", [21_000 + s for s in range(6)])
+@pytest.mark.parametrize("red", ["sum", "mean"])
+def test_tiled_fused_backward_random_instances(seed, red):
+    """bev_pool_fused's backward (bvp_tile_fused_backward_bf16: the softmax
+    re-formed per tile, bf16 gradients out) on random rigs against the fp64
+    restatement, and against the two-pass fallback (bvp_fused_backward_bf16:
+    fp32 softmax + gather backward + Jacobian kernel); either gradient alone
+    gives the same bits."""
+    inst = random_instance(seed, 96, 130, 40)
+    frustum, grid = specs_of(inst)
+    cache = bp.build_cache(rig_of(inst.cams), frustum, grid)
+    C = inst.features.shape[1]
+    if C == 0:
+        return
+    dev = torch.device("cuda")
+    lg = torch.from_numpy(inst.logits).to(dev).to(torch.bfloat16).requires_grad_(True)
+    cx = torch.from_numpy(inst.features).to(dev).to(torch.bfloat16).requires_grad_(True)
+    out = bp.bev_pool_fused(lg, cx, cache, grid, red)
+    g = np.random.default_rng(seed).standard_normal((C, grid.n_cells)).astype(np.float32)
+    out.backward(torch.from_numpy(g).to(dev).view_as(out))
+    want_l, want_c = o.fused_backward(o.bf16_round(inst.features), o.bf16_round(inst.logits),
+                                      cache.cell_of_point, g.astype(np.float64), cache.ranks,
+                                      cache.interval_starts, cache.interval_cells, red)
+    assert max_rel_dev(want_l, lg.grad.float().cpu().numpy()) <= BF16_TOL
+    assert max_rel_dev(want_c, cx.grad.float().cpu().numpy()) <= BF16_TOL
+    N, D, H, W = inst.logits.shape
+    mode = bp._lib.BVP_MEAN if red == "mean" else bp._lib.BVP_SUM
+    gd = torch.from_numpy(g).to(dev)[None]
+    l5, c5 = lg.detach()[None].contiguous(), cx.detach()[None].contiguous()
+    ws = torch.empty(int(bp._lib.load().bvp_fused_backward_workspace_bytes(
+        1, N, C, H, W, D, cache.n_int_max)), dtype=torch.uint8, device=dev)
+    fl, fc = torch.empty_like(l5), torch.empty_like(c5)
+    bp._lib.call("bvp_fused_backward_bf16", gd.data_ptr(), l5.data_ptr(), c5.data_ptr(),
+                 cache.d_interval_starts.data_ptr(), cache.d_interval_cells.data_ptr(),
+                 cache.d_cell_first.data_ptr(), cache.d_interval_of_point.data_ptr(), 1, N, C,
+                 H, W, D, grid.nx, grid.ny, cache.n_int_max, mode, fl.data_ptr(),
+                 fc.data_ptr(), ws.data_ptr(), ws.numel(),
+                 torch.cuda.current_stream().cuda_stream)
+    assert max_rel_dev(want_l, fl[0].float().cpu().numpy()) <= BF16_TOL
+    assert max_rel_dev(want_c, fc[0].float().cpu().numpy()) <= BF16_TOL
+    tp = cache.tile_plan(N, H, W, D)
+    tl2 = torch.full_like(l5, float("nan"))
+    tp.fused_backward_bf16(gd, l5, c5, 1, C, mode, tl2, None)
+    assert torch.equal(tl2[0], lg.grad)
+    tc2 = torch.full_like(c5, float("nan"))
+    tp.fused_backward_bf16(gd, l5, c5, 1, C, mode, None, tc2)
+    assert torch.equal(tc2[0], cx.grad)
+
+
 @pytest.mark.parametrize("seed", [30_000 + s for s in range(4)])
 def test_tile_path_random_deep_instances(seed):
     """Up to 600 depth bins (tiles of fewer rows, several rounds of depth
