@@ -489,7 +489,7 @@ def main():
 # ---------------------------------------------------------------------------
 
 def run_config_bh(args, bp, torch, tdist, dev, rank, world, local):
-    """B: the training step -- forward + gather backward through the
+    """B: the training step -- tiled forward + tiled adjoint through the
     autograd op, batch 4 per GPU (samples rank*4 .. rank*4+3).  H: one
     high-res sample per GPU with the association rebuilt every step
     (CacheBuilder + PoolPlan.run_uncached).  Inputs resident in HBM, L2
@@ -556,7 +556,7 @@ def run_config_bh(args, bp, torch, tdist, dev, rank, world, local):
     tot_ms = max_over_ranks(sum(step_ms), dev)
     if rank == 0:
         P = spec.n_points
-        what = ("training step: forward + gather backward (autograd), batch 4 per GPU"
+        what = ("training step: forward + tiled adjoint (autograd), batch 4 per GPU"
                 if name == "B" else
                 "high-res frame: association rebuilt every step + forward, 1 sample per GPU")
         cfg = config_dict(spec)
@@ -700,7 +700,7 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
     except Exception as exc:  # pragma: no cover
         out["prefixsum_baseline"] = {"error": str(exc)}
 
-    # training step, batch 4: forward + gather backward
+    # training step, batch 4: tiled forward + tiled adjoint
     B = 4
     Fb = feats.expand(B, *feats.shape[1:]).contiguous().requires_grad_(True)
     Db = dist.expand(B, *dist.shape[1:]).contiguous().requires_grad_(True)
@@ -713,6 +713,20 @@ def run_variants(bp, torch, dev, spec, rig, feats, dist, cache, grid, flush):
     rec("training_b4_fwd_bwd", ms,
         B * (ref_bytes + 8 * NHW * C + 4 * C * n_cells + 4 * P + 4 * C * n_int + 4 * NHW * C
              + 4 * P), samples=B)
+    # config F training step, batch 4: the fused forward and its tiled adjoint
+    # (bf16 logits / context in, bf16 gradients out); bytes: forward and
+    # backward each read the bf16 inputs, the map and its gradient, and the
+    # backward writes both bf16 gradients
+    LGb = lg.expand(B, *lg.shape[1:]).contiguous().requires_grad_(True)
+    CXb = cx.expand(B, *cx.shape[1:]).contiguous().requires_grad_(True)
+
+    def fused_train_step():
+        LGb.grad = CXb.grad = None
+        bp.bev_pool_fused(LGb, CXb, cache, grid).backward(g)
+    ms = _timeit(torch, fused_train_step, flush)
+    rec("training_fused_b4_fwd_bwd", ms,
+        B * (3 * (2 * P + 2 * NHW * C) + 2 * 4 * C * n_cells + 8 * n_in), samples=B,
+        path="bev_pool_fused forward + bvp_tile_fused_backward_bf16 (autograd)")
 
     # high-res stress: uncached geometry every frame + forward
     hs = bp.CONFIGS["H"]
