@@ -177,8 +177,11 @@ __device__ __forceinline__ void unstage_logit_grad(const ColumnXfer &x, __nv_bfl
     }
 }
 
+// Register budget per variant, measured at S, B=4 (ncu): fp32 265 us at 4
+// CTAs/SM (64 registers) against 289 at 3 (80); FU 336 at 4 against 323 at 3
+// (its softmax, row sums and logit write-out keep more values live).
 template <int CS, int CL, bool FU>
-__global__ void __launch_bounds__(kPoolThreads, 4)
+__global__ void __launch_bounds__(kPoolThreads, FU ? 3 : 4)
 tile_backward_kernel(TileBwdArgs a) {
     constexpr int CP = CS * 32;
     constexpr int FS = CP + 4;   // = 4 (mod 32): conflict-free fragment loads

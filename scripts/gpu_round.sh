@@ -13,4 +13,6 @@ timeout 300 python bench.py --impl reference --steps 5 --warmup 1 > $OUT/bench_r
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-variants > $OUT/bench_under_ncu.log 2>&1; echo "launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tile_pool_kernel|tile_finalize_kernel" -s 2 -c 2 -o $OUT/prof -f python scripts/prof_tile.py > $OUT/ncu.log 2>&1; echo "ncu rc=$?"
 bash scripts/sanitize_all.sh $OUT/san
+(python scripts/time_fused_train.py 1; python scripts/time_fused_train.py 4; python scripts/time_train.py 4) > $OUT/train_timings.txt 2>&1; echo "train timings rc=$?"
+for v in f32 fused; do ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none -k regex:tile_ --csv python scripts/prof_tile_bwd.py $v 2>/dev/null | grep '^"' > $OUT/bwd_launch_$v.csv; done
 ls -la $OUT
