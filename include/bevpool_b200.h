@@ -426,7 +426,7 @@ int bvp_tile_pool_f32(const float *features, const float *dist, const bvp_tile_p
  * grad_out (B,C,n_cells) and the forward's features / dist, grad_features
  * (B,N,C,H,W) and grad_dist (B,N,D,H,W) (either may be NULL: not computed),
  * every element written once (points out of range and pixels no point of
- * which is in range get 0).  rows: the same scratch as the forward's.
+ * which is in range get 0; with C = 0 grad_dist is all zeros).  rows: the same scratch as the forward's.
  * Deterministic; fp32 (<= ~1e-6 relative of the fp64 adjoint).  Tiles of
  * <= 32 rows (every plan bvp_tile_plan_init makes). */
 int bvp_tile_backward_f32(const float *grad_out, const float *features, const float *dist,

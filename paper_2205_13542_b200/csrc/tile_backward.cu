@@ -605,7 +605,14 @@ static int tile_backward_dispatch(const float *grad_out, const void *feats, cons
                 "the tiled backward takes SUM and MEAN only (mode %d)", mode);
     BVP_REQUIRE(C <= 128, BVP_ERR_UNSUPPORTED, "the tiled backward takes C <= 128 (C=%d)", C);
     BVP_REQUIRE(g.TH <= 32, BVP_ERR_UNSUPPORTED, "the tiled backward takes tiles of <= 32 rows");
-    if (C == 0 || (!grad_feats && !grad_dist)) return BVP_OK;
+    if (!grad_feats && !grad_dist) return BVP_OK;
+    if (C == 0) {  // no channels: the weights' gradient is zero (grad_features is empty)
+        if (grad_dist)
+            cudaMemsetAsync(grad_dist, 0,
+                            size_t(B) * g.N * g.D * g.H * g.W * (FU ? 2 : sizeof(float)),
+                            as_stream(stream));
+        return check_launch(FU ? "tile_fused_backward" : "tile_backward");
+    }
     BVP_REQUIRE(grad_out && feats && dist && rows, BVP_ERR_INVALID, "null pointer argument");
     BVP_REQUIRE(rows_bytes >= size_t(B) * plan->max_seg * C * sizeof(float), BVP_ERR_INVALID,
                 "segment-row scratch too small: need %zu bytes, got %zu",

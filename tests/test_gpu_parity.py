@@ -856,6 +856,28 @@ def test_tiled_backward_random_wide_instances(seed, red):
     assert torch.equal(tf, tf2)
 
 
+def test_tiled_adjoints_zero_channels():
+    """C = 0: the map is empty, so both adjoints write an all-zero weight /
+    logit gradient (and touch nothing else)."""
+    spec = bp.CONFIGS["T"]
+    f = spec.frustum
+    rig, _, logits, grid = bp.gen_workload(spec)
+    cache = bp.build_cache(rig, f, grid)
+    tp = cache.tile_plan(spec.n_cameras, f.height, f.width, f.depth_bins)
+    dev = torch.device("cuda")
+    N, D, H, W = logits.shape
+    g = torch.empty((1, 0, grid.n_cells), device=dev)
+    feats = torch.empty((1, N, 0, H, W), device=dev)
+    dist = torch.from_numpy(o.normalize_depth(logits)).to(dev)[None]
+    gw = torch.full_like(dist, float("nan"))
+    tp.backward_f32(g, feats, dist, 1, 0, bp._lib.BVP_SUM, None, gw)
+    assert (gw == 0).all()
+    lg = torch.from_numpy(logits).to(dev).to(torch.bfloat16)[None]
+    gl = torch.full_like(lg, float("nan"))
+    tp.fused_backward_bf16(g, lg, feats.to(torch.bfloat16), 1, 0, bp._lib.BVP_SUM, gl, None)
+    assert (gl == 0).all()
+
+
 @pytest.mark.parametrize("seed", [21_000 + s for s in range(6)])
 @pytest.mark.parametrize("red", ["sum", "mean"])
 def test_tiled_fused_backward_random_instances(seed, red):
