@@ -10,9 +10,14 @@
  *   per rig:    bvp_build_tile_plan_ranks (the tiled reduction's plan, from
  *                                       the association)
  *               bvp_tile_pool_f32      (the tiled reduction: the fast path)
+ *   training:   bvp_tile_backward_f32  (its adjoint, config B)
+ *               bvp_tile_pool_fused_bf16 + bvp_tile_fused_backward_bf16
+ *                                      (config F: bf16 logits and context,
+ *                                       forward and adjoint)
  *
- * Writes the inputs, the cache's ranks / interval table and both maps to
- * <out_dir>/*.bin so tests/test_c_abi.py can check them against the oracle.
+ * Writes the inputs, the cache's ranks / interval table, the maps and the
+ * gradients to <out_dir>/<name>.bin so tests/test_c_abi.py can check them against
+ * the oracle.
  *
  *   gcc -O2 examples/c_abi_pool.c -Iinclude -I/usr/local/cuda/include \
  *       -Lpaper_2205_13542_b200 -lbevpool_sm100 -L/usr/local/cuda/lib64 -lcudart \
@@ -62,6 +67,13 @@ static int dump(const char *dir, const char *name, const void *dev, size_t bytes
     fclose(f);
     free(h);
     return 0;
+}
+
+/* fp32 -> bf16 bits, round to nearest even (finite inputs) */
+static uint16_t to_bf16(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
 }
 
 static uint64_t lcg = 0x9E3779B97F4A7C15ull;
@@ -161,6 +173,34 @@ int main(int argc, char **argv) {
     float *out_tiled = dev_alloc(sizeof(float) * C * n_cells);
     CHECK_BVP(bvp_tile_pool_f32(feat, dist, &plan, 1, C, BVP_SUM, rows, rows_bytes, out_tiled,
                                 NULL));
+
+    /* training: the adjoint of the SUM map for a random grad_out (config B),
+     * then config F's fused forward and adjoint on bf16 copies of the inputs */
+    const size_t gmap_bytes = sizeof(float) * C * n_cells;
+    float *h_g = malloc(gmap_bytes);
+    for (int64_t i = 0; i < (int64_t)C * n_cells; ++i) h_g[i] = uniform(-1.f, 1.f);
+    const int64_t n_feat = (int64_t)N * C * H * W, n_pt = (int64_t)N * D * H * W;
+    uint16_t *h_lb = malloc(2 * n_pt), *h_cb = malloc(2 * n_feat);
+    for (int64_t i = 0; i < n_pt; ++i) h_lb[i] = to_bf16(h_logit[i]);
+    for (int64_t i = 0; i < n_feat; ++i) h_cb[i] = to_bf16(h_feat[i]);
+    float *g = dev_alloc(gmap_bytes), *grad_feat = dev_alloc(sizeof(float) * n_feat);
+    float *grad_dist = dev_alloc(sizeof(float) * n_pt), *out_fused = dev_alloc(gmap_bytes);
+    uint16_t *lb = dev_alloc(2 * n_pt), *cb = dev_alloc(2 * n_feat);
+    uint16_t *grad_logit = dev_alloc(2 * n_pt), *grad_ctx = dev_alloc(2 * n_feat);
+    if (!h_g || !h_lb || !h_cb || !g || !grad_feat || !grad_dist || !out_fused || !lb || !cb ||
+        !grad_logit || !grad_ctx) {
+        fprintf(stderr, "allocation failed\n");
+        return 1;
+    }
+    CHECK_CUDA(cudaMemcpy(g, h_g, gmap_bytes, cudaMemcpyHostToDevice));
+    CHECK_CUDA(cudaMemcpy(lb, h_lb, 2 * n_pt, cudaMemcpyHostToDevice));
+    CHECK_CUDA(cudaMemcpy(cb, h_cb, 2 * n_feat, cudaMemcpyHostToDevice));
+    CHECK_BVP(bvp_tile_backward_f32(g, feat, dist, &plan, 1, C, BVP_SUM, rows, rows_bytes,
+                                    grad_feat, grad_dist, NULL));
+    CHECK_BVP(bvp_tile_pool_fused_bf16(lb, cb, &plan, 1, C, BVP_SUM, rows, rows_bytes, out_fused,
+                                       NULL));
+    CHECK_BVP(bvp_tile_fused_backward_bf16(g, lb, cb, &plan, 1, C, BVP_SUM, rows, rows_bytes,
+                                           grad_logit, grad_ctx, NULL));
     CHECK_CUDA(cudaDeviceSynchronize());
 
     /* fast vs exact, the reference's tolerance metric max|a-b| / max(1,|a|) */
@@ -185,7 +225,15 @@ int main(int argc, char **argv) {
         dump(out_dir, "interval_cells", icells, 4 * host_counts[1]) ||
         dump(out_dir, "out_exact", out_exact, map_bytes) ||
         dump(out_dir, "out_fast", out_fast, map_bytes) ||
-        dump(out_dir, "out_tiled", out_tiled, map_bytes)) {
+        dump(out_dir, "out_tiled", out_tiled, map_bytes) ||
+        dump(out_dir, "grad_out", g, gmap_bytes) ||
+        dump(out_dir, "grad_features", grad_feat, sizeof(float) * n_feat) ||
+        dump(out_dir, "grad_dist", grad_dist, sizeof(float) * n_pt) ||
+        dump(out_dir, "logits_bf16", lb, 2 * n_pt) ||
+        dump(out_dir, "context_bf16", cb, 2 * n_feat) ||
+        dump(out_dir, "out_fused", out_fused, gmap_bytes) ||
+        dump(out_dir, "grad_logits", grad_logit, 2 * n_pt) ||
+        dump(out_dir, "grad_context", grad_ctx, 2 * n_feat)) {
         fprintf(stderr, "writing %s failed\n", out_dir);
         return 1;
     }

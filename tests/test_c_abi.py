@@ -61,6 +61,22 @@ def test_c_host_pipeline_matches_oracle(tmp_path):
     np.testing.assert_array_equal(load("out_exact", np.float32).reshape(want.shape), want)
     assert o.max_rel_dev(want, load("out_fast", np.float32).reshape(want.shape)) <= 1e-5
     assert o.max_rel_dev(want, load("out_tiled", np.float32).reshape(want.shape)) <= 1e-5
+    # training from C: the tiled adjoint (fp32, 1e-5) and config F's fused
+    # forward (1e-5 of the bf16-input restatement) and adjoint (1e-2)
+    g = load("grad_out", np.float32).reshape(C, NX * NY).astype(np.float64)
+    gf, gw = o.pool_backward(feats, dist, want_cells, g, ranks, starts, icells, "sum")
+    assert o.max_rel_dev(gf, load("grad_features", np.float32).reshape(gf.shape)) <= 1e-5
+    assert o.max_rel_dev(gw, load("grad_dist", np.float32).reshape(gw.shape)) <= 1e-5
+
+    def bf16(name, shape):
+        return (load(name, np.uint16).astype(np.uint32) << 16).view(np.float32).reshape(shape)
+
+    lb, cb = bf16("logits_bf16", (1, D, H, W)), bf16("context_bf16", (1, C, H, W))
+    want_f = o.fused_pool(cb, lb, ranks, starts, icells, NX * NY, "sum")
+    assert o.max_rel_dev(want_f, load("out_fused", np.float32).reshape(want_f.shape)) <= 1e-5
+    want_l, want_c = o.fused_backward(cb, lb, want_cells, g, ranks, starts, icells, "sum")
+    assert o.max_rel_dev(want_l, bf16("grad_logits", want_l.shape)) <= 1e-2
+    assert o.max_rel_dev(want_c, bf16("grad_context", want_c.shape)) <= 1e-2
 
 
 def build_interval_reduce(tmp_path):
