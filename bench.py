@@ -57,9 +57,10 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="S", choices=["S", "B", "H"],
-                    help="S: cached forward, 1 sample/GPU (the headline); B: training step "
-                         "(forward + backward), batch 4/GPU; H: high-res frame with the "
+    ap.add_argument("--config", default="S", choices=["S", "F", "B", "H"],
+                    help="S: cached forward, 1 sample/GPU (the headline); F: the fused bf16 "
+                         "lift+pool forward from logits and context, 1 sample/GPU; B: training "
+                         "step (forward + backward), batch 4/GPU; H: high-res frame with the "
                          "association rebuilt every step, 1 sample/GPU")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -489,7 +490,9 @@ def main():
 # ---------------------------------------------------------------------------
 
 def run_config_bh(args, bp, torch, tdist, dev, rank, world, local):
-    """B: the training step -- tiled forward + tiled adjoint through the
+    """F: the fused lift+pool forward (bf16 logits and context -> fp32 map,
+    the depth softmax formed per tile) through bp.pool_fused, one sample per
+    GPU.  B: the training step -- tiled forward + tiled adjoint through the
     autograd op, batch 4 per GPU (samples rank*4 .. rank*4+3).  H: one
     high-res sample per GPU with the association rebuilt every step
     (CacheBuilder + PoolPlan.run_uncached).  Inputs resident in HBM, L2
@@ -497,21 +500,30 @@ def run_config_bh(args, bp, torch, tdist, dev, rank, world, local):
     from paper_2205_13542_b200.shard import gather_scalars, max_over_ranks, sample_seeds
 
     name = args.config
-    spec = bp.CONFIGS["S" if name == "B" else "H"]
+    spec = bp.CONFIGS["H" if name == "H" else "S"]
     f = spec.frustum
     B_local = 4 if name == "B" else 1
     seeds = sample_seeds(world * B_local, rank, world)
     rig, _, _, grid = bp.gen_workload(spec)
-    feats, dists = [], []
+    feats, dists, logits = [], [], []
     for sd in seeds:
         _, fr, lr, _ = bp.gen_workload(bp.WorkloadSpec(spec.n_cameras, f, spec.grid,
                                                        spec.channels, sd))
         feats.append(torch.from_numpy(fr))
+        logits.append(torch.from_numpy(lr))
         dists.append(bp.normalize_depth(torch.from_numpy(lr).to(dev)).cpu())
     F = torch.stack(feats).to(dev)
     Dd = torch.stack(dists).to(dev)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    if name == "B":
+    if name == "F":
+        cache = bp.build_cache(rig, f, grid, device=dev)
+        LG = torch.stack(logits).to(dev).to(torch.bfloat16)
+        CX = F.to(torch.bfloat16)
+
+        def step():
+            bp.pool_fused(LG, CX, cache, grid)
+        launches = None
+    elif name == "B":
         cache = bp.build_cache(rig, f, grid, device=dev)
         Fg = F.clone().requires_grad_(True)
         Dg = Dd.clone().requires_grad_(True)
@@ -556,15 +568,19 @@ def run_config_bh(args, bp, torch, tdist, dev, rank, world, local):
     tot_ms = max_over_ranks(sum(step_ms), dev)
     if rank == 0:
         P = spec.n_points
-        what = ("training step: forward + tiled adjoint (autograd), batch 4 per GPU"
-                if name == "B" else
-                "high-res frame: association rebuilt every step + forward, 1 sample per GPU")
+        what = {"F": "fused bf16 lift+pool forward (bp.pool_fused: depth softmax per tile, "
+                     "no dist or frustum tensor), 1 sample per GPU",
+                "B": "training step: forward + tiled adjoint (autograd), batch 4 per GPU",
+                "H": "high-res frame: association rebuilt every step + forward, 1 sample per GPU"
+                }[name]
         cfg = config_dict(spec)
         cfg.update({"workload": f"config {name} ({what})", "batch_per_gpu": B_local})
         line = {"metric": METRIC, "value": world * B_local * P * K / (tot_ms * 1e-3),
                 "unit": UNIT, "n_gpus": world, "steps": K, "warmup": max(3, args.warmup),
                 "ms_per_step": tot_ms / K, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference gen_workload)",
+                "vs_baseline": None,
+                "dtype": "bf16 in / f32 accumulate" if name == "F" else "f32",
+                "data": "synthetic (reference gen_workload)",
                 "config": cfg,
                 "parallelism": f"batch-sharded x{world}, no collective in the step",
                 "timing": "CUDA events, L2 flushed (512 MiB write) before every step, max over ranks",
