@@ -1,5 +1,7 @@
-// tile_backward.cu -- the adjoint of the tiled reduction (config B):
-// bvp_tile_backward_f32.  See tile.cu for the forward it inverts.
+// tile_backward.cu -- the adjoint of the tiled reduction: config B's
+// bvp_tile_backward_f32 and config F's bvp_tile_fused_backward_bf16 (one
+// kernel, FU selecting the bf16 / softmax variant).  See tile.cu for the
+// forward it inverts.
 #include "tile.cuh"
 
 namespace bvp {
