@@ -667,6 +667,16 @@ seg_sort_long_kernel(uint32_t *__restrict__ ranks, const uint32_t *__restrict__ 
     }
 }
 
+__global__ void zero_words3_kernel(uint32_t *__restrict__ a, int64_t na, uint32_t *__restrict__ b,
+                                   int64_t nb, uint32_t *__restrict__ c, int64_t nc) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < na + nb + nc; i += stride) {
+        if (i < na) a[i] = 0u;
+        else if (i < na + nb) b[i - na] = 0u;
+        else c[i - na - nb] = 0u;
+    }
+}
+
 // ---- workspace layout -------------------------------------------------------
 struct SortLayout {
     int key_bits, passes, digit_bits;
@@ -735,16 +745,18 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
     auto *total64 = reinterpret_cast<unsigned long long *>(w + L.off_total64);
     auto *total32 = reinterpret_cast<uint32_t *>(w + L.off_total32);
 
-    cudaMemsetAsync(cell_count, 0, 4 * size_t(n_cells), s);
     const unsigned cb = static_cast<unsigned>(std::min<int64_t>(ceil_div(n_cells, 256), 4096));
     if (P <= kCountSortMaxRun * n_cells) {  // counting sort: short runs per key
         uint32_t *slot = ka;
         auto *long_list = reinterpret_cast<uint32_t *>(w + L.off_long);
         auto *n_long = reinterpret_cast<uint32_t *>(w + L.off_nlong);
-        cudaMemsetAsync(n_long, 0, 8, s);
         size_t flag_bytes = 0;
         void *flags = scan_flags(part64, n_cells, &flag_bytes);
-        cudaMemsetAsync(flags, 0, flag_bytes, s);  // the scan's flags, before the front end
+        // the per-cell counters, the long-run count and the scan's flags in
+        // one launch (three memsets measured as three dependent launches)
+        zero_words3_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, n_long, 2,
+                                              static_cast<uint32_t *>(flags),
+                                              int64_t(flag_bytes / 4));
         if (cams)
             count_front_kernel<<<148 * 8, 256, 0, s>>>(cams, *fp, *gp, cells, cell_count, slot);
         else
@@ -787,6 +799,7 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         if (rc_r != BVP_OK) return rc_r;
         return check_launch("sort_intervals");
     }
+    cudaMemsetAsync(cell_count, 0, 4 * size_t(n_cells), s);
     const unsigned tiles = static_cast<unsigned>(L.n_tiles);
     if (cams)
         pass0_front_kernel<true><<<tiles, kSortThreads, 0, s>>>(
