@@ -372,6 +372,11 @@ count_front_kernel(const double *__restrict__ cams, FrustumParams f, GridParams 
     const uint32_t npix = static_cast<uint32_t>(f.N) * f.H * f.W;
     const uint32_t ntiles = (npix + kFrontPix - 1) / kFrontPix;
     const uint32_t D = static_cast<uint32_t>(f.D);
+    // programmatic dependent launch both ways: the scan after this kernel
+    // may be scheduled now (it waits for this grid's completion), and this
+    // kernel's geometry runs before its wait for the zero fill ahead of it
+    asm volatile("griddepcontrol.launch_dependents;");
+    bool waited = false;
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t q = tile * kFrontPix + lane;
         const bool valid = q < npix;
@@ -387,6 +392,10 @@ count_front_kernel(const double *__restrict__ cams, FrustumParams f, GridParams 
             for (int dd = warp; dd < nd; dd += 8) {
                 const uint32_t cc = valid ? cell_at(c, f, g, dx, dy, static_cast<int>(d0) + dd)
                                           : kOOR;
+                if (!waited) {  // the counters' zero fill (PDL)
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    waited = true;
+                }
                 s_slot[dd][lane] = claim_slot(cc, cell_count);
                 s_cell[dd][lane] = cc;
             }
@@ -757,12 +766,22 @@ static int sort_impl(const double *cams, const FrustumParams *fp, const GridPara
         zero_words3_kernel<<<cb, 256, 0, s>>>(cell_count, n_cells, n_long, 2,
                                               static_cast<uint32_t *>(flags),
                                               int64_t(flag_bytes / 4));
-        if (cams)
-            count_front_kernel<<<148 * 8, 256, 0, s>>>(cams, *fp, *gp, cells, cell_count, slot);
-        else
+        if (cams) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(148 * 8);
+            cfg.blockDim = dim3(256);
+            cfg.stream = s;
+            cudaLaunchAttribute at1[1];
+            at1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at1[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at1;
+            cfg.numAttrs = 1;
+            cudaLaunchKernelEx(&cfg, count_front_kernel, cams, *fp, *gp, cells, cell_count, slot);
+        } else {
             count_cells_kernel<<<148 * 8, 256, 0, s>>>(cells, P, cell_count, slot);
+        }
         device_excl_scan_xf<unsigned long long>(cell_count, packed, n_cells, part64, total64,
-                                                PackCount{}, s, true);
+                                                PackCount{}, s, true, cams != nullptr);
         // the interval tables (and what hangs on them) on a side stream, beside
         // the rank scatter; the run sorts need both
         SideFork tables(s, 1);

@@ -178,6 +178,8 @@ scan_onepass_kernel(const In *__restrict__ in, int64_t n, T *out, T *part, int64
     T *agg = part, *incl = part + nb;
     uint32_t *flags = reinterpret_cast<uint32_t *>(part + 2 * nb), *ticket = flags + nb;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // (a programmatic dependent launch waits here for its producer; else a no-op)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
     __syncthreads();
     const int64_t tile = s_tile;
@@ -277,9 +279,11 @@ static void *scan_flags(T *partials, int64_t n, size_t *bytes) {
     return partials + 2 * nb;
 }
 
+// pdl: launched as a programmatic dependent of the kernel before it on s
+// (the kernel waits for that grid before its first access).
 template <typename T, typename In, typename Xf>
 static void device_excl_scan_xf(const In *in, T *out, int64_t n, T *partials, T *total, Xf xf,
-                                cudaStream_t s, bool flags_zeroed = false) {
+                                cudaStream_t s, bool flags_zeroed = false, bool pdl = false) {
     static_assert(is_exact_scan<T>::value, "the transformed scan is the one-pass form");
     const int64_t nb = ceil_div(n, kScanChunk);
     if (nb == 0) {
@@ -287,6 +291,20 @@ static void device_excl_scan_xf(const In *in, T *out, int64_t n, T *partials, T 
         return;
     }
     if (!flags_zeroed) cudaMemsetAsync(partials + 2 * nb, 0, size_t(nb + 1) * sizeof(uint32_t), s);
+    if (pdl && flags_zeroed) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)nb);
+        cfg.blockDim = dim3(kScanThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at1[1];
+        at1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at1[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at1;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, scan_onepass_kernel<T, In, Xf>, in, n, out, partials, nb, total,
+                           xf);
+        return;
+    }
     scan_onepass_kernel<T, In, Xf><<<(unsigned)nb, kScanThreads, 0, s>>>(in, n, out, partials, nb,
                                                                         total, xf);
 }
