@@ -44,8 +44,8 @@ def test_two_ranks_config_S():
     assert line["ms_per_step"] >= max(mr["per_rank_step_ms"]) - 1e-9  # max over ranks
 
 
-@pytest.mark.parametrize("config", ["B", "H"])
-def test_two_ranks_configs_B_H(config):
+@pytest.mark.parametrize("config", ["F", "B", "H"])
+def test_two_ranks_configs_F_B_H(config):
     line = _torchrun("--config", config, "--steps", "2", "--warmup", "3")
     assert line["n_gpus"] == 2
     assert len(line["latency_ms"]["per_rank_step_ms"]) == 2
